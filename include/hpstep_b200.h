@@ -1,0 +1,122 @@
+/*
+ * hpstep_b200.h -- C ABI of the B200 (sm_100a) HPS stage-solve library.
+ *
+ * Drop-in boundary for the per-ESDIRK-stage HPS solve of arXiv 2306.02526's
+ * reference package `hpstep` (/root/reference/pkg/src/hpstep).  The reference
+ * is pure Python, so its "plugin boundary" is the Python class API; each entry
+ * point below replaces the reference code cited beside it, and the Python
+ * package `paper_2306_02526_b200` binds them with ctypes exactly as a
+ * maintainer would from `hpstep`.
+ *
+ * Conventions
+ *   - plain C types only; every `const double* / double*` argument named
+ *     "device" is a CUDA device pointer owned by the caller (e.g. a torch
+ *     tensor); host descriptors are copied during the call.
+ *   - `stream` is a cudaStream_t passed as void*; all device work is
+ *     stream-ordered and never synchronises the host, except
+ *     hps_ops_build (which must read pivots to report singular nodes).
+ *   - return value 0 = success; < 0 = failure with a message available from
+ *     hps_last_error() (thread-local).  HPS_ERR_SINGULAR additionally sets
+ *     hps_last_error_node() to the DFS node index of the first singular
+ *     block (reference: SingularMatrixError context "leaf node i" /
+ *     "merge node i", linalg.py:36-42, solver.py:60,72).
+ *   - operator sets are immutable after build; any number of concurrent
+ *     solves may share one (solver.py:84-89) as long as each passes its own
+ *     workspace.
+ */
+#ifndef HPSTEP_B200_H
+#define HPSTEP_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_OK 0
+#define HPS_ERR_ARG (-1)
+#define HPS_ERR_CUDA (-2)
+#define HPS_ERR_SINGULAR (-3)
+
+typedef struct hps_plan hps_plan; /* tree shape + per-level index maps (device) */
+typedef struct hps_ops hps_ops;   /* device operator set of one shift        */
+
+/* Tree description (host arrays, copied).  Replaces the DomainTree numbering
+ * consumed by the solver (tree.py:123-156, 216-280, 374-404).
+ * Levels are the parent levels of the binary tree, root first.
+ * lvl_shape[5*d + {0..4}] = {c, n3, n1a, n2b, nbc}: node count, |J3|, |J1|,
+ * |J2| and the child boundary size.  The per-level child-local maps i1a,
+ * i3a, i2b, i3b are shared by every node of a level; gidx_bnd (c x n12) and
+ * j3 (c x n3) are the global DOF ids of each node's boundary / interface. */
+typedef struct {
+  int n1, n2, p;
+  int depth;              /* number of parent levels = log2(n1*n2)          */
+  long long N;            /* global DOFs                                     */
+  int L, ni, nb, nbd;     /* leaves, interior / boundary DOFs per leaf, |boundary| */
+  const int* lvl_shape;
+  const int* const* lvl_i1a;
+  const int* const* lvl_i3a;
+  const int* const* lvl_i2b;
+  const int* const* lvl_i3b;
+  const int* const* lvl_gidx_bnd;
+  const int* const* lvl_j3;
+  const long long* const* lvl_node_index; /* DFS node index per level node  */
+  const int* leaf_bnd_gidx;                /* L x nb                          */
+  const long long* leaf_node_index;        /* L                               */
+  const int* boundary_ids;                 /* nbd, ascending                  */
+} hps_plan_desc;
+
+/* Build inputs (host arrays, copied).  Replaces build_leaf / merge / _build
+ * (solver.py:53-158) for the shifted operator sigma*I + dt_gamma*A. */
+typedef struct {
+  double sigma, dt_gamma;
+  int shared_leaf;     /* 1: constant coefficients, one leaf operator set   */
+  int keep_dtn;        /* keep every level's DtN map T (tests, save/load)    */
+  const double* coef;  /* Lc x 5 x ni: c11,c22,c1,c2,c at interior points (Lc = 1 or L) */
+  int has_c1, has_c2, has_c;
+  const double* D2x;   /* ni x m interior stencil rows (operators.py:180-181) */
+  const double* D2y;
+  const double* D1x;
+  const double* D1y;
+  const double* D_bnd; /* nb x m flux rows (operators.py:188-190)            */
+} hps_build_desc;
+
+int hps_version(void);
+const char* hps_last_error(void);
+long long hps_last_error_node(void);
+
+int hps_plan_create(const hps_plan_desc* desc, hps_plan** out);
+void hps_plan_destroy(hps_plan* plan);
+
+/* HpsOperatorSet.__init__ / build() (solver.py:91-158, 380-390). */
+int hps_ops_build(const hps_plan* plan, const hps_build_desc* desc, void* stream, hps_ops** out);
+void hps_ops_destroy(hps_ops* ops);
+size_t hps_ops_device_bytes(const hps_ops* ops);
+
+/* Copy one operator block to host memory (test hooks leaf_operators /
+ * merge_operators, solver.py:339-348).  which: leaf 0=Ainv (ni x ni),
+ * 1=S (ni x nb), 2=T (nb x nb, keep_dtn only); merge 0=Xinv (n3 x n3),
+ * 1=Tstack (n12 x n3), 2=S (n3 x n12), 3=T (n12 x n12, keep_dtn only).
+ * `level` is the parent level (root = 0), `node` the position on it. */
+int hps_ops_get_leaf(const hps_ops* ops, int which, int leaf, double* host_out);
+int hps_ops_get_merge(const hps_ops* ops, int level, int node, int which, double* host_out);
+
+size_t hps_solve_workspace_bytes(const hps_plan* plan, int k);
+
+/* HpsOperatorSet._solve (solver.py:201-276) for k stacked right-hand sides:
+ *   fb   device k x nbd Dirichlet values (row stride ld_f; ld_f = 0 broadcasts)
+ *   g    device body load, read at leaf interiors [0, L*ni) only, row stride
+ *        ld_g; NULL = homogeneous solve (solve_homogeneous)
+ *   jump device interface flux jumps (row stride ld_jump) or NULL; with
+ *        inv_dt = 1/dt this is solve_penalized (solver.py:188-199, 249-250)
+ *   u    device k x N output (row stride ld_u), every DOF written
+ *   ws   device workspace of >= hps_solve_workspace_bytes(plan, k) bytes */
+int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
+              long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
+              long long ld_u, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPSTEP_B200_H */

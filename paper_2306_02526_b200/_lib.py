@@ -1,0 +1,123 @@
+"""ctypes binding of the C ABI declared in include/hpstep_b200.h.
+
+The shared library is built in-tree (``paper_2306_02526_b200/lib``) by
+``__graft_entry__.build()``.  There is no fallback: if the library or a CUDA
+device is missing, every device entry point raises.
+"""
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import HpstepError, SingularMatrixError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhpstep_b200.so")
+
+HPS_OK = 0
+HPS_ERR_SINGULAR = -3
+
+c_int_p = ctypes.POINTER(ctypes.c_int)
+c_ll_p = ctypes.POINTER(ctypes.c_longlong)
+c_double_p = ctypes.POINTER(ctypes.c_double)
+
+
+class PlanDesc(ctypes.Structure):
+    _fields_ = [
+        ("n1", ctypes.c_int), ("n2", ctypes.c_int), ("p", ctypes.c_int),
+        ("depth", ctypes.c_int), ("N", ctypes.c_longlong),
+        ("L", ctypes.c_int), ("ni", ctypes.c_int), ("nb", ctypes.c_int), ("nbd", ctypes.c_int),
+        ("lvl_shape", c_int_p),
+        ("lvl_i1a", ctypes.POINTER(c_int_p)), ("lvl_i3a", ctypes.POINTER(c_int_p)),
+        ("lvl_i2b", ctypes.POINTER(c_int_p)), ("lvl_i3b", ctypes.POINTER(c_int_p)),
+        ("lvl_gidx_bnd", ctypes.POINTER(c_int_p)), ("lvl_j3", ctypes.POINTER(c_int_p)),
+        ("lvl_node_index", ctypes.POINTER(c_ll_p)),
+        ("leaf_bnd_gidx", c_int_p), ("leaf_node_index", c_ll_p), ("boundary_ids", c_int_p),
+    ]
+
+
+class BuildDesc(ctypes.Structure):
+    _fields_ = [
+        ("sigma", ctypes.c_double), ("dt_gamma", ctypes.c_double),
+        ("shared_leaf", ctypes.c_int), ("keep_dtn", ctypes.c_int),
+        ("coef", c_double_p), ("has_c1", ctypes.c_int), ("has_c2", ctypes.c_int),
+        ("has_c", ctypes.c_int),
+        ("D2x", c_double_p), ("D2y", c_double_p), ("D1x", c_double_p), ("D1y", c_double_p),
+        ("D_bnd", c_double_p),
+    ]
+
+
+# exported symbols and their signatures (every name declared in include/hpstep_b200.h)
+SIGNATURES = {
+    "hps_version": (ctypes.c_int, []),
+    "hps_last_error": (ctypes.c_char_p, []),
+    "hps_last_error_node": (ctypes.c_longlong, []),
+    "hps_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(ctypes.c_void_p)]),
+    "hps_plan_destroy": (None, [ctypes.c_void_p]),
+    "hps_ops_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BuildDesc), ctypes.c_void_p,
+                                     ctypes.POINTER(ctypes.c_void_p)]),
+    "hps_ops_destroy": (None, [ctypes.c_void_p]),
+    "hps_ops_device_bytes": (ctypes.c_size_t, [ctypes.c_void_p]),
+    "hps_ops_get_leaf": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_double_p]),
+    "hps_ops_get_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                         c_double_p]),
+    "hps_solve_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int]),
+    "hps_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
+                                 ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,
+                                 ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p,
+                                 ctypes.c_longlong, ctypes.c_void_p, ctypes.c_size_t,
+                                 ctypes.c_void_p]),
+}
+
+_lib = None
+
+
+def load():
+    """Load the library (no CUDA device needed just to load it)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise HpstepError(
+                f"CUDA library not built: {LIB_PATH} is missing "
+                "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error():
+    lib = load()
+    return lib.hps_last_error().decode(errors="replace")
+
+
+def check(rc, what):
+    if rc == HPS_OK:
+        return
+    lib = load()
+    msg = last_error()
+    if rc == HPS_ERR_SINGULAR:
+        # message ends with "[leaf node i]" / "[merge node i]" (SingularMatrixError context)
+        body, _, ctx = msg.rpartition(" [")
+        raise SingularMatrixError(body, context=ctx.rstrip("]") or None)
+    raise HpstepError(f"{what} failed ({rc}): {msg} (node {lib.hps_last_error_node()})")
+
+
+def int_ptr(a):
+    return a.ctypes.data_as(c_int_p)
+
+
+def ll_ptr(a):
+    return a.ctypes.data_as(c_ll_p)
+
+
+def dbl_ptr(a):
+    return a.ctypes.data_as(c_double_p)
+
+
+def as_i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)

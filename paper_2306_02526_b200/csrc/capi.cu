@@ -1,0 +1,359 @@
+// C ABI (include/hpstep_b200.h): plan / operator-set lifecycle and solve.
+#include <math.h>
+#include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/hpstep_b200.h"
+#include "hps_plan.cuh"
+
+namespace hpsb {
+
+static thread_local char g_err[1024] = {0};
+static thread_local long long g_err_node = -1;
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void set_error_node(long long node) { g_err_node = node; }
+
+int gj_invert(int n, int batch, double* A, double* X, int ldx, long long sX, double* stats, cudaStream_t st);
+int leaf_assemble(int Lc, int ni, int nb, const double* cv, int has_c1, int has_c2, int has_c,
+                  const double* D2x, const double* D2y, const double* D1x, const double* D1y, double sigma,
+                  double dtg, double* Aii, double* Aib, cudaStream_t st);
+int merge_gather(int c, int n3, int n1a, int n2b, int nbc, const double* Tc, long long sTc, const int* i1a,
+                 const int* i3a, const int* i2b, const int* i3b, double* X33, double* R, double* Tst, int ld3,
+                 double* Tnew, cudaStream_t st);
+int broadcast_copies(long long n, int copies, double* base, cudaStream_t st);
+
+static const double kPivotRtol = 1e-13;  // linalg.py:17
+
+template <class T>
+static int upload(const T* host, size_t count, T** dev) {
+  *dev = nullptr;
+  if (count == 0) return 0;
+  HPSB_CUDA(cudaMalloc((void**)dev, count * sizeof(T)));
+  HPSB_CUDA(cudaMemcpy(*dev, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+static int even(int n) { return (n + 1) & ~1; }
+
+// Returns the first failing batch entry (or -1) under the reference policy.
+static int check_pivots(const double* dstats, int batch, int n, std::vector<double>& hs, cudaStream_t st) {
+  hs.resize(2 * (size_t)batch);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -2;
+  if (cudaMemcpy(hs.data(), dstats, hs.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return -2;
+  for (int b = 0; b < batch; ++b) {
+    double pmin = hs[2 * b], pmax = hs[2 * b + 1];
+    if (n > 0 && (!(pmax > 0.0) || !(pmin > kPivotRtol * pmax))) return b;
+  }
+  return -1;
+}
+
+static int singular(int n, double pmin, double pmax, const char* kind, long long node) {
+  set_error("matrix of size %d is singular to tolerance %g (min/max pivot = %.3e/%.3e) [%s node %lld]", n,
+            kPivotRtol, pmin, pmax, kind, node);
+  set_error_node(node);
+  return HPS_ERR_SINGULAR;
+}
+
+}  // namespace hpsb
+
+using namespace hpsb;
+
+struct hps_plan { Plan P; std::vector<void*> allocs; };
+struct hps_ops { Ops O; };
+
+extern "C" {
+
+int hps_version(void) { return 1; }
+const char* hps_last_error(void) { return g_err; }
+long long hps_last_error_node(void) { return g_err_node; }
+
+int hps_plan_create(const hps_plan_desc* d, hps_plan** out) {
+  *out = nullptr;
+  g_err_node = -1;
+  if (!d || d->n1 <= 0 || d->n2 <= 0 || d->p < 4 || d->depth < 0) {
+    set_error("hps_plan_create: invalid descriptor");
+    return HPS_ERR_ARG;
+  }
+  hps_plan* h = new hps_plan();
+  Plan& P = h->P;
+  P.n1 = d->n1; P.n2 = d->n2; P.p = d->p; P.q = d->p - 2;
+  P.ni = d->ni; P.nb = d->nb; P.L = d->L; P.depth = d->depth; P.nbd = d->nbd; P.N = d->N;
+  P.ldi = even(P.ni); P.ldb = even(P.nb);
+  P.lv.resize(P.depth);
+  int rc = 0;
+  auto up = [&](const int* src, size_t n, int** dst) {
+    if (rc) return;
+    rc = upload(src, n, dst);
+    if (!rc && *dst) h->allocs.push_back(*dst);
+  };
+  for (int l = 0; l < P.depth && !rc; ++l) {
+    Level& lv = P.lv[l];
+    lv.c = d->lvl_shape[5 * l]; lv.n3 = d->lvl_shape[5 * l + 1]; lv.n1a = d->lvl_shape[5 * l + 2];
+    lv.n2b = d->lvl_shape[5 * l + 3]; lv.nbc = d->lvl_shape[5 * l + 4];
+    lv.n12 = lv.n1a + lv.n2b; lv.ld3 = even(lv.n3); lv.ld12 = even(lv.n12);
+    lv.h_i1a.assign(d->lvl_i1a[l], d->lvl_i1a[l] + lv.n1a);
+    lv.h_i3a.assign(d->lvl_i3a[l], d->lvl_i3a[l] + lv.n3);
+    lv.h_i2b.assign(d->lvl_i2b[l], d->lvl_i2b[l] + lv.n2b);
+    lv.h_i3b.assign(d->lvl_i3b[l], d->lvl_i3b[l] + lv.n3);
+    up(d->lvl_i1a[l], lv.n1a, &lv.i1a);
+    up(d->lvl_i3a[l], lv.n3, &lv.i3a);
+    up(d->lvl_i2b[l], lv.n2b, &lv.i2b);
+    up(d->lvl_i3b[l], lv.n3, &lv.i3b);
+    up(d->lvl_gidx_bnd[l], (size_t)lv.c * lv.n12, &lv.gidx_bnd);
+    up(d->lvl_j3[l], (size_t)lv.c * lv.n3, &lv.j3);
+    lv.node_index.assign(d->lvl_node_index[l], d->lvl_node_index[l] + lv.c);
+  }
+  up(d->leaf_bnd_gidx, (size_t)P.L * P.nb, &P.leaf_bnd_gidx);
+  up(d->boundary_ids, (size_t)P.nbd, &P.boundary_ids);
+  P.leaf_node_index.assign(d->leaf_node_index, d->leaf_node_index + P.L);
+  if (rc) { hps_plan_destroy(h); return rc; }
+  *out = h;
+  return HPS_OK;
+}
+
+void hps_plan_destroy(hps_plan* h) {
+  if (!h) return;
+  for (void* p : h->allocs) cudaFree(p);
+  delete h;
+}
+
+static double* ops_alloc(Ops& O, size_t doubles, bool zero) {
+  double* p = nullptr;
+  if (doubles == 0) doubles = 1;
+  if (cudaMalloc(&p, doubles * 8) != cudaSuccess) return nullptr;
+  if (zero) cudaMemset(p, 0, doubles * 8);
+  O.allocs.push_back(p);
+  O.bytes += doubles * 8;
+  return p;
+}
+
+void hps_ops_destroy(hps_ops* h) {
+  if (!h) return;
+  for (void* p : h->O.allocs) cudaFree(p);
+  delete h;
+}
+
+size_t hps_ops_device_bytes(const hps_ops* h) { return h ? h->O.bytes : 0; }
+
+int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps_ops** out) {
+  *out = nullptr;
+  g_err_node = -1;
+  if (!hp || !d) { set_error("hps_ops_build: null argument"); return HPS_ERR_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const Plan& P = hp->P;
+  hps_ops* h = new hps_ops();
+  Ops& O = h->O;
+  O.plan = const_cast<Plan*>(&P);
+  O.sigma = d->sigma; O.dtg = d->dt_gamma;
+  O.shared_leaf = d->shared_leaf ? 1 : 0;
+  O.Lc = O.shared_leaf ? 1 : P.L;
+  O.lo.resize(P.depth);
+  const int ni = P.ni, nb = P.nb, m = ni + nb, Lc = O.Lc;
+  std::vector<void*> tmp;
+  auto fail = [&](int rc) {
+    for (void* p : tmp) cudaFree(p);
+    hps_ops_destroy(h);
+    return rc;
+  };
+  auto talloc = [&](size_t doubles) -> double* {
+    double* p = nullptr;
+    if (doubles == 0) doubles = 1;
+    if (cudaMalloc(&p, doubles * 8) != cudaSuccess) return nullptr;
+    tmp.push_back(p);
+    return p;
+  };
+  auto tfree = [&](double* p) {
+    if (!p) return;
+    auto it = std::find(tmp.begin(), tmp.end(), (void*)p);
+    if (it != tmp.end()) { cudaFree(p); tmp.erase(it); }
+  };
+  // stencil rows, coefficients
+  double *dD2x, *dD2y, *dD1x, *dD1y, *dcoef;
+  std::vector<double> Dbi((size_t)nb * ni), Dbb((size_t)nb * nb);
+  for (int r = 0; r < nb; ++r) {
+    for (int c = 0; c < ni; ++c) Dbi[(size_t)r * ni + c] = d->D_bnd[(size_t)r * m + c];
+    for (int c = 0; c < nb; ++c) Dbb[(size_t)r * nb + c] = d->D_bnd[(size_t)r * m + ni + c];
+  }
+  double* dDbb;
+  if (int rc = upload(d->D2x, (size_t)ni * m, &dD2x)) return fail(rc);
+  tmp.push_back(dD2x);
+  if (int rc = upload(d->D2y, (size_t)ni * m, &dD2y)) return fail(rc);
+  tmp.push_back(dD2y);
+  if (int rc = upload(d->D1x, (size_t)ni * m, &dD1x)) return fail(rc);
+  tmp.push_back(dD1x);
+  if (int rc = upload(d->D1y, (size_t)ni * m, &dD1y)) return fail(rc);
+  tmp.push_back(dD1y);
+  if (int rc = upload(d->coef, (size_t)Lc * 5 * ni, &dcoef)) return fail(rc);
+  tmp.push_back(dcoef);
+  if (int rc = upload(Dbb.data(), Dbb.size(), &dDbb)) return fail(rc);
+  tmp.push_back(dDbb);
+  O.D_bi = ops_alloc(O, (size_t)nb * ni, false);
+  if (!O.D_bi) { set_error("out of device memory"); return fail(HPS_ERR_CUDA); }
+  if (cudaMemcpy(O.D_bi, Dbi.data(), Dbi.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    set_error("copy failed");
+    return fail(HPS_ERR_CUDA);
+  }
+
+  // ---- leaves (solver.py:53-64, 112-125)
+  double* Aii = talloc((size_t)Lc * ni * ni);
+  double* Aib = talloc((size_t)Lc * ni * nb);
+  double* stats = talloc(2 * (size_t)std::max(Lc, 1));
+  O.Ainv = ops_alloc(O, (size_t)Lc * ni * P.ldi, true);
+  O.S_leaf = ops_alloc(O, (size_t)Lc * ni * P.ldb, true);
+  double* Tleaf = d->keep_dtn ? ops_alloc(O, (size_t)Lc * nb * nb, false) : talloc((size_t)Lc * nb * nb);
+  if (!Aii || !Aib || !stats || !O.Ainv || !O.S_leaf || !Tleaf) {
+    set_error("out of device memory (leaf build)");
+    return fail(HPS_ERR_CUDA);
+  }
+  if (d->keep_dtn) O.T_leaf = Tleaf;
+  if (int rc = leaf_assemble(Lc, ni, nb, dcoef, d->has_c1, d->has_c2, d->has_c, dD2x, dD2y, dD1x, dD1y,
+                             d->sigma, d->dt_gamma, Aii, Aib, st))
+    return fail(rc);
+  if (int rc = gj_invert(ni, Lc, Aii, O.Ainv, P.ldi, (long long)ni * P.ldi, stats, st)) return fail(rc);
+  {
+    std::vector<double> hs;
+    int bad = check_pivots(stats, Lc, ni, hs, st);
+    if (bad == -2) { set_error("cuda error during leaf build"); return fail(HPS_ERR_CUDA); }
+    if (bad >= 0) return fail(singular(ni, hs[2 * bad], hs[2 * bad + 1], "leaf", P.leaf_node_index[bad]));
+  }
+  {
+    GemmArgs a{};  // S = -Ainv A_ib
+    a.M = ni; a.N = nb; a.K = ni; a.alpha = -1.0; a.beta = 0.0;
+    a.A = O.Ainv; a.lda = P.ldi; a.sA = (long long)ni * P.ldi; a.tA = 0;
+    a.B = Aib; a.ldb = nb; a.sB = (long long)ni * nb; a.tB = 0;
+    a.C = O.S_leaf; a.ldc = P.ldb; a.sC = (long long)ni * P.ldb; a.batch = Lc;
+    if (int rc = gemm(a, st)) return fail(rc);
+    GemmArgs t{};  // T = D_bi S + D_bb
+    t.M = nb; t.N = nb; t.K = ni; t.alpha = 1.0; t.beta = 1.0;
+    t.A = O.D_bi; t.lda = ni; t.sA = 0; t.tA = 0;
+    t.B = O.S_leaf; t.ldb = P.ldb; t.sB = (long long)ni * P.ldb; t.tB = 0;
+    t.D = dDbb; t.ldd = nb; t.sD = 0;
+    t.C = Tleaf; t.ldc = nb; t.sC = (long long)nb * nb; t.batch = Lc;
+    if (int rc = gemm(t, st)) return fail(rc);
+  }
+  tfree(Aii); tfree(Aib); tfree(stats);
+
+  // ---- merges, deepest level first (solver.py:127-155)
+  double* Tchild = Tleaf;
+  long long sTchild = O.shared_leaf ? 0 : (long long)nb * nb;
+  for (int l = P.depth - 1; l >= 0; --l) {
+    const Level& lv = P.lv[l];
+    LevelOps& lo = O.lo[l];
+    const int ce = O.shared_leaf ? 1 : lv.c;
+    const int n3 = lv.n3, n12 = lv.n12;
+    lo.Xinv = ops_alloc(O, (size_t)lv.c * n3 * lv.ld3, true);
+    lo.Tst = ops_alloc(O, (size_t)lv.c * n12 * lv.ld3, true);
+    lo.S = ops_alloc(O, (size_t)lv.c * n3 * lv.ld12, true);
+    // every level's DtN map feeds its parent; the root's is kept (solver.py:155)
+    const bool needT = true;
+    const bool keepT = d->keep_dtn || l == 0;
+    double* Tnew = keepT ? ops_alloc(O, (size_t)ce * n12 * n12, false) : talloc((size_t)ce * n12 * n12);
+    double* X33 = talloc((size_t)ce * n3 * n3);
+    double* R = talloc((size_t)ce * n3 * n12);
+    double* lst = talloc(2 * (size_t)ce);
+    if (!lo.Xinv || !lo.Tst || !lo.S || (needT && !Tnew) || !X33 || !R || !lst) {
+      set_error("out of device memory (merge level %d)", l);
+      return fail(HPS_ERR_CUDA);
+    }
+    if (int rc = merge_gather(ce, n3, lv.n1a, lv.n2b, lv.nbc, Tchild, sTchild, lv.i1a, lv.i3a, lv.i2b, lv.i3b,
+                              X33, R, lo.Tst, lv.ld3, Tnew, st))
+      return fail(rc);
+    if (int rc = gj_invert(n3, ce, X33, lo.Xinv, lv.ld3, (long long)n3 * lv.ld3, lst, st)) return fail(rc);
+    {
+      std::vector<double> hs;
+      int bad = check_pivots(lst, ce, n3, hs, st);
+      if (bad == -2) { set_error("cuda error during merge build"); return fail(HPS_ERR_CUDA); }
+      if (bad >= 0) return fail(singular(n3, hs[2 * bad], hs[2 * bad + 1], "merge", lv.node_index[bad]));
+    }
+    GemmArgs a{};  // S = Xinv [-Ta31 | Tb32]
+    a.M = n3; a.N = n12; a.K = n3; a.alpha = 1.0; a.beta = 0.0;
+    a.A = lo.Xinv; a.lda = lv.ld3; a.sA = (long long)n3 * lv.ld3; a.tA = 0;
+    a.B = R; a.ldb = n12; a.sB = (long long)n3 * n12; a.tB = 0;
+    a.C = lo.S; a.ldc = lv.ld12; a.sC = (long long)n3 * lv.ld12; a.batch = ce;
+    if (int rc = gemm(a, st)) return fail(rc);
+    if (needT) {
+      GemmArgs t{};  // T = blkdiag + Tstack S
+      t.M = n12; t.N = n12; t.K = n3; t.alpha = 1.0; t.beta = 1.0;
+      t.A = lo.Tst; t.lda = lv.ld3; t.sA = (long long)n12 * lv.ld3; t.tA = 0;
+      t.B = lo.S; t.ldb = lv.ld12; t.sB = (long long)n3 * lv.ld12; t.tB = 0;
+      t.D = Tnew; t.ldd = n12; t.sD = (long long)n12 * n12;
+      t.C = Tnew; t.ldc = n12; t.sC = (long long)n12 * n12; t.batch = ce;
+      if (int rc = gemm(t, st)) return fail(rc);
+    }
+    if (ce < lv.c) {  // constant coefficients: every node of a level is identical
+      if (int rc = broadcast_copies((long long)n3 * lv.ld3, lv.c, lo.Xinv, st)) return fail(rc);
+      if (int rc = broadcast_copies((long long)n12 * lv.ld3, lv.c, lo.Tst, st)) return fail(rc);
+      if (int rc = broadcast_copies((long long)n3 * lv.ld12, lv.c, lo.S, st)) return fail(rc);
+    }
+    if (!d->keep_dtn) tfree(Tchild);
+    tfree(X33); tfree(R); tfree(lst);
+    if (keepT) lo.T = Tnew;
+    Tchild = Tnew;
+    sTchild = O.shared_leaf ? 0 : (long long)n12 * n12;
+  }
+  if (P.depth > 0) O.root_T = O.lo[0].T;
+  if (cudaStreamSynchronize(st) != cudaSuccess) {
+    set_error("cuda error at end of build: %s", cudaGetErrorString(cudaGetLastError()));
+    return fail(HPS_ERR_CUDA);
+  }
+  for (void* p : tmp) cudaFree(p);
+  *out = h;
+  return HPS_OK;
+}
+
+int hps_ops_get_leaf(const hps_ops* h, int which, int leaf, double* host) {
+  if (!h) return HPS_ERR_ARG;
+  const Ops& O = h->O;
+  const Plan& P = *O.plan;
+  int l = O.shared_leaf ? 0 : leaf;
+  if (leaf < 0 || leaf >= P.L) { set_error("leaf out of range"); return HPS_ERR_ARG; }
+  const double* src; int rows, cols, ld;
+  if (which == 0) { src = O.Ainv + (size_t)l * P.ni * P.ldi; rows = P.ni; cols = P.ni; ld = P.ldi; }
+  else if (which == 1) { src = O.S_leaf + (size_t)l * P.ni * P.ldb; rows = P.ni; cols = P.nb; ld = P.ldb; }
+  else if (which == 2 && O.T_leaf) { src = O.T_leaf + (size_t)l * P.nb * P.nb; rows = P.nb; cols = P.nb; ld = P.nb; }
+  else { set_error("leaf block %d not available", which); return HPS_ERR_ARG; }
+  HPSB_CUDA(cudaDeviceSynchronize());
+  HPSB_CUDA(cudaMemcpy2D(host, cols * 8, src, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost));
+  return HPS_OK;
+}
+
+int hps_ops_get_merge(const hps_ops* h, int level, int node, int which, double* host) {
+  if (!h) return HPS_ERR_ARG;
+  const Ops& O = h->O;
+  const Plan& P = *O.plan;
+  if (level < 0 || level >= P.depth) { set_error("level out of range"); return HPS_ERR_ARG; }
+  const Level& lv = P.lv[level];
+  const LevelOps& lo = O.lo[level];
+  if (node < 0 || node >= lv.c) { set_error("node out of range"); return HPS_ERR_ARG; }
+  const double* src; int rows, cols, ld;
+  if (which == 0) { src = lo.Xinv + (size_t)node * lv.n3 * lv.ld3; rows = lv.n3; cols = lv.n3; ld = lv.ld3; }
+  else if (which == 1) { src = lo.Tst + (size_t)node * lv.n12 * lv.ld3; rows = lv.n12; cols = lv.n3; ld = lv.ld3; }
+  else if (which == 2) { src = lo.S + (size_t)node * lv.n3 * lv.ld12; rows = lv.n3; cols = lv.n12; ld = lv.ld12; }
+  else if (which == 3 && lo.T) {
+    int nn = O.shared_leaf ? 0 : node;
+    src = lo.T + (size_t)nn * lv.n12 * lv.n12; rows = lv.n12; cols = lv.n12; ld = lv.n12;
+  } else { set_error("merge block %d not available", which); return HPS_ERR_ARG; }
+  HPSB_CUDA(cudaDeviceSynchronize());
+  HPSB_CUDA(cudaMemcpy2D(host, cols * 8, src, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost));
+  return HPS_OK;
+}
+
+size_t hps_solve_workspace_bytes(const hps_plan* h, int k) { return h ? workspace_bytes(h->P, k) : 0; }
+
+int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
+              const double* jump, long long ld_jump, double inv_dt, double* u, long long ld_u, void* ws,
+              size_t ws_bytes, void* stream) {
+  if (!h || !fb || !u || !ws) { set_error("hps_solve: null argument"); return HPS_ERR_ARG; }
+  return solve(h->O, k, fb, ld_f, g, ld_g, jump, ld_jump, inv_dt, u, ld_u, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

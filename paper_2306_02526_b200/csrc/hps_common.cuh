@@ -1,0 +1,56 @@
+// Common helpers for the hpstep-b200 CUDA library (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+namespace hpsb {
+
+constexpr int kNumSMs = 148;  // B200
+
+// thread-local last error, surfaced through hps_last_error()
+void set_error(const char* fmt, ...);
+void set_error_node(long long node);
+
+#define HPSB_CUDA(expr)                                                        \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      ::hpsb::set_error("%s:%d: %s -> %s", __FILE__, __LINE__, #expr,          \
+                        cudaGetErrorString(_e));                               \
+      return -2;                                                               \
+    }                                                                          \
+  } while (0)
+
+#define HPSB_LAUNCH_CHECK()                                                    \
+  do {                                                                         \
+    cudaError_t _e = cudaGetLastError();                                       \
+    if (_e != cudaSuccess) {                                                   \
+      ::hpsb::set_error("%s:%d: launch failed: %s", __FILE__, __LINE__,         \
+                        cudaGetErrorString(_e));                               \
+      return -2;                                                               \
+    }                                                                          \
+  } while (0)
+
+__host__ __device__ inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// Batched FP64 GEMM:  C[b] = alpha * op(A[b]) * op(B[b]) + beta * D[b]
+// row-major operands; op(X) = X or X^T.  D may alias C (beta applied to D).
+// Any stride may be 0 (broadcast one matrix over the batch).
+// ---------------------------------------------------------------------------
+struct GemmArgs {
+  int M, N, K;
+  double alpha, beta;
+  const double* A; long long lda, sA; int tA;
+  const double* B; long long ldb, sB; int tB;
+  const double* D; long long ldd, sD;
+  double* C; long long ldc, sC;
+  int batch;
+};
+int gemm(const GemmArgs& g, cudaStream_t st);
+
+}  // namespace hpsb

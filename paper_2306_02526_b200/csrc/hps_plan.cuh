@@ -1,0 +1,102 @@
+// Internal plan / operator-set structures (device-resident, level-contiguous).
+#pragma once
+
+#include <vector>
+
+#include "hps_common.cuh"
+
+namespace hpsb {
+
+// One parent level of the binary tree (level 0 = root).  All nodes of a
+// level share the same shapes and the same child-local index maps
+// (i1a, i3a, i2b, i3b); only the global ids (gidx_bnd, j3) differ per node.
+struct Level {
+  int c = 0;       // nodes on the level
+  int n3 = 0;      // |J3| interface size
+  int n1a = 0;     // |J1| (alpha's outer boundary)
+  int n2b = 0;     // |J2|
+  int n12 = 0;     // n1a + n2b = node boundary size
+  int nbc = 0;     // child boundary size (= n1a + n3 = n2b + n3)
+  int ld3 = 0;     // even-padded row length for n3-column matrices
+  int ld12 = 0;    // even-padded row length for n12-column matrices
+  int *i1a = nullptr, *i3a = nullptr, *i2b = nullptr, *i3b = nullptr;  // device
+  int* gidx_bnd = nullptr;  // device, c x n12 global ids
+  int* j3 = nullptr;        // device, c x n3 global ids
+  std::vector<long long> node_index;  // host: DFS node index (error reports)
+  std::vector<int> h_i1a, h_i3a, h_i2b, h_i3b;
+};
+
+struct Plan {
+  int n1 = 0, n2 = 0, p = 0, q = 0, ni = 0, nb = 0, L = 0, depth = 0, nbd = 0;
+  long long N = 0;
+  std::vector<Level> lv;          // depth entries, root first
+  int* leaf_bnd_gidx = nullptr;   // device L x nb
+  int* boundary_ids = nullptr;    // device nbd
+  std::vector<long long> leaf_node_index;  // host
+  int ldi = 0;                    // even-padded ni
+  int ldb = 0;                    // even-padded nb
+};
+
+struct LevelOps {
+  double* Xinv = nullptr;  // c x n3 x ld3
+  double* Tst = nullptr;   // c x n12 x ld3
+  double* S = nullptr;     // c x n3 x ld12
+  double* T = nullptr;     // c x n12 x n12 (only when keep_dtn)
+};
+
+struct Ops {
+  Plan* plan = nullptr;
+  double sigma = 0.0, dtg = 0.0;
+  int shared_leaf = 1;         // constant coefficients: one leaf operator set
+  int Lc = 1;                  // number of stored leaf operator sets (1 or L)
+  double* Ainv = nullptr;      // Lc x ni x ldi
+  double* S_leaf = nullptr;    // Lc x ni x ldb
+  double* T_leaf = nullptr;    // Lc x nb x nb (kept only when keep_dtn)
+  double* D_bi = nullptr;      // nb x ni (shared stencil rows)
+  std::vector<LevelOps> lo;    // depth entries, root first
+  double* root_T = nullptr;    // n12 x n12 of the root (keep_dtn)
+  size_t bytes = 0;            // device bytes owned
+  std::vector<void*> allocs;
+};
+
+// per-solve workspace carve-up (per-rhs strides in doubles)
+struct Workspace {
+  double* W = nullptr;      // k x L x ni
+  double* Hleaf = nullptr;  // k x L x nb
+  double* Ub = nullptr;     // k x L x nb
+  std::vector<double*> H;   // per level d (d>=1): k x c x n12
+  std::vector<double*> W3;  // per level: k x c x n3
+};
+size_t workspace_bytes(const Plan& P, int k);
+void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
+
+// level GEMV launcher (see level_gemv.cu)
+enum GemvMode { GEMV_UPX = 0, GEMV_UPT = 1, GEMV_DOWN = 2, GEMV_LEAF = 3 };
+
+struct GemvArgs {
+  int mode;
+  int c;                        // number of matrices (nodes / leaves)
+  int R, C, ldm;                // rows, columns, padded row length (even)
+  const double* M; long long sM;
+  int k;                        // right-hand sides
+  // UPX / UPT
+  const double* Hc; int nbc; long long Hc_k;
+  double* Hout; int n12; long long Hout_k;
+  double* W3; int n3; long long W3_k;
+  const int *i1a, *i3a, *i2b, *i3b; int n1a;
+  const double* jump; long long jump_k; double inv_dt; const int* j3;
+  // DOWN
+  double* u; long long u_k; const int* gidx;
+  // LEAF: y[b] = M[b] x[b] (+ add[b])
+  const double* xin; long long xin_k, xin_s;
+  double* yout; long long yout_k, yout_s;
+  const double* yadd; long long yadd_k, yadd_s;
+};
+int gemv_level(const GemvArgs& a, cudaStream_t st);
+
+// solve entry (solve.cu)
+int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
+          const double* jump, long long ld_jump, double inv_dt, double* u, long long ld_u,
+          void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace hpsb

@@ -1,0 +1,180 @@
+// The per-stage HPS solve (solver.py:201-276) as a sequence of level-batched
+// launches on one stream: boundary scatter, leaf upward pass, level upward
+// merges (deepest first), level downward sweep (root first), leaf downward
+// reconstruction.  No host synchronisation; capturable in a CUDA graph.
+#include "hps_plan.cuh"
+
+namespace hpsb {
+
+namespace {
+
+__global__ void k_bnd_scatter(int k, int nbd, const int* __restrict__ ids, const double* __restrict__ fb,
+                              long long ld_f, double* __restrict__ u, long long ld_u) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)k * nbd) return;
+  int kk = (int)(e / nbd), i = (int)(e % nbd);
+  u[kk * ld_u + ids[i]] = fb[kk * ld_f + i];
+}
+
+__global__ void k_leaf_gather(int k, int L, int nb, const int* __restrict__ lbg, const double* __restrict__ u,
+                              long long ld_u, double* __restrict__ ub) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long per = (long long)L * nb;
+  if (e >= (long long)k * per) return;
+  int kk = (int)(e / per);
+  long long r = e % per;
+  ub[kk * per + r] = u[kk * ld_u + lbg[r]];
+}
+
+}  // namespace
+
+size_t workspace_bytes(const Plan& P, int k) {
+  size_t n = 0;
+  auto add = [&](long long cnt) { n += ((size_t)cnt * k * 8 + 255) & ~(size_t)255; };
+  add((long long)P.L * P.ni);
+  add((long long)P.L * P.nb);
+  add((long long)P.L * P.nb);
+  for (int d = 0; d < P.depth; ++d) {
+    if (d >= 1) add((long long)P.lv[d].c * P.lv[d].n12);
+    add((long long)P.lv[d].c * P.lv[d].n3);
+  }
+  return n + 256;
+}
+
+void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
+  char* p = (char*)(((uintptr_t)base + 255) & ~(uintptr_t)255);
+  auto take = [&](long long cnt) {
+    double* r = (double*)p;
+    p += ((size_t)cnt * k * 8 + 255) & ~(size_t)255;
+    return r;
+  };
+  ws.W = take((long long)P.L * P.ni);
+  ws.Hleaf = take((long long)P.L * P.nb);
+  ws.Ub = take((long long)P.L * P.nb);
+  ws.H.assign(P.depth, nullptr);
+  ws.W3.assign(P.depth, nullptr);
+  for (int d = 0; d < P.depth; ++d) {
+    if (d >= 1) ws.H[d] = take((long long)P.lv[d].c * P.lv[d].n12);
+    ws.W3[d] = take((long long)P.lv[d].c * P.lv[d].n3);
+  }
+}
+
+int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
+          const double* jump, long long ld_jump, double inv_dt, double* u, long long ld_u,
+          void* wsp, size_t ws_bytes, cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  if (k <= 0) return 0;
+  if (ws_bytes < workspace_bytes(P, k)) {
+    set_error("solve: workspace too small (%zu < %zu)", ws_bytes, workspace_bytes(P, k));
+    return -1;
+  }
+  Workspace ws;
+  carve_workspace(P, k, wsp, ws);
+  const long long Lni = (long long)P.L * P.ni, Lnb = (long long)P.L * P.nb;
+  const int T = 256;
+
+  // (1) Dirichlet data into u (solver.py:259-260)
+  {
+    long long n = (long long)k * P.nbd;
+    if (n > 0) {
+      k_bnd_scatter<<<(unsigned)cdiv(n, T), T, 0, st>>>(k, P.nbd, P.boundary_ids, fb, ld_f, u, ld_u);
+      HPSB_LAUNCH_CHECK();
+    }
+  }
+
+  const bool up = (g != nullptr) || (jump != nullptr);
+  // (2) leaf particular solutions and their fluxes (solver.py:219-230)
+  if (g) {
+    if (ops.shared_leaf) {
+      // W^T (L x ni) = G_int^T (L x ni) * Ainv^T, one GEMM per rhs
+      GemmArgs a{};
+      a.M = P.L; a.N = P.ni; a.K = P.ni; a.alpha = 1.0; a.beta = 0.0;
+      a.A = g; a.lda = P.ni; a.sA = ld_g; a.tA = 0;
+      a.B = ops.Ainv; a.ldb = P.ldi; a.sB = 0; a.tB = 1;
+      a.C = ws.W; a.ldc = P.ni; a.sC = Lni; a.batch = k;
+      if (int rc = gemm(a, st)) return rc;
+    } else {
+      GemvArgs a{};
+      a.mode = GEMV_LEAF; a.c = P.L; a.R = P.ni; a.C = P.ni; a.ldm = P.ldi;
+      a.M = ops.Ainv; a.sM = (long long)P.ni * P.ldi; a.k = k;
+      a.xin = g; a.xin_k = ld_g; a.xin_s = P.ni;
+      a.yout = ws.W; a.yout_k = Lni; a.yout_s = P.ni;
+      if (int rc = gemv_level(a, st)) return rc;
+    }
+    // H^T (k*L x nb) = W (k*L x ni) * D_bi^T
+    GemmArgs h{};
+    h.M = k * P.L; h.N = P.nb; h.K = P.ni; h.alpha = 1.0; h.beta = 0.0;
+    h.A = ws.W; h.lda = P.ni; h.sA = 0; h.tA = 0;
+    h.B = ops.D_bi; h.ldb = P.ni; h.sB = 0; h.tB = 1;
+    h.C = ws.Hleaf; h.ldc = P.nb; h.sC = 0; h.batch = 1;
+    if (int rc = gemm(h, st)) return rc;
+  } else if (jump) {
+    HPSB_CUDA(cudaMemsetAsync(ws.Hleaf, 0, (size_t)k * Lnb * 8, st));
+  }
+
+  // (3) upward merges, deepest level first (solver.py:243-256)
+  if (up) {
+    for (int d = P.depth - 1; d >= 0; --d) {
+      const Level& lv = P.lv[d];
+      const LevelOps& lo = ops.lo[d];
+      const double* Hc = (d == P.depth - 1) ? ws.Hleaf : ws.H[d + 1];
+      long long Hc_k = (d == P.depth - 1) ? Lnb : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
+      GemvArgs a{};
+      a.c = lv.c; a.k = k;
+      a.Hc = Hc; a.nbc = lv.nbc; a.Hc_k = Hc_k;
+      a.W3 = ws.W3[d]; a.n3 = lv.n3; a.W3_k = (long long)lv.c * lv.n3;
+      a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
+      a.n12 = lv.n12;
+      a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt; a.j3 = lv.j3;
+      a.mode = GEMV_UPX; a.R = lv.n3; a.C = lv.n3; a.ldm = lv.ld3;
+      a.M = lo.Xinv; a.sM = (long long)lv.n3 * lv.ld3;
+      if (int rc = gemv_level(a, st)) return rc;
+      if (d == 0) break;  // the root's outer flux is never consumed
+      a.mode = GEMV_UPT; a.R = lv.n12; a.C = lv.n3; a.ldm = lv.ld3;
+      a.M = lo.Tst; a.sM = (long long)lv.n12 * lv.ld3;
+      a.Hout = ws.H[d]; a.Hout_k = (long long)lv.c * lv.n12;
+      if (int rc = gemv_level(a, st)) return rc;
+    }
+  }
+
+  // (4) downward sweep, root first (solver.py:258-268)
+  for (int d = 0; d < P.depth; ++d) {
+    const Level& lv = P.lv[d];
+    const LevelOps& lo = ops.lo[d];
+    GemvArgs a{};
+    a.mode = GEMV_DOWN; a.c = lv.c; a.k = k;
+    a.R = lv.n3; a.C = lv.n12; a.ldm = lv.ld12;
+    a.M = lo.S; a.sM = (long long)lv.n3 * lv.ld12;
+    a.u = u; a.u_k = ld_u; a.gidx = lv.gidx_bnd; a.j3 = lv.j3;
+    a.n3 = lv.n3; a.n12 = lv.n12;
+    a.W3 = up ? ws.W3[d] : nullptr; a.W3_k = (long long)lv.c * lv.n3;
+    if (int rc = gemv_level(a, st)) return rc;
+  }
+
+  // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
+  {
+    long long n = (long long)k * Lnb;
+    k_leaf_gather<<<(unsigned)cdiv(n, T), T, 0, st>>>(k, P.L, P.nb, P.leaf_bnd_gidx, u, ld_u, ws.Ub);
+    HPSB_LAUNCH_CHECK();
+    if (ops.shared_leaf) {
+      GemmArgs a{};
+      a.M = P.L; a.N = P.ni; a.K = P.nb; a.alpha = 1.0;
+      a.A = ws.Ub; a.lda = P.nb; a.sA = Lnb; a.tA = 0;
+      a.B = ops.S_leaf; a.ldb = P.ldb; a.sB = 0; a.tB = 1;
+      a.beta = g ? 1.0 : 0.0; a.D = g ? ws.W : nullptr; a.ldd = P.ni; a.sD = Lni;
+      a.C = u; a.ldc = P.ni; a.sC = ld_u; a.batch = k;
+      if (int rc = gemm(a, st)) return rc;
+    } else {
+      GemvArgs a{};
+      a.mode = GEMV_LEAF; a.c = P.L; a.R = P.ni; a.C = P.nb; a.ldm = P.ldb;
+      a.M = ops.S_leaf; a.sM = (long long)P.ni * P.ldb; a.k = k;
+      a.xin = ws.Ub; a.xin_k = Lnb; a.xin_s = P.nb;
+      a.yout = u; a.yout_k = ld_u; a.yout_s = P.ni;
+      a.yadd = g ? ws.W : nullptr; a.yadd_k = Lni; a.yadd_s = P.ni;
+      if (int rc = gemv_level(a, st)) return rc;
+    }
+  }
+  return 0;
+}
+
+}  // namespace hpsb

@@ -1,0 +1,354 @@
+"""Drop-in ``HpsOperatorSet`` / ``build`` backed by the sm_100a library.
+
+Mirrors the reference API (solver.py:84-390 of hpstep): same constructor,
+``solve_with_body_load`` / ``solve_homogeneous`` / ``solve_penalized``, the
+``sigma`` / ``dt_gamma`` / ``shift`` properties, the squeeze rule, the
+boundary-shape ``ValueError``, ``InvalidStepError`` for dt <= 0 and
+``SingularMatrixError`` naming the node.  The build and every solve run on
+the GPU (no CPU fallback): numpy inputs are copied to the device and the
+result copied back; torch CUDA tensors stay on the device.
+"""
+
+import ctypes
+import hashlib
+import pickle
+
+import numpy as np
+
+from . import _lib
+from .device import cuda_device, current_stream_handle, ndim, torch
+from .errors import HpstepError, InvalidStepError
+from .operators import EllipticDiscretization
+
+FORMAT_VERSION = 1
+
+
+class DevicePlan:
+    """Device copy of the tree numbering (one per tree and device)."""
+
+    def __init__(self, tree):
+        lib = _lib.load()
+        cuda_device()  # raises without a GPU
+        self.tree = tree
+        lms = tree.level_maps
+        keep = []
+
+        def arr(a, dt=np.int32):
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a
+
+        shape = arr([v for lm in lms for v in (lm.count, lm.n3, lm.n1a, lm.n2b, lm.nbc)] or [0])
+        IP = _lib.c_int_p * max(1, len(lms))
+        LP = _lib.c_ll_p * max(1, len(lms))
+
+        def ptrs(key, dt=np.int32, T=IP, conv=_lib.int_ptr):
+            return T(*[conv(arr(getattr(lm, key), dt)) for lm in lms])
+
+        d = _lib.PlanDesc()
+        d.n1, d.n2, d.p, d.depth = tree.n1, tree.n2, tree.p, tree.depth
+        d.N, d.L, d.ni, d.nb = tree.N, tree.L, tree.ni, tree.nb
+        d.nbd = tree.boundary_ids.size
+        d.lvl_shape = _lib.int_ptr(shape)
+        d.lvl_i1a, d.lvl_i3a = ptrs("i1a"), ptrs("i3a")
+        d.lvl_i2b, d.lvl_i3b = ptrs("i2b"), ptrs("i3b")
+        d.lvl_gidx_bnd, d.lvl_j3 = ptrs("gidx_bnd"), ptrs("j3")
+        d.lvl_node_index = ptrs("node_index", np.int64, LP, _lib.ll_ptr)
+        d.leaf_bnd_gidx = _lib.int_ptr(arr(tree.leaf_bnd_gidx))
+        d.leaf_node_index = _lib.ll_ptr(arr(tree.leaves, np.int64))
+        d.boundary_ids = _lib.int_ptr(arr(tree.boundary_ids))
+        h = ctypes.c_void_p()
+        _lib.check(lib.hps_plan_create(ctypes.byref(d), ctypes.byref(h)), "hps_plan_create")
+        self.handle = h
+        self._lib = lib
+        self._ws = {}
+        dev = cuda_device()
+        self.boundary_ids = torch.as_tensor(tree.boundary_ids, device=dev)
+
+    def workspace(self, k):
+        ws = self._ws.get(k)
+        if ws is None:
+            nbytes = self._lib.hps_solve_workspace_bytes(self.handle, k)
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=cuda_device())
+            self._ws[k] = ws
+        return ws
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.hps_plan_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def device_plan(tree):
+    p = getattr(tree, "_device_plan", None)
+    if p is None:
+        p = DevicePlan(tree)
+        tree._device_plan = p
+    return p
+
+
+class _InverseFactor:
+    """Stand-in for ``DenseFactorization`` over a downloaded explicit inverse."""
+
+    def __init__(self, inv):
+        self.inv = inv
+        self.n = inv.shape[0]
+
+    def solve(self, B):
+        return self.inv @ np.asarray(B, dtype=float)
+
+
+class LeafOperators:
+    def __init__(self, S, T, Aii_factor, D_edge):
+        self.S, self.T, self.Aii_factor, self.D_edge = S, T, Aii_factor, D_edge
+
+
+class MergeOperators:
+    def __init__(self, S, X33_factor, Tstack, T=None):
+        self.S, self.X33_factor, self.Tstack, self.T = S, X33_factor, Tstack, T
+
+
+class HpsOperatorSet:
+    """Per-node HPS operators of ``sigma*I + dt_gamma*A``, resident on the GPU.
+
+    Read-only after construction; concurrent solves on different streams are
+    safe (each stream gets its own workspace).
+    """
+
+    def __init__(self, disc, sigma, dt_gamma, keep_dtn=False, threads=None):
+        self.disc = disc
+        self.tree = disc.tree
+        self.sigma = float(sigma)
+        self.dt_gamma = float(dt_gamma)
+        self.keep_dtn = bool(keep_dtn)
+        st = disc.stencil
+        self.D_bi = st.D_bnd[:, :st.ni]
+        self.plan = device_plan(self.tree)
+        self._build()
+
+    @property
+    def shift(self):
+        return self.dt_gamma
+
+    def _build(self):
+        disc, st = self.disc, self.disc.stencil
+        lib = self.plan._lib
+        ni = st.ni
+        samp = disc.coefficient_samples()[:, :, :ni]          # interior points only
+        cf = disc.coeffs
+        keep = [np.ascontiguousarray(samp, dtype=float)]
+        rows = [np.ascontiguousarray(M[:ni], dtype=float) for M in (st.D2x, st.D2y, st.D1x, st.D1y)]
+        dbnd = np.ascontiguousarray(st.D_bnd, dtype=float)
+        keep += rows + [dbnd]
+        d = _lib.BuildDesc()
+        d.sigma, d.dt_gamma = self.sigma, self.dt_gamma
+        d.shared_leaf = 1 if cf.is_constant else 0
+        d.keep_dtn = 1 if self.keep_dtn else 0
+        d.coef = _lib.dbl_ptr(keep[0])
+        d.has_c1 = int(cf.c1 is not None)
+        d.has_c2 = int(cf.c2 is not None)
+        d.has_c = int(cf.c is not None)
+        d.D2x, d.D2y, d.D1x, d.D1y = (_lib.dbl_ptr(r) for r in rows)
+        d.D_bnd = _lib.dbl_ptr(dbnd)
+        h = ctypes.c_void_p()
+        rc = lib.hps_ops_build(self.plan.handle, ctypes.byref(d), current_stream_handle(),
+                               ctypes.byref(h))
+        _lib.check(rc, "hps_ops_build")
+        self.handle = h
+        self._lib = lib
+        self.parent_order = [int(i) for lm in self.tree.level_maps for i in lm.node_index]
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self._lib.hps_ops_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    @property
+    def device_bytes(self):
+        return int(self._lib.hps_ops_device_bytes(self.handle))
+
+    # -- solves ------------------------------------------------------------------
+    def solve_homogeneous(self, f):
+        return self._solve(f, None, None, None)
+
+    def solve_with_body_load(self, f, g):
+        return self._solve(f, g, None, None)
+
+    def solve_penalized(self, f, g, flux_jump, dt):
+        if dt <= 0:
+            raise InvalidStepError(f"time step must be positive, got {dt}")
+        return self._solve(f, g, flux_jump, 1.0 / dt)
+
+    def _boundary_values(self, f, dev):
+        """(kf, nbd) device tensor from scalar / (nbd,) / (N,) / stacked data
+        (reference solver.py:162-174)."""
+        tree = self.tree
+        nbd = tree.boundary_ids.size
+        if torch.is_tensor(f):
+            F = f.to(device=dev, dtype=torch.float64)
+        else:
+            F = np.asarray(f, dtype=float)
+            if F.ndim == 0:
+                return torch.full((1, nbd), float(F), dtype=torch.float64, device=dev)
+            if F.shape[-1] == tree.N:
+                F = np.atleast_2d(F)[:, tree.boundary_ids]
+            elif F.shape[-1] != nbd:
+                raise ValueError(f"boundary data must have trailing size {nbd} or {tree.N}, "
+                                 f"got {F.shape}")
+            return torch.as_tensor(np.ascontiguousarray(np.atleast_2d(F)), device=dev)
+        if F.ndim == 0:
+            return F.reshape(1, 1).expand(1, nbd).contiguous()
+        if F.shape[-1] == tree.N:
+            return torch.atleast_2d(F)[:, self.plan.boundary_ids].contiguous()
+        if F.shape[-1] == nbd:
+            return torch.atleast_2d(F).contiguous()
+        raise ValueError(f"boundary data must have trailing size {nbd} or {tree.N}, "
+                         f"got {tuple(F.shape)}")
+
+    def _solve(self, f, g, flux_jump, inv_dt, out=None):
+        tree = self.tree
+        dev = cuda_device()
+        as_numpy = not any(torch.is_tensor(x) for x in (f, g, flux_jump))
+        fb = self._boundary_values(f, dev)
+        k = fb.shape[0]
+        squeeze = (ndim(f) <= 1) if g is None else (ndim(g) == 1)
+        G = None
+        if g is not None:
+            G = torch.atleast_2d(torch.as_tensor(g, dtype=torch.float64, device=dev))
+            k = max(k, G.shape[0])
+        J = None
+        if flux_jump is not None:
+            J = torch.atleast_2d(torch.as_tensor(flux_jump, dtype=torch.float64, device=dev))
+            if G is None:
+                k = max(k, J.shape[0])
+        ld_f = fb.shape[1] if fb.shape[0] > 1 else 0
+        if fb.shape[0] not in (1, k):
+            raise ValueError(f"boundary data has {fb.shape[0]} rows for {k} right-hand sides")
+        for name, X in (("body load", G), ("flux jump", J)):
+            if X is not None and (X.shape[-1] != tree.N or X.shape[0] not in (1, k)):
+                raise ValueError(f"{name} must have shape ({k}, {tree.N}), got {tuple(X.shape)}")
+        G = None if G is None else G.contiguous()
+        J = None if J is None else J.contiguous()
+        U = out if out is not None else torch.empty((k, tree.N), dtype=torch.float64, device=dev)
+        ws = self.plan.workspace(k)
+        ld_g = 0 if G is None or G.shape[0] == 1 else tree.N
+        ld_j = 0 if J is None or J.shape[0] == 1 else tree.N
+        rc = self._lib.hps_solve(
+            self.handle, k, fb.data_ptr(), ld_f,
+            None if G is None else G.data_ptr(), ld_g,
+            None if J is None else J.data_ptr(), ld_j,
+            0.0 if inv_dt is None else float(inv_dt),
+            U.data_ptr(), tree.N, ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_solve")
+        res = U[0] if squeeze else U
+        if as_numpy:
+            return res.cpu().numpy()
+        return res
+
+    # -- operator views (reference solver.py:339-348) ---------------------------------
+    def _leaf_block(self, which, leaf):
+        st = self.disc.stencil
+        shape = {0: (st.ni, st.ni), 1: (st.ni, st.nb), 2: (st.nb, st.nb)}[which]
+        out = np.empty(shape)
+        _lib.check(self._lib.hps_ops_get_leaf(self.handle, which, leaf, _lib.dbl_ptr(out)),
+                   "hps_ops_get_leaf")
+        return out
+
+    def _merge_block(self, level, pos, which):
+        lm = self.tree.level_maps[level]
+        shape = {0: (lm.n3, lm.n3), 1: (lm.n12, lm.n3), 2: (lm.n3, lm.n12), 3: (lm.n12, lm.n12)}[which]
+        out = np.empty(shape)
+        _lib.check(self._lib.hps_ops_get_merge(self.handle, level, pos, which, _lib.dbl_ptr(out)),
+                   "hps_ops_get_merge")
+        return out
+
+    def leaf_operators(self, leaf_id):
+        T = self._leaf_block(2, leaf_id) if self.keep_dtn else None
+        return LeafOperators(S=self._leaf_block(1, leaf_id), T=T,
+                             Aii_factor=_InverseFactor(self._leaf_block(0, leaf_id)),
+                             D_edge=self.disc.stencil.D_bnd)
+
+    def _locate(self, node_index):
+        for d, lm in enumerate(self.tree.level_maps):
+            hit = np.nonzero(lm.node_index == node_index)[0]
+            if hit.size:
+                return d, int(hit[0])
+        raise KeyError(node_index)
+
+    def merge_operators(self, node_index):
+        d, pos = self._locate(node_index)
+        T = self._merge_block(d, pos, 3) if (self.keep_dtn or d == 0) else None
+        return MergeOperators(S=self._merge_block(d, pos, 2),
+                              X33_factor=_InverseFactor(self._merge_block(d, pos, 0)),
+                              Tstack=self._merge_block(d, pos, 1), T=T)
+
+    @property
+    def merges(self):
+        return {i: _LazyMerge(self, i) for i in self.parent_order}
+
+    @property
+    def leaf_factors(self):
+        return _LeafFactors(self)
+
+    @property
+    def S_leaf(self):
+        S0 = self._leaf_block(1, 0)
+        if self.disc.coeffs.is_constant:
+            return np.broadcast_to(S0, (self.tree.L,) + S0.shape)
+        return np.stack([self._leaf_block(1, l) for l in range(self.tree.L)])
+
+    @property
+    def root_T(self):
+        return self._merge_block(0, 0, 3) if self.tree.depth > 0 else None
+
+    # -- persistence (reference solver.py:280-337) -----------------------------------
+    def header(self):
+        tree = self.tree
+        return {"version": FORMAT_VERSION, "dim": tree.dim, "bounds": tree.bounds, "n1": tree.n1,
+                "n2": tree.n2, "p": tree.p, "sigma": self.sigma, "dt_gamma": self.dt_gamma,
+                "coeff_hash": coefficient_hash(self.disc)}
+
+
+class _LazyMerge:
+    def __init__(self, ops, idx):
+        self._ops, self._idx = ops, idx
+
+    def __getattr__(self, name):
+        mo = self._ops.merge_operators(self._idx)
+        return getattr(mo, name)
+
+
+class _LeafFactors:
+    def __init__(self, ops):
+        self._ops = ops
+
+    def __len__(self):
+        return self._ops.tree.L
+
+    def __getitem__(self, i):
+        return _InverseFactor(self._ops._leaf_block(0, i))
+
+
+def coefficient_hash(disc):
+    """Hash of coefficient samples identifying the operator (solver.py:351-361)."""
+    pts = [disc.leaf_points(0)]
+    if disc.tree.leaf_count > 1:
+        pts.append(disc.leaf_points(disc.tree.leaf_count - 1))
+    h = hashlib.sha256()
+    for p in pts:
+        s = disc.coeffs.evaluate(p)
+        for key in sorted(s):
+            h.update(np.ascontiguousarray(s[key]).tobytes())
+    return h.hexdigest()
+
+
+def build(tree, coeffs, sigma=0.0, dt_gamma=1.0, disc=None, keep_dtn=False, threads=None):
+    """Build the operator set for ``sigma*I + dt_gamma*A`` on the GPU."""
+    if disc is None:
+        disc = EllipticDiscretization(tree, coeffs)
+    return HpsOperatorSet(disc, sigma=sigma, dt_gamma=dt_gamma, keep_dtn=keep_dtn, threads=threads)

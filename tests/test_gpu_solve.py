@@ -1,0 +1,69 @@
+"""Device solve / build parity against the reference goldens (needs a B200)."""
+
+import numpy as np
+import pytest
+
+from tests.problems import SOLVE_CASES, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10   # north-star parity bar: relative L2 per solve
+
+
+def _ops(z, name, keep_dtn=True):
+    import paper_2306_02526_b200 as hb
+    fields, bounds = SOLVE_CASES[name]
+    n1, n2, p = (int(v) for v in z["shape"])
+    tree = hb.build_tree(bounds, n1, n2, p)
+    coeffs = hb.OperatorCoefficients(**fields())
+    ops = hb.build(tree, coeffs, sigma=float(z["sigma"]), dt_gamma=float(z["dt_gamma"]),
+                   keep_dtn=keep_dtn)
+    return tree, ops
+
+
+@pytest.mark.parametrize("name", sorted(SOLVE_CASES))
+def test_device_solve_matches_reference(golden, name):
+    z = golden("solve_" + name)
+    tree, ops = _ops(z, name)
+    u = ops.solve_with_body_load(z["f"], z["g"])
+    assert u.shape == z["u"].shape
+    assert rel_l2(u, z["u"]) < TOL
+    uh = ops.solve_homogeneous(z["f"])
+    assert rel_l2(uh, z["u_hom"]) < TOL
+    if "u_pen" in z:
+        up = ops.solve_penalized(z["f"], z["g"], z["jump"], float(z["dt_pen"]))
+        assert rel_l2(up, z["u_pen"]) < TOL
+
+
+@pytest.mark.parametrize("name", sorted(SOLVE_CASES))
+def test_device_build_matches_reference(golden, name):
+    z = golden("solve_" + name)
+    tree, ops = _ops(z, name)
+    lo = ops.leaf_operators(0)
+    assert rel_l2(lo.S, z["S_leaf0"]) < TOL
+    assert rel_l2(lo.T, z["T_leaf0"]) < TOL
+    if "root_S" in z:
+        mo = ops.merge_operators(0)
+        assert rel_l2(mo.S, z["root_S"]) < TOL
+        assert rel_l2(mo.Tstack, z["root_Tstack"]) < TOL
+        assert rel_l2(mo.T, z["root_T"]) < TOL
+
+
+def test_device_solve_torch_inputs_stay_on_device(golden):
+    import torch
+    z = golden("solve_lap2x2p10")
+    tree, ops = _ops(z, "lap2x2p10", keep_dtn=False)
+    f = torch.as_tensor(z["f"], device="cuda")
+    g = torch.as_tensor(z["g"], device="cuda")
+    u = ops.solve_with_body_load(f, g)
+    assert u.is_cuda and u.shape == (tree.N,)
+    assert rel_l2(u.cpu().numpy(), z["u"]) < TOL
+
+
+def test_device_singular_leaf_names_node():
+    import paper_2306_02526_b200 as hb
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 1, 1, 8)
+    zero = hb.OperatorCoefficients(c11=0.0, c22=0.0)
+    with pytest.raises(hb.SingularMatrixError) as exc:
+        hb.build(tree, zero, sigma=0.0, dt_gamma=1.0)
+    assert "leaf node" in str(exc.value)

@@ -1,0 +1,86 @@
+"""Product host logic (no GPU): tree numbering and stencil against the reference
+goldens and the oracle; the C-ABI library loads and exports every symbol."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import hps_oracle as O
+
+TREES = ["2x2p6", "4x2p9", "4x4p7", "8x8p12", "rect4x2p8", "rect2x4p8"]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("name", TREES)
+def test_product_tree_matches_reference(golden, name):
+    from paper_2306_02526_b200.tree import build_tree
+    z = golden("tree_" + name)
+    n1, n2, p = (int(v) for v in z["shape"])
+    t = build_tree(z["bounds"], n1, n2, p)
+    assert t.N == int(z["N"])
+    assert np.array_equal(t.points, z["points"])
+    for key in ("boundary_ids", "interface_ids", "multiplicity", "leaf_int_gidx",
+                "leaf_bnd_gidx", "leaf_bnd_sign"):
+        assert np.array_equal(getattr(t, key), z[key]), key
+    parents = [k for lvl in t.levels for k in lvl if not t.nodes[k].is_leaf]
+    assert np.array_equal(parents, z["parents"])
+    for key in ("j3", "i1a", "i3a", "i2b", "i3b", "gidx_bnd"):
+        got = np.concatenate([getattr(t.nodes[k], key) for k in parents])
+        assert np.array_equal(got, z[key]), key
+
+
+@pytest.mark.parametrize("name", TREES)
+def test_product_stencil_matches_oracle(golden, name):
+    from paper_2306_02526_b200.operators import LeafStencil
+    from paper_2306_02526_b200.tree import build_tree
+    z = golden("tree_" + name)
+    n1, n2, p = (int(v) for v in z["shape"])
+    st = LeafStencil(build_tree(z["bounds"], n1, n2, p))
+    ost = O.OStencil(O.OTree(z["bounds"], n1, n2, p))
+    for key in ("D1x", "D2x", "D1y", "D2y", "D_bnd", "Ex1", "Ex2", "Ey1", "Ey2", "local_xy"):
+        assert np.array_equal(getattr(st, key), getattr(ost, key)), key
+
+
+def test_level_maps_uniform_and_shapes_large():
+    """C2-shaped tree: closed-form level shapes and uniform maps."""
+    from paper_2306_02526_b200.tree import build_tree
+    t = build_tree(((0.0, 1.0), (0.0, 1.0)), 128, 128, 16)
+    assert t.N == 3673600 and t.depth == 14
+    q = 14
+    for d, lm in enumerate(t.level_maps):
+        m = 128 >> (d // 2)
+        if d % 2 == 0:
+            assert (lm.n3, lm.n12) == (m * q, 4 * m * q)
+        else:
+            assert (lm.n3, lm.n12) == (m * q // 2, 3 * m * q)
+        assert lm.gidx_bnd.shape == (2 ** d, lm.n12)
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2306_02526_b200 import _lib
+    lib = _lib.load()
+    hdr = open(os.path.join(ROOT, "include", "hpstep_b200.h")).read()
+    names = set(re.findall(r"\b(hps_[a-z_]+)\s*\(", hdr))
+    assert names, "no declarations parsed"
+    for n in sorted(names):
+        assert hasattr(lib, n), n
+    assert names <= set(_lib.SIGNATURES), names - set(_lib.SIGNATURES)
+    assert lib.hps_version() == 1
+
+
+def test_product_has_no_cpu_fallback():
+    """The product package never imports the oracle, and fails loudly without a GPU."""
+    import paper_2306_02526_b200 as hb
+    pkg = os.path.dirname(hb.__file__)
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert "oracle" not in src.replace("the oracle", ""), fn
+    import torch
+    if not torch.cuda.is_available():
+        t = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 6)
+        with pytest.raises(hb.HpstepError):
+            hb.build(t, hb.OperatorCoefficients(c11=1.0, c22=1.0))
