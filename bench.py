@@ -1,0 +1,394 @@
+"""Benchmark of the per-stage HPS solve path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A *step* is one ESDIRK4 (ARK4(3)6L[2]SA) time step of the configured problem
+through the drop-in ``TimeStepper`` -- 5 implicit HPS stage solves plus the
+device stage right-hand-side assembly -- with the state resident in HBM.
+``value`` = DOF*stages/s = N_dof * 5 * K / (device time of K steps), summed
+over ranks (each rank runs its own replica: ``scaling`` "weak").
+``e2e`` is the same metric through the public API with the state copied in
+from pinned host memory and the result read back every step.
+``roofline`` is for the stage solve (the ~2*depth+5 level-batched kernels of
+``hps_solve``): algorithmic bytes per solve over
+the CUDA-event duration of the solves inside the timed region.
+``cpu_baseline`` times the CPU oracle port (numpy/scipy, all host cores) on a
+bounded sample: the 64x64-leaf subtree of the same problem (same p, dt), one
+step, build excluded.
+``--impl reference`` times that CPU path alone (the reference is pure Python
+and cannot be installed on the GPU box).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HPS stage solves/sec (DOF·stages/s), 2D ESDIRK4 fp64; % of HBM roofline"
+UNIT = "DOF*stages/s"
+TWO_PI = 2 * np.pi
+
+# BASELINE.json configs (single-GPU workloads); C2 is the metric's config
+CONFIGS = {
+    "C1": dict(n=8, p=12, dt=1e-3, kind="heat", k=1),
+    "C2": dict(n=128, p=16, dt=1e-4, kind="heat", k=1),
+    "C3": dict(n=256, p=12, dt=1e-3, kind="allen_cahn", k=1),
+    "C4": dict(n=512, p=10, dt=1e-5, kind="burgers_var", k=1),
+    "C5": dict(n=128, p=16, dt=1e-4, kind="ensemble", k=64),
+}
+SAMPLE_N = 64      # CPU sample: the 64x64-leaf subtree of the configured problem
+
+
+def phi(pts):
+    return np.sin(TWO_PI * pts[:, 0]) * np.sin(TWO_PI * pts[:, 1])
+
+
+def sine_modes(seed, k=None, mmax=8, nmax=4):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-1.0, 1.0, size=(mmax, nmax) if k is None else (k, mmax, nmax))
+
+
+def sine_field(coef, pts):
+    x, y = pts[:, 0], pts[:, 1]
+    mmax, nmax = coef.shape[-2:]
+    sx = np.stack([np.sin(m * np.pi * x) for m in range(1, mmax + 1)])
+    sy = np.stack([np.sin(n * np.pi * y) for n in range(1, nmax + 1)])
+    if coef.ndim == 2:
+        return np.einsum("mn,mp,np->p", coef, sx, sy)
+    return np.einsum("kmn,mp,np->kp", coef, sx, sy)
+
+
+def c4_fields():
+    a = lambda x, y: 1 + 0.5 * np.sin(TWO_PI * x) * np.cos(TWO_PI * y)
+    ax = lambda x, y: np.pi * np.cos(TWO_PI * x) * np.cos(TWO_PI * y)
+    ay = lambda x, y: -np.pi * np.sin(TWO_PI * x) * np.sin(TWO_PI * y)
+    return dict(c11=a, c22=a, c1=lambda x, y: -(ax(x, y) + 1.0), c2=lambda x, y: -(ay(x, y) + 0.5))
+
+
+def make_problem(mod, cfg):
+    """ParabolicProblem of the config for the package ``mod`` (ours or the
+    oracle-facing description); returns (problem kwargs)."""
+    kind = cfg["kind"]
+    if kind == "heat":
+        q = mod.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
+        f = mod.SeparableField.product(phi, np.cos)
+        return dict(coeffs=mod.OperatorCoefficients(c11=1.0, c22=1.0), q=q, f=f,
+                    u0=lambda pts: phi(pts))
+    if kind == "allen_cahn":
+        coef = sine_modes(0)
+        return dict(coeffs=mod.OperatorCoefficients(c11=0.01, c22=0.01),
+                    g=lambda t, u, ux, uy: u - u ** 3, u0=lambda pts: sine_field(coef, pts),
+                    time_independent_bc=True)
+    if kind == "burgers_var":
+        coef = sine_modes(1)
+        return dict(coeffs=mod.OperatorCoefficients(**c4_fields()),
+                    g=lambda t, u, ux, uy: -u * ux, u0=lambda pts: sine_field(coef, pts),
+                    time_independent_bc=True)
+    if kind == "ensemble":
+        coef = sine_modes(2, k=cfg["k"])
+        q = mod.SeparableField.product(lambda pts: sine_field(coef, pts))
+        return dict(coeffs=mod.OperatorCoefficients(c11=1.0, c22=1.0), q=q,
+                    u0=lambda pts: np.zeros((cfg["k"], pts.shape[0])), time_independent_bc=True,
+                    ncomp=cfg["k"])
+    raise ValueError(kind)
+
+
+def solve_bytes(tree, k, const_leaf):
+    """Algorithmic HBM bytes of one stage solve; the root's
+    Tstack is never applied (its flux has no consumer) and is not counted."""
+    ni, nb, L = tree.ni, tree.nb, tree.L
+    ops = 0
+    vec = L * (2 * ni + 2 * nb)
+    for d, lm in enumerate(tree.level_maps):
+        c, n3, n12 = lm.count, lm.n3, lm.n12
+        ops += c * (n3 * n3 + n3 * n12 + (n12 * n3 if d > 0 else 0))
+        vec += c * (3 * n12 + 2 * n3)
+    lam = 1 if const_leaf else L
+    ops += lam * (ni * ni + ni * nb) + nb * ni
+    return 8 * ops, 8 * k * vec
+
+
+def solve_flops(tree, k):
+    ni, nb, L = tree.ni, tree.nb, tree.L
+    e = L * (ni * ni + 2 * ni * nb)
+    for d, lm in enumerate(tree.level_maps):
+        e += lm.count * (lm.n3 * lm.n3 + lm.n3 * lm.n12 + (lm.n12 * lm.n3 if d > 0 else 0))
+    return 2 * k * e
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+def profiled_traffic(config):
+    """dram bytes per solve from a committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(config)
+    except (OSError, ValueError):
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+
+def cpu_oracle_sample(cfg, steps, warmup):
+    """Times the oracle port on the SAMPLE_N x SAMPLE_N subtree of the config."""
+    from oracle import hps_oracle as O  # checker / CPU baseline only
+    n = min(SAMPLE_N, cfg["n"])
+    tree = O.OTree(((0.0, 1.0), (0.0, 1.0)), n, n, cfg["p"])
+    kind = cfg["kind"]
+    kw = {}
+    if kind == "heat":
+        kw = dict(q=lambda t, pts: phi(pts) * (-np.sin(t) + 8 * np.pi ** 2 * np.cos(t)),
+                  f=lambda t, pts: phi(pts) * np.cos(t))
+        coeffs, u = O.OCoeffs(c11=1.0, c22=1.0), phi(tree.points)
+    elif kind == "allen_cahn":
+        coeffs = O.OCoeffs(c11=0.01, c22=0.01)
+        kw = dict(g=lambda t, u, ux, uy: u - u ** 3)
+        u = sine_field(sine_modes(0), tree.points)
+    elif kind == "burgers_var":
+        coeffs = O.OCoeffs(**c4_fields())
+        kw = dict(g=lambda t, u, ux, uy: -u * ux)
+        u = sine_field(sine_modes(1), tree.points)
+    else:
+        coeffs = O.OCoeffs(c11=1.0, c22=1.0)
+        coef = sine_modes(2, k=cfg["k"])
+        kw = dict(q=lambda t, pts: sine_field(coef, pts), ncomp=cfg["k"])
+        u = np.zeros((cfg["k"], tree.N))
+    st = O.OStepper(tree, coeffs, O.ark4_tableau(), cfg["dt"], **kw)
+    t = 0.0
+    for _ in range(warmup):
+        t, u = st.run(t, u, 1)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        t, u = st.run(t, u, 1)
+        times.append(time.perf_counter() - t0)
+    k = cfg["k"]
+    val = tree.N * k * 5 * len(times) / sum(times)
+    sample = (f"{n}x{n}-leaf subtree, p={cfg['p']}, k={k}, {len(times)} ARK4 step(s) "
+              f"({5 * len(times)} stage solves + RHS), N={tree.N}, build excluded")
+    return val, sample, times
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    val, sample, times = cpu_oracle_sample(cfg, max(1, args.steps), max(0, args.warmup))
+    cores = os.cpu_count()
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} (CPU sample)", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200 import _lib
+
+    lib = _lib.load()
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), cfg["n"], cfg["n"], cfg["p"])
+    prob = hb.ParabolicProblem(**make_problem(hb, cfg))
+    t0 = time.perf_counter()
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"])
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    k = cfg["k"]
+    state = st.initial_state()
+    state = hb.StepperState(state.t, state.u_device)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        state = st.run(state, 1)
+    barrier()
+    st.solve_timer = []
+    n0 = lib.hps_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        state = st.run(state, args.steps, check_every=max(1, args.steps))
+        ev1.record()
+        barrier()
+    launches = lib.hps_launch_count() - n0
+    ms = ev0.elapsed_time(ev1)
+    solve_ms = [a.elapsed_time(b) for a, b in st.solve_timer]
+    st.solve_timer = None
+    ms = max_over_ranks(ms)
+    dof_stages = tree.N * k * 5 * args.steps
+    value = dof_stages / (ms * 1e-3) * world
+
+    # e2e: public API with host state in / host result out every step
+    e2e_steps = args.e2e_steps or max(3, args.steps // 2)
+    uh = torch.empty((k, tree.N) if k > 1 else (tree.N,), dtype=torch.float64).pin_memory()
+    uh.copy_(state.u_device.cpu())
+    out = torch.empty_like(uh).pin_memory()
+    s = hb.StepperState(state.t, uh)
+    s = st.step(s)            # warm
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        s = st.step(hb.StepperState(s.t, uh))
+        out.copy_(s.u_device, non_blocking=True)
+    e1.record()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_val = tree.N * k * 5 * e2e_steps / (e2e_ms * 1e-3) * world
+    nbytes = uh.numel() * 8
+
+    # roofline of the stage solve
+    b_op, b_vec = solve_bytes(tree, k, prob.coeffs.is_constant)
+    avg_solve = statistics.mean(solve_ms)
+    achieved = (b_op + b_vec) / (avg_solve * 1e-3) / 1e9
+    peak, src = peaks()
+    flops = solve_flops(tree, k)
+    traffic = profiled_traffic(args.config)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        val, sample, _ = cpu_oracle_sample(cfg, 1, 0)
+        cpu = {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": sample}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (manufactured / seeded analytic fields; no dataset)",
+        "config": {"workload": f"{args.config}: {cfg['n']}x{cfg['n']} leaves, p={cfg['p']}, "
+                               f"{cfg['kind']}, ARK4 dt={cfg['dt']}, k={k}, one ARK4 step per "
+                               f"bench step (5 stage solves)",
+                   "N_dof": tree.N, "parallelism": f"replicas x{world}",
+                   "l2": "inputs larger than L2 (operators %.2f GB)" % (b_op / 1e9)},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                "d2h_bytes_per_step": nbytes},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "hps_solve (level-batched GEMV sweep)",
+                     "algorithmic_bytes_per_solve": b_op + b_vec, "peak_source": src,
+                     "solve_ms": avg_solve, "solves_timed": len(solve_ms),
+                     "gflops_per_solve": flops / 1e9},
+        "clocks": clk.summary(),
+        "build_s": build_s,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

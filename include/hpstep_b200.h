@@ -82,6 +82,7 @@ typedef struct {
 } hps_build_desc;
 
 int hps_version(void);
+long long hps_launch_count(void); /* kernels launched by this library so far */
 const char* hps_last_error(void);
 long long hps_last_error_node(void);
 
@@ -114,6 +115,54 @@ size_t hps_solve_workspace_bytes(const hps_plan* plan, int k);
 int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
               long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
               long long ld_u, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Stage right-hand-side assembly (timestep.py:237-266 and the leaf-local
+ * evaluations of operators.py:276-346).
+ * ------------------------------------------------------------------------ */
+typedef struct hps_disc hps_disc; /* device leaf stencil + coefficient samples */
+
+/* EllipticDiscretization (operators.py:219-236) as seen by the evaluations:
+ * 1D CGL derivative matrices of the leaf grid (p x p, descending nodes) and
+ * the edge-local ones on the p-2 interior nodes (operators.py:192-213),
+ * coefficient samples at the m = ni + nb leaf-local points, the reference's
+ * leaf_bnd_sign (tree.py:382-403) as int8. */
+typedef struct {
+  const double *d1x, *d2x, *d1y, *d2y; /* p x p  */
+  const double *ex1, *ex2, *ey1, *ey2; /* (p-2) x (p-2) */
+  int Lc;                              /* 1 (constant) or L sample sets        */
+  const double* coef;                  /* Lc x 5 x m: c11, c22, c1, c2, c       */
+  int has_c1, has_c2, has_c;
+  const signed char* leaf_bnd_sign;    /* L x nb, 0 on the domain boundary     */
+} hps_disc_desc;
+
+int hps_disc_create(const hps_plan* plan, const hps_disc_desc* desc, hps_disc** out);
+void hps_disc_destroy(hps_disc* disc);
+
+/* One pass over the leaves of k stacked grid vectors u (row stride ld_u).
+ * Each non-NULL output (row stride ld_o) receives:
+ *   lu_int  L u at leaf-interior DOFs [0, L*ni) only (stage history)
+ *   lu      apply_lop (operators.py:276-301), interface-averaged, every DOF
+ *   ux, uy  gradient (operators.py:303-317), interface-averaged
+ *   jump    flux_jump (operators.py:319-336), zero off the interfaces
+ * guard (device double, may be NULL) is raised to max |u| over every DOF
+ * (NaN sticks), the divergence guard of timestep.py:198-203. */
+int hps_leaf_eval(const hps_disc* disc, int k, const double* u, long long ld_u, double* lu_int,
+                  double* lu, double* ux, double* uy, double* jump, long long ld_o, double* guard,
+                  void* stream);
+
+/* out[r][0:n) = sum_t coefs[t] * vecs[t][r*lds[t] + (0:n)] for r < k
+ * (lds[t] = 0 broadcasts one vector over the rows); at most 24 terms.
+ * The ARK stage combinations of timestep.py:255-257 and 263-264. */
+int hps_combine(int k, long long n, int nterms, const double* coefs, const double* const* vecs,
+                const long long* lds, double* out, long long ld_out, double* guard, void* stream);
+
+/* guard = max(guard, max |x|) over k rows of n values. */
+int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard, void* stream);
+
+/* u[r][boundary_ids] = fb[r] (timestep.py:265). */
+int hps_put_boundary(const hps_plan* plan, int k, const double* fb, long long ld_f, double* u,
+                     long long ld_u, void* stream);
 
 #ifdef __cplusplus
 }

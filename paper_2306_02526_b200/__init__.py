@@ -11,6 +11,9 @@ from .errors import (ConfigError, DivergenceError, HpstepError, InvalidStepError
                      SingularMatrixError, UnknownTableauError, UnsupportedConfigurationError)
 from .operators import EllipticDiscretization, LeafStencil, OperatorCoefficients, shift_reaction
 from .solver import HpsOperatorSet, build
+from .tableaux import ButcherPair, available_tableaux, load_tableau
+from .timestep import (ParabolicProblem, SeparableField, StepperState, TimeStepper,
+                       evaluate_nonlinear)
 from .tree import DomainTree, TreeNode, build_tree
 
 __version__ = "0.1.0"
@@ -20,5 +23,6 @@ __all__ = [
     "InvalidStepError", "SingularMatrixError", "UnknownTableauError",
     "UnsupportedConfigurationError", "EllipticDiscretization", "LeafStencil",
     "OperatorCoefficients", "shift_reaction", "HpsOperatorSet", "build", "DomainTree",
-    "TreeNode", "build_tree",
+    "TreeNode", "build_tree", "ButcherPair", "available_tableaux", "load_tableau",
+    "ParabolicProblem", "SeparableField", "StepperState", "TimeStepper", "evaluate_nonlinear",
 ]

@@ -48,9 +48,24 @@ class BuildDesc(ctypes.Structure):
     ]
 
 
+class DiscDesc(ctypes.Structure):
+    _fields_ = [
+        ("d1x", c_double_p), ("d2x", c_double_p), ("d1y", c_double_p), ("d2y", c_double_p),
+        ("ex1", c_double_p), ("ex2", c_double_p), ("ey1", c_double_p), ("ey2", c_double_p),
+        ("Lc", ctypes.c_int), ("coef", c_double_p),
+        ("has_c1", ctypes.c_int), ("has_c2", ctypes.c_int), ("has_c", ctypes.c_int),
+        ("leaf_bnd_sign", ctypes.POINTER(ctypes.c_byte)),
+    ]
+
+
+_vp = ctypes.c_void_p
+_ll = ctypes.c_longlong
+_i = ctypes.c_int
+
 # exported symbols and their signatures (every name declared in include/hpstep_b200.h)
 SIGNATURES = {
     "hps_version": (ctypes.c_int, []),
+    "hps_launch_count": (ctypes.c_longlong, []),
     "hps_last_error": (ctypes.c_char_p, []),
     "hps_last_error_node": (ctypes.c_longlong, []),
     "hps_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(ctypes.c_void_p)]),
@@ -68,6 +83,13 @@ SIGNATURES = {
                                  ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p,
                                  ctypes.c_longlong, ctypes.c_void_p, ctypes.c_size_t,
                                  ctypes.c_void_p]),
+    "hps_disc_create": (_i, [_vp, ctypes.POINTER(DiscDesc), ctypes.POINTER(_vp)]),
+    "hps_disc_destroy": (None, [_vp]),
+    "hps_leaf_eval": (_i, [_vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp]),
+    "hps_combine": (_i, [_i, _ll, _i, c_double_p, ctypes.POINTER(_vp), c_ll_p, _vp, _ll, _vp,
+                         _vp]),
+    "hps_maxabs": (_i, [_i, _ll, _vp, _ll, _vp, _vp]),
+    "hps_put_boundary": (_i, [_vp, _i, _vp, _ll, _vp, _ll, _vp]),
 }
 
 _lib = None

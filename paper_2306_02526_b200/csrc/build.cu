@@ -345,6 +345,7 @@ int gj_invert(int n, int batch, double* A, double* X, int ldx, long long sX, dou
                                                 nrb, piv, stats);
     double* t = cur; cur = nxt; nxt = t;
   }
+  g_launches.fetch_add(n - 1, std::memory_order_relaxed);  // n step launches, one check
   HPSB_LAUNCH_CHECK();
   k_gj_unscramble<<<dim3(min(n, 1024), batch), 256, (size_t)n * 4, st>>>(n, cur, sA, piv, X, ldx, sX);
   HPSB_LAUNCH_CHECK();

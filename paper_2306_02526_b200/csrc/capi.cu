@@ -11,6 +11,7 @@
 
 namespace hpsb {
 
+std::atomic<long long> g_launches{0};
 static thread_local char g_err[1024] = {0};
 static thread_local long long g_err_node = -1;
 
@@ -67,12 +68,11 @@ static int singular(int n, double pmin, double pmax, const char* kind, long long
 
 using namespace hpsb;
 
-struct hps_plan { Plan P; std::vector<void*> allocs; };
-struct hps_ops { Ops O; };
 
 extern "C" {
 
 int hps_version(void) { return 1; }
+long long hps_launch_count(void) { return g_launches.load(); }
 const char* hps_last_error(void) { return g_err; }
 long long hps_last_error_node(void) { return g_err_node; }
 

@@ -5,6 +5,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <string>
 
 namespace hpsb {
@@ -25,8 +26,13 @@ void set_error_node(long long node);
     }                                                                          \
   } while (0)
 
+// kernel launches issued by this library (hps_launch_count); every launch
+// site is followed by HPSB_LAUNCH_CHECK
+extern std::atomic<long long> g_launches;
+
 #define HPSB_LAUNCH_CHECK()                                                    \
   do {                                                                         \
+    ::hpsb::g_launches.fetch_add(1, std::memory_order_relaxed);                \
     cudaError_t _e = cudaGetLastError();                                       \
     if (_e != cudaSuccess) {                                                   \
       ::hpsb::set_error("%s:%d: launch failed: %s", __FILE__, __LINE__,         \

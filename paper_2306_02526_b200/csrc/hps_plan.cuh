@@ -100,3 +100,7 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
           void* ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace hpsb
+
+// opaque handles of the C ABI (include/hpstep_b200.h)
+struct hps_plan { hpsb::Plan P; std::vector<void*> allocs; };
+struct hps_ops { hpsb::Ops O; };

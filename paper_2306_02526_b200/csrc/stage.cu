@@ -1,0 +1,400 @@
+// Stage right-hand-side kernels of the IMEX ARK stepper (sm_100a, FP64).
+//
+//   k_leaf_eval : leaf-local spectral evaluations of a grid vector, the
+//                 tensor-product form of the reference's dense leaf products
+//                 (operators.py:276-336):
+//                   L u  = c11 u_xx + c22 u_yy - c1 u_x - c2 u_y - c u
+//                   grad = (u_x, u_y)
+//                   flux jump = sign * D_bnd u  (edge points only)
+//                 Every leaf's p x p grid (corners unused) is staged in shared
+//                 memory from the global vector (interiors are one contiguous
+//                 run per leaf, edges are gathered through leaf_bnd_gidx);
+//                 derivative rows are p-term sums along grid lines, with the
+//                 edge-local (p-2)-node rows for tangential derivatives at edge
+//                 points (operators.py:192-213).  Interface values are the mean
+//                 of the two abutting leaves (operators.py:339-346): the
+//                 interior is written directly, edge points accumulate w*value
+//                 with w = 1/multiplicity (exact for multiplicity 1 or 2, and
+//                 order independent for two addends).
+//                 The kernel also folds a max|u| / non-finite reduction over
+//                 every value it stages (the divergence guard of
+//                 timestep.py:198-203).
+//   k_combine   : out = sum_m c_m v_m over a DOF range (the ARK stage
+//                 combinations, timestep.py:255-257 and 263-264).
+//   k_maxabs    : guard reduction of a vector.
+#include "../../include/hpstep_b200.h"
+#include "hps_plan.cuh"
+
+namespace hpsb {
+
+struct Disc {
+  const Plan* P = nullptr;
+  int p = 0, q = 0, ni = 0, nb = 0, m = 0, L = 0;
+  int Lc = 1;                     // coefficient sample sets (1 = constant)
+  int has_c1 = 0, has_c2 = 0, has_c = 0;
+  double cc[5] = {0, 0, 0, 0, 0};  // constant coefficients (Lc == 1)
+  double* coef = nullptr;         // Lc x 5 x m (device) when Lc > 1
+  double* mats = nullptr;         // d1x d2x d1y d2y (p*p each) ex1 ex2 ey1 ey2 (q*q each)
+  signed char* sign = nullptr;    // L x nb leaf_bnd_sign (device)
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+constexpr int NT = 256;
+
+struct EvalArgs {
+  int k;
+  const double* u; long long ld_u;
+  int L, p, q, ni, nb, m, lpb;
+  long long N;
+  const int* lbg;                   // L x nb
+  const signed char* sign;          // L x nb
+  const double* mats;
+  int Lc; const double* coef; double cc[5]; int has_c1, has_c2, has_c;
+  // outputs (nullptr = not requested), all row stride ld_o
+  double* lu_int;                   // L u at interior points only (no averaging)
+  double* lu;                       // L u at every DOF, interface-averaged
+  double* ux; double* uy;           // gradient, interface-averaged
+  double* jump;                     // signed flux jumps at edge points
+  long long ld_o;
+  unsigned long long* guard;        // max |u| bits (nullptr = off)
+};
+
+// running max |v| that keeps NaN sticky (fmax would drop it)
+__device__ __forceinline__ void gacc(double& g, double v) {
+  double av = fabs(v);
+  g = (av > g || av != av) ? av : g;
+}
+
+__device__ __forceinline__ void guard_max(unsigned long long* slot, double v) {
+  // |v| as an unsigned bit pattern orders like the value; NaN sorts above inf
+  unsigned long long b = __double_as_longlong(fabs(v));
+  for (int off = 16; off > 0; off >>= 1) {
+    unsigned long long o = __shfl_xor_sync(0xffffffffu, b, off);
+    b = o > b ? o : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(slot, b);
+}
+
+// local edge index e -> grid (xi, yi): east (xi = 0), north/south interleaved,
+// west (xi = p-1); reference tree.py:236-243 / operators.py:172-178
+__device__ __forceinline__ void edge_xy(int e, int p, int q, int& xi, int& yi) {
+  if (e < q) { xi = 0; yi = e + 1; }
+  else if (e < 3 * q) { int j = e - q; xi = j / 2 + 1; yi = (j & 1) ? p - 1 : 0; }
+  else { xi = p - 1; yi = e - 3 * q + 1; }
+}
+
+__global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
+  extern __shared__ double sm[];
+  const int p = a.p, q = a.q, pp = p * p, qq = q * q;
+  double* d1x = sm;
+  double* d2x = d1x + pp;
+  double* d1y = d2x + pp;
+  double* d2y = d1y + pp;
+  double* ex1 = d2y + pp;
+  double* ex2 = ex1 + qq;
+  double* ey1 = ex2 + qq;
+  double* ey2 = ey1 + qq;
+  double* U = ey2 + qq;  // lpb x p x p
+  const int tid = threadIdx.x;
+  for (int e = tid; e < 4 * pp + 4 * qq; e += NT) sm[e] = a.mats[e];
+  const int kk = blockIdx.y;
+  const int l0 = blockIdx.x * a.lpb;
+  const int nl = min(a.lpb, a.L - l0);
+  const double* u = a.u + kk * a.ld_u;
+  double gmax = 0.0;
+  // interior: one contiguous run of nl*ni values
+  for (int e = tid; e < nl * a.ni; e += NT) {
+    int ll = e / a.ni, i = e % a.ni;
+    double v = u[(long long)l0 * a.ni + e];
+    U[ll * pp + (i / q + 1) * p + (i % q + 1)] = v;
+    gacc(gmax, v);
+  }
+  for (int e = tid; e < nl * a.nb; e += NT) {
+    int ll = e / a.nb, j = e % a.nb, xi, yi;
+    edge_xy(j, p, q, xi, yi);
+    double v = u[a.lbg[(long long)(l0 + ll) * a.nb + j]];
+    U[ll * pp + xi * p + yi] = v;
+    gacc(gmax, v);
+  }
+  if (a.guard) guard_max(a.guard, gmax);
+  __syncthreads();
+
+  const bool want_all = a.lu || a.ux || a.uy;
+  const int npts = want_all ? a.m : (a.lu_int ? a.ni : 0);
+  const long long ob = kk * a.ld_o;
+  for (int e = tid; e < nl * npts; e += NT) {
+    const int ll = e / npts, t = e % npts, l = l0 + ll;
+    int xi, yi;
+    const bool inner = t < a.ni;
+    if (inner) { xi = t / q + 1; yi = t % q + 1; }
+    else edge_xy(t - a.ni, p, q, xi, yi);
+    const double* G = U + ll * pp;
+    const bool vert = !inner && (xi == 0 || xi == p - 1);
+    const bool horz = !inner && !vert;
+    double ux = 0.0, uxx = 0.0, uy = 0.0, uyy = 0.0;
+    if (horz) {  // tangential x on north/south edges: edge-local rows
+      const double* r1 = ex1 + (xi - 1) * q;
+      const double* r2 = ex2 + (xi - 1) * q;
+      for (int s = 0; s < q; ++s) {
+        double v = G[(s + 1) * p + yi];
+        ux = fma(r1[s], v, ux);
+        uxx = fma(r2[s], v, uxx);
+      }
+    } else {
+      const double* r1 = d1x + xi * p;
+      const double* r2 = d2x + xi * p;
+      for (int s = 0; s < p; ++s) {
+        double v = G[s * p + yi];
+        ux = fma(r1[s], v, ux);
+        uxx = fma(r2[s], v, uxx);
+      }
+    }
+    if (vert) {  // tangential y on east/west edges
+      const double* r1 = ey1 + (yi - 1) * q;
+      const double* r2 = ey2 + (yi - 1) * q;
+      for (int s = 0; s < q; ++s) {
+        double v = G[xi * p + s + 1];
+        uy = fma(r1[s], v, uy);
+        uyy = fma(r2[s], v, uyy);
+      }
+    } else {
+      const double* r1 = d1y + yi * p;
+      const double* r2 = d2y + yi * p;
+      for (int s = 0; s < p; ++s) {
+        double v = G[xi * p + s];
+        uy = fma(r1[s], v, uy);
+        uyy = fma(r2[s], v, uyy);
+      }
+    }
+    double lop = 0.0;
+    if (a.lu || (a.lu_int && inner)) {
+      double c11, c22, c1, c2, c0;
+      if (a.Lc == 1) { c11 = a.cc[0]; c22 = a.cc[1]; c1 = a.cc[2]; c2 = a.cc[3]; c0 = a.cc[4]; }
+      else {
+        const double* cv = a.coef + (long long)l * 5 * a.m;
+        c11 = cv[t]; c22 = cv[a.m + t]; c1 = cv[2 * a.m + t]; c2 = cv[3 * a.m + t]; c0 = cv[4 * a.m + t];
+      }
+      // operators.py:292-300, in the same association, without contraction
+      lop = __dmul_rn(c11, uxx);
+      lop = __dadd_rn(lop, __dmul_rn(c22, uyy));
+      if (a.has_c1) lop = __dsub_rn(lop, __dmul_rn(c1, ux));
+      if (a.has_c2) lop = __dsub_rn(lop, __dmul_rn(c2, uy));
+      if (a.has_c) lop = __dsub_rn(lop, __dmul_rn(c0, G[xi * p + yi]));
+    }
+    if (inner) {
+      const long long gi = (long long)l * a.ni + t;
+      if (a.lu_int) a.lu_int[ob + gi] = lop;
+      if (a.lu) a.lu[ob + gi] = lop;
+      if (a.ux) a.ux[ob + gi] = ux;
+      if (a.uy) a.uy[ob + gi] = uy;
+    } else {
+      const int j = t - a.ni;
+      const long long gi = a.lbg[(long long)l * a.nb + j];
+      const double w = a.sign[(long long)l * a.nb + j] ? 0.5 : 1.0;
+      if (a.lu) atomicAdd(a.lu + ob + gi, w * lop);
+      if (a.ux) atomicAdd(a.ux + ob + gi, w * ux);
+      if (a.uy) atomicAdd(a.uy + ob + gi, w * uy);
+    }
+  }
+  if (a.jump) {
+    // flux rows: normal derivative from the full tensor line (operators.py:188-190)
+    for (int e = tid; e < nl * a.nb; e += NT) {
+      const int ll = e / a.nb, j = e % a.nb, l = l0 + ll;
+      const signed char sg = a.sign[(long long)l * a.nb + j];
+      if (!sg) continue;
+      int xi, yi;
+      edge_xy(j, p, q, xi, yi);
+      const double* G = U + ll * pp;
+      double v = 0.0;
+      if (xi == 0 || xi == p - 1) {
+        const double* r = d1x + xi * p;
+        for (int s = 0; s < p; ++s) v = fma(r[s], G[s * p + yi], v);
+      } else {
+        const double* r = d1y + yi * p;
+        for (int s = 0; s < p; ++s) v = fma(r[s], G[xi * p + s], v);
+      }
+      atomicAdd(a.jump + ob + a.lbg[(long long)l * a.nb + j], sg > 0 ? v : -v);
+    }
+  }
+}
+
+constexpr int MAXT = 24;
+struct CombineArgs {
+  int nt, k;
+  long long n;                 // DOFs per row
+  double c[MAXT];
+  const double* v[MAXT];
+  long long ld[MAXT];          // row stride of term m (0 = broadcast over rows)
+  double* out; long long ld_out;
+  unsigned long long* guard;
+};
+
+__global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
+  const int kk = blockIdx.y;
+  double gmax = 0.0;
+  const long long stride = (long long)gridDim.x * NT;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < a.n; e += stride) {
+    double s = 0.0;
+    for (int t = 0; t < a.nt; ++t) s = fma(a.c[t], __ldcs(a.v[t] + kk * a.ld[t] + e), s);
+    a.out[kk * a.ld_out + e] = s;
+    gacc(gmax, s);
+  }
+  if (a.guard) guard_max(a.guard, gmax);
+}
+
+__global__ void __launch_bounds__(NT) k_maxabs(int k, long long n, const double* x, long long ld,
+                                                unsigned long long* guard) {
+  const int kk = blockIdx.y;
+  double gmax = 0.0;
+  const long long stride = (long long)gridDim.x * NT;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < n; e += stride) {
+    double v = x[kk * ld + e];
+    gacc(gmax, v);
+  }
+  guard_max(guard, gmax);
+}
+
+__global__ void k_bnd_put(int k, int nbd, const int* __restrict__ ids, const double* __restrict__ fb,
+                          long long ld_f, double* __restrict__ u, long long ld_u) {
+  long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= (long long)k * nbd) return;
+  int kk = (int)(e / nbd), i = (int)(e % nbd);
+  u[kk * ld_u + ids[i]] = fb[kk * ld_f + i];
+}
+
+unsigned stream_blocks(long long n) {
+  long long b = cdiv(n, (long long)NT * 4);
+  long long cap = (long long)kNumSMs * 8;
+  return (unsigned)std::max<long long>(1, std::min(b, cap));
+}
+
+}  // namespace
+
+}  // namespace hpsb
+
+using namespace hpsb;
+
+struct hps_disc { Disc D; };
+
+extern "C" {
+
+int hps_disc_create(const hps_plan* pv, const hps_disc_desc* d, hps_disc** out) {
+  *out = nullptr;
+  if (!pv || !d) { set_error("hps_disc_create: null argument"); return HPS_ERR_ARG; }
+  const Plan& P = pv->P;
+  hps_disc* h = new hps_disc();
+  Disc& D = h->D;
+  D.P = &P;
+  D.p = P.p; D.q = P.q; D.ni = P.ni; D.nb = P.nb; D.m = P.ni + P.nb; D.L = P.L;
+  D.Lc = d->Lc; D.has_c1 = d->has_c1; D.has_c2 = d->has_c2; D.has_c = d->has_c;
+  const int p = D.p, q = D.q;
+  const size_t nm = 4 * (size_t)p * p + 4 * (size_t)q * q;
+  auto fail = [&](const char* what) {
+    set_error("hps_disc_create: %s", what);
+    for (void* x : D.allocs) cudaFree(x);
+    delete h;
+    return HPS_ERR_CUDA;
+  };
+  std::vector<double> mats(nm);
+  const double* src[8] = {d->d1x, d->d2x, d->d1y, d->d2y, d->ex1, d->ex2, d->ey1, d->ey2};
+  size_t o = 0;
+  for (int i = 0; i < 8; ++i) {
+    size_t cnt = i < 4 ? (size_t)p * p : (size_t)q * q;
+    memcpy(mats.data() + o, src[i], cnt * 8);
+    o += cnt;
+  }
+  if (cudaMalloc(&D.mats, nm * 8) != cudaSuccess) return fail("out of device memory");
+  D.allocs.push_back(D.mats);
+  if (cudaMemcpy(D.mats, mats.data(), nm * 8, cudaMemcpyHostToDevice) != cudaSuccess) return fail("copy");
+  if (D.Lc == 1) {
+    for (int i = 0; i < 5; ++i) D.cc[i] = d->coef[(size_t)i * D.m];
+  } else {
+    size_t n = (size_t)D.Lc * 5 * D.m;
+    if (cudaMalloc(&D.coef, n * 8) != cudaSuccess) return fail("out of device memory");
+    D.allocs.push_back(D.coef);
+    if (cudaMemcpy(D.coef, d->coef, n * 8, cudaMemcpyHostToDevice) != cudaSuccess) return fail("copy");
+  }
+  size_t ns = (size_t)P.L * P.nb;
+  if (cudaMalloc(&D.sign, ns) != cudaSuccess) return fail("out of device memory");
+  D.allocs.push_back(D.sign);
+  if (cudaMemcpy(D.sign, d->leaf_bnd_sign, ns, cudaMemcpyHostToDevice) != cudaSuccess) return fail("copy");
+  *out = h;
+  return HPS_OK;
+}
+
+void hps_disc_destroy(hps_disc* h) {
+  if (!h) return;
+  for (void* x : h->D.allocs) cudaFree(x);
+  delete h;
+}
+
+int hps_leaf_eval(const hps_disc* h, int k, const double* u, long long ld_u, double* lu_int, double* lu,
+                  double* ux, double* uy, double* jump, long long ld_o, double* guard, void* stream) {
+  if (!h || !u) { set_error("hps_leaf_eval: null argument"); return HPS_ERR_ARG; }
+  if (k <= 0) return HPS_OK;
+  const Disc& D = h->D;
+  const Plan& P = *D.P;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long Lni = (long long)P.L * P.ni;
+  // averaged outputs accumulate at edge DOFs; the flux jump is zero off the edges
+  for (double* o : {lu, ux, uy}) {
+    if (!o) continue;
+    for (int kk = 0; kk < k; ++kk)
+      HPSB_CUDA(cudaMemsetAsync(o + kk * ld_o + Lni, 0, (size_t)(P.N - Lni) * 8, st));
+  }
+  if (jump)
+    for (int kk = 0; kk < k; ++kk) HPSB_CUDA(cudaMemsetAsync(jump + kk * ld_o, 0, (size_t)P.N * 8, st));
+  EvalArgs a{};
+  a.k = k; a.u = u; a.ld_u = ld_u;
+  a.L = P.L; a.p = D.p; a.q = D.q; a.ni = D.ni; a.nb = D.nb; a.m = D.m; a.N = P.N;
+  a.lpb = std::max(1, NT / (D.p * D.p));
+  a.lbg = P.leaf_bnd_gidx; a.sign = D.sign; a.mats = D.mats;
+  a.Lc = D.Lc; a.coef = D.coef;
+  for (int i = 0; i < 5; ++i) a.cc[i] = D.cc[i];
+  a.has_c1 = D.has_c1; a.has_c2 = D.has_c2; a.has_c = D.has_c;
+  a.lu_int = lu_int; a.lu = lu; a.ux = ux; a.uy = uy; a.jump = jump; a.ld_o = ld_o;
+  a.guard = reinterpret_cast<unsigned long long*>(guard);
+  const int pp = D.p * D.p, qq = D.q * D.q;
+  size_t smem = (size_t)(4 * pp + 4 * qq + a.lpb * pp) * 8;
+  dim3 grid((unsigned)cdiv(P.L, a.lpb), (unsigned)k);
+  k_leaf_eval<<<grid, NT, smem, st>>>(a);
+  HPSB_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+int hps_combine(int k, long long n, int nterms, const double* coefs, const double* const* vecs,
+                const long long* lds, double* out, long long ld_out, double* guard, void* stream) {
+  if (k <= 0 || n <= 0) return HPS_OK;
+  if (nterms < 0 || nterms > MAXT) { set_error("hps_combine: %d terms (max %d)", nterms, MAXT); return HPS_ERR_ARG; }
+  CombineArgs a{};
+  a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out;
+  for (int t = 0; t < nterms; ++t) { a.c[t] = coefs[t]; a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
+  a.guard = reinterpret_cast<unsigned long long*>(guard);
+  dim3 grid(stream_blocks(n), (unsigned)k);
+  k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  HPSB_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard, void* stream) {
+  if (k <= 0 || n <= 0) return HPS_OK;
+  dim3 grid(stream_blocks(n), (unsigned)k);
+  k_maxabs<<<grid, NT, 0, (cudaStream_t)stream>>>(k, n, x, ld, reinterpret_cast<unsigned long long*>(guard));
+  HPSB_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+int hps_put_boundary(const hps_plan* pv, int k, const double* fb, long long ld_f, double* u,
+                     long long ld_u, void* stream) {
+  if (!pv) { set_error("hps_put_boundary: null plan"); return HPS_ERR_ARG; }
+  const Plan& P = pv->P;
+  long long n = (long long)k * P.nbd;
+  if (n <= 0) return HPS_OK;
+  k_bnd_put<<<(unsigned)cdiv(n, NT), NT, 0, (cudaStream_t)stream>>>(k, P.nbd, P.boundary_ids, fb, ld_f, u, ld_u);
+  HPSB_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+}  // extern "C"

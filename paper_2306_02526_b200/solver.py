@@ -250,6 +250,23 @@ class HpsOperatorSet:
             return res.cpu().numpy()
         return res
 
+    def solve_device(self, fb, body, out, jump=None, inv_dt=None):
+        """Stream-ordered device solve without validation or host copies (the
+        stepper's entry).  ``fb`` (1 or k, nbd); ``body`` (k, >= L*ni) read at
+        leaf interiors only, or None; ``jump`` (k, N) or None; ``out`` (k, N)."""
+        k = out.shape[0]
+        ld_f = 0 if fb.shape[0] == 1 else fb.stride(0)
+        ld_g = 0 if body is None or body.shape[0] == 1 else body.stride(0)
+        ld_j = 0 if jump is None or jump.shape[0] == 1 else jump.stride(0)
+        ws = self.plan.workspace(k)
+        rc = self._lib.hps_solve(
+            self.handle, k, fb.data_ptr(), ld_f, None if body is None else body.data_ptr(), ld_g,
+            None if jump is None else jump.data_ptr(), ld_j,
+            0.0 if inv_dt is None else float(inv_dt), out.data_ptr(), out.stride(0),
+            ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_solve")
+        return out
+
     # -- operator views (reference solver.py:339-348) ---------------------------------
     def _leaf_block(self, which, leaf):
         st = self.disc.stencil

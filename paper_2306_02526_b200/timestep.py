@@ -1,0 +1,627 @@
+"""IMEX ARK time stepping with every stage on the GPU (drop-in for
+``hpstep.timestep``, reference timestep.py:36-333).
+
+The stage formulation (timestep.py:237-266) is the hot path:
+
+    (I - dt*gamma*L) u_i = u^n + dt*sum_{j<i} a_ij L u_j + dt*sum_{j<i} ahat_ij (q_j + g_j)
+
+Device data flow per stage i (k stacked right-hand sides, N DOFs):
+
+* ``L u_j`` is kept only at the leaf-interior DOFs ``[0, L*ni)`` -- the solve
+  reads its body load nowhere else (solver.py:220) -- as ``(k, L*ni)``
+  history rows written by one ``hps_leaf_eval`` pass over ``u_j``;
+* ``q`` is either a :class:`SeparableField` (spatial parts resident on the
+  device, time factors folded into the combination coefficients, nothing
+  stored per stage) or any callable, evaluated per stage into a history row;
+* ``g(t, u, u_x, u_y)`` receives device tensors (u and the interface-averaged
+  gradient from ``hps_leaf_eval``); a callable that cannot run on torch
+  tensors is evaluated on the host from downloaded arrays;
+* one ``hps_combine`` forms the stage body load over ``[0, L*ni)``, one
+  ``hps_solve`` produces ``u_i``, the divergence guard (timestep.py:198-203)
+  is a max|u| reduction fused into the next leaf pass and checked on the host
+  once per step (or once per ``run`` chunk), raising ``DivergenceError`` with
+  the step index the reference would report;
+* the update ``u_s + dt*sum_j (bhat_j - ahat_sj)(q_j + g_j)`` is one more
+  ``hps_combine`` over all N DOFs followed by the boundary overwrite.
+
+Backward Euler (timestep.py:231-235) and the slope / penalized-slope
+formulations (timestep.py:268-328) reuse the same device pieces.
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .device import cuda_device, current_stream_handle, torch
+from .errors import DivergenceError, UnsupportedConfigurationError
+from .operators import EllipticDiscretization
+from .solver import HpsOperatorSet, device_plan
+from .tableaux import ButcherPair, load_tableau
+
+DIVERGENCE_LIMIT = 1e12
+
+
+# ---------------------------------------------------------------------------
+# problem data
+# ---------------------------------------------------------------------------
+
+class SeparableField:
+    """A field ``F(t, pts) = sum_m s_m(t) * phi_m(pts)``.
+
+    Callable exactly like the reference's field callables (``F(t, pts)``), so
+    problems written with it run unchanged on the reference.  The device
+    stepper evaluates every ``phi_m`` once at the grid points, keeps it
+    resident, and folds ``s_m(t)`` into scalar coefficients: no per-stage
+    field evaluation or host traffic.  ``s_m = None`` means constant in time.
+    ``phi_m(pts)`` returns ``(n,)`` or ``(ncomp, n)``.
+    """
+
+    def __init__(self, terms):
+        self.terms = [(phi, s) for phi, s in terms]
+
+    @classmethod
+    def product(cls, phi, s=None):
+        return cls([(phi, s)])
+
+    def factors(self, t):
+        return [1.0 if s is None else float(s(t)) for _, s in self.terms]
+
+    def __call__(self, t, pts):
+        out = 0.0
+        for (phi, _), f in zip(self.terms, self.factors(t)):
+            out = out + f * np.asarray(phi(pts), dtype=float)
+        return out
+
+
+class ParabolicProblem:
+    """``u_t = L u + q + g(u)`` with Dirichlet data ``f`` (reference
+    timestep.py:36-61); ``coeffs`` holds ``A = -L``."""
+
+    def __init__(self, coeffs, q=None, g=None, f=None, f_t=None, u0=None,
+                 time_independent_bc=False, ncomp=1, name="problem"):
+        self.coeffs = coeffs
+        self.q = q
+        self.g = g
+        self.f = f
+        self.f_t = f_t
+        self.u0 = u0
+        self.time_independent_bc = time_independent_bc
+        self.ncomp = ncomp
+        self.name = name
+
+    @property
+    def is_linear(self):
+        return self.g is None
+
+
+class StepperState:
+    """Time and solution.  The solution stays on the device between steps;
+    ``.u`` materialises a host array (cached) for reference-style callers."""
+
+    def __init__(self, t, u):
+        self.t = float(t)
+        self.u = u
+
+    @property
+    def u(self):
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+        return self._host.numpy() if torch.is_tensor(self._host) else self._host
+
+    @u.setter
+    def u(self, v):
+        if torch.is_tensor(v) and v.is_cuda:
+            self._dev, self._host = v, None
+        elif torch.is_tensor(v):          # host tensor (e.g. pinned): copied on first use
+            self._dev, self._host = None, v
+        else:
+            self._dev, self._host = None, np.asarray(v, dtype=float)
+
+    @property
+    def u_device(self):
+        if self._dev is None:
+            src = self._host if torch.is_tensor(self._host) else torch.from_numpy(self._host)
+            self._dev = src.to(cuda_device(), non_blocking=True)
+        return self._dev
+
+
+# ---------------------------------------------------------------------------
+# device leaf evaluations (apply_lop / gradient / flux_jump)
+# ---------------------------------------------------------------------------
+
+class DeviceDiscretization:
+    """Device side of ``EllipticDiscretization`` (operators.py:276-346)."""
+
+    def __init__(self, disc):
+        lib = _lib.load()
+        self.disc, self.tree = disc, disc.tree
+        self.plan = device_plan(self.tree)
+        st, cf = disc.stencil, disc.coeffs
+        samp = np.ascontiguousarray(disc.coefficient_samples(), dtype=float)
+        keep = [np.ascontiguousarray(a, dtype=float)
+                for a in (st.d1x, st.d2x, st.d1y, st.d2y, st.ex1, st.ex2, st.ey1, st.ey2)]
+        sign = np.ascontiguousarray(self.tree.leaf_bnd_sign, dtype=np.int8)
+        d = _lib.DiscDesc()
+        d.d1x, d.d2x, d.d1y, d.d2y, d.ex1, d.ex2, d.ey1, d.ey2 = (_lib.dbl_ptr(a) for a in keep)
+        d.Lc = samp.shape[0]
+        d.coef = _lib.dbl_ptr(samp)
+        d.has_c1, d.has_c2, d.has_c = (int(v is not None) for v in (cf.c1, cf.c2, cf.c))
+        d.leaf_bnd_sign = sign.ctypes.data_as(ctypes.POINTER(ctypes.c_byte))
+        h = ctypes.c_void_p()
+        _lib.check(lib.hps_disc_create(self.plan.handle, ctypes.byref(d), ctypes.byref(h)),
+                   "hps_disc_create")
+        self.handle, self._lib = h, lib
+        self.Lni = self.tree.L * self.tree.ni
+
+    def __del__(self):
+        try:
+            if self.handle:
+                self._lib.hps_disc_destroy(self.handle)
+        except Exception:
+            pass
+
+    def eval(self, U, lu_int=None, lu=None, ux=None, uy=None, jump=None, guard=None, ld_o=None):
+        """One leaf pass over the (k, N) device tensor U (row stride U.stride(0))."""
+        outs = [lu_int, lu, ux, uy, jump]
+        if ld_o is None:
+            ld_o = next((o.stride(0) for o in outs if o is not None), 0)
+        ptr = lambda o: None if o is None else o.data_ptr()
+        rc = self._lib.hps_leaf_eval(self.handle, U.shape[0], U.data_ptr(), U.stride(0),
+                                     *[ptr(o) for o in outs], ld_o, ptr(guard),
+                                     current_stream_handle())
+        _lib.check(rc, "hps_leaf_eval")
+
+    def _prep(self, u):
+        as_numpy = not torch.is_tensor(u)
+        squeeze = (np.ndim(u) if as_numpy else u.dim()) == 1
+        U = torch.atleast_2d(torch.as_tensor(u, dtype=torch.float64, device=cuda_device()))
+        return U.contiguous(), as_numpy, squeeze
+
+    @staticmethod
+    def _ret(X, as_numpy, squeeze):
+        X = X[0] if squeeze else X
+        return X.cpu().numpy() if as_numpy else X
+
+    def apply_lop(self, u):
+        U, a, s = self._prep(u)
+        out = torch.empty_like(U)
+        self.eval(U, lu=out)
+        return self._ret(out, a, s)
+
+    def apply_lop_interior(self, U, out):
+        self.eval(U, lu_int=out)
+        return out
+
+    def gradient(self, u):
+        U, a, s = self._prep(u)
+        ux, uy = torch.empty_like(U), torch.empty_like(U)
+        self.eval(U, ux=ux, uy=uy)
+        return self._ret(ux, a, s), self._ret(uy, a, s)
+
+    def flux_jump(self, u):
+        U, a, s = self._prep(u)
+        out = torch.empty_like(U)
+        self.eval(U, jump=out)
+        return self._ret(out, a, s)
+
+
+def device_discretization(disc):
+    dd = disc._device.get("eval")
+    if dd is None:
+        dd = DeviceDiscretization(disc)
+        disc._device["eval"] = dd
+    return dd
+
+
+def combine(terms, out, n=None, guard=None):
+    """out[:, :n] = sum c * v over (coef, tensor) terms (rows broadcast when a
+    term has a single row)."""
+    lib = _lib.load()
+    terms = [(float(c), v) for c, v in terms if c != 0.0]
+    k = out.shape[0]
+    n = out.shape[1] if n is None else n
+    nt = len(terms)
+    coefs = (ctypes.c_double * max(1, nt))(*[c for c, _ in terms])
+    vecs = (ctypes.c_void_p * max(1, nt))(*[v.data_ptr() for _, v in terms])
+    lds = (ctypes.c_longlong * max(1, nt))(*[0 if v.shape[0] == 1 else v.stride(0)
+                                              for _, v in terms])
+    rc = lib.hps_combine(k, n, nt, coefs, vecs, lds, out.data_ptr(), out.stride(0),
+                         None if guard is None else guard.data_ptr(), current_stream_handle())
+    _lib.check(rc, "hps_combine")
+    return out
+
+
+def evaluate_nonlinear(disc, problem, t, u):
+    """Pointwise g with leaf-local spectral derivatives (timestep.py:64-78)."""
+    as_numpy = not torch.is_tensor(u)
+    squeeze = (np.ndim(u) if as_numpy else u.dim()) == 1
+    dd = device_discretization(disc)
+    U = torch.atleast_2d(torch.as_tensor(u, dtype=torch.float64, device=cuda_device())).contiguous()
+    if problem.g is None:
+        out = torch.zeros_like(U)
+    else:
+        ux, uy = torch.empty_like(U), torch.empty_like(U)
+        dd.eval(U, ux=ux, uy=uy)
+        out = _call_g(problem.g, t, U, ux, uy)
+    out = out[0] if squeeze else out
+    return out.cpu().numpy() if as_numpy else out
+
+
+def _call_g(g, t, U, ux, uy):
+    """g on device tensors when it accepts them, else on host copies."""
+    if getattr(g, "_hb_torch", True):
+        try:
+            r = g(t, U, ux, uy)
+            if torch.is_tensor(r) and r.is_cuda:
+                return torch.broadcast_to(r.to(torch.float64), U.shape)
+        except Exception:
+            pass
+        try:
+            g._hb_torch = False
+        except AttributeError:
+            pass
+    r = np.asarray(g(t, U.cpu().numpy(), ux.cpu().numpy(), uy.cpu().numpy()), dtype=float)
+    return torch.as_tensor(np.broadcast_to(r, U.shape), device=U.device).contiguous()
+
+
+# ---------------------------------------------------------------------------
+# the stepper
+# ---------------------------------------------------------------------------
+
+class _Field:
+    """Device evaluation of a field callable at a fixed point set."""
+
+    def __init__(self, fn, pts, k, dev):
+        self.fn, self.pts, self.k, self.dev = fn, pts, k, dev
+        self.n = pts.shape[0]
+        self.sep = None
+        if fn is None:
+            self.zero = torch.zeros((1, self.n), dtype=torch.float64, device=dev)
+        elif isinstance(fn, SeparableField):
+            self.sep = [self._stack(phi(pts)) for phi, _ in fn.terms]
+
+    def _stack(self, vals):
+        a = np.asarray(vals, dtype=float)
+        a = a.reshape(self.k, self.n) if (a.ndim > 1 or self.k == 1) else a.reshape(1, self.n)
+        return torch.as_tensor(np.ascontiguousarray(a), device=self.dev)
+
+    def terms(self, t, scale=1.0):
+        """(coef, tensor) terms of scale*F(t); evaluates non-separable F now."""
+        if self.fn is None:
+            return []
+        if self.sep is not None:
+            return [(scale * f, phi) for f, phi in zip(self.fn.factors(t), self.sep)]
+        return [(scale, self._stack(self.fn(t, self.pts)))]
+
+    def value(self, t, out=None):
+        """(k or 1, n) tensor of F(t)."""
+        if self.fn is None:
+            return self.zero
+        if self.sep is not None:
+            rows = max(v.shape[0] for v in self.sep)
+            out = torch.empty((rows, self.n), dtype=torch.float64, device=self.dev) \
+                if out is None else out
+            return combine(self.terms(t), out)
+        return self._stack(self.fn(t, self.pts))
+
+
+class TimeStepper:
+    """Fixed-step IMEX integrator (reference timestep.py:89-328) whose stages
+    run on the GPU.  Same constructor, ``set_dt`` / ``shift`` / ``step`` /
+    ``run`` / ``initial_state`` and exceptions."""
+
+    def __init__(self, tree, problem, tableau, dt, formulation="stage", disc=None, threads=None):
+        if formulation not in ("stage", "slope", "slope-penalized"):
+            raise UnsupportedConfigurationError(f"unknown formulation {formulation!r}")
+        self.tree = tree
+        self.problem = problem
+        self.pair = tableau if hasattr(tableau, "Ahat") else load_tableau(tableau)
+        self.formulation = formulation
+        self.penalized = formulation == "slope-penalized"
+        self.disc = disc or EllipticDiscretization(tree, problem.coeffs)
+        self.threads = threads
+        self._step_count = 0
+        if formulation != "stage":
+            if not problem.is_linear and not problem.time_independent_bc:
+                raise UnsupportedConfigurationError(
+                    "slope formulation with a nonlinear term requires time-independent boundary "
+                    "data (slope variables have no boundary interpretation otherwise)")
+            if (problem.is_linear and not problem.time_independent_bc
+                    and problem.f is not None and problem.f_t is None):
+                raise UnsupportedConfigurationError(
+                    "slope formulation with time-dependent boundary data requires f_t")
+        if not problem.is_linear and self.pair.Ahat is None and self.pair.s > 1:
+            raise UnsupportedConfigurationError(
+                f"tableau {self.pair.name} has no explicit half for g")
+        self._bnd_pts = tree.points[tree.boundary_ids]
+        self._all_pts = tree.points
+        self._dev = cuda_device()
+        self._dd = device_discretization(self.disc)
+        self._plan = device_plan(tree)
+        k = problem.ncomp
+        self._k = k
+        self._F = _Field(problem.f, self._bnd_pts, k, self._dev)
+        self._Ft = _Field(None if problem.time_independent_bc else problem.f_t, self._bnd_pts, k,
+                          self._dev)
+        self._Q = _Field(problem.q, self._all_pts, k, self._dev)
+        self._bufs = {}
+        self.solve_timer = None
+        self.dt = None
+        self.ops = None
+        self.ops_id = None
+        self.set_dt(dt)
+
+    # -- operator cache ------------------------------------------------------------------
+    @property
+    def shift(self):
+        return self.dt * self.pair.gamma
+
+    def set_dt(self, dt):
+        """Set the step size, rebuilding the cached operator set (timestep.py:142-157)."""
+        if dt <= 0:
+            raise ValueError(f"dt must be positive, got {dt}")
+        if self.dt == dt and self.ops is not None:
+            return
+        self.dt = float(dt)
+        self.ops = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=self.dt * self.pair.gamma,
+                                  threads=self.threads)
+        if self.formulation != "stage" and self.ops_id is None:
+            self.ops_id = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=0.0, threads=self.threads)
+
+    def _check_ops(self):
+        if self.ops is None or self.ops.dt_gamma != self.dt * self.pair.gamma \
+                or self.ops.sigma != 1.0:
+            raise UnsupportedConfigurationError(
+                "cached operator set does not match dt*gamma; call set_dt")
+
+    # -- device buffers ------------------------------------------------------------------
+    def _buf(self, name, shape):
+        b = self._bufs.get(name)
+        if b is None or tuple(b.shape) != tuple(shape):
+            b = torch.empty(shape, dtype=torch.float64, device=self._dev)
+            self._bufs[name] = b
+        return b
+
+    def _bc(self, t):
+        return self._F.value(t)
+
+    def _bc_t(self, t):
+        return self._Ft.value(t)
+
+    def _g(self, t, U, out=None):
+        """g(t, U) with the interface-averaged device gradient (timestep.py:192-196)."""
+        if self.problem.g is None:
+            return None
+        ux, uy = self._buf("gx", U.shape), self._buf("gy", U.shape)
+        self._dd.eval(U, ux=ux, uy=uy)
+        r = _call_g(self.problem.g, t, U, ux, uy)
+        if out is not None:
+            out.copy_(r)
+            return out
+        return r
+
+    def initial_state(self):
+        u0 = np.asarray(self.problem.u0(self._all_pts), dtype=float)
+        k, N = self._k, self.tree.N
+        u0 = u0.reshape(k, N) if (u0.ndim > 1 or k == 1) else np.broadcast_to(u0, (k, N))
+        return StepperState(0.0, u0 if k > 1 else u0[0])
+
+    # -- stepping ------------------------------------------------------------------------
+    def step(self, state):
+        """Advance one step of size dt, returning a new state (timestep.py:211-224)."""
+        new, guards = self._advance(state)
+        self._raise_if_diverged(guards, self._step_count)
+        self._step_count += 1
+        return new
+
+    def run(self, state, nsteps, check_every=32):
+        """``nsteps`` steps; the divergence guard is read back once per
+        ``check_every`` steps (the first failing step is reported exactly)."""
+        pending = []
+        for _ in range(nsteps):
+            state, guards = self._advance(state)
+            pending.append(guards)
+            if len(pending) >= check_every:
+                self._drain(pending)
+        self._drain(pending)
+        return state
+
+    def _drain(self, pending):
+        if not pending:
+            return
+        host = torch.stack(pending).cpu().numpy()
+        for g in host:
+            self._raise_if_diverged(g, self._step_count, host_vals=True)
+            self._step_count += 1
+        pending.clear()
+
+    def _raise_if_diverged(self, guards, step, host_vals=False):
+        """guards = [stage maxima..., final max]; a stage failure reports the
+        step count before the increment, the final one after (timestep.py:219-222)."""
+        g = guards if host_vals else guards.cpu().numpy()
+        for i, mx in enumerate(g):
+            if not np.isfinite(mx) or mx > DIVERGENCE_LIMIT:
+                final = i == len(g) - 1
+                n = step + 1 if final else step
+                raise DivergenceError(f"solution diverged at step {n} (max|u| = {mx:.3e})", step=n)
+
+    def _advance(self, state):
+        self._check_ops()
+        squeeze = (state.u_device.dim() == 1)
+        u = torch.atleast_2d(state.u_device)
+        if u.dtype != torch.float64:
+            u = u.to(torch.float64)
+        u = u.contiguous()
+        s = self.pair.s
+        guards = torch.zeros(s, dtype=torch.float64, device=self._dev)
+        if s == 1:
+            unew = self._step_backward_euler(state.t, u, guards)
+        elif self.formulation == "stage":
+            unew = self._step_stage(state.t, u, guards)
+        else:
+            unew = self._step_slope(state.t, u, guards)
+        return StepperState(state.t + self.dt, unew[0] if squeeze else unew), guards
+
+    def _solve(self, ops, fb, body, out, jump=None, inv_dt=None):
+        tm = self.solve_timer
+        if tm is not None:                      # bench hook: CUDA events around each solve
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+        ops.solve_device(fb, body, out, jump=jump, inv_dt=inv_dt)
+        if tm is not None:
+            e1.record()
+            tm.append((e0, e1))
+        return out
+
+    def _step_backward_euler(self, t, u, guards):
+        dt, k, N = self.dt, u.shape[0], self.tree.N
+        t1 = t + dt
+        r = self._buf("r", (k, self._dd.Lni))
+        terms = [(1.0, u)] + self._Q.terms(t1, dt)
+        G = self._g(t, u)
+        if G is not None:
+            terms.append((dt, G))
+        combine(terms, r, n=self._dd.Lni)
+        unew = torch.empty((k, N), dtype=torch.float64, device=self._dev)
+        self._solve(self.ops, self._bc(t1), r, unew)
+        _lib.check(_lib.load().hps_maxabs(k, N, unew.data_ptr(), N, guards[0].data_ptr(),
+                                          current_stream_handle()), "hps_maxabs")
+        return unew
+
+    def _step_stage(self, t, u, guards):
+        """timestep.py:237-266 on the device."""
+        pair, dt = self.pair, self.dt
+        s, k, N, Lni = pair.s, u.shape[0], self.tree.N, self._dd.Lni
+        A, Ah = pair.A, pair.Ahat
+        Lu = self._buf("Lu", (s, k, Lni))
+        nonlin = self.problem.g is not None
+        QG = self._buf("QG", (s, k, N)) if (nonlin or (self._Q.fn is not None and self._Q.sep is None)) \
+            else None
+        qsep = self._Q.sep
+        qfac = []                                    # per stage: separable q time factors
+        r = self._buf("r", (k, Lni))
+        U = [self._buf("u0", (k, N)), self._buf("u1", (k, N))]
+
+        def stage_q_g(i, ti, ui):
+            if qsep is not None:
+                qfac.append(self._Q.fn.factors(ti))
+            if QG is not None:
+                terms = [] if qsep is not None else self._Q.terms(ti)
+                G = self._g(ti, ui)
+                if G is not None:
+                    terms.append((1.0, G))
+                if terms:
+                    combine(terms, QG[i])
+                else:
+                    QG[i].zero_()
+
+        self._dd.eval(u, lu_int=Lu[0])
+        stage_q_g(0, t + pair.c[0] * dt, u)
+        ui = u
+        for i in range(1, s):
+            ti = t + pair.c[i] * dt
+            terms = [(1.0, u)]
+            terms += [(dt * A[i, j], Lu[j]) for j in range(i)]
+            if QG is not None:
+                terms += [(dt * Ah[i, j], QG[j]) for j in range(i)]
+            if qsep is not None:
+                for m, phi in enumerate(qsep):
+                    terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), phi))
+            combine(terms, r, n=Lni)
+            ui = U[i & 1]
+            self._solve(self.ops, self._bc(ti), r, ui)
+            if i < s - 1:
+                self._dd.eval(ui, lu_int=Lu[i], guard=guards[i - 1])
+            else:
+                _lib.check(_lib.load().hps_maxabs(k, N, ui.data_ptr(), N, guards[i - 1].data_ptr(),
+                                                  current_stream_handle()), "hps_maxabs")
+            stage_q_g(i, ti, ui)
+        w = pair.bhat - Ah[s - 1]
+        terms = [(1.0, ui)]
+        if QG is not None:
+            terms += [(dt * w[j], QG[j]) for j in range(s)]
+        if qsep is not None:
+            for m, phi in enumerate(qsep):
+                terms.append((sum(dt * w[j] * qfac[j][m] for j in range(s)), phi))
+        unew = torch.empty((k, N), dtype=torch.float64, device=self._dev)
+        combine(terms, unew)
+        fb = self._bc(t + dt)
+        lib = _lib.load()
+        _lib.check(lib.hps_put_boundary(self._plan.handle, k, fb.data_ptr(),
+                                        0 if fb.shape[0] == 1 else fb.stride(0), unew.data_ptr(), N,
+                                        current_stream_handle()), "hps_put_boundary")
+        _lib.check(lib.hps_maxabs(k, N, unew.data_ptr(), N, guards[s - 1].data_ptr(),
+                                  current_stream_handle()), "hps_maxabs")
+        return unew
+
+    # -- slope formulations (timestep.py:268-328) ----------------------------------------
+    def _slope_assign(self, bc, body, jump, out):
+        if jump is not None:
+            return self._solve(self.ops_id, bc, body, out, jump=jump, inv_dt=1.0 / self.dt)
+        return self._solve(self.ops_id, bc, body, out)
+
+    def _step_slope(self, t, u, guards):
+        pair, dt = self.pair, self.dt
+        s, k, N, Lni = pair.s, u.shape[0], self.tree.N, self._dd.Lni
+        A, Ah = pair.A, pair.Ahat
+        nonlinear = not self.problem.is_linear
+        dev = self._dev
+        jump = None
+        if self.penalized:
+            jump = self._buf("jump", (k, N))
+            self._dd.eval(u, jump=jump)
+        Lun = self._buf("Lun", (k, Lni))
+        self._dd.eval(u, lu_int=Lun)
+        K = torch.empty((s, k, N), dtype=torch.float64, device=dev)
+        LK = self._buf("LK", (s, k, Lni))
+        r = self._buf("r", (k, Lni))
+        zero_bc = torch.zeros((1, self._bnd_pts.shape[0]), dtype=torch.float64, device=dev)
+        t0 = t + pair.c[0] * dt
+        combine([(1.0, Lun)] + self._Q.terms(t0), r, n=Lni)
+        self._slope_assign(self._bc_t(t0), r, jump, K[0])
+        self._dd.eval(K[0], lu_int=LK[0])
+        if nonlinear:
+            Lv = torch.empty((s, k, N), dtype=torch.float64, device=dev)
+            Ls = self._buf("Ls", (s, k, Lni))
+            gb = self._buf("gbody", (k, N))
+            self._g(t0, u, out=gb)
+            self._slope_assign(zero_bc, gb, None, Lv[0])
+            self._dd.eval(Lv[0], lu_int=Ls[0])
+        for i in range(1, s):
+            ti = t + pair.c[i] * dt
+            terms = [(1.0, Lun)] + [(dt * A[i, j], LK[j]) for j in range(i)] + self._Q.terms(ti)
+            if nonlinear:
+                terms += [(dt * Ah[i, j], Ls[j]) for j in range(i)]
+            combine(terms, r, n=Lni)
+            if self.penalized:
+                self._solve(self.ops, self._bc_t(ti), r, K[i], jump=jump, inv_dt=1.0 / dt)
+            else:
+                self._solve(self.ops, self._bc_t(ti), r, K[i])
+            need_lk = i < s - 1 or nonlinear
+            if need_lk:
+                self._dd.eval(K[i], lu_int=LK[i], guard=guards[i - 1])
+            else:
+                _lib.check(_lib.load().hps_maxabs(k, N, K[i].data_ptr(), N,
+                                                  guards[i - 1].data_ptr(),
+                                                  current_stream_handle()), "hps_maxabs")
+            if nonlinear:
+                v = self._buf("v", (k, N))
+                combine([(1.0, u)] + [(dt * A[i, j], K[j]) for j in range(i + 1)]
+                        + [(dt * Ah[i, j], Lv[j]) for j in range(i)], v)
+                self._g(ti, v, out=gb)
+                self._slope_assign(zero_bc, gb, None, Lv[i])
+                self._dd.eval(Lv[i], lu_int=Ls[i])
+        terms = [(1.0, u)] + [(dt * pair.b[j], K[j]) for j in range(s)]
+        if nonlinear:
+            terms += [(dt * pair.bhat[j], Lv[j]) for j in range(s)]
+        unew = torch.empty((k, N), dtype=torch.float64, device=dev)
+        combine(terms, unew)
+        _lib.check(_lib.load().hps_maxabs(k, N, unew.data_ptr(), N, guards[s - 1].data_ptr(),
+                                          current_stream_handle()), "hps_maxabs")
+        return unew
+
+
+def scalar_stability_function(pair, z):
+    """Amplification factor of the implicit half on u' = lambda*u."""
+    return pair.stability_function(z)

@@ -200,7 +200,45 @@ def be_case():
     save("step_be", u3=s.u, dt=1e-2)
 
 
+def evals_case():
+    """apply_lop / gradient / flux_jump (operators.py:276-336), variable
+    coefficients on a 4x2 p=9 tree, k=2 stacked seeded fields."""
+    tree = build_tree(UNIT, 4, 2, 9)
+    disc = EllipticDiscretization(tree, coeffs_var_test())
+    rng = np.random.default_rng(31)
+    u = rng.standard_normal((2, tree.N))
+    ux, uy = disc.gradient(u)
+    save("evals_var4x2p9", u=u, lu=disc.apply_lop(u), ux=ux, uy=uy, jump=disc.flux_jump(u),
+         lu1=disc.apply_lop(u[0]))
+
+
+def slope_cases():
+    """Slope / penalized-slope formulations (timestep.py:268-328) at 4x4 p=10:
+    linear heat with time-dependent BC (f_t given) and nonlinear Allen-Cahn."""
+    tree = build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    ut = lambda t, pts: -phi(pts) * np.sin(t)
+    lap = OperatorCoefficients(c11=1.0, c22=1.0, dim=2)
+    out = {}
+    for form in ("slope", "slope-penalized"):
+        prob = ParabolicProblem(coeffs=lap, q=q, f=uex, f_t=ut, u0=lambda pts: uex(0.0, pts))
+        st = TimeStepper(tree, prob, "ARK4", dt=1e-3, formulation=form)
+        s = st.run(st.initial_state(), 3)
+        out[form.replace("-", "_")] = s.u.copy()
+    coef = sine_modes(3)
+    prob = ParabolicProblem(coeffs=OperatorCoefficients(c11=0.01, c22=0.01, dim=2),
+                            g=lambda t, u, ux, uy: u - u ** 3,
+                            u0=lambda pts: sine_field(coef, pts), time_independent_bc=True)
+    st = TimeStepper(tree, prob, "ARK4", dt=1e-2, formulation="slope-penalized")
+    s = st.run(st.initial_state(), 3)
+    save("step_slope", modes=coef, **out, ac_pen=s.u.copy())
+
+
 def main():
+    if "--only" in sys.argv:
+        for name in sys.argv[sys.argv.index("--only") + 1:]:
+            globals()[name]()
+        return
     tree_case("2x2p6", UNIT, 2, 2, 6)
     tree_case("4x2p9", UNIT, 4, 2, 9)
     tree_case("4x4p7", UNIT, 4, 4, 7)
@@ -220,6 +258,8 @@ def main():
     burgers_var_case()
     ensemble_case()
     be_case()
+    evals_case()
+    slope_cases()
 
 
 if __name__ == "__main__":

@@ -1,0 +1,181 @@
+"""Device time stepping and leaf evaluations against vectors produced by the
+real reference (tests/golden/make_golden.py).  Needs a B200."""
+
+import numpy as np
+import pytest
+
+from tests.problems import (UNIT, c4_fields, heat_manufactured, lap_fields, rel_l2, sine_field,
+                            var_test_fields)
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10   # north-star parity bar (relative L2, per stage and at the final time)
+
+
+def _hb():
+    import paper_2306_02526_b200 as hb
+    return hb
+
+
+def test_leaf_evaluations_match_reference(golden):
+    hb = _hb()
+    z = golden("evals_var4x2p9")
+    tree = hb.build_tree(UNIT, 4, 2, 9)
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(**var_test_fields()))
+    assert rel_l2(disc.apply_lop(z["u"]), z["lu"]) < 1e-13
+    lu1 = disc.apply_lop(z["u"][0])
+    assert lu1.shape == z["lu1"].shape and rel_l2(lu1, z["lu1"]) < 1e-13
+    ux, uy = disc.gradient(z["u"])
+    assert rel_l2(ux, z["ux"]) < 1e-13 and rel_l2(uy, z["uy"]) < 1e-13
+    assert rel_l2(disc.flux_jump(z["u"]), z["jump"]) < 1e-13
+
+
+def _c1_stepper(hb, separable):
+    tree = hb.build_tree(UNIT, 8, 8, 12)
+    phi, uex, q = heat_manufactured()
+    if separable:
+        qf = hb.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
+        ff = hb.SeparableField.product(phi, np.cos)
+    else:
+        qf, ff = q, uex
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0), q=qf, f=ff,
+                               u0=lambda pts: uex(0.0, pts))
+    return tree, hb.TimeStepper(tree, prob, "ARK4", dt=1e-3), uex
+
+
+@pytest.mark.parametrize("separable", [True, False])
+def test_c1_heat_matches_reference(golden, separable):
+    hb = _hb()
+    z = golden("step_c1")
+    tree, st, uex = _c1_stepper(hb, separable)
+    stages = []
+    orig = st.ops.solve_device
+
+    def rec(fb, body, out, **kw):
+        r = orig(fb, body, out, **kw)
+        stages.append(out[0].cpu().numpy().copy())
+        return r
+
+    st.ops.solve_device = rec
+    s = st.step(st.initial_state())
+    st.ops.solve_device = orig
+    for i, (a, b) in enumerate(zip(stages, z["stages"])):
+        assert rel_l2(a, b) < TOL, f"stage {i + 1}"
+    assert isinstance(s.u, np.ndarray) and s.u.shape == (tree.N,)
+    assert rel_l2(s.u, z["u1"]) < TOL
+    s = st.run(s, 9)
+    assert rel_l2(s.u, z["u10"]) < TOL
+    s = st.run(s, 90)
+    assert abs(s.t - float(z["t100"])) < 1e-12
+    assert rel_l2(s.u, z["u100"]) < TOL
+    assert np.abs(s.u - uex(s.t, tree.points)).max() < 1e-10
+
+
+def test_allen_cahn_matches_reference(golden):
+    hb = _hb()
+    z = golden("step_allen_cahn")
+    tree = hb.build_tree(UNIT, 8, 8, 12)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=0.01, c22=0.01),
+                               g=lambda t, u, ux, uy: u - u ** 3,
+                               u0=lambda pts: sine_field(z["modes"], pts), time_independent_bc=True)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=float(z["dt"]))
+    s = st.step(st.initial_state())
+    assert rel_l2(s.u, z["u1"]) < TOL
+    s = st.run(s, 9)
+    assert rel_l2(s.u, z["u10"]) < TOL
+
+
+def test_burgers_variable_coefficients_matches_reference(golden):
+    hb = _hb()
+    z = golden("step_burgers_var")
+    tree = hb.build_tree(UNIT, 8, 8, 10)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**c4_fields()),
+                               g=lambda t, u, ux, uy: -u * ux,
+                               u0=lambda pts: sine_field(z["modes"], pts), time_independent_bc=True)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=float(z["dt"]))
+    s = st.step(st.initial_state())
+    assert rel_l2(s.u, z["u1"]) < TOL
+    s = st.run(s, 4)
+    assert rel_l2(s.u, z["u5"]) < TOL
+
+
+@pytest.mark.parametrize("separable", [True, False])
+def test_ensemble_matches_reference(golden, separable):
+    hb = _hb()
+    z = golden("step_ensemble")
+    coef = z["modes"]
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    qf = (hb.SeparableField.product(lambda pts: sine_field(coef, pts)) if separable
+          else (lambda t, pts: sine_field(coef, pts)))
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**lap_fields()), q=qf,
+                               u0=lambda pts: np.zeros((4, pts.shape[0])),
+                               time_independent_bc=True, ncomp=4)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=float(z["dt"]))
+    s = st.run(st.initial_state(), 3)
+    assert s.u.shape == (4, tree.N)
+    assert rel_l2(s.u, z["u3"]) < TOL
+
+
+def test_backward_euler_matches_reference(golden):
+    hb = _hb()
+    z = golden("step_be")
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**lap_fields()), q=q, f=uex,
+                               u0=lambda pts: uex(0.0, pts))
+    st = hb.TimeStepper(tree, prob, "BE", dt=float(z["dt"]))
+    s = st.run(st.initial_state(), 3)
+    assert rel_l2(s.u, z["u3"]) < TOL
+
+
+@pytest.mark.parametrize("form", ["slope", "slope-penalized"])
+def test_slope_formulations_match_reference(golden, form):
+    hb = _hb()
+    z = golden("step_slope")
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**lap_fields()), q=q, f=uex,
+                               f_t=lambda t, pts: -phi(pts) * np.sin(t),
+                               u0=lambda pts: uex(0.0, pts))
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=1e-3, formulation=form)
+    s = st.run(st.initial_state(), 3)
+    assert rel_l2(s.u, z[form.replace("-", "_")]) < TOL
+
+
+def test_nonlinear_penalized_slope_matches_reference(golden):
+    hb = _hb()
+    z = golden("step_slope")
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=0.01, c22=0.01),
+                               g=lambda t, u, ux, uy: u - u ** 3,
+                               u0=lambda pts: sine_field(z["modes"], pts), time_independent_bc=True)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=1e-2, formulation="slope-penalized")
+    s = st.run(st.initial_state(), 3)
+    assert rel_l2(s.u, z["ac_pen"]) < TOL
+
+
+def test_divergence_guard_reports_step():
+    hb = _hb()
+    tree = hb.build_tree(UNIT, 2, 2, 8)
+    # explosive reaction: u_t = Lu + 1e4 u^2 blows up within a few steps
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0),
+                               g=lambda t, u, ux, uy: 1e4 * u * u,
+                               u0=lambda pts: 10.0 + 0 * pts[:, 0], time_independent_bc=True,
+                               f=lambda t, pts: 10.0 + 0 * pts[:, 0])
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=1e-2)
+    with pytest.raises(hb.DivergenceError) as e:
+        st.run(st.initial_state(), 50)
+    assert e.value.step is not None and e.value.step <= 50
+
+
+def test_mismatched_shift_is_rejected():
+    hb = _hb()
+    tree = hb.build_tree(UNIT, 2, 2, 8)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0),
+                               u0=lambda pts: 0 * pts[:, 0])
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=1e-2)
+    st.dt = 2e-2
+    with pytest.raises(hb.UnsupportedConfigurationError):
+        st.step(st.initial_state())
+    st.set_dt(5e-3)
+    st.step(st.initial_state())

@@ -120,3 +120,15 @@ def test_oracle_backward_euler_matches_reference(golden):
     st = O.OStepper(tree, O.OCoeffs(**lap_fields()), O.be_tableau(), float(z["dt"]), q=q, f=uex)
     t, u = st.run(0.0, uex(0.0, tree.points), 3)
     assert rel_l2(u, z["u3"]) < 1e-13
+
+
+def test_oracle_leaf_evaluations_match_reference(golden):
+    from tests.problems import var_test_fields
+    z = golden("evals_var4x2p9")
+    tree = O.OTree(UNIT, 4, 2, 9)
+    disc = O.ODisc(tree, O.OCoeffs(**var_test_fields()))
+    assert rel_l2(disc.apply_lop(z["u"]), z["lu"]) < 1e-13
+    assert rel_l2(disc.apply_lop(z["u"][0]), z["lu1"]) < 1e-13
+    ux, uy = disc.gradient(z["u"])
+    assert rel_l2(ux, z["ux"]) < 1e-13 and rel_l2(uy, z["uy"]) < 1e-13
+    assert rel_l2(disc.flux_jump(z["u"]), z["jump"]) < 1e-13
