@@ -30,7 +30,6 @@ int leaf_assemble(int Lc, int ni, int nb, const double* cv, int has_c1, int has_
 int merge_gather(int c, int n3, int n1a, int n2b, int nbc, const double* Tc, long long sTc, const int* i1a,
                  const int* i3a, const int* i2b, const int* i3b, double* X33, double* R, double* Tst, int ld3,
                  double* Tnew, cudaStream_t st);
-int broadcast_copies(long long n, int copies, double* base, cudaStream_t st);
 
 static const double kPivotRtol = 1e-13;  // linalg.py:17
 
@@ -207,18 +206,24 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   double* Aii = talloc((size_t)Lc * ni * ni);
   double* Aib = talloc((size_t)Lc * ni * nb);
   double* stats = talloc(2 * (size_t)std::max(Lc, 1));
-  O.Ainv = ops_alloc(O, (size_t)Lc * ni * P.ldi, true);
-  O.S_leaf = ops_alloc(O, (size_t)Lc * ni * P.ldb, true);
+  // shared leaf: row-major operands of the leaf GEMMs; per-leaf: build row-major, then pack
+  // shared leaf: rows ni..ni+nb-1 hold D_bi Ainv, so the solve's leaf pass is one GEMM for [w | h]
+  double* Ainv = O.shared_leaf ? ops_alloc(O, (size_t)(ni + nb) * P.ldi, true) : talloc((size_t)Lc * ni * P.ldi);
+  double* Sl = O.shared_leaf ? ops_alloc(O, (size_t)Lc * ni * P.ldb, true) : talloc((size_t)Lc * ni * P.ldb);
   double* Tleaf = d->keep_dtn ? ops_alloc(O, (size_t)Lc * nb * nb, false) : talloc((size_t)Lc * nb * nb);
-  if (!Aii || !Aib || !stats || !O.Ainv || !O.S_leaf || !Tleaf) {
+  if (!Aii || !Aib || !stats || !Ainv || !Sl || !Tleaf) {
     set_error("out of device memory (leaf build)");
     return fail(HPS_ERR_CUDA);
+  }
+  if (!O.shared_leaf) {
+    cudaMemsetAsync(Ainv, 0, (size_t)Lc * ni * P.ldi * 8, st);
+    cudaMemsetAsync(Sl, 0, (size_t)Lc * ni * P.ldb * 8, st);
   }
   if (d->keep_dtn) O.T_leaf = Tleaf;
   if (int rc = leaf_assemble(Lc, ni, nb, dcoef, d->has_c1, d->has_c2, d->has_c, dD2x, dD2y, dD1x, dD1y,
                              d->sigma, d->dt_gamma, Aii, Aib, st))
     return fail(rc);
-  if (int rc = gj_invert(ni, Lc, Aii, O.Ainv, P.ldi, (long long)ni * P.ldi, stats, st)) return fail(rc);
+  if (int rc = gj_invert(ni, Lc, Aii, Ainv, P.ldi, (long long)ni * P.ldi, stats, st)) return fail(rc);
   {
     std::vector<double> hs;
     int bad = check_pivots(stats, Lc, ni, hs, st);
@@ -228,17 +233,37 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   {
     GemmArgs a{};  // S = -Ainv A_ib
     a.M = ni; a.N = nb; a.K = ni; a.alpha = -1.0; a.beta = 0.0;
-    a.A = O.Ainv; a.lda = P.ldi; a.sA = (long long)ni * P.ldi; a.tA = 0;
+    a.A = Ainv; a.lda = P.ldi; a.sA = (long long)ni * P.ldi; a.tA = 0;
     a.B = Aib; a.ldb = nb; a.sB = (long long)ni * nb; a.tB = 0;
-    a.C = O.S_leaf; a.ldc = P.ldb; a.sC = (long long)ni * P.ldb; a.batch = Lc;
+    a.C = Sl; a.ldc = P.ldb; a.sC = (long long)ni * P.ldb; a.batch = Lc;
     if (int rc = gemm(a, st)) return fail(rc);
     GemmArgs t{};  // T = D_bi S + D_bb
     t.M = nb; t.N = nb; t.K = ni; t.alpha = 1.0; t.beta = 1.0;
     t.A = O.D_bi; t.lda = ni; t.sA = 0; t.tA = 0;
-    t.B = O.S_leaf; t.ldb = P.ldb; t.sB = (long long)ni * P.ldb; t.tB = 0;
+    t.B = Sl; t.ldb = P.ldb; t.sB = (long long)ni * P.ldb; t.tB = 0;
     t.D = dDbb; t.ldd = nb; t.sD = 0;
     t.C = Tleaf; t.ldc = nb; t.sC = (long long)nb * nb; t.batch = Lc;
     if (int rc = gemm(t, st)) return fail(rc);
+  }
+  if (O.shared_leaf) {
+    GemmArgs e{};  // E = D_bi Ainv (nb x ni) below Ainv
+    e.M = nb; e.N = ni; e.K = ni; e.alpha = 1.0; e.beta = 0.0;
+    e.A = O.D_bi; e.lda = ni; e.sA = 0; e.tA = 0;
+    e.B = Ainv; e.ldb = P.ldi; e.sB = 0; e.tB = 0;
+    e.C = Ainv + (size_t)ni * P.ldi; e.ldc = P.ldi; e.sC = 0; e.batch = 1;
+    if (int rc = gemm(e, st)) return fail(rc);
+    O.Ainv = Ainv;
+    O.S_leaf = Sl;
+  } else {
+    O.pAinv = make_panel(P.L, ni, ni);
+    O.pSleaf = make_panel(P.L, ni, nb);
+    O.pAinv.base = ops_alloc(O, O.pAinv.doubles(), false);
+    O.pSleaf.base = ops_alloc(O, O.pSleaf.doubles(), false);
+    if (!O.pAinv.base || !O.pSleaf.base) { set_error("out of device memory (leaf panels)"); return fail(HPS_ERR_CUDA); }
+    if (int rc = pack_panel(Ainv, (long long)ni * P.ldi, P.ldi, O.pAinv, st)) return fail(rc);
+    if (int rc = pack_panel(Sl, (long long)ni * P.ldb, P.ldb, O.pSleaf, st)) return fail(rc);
+    tfree(Ainv);
+    tfree(Sl);
   }
   tfree(Aii); tfree(Aib); tfree(stats);
 
@@ -250,24 +275,32 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     LevelOps& lo = O.lo[l];
     const int ce = O.shared_leaf ? 1 : lv.c;
     const int n3 = lv.n3, n12 = lv.n12;
-    lo.Xinv = ops_alloc(O, (size_t)lv.c * n3 * lv.ld3, true);
-    lo.Tst = ops_alloc(O, (size_t)lv.c * n12 * lv.ld3, true);
-    lo.S = ops_alloc(O, (size_t)lv.c * n3 * lv.ld12, true);
+    double* Xinv = talloc((size_t)ce * n3 * lv.ld3);
+    double* Tst = talloc((size_t)ce * n12 * lv.ld3);
+    double* S = talloc((size_t)ce * n3 * lv.ld12);
     // every level's DtN map feeds its parent; the root's is kept (solver.py:155)
-    const bool needT = true;
     const bool keepT = d->keep_dtn || l == 0;
     double* Tnew = keepT ? ops_alloc(O, (size_t)ce * n12 * n12, false) : talloc((size_t)ce * n12 * n12);
     double* X33 = talloc((size_t)ce * n3 * n3);
     double* R = talloc((size_t)ce * n3 * n12);
     double* lst = talloc(2 * (size_t)ce);
-    if (!lo.Xinv || !lo.Tst || !lo.S || (needT && !Tnew) || !X33 || !R || !lst) {
+    lo.Xinv = make_panel(lv.c, n3, n3);
+    lo.Tst = make_panel(lv.c, n12, n3);
+    lo.S = make_panel(lv.c, n3, n12);
+    lo.Xinv.base = ops_alloc(O, lo.Xinv.doubles(), false);
+    lo.Tst.base = ops_alloc(O, lo.Tst.doubles(), false);
+    lo.S.base = ops_alloc(O, lo.S.doubles(), false);
+    if (!Xinv || !Tst || !S || !Tnew || !X33 || !R || !lst || !lo.Xinv.base || !lo.Tst.base || !lo.S.base) {
       set_error("out of device memory (merge level %d)", l);
       return fail(HPS_ERR_CUDA);
     }
+    cudaMemsetAsync(Xinv, 0, (size_t)ce * n3 * lv.ld3 * 8, st);
+    cudaMemsetAsync(Tst, 0, (size_t)ce * n12 * lv.ld3 * 8, st);
+    cudaMemsetAsync(S, 0, (size_t)ce * n3 * lv.ld12 * 8, st);
     if (int rc = merge_gather(ce, n3, lv.n1a, lv.n2b, lv.nbc, Tchild, sTchild, lv.i1a, lv.i3a, lv.i2b, lv.i3b,
-                              X33, R, lo.Tst, lv.ld3, Tnew, st))
+                              X33, R, Tst, lv.ld3, Tnew, st))
       return fail(rc);
-    if (int rc = gj_invert(n3, ce, X33, lo.Xinv, lv.ld3, (long long)n3 * lv.ld3, lst, st)) return fail(rc);
+    if (int rc = gj_invert(n3, ce, X33, Xinv, lv.ld3, (long long)n3 * lv.ld3, lst, st)) return fail(rc);
     {
       std::vector<double> hs;
       int bad = check_pivots(lst, ce, n3, hs, st);
@@ -276,24 +309,26 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     }
     GemmArgs a{};  // S = Xinv [-Ta31 | Tb32]
     a.M = n3; a.N = n12; a.K = n3; a.alpha = 1.0; a.beta = 0.0;
-    a.A = lo.Xinv; a.lda = lv.ld3; a.sA = (long long)n3 * lv.ld3; a.tA = 0;
+    a.A = Xinv; a.lda = lv.ld3; a.sA = (long long)n3 * lv.ld3; a.tA = 0;
     a.B = R; a.ldb = n12; a.sB = (long long)n3 * n12; a.tB = 0;
-    a.C = lo.S; a.ldc = lv.ld12; a.sC = (long long)n3 * lv.ld12; a.batch = ce;
+    a.C = S; a.ldc = lv.ld12; a.sC = (long long)n3 * lv.ld12; a.batch = ce;
     if (int rc = gemm(a, st)) return fail(rc);
-    if (needT) {
+    {
       GemmArgs t{};  // T = blkdiag + Tstack S
       t.M = n12; t.N = n12; t.K = n3; t.alpha = 1.0; t.beta = 1.0;
-      t.A = lo.Tst; t.lda = lv.ld3; t.sA = (long long)n12 * lv.ld3; t.tA = 0;
-      t.B = lo.S; t.ldb = lv.ld12; t.sB = (long long)n3 * lv.ld12; t.tB = 0;
+      t.A = Tst; t.lda = lv.ld3; t.sA = (long long)n12 * lv.ld3; t.tA = 0;
+      t.B = S; t.ldb = lv.ld12; t.sB = (long long)n3 * lv.ld12; t.tB = 0;
       t.D = Tnew; t.ldd = n12; t.sD = (long long)n12 * n12;
       t.C = Tnew; t.ldc = n12; t.sC = (long long)n12 * n12; t.batch = ce;
       if (int rc = gemm(t, st)) return fail(rc);
     }
-    if (ce < lv.c) {  // constant coefficients: every node of a level is identical
-      if (int rc = broadcast_copies((long long)n3 * lv.ld3, lv.c, lo.Xinv, st)) return fail(rc);
-      if (int rc = broadcast_copies((long long)n12 * lv.ld3, lv.c, lo.Tst, st)) return fail(rc);
-      if (int rc = broadcast_copies((long long)n3 * lv.ld12, lv.c, lo.S, st)) return fail(rc);
-    }
+    // pack into the streaming layout; constant coefficients: every node of a
+    // level is identical (solver.py stores one copy per node, so do we)
+    const long long bx = ce < lv.c ? 0 : 1;
+    if (int rc = pack_panel(Xinv, bx * n3 * lv.ld3, lv.ld3, lo.Xinv, st)) return fail(rc);
+    if (int rc = pack_panel(Tst, bx * n12 * lv.ld3, lv.ld3, lo.Tst, st)) return fail(rc);
+    if (int rc = pack_panel(S, bx * n3 * lv.ld12, lv.ld12, lo.S, st)) return fail(rc);
+    tfree(Xinv); tfree(Tst); tfree(S);
     if (!d->keep_dtn) tfree(Tchild);
     tfree(X33); tfree(R); tfree(lst);
     if (keepT) lo.T = Tnew;
@@ -310,12 +345,26 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   return HPS_OK;
 }
 
+static int copy_panel_block(const Panel& pn, int node, double* host) {
+  double* tmp = nullptr;
+  HPSB_CUDA(cudaDeviceSynchronize());
+  HPSB_CUDA(cudaMalloc(&tmp, (size_t)pn.R * pn.C * 8 + 8));
+  int rc = unpack_panel(pn, node, tmp, 0);
+  if (!rc && cudaMemcpy(host, tmp, (size_t)pn.R * pn.C * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    set_error("copy failed");
+    rc = HPS_ERR_CUDA;
+  }
+  cudaFree(tmp);
+  return rc;
+}
+
 int hps_ops_get_leaf(const hps_ops* h, int which, int leaf, double* host) {
   if (!h) return HPS_ERR_ARG;
   const Ops& O = h->O;
   const Plan& P = *O.plan;
   int l = O.shared_leaf ? 0 : leaf;
   if (leaf < 0 || leaf >= P.L) { set_error("leaf out of range"); return HPS_ERR_ARG; }
+  if (!O.shared_leaf && which <= 1) return copy_panel_block(which == 0 ? O.pAinv : O.pSleaf, leaf, host);
   const double* src; int rows, cols, ld;
   if (which == 0) { src = O.Ainv + (size_t)l * P.ni * P.ldi; rows = P.ni; cols = P.ni; ld = P.ldi; }
   else if (which == 1) { src = O.S_leaf + (size_t)l * P.ni * P.ldb; rows = P.ni; cols = P.nb; ld = P.ldb; }
@@ -334,17 +383,18 @@ int hps_ops_get_merge(const hps_ops* h, int level, int node, int which, double* 
   const Level& lv = P.lv[level];
   const LevelOps& lo = O.lo[level];
   if (node < 0 || node >= lv.c) { set_error("node out of range"); return HPS_ERR_ARG; }
-  const double* src; int rows, cols, ld;
-  if (which == 0) { src = lo.Xinv + (size_t)node * lv.n3 * lv.ld3; rows = lv.n3; cols = lv.n3; ld = lv.ld3; }
-  else if (which == 1) { src = lo.Tst + (size_t)node * lv.n12 * lv.ld3; rows = lv.n12; cols = lv.n3; ld = lv.ld3; }
-  else if (which == 2) { src = lo.S + (size_t)node * lv.n3 * lv.ld12; rows = lv.n3; cols = lv.n12; ld = lv.ld12; }
-  else if (which == 3 && lo.T) {
+  if (which == 0) return copy_panel_block(lo.Xinv, node, host);
+  if (which == 1) return copy_panel_block(lo.Tst, node, host);
+  if (which == 2) return copy_panel_block(lo.S, node, host);
+  if (which == 3 && lo.T) {
     int nn = O.shared_leaf ? 0 : node;
-    src = lo.T + (size_t)nn * lv.n12 * lv.n12; rows = lv.n12; cols = lv.n12; ld = lv.n12;
-  } else { set_error("merge block %d not available", which); return HPS_ERR_ARG; }
-  HPSB_CUDA(cudaDeviceSynchronize());
-  HPSB_CUDA(cudaMemcpy2D(host, cols * 8, src, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost));
-  return HPS_OK;
+    HPSB_CUDA(cudaDeviceSynchronize());
+    HPSB_CUDA(cudaMemcpy(host, lo.T + (size_t)nn * lv.n12 * lv.n12, (size_t)lv.n12 * lv.n12 * 8,
+                         cudaMemcpyDeviceToHost));
+    return HPS_OK;
+  }
+  set_error("merge block %d not available", which);
+  return HPS_ERR_ARG;
 }
 
 size_t hps_solve_workspace_bytes(const hps_plan* h, int k) { return h ? workspace_bytes(h->P, k) : 0; }

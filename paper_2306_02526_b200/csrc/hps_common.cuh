@@ -58,5 +58,7 @@ struct GemmArgs {
   int batch;
 };
 int gemm(const GemmArgs& g, cudaStream_t st);
+// A * Bt^T on the FP64 tensor pipe when aligned (mma_gemm.cu), else gemm()
+int gemm_nt(const GemmArgs& g, cudaStream_t st);
 
 }  // namespace hpsb

@@ -1,6 +1,7 @@
 // Internal plan / operator-set structures (device-resident, level-contiguous).
 #pragma once
 
+#include <algorithm>
 #include <vector>
 
 #include "hps_common.cuh"
@@ -37,11 +38,41 @@ struct Plan {
   int ldb = 0;                    // even-padded nb
 };
 
+// Streaming layout of one operator family of a level ("panel"): the level's
+// c matrices (R x C each) are stacked into a row space of c*R rows (node-major),
+// cut into tiles of TR consecutive rows, and every tile is stored column-major
+// ([C][TR], rows zero-padded).  A CTA streams one tile (or a column chunk of
+// it) as one contiguous run; each thread owns two adjacent rows (16-byte
+// loads), so no cross-lane reduction is needed and every output is a
+// sequential sum (bitwise reproducible).
+constexpr int kPanelRows = 512;
+
+struct Panel {
+  double* base = nullptr;
+  int c = 0, R = 0, C = 0;
+  int TR = kPanelRows;
+  int ntiles = 0;
+  size_t doubles() const { return (size_t)ntiles * C * TR; }
+};
+Panel make_panel(int c, int R, int C);
+
+// launch-time split of a panel for k right-hand sides (split-K over columns)
+struct PanelSplit {
+  int KM = 1, kgroups = 1;  // rhs per pass, passes
+  int nsplit = 1, CK = 0;   // column chunks
+  int nodes = 1;            // max nodes touched by one tile
+  int XS = 1;               // staged x row stride (odd)
+  size_t smem = 0;
+  size_t part_doubles = 0;  // split-K partials
+  int counters = 0;         // split-K semaphores
+};
+PanelSplit panel_split(const Panel& pn, int k);
+
 struct LevelOps {
-  double* Xinv = nullptr;  // c x n3 x ld3
-  double* Tst = nullptr;   // c x n12 x ld3
-  double* S = nullptr;     // c x n3 x ld12
-  double* T = nullptr;     // c x n12 x n12 (only when keep_dtn)
+  Panel Xinv;              // n3 x n3 per node
+  Panel Tst;               // n12 x n3
+  Panel S;                 // n3 x n12
+  double* T = nullptr;     // c x n12 x n12 row-major (only when keep_dtn)
 };
 
 struct Ops {
@@ -49,8 +80,9 @@ struct Ops {
   double sigma = 0.0, dtg = 0.0;
   int shared_leaf = 1;         // constant coefficients: one leaf operator set
   int Lc = 1;                  // number of stored leaf operator sets (1 or L)
-  double* Ainv = nullptr;      // Lc x ni x ldi
-  double* S_leaf = nullptr;    // Lc x ni x ldb
+  double* Ainv = nullptr;      // shared leaf: [Ainv; D_bi Ainv], (ni+nb) x ldi row-major (GEMM operand)
+  double* S_leaf = nullptr;    // shared leaf: ni x ldb row-major
+  Panel pAinv, pSleaf;         // per-leaf operators (variable coefficients)
   double* T_leaf = nullptr;    // Lc x nb x nb (kept only when keep_dtn)
   double* D_bi = nullptr;      // nb x ni (shared stencil rows)
   std::vector<LevelOps> lo;    // depth entries, root first
@@ -59,13 +91,18 @@ struct Ops {
   std::vector<void*> allocs;
 };
 
+int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st);
+int unpack_panel(const Panel& pn, int node, double* dst, cudaStream_t st);  // dst R x C row-major
+
 // per-solve workspace carve-up (per-rhs strides in doubles)
 struct Workspace {
-  double* W = nullptr;      // k x L x ni
+  double* W = nullptr;      // k x L x (ni+nb): [w | h] rows (shared leaf) or w (ld ni)
   double* Hleaf = nullptr;  // k x L x nb
   double* Ub = nullptr;     // k x L x nb
   std::vector<double*> H;   // per level d (d>=1): k x c x n12
   std::vector<double*> W3;  // per level: k x c x n3
+  double* part = nullptr;   // split-K partials
+  unsigned* cnt = nullptr;  // split-K semaphores (zero between launches)
 };
 size_t workspace_bytes(const Plan& P, int k);
 void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
@@ -75,12 +112,9 @@ enum GemvMode { GEMV_UPX = 0, GEMV_UPT = 1, GEMV_DOWN = 2, GEMV_LEAF = 3 };
 
 struct GemvArgs {
   int mode;
-  int c;                        // number of matrices (nodes / leaves)
-  int R, C, ldm;                // rows, columns, padded row length (even)
-  const double* M; long long sM;
   int k;                        // right-hand sides
   // UPX / UPT
-  const double* Hc; int nbc; long long Hc_k;
+  const double* Hc; int nbc; long long Hc_k, Hc_s;  // child fluxes: per-child stride Hc_s
   double* Hout; int n12; long long Hout_k;
   double* W3; int n3; long long W3_k;
   const int *i1a, *i3a, *i2b, *i3b; int n1a;
@@ -91,8 +125,10 @@ struct GemvArgs {
   const double* xin; long long xin_k, xin_s;
   double* yout; long long yout_k, yout_s;
   const double* yadd; long long yadd_k, yadd_s;
+  // split-K scratch
+  double* part; unsigned* cnt;
 };
-int gemv_level(const GemvArgs& a, cudaStream_t st);
+int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st);
 
 // solve entry (solve.cu)
 int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,

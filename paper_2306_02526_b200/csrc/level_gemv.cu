@@ -6,26 +6,74 @@
 //   DOWN: u[j3] = S u[gidx_bnd] (+ w3)                          (solver.py:261-268)
 //   LEAF: y    = M x (+ add)   per leaf (variable-coefficient leaves,
 //                               solver.py:225-227 and 269-272)
-// Operators are stored node-contiguous, row-major, rows padded to an even
-// length, so each node's matrix is one contiguous HBM stream read once per
-// solve with 16-byte streaming loads (ld.global.cs).  The gathered input
-// vector of each node is staged in shared memory (column chunks), groups of
-// G lanes own rows and reduce with xor-shuffles, and the mode-specific
-// gather / scatter is fused into the prologue / epilogue.
+//
+// Operators live in the "panel" layout (hps_plan.cuh): the level's row space
+// (c nodes x R rows) is cut into 512-row tiles stored column-major.  CTA =
+// one tile x one column chunk: it stages the chunk of every touched node's
+// input vector in shared memory (mode-specific gather fused in), then each
+// of its 256 threads owns two adjacent rows and walks the columns issuing U
+// independent 16-byte streaming loads (ld.global.cs) before consuming them,
+// so every CTA keeps U*4 KB of one contiguous HBM region in flight.
+// Outputs are plain sequential sums.  When a level has too few tiles to fill
+// the machine (top levels: 1-64 huge nodes) the columns are split across
+// CTAs; partial sums go to the workspace and the last CTA of a tile (counted
+// with a semaphore, reset for the next launch) adds them in chunk order, so
+// results stay bitwise reproducible.
 #include "hps_plan.cuh"
 
 namespace hpsb {
 
+// Tile height: 512 rows (256 threads) unless that leaves too few tiles to
+// fill the machine, then 256 or 128 rows (smaller CTAs, more of them
+// resident per SM, which overlaps one CTA's gather with another's stream).
+Panel make_panel(int c, int R, int C) {
+  Panel p;
+  p.c = c; p.R = R; p.C = C;
+  const long long rows = (long long)c * R;
+  p.TR = kPanelRows;
+  while (p.TR > 128 && cdiv(rows, p.TR) < 4LL * kNumSMs) p.TR /= 2;
+  p.ntiles = (int)cdiv(rows, p.TR);
+  return p;
+}
+
 namespace {
 
 constexpr int NT = 256;
-constexpr int MAXS = 4;  // rows per lane-group per block
+constexpr int kTargetThreads = kNumSMs * 1536;
+constexpr size_t kMaxStage = 64 * 1024;
+
+}  // namespace
+
+PanelSplit panel_split(const Panel& pn, int k) {
+  PanelSplit s;
+  s.KM = k == 1 ? 1 : 4;
+  s.kgroups = (int)cdiv(k, s.KM);
+  s.nodes = (int)std::min<long long>(pn.c, (pn.TR - 1) / pn.R + 2);
+  long long base = (long long)pn.ntiles * s.kgroups;
+  int ns = (int)std::max<long long>(1, cdiv(kTargetThreads / (pn.TR / 2), base));
+  ns = std::min(ns, std::max(1, pn.C / 16));
+  int CK = (int)cdiv(pn.C, ns);
+  auto xs = [](int ck) { return ck | 1; };
+  long long cap = (long long)(kMaxStage / 8) / ((long long)s.nodes * s.KM);
+  if (xs(CK) > cap) CK = (int)std::max<long long>(1, (cap - 1) & ~1LL);
+  s.CK = CK;
+  s.nsplit = (int)cdiv(pn.C, CK);
+  s.XS = xs(CK);
+  s.smem = (size_t)s.nodes * s.KM * s.XS * 8;
+  if (s.nsplit > 1) {
+    s.part_doubles = (size_t)s.kgroups * s.KM * s.nsplit * pn.ntiles * pn.TR;
+    s.counters = pn.ntiles * s.kgroups;
+  }
+  return s;
+}
+
+namespace {
 
 template <int MODE>
 __device__ __forceinline__ double xval(const GemvArgs& a, int node, int kg, int col) {
   if (MODE == GEMV_UPX) {
-    const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.nbc;
-    const double* Hb = Ha + a.nbc;
+    const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
+    const double* Hb = Ha + a.Hc_s;
     double v = Hb[a.i3b[col]] - Ha[a.i3a[col]];
     if (a.jump) v = v - a.inv_dt * a.jump[kg * a.jump_k + a.j3[(long long)node * a.n3 + col]];
     return v;
@@ -43,8 +91,8 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int node, int r, int
   if (MODE == GEMV_UPX) {
     a.W3[kg * a.W3_k + (long long)node * a.n3 + r] = y;
   } else if (MODE == GEMV_UPT) {
-    const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.nbc;
-    const double* Hb = Ha + a.nbc;
+    const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
+    const double* Hb = Ha + a.Hc_s;
     double base = (r < a.n1a) ? Ha[a.i1a[r]] : Hb[a.i2b[r - a.n1a]];
     a.Hout[kg * a.Hout_k + (long long)node * a.n12 + r] = base + y;
   } else if (MODE == GEMV_DOWN) {
@@ -58,173 +106,181 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int node, int r, int
   }
 }
 
-template <int MODE, int G, int KM>
-__global__ void __launch_bounds__(NT) k_gemv(GemvArgs a, int npb, int rpb, int CH) {
+template <int MODE, int KM, int U>
+__global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit sp) {
   extern __shared__ double xs[];
+  __shared__ unsigned s_last;
   const int tid = threadIdx.x;
-  const int gl = tid & (G - 1);
-  const int grp = tid / G;
-  constexpr int NGRP = NT / G;
-  const int k0 = blockIdx.y * KM;
+  const int tile = blockIdx.x / sp.nsplit, split = blockIdx.x % sp.nsplit;
+  const int kg0 = blockIdx.y * KM;
+  const int R = pn.R, TR = pn.TR;
+  const long long P = (long long)pn.c * R;
+  const long long p0 = (long long)tile * TR;
+  const int n0 = (int)(p0 / R);
+  const int nn = (int)((std::min(P, p0 + TR) - 1) / R) - n0 + 1;
+  const int c0 = split * sp.CK, cw = min(sp.CK, pn.C - c0);
+  const int XS = sp.XS;
 
-  int node0, rbeg, rend;
-  if (npb > 1 || rpb >= a.R) {
-    node0 = blockIdx.x * npb; rbeg = 0; rend = a.R;
-  } else {
-    int splits = (a.R + rpb - 1) / rpb;
-    node0 = blockIdx.x / splits;
-    rbeg = (blockIdx.x % splits) * rpb;
-    rend = min(a.R, rbeg + rpb);
+  const long long pa = p0 + 2 * tid;
+  const int cs = TR / 2;
+  const double2* M = reinterpret_cast<const double2*>(pn.base + (size_t)tile * pn.C * TR + (size_t)c0 * TR) + tid;
+  // the first batch of the operator stream does not depend on x: issue it
+  // before the gather so the two latencies overlap
+  double2 m[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) m[u] = u < cw ? __ldcs(M + (size_t)u * cs) : make_double2(0.0, 0.0);
+
+  // stage x chunks of the touched nodes: xs[(node*KM + kk)*XS + col]
+  for (int e = tid; e < nn * KM * cw; e += blockDim.x) {
+    const int col = e % cw, t2 = e / cw, kk = t2 % KM, nl = t2 / KM, kg = kg0 + kk;
+    xs[(nl * KM + kk) * XS + col] = kg < a.k ? xval<MODE>(a, n0 + nl, kg, c0 + col) : 0.0;
   }
-  const int nn = min(npb, a.c - node0);
-  const int rpn = rend - rbeg;
-  const int nrows = nn * rpn;
+  __syncthreads();
 
-  // per-slot row pointers and shared-memory x offsets (x chunk laid out [node][k][col])
-  const double* mp[MAXS];
-  int xnode[MAXS];
-  bool live[MAXS];
-#pragma unroll
-  for (int i = 0; i < MAXS; ++i) {
-    int s = grp + i * NGRP;
-    live[i] = s < nrows;
-    int nl = live[i] ? s / rpn : 0;
-    int r = live[i] ? rbeg + s % rpn : 0;
-    xnode[i] = nl;
-    mp[i] = a.M + (long long)(node0 + nl) * a.sM + (long long)r * a.ldm;
-  }
+  const int na = (int)(std::min(pa, P - 1) / R) - n0;
+  const int nb = (int)(std::min(pa + 1, P - 1) / R) - n0;
+  const double* xa = xs + na * KM * XS;
+  const double* xb = xs + nb * KM * XS;
 
-  double acc[MAXS][KM];
+  double acc0[KM], acc1[KM];
 #pragma unroll
-  for (int i = 0; i < MAXS; ++i)
+  for (int kk = 0; kk < KM; ++kk) { acc0[kk] = 0.0; acc1[kk] = 0.0; }
+  for (int col = 0; col < cw; col += U) {
+    // software pipeline: next batch in flight while this one is consumed
+    double2 nx[U];
 #pragma unroll
-    for (int kk = 0; kk < KM; ++kk) acc[i][kk] = 0.0;
-
-  for (int c0 = 0; c0 < a.C; c0 += CH) {
-    const int cw = min(CH, a.C - c0);
-    const int cwp = (cw + 1) & ~1;
-    if (c0 > 0) __syncthreads();
-    for (int e = tid; e < nn * KM * cwp; e += NT) {
-      int j = e % cwp;
-      int t2 = e / cwp;
-      int kk = t2 % KM, nl = t2 / KM;
-      int kg = k0 + kk, col = c0 + j;
-      double v = 0.0;
-      if (kg < a.k && col < a.C) v = xval<MODE>(a, node0 + nl, kg, col);
-      xs[(nl * KM + kk) * cwp + j] = v;
-    }
-    __syncthreads();
-    const int n2 = cwp >> 1;
-#pragma unroll 2
-    for (int j2 = gl; j2 < n2; j2 += G) {
-      double2 m[MAXS];
+    for (int u = 0; u < U; ++u)
+      nx[u] = col + U + u < cw ? __ldcs(M + (size_t)(col + U + u) * cs) : make_double2(0.0, 0.0);
 #pragma unroll
-      for (int i = 0; i < MAXS; ++i)
-        if (live[i]) m[i] = __ldcs(reinterpret_cast<const double2*>(mp[i] + c0) + j2);
-#pragma unroll
-      for (int i = 0; i < MAXS; ++i) {
-        if (!live[i]) continue;
+    for (int u = 0; u < U; ++u) {
+      if (col + u < cw) {
 #pragma unroll
         for (int kk = 0; kk < KM; ++kk) {
-          const double2 x = *reinterpret_cast<const double2*>(xs + (xnode[i] * KM + kk) * cwp + 2 * j2);
-          acc[i][kk] = fma(m[i].x, x.x, acc[i][kk]);
-          acc[i][kk] = fma(m[i].y, x.y, acc[i][kk]);
+          acc0[kk] = fma(m[u].x, xa[kk * XS + col + u], acc0[kk]);
+          acc1[kk] = fma(m[u].y, xb[kk * XS + col + u], acc1[kk]);
         }
       }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) m[u] = nx[u];
   }
 
-#pragma unroll
-  for (int i = 0; i < MAXS; ++i) {
+  if (sp.nsplit > 1) {
+    const long long Pp = (long long)pn.ntiles * TR;
+    double* part = a.part + ((long long)blockIdx.y * KM * sp.nsplit) * Pp;
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) {
-      double v = acc[i][kk];
-#pragma unroll
-      for (int off = G / 2; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off, G);
-      acc[i][kk] = v;
+      double2 v = make_double2(acc0[kk], acc1[kk]);
+      *reinterpret_cast<double2*>(part + ((long long)kk * sp.nsplit + split) * Pp + pa) = v;
     }
-  }
-  if (gl == 0) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      unsigned old = atomicAdd(a.cnt + (size_t)tile * gridDim.y + blockIdx.y, 1u);
+      s_last = (old == (unsigned)sp.nsplit - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i) {
-      if (!live[i]) continue;
-      int s = grp + i * NGRP;
-      int nl = s / rpn, r = rbeg + s % rpn;
-#pragma unroll
-      for (int kk = 0; kk < KM; ++kk) {
-        int kg = k0 + kk;
-        if (kg < a.k) epilogue<MODE>(a, node0 + nl, r, kg, acc[i][kk]);
+    for (int kk = 0; kk < KM; ++kk) {
+      double s0 = 0.0, s1 = 0.0;
+      for (int s = 0; s < sp.nsplit; ++s) {
+        double2 v = __ldcg(reinterpret_cast<const double2*>(part + ((long long)kk * sp.nsplit + s) * Pp + pa));
+        s0 += v.x;
+        s1 += v.y;
       }
+      acc0[kk] = s0;
+      acc1[kk] = s1;
     }
+    if (tid == 0) a.cnt[(size_t)tile * gridDim.y + blockIdx.y] = 0u;
+  }
+#pragma unroll
+  for (int kk = 0; kk < KM; ++kk) {
+    const int kg = kg0 + kk;
+    if (kg >= a.k) continue;
+    if (pa < P) epilogue<MODE>(a, n0 + na, (int)(pa - (long long)(n0 + na) * R), kg, acc0[kk]);
+    if (pa + 1 < P) epilogue<MODE>(a, n0 + nb, (int)(pa + 1 - (long long)(n0 + nb) * R), kg, acc1[kk]);
   }
 }
 
-template <int MODE, int G, int KM>
-int launch(const GemvArgs& a, int npb, int rpb, int CH, unsigned blocks, cudaStream_t st) {
-  int cwp = (CH + 1) & ~1;
-  size_t smem = (size_t)npb * KM * cwp * sizeof(double);
+template <int MODE, int KM, int U>
+int launch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_gemv<MODE, G, KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaFuncSetAttribute(k_panel<MODE, KM, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxStage);
     attr_set = true;
   }
-  dim3 grid(blocks, (unsigned)((a.k + KM - 1) / KM));
-  k_gemv<MODE, G, KM><<<grid, NT, smem, st>>>(a, npb, rpb, CH);
+  dim3 grid((unsigned)((long long)pn.ntiles * sp.nsplit), (unsigned)sp.kgroups);
+  k_panel<MODE, KM, U><<<grid, pn.TR / 2, sp.smem, st>>>(a, pn, sp);
   HPSB_LAUNCH_CHECK();
   return 0;
 }
 
 template <int MODE>
-int dispatch(const GemvArgs& a, int G, int KM, int npb, int rpb, int CH, unsigned blocks,
-             cudaStream_t st) {
-#define HPSB_G(GG)                                                                   \
-  if (G == GG) {                                                                     \
-    if (KM == 1) return launch<MODE, GG, 1>(a, npb, rpb, CH, blocks, st);            \
-    return launch<MODE, GG, 4>(a, npb, rpb, CH, blocks, st);                         \
+int dispatch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_t st) {
+  if (sp.KM == 1) return launch<MODE, 1, 8>(a, pn, sp, st);
+  return launch<MODE, 4, 4>(a, pn, sp, st);
+}
+
+__global__ void k_pack(const double* __restrict__ src, long long s_node, int ld, Panel pn) {
+  const long long total = (long long)pn.ntiles * pn.C * pn.TR;
+  const long long P = (long long)pn.c * pn.R;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long tile = e / ((long long)pn.C * pn.TR);
+    const long long rem = e % ((long long)pn.C * pn.TR);
+    const int col = (int)(rem / pn.TR), r = (int)(rem % pn.TR);
+    const long long p = tile * pn.TR + r;
+    double v = 0.0;
+    if (p < P) v = src[(p / pn.R) * s_node + (p % pn.R) * (long long)ld + col];
+    pn.base[e] = v;
   }
-  HPSB_G(8) HPSB_G(16) HPSB_G(32)
-#undef HPSB_G
-  set_error("gemv: bad group size %d", G);
-  return -1;
+}
+
+__global__ void k_unpack(Panel pn, int node, double* __restrict__ dst) {
+  const long long n = (long long)pn.R * pn.C;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e / pn.C), col = (int)(e % pn.C);
+    const long long p = (long long)node * pn.R + row;
+    dst[e] = pn.base[(p / pn.TR) * pn.C * pn.TR + (long long)col * pn.TR + p % pn.TR];
+  }
 }
 
 }  // namespace
 
-int gemv_level(const GemvArgs& a, cudaStream_t st) {
-  if (a.c <= 0 || a.R <= 0 || a.k <= 0) return 0;
-  // lane-group size: enough lanes to cover a row with 16-byte loads
-  int half = (a.C + 1) / 2;
-  int G = 32;
-  if (half <= 8) G = 8; else if (half <= 16) G = 16;
-  const int ngrp = NT / G;
-  const int KM = a.k == 1 ? 1 : 4;
-  const int max_rows = ngrp * MAXS;
-  const int target_blocks = 4 * kNumSMs;
-  int npb = 1, rpb = a.R;
-  if (a.R <= max_rows) {
-    npb = max_rows / a.R;
-    int cap = a.c / target_blocks;
-    if (cap < 1) cap = 1;
-    if (npb > cap) npb = cap;
-    if (npb < 1) npb = 1;
-  } else {
-    rpb = max_rows;
-    while (rpb > ngrp && (long long)a.c * ((a.R + rpb - 1) / rpb) < target_blocks) rpb /= 2;
+int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
+  if (pn.c <= 0 || pn.R <= 0 || a.k <= 0) return 0;
+  const PanelSplit sp = panel_split(pn, a.k);
+  if (sp.nsplit > 1 && (!a.part || !a.cnt)) {
+    set_error("gemv: split-K needs workspace");
+    return -1;
   }
-  // column chunk so the staged x (npb nodes x KM rhs) fits in ~48 KB
-  long long cap_cols = (48 * 1024 / 8) / ((long long)npb * KM);
-  int CH = (int)(cap_cols & ~1LL);
-  if (CH >= a.C) CH = (a.C + 1) & ~1;
-  if (CH < 2) { set_error("gemv: chunk too small"); return -1; }
-  unsigned blocks;
-  if (npb > 1 || rpb >= a.R) blocks = (unsigned)((a.c + npb - 1) / npb);
-  else blocks = (unsigned)((long long)a.c * ((a.R + rpb - 1) / rpb));
   switch (a.mode) {
-    case GEMV_UPX: return dispatch<GEMV_UPX>(a, G, KM, npb, rpb, CH, blocks, st);
-    case GEMV_UPT: return dispatch<GEMV_UPT>(a, G, KM, npb, rpb, CH, blocks, st);
-    case GEMV_DOWN: return dispatch<GEMV_DOWN>(a, G, KM, npb, rpb, CH, blocks, st);
-    default: return dispatch<GEMV_LEAF>(a, G, KM, npb, rpb, CH, blocks, st);
+    case GEMV_UPX: return dispatch<GEMV_UPX>(a, pn, sp, st);
+    case GEMV_UPT: return dispatch<GEMV_UPT>(a, pn, sp, st);
+    case GEMV_DOWN: return dispatch<GEMV_DOWN>(a, pn, sp, st);
+    default: return dispatch<GEMV_LEAF>(a, pn, sp, st);
   }
+}
+
+int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st) {
+  long long total = (long long)pn.ntiles * pn.C * pn.TR;
+  if (total <= 0) return 0;
+  unsigned blocks = (unsigned)std::min<long long>(cdiv(total, 256), (long long)kNumSMs * 32);
+  k_pack<<<blocks, 256, 0, st>>>(src, s_node, ld, pn);
+  HPSB_LAUNCH_CHECK();
+  return 0;
+}
+
+int unpack_panel(const Panel& pn, int node, double* dst, cudaStream_t st) {
+  long long n = (long long)pn.R * pn.C;
+  if (n <= 0) return 0;
+  unsigned blocks = (unsigned)std::min<long long>(cdiv(n, 256), (long long)kNumSMs * 8);
+  k_unpack<<<blocks, 256, 0, st>>>(pn, node, dst);
+  HPSB_LAUNCH_CHECK();
+  return 0;
 }
 
 }  // namespace hpsb

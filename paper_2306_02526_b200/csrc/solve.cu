@@ -28,16 +28,43 @@ __global__ void k_leaf_gather(int k, int L, int nb, const int* __restrict__ lbg,
 
 }  // namespace
 
+// every panel a solve may launch, for sizing the split-K scratch
+static void solve_panels(const Plan& P, std::vector<Panel>& out) {
+  out.clear();
+  out.push_back(make_panel(P.L, P.ni, P.ni));
+  out.push_back(make_panel(P.L, P.ni, P.nb));
+  for (const Level& lv : P.lv) {
+    out.push_back(make_panel(lv.c, lv.n3, lv.n3));
+    out.push_back(make_panel(lv.c, lv.n12, lv.n3));
+    out.push_back(make_panel(lv.c, lv.n3, lv.n12));
+  }
+}
+
+static void scratch_sizes(const Plan& P, int k, size_t& part, size_t& cnt) {
+  std::vector<Panel> pns;
+  solve_panels(P, pns);
+  part = 0; cnt = 0;
+  for (const Panel& pn : pns) {
+    PanelSplit sp = panel_split(pn, k);
+    part = std::max(part, sp.part_doubles);
+    cnt = std::max(cnt, (size_t)sp.counters);
+  }
+}
+
 size_t workspace_bytes(const Plan& P, int k) {
   size_t n = 0;
   auto add = [&](long long cnt) { n += ((size_t)cnt * k * 8 + 255) & ~(size_t)255; };
-  add((long long)P.L * P.ni);
+  add((long long)P.L * (P.ni + P.nb));
   add((long long)P.L * P.nb);
   add((long long)P.L * P.nb);
   for (int d = 0; d < P.depth; ++d) {
     if (d >= 1) add((long long)P.lv[d].c * P.lv[d].n12);
     add((long long)P.lv[d].c * P.lv[d].n3);
   }
+  size_t part, cnt;
+  scratch_sizes(P, k, part, cnt);
+  n += (part * 8 + 255) & ~(size_t)255;
+  n += (cnt * 4 + 255) & ~(size_t)255;
   return n + 256;
 }
 
@@ -48,7 +75,7 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
     p += ((size_t)cnt * k * 8 + 255) & ~(size_t)255;
     return r;
   };
-  ws.W = take((long long)P.L * P.ni);
+  ws.W = take((long long)P.L * (P.ni + P.nb));
   ws.Hleaf = take((long long)P.L * P.nb);
   ws.Ub = take((long long)P.L * P.nb);
   ws.H.assign(P.depth, nullptr);
@@ -57,6 +84,11 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
     if (d >= 1) ws.H[d] = take((long long)P.lv[d].c * P.lv[d].n12);
     ws.W3[d] = take((long long)P.lv[d].c * P.lv[d].n3);
   }
+  size_t part, cnt;
+  scratch_sizes(P, k, part, cnt);
+  ws.part = (double*)p;
+  p += (part * 8 + 255) & ~(size_t)255;
+  ws.cnt = (unsigned*)p;  // zeroed by the caller when the workspace is created
 }
 
 int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
@@ -83,31 +115,36 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
   }
 
   const bool up = (g != nullptr) || (jump != nullptr);
+  const int nw = P.ni + P.nb;
+  // leaf outputs: W (row stride ldw, rhs stride sw) and H (child stride hs, rhs stride sh)
+  long long ldw = P.ni, sw = Lni, hs = P.nb, sh = Lnb;
+  const double* Hleaf = ws.Hleaf;
   // (2) leaf particular solutions and their fluxes (solver.py:219-230)
   if (g) {
     if (ops.shared_leaf) {
-      // W^T (L x ni) = G_int^T (L x ni) * Ainv^T, one GEMM per rhs
+      // [W | H] (L x (ni+nb)) = G_int (L x ni) * [Ainv; D_bi Ainv]^T, one GEMM per rhs
       GemmArgs a{};
-      a.M = P.L; a.N = P.ni; a.K = P.ni; a.alpha = 1.0; a.beta = 0.0;
+      a.M = P.L; a.N = nw; a.K = P.ni; a.alpha = 1.0; a.beta = 0.0;
       a.A = g; a.lda = P.ni; a.sA = ld_g; a.tA = 0;
       a.B = ops.Ainv; a.ldb = P.ldi; a.sB = 0; a.tB = 1;
-      a.C = ws.W; a.ldc = P.ni; a.sC = Lni; a.batch = k;
-      if (int rc = gemm(a, st)) return rc;
+      a.C = ws.W; a.ldc = nw; a.sC = (long long)P.L * nw; a.batch = k;
+      if (int rc = gemm_nt(a, st)) return rc;
+      ldw = nw; sw = (long long)P.L * nw; hs = nw; sh = sw;
+      Hleaf = ws.W + P.ni;
     } else {
       GemvArgs a{};
-      a.mode = GEMV_LEAF; a.c = P.L; a.R = P.ni; a.C = P.ni; a.ldm = P.ldi;
-      a.M = ops.Ainv; a.sM = (long long)P.ni * P.ldi; a.k = k;
+      a.mode = GEMV_LEAF; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
       a.xin = g; a.xin_k = ld_g; a.xin_s = P.ni;
       a.yout = ws.W; a.yout_k = Lni; a.yout_s = P.ni;
-      if (int rc = gemv_level(a, st)) return rc;
+      if (int rc = gemv_level(a, ops.pAinv, st)) return rc;
+      // H (k*L x nb) = W (k*L x ni) * D_bi^T
+      GemmArgs h{};
+      h.M = k * P.L; h.N = P.nb; h.K = P.ni; h.alpha = 1.0; h.beta = 0.0;
+      h.A = ws.W; h.lda = P.ni; h.sA = 0; h.tA = 0;
+      h.B = ops.D_bi; h.ldb = P.ni; h.sB = 0; h.tB = 1;
+      h.C = ws.Hleaf; h.ldc = P.nb; h.sC = 0; h.batch = 1;
+      if (int rc = gemm_nt(h, st)) return rc;
     }
-    // H^T (k*L x nb) = W (k*L x ni) * D_bi^T
-    GemmArgs h{};
-    h.M = k * P.L; h.N = P.nb; h.K = P.ni; h.alpha = 1.0; h.beta = 0.0;
-    h.A = ws.W; h.lda = P.ni; h.sA = 0; h.tA = 0;
-    h.B = ops.D_bi; h.ldb = P.ni; h.sB = 0; h.tB = 1;
-    h.C = ws.Hleaf; h.ldc = P.nb; h.sC = 0; h.batch = 1;
-    if (int rc = gemm(h, st)) return rc;
   } else if (jump) {
     HPSB_CUDA(cudaMemsetAsync(ws.Hleaf, 0, (size_t)k * Lnb * 8, st));
   }
@@ -117,23 +154,22 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
     for (int d = P.depth - 1; d >= 0; --d) {
       const Level& lv = P.lv[d];
       const LevelOps& lo = ops.lo[d];
-      const double* Hc = (d == P.depth - 1) ? ws.Hleaf : ws.H[d + 1];
-      long long Hc_k = (d == P.depth - 1) ? Lnb : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
+      const bool leafc = d == P.depth - 1;
       GemvArgs a{};
-      a.c = lv.c; a.k = k;
-      a.Hc = Hc; a.nbc = lv.nbc; a.Hc_k = Hc_k;
+      a.k = k; a.part = ws.part; a.cnt = ws.cnt;
+      a.Hc = leafc ? Hleaf : ws.H[d + 1]; a.nbc = lv.nbc;
+      a.Hc_k = leafc ? sh : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
+      a.Hc_s = leafc ? hs : lv.nbc;
       a.W3 = ws.W3[d]; a.n3 = lv.n3; a.W3_k = (long long)lv.c * lv.n3;
       a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
       a.n12 = lv.n12;
       a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt; a.j3 = lv.j3;
-      a.mode = GEMV_UPX; a.R = lv.n3; a.C = lv.n3; a.ldm = lv.ld3;
-      a.M = lo.Xinv; a.sM = (long long)lv.n3 * lv.ld3;
-      if (int rc = gemv_level(a, st)) return rc;
+      a.mode = GEMV_UPX;
+      if (int rc = gemv_level(a, lo.Xinv, st)) return rc;
       if (d == 0) break;  // the root's outer flux is never consumed
-      a.mode = GEMV_UPT; a.R = lv.n12; a.C = lv.n3; a.ldm = lv.ld3;
-      a.M = lo.Tst; a.sM = (long long)lv.n12 * lv.ld3;
+      a.mode = GEMV_UPT;
       a.Hout = ws.H[d]; a.Hout_k = (long long)lv.c * lv.n12;
-      if (int rc = gemv_level(a, st)) return rc;
+      if (int rc = gemv_level(a, lo.Tst, st)) return rc;
     }
   }
 
@@ -142,13 +178,11 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
     const Level& lv = P.lv[d];
     const LevelOps& lo = ops.lo[d];
     GemvArgs a{};
-    a.mode = GEMV_DOWN; a.c = lv.c; a.k = k;
-    a.R = lv.n3; a.C = lv.n12; a.ldm = lv.ld12;
-    a.M = lo.S; a.sM = (long long)lv.n3 * lv.ld12;
+    a.mode = GEMV_DOWN; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
     a.u = u; a.u_k = ld_u; a.gidx = lv.gidx_bnd; a.j3 = lv.j3;
     a.n3 = lv.n3; a.n12 = lv.n12;
     a.W3 = up ? ws.W3[d] : nullptr; a.W3_k = (long long)lv.c * lv.n3;
-    if (int rc = gemv_level(a, st)) return rc;
+    if (int rc = gemv_level(a, lo.S, st)) return rc;
   }
 
   // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
@@ -161,17 +195,16 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
       a.M = P.L; a.N = P.ni; a.K = P.nb; a.alpha = 1.0;
       a.A = ws.Ub; a.lda = P.nb; a.sA = Lnb; a.tA = 0;
       a.B = ops.S_leaf; a.ldb = P.ldb; a.sB = 0; a.tB = 1;
-      a.beta = g ? 1.0 : 0.0; a.D = g ? ws.W : nullptr; a.ldd = P.ni; a.sD = Lni;
+      a.beta = g ? 1.0 : 0.0; a.D = g ? ws.W : nullptr; a.ldd = ldw; a.sD = sw;
       a.C = u; a.ldc = P.ni; a.sC = ld_u; a.batch = k;
-      if (int rc = gemm(a, st)) return rc;
+      if (int rc = gemm_nt(a, st)) return rc;
     } else {
       GemvArgs a{};
-      a.mode = GEMV_LEAF; a.c = P.L; a.R = P.ni; a.C = P.nb; a.ldm = P.ldb;
-      a.M = ops.S_leaf; a.sM = (long long)P.ni * P.ldb; a.k = k;
+      a.mode = GEMV_LEAF; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
       a.xin = ws.Ub; a.xin_k = Lnb; a.xin_s = P.nb;
       a.yout = u; a.yout_k = ld_u; a.yout_s = P.ni;
       a.yadd = g ? ws.W : nullptr; a.yadd_k = Lni; a.yadd_s = P.ni;
-      if (int rc = gemv_level(a, st)) return rc;
+      if (int rc = gemv_level(a, ops.pSleaf, st)) return rc;
     }
   }
   return 0;

@@ -67,14 +67,23 @@ __device__ __forceinline__ void gacc(double& g, double v) {
   g = (av > g || av != av) ? av : g;
 }
 
+// block-wide max |v| then one atomic per block, skipped when the running
+// maximum already covers it (thousands of blocks would otherwise serialise
+// on one address)
 __device__ __forceinline__ void guard_max(unsigned long long* slot, double v) {
+  __shared__ unsigned long long s_w[NT / 32];
   // |v| as an unsigned bit pattern orders like the value; NaN sorts above inf
   unsigned long long b = __double_as_longlong(fabs(v));
   for (int off = 16; off > 0; off >>= 1) {
     unsigned long long o = __shfl_xor_sync(0xffffffffu, b, off);
     b = o > b ? o : b;
   }
-  if ((threadIdx.x & 31) == 0 && b) atomicMax(slot, b);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = b;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) b = s_w[w] > b ? s_w[w] : b;
+    if (b && b > __ldcg(slot)) atomicMax(slot, b);
+  }
 }
 
 // local edge index e -> grid (xi, yi): east (xi = 0), north/south interleaved,
@@ -87,7 +96,10 @@ __device__ __forceinline__ void edge_xy(int e, int p, int q, int& xi, int& yi) {
 
 __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
   extern __shared__ double sm[];
-  const int p = a.p, q = a.q, pp = p * p, qq = q * q;
+  // row strides padded to odd lengths: lanes walking different rows of a
+  // matrix / grid at the same column hit different banks
+  const int p = a.p, q = a.q, PS = (p + 1) | 1, QS = (q + 1) | 1;
+  const int pp = p * PS, qq = q * QS;
   double* d1x = sm;
   double* d2x = d1x + pp;
   double* d1y = d2x + pp;
@@ -96,34 +108,42 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
   double* ex2 = ex1 + qq;
   double* ey1 = ex2 + qq;
   double* ey2 = ey1 + qq;
-  double* U = ey2 + qq;  // lpb x p x p
+  double* U = ey2 + qq;  // lpb x p x PS
   const int tid = threadIdx.x;
-  for (int e = tid; e < 4 * pp + 4 * qq; e += NT) sm[e] = a.mats[e];
+  for (int e = tid; e < 4 * p * p; e += NT) {
+    int mtx = e / (p * p), r = e % (p * p);
+    sm[mtx * pp + (r / p) * PS + r % p] = a.mats[e];
+  }
+  for (int e = tid; e < 4 * q * q; e += NT) {
+    int mtx = e / (q * q), r = e % (q * q);
+    ex1[mtx * qq + (r / q) * QS + r % q] = a.mats[4 * p * p + e];
+  }
   const int kk = blockIdx.y;
-  const int l0 = blockIdx.x * a.lpb;
-  const int nl = min(a.lpb, a.L - l0);
   const double* u = a.u + kk * a.ld_u;
   double gmax = 0.0;
+  const bool want_all = a.lu || a.ux || a.uy;
+  const int npts = want_all ? a.m : (a.lu_int ? a.ni : 0);
+  const long long ob = kk * a.ld_o;
+  // persistent over leaf groups: the stencil matrices are staged once per CTA
+  for (int l0 = blockIdx.x * a.lpb; l0 < a.L; l0 += gridDim.x * a.lpb) {
+  const int nl = min(a.lpb, a.L - l0);
+  __syncthreads();
   // interior: one contiguous run of nl*ni values
   for (int e = tid; e < nl * a.ni; e += NT) {
     int ll = e / a.ni, i = e % a.ni;
     double v = u[(long long)l0 * a.ni + e];
-    U[ll * pp + (i / q + 1) * p + (i % q + 1)] = v;
+    U[ll * pp + (i / q + 1) * PS + (i % q + 1)] = v;
     gacc(gmax, v);
   }
   for (int e = tid; e < nl * a.nb; e += NT) {
     int ll = e / a.nb, j = e % a.nb, xi, yi;
     edge_xy(j, p, q, xi, yi);
     double v = u[a.lbg[(long long)(l0 + ll) * a.nb + j]];
-    U[ll * pp + xi * p + yi] = v;
+    U[ll * pp + xi * PS + yi] = v;
     gacc(gmax, v);
   }
-  if (a.guard) guard_max(a.guard, gmax);
   __syncthreads();
 
-  const bool want_all = a.lu || a.ux || a.uy;
-  const int npts = want_all ? a.m : (a.lu_int ? a.ni : 0);
-  const long long ob = kk * a.ld_o;
   for (int e = tid; e < nl * npts; e += NT) {
     const int ll = e / npts, t = e % npts, l = l0 + ll;
     int xi, yi;
@@ -135,35 +155,35 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
     const bool horz = !inner && !vert;
     double ux = 0.0, uxx = 0.0, uy = 0.0, uyy = 0.0;
     if (horz) {  // tangential x on north/south edges: edge-local rows
-      const double* r1 = ex1 + (xi - 1) * q;
-      const double* r2 = ex2 + (xi - 1) * q;
+      const double* r1 = ex1 + (xi - 1) * QS;
+      const double* r2 = ex2 + (xi - 1) * QS;
       for (int s = 0; s < q; ++s) {
-        double v = G[(s + 1) * p + yi];
+        double v = G[(s + 1) * PS + yi];
         ux = fma(r1[s], v, ux);
         uxx = fma(r2[s], v, uxx);
       }
     } else {
-      const double* r1 = d1x + xi * p;
-      const double* r2 = d2x + xi * p;
+      const double* r1 = d1x + xi * PS;
+      const double* r2 = d2x + xi * PS;
       for (int s = 0; s < p; ++s) {
-        double v = G[s * p + yi];
+        double v = G[s * PS + yi];
         ux = fma(r1[s], v, ux);
         uxx = fma(r2[s], v, uxx);
       }
     }
     if (vert) {  // tangential y on east/west edges
-      const double* r1 = ey1 + (yi - 1) * q;
-      const double* r2 = ey2 + (yi - 1) * q;
+      const double* r1 = ey1 + (yi - 1) * QS;
+      const double* r2 = ey2 + (yi - 1) * QS;
       for (int s = 0; s < q; ++s) {
-        double v = G[xi * p + s + 1];
+        double v = G[xi * PS + s + 1];
         uy = fma(r1[s], v, uy);
         uyy = fma(r2[s], v, uyy);
       }
     } else {
-      const double* r1 = d1y + yi * p;
-      const double* r2 = d2y + yi * p;
+      const double* r1 = d1y + yi * PS;
+      const double* r2 = d2y + yi * PS;
       for (int s = 0; s < p; ++s) {
-        double v = G[xi * p + s];
+        double v = G[xi * PS + s];
         uy = fma(r1[s], v, uy);
         uyy = fma(r2[s], v, uyy);
       }
@@ -181,7 +201,7 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
       lop = __dadd_rn(lop, __dmul_rn(c22, uyy));
       if (a.has_c1) lop = __dsub_rn(lop, __dmul_rn(c1, ux));
       if (a.has_c2) lop = __dsub_rn(lop, __dmul_rn(c2, uy));
-      if (a.has_c) lop = __dsub_rn(lop, __dmul_rn(c0, G[xi * p + yi]));
+      if (a.has_c) lop = __dsub_rn(lop, __dmul_rn(c0, G[xi * PS + yi]));
     }
     if (inner) {
       const long long gi = (long long)l * a.ni + t;
@@ -209,15 +229,90 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
       const double* G = U + ll * pp;
       double v = 0.0;
       if (xi == 0 || xi == p - 1) {
-        const double* r = d1x + xi * p;
-        for (int s = 0; s < p; ++s) v = fma(r[s], G[s * p + yi], v);
+        const double* r = d1x + xi * PS;
+        for (int s = 0; s < p; ++s) v = fma(r[s], G[s * PS + yi], v);
       } else {
-        const double* r = d1y + yi * p;
-        for (int s = 0; s < p; ++s) v = fma(r[s], G[xi * p + s], v);
+        const double* r = d1y + yi * PS;
+        for (int s = 0; s < p; ++s) v = fma(r[s], G[xi * PS + s], v);
       }
       atomicAdd(a.jump + ob + a.lbg[(long long)l * a.nb + j], sg > 0 ? v : -v);
     }
   }
+  }  // leaf groups
+  if (a.guard) guard_max(a.guard, gmax);
+}
+
+// Interior-only L u (the stage history, timestep.py:253-261): thread <->
+// fixed interior point of the CTA's leaf slot, its derivative rows held in
+// registers across the persistent leaf loop, so the inner loops read only
+// the staged grid values from shared memory.
+template <int P, bool G1>
+__global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
+  extern __shared__ double U[];  // lpb x P x PS
+  constexpr int Q = P - 2, NI = Q * Q, PS = (P + 1) | 1, PP = P * PS;
+  const int tid = threadIdx.x, lpb = a.lpb;
+  const int kk = blockIdx.y;
+  const double* u = a.u + kk * a.ld_u;
+  const long long ob = kk * a.ld_o;
+  const bool active = tid < lpb * NI;
+  const int ll = tid / NI, t = tid % NI, xi = t / Q + 1, yi = t % Q + 1;
+  double rxx[P], ryy[P], rx[G1 ? P : 1], ry[G1 ? P : 1];
+  const double* mats = a.mats;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    if (G1) rx[s] = mats[xi * P + s];
+    rxx[s] = mats[P * P + xi * P + s];
+    if (G1) ry[s] = mats[2 * P * P + yi * P + s];
+    ryy[s] = mats[3 * P * P + yi * P + s];
+  }
+  double gmax = 0.0;
+  for (int l0 = blockIdx.x * lpb; l0 < a.L; l0 += gridDim.x * lpb) {
+    const int nl = min(lpb, a.L - l0);
+    __syncthreads();
+    for (int e = tid; e < nl * NI; e += NT) {
+      int l2 = e / NI, i = e % NI;
+      double v = u[(long long)l0 * NI + e];
+      U[l2 * PP + (i / Q + 1) * PS + (i % Q + 1)] = v;
+      gacc(gmax, v);
+    }
+    for (int e = tid; e < nl * 4 * Q; e += NT) {
+      int l2 = e / (4 * Q), j = e % (4 * Q), x, y;
+      edge_xy(j, P, Q, x, y);
+      double v = u[a.lbg[(long long)(l0 + l2) * 4 * Q + j]];
+      U[l2 * PP + x * PS + y] = v;
+      gacc(gmax, v);
+    }
+    __syncthreads();
+    if (!active || ll >= nl) continue;
+    const double* G = U + ll * PP;
+    double ux = 0.0, uxx = 0.0, uy = 0.0, uyy = 0.0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const double v = G[s * PS + yi];
+      uxx = fma(rxx[s], v, uxx);
+      if (G1) ux = fma(rx[G1 ? s : 0], v, ux);
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const double v = G[xi * PS + s];
+      uyy = fma(ryy[s], v, uyy);
+      if (G1) uy = fma(ry[G1 ? s : 0], v, uy);
+    }
+    const int l = l0 + ll;
+    double c11, c22, c1, c2, c0;
+    if (a.Lc == 1) { c11 = a.cc[0]; c22 = a.cc[1]; c1 = a.cc[2]; c2 = a.cc[3]; c0 = a.cc[4]; }
+    else {
+      const double* cv = a.coef + (long long)l * 5 * a.m;
+      c11 = cv[t]; c22 = cv[a.m + t]; c1 = cv[2 * a.m + t]; c2 = cv[3 * a.m + t]; c0 = cv[4 * a.m + t];
+    }
+    double lop = __dmul_rn(c11, uxx);
+    lop = __dadd_rn(lop, __dmul_rn(c22, uyy));
+    if (a.has_c1) lop = __dsub_rn(lop, __dmul_rn(c1, ux));
+    if (a.has_c2) lop = __dsub_rn(lop, __dmul_rn(c2, uy));
+    if (a.has_c) lop = __dsub_rn(lop, __dmul_rn(c0, G[xi * PS + yi]));
+    a.lu_int[ob + (long long)l * NI + t] = lop;
+  }
+  if (a.guard) guard_max(a.guard, gmax);
 }
 
 constexpr int MAXT = 24;
@@ -356,9 +451,28 @@ int hps_leaf_eval(const hps_disc* h, int k, const double* u, long long ld_u, dou
   a.has_c1 = D.has_c1; a.has_c2 = D.has_c2; a.has_c = D.has_c;
   a.lu_int = lu_int; a.lu = lu; a.ux = ux; a.uy = uy; a.jump = jump; a.ld_o = ld_o;
   a.guard = reinterpret_cast<unsigned long long*>(guard);
-  const int pp = D.p * D.p, qq = D.q * D.q;
+  const int PS = (D.p + 1) | 1, QS = (D.q + 1) | 1;
+  const int pp = D.p * PS, qq = D.q * QS;
+  unsigned groups = (unsigned)cdiv(P.L, a.lpb);
+  dim3 grid(std::min(groups, (unsigned)(kNumSMs * 8)), (unsigned)k);
+  const bool int_only = lu_int && !lu && !ux && !uy && !jump;
+  if (int_only && (D.p == 10 || D.p == 12 || D.p == 16)) {
+    a.lpb = std::max(1, NT / (D.ni));
+    groups = (unsigned)cdiv(P.L, a.lpb);
+    grid.x = std::min(groups, (unsigned)(kNumSMs * 8));
+    size_t sm2 = (size_t)a.lpb * pp * 8;
+    const bool g1 = D.has_c1 || D.has_c2;
+#define HPSB_LOP(PP)                                                        \
+    if (D.p == PP) {                                                        \
+      if (g1) k_leaf_lop_int<PP, true><<<grid, NT, sm2, st>>>(a);           \
+      else k_leaf_lop_int<PP, false><<<grid, NT, sm2, st>>>(a);             \
+    }
+    HPSB_LOP(10) HPSB_LOP(12) HPSB_LOP(16)
+#undef HPSB_LOP
+    HPSB_LAUNCH_CHECK();
+    return HPS_OK;
+  }
   size_t smem = (size_t)(4 * pp + 4 * qq + a.lpb * pp) * 8;
-  dim3 grid((unsigned)cdiv(P.L, a.lpb), (unsigned)k);
   k_leaf_eval<<<grid, NT, smem, st>>>(a);
   HPSB_LAUNCH_CHECK();
   return HPS_OK;

@@ -69,7 +69,7 @@ class DevicePlan:
         ws = self._ws.get(k)
         if ws is None:
             nbytes = self._lib.hps_solve_workspace_bytes(self.handle, k)
-            ws = torch.empty(nbytes, dtype=torch.uint8, device=cuda_device())
+            ws = torch.zeros(nbytes, dtype=torch.uint8, device=cuda_device())  # split-K semaphores start at 0
             self._ws[k] = ws
         return ws
 
