@@ -97,7 +97,9 @@ size_t hps_ops_device_bytes(const hps_ops* ops);
 /* Copy one operator block to host memory (test hooks leaf_operators /
  * merge_operators, solver.py:339-348).  which: leaf 0=Ainv (ni x ni),
  * 1=S (ni x nb), 2=T (nb x nb, keep_dtn only); merge 0=Xinv (n3 x n3),
- * 1=Tstack (n12 x n3), 2=S (n3 x n12), 3=T (n12 x n12, keep_dtn only).
+ * 1=Tstack (n12 x n3, root only), 2=S (n3 x n12), 3=T (n12 x n12, keep_dtn
+ * or root), 4=Tstack Xinv (n12 x n3, non-root: the flux rows of the stacked
+ * up-pass operator; Tstack = (Tstack Xinv) Xinv^-1).
  * `level` is the parent level (root = 0), `node` the position on it. */
 int hps_ops_get_leaf(const hps_ops* ops, int which, int leaf, double* host_out);
 int hps_ops_get_merge(const hps_ops* ops, int level, int node, int which, double* host_out);

@@ -1,9 +1,11 @@
 // C ABI (include/hpstep_b200.h): plan / operator-set lifecycle and solve.
 #include <math.h>
+#include <stdlib.h>
 #include <stdarg.h>
 #include <string.h>
 
 #include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/hpstep_b200.h"
@@ -23,6 +25,14 @@ void set_error(const char* fmt, ...) {
 }
 void set_error_node(long long node) { g_err_node = node; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 int gj_invert(int n, int batch, double* A, double* X, int ldx, long long sX, double* stats, cudaStream_t st);
 int leaf_assemble(int Lc, int ni, int nb, const double* cv, int has_c1, int has_c2, int has_c,
                   const double* D2x, const double* D2y, const double* D1x, const double* D1y, double sigma,
@@ -32,6 +42,55 @@ int merge_gather(int c, int n3, int n1a, int n2b, int nbc, const double* Tc, lon
                  double* Tnew, cudaStream_t st);
 
 static const double kPivotRtol = 1e-13;  // linalg.py:17
+
+// Subtree-local slot numbering for the fused levels (see Plan::sub_slots),
+// built from subtree b; false if some id is not covered.
+static bool subtree_slots(const Plan& P, const int* const* gb, const int* const* j3, const int* lbg, int b,
+                          std::vector<int>& slots, std::vector<long long>& off, std::vector<int>& jbase,
+                          int& nslots) {
+  const int nf = P.depth - P.dF;
+  std::unordered_map<int, int> m;
+  int ns = 0;
+  const Level& R = P.lv[P.dF];
+  for (int col = 0; col < R.n12; ++col) m[gb[P.dF][(size_t)b * R.n12 + col]] = ns++;
+  jbase.assign(nf, 0);
+  for (int e = 0; e < nf; ++e) {
+    const int d = P.dF + e, npn = 1 << e;
+    const Level& L = P.lv[d];
+    jbase[e] = ns;
+    for (int j = 0; j < npn; ++j)
+      for (int r = 0; r < L.n3; ++r) m[j3[d][((size_t)b * npn + j) * L.n3 + r]] = ns++;
+  }
+  nslots = ns;
+  slots.clear();
+  off.assign(nf + 1, 0);
+  auto slot = [&](int id, int& out) {
+    auto it = m.find(id);
+    if (it == m.end()) return false;
+    out = it->second;
+    return true;
+  };
+  for (int e = 0; e < nf; ++e) {
+    const int d = P.dF + e, npn = 1 << e;
+    const Level& L = P.lv[d];
+    off[e] = (long long)slots.size();
+    for (int j = 0; j < npn; ++j)
+      for (int col = 0; col < L.n12; ++col) {
+        int sl;
+        if (!slot(gb[d][((size_t)b * npn + j) * L.n12 + col], sl)) return false;
+        slots.push_back(sl);
+      }
+  }
+  off[nf] = (long long)slots.size();
+  const int nl = 1 << nf;
+  for (int j = 0; j < nl; ++j)
+    for (int col = 0; col < P.nb; ++col) {
+      int sl;
+      if (!slot(lbg[((size_t)b * nl + j) * P.nb + col], sl)) return false;
+      slots.push_back(sl);
+    }
+  return true;
+}
 
 template <class T>
 static int upload(const T* host, size_t count, T** dev) {
@@ -110,6 +169,24 @@ int hps_plan_create(const hps_plan_desc* d, hps_plan** out) {
     up(d->lvl_gidx_bnd[l], (size_t)lv.c * lv.n12, &lv.gidx_bnd);
     up(d->lvl_j3[l], (size_t)lv.c * lv.n3, &lv.j3);
     lv.node_index.assign(d->lvl_node_index[l], d->lvl_node_index[l] + lv.c);
+  }
+  P.dF = fuse_level(P);
+  if (!rc && P.dF < P.depth) {
+    std::vector<int> s0, s1;
+    std::vector<long long> o0, o1;
+    std::vector<int> j0, j1;
+    int n0 = 0, n1 = 0;
+    const int last = P.lv[P.dF].c - 1;
+    bool ok = subtree_slots(P, d->lvl_gidx_bnd, d->lvl_j3, d->leaf_bnd_gidx, 0, s0, o0, j0, n0) &&
+              subtree_slots(P, d->lvl_gidx_bnd, d->lvl_j3, d->leaf_bnd_gidx, last, s1, o1, j1, n1) &&
+              s0 == s1 && n0 == n1;
+    if (ok) {
+      P.sub_local = true;
+      P.sub_nslots = n0;
+      P.sub_slot_off = o0;
+      P.sub_j3_base = j0;
+      up(s0.data(), s0.size(), &P.sub_slots);
+    }
   }
   up(d->leaf_bnd_gidx, (size_t)P.L * P.nb, &P.leaf_bnd_gidx);
   up(d->boundary_ids, (size_t)P.nbd, &P.boundary_ids);
@@ -284,13 +361,19 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     double* X33 = talloc((size_t)ce * n3 * n3);
     double* R = talloc((size_t)ce * n3 * n12);
     double* lst = talloc(2 * (size_t)ce);
-    lo.Xinv = make_panel(lv.c, n3, n3);
-    lo.Tst = make_panel(lv.c, n12, n3);
-    lo.S = make_panel(lv.c, n3, n12);
-    lo.Xinv.base = ops_alloc(O, lo.Xinv.doubles(), false);
-    lo.Tst.base = ops_alloc(O, lo.Tst.doubles(), false);
+    const int nup = n3 + (l > 0 ? n12 : 0);
+    if (l >= P.dF) {  // fused subtree levels: node-aligned tiles
+      const int npn = 1 << (l - P.dF);
+      lo.Up = make_panel_nodes(lv.c, nup, n3, npn);
+      lo.S = make_panel_nodes(lv.c, n3, n12, npn);
+    } else {
+      lo.Up = make_panel(lv.c, nup, n3);
+      lo.S = make_panel(lv.c, n3, n12);
+    }
+    lo.Up.base = ops_alloc(O, lo.Up.doubles(), false);
     lo.S.base = ops_alloc(O, lo.S.doubles(), false);
-    if (!Xinv || !Tst || !S || !Tnew || !X33 || !R || !lst || !lo.Xinv.base || !lo.Tst.base || !lo.S.base) {
+    double* TX = l > 0 ? talloc((size_t)ce * n12 * lv.ld3) : nullptr;
+    if (!Xinv || !Tst || !S || !Tnew || !X33 || !R || !lst || !lo.Up.base || !lo.S.base || (l > 0 && !TX)) {
       set_error("out of device memory (merge level %d)", l);
       return fail(HPS_ERR_CUDA);
     }
@@ -325,10 +408,24 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     // pack into the streaming layout; constant coefficients: every node of a
     // level is identical (solver.py stores one copy per node, so do we)
     const long long bx = ce < lv.c ? 0 : 1;
-    if (int rc = pack_panel(Xinv, bx * n3 * lv.ld3, lv.ld3, lo.Xinv, st)) return fail(rc);
-    if (int rc = pack_panel(Tst, bx * n12 * lv.ld3, lv.ld3, lo.Tst, st)) return fail(rc);
+    if (l > 0) {
+      GemmArgs x{};  // TX = Tstack X33^-1: the flux rows of the stacked up-pass operator
+      x.M = n12; x.N = n3; x.K = n3; x.alpha = 1.0; x.beta = 0.0;
+      x.A = Tst; x.lda = lv.ld3; x.sA = (long long)n12 * lv.ld3; x.tA = 0;
+      x.B = Xinv; x.ldb = lv.ld3; x.sB = (long long)n3 * lv.ld3; x.tB = 0;
+      x.C = TX; x.ldc = lv.ld3; x.sC = (long long)n12 * lv.ld3; x.batch = ce;
+      if (int rc = gemm(x, st)) return fail(rc);
+    }
+    if (int rc = pack_panel2(Xinv, bx * n3 * lv.ld3, lv.ld3, n3, l > 0 ? TX : Xinv, bx * n12 * lv.ld3, lv.ld3,
+                             lo.Up, st))
+      return fail(rc);
     if (int rc = pack_panel(S, bx * n3 * lv.ld12, lv.ld12, lo.S, st)) return fail(rc);
-    tfree(Xinv); tfree(Tst); tfree(S);
+    if (l == 0) {  // the reference keeps every merge's Tstack; the solve never reads the root's
+      O.root_Tst = ops_alloc(O, (size_t)n12 * lv.ld3, false);
+      if (!O.root_Tst) { set_error("out of device memory (root Tstack)"); return fail(HPS_ERR_CUDA); }
+      HPSB_CUDA(cudaMemcpyAsync(O.root_Tst, Tst, (size_t)n12 * lv.ld3 * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    tfree(Xinv); tfree(Tst); tfree(S); tfree(TX);
     if (!d->keep_dtn) tfree(Tchild);
     tfree(X33); tfree(R); tfree(lst);
     if (keepT) lo.T = Tnew;
@@ -345,12 +442,13 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   return HPS_OK;
 }
 
-static int copy_panel_block(const Panel& pn, int node, double* host) {
+static int copy_panel_block(const Panel& pn, int node, double* host, int row0 = 0, int nrows = -1) {
   double* tmp = nullptr;
+  if (nrows < 0) nrows = pn.R;
   HPSB_CUDA(cudaDeviceSynchronize());
-  HPSB_CUDA(cudaMalloc(&tmp, (size_t)pn.R * pn.C * 8 + 8));
-  int rc = unpack_panel(pn, node, tmp, 0);
-  if (!rc && cudaMemcpy(host, tmp, (size_t)pn.R * pn.C * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
+  HPSB_CUDA(cudaMalloc(&tmp, (size_t)nrows * pn.C * 8 + 8));
+  int rc = unpack_panel(pn, node, row0, nrows, tmp, 0);
+  if (!rc && cudaMemcpy(host, tmp, (size_t)nrows * pn.C * 8, cudaMemcpyDeviceToHost) != cudaSuccess) {
     set_error("copy failed");
     rc = HPS_ERR_CUDA;
   }
@@ -383,8 +481,17 @@ int hps_ops_get_merge(const hps_ops* h, int level, int node, int which, double* 
   const Level& lv = P.lv[level];
   const LevelOps& lo = O.lo[level];
   if (node < 0 || node >= lv.c) { set_error("node out of range"); return HPS_ERR_ARG; }
-  if (which == 0) return copy_panel_block(lo.Xinv, node, host);
-  if (which == 1) return copy_panel_block(lo.Tst, node, host);
+  if (which == 0) return copy_panel_block(lo.Up, node, host, 0, lv.n3);
+  if (which == 1) {
+    if (level > 0) { set_error("Tstack of level %d is stored as Tstack X33^-1 (which=4)", level); return HPS_ERR_ARG; }
+    HPSB_CUDA(cudaDeviceSynchronize());
+    HPSB_CUDA(cudaMemcpy2D(host, lv.n3 * 8, O.root_Tst, lv.ld3 * 8, lv.n3 * 8, lv.n12, cudaMemcpyDeviceToHost));
+    return HPS_OK;
+  }
+  if (which == 4) {
+    if (level == 0) { set_error("the root has no flux rows"); return HPS_ERR_ARG; }
+    return copy_panel_block(lo.Up, node, host, lv.n3, lv.n12);
+  }
   if (which == 2) return copy_panel_block(lo.S, node, host);
   if (which == 3 && lo.T) {
     int nn = O.shared_leaf ? 0 : node;

@@ -24,6 +24,8 @@ __global__ void __launch_bounds__(NT) k_gemm(GemmArgs g, int tilesM, int tilesN)
   const double* __restrict__ A = g.A + (long long)b * g.sA;
   const double* __restrict__ B = g.B + (long long)b * g.sB;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  pdl_trigger();
+  pdl_wait();
 
   double ra[4], rb[4];
   auto loadA = [&](int k0) {
@@ -120,11 +122,11 @@ int gemm(const GemmArgs& g, cudaStream_t st) {
   if (blocks > 0x7fffffffLL) { set_error("gemm grid too large"); return -1; }
   dim3 grid((unsigned)blocks);
   if (g.tA) {
-    if (g.tB) k_gemm<1, 1><<<grid, NT, 0, st>>>(g, tm, tn);
-    else k_gemm<1, 0><<<grid, NT, 0, st>>>(g, tm, tn);
+    if (g.tB) HPSB_CUDA(launch_pdl(k_gemm<1, 1>, grid, dim3(NT), 0, st, g, tm, tn));
+    else HPSB_CUDA(launch_pdl(k_gemm<1, 0>, grid, dim3(NT), 0, st, g, tm, tn));
   } else {
-    if (g.tB) k_gemm<0, 1><<<grid, NT, 0, st>>>(g, tm, tn);
-    else k_gemm<0, 0><<<grid, NT, 0, st>>>(g, tm, tn);
+    if (g.tB) HPSB_CUDA(launch_pdl(k_gemm<0, 1>, grid, dim3(NT), 0, st, g, tm, tn));
+    else HPSB_CUDA(launch_pdl(k_gemm<0, 0>, grid, dim3(NT), 0, st, g, tm, tn));
   }
   HPSB_LAUNCH_CHECK();
   return 0;

@@ -6,6 +6,7 @@
 #include <stdio.h>
 
 #include <atomic>
+#include <utility>
 #include <string>
 
 namespace hpsb {
@@ -42,6 +43,35 @@ extern std::atomic<long long> g_launches;
   } while (0)
 
 __host__ __device__ inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+): the solve is a chain of ~30
+// dependent kernels on one stream.  Every kernel of the chain triggers its
+// dependents on entry and waits for its predecessor (griddepcontrol.wait)
+// only before touching vectors; loads of the immutable operators may be
+// issued before the wait, so a kernel's launch, prologue and first operator
+// batch overlap the tail of the previous one.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+bool pdl_enabled();  // HPSB_NO_PDL=1 disables
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // Batched FP64 GEMM:  C[b] = alpha * op(A[b]) * op(B[b]) + beta * D[b]

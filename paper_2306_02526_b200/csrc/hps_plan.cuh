@@ -34,6 +34,16 @@ struct Plan {
   int* leaf_bnd_gidx = nullptr;   // device L x nb
   int* boundary_ids = nullptr;    // device nbd
   std::vector<long long> leaf_node_index;  // host
+  int dF = 0;                     // levels d >= dF run as fused subtree kernels
+  // subtree-local numbering of the DOFs a fused subtree touches (the same for
+  // every level-dF subtree): slots [0, n12_dF) = the subtree root's boundary,
+  // then every subtree node's interface (j3) level by level.  sub_slots maps
+  // each fused level's gidx_bnd (and the leaves' boundaries) to slots.
+  bool sub_local = false;
+  int sub_nslots = 0;
+  int* sub_slots = nullptr;                 // device
+  std::vector<long long> sub_slot_off;      // per fused level, then the leaves
+  std::vector<int> sub_j3_base;             // first slot of level e's interfaces
   int ldi = 0;                    // even-padded ni
   int ldb = 0;                    // even-padded nb
 };
@@ -50,11 +60,16 @@ constexpr int kPanelRows = 512;
 struct Panel {
   double* base = nullptr;
   int c = 0, R = 0, C = 0;
-  int TR = kPanelRows;
+  int TR = kPanelRows;  // logical rows per tile
+  int TS = kPanelRows;  // stored rows per tile (even; > TR only for node-aligned tiles)
   int ntiles = 0;
-  size_t doubles() const { return (size_t)ntiles * C * TR; }
+  size_t doubles() const { return (size_t)ntiles * C * TS; }
 };
+// wide levels: power-of-two tiles (TS = TR)
 Panel make_panel(int c, int R, int C);
+// fused (subtree) levels: one tile = the npn nodes of one subtree, so one
+// CTA finds all of its operator rows for a level in one contiguous tile
+Panel make_panel_nodes(int c, int R, int C, int npn);
 
 // launch-time split of a panel for k right-hand sides (split-K over columns)
 struct PanelSplit {
@@ -69,8 +84,10 @@ struct PanelSplit {
 PanelSplit panel_split(const Panel& pn, int k);
 
 struct LevelOps {
-  Panel Xinv;              // n3 x n3 per node
-  Panel Tst;               // n12 x n3
+  // up-pass operator of a node: [X33^-1; Tstack X33^-1], (n3 + n12) x n3
+  // (root: X33^-1 only).  Both halves act on the same r3, so w3 and the
+  // node's outgoing flux h = [ha; hb] + (Tstack X33^-1) r3 come out of one pass.
+  Panel Up;
   Panel S;                 // n3 x n12
   double* T = nullptr;     // c x n12 x n12 row-major (only when keep_dtn)
 };
@@ -87,12 +104,16 @@ struct Ops {
   double* D_bi = nullptr;      // nb x ni (shared stencil rows)
   std::vector<LevelOps> lo;    // depth entries, root first
   double* root_T = nullptr;    // n12 x n12 of the root (keep_dtn)
+  double* root_Tst = nullptr;  // root Tstack, n12 x ld3 row-major (test hooks only)
   size_t bytes = 0;            // device bytes owned
   std::vector<void*> allocs;
 };
 
 int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st);
-int unpack_panel(const Panel& pn, int node, double* dst, cudaStream_t st);  // dst R x C row-major
+// rows [0, R1) of each node from src1, rows [R1, R) from src2
+int pack_panel2(const double* src1, long long s1, int ld1, int R1, const double* src2, long long s2, int ld2,
+                const Panel& pn, cudaStream_t st);
+int unpack_panel(const Panel& pn, int node, int row0, int nrows, double* dst, cudaStream_t st);  // nrows x C
 
 // per-solve workspace carve-up (per-rhs strides in doubles)
 struct Workspace {
@@ -108,7 +129,7 @@ size_t workspace_bytes(const Plan& P, int k);
 void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
 
 // level GEMV launcher (see level_gemv.cu)
-enum GemvMode { GEMV_UPX = 0, GEMV_UPT = 1, GEMV_DOWN = 2, GEMV_LEAF = 3 };
+enum GemvMode { GEMV_UP = 0, GEMV_DOWN = 2, GEMV_LEAF = 3 };
 
 struct GemvArgs {
   int mode;
@@ -129,6 +150,13 @@ struct GemvArgs {
   double* part; unsigned* cnt;
 };
 int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st);
+
+// fused subtree kernels (subtree.cu) for the narrow levels dF..depth-1
+int fuse_level(const Plan& P);
+int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, long long sh, long long hs,
+               const double* jump, long long ld_jump, double inv_dt, cudaStream_t st);
+int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u,
+                 cudaStream_t st);
 
 // solve entry (solve.cu)
 int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,

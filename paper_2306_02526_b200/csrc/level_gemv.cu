@@ -1,8 +1,9 @@
 // Level-batched streaming GEMV for the HPS solve (sm_100a, FP64, HBM-bound).
 //
 // One launch applies one operator family of one tree level to every node:
-//   UPX : w3   = X33^-1 (hb[i3b] - ha[i3a] [- jump/dt])        (solver.py:246-251)
-//   UPT : h    = [ha[i1a]; hb[i2b]] + Tstack w3                 (solver.py:252-254)
+//   UP  : r3 = hb[i3b] - ha[i3a] [- jump/dt]                    (solver.py:246-250)
+//         w3 = X33^-1 r3, h = [ha[i1a]; hb[i2b]] + (Tstack X33^-1) r3
+//         (solver.py:251-254) -- one stacked operator, one pass
 //   DOWN: u[j3] = S u[gidx_bnd] (+ w3)                          (solver.py:261-268)
 //   LEAF: y    = M x (+ add)   per leaf (variable-coefficient leaves,
 //                               solver.py:225-227 and 269-272)
@@ -20,27 +21,42 @@
 // with a semaphore, reset for the next launch) adds them in chunk order, so
 // results stay bitwise reproducible.
 #include "hps_plan.cuh"
+#include "stream.cuh"
 
 namespace hpsb {
 
-// Tile height: 512 rows (256 threads) unless that leaves too few tiles to
-// fill the machine, then 256 or 128 rows (smaller CTAs, more of them
-// resident per SM, which overlaps one CTA's gather with another's stream).
+// Tile height: 512 rows (256 threads, two rows each) unless that leaves too
+// few tiles to spread over the SMs, then down to 64 rows (one warp).  The
+// total thread count of a launch is (rows/2) x (column splits), whatever the
+// tile height; the height only sets how evenly the tiles land on the SMs.
 Panel make_panel(int c, int R, int C) {
   Panel p;
   p.c = c; p.R = R; p.C = C;
   const long long rows = (long long)c * R;
   p.TR = kPanelRows;
-  while (p.TR > 128 && cdiv(rows, p.TR) < 4LL * kNumSMs) p.TR /= 2;
+  while (p.TR > 64 && cdiv(rows, p.TR) < 2LL * kNumSMs) p.TR /= 2;
+  p.TS = p.TR;
   p.ntiles = (int)cdiv(rows, p.TR);
+  return p;
+}
+
+Panel make_panel_nodes(int c, int R, int C, int npn) {
+  Panel p;
+  p.c = c; p.R = R; p.C = C;
+  p.TR = npn * R;
+  p.TS = (p.TR + 1) & ~1;
+  p.ntiles = (int)cdiv(c, npn);
   return p;
 }
 
 namespace {
 
 constexpr int NT = 256;
-constexpr int kTargetThreads = kNumSMs * 1536;
+// threads per launch: each keeps 2 batches of U=16 16-byte loads in flight,
+// so ~400 threads per SM cover HBM latency several times over
+constexpr int kTargetThreads = kNumSMs * 384;
 constexpr size_t kMaxStage = 64 * 1024;
+constexpr int kMaxSplit = 32;  // bounds the serial partial-sum tail of the last CTA
 
 }  // namespace
 
@@ -50,8 +66,9 @@ PanelSplit panel_split(const Panel& pn, int k) {
   s.kgroups = (int)cdiv(k, s.KM);
   s.nodes = (int)std::min<long long>(pn.c, (pn.TR - 1) / pn.R + 2);
   long long base = (long long)pn.ntiles * s.kgroups;
-  int ns = (int)std::max<long long>(1, cdiv(kTargetThreads / (pn.TR / 2), base));
+  int ns = (int)std::max<long long>(1, cdiv(kTargetThreads, base * (pn.TR / 2)));
   ns = std::min(ns, std::max(1, pn.C / 16));
+  ns = std::min(ns, kMaxSplit);
   int CK = (int)cdiv(pn.C, ns);
   auto xs = [](int ck) { return ck | 1; };
   long long cap = (long long)(kMaxStage / 8) / ((long long)s.nodes * s.KM);
@@ -71,14 +88,12 @@ namespace {
 
 template <int MODE>
 __device__ __forceinline__ double xval(const GemvArgs& a, int node, int kg, int col) {
-  if (MODE == GEMV_UPX) {
+  if (MODE == GEMV_UP) {
     const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
     const double* Hb = Ha + a.Hc_s;
     double v = Hb[a.i3b[col]] - Ha[a.i3a[col]];
     if (a.jump) v = v - a.inv_dt * a.jump[kg * a.jump_k + a.j3[(long long)node * a.n3 + col]];
     return v;
-  } else if (MODE == GEMV_UPT) {
-    return a.W3[kg * a.W3_k + (long long)node * a.n3 + col];
   } else if (MODE == GEMV_DOWN) {
     return a.u[kg * a.u_k + a.gidx[(long long)node * a.n12 + col]];
   } else {
@@ -88,13 +103,16 @@ __device__ __forceinline__ double xval(const GemvArgs& a, int node, int kg, int 
 
 template <int MODE>
 __device__ __forceinline__ void epilogue(const GemvArgs& a, int node, int r, int kg, double y) {
-  if (MODE == GEMV_UPX) {
-    a.W3[kg * a.W3_k + (long long)node * a.n3 + r] = y;
-  } else if (MODE == GEMV_UPT) {
-    const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
-    const double* Hb = Ha + a.Hc_s;
-    double base = (r < a.n1a) ? Ha[a.i1a[r]] : Hb[a.i2b[r - a.n1a]];
-    a.Hout[kg * a.Hout_k + (long long)node * a.n12 + r] = base + y;
+  if (MODE == GEMV_UP) {
+    if (r < a.n3) {
+      a.W3[kg * a.W3_k + (long long)node * a.n3 + r] = y;
+    } else {
+      r -= a.n3;
+      const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
+      const double* Hb = Ha + a.Hc_s;
+      double base = (r < a.n1a) ? Ha[a.i1a[r]] : Hb[a.i2b[r - a.n1a]];
+      a.Hout[kg * a.Hout_k + (long long)node * a.n12 + r] = base + y;
+    }
   } else if (MODE == GEMV_DOWN) {
     double v = y;
     if (a.W3) v = v + a.W3[kg * a.W3_k + (long long)node * a.n3 + r];
@@ -120,15 +138,17 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
   const int nn = (int)((std::min(P, p0 + TR) - 1) / R) - n0 + 1;
   const int c0 = split * sp.CK, cw = min(sp.CK, pn.C - c0);
   const int XS = sp.XS;
+  pdl_trigger();
 
   const long long pa = p0 + 2 * tid;
   const int cs = TR / 2;
   const double2* M = reinterpret_cast<const double2*>(pn.base + (size_t)tile * pn.C * TR + (size_t)c0 * TR) + tid;
   // the first batch of the operator stream does not depend on x: issue it
   // before the gather so the two latencies overlap
-  double2 m[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) m[u] = u < cw ? __ldcs(M + (size_t)u * cs) : make_double2(0.0, 0.0);
+  double2 A[U];
+  if (cw >= U) load_batch<U>(A, M, cs, 0);
+
+  pdl_wait();  // vectors below are produced by the previous kernel of the chain
 
   // stage x chunks of the touched nodes: xs[(node*KM + kk)*XS + col]
   for (int e = tid; e < nn * KM * cw; e += blockDim.x) {
@@ -139,31 +159,10 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
 
   const int na = (int)(std::min(pa, P - 1) / R) - n0;
   const int nb = (int)(std::min(pa + 1, P - 1) / R) - n0;
-  const double* xa = xs + na * KM * XS;
-  const double* xb = xs + nb * KM * XS;
-
   double acc0[KM], acc1[KM];
 #pragma unroll
   for (int kk = 0; kk < KM; ++kk) { acc0[kk] = 0.0; acc1[kk] = 0.0; }
-  for (int col = 0; col < cw; col += U) {
-    // software pipeline: next batch in flight while this one is consumed
-    double2 nx[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      nx[u] = col + U + u < cw ? __ldcs(M + (size_t)(col + U + u) * cs) : make_double2(0.0, 0.0);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (col + u < cw) {
-#pragma unroll
-        for (int kk = 0; kk < KM; ++kk) {
-          acc0[kk] = fma(m[u].x, xa[kk * XS + col + u], acc0[kk]);
-          acc1[kk] = fma(m[u].y, xb[kk * XS + col + u], acc1[kk]);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) m[u] = nx[u];
-  }
+  stream_cols<KM, U>(A, M, cs, 0, cw, xs, na * KM * XS, nb * KM * XS, XS, acc0, acc1);
 
   if (sp.nsplit > 1) {
     const long long Pp = (long long)pn.ntiles * TR;
@@ -185,6 +184,7 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) {
       double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
       for (int s = 0; s < sp.nsplit; ++s) {
         double2 v = __ldcg(reinterpret_cast<const double2*>(part + ((long long)kk * sp.nsplit + s) * Pp + pa));
         s0 += v.x;
@@ -212,7 +212,7 @@ int launch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_
     attr_set = true;
   }
   dim3 grid((unsigned)((long long)pn.ntiles * sp.nsplit), (unsigned)sp.kgroups);
-  k_panel<MODE, KM, U><<<grid, pn.TR / 2, sp.smem, st>>>(a, pn, sp);
+  HPSB_CUDA(launch_pdl(k_panel<MODE, KM, U>, grid, dim3(pn.TR / 2), sp.smem, st, a, pn, sp));
   HPSB_LAUNCH_CHECK();
   return 0;
 }
@@ -223,28 +223,33 @@ int dispatch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStrea
   return launch<MODE, 4, 4>(a, pn, sp, st);
 }
 
-__global__ void k_pack(const double* __restrict__ src, long long s_node, int ld, Panel pn) {
-  const long long total = (long long)pn.ntiles * pn.C * pn.TR;
+__global__ void k_pack(const double* __restrict__ src1, long long s1, int ld1, int R1,
+                       const double* __restrict__ src2, long long s2, int ld2, Panel pn) {
+  const long long total = (long long)pn.ntiles * pn.C * pn.TS;
   const long long P = (long long)pn.c * pn.R;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long tile = e / ((long long)pn.C * pn.TR);
-    const long long rem = e % ((long long)pn.C * pn.TR);
-    const int col = (int)(rem / pn.TR), r = (int)(rem % pn.TR);
+    const long long tile = e / ((long long)pn.C * pn.TS);
+    const long long rem = e % ((long long)pn.C * pn.TS);
+    const int col = (int)(rem / pn.TS), r = (int)(rem % pn.TS);
     const long long p = tile * pn.TR + r;
     double v = 0.0;
-    if (p < P) v = src[(p / pn.R) * s_node + (p % pn.R) * (long long)ld + col];
+    if (r < pn.TR && p < P) {
+      const long long node = p / pn.R;
+      const int rr = (int)(p % pn.R);
+      v = rr < R1 ? src1[node * s1 + (long long)rr * ld1 + col] : src2[node * s2 + (long long)(rr - R1) * ld2 + col];
+    }
     pn.base[e] = v;
   }
 }
 
-__global__ void k_unpack(Panel pn, int node, double* __restrict__ dst) {
-  const long long n = (long long)pn.R * pn.C;
+__global__ void k_unpack(Panel pn, int node, int row0, int nrows, double* __restrict__ dst) {
+  const long long n = (long long)nrows * pn.C;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
-    const int row = (int)(e / pn.C), col = (int)(e % pn.C);
+    const int row = (int)(e / pn.C) + row0, col = (int)(e % pn.C);
     const long long p = (long long)node * pn.R + row;
-    dst[e] = pn.base[(p / pn.TR) * pn.C * pn.TR + (long long)col * pn.TR + p % pn.TR];
+    dst[e] = pn.base[(p / pn.TR) * pn.C * pn.TS + (long long)col * pn.TS + p % pn.TR];
   }
 }
 
@@ -252,33 +257,41 @@ __global__ void k_unpack(Panel pn, int node, double* __restrict__ dst) {
 
 int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
   if (pn.c <= 0 || pn.R <= 0 || a.k <= 0) return 0;
+  if (pn.TS != pn.TR) {
+    set_error("gemv: node-aligned panel passed to the level kernel");
+    return -1;
+  }
   const PanelSplit sp = panel_split(pn, a.k);
   if (sp.nsplit > 1 && (!a.part || !a.cnt)) {
     set_error("gemv: split-K needs workspace");
     return -1;
   }
   switch (a.mode) {
-    case GEMV_UPX: return dispatch<GEMV_UPX>(a, pn, sp, st);
-    case GEMV_UPT: return dispatch<GEMV_UPT>(a, pn, sp, st);
+    case GEMV_UP: return dispatch<GEMV_UP>(a, pn, sp, st);
     case GEMV_DOWN: return dispatch<GEMV_DOWN>(a, pn, sp, st);
     default: return dispatch<GEMV_LEAF>(a, pn, sp, st);
   }
 }
 
-int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st) {
-  long long total = (long long)pn.ntiles * pn.C * pn.TR;
+int pack_panel2(const double* src1, long long s1, int ld1, int R1, const double* src2, long long s2, int ld2,
+                const Panel& pn, cudaStream_t st) {
+  long long total = (long long)pn.ntiles * pn.C * pn.TS;
   if (total <= 0) return 0;
   unsigned blocks = (unsigned)std::min<long long>(cdiv(total, 256), (long long)kNumSMs * 32);
-  k_pack<<<blocks, 256, 0, st>>>(src, s_node, ld, pn);
+  k_pack<<<blocks, 256, 0, st>>>(src1, s1, ld1, R1, src2, s2, ld2, pn);
   HPSB_LAUNCH_CHECK();
   return 0;
 }
 
-int unpack_panel(const Panel& pn, int node, double* dst, cudaStream_t st) {
-  long long n = (long long)pn.R * pn.C;
+int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st) {
+  return pack_panel2(src, s_node, ld, pn.R, src, s_node, ld, pn, st);
+}
+
+int unpack_panel(const Panel& pn, int node, int row0, int nrows, double* dst, cudaStream_t st) {
+  long long n = (long long)nrows * pn.C;
   if (n <= 0) return 0;
   unsigned blocks = (unsigned)std::min<long long>(cdiv(n, 256), (long long)kNumSMs * 8);
-  k_unpack<<<blocks, 256, 0, st>>>(pn, node, dst);
+  k_unpack<<<blocks, 256, 0, st>>>(pn, node, row0, nrows, dst);
   HPSB_LAUNCH_CHECK();
   return 0;
 }

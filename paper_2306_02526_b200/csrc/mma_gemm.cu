@@ -49,6 +49,8 @@ __global__ void __launch_bounds__(WM* WN * 32) k_mma_nt(GemmArgs g, int tilesM, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WN, wn = warp % WN;
   const int nk = (g.K + BK - 1) / BK;
+  pdl_trigger();
+  pdl_wait();
 
   auto issue = [&](int kt, int buf) {
     const int k0 = kt * BK;
@@ -132,7 +134,7 @@ int launch_nt(const GemmArgs& g, cudaStream_t st) {
   int tm = (int)cdiv(g.M, BM), tn = (int)cdiv(g.N, BN);
   long long blocks = (long long)tm * tn * g.batch;
   if (blocks > 0x7fffffffLL) { set_error("gemm grid too large"); return -1; }
-  k_mma_nt<WM, WN><<<(unsigned)blocks, WM * WN * 32, smem, st>>>(g, tm, tn);
+  HPSB_CUDA(launch_pdl(k_mma_nt<WM, WN>, dim3((unsigned)blocks), dim3(WM * WN * 32), smem, st, g, tm, tn));
   HPSB_LAUNCH_CHECK();
   return 0;
 }

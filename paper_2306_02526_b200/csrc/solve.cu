@@ -10,6 +10,8 @@ namespace {
 
 __global__ void k_bnd_scatter(int k, int nbd, const int* __restrict__ ids, const double* __restrict__ fb,
                               long long ld_f, double* __restrict__ u, long long ld_u) {
+  pdl_trigger();
+  pdl_wait();
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= (long long)k * nbd) return;
   int kk = (int)(e / nbd), i = (int)(e % nbd);
@@ -18,6 +20,8 @@ __global__ void k_bnd_scatter(int k, int nbd, const int* __restrict__ ids, const
 
 __global__ void k_leaf_gather(int k, int L, int nb, const int* __restrict__ lbg, const double* __restrict__ u,
                               long long ld_u, double* __restrict__ ub) {
+  pdl_trigger();
+  pdl_wait();
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   long long per = (long long)L * nb;
   if (e >= (long long)k * per) return;
@@ -33,9 +37,9 @@ static void solve_panels(const Plan& P, std::vector<Panel>& out) {
   out.clear();
   out.push_back(make_panel(P.L, P.ni, P.ni));
   out.push_back(make_panel(P.L, P.ni, P.nb));
-  for (const Level& lv : P.lv) {
-    out.push_back(make_panel(lv.c, lv.n3, lv.n3));
-    out.push_back(make_panel(lv.c, lv.n12, lv.n3));
+  for (int d = 0; d < P.dF; ++d) {  // wide levels only; fused levels use no split-K
+    const Level& lv = P.lv[d];
+    out.push_back(make_panel(lv.c, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3));
     out.push_back(make_panel(lv.c, lv.n3, lv.n12));
   }
 }
@@ -109,7 +113,8 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
   {
     long long n = (long long)k * P.nbd;
     if (n > 0) {
-      k_bnd_scatter<<<(unsigned)cdiv(n, T), T, 0, st>>>(k, P.nbd, P.boundary_ids, fb, ld_f, u, ld_u);
+      HPSB_CUDA(launch_pdl(k_bnd_scatter, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.nbd, P.boundary_ids,
+                           fb, ld_f, u, ld_u));
       HPSB_LAUNCH_CHECK();
     }
   }
@@ -149,9 +154,11 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
     HPSB_CUDA(cudaMemsetAsync(ws.Hleaf, 0, (size_t)k * Lnb * 8, st));
   }
 
-  // (3) upward merges, deepest level first (solver.py:243-256)
+  // (3) upward merges, deepest level first (solver.py:243-256): the fused
+  // subtree levels in one launch, then one launch per family on wide levels
   if (up) {
-    for (int d = P.depth - 1; d >= 0; --d) {
+    if (int rc = subtree_up(ops, ws, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
+    for (int d = P.dF - 1; d >= 0; --d) {
       const Level& lv = P.lv[d];
       const LevelOps& lo = ops.lo[d];
       const bool leafc = d == P.depth - 1;
@@ -164,17 +171,14 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
       a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
       a.n12 = lv.n12;
       a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt; a.j3 = lv.j3;
-      a.mode = GEMV_UPX;
-      if (int rc = gemv_level(a, lo.Xinv, st)) return rc;
-      if (d == 0) break;  // the root's outer flux is never consumed
-      a.mode = GEMV_UPT;
-      a.Hout = ws.H[d]; a.Hout_k = (long long)lv.c * lv.n12;
-      if (int rc = gemv_level(a, lo.Tst, st)) return rc;
+      a.mode = GEMV_UP;  // the root's panel has no flux rows (its outer flux is never consumed)
+      a.Hout = d > 0 ? ws.H[d] : nullptr; a.Hout_k = (long long)lv.c * lv.n12;
+      if (int rc = gemv_level(a, lo.Up, st)) return rc;
     }
   }
 
   // (4) downward sweep, root first (solver.py:258-268)
-  for (int d = 0; d < P.depth; ++d) {
+  for (int d = 0; d < P.dF; ++d) {
     const Level& lv = P.lv[d];
     const LevelOps& lo = ops.lo[d];
     GemvArgs a{};
@@ -184,11 +188,13 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
     a.W3 = up ? ws.W3[d] : nullptr; a.W3_k = (long long)lv.c * lv.n3;
     if (int rc = gemv_level(a, lo.S, st)) return rc;
   }
+  if (int rc = subtree_down(ops, ws, k, up, u, ld_u, st)) return rc;
 
   // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
   {
     long long n = (long long)k * Lnb;
-    k_leaf_gather<<<(unsigned)cdiv(n, T), T, 0, st>>>(k, P.L, P.nb, P.leaf_bnd_gidx, u, ld_u, ws.Ub);
+    HPSB_CUDA(launch_pdl(k_leaf_gather, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.L, P.nb,
+                         (const int*)P.leaf_bnd_gidx, (const double*)u, ld_u, ws.Ub));
     HPSB_LAUNCH_CHECK();
     if (ops.shared_leaf) {
       GemmArgs a{};

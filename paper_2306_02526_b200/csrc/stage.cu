@@ -249,13 +249,14 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
 template <int P, bool G1>
 __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
   extern __shared__ double U[];  // lpb x P x PS
-  constexpr int Q = P - 2, NI = Q * Q, PS = (P + 1) | 1, PP = P * PS;
+  constexpr int Q = P - 2, NI = Q * Q, PS = (P + 1) | 1, PP = P * PS, NB = 4 * Q;
+  constexpr int LANES = NT / NI;  // threads sharing one interior point (over leaves)
   const int tid = threadIdx.x, lpb = a.lpb;
   const int kk = blockIdx.y;
   const double* u = a.u + kk * a.ld_u;
   const long long ob = kk * a.ld_o;
-  const bool active = tid < lpb * NI;
-  const int ll = tid / NI, t = tid % NI, xi = t / Q + 1, yi = t % Q + 1;
+  const bool active = tid < LANES * NI;
+  const int t = tid % NI, lane0 = tid / NI, xi = t / Q + 1, yi = t % Q + 1;
   double rxx[P], ryy[P], rx[G1 ? P : 1], ry[G1 ? P : 1];
   const double* mats = a.mats;
 #pragma unroll
@@ -275,42 +276,44 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
       U[l2 * PP + (i / Q + 1) * PS + (i % Q + 1)] = v;
       gacc(gmax, v);
     }
-    for (int e = tid; e < nl * 4 * Q; e += NT) {
-      int l2 = e / (4 * Q), j = e % (4 * Q), x, y;
+    for (int e = tid; e < nl * NB; e += NT) {
+      int l2 = e / NB, j = e % NB, x, y;
       edge_xy(j, P, Q, x, y);
-      double v = u[a.lbg[(long long)(l0 + l2) * 4 * Q + j]];
+      double v = u[a.lbg[(long long)l0 * NB + e]];
       U[l2 * PP + x * PS + y] = v;
       gacc(gmax, v);
     }
     __syncthreads();
-    if (!active || ll >= nl) continue;
-    const double* G = U + ll * PP;
-    double ux = 0.0, uxx = 0.0, uy = 0.0, uyy = 0.0;
+    if (!active) continue;
+    for (int ll = lane0; ll < nl; ll += LANES) {
+      const double* G = U + ll * PP;
+      double ux = 0.0, uxx = 0.0, uy = 0.0, uyy = 0.0;
 #pragma unroll
-    for (int s = 0; s < P; ++s) {
-      const double v = G[s * PS + yi];
-      uxx = fma(rxx[s], v, uxx);
-      if (G1) ux = fma(rx[G1 ? s : 0], v, ux);
-    }
+      for (int s = 0; s < P; ++s) {
+        const double v = G[s * PS + yi];
+        uxx = fma(rxx[s], v, uxx);
+        if (G1) ux = fma(rx[G1 ? s : 0], v, ux);
+      }
 #pragma unroll
-    for (int s = 0; s < P; ++s) {
-      const double v = G[xi * PS + s];
-      uyy = fma(ryy[s], v, uyy);
-      if (G1) uy = fma(ry[G1 ? s : 0], v, uy);
+      for (int s = 0; s < P; ++s) {
+        const double v = G[xi * PS + s];
+        uyy = fma(ryy[s], v, uyy);
+        if (G1) uy = fma(ry[G1 ? s : 0], v, uy);
+      }
+      const int l = l0 + ll;
+      double c11, c22, c1, c2, c0;
+      if (a.Lc == 1) { c11 = a.cc[0]; c22 = a.cc[1]; c1 = a.cc[2]; c2 = a.cc[3]; c0 = a.cc[4]; }
+      else {
+        const double* cv = a.coef + (long long)l * 5 * a.m;
+        c11 = cv[t]; c22 = cv[a.m + t]; c1 = cv[2 * a.m + t]; c2 = cv[3 * a.m + t]; c0 = cv[4 * a.m + t];
+      }
+      double lop = __dmul_rn(c11, uxx);
+      lop = __dadd_rn(lop, __dmul_rn(c22, uyy));
+      if (a.has_c1) lop = __dsub_rn(lop, __dmul_rn(c1, ux));
+      if (a.has_c2) lop = __dsub_rn(lop, __dmul_rn(c2, uy));
+      if (a.has_c) lop = __dsub_rn(lop, __dmul_rn(c0, G[xi * PS + yi]));
+      a.lu_int[ob + (long long)l * NI + t] = lop;
     }
-    const int l = l0 + ll;
-    double c11, c22, c1, c2, c0;
-    if (a.Lc == 1) { c11 = a.cc[0]; c22 = a.cc[1]; c1 = a.cc[2]; c2 = a.cc[3]; c0 = a.cc[4]; }
-    else {
-      const double* cv = a.coef + (long long)l * 5 * a.m;
-      c11 = cv[t]; c22 = cv[a.m + t]; c1 = cv[2 * a.m + t]; c2 = cv[3 * a.m + t]; c0 = cv[4 * a.m + t];
-    }
-    double lop = __dmul_rn(c11, uxx);
-    lop = __dadd_rn(lop, __dmul_rn(c22, uyy));
-    if (a.has_c1) lop = __dsub_rn(lop, __dmul_rn(c1, ux));
-    if (a.has_c2) lop = __dsub_rn(lop, __dmul_rn(c2, uy));
-    if (a.has_c) lop = __dsub_rn(lop, __dmul_rn(c0, G[xi * PS + yi]));
-    a.lu_int[ob + (long long)l * NI + t] = lop;
   }
   if (a.guard) guard_max(a.guard, gmax);
 }
@@ -457,7 +460,7 @@ int hps_leaf_eval(const hps_disc* h, int k, const double* u, long long ld_u, dou
   dim3 grid(std::min(groups, (unsigned)(kNumSMs * 8)), (unsigned)k);
   const bool int_only = lu_int && !lu && !ux && !uy && !jump;
   if (int_only && (D.p == 10 || D.p == 12 || D.p == 16)) {
-    a.lpb = std::max(1, NT / (D.ni));
+    a.lpb = std::max(1, 2048 / (D.p * D.p));  // ~2K staged values per iteration
     groups = (unsigned)cdiv(P.L, a.lpb);
     grid.x = std::min(groups, (unsigned)(kNumSMs * 8));
     size_t sm2 = (size_t)a.lpb * pp * 8;

@@ -1,0 +1,57 @@
+// Column-streaming core shared by the level and subtree GEMV kernels.
+//
+// A thread owns two adjacent rows of a column-major panel tile (one 16-byte
+// load per column) and accumulates acc{0,1}[kk] += M[col].{x,y} * x[kk][col]
+// with x in shared memory.  Two register batches of U columns alternate
+// without copies (a copy would force a wait on the in-flight loads), so one
+// batch is always in flight while the other is consumed.
+#pragma once
+
+#include "hps_common.cuh"
+
+namespace hpsb {
+
+template <int U>
+__device__ __forceinline__ void load_batch(double2 (&m)[U], const double2* __restrict__ M, int cs, int col) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) m[u] = __ldcs(M + (size_t)(col + u) * cs);
+}
+
+template <int KM, int U>
+__device__ __forceinline__ void fma_batch(const double2 (&m)[U], const double* xs, int oa, int ob, int XS, int col,
+                                          double (&acc0)[KM], double (&acc1)[KM]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int kk = 0; kk < KM; ++kk) {
+      acc0[kk] = fma(m[u].x, xs[oa + kk * XS + col + u], acc0[kk]);
+      acc1[kk] = fma(m[u].y, xs[ob + kk * XS + col + u], acc1[kk]);
+    }
+}
+
+// A must already hold columns [c0, c0+U) when (c1 - c0) >= U.
+template <int KM, int U>
+__device__ __forceinline__ void stream_cols(double2 (&A)[U], const double2* __restrict__ M, int cs, int c0, int c1,
+                                            const double* xs, int oa, int ob, int XS, double (&acc0)[KM],
+                                            double (&acc1)[KM]) {
+  double2 B[U];
+  const int nfull = (c1 - c0) / U;
+  int b = 0;
+  for (; b + 1 < nfull; b += 2) {
+    load_batch<U>(B, M, cs, c0 + (b + 1) * U);
+    fma_batch<KM, U>(A, xs, oa, ob, XS, c0 + b * U, acc0, acc1);
+    if (b + 2 < nfull) load_batch<U>(A, M, cs, c0 + (b + 2) * U);
+    fma_batch<KM, U>(B, xs, oa, ob, XS, c0 + (b + 1) * U, acc0, acc1);
+  }
+  if (b < nfull) fma_batch<KM, U>(A, xs, oa, ob, XS, c0 + b * U, acc0, acc1);
+  for (int col = c0 + nfull * U; col < c1; ++col) {
+    const double2 m = __ldcs(M + (size_t)col * cs);
+#pragma unroll
+    for (int kk = 0; kk < KM; ++kk) {
+      acc0[kk] = fma(m.x, xs[oa + kk * XS + col], acc0[kk]);
+      acc1[kk] = fma(m.y, xs[ob + kk * XS + col], acc1[kk]);
+    }
+  }
+}
+
+}  // namespace hpsb

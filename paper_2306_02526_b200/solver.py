@@ -278,7 +278,11 @@ class HpsOperatorSet:
 
     def _merge_block(self, level, pos, which):
         lm = self.tree.level_maps[level]
-        shape = {0: (lm.n3, lm.n3), 1: (lm.n12, lm.n3), 2: (lm.n3, lm.n12), 3: (lm.n12, lm.n12)}[which]
+        if which == 1 and level > 0:
+            # stored as the flux rows Tstack X33^-1 of the stacked up-pass operator
+            return self._merge_block(level, pos, 4) @ np.linalg.inv(self._merge_block(level, pos, 0))
+        shape = {0: (lm.n3, lm.n3), 1: (lm.n12, lm.n3), 2: (lm.n3, lm.n12), 3: (lm.n12, lm.n12),
+                 4: (lm.n12, lm.n3)}[which]
         out = np.empty(shape)
         _lib.check(self._lib.hps_ops_get_merge(self.handle, level, pos, which, _lib.dbl_ptr(out)),
                    "hps_ops_get_merge")
