@@ -143,6 +143,10 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()   # nvidia-smi takes a while to start: wait for its first row
+            while not self.rows and time.time() - t0 < 5.0:
+                time.sleep(0.02)
+            self.n0 = len(self.rows)
         except OSError:
             self.proc = None
         return self
@@ -153,6 +157,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc is not None:
+            t0 = time.time()   # at least one row from inside / right at the end of the region
+            while len(self.rows) <= self.n0 and time.time() - t0 < 1.0:
+                time.sleep(0.02)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -313,11 +320,16 @@ def main():
     st.solve_timer = []
     n0 = lib.hps_launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    prof = os.environ.get("HPSB_PROFILE_RANGE") == "1"   # ncu --profile-from-start off
     with ClockSampler(local) as clk:
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         ev0.record()
         state = st.run(state, args.steps, check_every=max(1, args.steps))
         ev1.record()
         barrier()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
     launches = lib.hps_launch_count() - n0
     ms = ev0.elapsed_time(ev1)
     solve_ms = [a.elapsed_time(b) for a, b in st.solve_timer]

@@ -79,7 +79,16 @@ typedef struct {
   const double* D1x;
   const double* D1y;
   const double* D_bnd; /* nb x m flux rows (operators.py:188-190)            */
+  int layout;          /* HPS_LAYOUT_PER_NODE: one operator copy per node,
+                          streamed from HBM every solve (what the reference
+                          stores, solver.py:137-151); HPS_LAYOUT_SHARED: one
+                          copy per level, level applies run as tensor-core
+                          GEMMs (constant coefficients only, where every node
+                          of a level has bitwise the same operators)          */
 } hps_build_desc;
+
+#define HPS_LAYOUT_PER_NODE 0
+#define HPS_LAYOUT_SHARED 1
 
 int hps_version(void);
 long long hps_launch_count(void); /* kernels launched by this library so far */

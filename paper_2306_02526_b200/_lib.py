@@ -45,7 +45,12 @@ class BuildDesc(ctypes.Structure):
         ("has_c", ctypes.c_int),
         ("D2x", c_double_p), ("D2y", c_double_p), ("D1x", c_double_p), ("D1y", c_double_p),
         ("D_bnd", c_double_p),
+        ("layout", ctypes.c_int),
     ]
+
+
+LAYOUT_PER_NODE = 0
+LAYOUT_SHARED = 1
 
 
 class DiscDesc(ctypes.Structure):

@@ -231,6 +231,12 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   O.plan = const_cast<Plan*>(&P);
   O.sigma = d->sigma; O.dtg = d->dt_gamma;
   O.shared_leaf = d->shared_leaf ? 1 : 0;
+  if (d->layout == HPS_LAYOUT_SHARED && !O.shared_leaf) {
+    set_error("hps_ops_build: the shared layout needs constant coefficients");
+    delete h;
+    return HPS_ERR_ARG;
+  }
+  O.shared_levels = d->layout == HPS_LAYOUT_SHARED ? 1 : 0;
   O.Lc = O.shared_leaf ? 1 : P.L;
   O.lo.resize(P.depth);
   const int ni = P.ni, nb = P.nb, m = ni + nb, Lc = O.Lc;
@@ -362,7 +368,16 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     double* R = talloc((size_t)ce * n3 * n12);
     double* lst = talloc(2 * (size_t)ce);
     const int nup = n3 + (l > 0 ? n12 : 0);
-    if (l >= P.dF) {  // fused subtree levels: node-aligned tiles
+    if (O.shared_levels && l >= P.dF) {  // fused levels: ONE node-aligned tile read by every subtree CTA
+      const int npn = 1 << (l - P.dF);
+      lo.Up = make_panel_nodes(npn, nup, n3, npn);
+      lo.S = make_panel_nodes(npn, n3, n12, npn);
+    } else if (O.shared_levels) {  // wide levels: one-node panels (or GEMM operands only)
+      if (lv.c < kSharedGemmNodes) {
+        lo.Up = make_panel(1, nup, n3);
+        lo.S = make_panel(1, n3, n12);
+      }
+    } else if (l >= P.dF) {  // fused subtree levels: node-aligned tiles
       const int npn = 1 << (l - P.dF);
       lo.Up = make_panel_nodes(lv.c, nup, n3, npn);
       lo.S = make_panel_nodes(lv.c, n3, n12, npn);
@@ -370,10 +385,16 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
       lo.Up = make_panel(lv.c, nup, n3);
       lo.S = make_panel(lv.c, n3, n12);
     }
-    lo.Up.base = ops_alloc(O, lo.Up.doubles(), false);
-    lo.S.base = ops_alloc(O, lo.S.doubles(), false);
+    if (lo.Up.c) lo.Up.base = ops_alloc(O, lo.Up.doubles(), false);
+    if (lo.S.c) lo.S.base = ops_alloc(O, lo.S.doubles(), false);
+    if (O.shared_levels) {
+      lo.Ush = ops_alloc(O, (size_t)nup * lv.ld3, true);
+      lo.Ssh = ops_alloc(O, (size_t)n3 * lv.ld12, true);
+    }
     double* TX = l > 0 ? talloc((size_t)ce * n12 * lv.ld3) : nullptr;
-    if (!Xinv || !Tst || !S || !Tnew || !X33 || !R || !lst || !lo.Up.base || !lo.S.base || (l > 0 && !TX)) {
+    const bool ok_ops = O.shared_levels ? (lo.Ush && lo.Ssh && (!lo.Up.c || (lo.Up.base && lo.S.base)))
+                                        : (lo.Up.base && lo.S.base);
+    if (!Xinv || !Tst || !S || !Tnew || !X33 || !R || !lst || !ok_ops || (l > 0 && !TX)) {
       set_error("out of device memory (merge level %d)", l);
       return fail(HPS_ERR_CUDA);
     }
@@ -416,10 +437,19 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
       x.C = TX; x.ldc = lv.ld3; x.sC = (long long)n12 * lv.ld3; x.batch = ce;
       if (int rc = gemm(x, st)) return fail(rc);
     }
-    if (int rc = pack_panel2(Xinv, bx * n3 * lv.ld3, lv.ld3, n3, l > 0 ? TX : Xinv, bx * n12 * lv.ld3, lv.ld3,
-                             lo.Up, st))
-      return fail(rc);
-    if (int rc = pack_panel(S, bx * n3 * lv.ld12, lv.ld12, lo.S, st)) return fail(rc);
+    if (lo.Up.base) {
+      if (int rc = pack_panel2(Xinv, bx * n3 * lv.ld3, lv.ld3, n3, l > 0 ? TX : Xinv, bx * n12 * lv.ld3, lv.ld3,
+                               lo.Up, st))
+        return fail(rc);
+      if (int rc = pack_panel(S, bx * n3 * lv.ld12, lv.ld12, lo.S, st)) return fail(rc);
+    }
+    if (O.shared_levels) {
+      HPSB_CUDA(cudaMemcpyAsync(lo.Ush, Xinv, (size_t)n3 * lv.ld3 * 8, cudaMemcpyDeviceToDevice, st));
+      if (l > 0)
+        HPSB_CUDA(cudaMemcpyAsync(lo.Ush + (size_t)n3 * lv.ld3, TX, (size_t)n12 * lv.ld3 * 8,
+                                  cudaMemcpyDeviceToDevice, st));
+      HPSB_CUDA(cudaMemcpyAsync(lo.Ssh, S, (size_t)n3 * lv.ld12 * 8, cudaMemcpyDeviceToDevice, st));
+    }
     if (l == 0) {  // the reference keeps every merge's Tstack; the solve never reads the root's
       O.root_Tst = ops_alloc(O, (size_t)n12 * lv.ld3, false);
       if (!O.root_Tst) { set_error("out of device memory (root Tstack)"); return fail(HPS_ERR_CUDA); }
@@ -481,6 +511,15 @@ int hps_ops_get_merge(const hps_ops* h, int level, int node, int which, double* 
   const Level& lv = P.lv[level];
   const LevelOps& lo = O.lo[level];
   if (node < 0 || node >= lv.c) { set_error("node out of range"); return HPS_ERR_ARG; }
+  if (O.shared_levels && (which == 0 || which == 2 || which == 4)) {  // one operator for every node
+    const double* src = which == 0 ? lo.Ush : which == 4 ? lo.Ush + (size_t)lv.n3 * lv.ld3 : lo.Ssh;
+    const int rows = which == 4 ? lv.n12 : lv.n3, cols = which == 2 ? lv.n12 : lv.n3;
+    const int ld = which == 2 ? lv.ld12 : lv.ld3;
+    if (which == 4 && level == 0) { set_error("the root has no flux rows"); return HPS_ERR_ARG; }
+    HPSB_CUDA(cudaDeviceSynchronize());
+    HPSB_CUDA(cudaMemcpy2D(host, cols * 8, src, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost));
+    return HPS_OK;
+  }
   if (which == 0) return copy_panel_block(lo.Up, node, host, 0, lv.n3);
   if (which == 1) {
     if (level > 0) { set_error("Tstack of level %d is stored as Tstack X33^-1 (which=4)", level); return HPS_ERR_ARG; }

@@ -1,0 +1,233 @@
+// Shared-layout level applies (constant coefficients).
+//
+// With constant coefficients every node of a level has bitwise the same
+// operators (the reference still stores one copy per node, solver.py:137-151),
+// so a level apply is a real GEMM: the level's operator times the matrix
+// whose columns are the nodes' input vectors.  Posed node-major,
+//     Y (nodes x R) = X (nodes x K) * Op^T,   Op = [X33^-1; Tstack X33^-1] (up)
+//                                                   or S (down),
+// it is the "NT" product of mma_gemm.cu with the node vectors gathered
+// straight into the A tiles (r3 = hb[i3b] - ha[i3a] [- jump/dt] for the up
+// pass, u[gidx_bnd] for the down pass) and a scattering epilogue (w3 / the
+// node's flux / u[j3]).  The FP64 tensor pipe (DMMA m8n8k4) does the math;
+// the operator tiles come from L2.  Levels with fewer than kSharedGemmNodes
+// nodes (the top of the tree: few nodes, operators up to hundreds of MB) use
+// the streaming panel kernel on a one-node panel, one virtual tile per
+// (node, tile): the operator is read from HBM once and re-read from L2.
+#include "hps_plan.cuh"
+
+namespace hpsb {
+
+namespace {
+
+constexpr int BK = 16;
+constexpr int SROW = BK + 4;
+constexpr int BM = 64;  // nodes per CTA tile (2 warps of 32 rows)
+
+enum GsMode { GS_UP = 0, GS_DOWN = 1 };
+
+struct GsArgs {
+  int M, N, K;                 // nodes, operator rows, operator columns
+  const double* B; int ldb;    // operator, N x K row-major
+  GemvArgs g;                  // gathers / scatters (same fields as the streaming kernels)
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int MODE>
+__device__ __forceinline__ double gs_x(const GemvArgs& a, int node, int kg, int col) {
+  if (MODE == GS_UP) {
+    const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
+    const double* Hb = Ha + a.Hc_s;
+    double v = Hb[a.i3b[col]] - Ha[a.i3a[col]];
+    if (a.jump) v = v - a.inv_dt * a.jump[kg * a.jump_k + a.j3[(long long)node * a.n3 + col]];
+    return v;
+  } else {
+    return a.u[kg * a.u_k + a.gidx[(long long)node * a.n12 + col]];
+  }
+}
+
+template <int MODE>
+__device__ __forceinline__ void gs_out(const GemvArgs& a, int node, int r, int kg, double y) {
+  if (MODE == GS_UP) {
+    if (r < a.n3) {
+      a.W3[kg * a.W3_k + (long long)node * a.n3 + r] = y;
+    } else {
+      r -= a.n3;
+      const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
+      const double* Hb = Ha + a.Hc_s;
+      const double base = (r < a.n1a) ? Ha[a.i1a[r]] : Hb[a.i2b[r - a.n1a]];
+      a.Hout[kg * a.Hout_k + (long long)node * a.n12 + r] = base + y;
+    }
+  } else {
+    double v = y;
+    if (a.W3) v = v + a.W3[kg * a.W3_k + (long long)node * a.n3 + r];
+    a.u[kg * a.u_k + a.j3[(long long)node * a.n3 + r]] = v;
+  }
+}
+
+template <int MODE, int WN>
+__global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
+  constexpr int BN = 32 * WN, NT = 64 * WN;
+  constexpr int AE = BM * BK / NT, BE = BN * BK / NT;  // staged elements per thread
+  extern __shared__ double sm[];
+  double* As = sm;                  // [2][BM][SROW]
+  double* Bs = sm + 2 * BM * SROW;  // [2][BN][SROW]
+  const int tm = blockIdx.x / tilesN, tn = blockIdx.x % tilesN;
+  const int m0 = tm * BM, n0 = tn * BN, kg = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int nk = (a.K + BK - 1) / BK;
+  pdl_trigger();
+
+  double ra[AE], rb[BE];
+  auto load_b = [&](int kt) {  // the operator does not depend on the previous kernel
+#pragma unroll
+    for (int i = 0; i < BE; ++i) {
+      const int e = tid + NT * i, r = e / BK, c = e % BK;
+      const int gn = n0 + r, gk = kt * BK + c;
+      rb[i] = (gn < a.N && gk < a.K) ? a.B[(long long)gn * a.ldb + gk] : 0.0;
+    }
+  };
+  auto load_a = [&](int kt) {
+#pragma unroll
+    for (int i = 0; i < AE; ++i) {
+      const int e = tid + NT * i, r = e / BK, c = e % BK;
+      const int gm = m0 + r, gk = kt * BK + c;
+      ra[i] = (gm < a.M && gk < a.K) ? gs_x<MODE>(a.g, gm, kg, gk) : 0.0;
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < AE; ++i) {
+      const int e = tid + NT * i;
+      As[(buf * BM + e / BK) * SROW + e % BK] = ra[i];
+    }
+#pragma unroll
+    for (int i = 0; i < BE; ++i) {
+      const int e = tid + NT * i;
+      Bs[(buf * BN + e / BK) * SROW + e % BK] = rb[i];
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+
+  load_b(0);
+  pdl_wait();
+  load_a(0);
+  store(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) { load_b(kt + 1); load_a(kt + 1); }
+    const double* Ab = As + (buf * BM + wm * 32 + (lane >> 2)) * SROW + (lane & 3);
+    const double* Bb = Bs + (buf * BN + wn * 32 + (lane >> 2)) * SROW + (lane & 3);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Ab[i * 8 * SROW + kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bb[j * 8 * SROW + kk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    if (kt + 1 < nk) store(buf ^ 1);
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int node = m0 + wm * 32 + i * 8 + (lane >> 2);
+    if (node >= a.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+        if (r < a.N) gs_out<MODE>(a.g, node, r, kg, acc[i][j][h]);
+      }
+  }
+}
+
+template <int MODE, int WN>
+int launch_gs(const GsArgs& a, int k, cudaStream_t st) {
+  constexpr int BN = 32 * WN;
+  const size_t smem = (size_t)2 * (BM + BN) * SROW * 8;
+  static bool attr = false;
+  if (!attr) {
+    HPSB_CUDA(cudaFuncSetAttribute(k_gs<MODE, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const int tilesM = (int)cdiv(a.M, BM), tilesN = (int)cdiv(a.N, BN);
+  dim3 grid((unsigned)(tilesM * tilesN), (unsigned)k);
+  HPSB_CUDA(launch_pdl(k_gs<MODE, WN>, grid, dim3(64 * WN), smem, st, a, tilesN));
+  HPSB_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int MODE>
+int gs(const GsArgs& a, int k, cudaStream_t st) {
+  // operator rows per CTA tile: enough tiles to fill the SMs, little padding waste
+  const long long tilesM = cdiv(a.M, BM) * (long long)k;
+  if (a.N <= 32 || tilesM * cdiv(a.N, 64) < 2 * kNumSMs) return launch_gs<MODE, 1>(a, k, st);
+  if (a.N <= 64 || tilesM * cdiv(a.N, 128) < 2 * kNumSMs) return launch_gs<MODE, 2>(a, k, st);
+  return launch_gs<MODE, 4>(a, k, st);
+}
+
+}  // namespace
+
+int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const double* Hc, long long Hc_k,
+                    long long Hc_s, const double* jump, long long ld_jump, double inv_dt, cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  const Level& lv = P.lv[d];
+  const LevelOps& lo = ops.lo[d];
+  GemvArgs g{};
+  g.k = k; g.part = ws.part; g.cnt = ws.cnt;
+  g.Hc = Hc; g.nbc = lv.nbc; g.Hc_k = Hc_k; g.Hc_s = Hc_s;
+  g.W3 = ws.W3[d]; g.n3 = lv.n3; g.W3_k = (long long)lv.c * lv.n3;
+  g.i1a = lv.i1a; g.i3a = lv.i3a; g.i2b = lv.i2b; g.i3b = lv.i3b; g.n1a = lv.n1a; g.n12 = lv.n12;
+  g.jump = jump; g.jump_k = ld_jump; g.inv_dt = inv_dt; g.j3 = lv.j3;
+  g.Hout = d > 0 ? ws.H[d] : nullptr; g.Hout_k = (long long)lv.c * lv.n12;
+  if (lv.c < kSharedGemmNodes) {
+    g.mode = GEMV_UP;
+    g.shared = lv.c;
+    return gemv_level(g, lo.Up, st);
+  }
+  GsArgs a{};
+  a.M = lv.c; a.N = lv.n3 + (d > 0 ? lv.n12 : 0); a.K = lv.n3;
+  a.B = lo.Ush; a.ldb = lv.ld3; a.g = g;
+  return gs<GS_UP>(a, k, st);
+}
+
+int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
+                      cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  const Level& lv = P.lv[d];
+  const LevelOps& lo = ops.lo[d];
+  GemvArgs g{};
+  g.k = k; g.part = ws.part; g.cnt = ws.cnt;
+  g.u = u; g.u_k = ld_u; g.gidx = lv.gidx_bnd; g.j3 = lv.j3; g.n3 = lv.n3; g.n12 = lv.n12;
+  g.W3 = has_w3 ? ws.W3[d] : nullptr; g.W3_k = (long long)lv.c * lv.n3;
+  if (lv.c < kSharedGemmNodes) {
+    g.mode = GEMV_DOWN;
+    g.shared = lv.c;
+    return gemv_level(g, lo.S, st);
+  }
+  GsArgs a{};
+  a.M = lv.c; a.N = lv.n3; a.K = lv.n12;
+  a.B = lo.Ssh; a.ldb = lv.ld12; a.g = g;
+  return gs<GS_DOWN>(a, k, st);
+}
+
+}  // namespace hpsb

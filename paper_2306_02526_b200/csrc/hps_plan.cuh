@@ -81,7 +81,7 @@ struct PanelSplit {
   size_t part_doubles = 0;  // split-K partials
   int counters = 0;         // split-K semaphores
 };
-PanelSplit panel_split(const Panel& pn, int k);
+PanelSplit panel_split(const Panel& pn, int k, int vnodes = 1);
 
 struct LevelOps {
   // up-pass operator of a node: [X33^-1; Tstack X33^-1], (n3 + n12) x n3
@@ -89,6 +89,11 @@ struct LevelOps {
   // node's outgoing flux h = [ha; hb] + (Tstack X33^-1) r3 come out of one pass.
   Panel Up;
   Panel S;                 // n3 x n12
+  // shared layout (constant coefficients): the level's single operator pair,
+  // row-major (GEMM operands, levels with >= kSharedGemmNodes nodes) or as
+  // one-node panels (streaming kernel over virtual node tiles, other levels)
+  double* Ush = nullptr;   // (n3 + n12) x ld3
+  double* Ssh = nullptr;   // n3 x ld12
   double* T = nullptr;     // c x n12 x n12 row-major (only when keep_dtn)
 };
 
@@ -96,6 +101,7 @@ struct Ops {
   Plan* plan = nullptr;
   double sigma = 0.0, dtg = 0.0;
   int shared_leaf = 1;         // constant coefficients: one leaf operator set
+  int shared_levels = 0;       // HPS_LAYOUT_SHARED: one operator per level
   int Lc = 1;                  // number of stored leaf operator sets (1 or L)
   double* Ainv = nullptr;      // shared leaf: [Ainv; D_bi Ainv], (ni+nb) x ldi row-major (GEMM operand)
   double* S_leaf = nullptr;    // shared leaf: ni x ldb row-major
@@ -130,6 +136,7 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
 
 // level GEMV launcher (see level_gemv.cu)
 enum GemvMode { GEMV_UP = 0, GEMV_DOWN = 2, GEMV_LEAF = 3 };
+constexpr int kSharedGemmNodes = 1024;  // shared layout: levels with at least this many nodes use the GEMM
 
 struct GemvArgs {
   int mode;
@@ -148,6 +155,9 @@ struct GemvArgs {
   const double* yadd; long long yadd_k, yadd_s;
   // split-K scratch
   double* part; unsigned* cnt;
+  // shared layout: the one-node panel is applied to `shared` nodes (virtual
+  // tiles = node x tile); 0 = per-node panels
+  int shared;
 };
 int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st);
 
@@ -157,6 +167,12 @@ int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, 
                const double* jump, long long ld_jump, double inv_dt, cudaStream_t st);
 int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u,
                  cudaStream_t st);
+
+// shared-layout level applies (dedup.cu)
+int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const double* Hc, long long Hc_k,
+                    long long Hc_s, const double* jump, long long ld_jump, double inv_dt, cudaStream_t st);
+int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
+                      cudaStream_t st);
 
 // solve entry (solve.cu)
 int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,

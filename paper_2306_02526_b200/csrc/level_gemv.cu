@@ -52,20 +52,20 @@ Panel make_panel_nodes(int c, int R, int C, int npn) {
 namespace {
 
 constexpr int NT = 256;
-// threads per launch: each keeps 2 batches of U=16 16-byte loads in flight,
-// so ~400 threads per SM cover HBM latency several times over
-constexpr int kTargetThreads = kNumSMs * 384;
+// threads per launch: ~1K threads per SM, each with up to 2 batches of U=8
+// 16-byte loads in flight, cover HBM latency under full load
+constexpr int kTargetThreads = kNumSMs * 1024;
 constexpr size_t kMaxStage = 64 * 1024;
 constexpr int kMaxSplit = 32;  // bounds the serial partial-sum tail of the last CTA
 
 }  // namespace
 
-PanelSplit panel_split(const Panel& pn, int k) {
+PanelSplit panel_split(const Panel& pn, int k, int vnodes) {
   PanelSplit s;
-  s.KM = k == 1 ? 1 : 4;
+  s.KM = k == 1 ? 1 : k <= 4 ? 4 : k <= 8 ? 8 : 16;
   s.kgroups = (int)cdiv(k, s.KM);
   s.nodes = (int)std::min<long long>(pn.c, (pn.TR - 1) / pn.R + 2);
-  long long base = (long long)pn.ntiles * s.kgroups;
+  long long base = (long long)pn.ntiles * vnodes * s.kgroups;
   int ns = (int)std::max<long long>(1, cdiv(kTargetThreads, base * (pn.TR / 2)));
   ns = std::min(ns, std::max(1, pn.C / 16));
   ns = std::min(ns, kMaxSplit);
@@ -78,8 +78,8 @@ PanelSplit panel_split(const Panel& pn, int k) {
   s.XS = xs(CK);
   s.smem = (size_t)s.nodes * s.KM * s.XS * 8;
   if (s.nsplit > 1) {
-    s.part_doubles = (size_t)s.kgroups * s.KM * s.nsplit * pn.ntiles * pn.TR;
-    s.counters = pn.ntiles * s.kgroups;
+    s.part_doubles = (size_t)s.kgroups * s.KM * s.nsplit * pn.ntiles * pn.TR * vnodes;
+    s.counters = pn.ntiles * vnodes * s.kgroups;
   }
   return s;
 }
@@ -129,7 +129,10 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
   extern __shared__ double xs[];
   __shared__ unsigned s_last;
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x / sp.nsplit, split = blockIdx.x % sp.nsplit;
+  const int vt = blockIdx.x / sp.nsplit, split = blockIdx.x % sp.nsplit;
+  // shared operator: virtual tile vt = (node, tile of the one-node panel)
+  const int vnode = a.shared ? vt / pn.ntiles : 0;
+  const int tile = a.shared ? vt % pn.ntiles : vt;
   const int kg0 = blockIdx.y * KM;
   const int R = pn.R, TR = pn.TR;
   const long long P = (long long)pn.c * R;
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
   // stage x chunks of the touched nodes: xs[(node*KM + kk)*XS + col]
   for (int e = tid; e < nn * KM * cw; e += blockDim.x) {
     const int col = e % cw, t2 = e / cw, kk = t2 % KM, nl = t2 / KM, kg = kg0 + kk;
-    xs[(nl * KM + kk) * XS + col] = kg < a.k ? xval<MODE>(a, n0 + nl, kg, c0 + col) : 0.0;
+    xs[(nl * KM + kk) * XS + col] = kg < a.k ? xval<MODE>(a, a.shared ? vnode : n0 + nl, kg, c0 + col) : 0.0;
   }
   __syncthreads();
 
@@ -165,17 +168,19 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
   stream_cols<KM, U>(A, M, cs, 0, cw, xs, na * KM * XS, nb * KM * XS, XS, acc0, acc1);
 
   if (sp.nsplit > 1) {
-    const long long Pp = (long long)pn.ntiles * TR;
+    const long long Pp = (long long)pn.ntiles * TR * (a.shared ? a.shared : 1);
+    const long long pv = pa + (long long)vnode * pn.ntiles * TR;  // row in the (virtual) row space
+    const size_t cidx = ((size_t)vnode * pn.ntiles + tile) * gridDim.y + blockIdx.y;
     double* part = a.part + ((long long)blockIdx.y * KM * sp.nsplit) * Pp;
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) {
       double2 v = make_double2(acc0[kk], acc1[kk]);
-      *reinterpret_cast<double2*>(part + ((long long)kk * sp.nsplit + split) * Pp + pa) = v;
+      *reinterpret_cast<double2*>(part + ((long long)kk * sp.nsplit + split) * Pp + pv) = v;
     }
     __threadfence();
     __syncthreads();
     if (tid == 0) {
-      unsigned old = atomicAdd(a.cnt + (size_t)tile * gridDim.y + blockIdx.y, 1u);
+      unsigned old = atomicAdd(a.cnt + cidx, 1u);
       s_last = (old == (unsigned)sp.nsplit - 1);
     }
     __syncthreads();
@@ -186,21 +191,22 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll 8
       for (int s = 0; s < sp.nsplit; ++s) {
-        double2 v = __ldcg(reinterpret_cast<const double2*>(part + ((long long)kk * sp.nsplit + s) * Pp + pa));
+        double2 v = __ldcg(reinterpret_cast<const double2*>(part + ((long long)kk * sp.nsplit + s) * Pp + pv));
         s0 += v.x;
         s1 += v.y;
       }
       acc0[kk] = s0;
       acc1[kk] = s1;
     }
-    if (tid == 0) a.cnt[(size_t)tile * gridDim.y + blockIdx.y] = 0u;
+    if (tid == 0) a.cnt[cidx] = 0u;
   }
 #pragma unroll
   for (int kk = 0; kk < KM; ++kk) {
     const int kg = kg0 + kk;
     if (kg >= a.k) continue;
-    if (pa < P) epilogue<MODE>(a, n0 + na, (int)(pa - (long long)(n0 + na) * R), kg, acc0[kk]);
-    if (pa + 1 < P) epilogue<MODE>(a, n0 + nb, (int)(pa + 1 - (long long)(n0 + nb) * R), kg, acc1[kk]);
+    const int ra = (int)(pa - (long long)(n0 + na) * R), rb = (int)(pa + 1 - (long long)(n0 + nb) * R);
+    if (pa < P) epilogue<MODE>(a, a.shared ? vnode : n0 + na, ra, kg, acc0[kk]);
+    if (pa + 1 < P) epilogue<MODE>(a, a.shared ? vnode : n0 + nb, rb, kg, acc1[kk]);
   }
 }
 
@@ -211,7 +217,7 @@ int launch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_
     cudaFuncSetAttribute(k_panel<MODE, KM, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxStage);
     attr_set = true;
   }
-  dim3 grid((unsigned)((long long)pn.ntiles * sp.nsplit), (unsigned)sp.kgroups);
+  dim3 grid((unsigned)((long long)pn.ntiles * sp.nsplit * (a.shared ? a.shared : 1)), (unsigned)sp.kgroups);
   HPSB_CUDA(launch_pdl(k_panel<MODE, KM, U>, grid, dim3(pn.TR / 2), sp.smem, st, a, pn, sp));
   HPSB_LAUNCH_CHECK();
   return 0;
@@ -219,8 +225,12 @@ int launch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_
 
 template <int MODE>
 int dispatch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_t st) {
-  if (sp.KM == 1) return launch<MODE, 1, 8>(a, pn, sp, st);
-  return launch<MODE, 4, 4>(a, pn, sp, st);
+  switch (sp.KM) {
+    case 1: return launch<MODE, 1, 8>(a, pn, sp, st);
+    case 4: return launch<MODE, 4, 4>(a, pn, sp, st);
+    case 8: return launch<MODE, 8, 4>(a, pn, sp, st);
+    default: return launch<MODE, 16, 2>(a, pn, sp, st);
+  }
 }
 
 __global__ void k_pack(const double* __restrict__ src1, long long s1, int ld1, int R1,
@@ -261,7 +271,7 @@ int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
     set_error("gemv: node-aligned panel passed to the level kernel");
     return -1;
   }
-  const PanelSplit sp = panel_split(pn, a.k);
+  const PanelSplit sp = panel_split(pn, a.k, a.shared ? a.shared : 1);
   if (sp.nsplit > 1 && (!a.part || !a.cnt)) {
     set_error("gemv: split-K needs workspace");
     return -1;

@@ -32,24 +32,31 @@ __global__ void k_leaf_gather(int k, int L, int nb, const int* __restrict__ lbg,
 
 }  // namespace
 
-// every panel a solve may launch, for sizing the split-K scratch
-static void solve_panels(const Plan& P, std::vector<Panel>& out) {
+// every panel a solve may launch (with its rhs multiplier), for sizing the
+// split-K scratch: per-node wide levels, and the shared layout's one-node
+// panels whose launches carry (nodes x rhs) right-hand sides
+static void solve_panels(const Plan& P, std::vector<std::pair<Panel, int>>& out) {
   out.clear();
-  out.push_back(make_panel(P.L, P.ni, P.ni));
-  out.push_back(make_panel(P.L, P.ni, P.nb));
+  out.push_back({make_panel(P.L, P.ni, P.ni), 1});
+  out.push_back({make_panel(P.L, P.ni, P.nb), 1});
+  for (const Level& lv : P.lv)
+    if (lv.c < kSharedGemmNodes) {
+      out.push_back({make_panel(1, lv.n3 + lv.n12, lv.n3), lv.c});
+      out.push_back({make_panel(1, lv.n3, lv.n12), lv.c});
+    }
   for (int d = 0; d < P.dF; ++d) {  // wide levels only; fused levels use no split-K
     const Level& lv = P.lv[d];
-    out.push_back(make_panel(lv.c, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3));
-    out.push_back(make_panel(lv.c, lv.n3, lv.n12));
+    out.push_back({make_panel(lv.c, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3), 1});
+    out.push_back({make_panel(lv.c, lv.n3, lv.n12), 1});
   }
 }
 
 static void scratch_sizes(const Plan& P, int k, size_t& part, size_t& cnt) {
-  std::vector<Panel> pns;
+  std::vector<std::pair<Panel, int>> pns;
   solve_panels(P, pns);
   part = 0; cnt = 0;
-  for (const Panel& pn : pns) {
-    PanelSplit sp = panel_split(pn, k);
+  for (const auto& pk : pns) {
+    PanelSplit sp = panel_split(pk.first, k, pk.second);
     part = std::max(part, sp.part_doubles);
     cnt = std::max(cnt, (size_t)sp.counters);
   }
@@ -162,11 +169,16 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
       const Level& lv = P.lv[d];
       const LevelOps& lo = ops.lo[d];
       const bool leafc = d == P.depth - 1;
+      const double* Hc = leafc ? Hleaf : ws.H[d + 1];
+      const long long Hc_k = leafc ? sh : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
+      const long long Hc_s = leafc ? hs : lv.nbc;
+      if (ops.shared_levels) {
+        if (int rc = shared_level_up(ops, ws, d, k, Hc, Hc_k, Hc_s, jump, ld_jump, inv_dt, st)) return rc;
+        continue;
+      }
       GemvArgs a{};
       a.k = k; a.part = ws.part; a.cnt = ws.cnt;
-      a.Hc = leafc ? Hleaf : ws.H[d + 1]; a.nbc = lv.nbc;
-      a.Hc_k = leafc ? sh : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
-      a.Hc_s = leafc ? hs : lv.nbc;
+      a.Hc = Hc; a.nbc = lv.nbc; a.Hc_k = Hc_k; a.Hc_s = Hc_s;
       a.W3 = ws.W3[d]; a.n3 = lv.n3; a.W3_k = (long long)lv.c * lv.n3;
       a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
       a.n12 = lv.n12;
@@ -181,6 +193,10 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
   for (int d = 0; d < P.dF; ++d) {
     const Level& lv = P.lv[d];
     const LevelOps& lo = ops.lo[d];
+    if (ops.shared_levels) {
+      if (int rc = shared_level_down(ops, ws, d, k, up, u, ld_u, st)) return rc;
+      continue;
+    }
     GemvArgs a{};
     a.mode = GEMV_DOWN; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
     a.u = u; a.u_k = ld_u; a.gidx = lv.gidx_bnd; a.j3 = lv.j3;

@@ -20,7 +20,7 @@ namespace hpsb {
 
 namespace {
 
-constexpr int NT = 256;
+constexpr int NT = 128;          // 512 subtree CTAs of 128 threads fit one wave on 148 SMs
 constexpr int MAXF = 10;          // fused levels
 constexpr int kMaxRows = 2048;    // operator rows of one CTA on one level
 constexpr int U = 4;
@@ -103,7 +103,7 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
 }
 
 template <int KM>
-__global__ void __launch_bounds__(NT, KM == 1 ? 3 : 1) k_sub_up(SubArgs a) {
+__global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_up(SubArgs a) {
   extern __shared__ double sm[];
   double* Hs = sm;                    // children's fluxes of the current level [child][KM][nbc]
   double* Hn = Hs + KM * a.hcap;      // this level's fluxes [node][KM][n12]
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 3 : 1) k_sub_up(SubArgs a) {
     }
     __syncthreads();
     // [w3; h - base] = [X33^-1; Tstack X33^-1] r3 for the subtree's nodes of this level
-    tile_apply<KM>(L.Up, b, r3s, n3, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM>(L.Up, L.Up.ntiles == 1 ? 0 : b, r3s, n3, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       if (row < n3) {
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
       xs[(j * KM + kk) * n12 + col] = kg < a.k ? a.u[kg * a.u_k + L.gidx[(long long)(node0 + j) * n12 + col]] : 0.0;
     }
     __syncthreads();
-    tile_apply<KM>(L.S, b, xs, n12, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM>(L.S, L.S.ntiles == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       const long long nd = (long long)(node0 + j) * n3 + row;
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
 // boundary is read from u once, every interface value this CTA produces is
 // kept (and written through to u) so lower levels gather from shared memory.
 template <int KM>
-__global__ void __launch_bounds__(NT, KM == 1 ? 3 : 1) k_sub_down_local(SubArgs a) {
+__global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_down_local(SubArgs a) {
   extern __shared__ double sm[];
   double* red = sm;                        // 2 * NT * KM
   double* uloc = sm + 2 * NT * KM;         // [KM][nslots]
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 3 : 1) k_sub_down_local(SubArgs 
       xs[(j * KM + kk) * n12 + col] = uloc[kk * ns + sl[j * n12 + col]];
     }
     __syncthreads();
-    tile_apply<KM>(L.S, b, xs, n12, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM>(L.S, L.S.ntiles == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       const long long nd = (long long)(node0 + j) * n3 + row;

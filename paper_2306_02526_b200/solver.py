@@ -11,6 +11,7 @@ result copied back; torch CUDA tensors stay on the device.
 
 import ctypes
 import hashlib
+import os
 import pickle
 
 import numpy as np
@@ -117,12 +118,13 @@ class HpsOperatorSet:
     safe (each stream gets its own workspace).
     """
 
-    def __init__(self, disc, sigma, dt_gamma, keep_dtn=False, threads=None):
+    def __init__(self, disc, sigma, dt_gamma, keep_dtn=False, threads=None, layout=None):
         self.disc = disc
         self.tree = disc.tree
         self.sigma = float(sigma)
         self.dt_gamma = float(dt_gamma)
         self.keep_dtn = bool(keep_dtn)
+        self.layout = resolve_layout(layout, disc.coeffs)
         st = disc.stencil
         self.D_bi = st.D_bnd[:, :st.ni]
         self.plan = device_plan(self.tree)
@@ -152,6 +154,7 @@ class HpsOperatorSet:
         d.has_c = int(cf.c is not None)
         d.D2x, d.D2y, d.D1x, d.D1y = (_lib.dbl_ptr(r) for r in rows)
         d.D_bnd = _lib.dbl_ptr(dbnd)
+        d.layout = _lib.LAYOUT_SHARED if self.layout == "shared" else _lib.LAYOUT_PER_NODE
         h = ctypes.c_void_p()
         rc = lib.hps_ops_build(self.plan.handle, ctypes.byref(d), current_stream_handle(),
                                ctypes.byref(h))
@@ -368,8 +371,27 @@ def coefficient_hash(disc):
     return h.hexdigest()
 
 
-def build(tree, coeffs, sigma=0.0, dt_gamma=1.0, disc=None, keep_dtn=False, threads=None):
+def resolve_layout(layout, coeffs):
+    """Operator storage: "per_node" streams one operator copy per node from
+    HBM every solve (the reference's storage, solver.py:137-151); "shared"
+    keeps one copy per level and runs the level applies as tensor-core GEMMs
+    (constant coefficients only).  None / "auto" picks "shared" when the
+    coefficients are constant; the environment variable HPSB_LAYOUT
+    overrides the automatic choice."""
+    if layout in (None, "auto"):
+        layout = os.environ.get("HPSB_LAYOUT", "auto")
+        if layout == "auto":
+            layout = "shared" if coeffs.is_constant else "per_node"
+    if layout not in ("per_node", "shared"):
+        raise ValueError(f"unknown operator layout {layout!r}")
+    if layout == "shared" and not coeffs.is_constant:
+        layout = "per_node"      # every node differs: nothing to share
+    return layout
+
+
+def build(tree, coeffs, sigma=0.0, dt_gamma=1.0, disc=None, keep_dtn=False, threads=None, layout=None):
     """Build the operator set for ``sigma*I + dt_gamma*A`` on the GPU."""
     if disc is None:
         disc = EllipticDiscretization(tree, coeffs)
-    return HpsOperatorSet(disc, sigma=sigma, dt_gamma=dt_gamma, keep_dtn=keep_dtn, threads=threads)
+    return HpsOperatorSet(disc, sigma=sigma, dt_gamma=dt_gamma, keep_dtn=keep_dtn, threads=threads,
+                          layout=layout)

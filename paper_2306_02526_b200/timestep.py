@@ -311,7 +311,8 @@ class TimeStepper:
     run on the GPU.  Same constructor, ``set_dt`` / ``shift`` / ``step`` /
     ``run`` / ``initial_state`` and exceptions."""
 
-    def __init__(self, tree, problem, tableau, dt, formulation="stage", disc=None, threads=None):
+    def __init__(self, tree, problem, tableau, dt, formulation="stage", disc=None, threads=None,
+                 layout=None):
         if formulation not in ("stage", "slope", "slope-penalized"):
             raise UnsupportedConfigurationError(f"unknown formulation {formulation!r}")
         self.tree = tree
@@ -321,6 +322,7 @@ class TimeStepper:
         self.penalized = formulation == "slope-penalized"
         self.disc = disc or EllipticDiscretization(tree, problem.coeffs)
         self.threads = threads
+        self.layout = layout
         self._step_count = 0
         if formulation != "stage":
             if not problem.is_linear and not problem.time_independent_bc:
@@ -365,9 +367,10 @@ class TimeStepper:
             return
         self.dt = float(dt)
         self.ops = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=self.dt * self.pair.gamma,
-                                  threads=self.threads)
+                                  threads=self.threads, layout=self.layout)
         if self.formulation != "stage" and self.ops_id is None:
-            self.ops_id = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=0.0, threads=self.threads)
+            self.ops_id = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=0.0, threads=self.threads,
+                                         layout=self.layout)
 
     def _check_ops(self):
         if self.ops is None or self.ops.dt_gamma != self.dt * self.pair.gamma \

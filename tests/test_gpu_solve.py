@@ -10,21 +10,22 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-10   # north-star parity bar: relative L2 per solve
 
 
-def _ops(z, name, keep_dtn=True):
+def _ops(z, name, keep_dtn=True, layout=None):
     import paper_2306_02526_b200 as hb
     fields, bounds = SOLVE_CASES[name]
     n1, n2, p = (int(v) for v in z["shape"])
     tree = hb.build_tree(bounds, n1, n2, p)
     coeffs = hb.OperatorCoefficients(**fields())
     ops = hb.build(tree, coeffs, sigma=float(z["sigma"]), dt_gamma=float(z["dt_gamma"]),
-                   keep_dtn=keep_dtn)
+                   keep_dtn=keep_dtn, layout=layout)
     return tree, ops
 
 
+@pytest.mark.parametrize("layout", ["per_node", "shared"])
 @pytest.mark.parametrize("name", sorted(SOLVE_CASES))
-def test_device_solve_matches_reference(golden, name):
+def test_device_solve_matches_reference(golden, name, layout):
     z = golden("solve_" + name)
-    tree, ops = _ops(z, name)
+    tree, ops = _ops(z, name, layout=layout)
     u = ops.solve_with_body_load(z["f"], z["g"])
     assert u.shape == z["u"].shape
     assert rel_l2(u, z["u"]) < TOL
@@ -35,10 +36,11 @@ def test_device_solve_matches_reference(golden, name):
         assert rel_l2(up, z["u_pen"]) < TOL
 
 
+@pytest.mark.parametrize("layout", ["per_node", "shared"])
 @pytest.mark.parametrize("name", sorted(SOLVE_CASES))
-def test_device_build_matches_reference(golden, name):
+def test_device_build_matches_reference(golden, name, layout):
     z = golden("solve_" + name)
-    tree, ops = _ops(z, name)
+    tree, ops = _ops(z, name, layout=layout)
     lo = ops.leaf_operators(0)
     assert rel_l2(lo.S, z["S_leaf0"]) < TOL
     assert rel_l2(lo.T, z["T_leaf0"]) < TOL
@@ -67,3 +69,16 @@ def test_device_singular_leaf_names_node():
     with pytest.raises(hb.SingularMatrixError) as exc:
         hb.build(tree, zero, sigma=0.0, dt_gamma=1.0)
     assert "leaf node" in str(exc.value)
+
+
+@pytest.mark.parametrize("layout", ["per_node", "shared"])
+def test_device_solve_is_bitwise_reproducible_and_multi_rhs_consistent(golden, layout):
+    """test_solver.py:255-273: repeated solves are bitwise equal; a stacked
+    multi-RHS solve equals the loop of single solves to 1e-14."""
+    z = golden("solve_heat4x4p12k3")
+    tree, ops = _ops(z, "heat4x4p12k3", keep_dtn=False, layout=layout)
+    a = ops.solve_with_body_load(z["f"], z["g"])
+    b = ops.solve_with_body_load(z["f"], z["g"])
+    assert np.array_equal(a, b)
+    loop = np.stack([ops.solve_with_body_load(z["f"][i], z["g"][i]) for i in range(3)])
+    assert rel_l2(a, loop) < 1e-14

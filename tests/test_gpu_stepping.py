@@ -30,7 +30,7 @@ def test_leaf_evaluations_match_reference(golden):
     assert rel_l2(disc.flux_jump(z["u"]), z["jump"]) < 1e-13
 
 
-def _c1_stepper(hb, separable):
+def _c1_stepper(hb, separable, layout=None):
     tree = hb.build_tree(UNIT, 8, 8, 12)
     phi, uex, q = heat_manufactured()
     if separable:
@@ -40,14 +40,14 @@ def _c1_stepper(hb, separable):
         qf, ff = q, uex
     prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0), q=qf, f=ff,
                                u0=lambda pts: uex(0.0, pts))
-    return tree, hb.TimeStepper(tree, prob, "ARK4", dt=1e-3), uex
+    return tree, hb.TimeStepper(tree, prob, "ARK4", dt=1e-3, layout=layout), uex
 
 
-@pytest.mark.parametrize("separable", [True, False])
-def test_c1_heat_matches_reference(golden, separable):
+@pytest.mark.parametrize("separable,layout", [(True, "shared"), (False, "shared"), (True, "per_node")])
+def test_c1_heat_matches_reference(golden, separable, layout):
     hb = _hb()
     z = golden("step_c1")
-    tree, st, uex = _c1_stepper(hb, separable)
+    tree, st, uex = _c1_stepper(hb, separable, layout)
     stages = []
     orig = st.ops.solve_device
 
