@@ -117,6 +117,22 @@ def solve_bytes(tree, k, const_leaf):
     return 8 * ops, 8 * k * vec
 
 
+def solve_bytes_shared(tree, k):
+    """HBM bytes of one stage solve with the shared (per-level) layout: one
+    operator pair per level, the shared leaf operators, and the vectors."""
+    ni, nb, L = tree.ni, tree.nb, tree.L
+    ops = (ni * ni + ni * nb) + nb * ni + ni * nb
+    vec = L * (2 * ni + 2 * nb)
+    for d, lm in enumerate(tree.level_maps):
+        n3, n12 = lm.n3, lm.n12
+        ops += n3 * n3 + n3 * n12 + (n12 * n3 if d > 0 else 0)
+        vec += lm.count * (3 * n12 + 2 * n3)
+    return 8 * ops, 8 * k * vec
+
+
+FP64_TFLOPS = 37.0   # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.txt)
+
+
 def solve_flops(tree, k):
     ni, nb, L = tree.ni, tree.nb, tree.L
     e = L * (ni * ni + 2 * ni * nb)
@@ -273,6 +289,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--layout", default=None, choices=[None, "auto", "per_node", "shared"],
+                    help="operator storage (default: shared for constant coefficients)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -294,7 +312,7 @@ def main():
     tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), cfg["n"], cfg["n"], cfg["p"])
     prob = hb.ParabolicProblem(**make_problem(hb, cfg))
     t0 = time.perf_counter()
-    st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"])
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"], layout=args.layout)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     k = cfg["k"]
@@ -357,13 +375,31 @@ def main():
     e2e_val = tree.N * k * 5 * e2e_steps / (e2e_ms * 1e-3) * world
     nbytes = uh.numel() * 8
 
-    # roofline of the stage solve
-    b_op, b_vec = solve_bytes(tree, k, prob.coeffs.is_constant)
+    # roofline of the stage solve: HBM bytes actually required by the layout
+    # in use vs FP64 work; the bound is whichever takes longer at its peak
+    layout = st.ops.layout
+    if layout == "shared":
+        b_op, b_vec = solve_bytes_shared(tree, k)
+    else:
+        b_op, b_vec = solve_bytes(tree, k, prob.coeffs.is_constant)
     avg_solve = statistics.mean(solve_ms)
-    achieved = (b_op + b_vec) / (avg_solve * 1e-3) / 1e9
     peak, src = peaks()
     flops = solve_flops(tree, k)
-    traffic = profiled_traffic(args.config)
+    t_hbm = (b_op + b_vec) / (peak * 1e9)
+    t_fp64 = flops / (FP64_TFLOPS * 1e12)
+    traffic = profiled_traffic(f"{args.config}/{layout}")
+    if t_hbm >= t_fp64:
+        roof = {"bound": "hbm", "achieved": (b_op + b_vec) / (avg_solve * 1e-3) / 1e9, "peak": peak,
+                "unit": "GB/s", "peak_source": src}
+    else:
+        roof = {"bound": "tensor", "achieved": flops / (avg_solve * 1e-3) / 1e12, "peak": FP64_TFLOPS,
+                "unit": "TFLOP/s", "peak_source": "measured FP64 DMMA (profiles/r01_fp64_peak.txt)"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof.update({"traffic": traffic, "kernel": "hps_solve (one stage solve: leaf GEMMs + level sweeps)",
+                 "layout": layout, "algorithmic_bytes_per_solve": b_op + b_vec,
+                 "gflops_per_solve": flops / 1e9, "solve_ms": avg_solve, "solves_timed": len(solve_ms),
+                 "frac_hbm": (b_op + b_vec) / (avg_solve * 1e-3) / (peak * 1e9),
+                 "frac_fp64": flops / (avg_solve * 1e-3) / (FP64_TFLOPS * 1e12)})
 
     if rank != 0:
         if world > 1:
@@ -382,17 +418,12 @@ def main():
         "config": {"workload": f"{args.config}: {cfg['n']}x{cfg['n']} leaves, p={cfg['p']}, "
                                f"{cfg['kind']}, ARK4 dt={cfg['dt']}, k={k}, one ARK4 step per "
                                f"bench step (5 stage solves)",
-                   "N_dof": tree.N, "parallelism": f"replicas x{world}",
+                   "N_dof": tree.N, "parallelism": f"replicas x{world}", "layout": layout,
                    "l2": "inputs larger than L2 (operators %.2f GB)" % (b_op / 1e9)},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                 "d2h_bytes_per_step": nbytes},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "hps_solve (level-batched GEMV sweep)",
-                     "algorithmic_bytes_per_solve": b_op + b_vec, "peak_source": src,
-                     "solve_ms": avg_solve, "solves_timed": len(solve_ms),
-                     "gflops_per_solve": flops / 1e9},
+        "roofline": roof,
         "clocks": clk.summary(),
         "build_s": build_s,
         "cpu_baseline": cpu,

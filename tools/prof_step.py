@@ -20,11 +20,12 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--solve-only", action="store_true")
+    ap.add_argument("--layout", default=None)
     a = ap.parse_args()
     cfg = bench.CONFIGS[a.config]
     tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), cfg["n"], cfg["n"], cfg["p"])
     prob = hb.ParabolicProblem(**bench.make_problem(hb, cfg))
-    st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"])
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"], layout=a.layout)
     s = st.initial_state()
     s = hb.StepperState(s.t, s.u_device)
     s = st.run(s, a.warmup)
