@@ -168,6 +168,11 @@ int hps_leaf_eval(const hps_disc* disc, int k, const double* u, long long ld_u, 
 int hps_combine(int k, long long n, int nterms, const double* coefs, const double* const* vecs,
                 const long long* lds, double* out, long long ld_out, double* guard, void* stream);
 
+/* As hps_combine with the coefficients read from device memory at run time
+ * (dcoefs[t]), so a captured CUDA graph replays with per-step coefficients. */
+int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const double* const* vecs,
+                    const long long* lds, double* out, long long ld_out, double* guard, void* stream);
+
 /* guard = max(guard, max |x|) over k rows of n values. */
 int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard, void* stream);
 

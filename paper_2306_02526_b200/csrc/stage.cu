@@ -327,6 +327,7 @@ struct CombineArgs {
   long long ld[MAXT];          // row stride of term m (0 = broadcast over rows)
   double* out; long long ld_out;
   unsigned long long* guard;
+  const double* dc;            // device coefficient table (graph replay), else c[]
 };
 
 __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
   const long long stride = (long long)gridDim.x * NT;
   for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < a.n; e += stride) {
     double s = 0.0;
-    for (int t = 0; t < a.nt; ++t) s = fma(a.c[t], __ldcs(a.v[t] + kk * a.ld[t] + e), s);
+    for (int t = 0; t < a.nt; ++t) s = fma(a.dc ? __ldg(a.dc + t) : a.c[t], __ldcs(a.v[t] + kk * a.ld[t] + e), s);
     a.out[kk * a.ld_out + e] = s;
     gacc(gmax, s);
   }
@@ -488,6 +489,20 @@ int hps_combine(int k, long long n, int nterms, const double* coefs, const doubl
   CombineArgs a{};
   a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out;
   for (int t = 0; t < nterms; ++t) { a.c[t] = coefs[t]; a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
+  a.guard = reinterpret_cast<unsigned long long*>(guard);
+  dim3 grid(stream_blocks(n), (unsigned)k);
+  k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  HPSB_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const double* const* vecs,
+                    const long long* lds, double* out, long long ld_out, double* guard, void* stream) {
+  if (k <= 0 || n <= 0) return HPS_OK;
+  if (nterms < 0 || nterms > MAXT) { set_error("hps_combine_dev: %d terms (max %d)", nterms, MAXT); return HPS_ERR_ARG; }
+  CombineArgs a{};
+  a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out; a.dc = dcoefs;
+  for (int t = 0; t < nterms; ++t) { a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
   a.guard = reinterpret_cast<unsigned long long*>(guard);
   dim3 grid(stream_blocks(n), (unsigned)k);
   k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);

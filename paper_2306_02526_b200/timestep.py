@@ -29,12 +29,13 @@ formulations (timestep.py:268-328) reuse the same device pieces.
 """
 
 import ctypes
+import os
 
 import numpy as np
 
 from . import _lib
 from .device import cuda_device, current_stream_handle, torch
-from .errors import DivergenceError, UnsupportedConfigurationError
+from .errors import DivergenceError, HpstepError, UnsupportedConfigurationError
 from .operators import EllipticDiscretization
 from .solver import HpsOperatorSet, device_plan
 from .tableaux import ButcherPair, load_tableau
@@ -214,20 +215,54 @@ def device_discretization(disc):
     return dd
 
 
+class _CoefSink:
+    """Coefficient table of one captured step.  While a step is captured into
+    a CUDA graph every ``combine`` takes its coefficients from a device table
+    (slots in call order) instead of kernel arguments; a *dry* pass of the same
+    step code recomputes the table for the next time level without launching
+    anything, and the host copies it in before each replay."""
+
+    current = None
+
+    def __init__(self, dev=None, dry=False):
+        self.vals, self.dev, self.dry = [], dev, dry
+
+    def take(self, vals):
+        off = len(self.vals)
+        self.vals.extend(vals)
+        if self.dry:
+            return None
+        if len(self.vals) > self.dev.numel():
+            raise HpstepError("coefficient table overflow")
+        return self.dev.data_ptr() + 8 * off
+
+
 def combine(terms, out, n=None, guard=None):
     """out[:, :n] = sum c * v over (coef, tensor) terms (rows broadcast when a
     term has a single row)."""
     lib = _lib.load()
-    terms = [(float(c), v) for c, v in terms if c != 0.0]
+    sink = _CoefSink.current
+    if sink is None:
+        terms = [(float(c), v) for c, v in terms if c != 0.0]
+    else:
+        terms = [(float(c), v) for c, v in terms]   # fixed slots: zeros may become nonzero later
     k = out.shape[0]
     n = out.shape[1] if n is None else n
     nt = len(terms)
-    coefs = (ctypes.c_double * max(1, nt))(*[c for c, _ in terms])
+    dptr = sink.take([c for c, _ in terms]) if sink is not None else None
+    if sink is not None and sink.dry:
+        return out
     vecs = (ctypes.c_void_p * max(1, nt))(*[v.data_ptr() for _, v in terms])
     lds = (ctypes.c_longlong * max(1, nt))(*[0 if v.shape[0] == 1 else v.stride(0)
                                               for _, v in terms])
-    rc = lib.hps_combine(k, n, nt, coefs, vecs, lds, out.data_ptr(), out.stride(0),
-                         None if guard is None else guard.data_ptr(), current_stream_handle())
+    gptr = None if guard is None else guard.data_ptr()
+    if sink is None:
+        coefs = (ctypes.c_double * max(1, nt))(*[c for c, _ in terms])
+        rc = lib.hps_combine(k, n, nt, coefs, vecs, lds, out.data_ptr(), out.stride(0), gptr,
+                             current_stream_handle())
+    else:
+        rc = lib.hps_combine_dev(k, n, nt, dptr, vecs, lds, out.data_ptr(), out.stride(0), gptr,
+                                 current_stream_handle())
     _lib.check(rc, "hps_combine")
     return out
 
@@ -254,6 +289,10 @@ def _call_g(g, t, U, ux, uy):
         try:
             r = g(t, U, ux, uy)
             if torch.is_tensor(r) and r.is_cuda:
+                try:
+                    g._hb_torch = True
+                except AttributeError:
+                    pass
                 return torch.broadcast_to(r.to(torch.float64), U.shape)
         except Exception:
             pass
@@ -268,6 +307,10 @@ def _call_g(g, t, U, ux, uy):
 # ---------------------------------------------------------------------------
 # the stepper
 # ---------------------------------------------------------------------------
+
+class _CaptureFailed(Exception):
+    pass
+
 
 class _Field:
     """Device evaluation of a field callable at a fixed point set."""
@@ -348,6 +391,9 @@ class TimeStepper:
                           self._dev)
         self._Q = _Field(problem.q, self._all_pts, k, self._dev)
         self._bufs = {}
+        self._dry = False          # dry pass: record combination coefficients only
+        self._graph = None         # captured CUDA graph of one step (see _run_graph)
+        self._graph_failed = False
         self.solve_timer = None
         self.dt = None
         self.ops = None
@@ -397,6 +443,8 @@ class TimeStepper:
         if self.problem.g is None:
             return None
         ux, uy = self._buf("gx", U.shape), self._buf("gy", U.shape)
+        if self._dry:
+            return ux
         self._dd.eval(U, ux=ux, uy=uy)
         r = _call_g(self.problem.g, t, U, ux, uy)
         if out is not None:
@@ -413,6 +461,11 @@ class TimeStepper:
     # -- stepping ------------------------------------------------------------------------
     def step(self, state):
         """Advance one step of size dt, returning a new state (timestep.py:211-224)."""
+        if self._graph_eligible():
+            try:
+                return self._run_graph(state, 1, check_every=1)
+            except _CaptureFailed:
+                pass
         new, guards = self._advance(state)
         self._raise_if_diverged(guards, self._step_count)
         self._step_count += 1
@@ -421,6 +474,16 @@ class TimeStepper:
     def run(self, state, nsteps, check_every=32):
         """``nsteps`` steps; the divergence guard is read back once per
         ``check_every`` steps (the first failing step is reported exactly)."""
+        g = self.problem.g
+        if nsteps > 1 and g is not None and getattr(g, "_hb_torch", None) is None and \
+                self._graph_eligible(probe=True):
+            state = self.step(state)           # one eager step probes g on device tensors
+            nsteps -= 1
+        if nsteps > 0 and self._graph_eligible():
+            try:
+                return self._run_graph(state, nsteps, check_every)
+            except _CaptureFailed:
+                pass
         pending = []
         for _ in range(nsteps):
             state, guards = self._advance(state)
@@ -429,6 +492,112 @@ class TimeStepper:
                 self._drain(pending)
         self._drain(pending)
         return state
+
+    # -- CUDA-graph stepping -------------------------------------------------------------
+    def _graph_eligible(self, probe=False):
+        """One step is captured once and replayed when every field is device
+        resident (SeparableField or None), g runs on device tensors (probed by
+        an eager step), and the formulation is the stage one or BE."""
+        if os.environ.get("HPSB_NO_GRAPH") == "1" or self.solve_timer is not None or self._graph_failed:
+            return False
+        if self.pair.s > 1 and self.formulation != "stage":
+            return False
+        for F in (self._F, self._Q):
+            if F.fn is not None and F.sep is None:
+                return False
+        g = self.problem.g
+        return g is None or probe or getattr(g, "_hb_torch", None) is True
+
+    def _step_body(self, t, u, guards, out):
+        if self.pair.s == 1:
+            return self._step_backward_euler(t, u, guards, out=out)
+        return self._step_stage(t, u, guards, out=out)
+
+    def _dry_coefs(self, t, u, guards):
+        self._dry, _CoefSink.current = True, _CoefSink(dry=True)
+        try:
+            self._step_body(t, u, guards, u)
+            return _CoefSink.current.vals
+        finally:
+            self._dry, _CoefSink.current = False, None
+
+    def _capture(self, t, gin):
+        s, dev = self.pair.s, self._dev
+        guards = torch.zeros(s, dtype=torch.float64, device=dev)
+        vals = self._dry_coefs(t, gin, guards)
+        coef = torch.zeros(len(vals) + 8, dtype=torch.float64, device=dev)
+        coef[:len(vals)] = torch.as_tensor(vals, dtype=torch.float64)
+        # warm the captured code path once (kernel attributes, workspaces) on scratch data
+        scratch = gin.clone()
+        _CoefSink.current = _CoefSink(dev=coef)
+        try:
+            self._step_body(t, scratch, guards, scratch)
+        finally:
+            _CoefSink.current = None
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            _CoefSink.current = _CoefSink(dev=coef)
+            try:
+                guards.zero_()
+                self._step_body(t, gin, guards, gin)
+            finally:
+                _CoefSink.current = None
+        ring = 4
+        self._graph = dict(graph=graph, gin=gin, guards=guards, coef=coef, ncoef=len(vals), key=self._graph_key(gin),
+                           pinned=[torch.zeros(len(vals) + 8, dtype=torch.float64).pin_memory() for _ in range(ring)],
+                           events=[None] * ring, slot=0)
+
+    def _graph_key(self, u):
+        return (tuple(u.shape), self.dt, id(self.ops))
+
+    def _run_graph(self, state, nsteps, check_every):
+        self._check_ops()
+        src = state.u_device
+        squeeze = src.dim() == 1
+        src = torch.atleast_2d(src).to(torch.float64)
+        G = self._graph
+        if G is None or G["key"] != self._graph_key(src):
+            self._graph = None
+            try:
+                self._capture(state.t, src.clone())
+            except Exception as e:  # e.g. an op in g that cannot be captured
+                self._graph, self._graph_failed = None, True
+                torch.cuda.synchronize()
+                raise _CaptureFailed(str(e)) from e
+            G = self._graph
+        gin, guards, coef = G["gin"], G["guards"], G["coef"]
+        if src.data_ptr() != gin.data_ptr():
+            gin.copy_(src)
+        hist = torch.empty((max(1, min(check_every, nsteps)), guards.numel()), dtype=torch.float64,
+                           device=self._dev)
+        t = state.t
+        done = 0
+        for step in range(nsteps):
+            vals = self._dry_coefs(t, gin, guards)
+            if len(vals) != G["ncoef"]:
+                raise HpstepError("captured step and coefficient pass disagree")
+            slot = G["slot"]
+            G["slot"] = (slot + 1) % len(G["pinned"])
+            if G["events"][slot] is not None:
+                G["events"][slot].synchronize()      # the copy that last read this buffer is done
+            buf = G["pinned"][slot]
+            buf[:len(vals)] = torch.as_tensor(vals, dtype=torch.float64)
+            coef.copy_(buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            G["events"][slot] = ev
+            G["graph"].replay()
+            hist[(step - done) % hist.shape[0]].copy_(guards)
+            t += self.dt
+            if step + 1 - done == hist.shape[0] or step + 1 == nsteps:
+                host = hist[:step + 1 - done].cpu().numpy()
+                for g in host:
+                    self._raise_if_diverged(g, self._step_count, host_vals=True)
+                    self._step_count += 1
+                done = step + 1
+        u = gin.clone()
+        return StepperState(t, u[0] if squeeze else u)
 
     def _drain(self, pending):
         if not pending:
@@ -466,7 +635,27 @@ class TimeStepper:
             unew = self._step_slope(state.t, u, guards)
         return StepperState(state.t + self.dt, unew[0] if squeeze else unew), guards
 
+    # device work of a step, skipped on a dry pass
+    def _eval(self, U, **kw):
+        if not self._dry:
+            self._dd.eval(U, **kw)
+
+    def _maxabs(self, x, guard):
+        if not self._dry:
+            k, n = x.shape
+            _lib.check(_lib.load().hps_maxabs(k, n, x.data_ptr(), x.stride(0), guard.data_ptr(),
+                                              current_stream_handle()), "hps_maxabs")
+
+    def _put_boundary(self, fb, u):
+        if not self._dry:
+            _lib.check(_lib.load().hps_put_boundary(self._plan.handle, u.shape[0], fb.data_ptr(),
+                                                    0 if fb.shape[0] == 1 else fb.stride(0),
+                                                    u.data_ptr(), u.stride(0), current_stream_handle()),
+                       "hps_put_boundary")
+
     def _solve(self, ops, fb, body, out, jump=None, inv_dt=None):
+        if self._dry:
+            return out
         tm = self.solve_timer
         if tm is not None:                      # bench hook: CUDA events around each solve
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -477,7 +666,7 @@ class TimeStepper:
             tm.append((e0, e1))
         return out
 
-    def _step_backward_euler(self, t, u, guards):
+    def _step_backward_euler(self, t, u, guards, out=None):
         dt, k, N = self.dt, u.shape[0], self.tree.N
         t1 = t + dt
         r = self._buf("r", (k, self._dd.Lni))
@@ -486,13 +675,12 @@ class TimeStepper:
         if G is not None:
             terms.append((dt, G))
         combine(terms, r, n=self._dd.Lni)
-        unew = torch.empty((k, N), dtype=torch.float64, device=self._dev)
+        unew = torch.empty((k, N), dtype=torch.float64, device=self._dev) if out is None else out
         self._solve(self.ops, self._bc(t1), r, unew)
-        _lib.check(_lib.load().hps_maxabs(k, N, unew.data_ptr(), N, guards[0].data_ptr(),
-                                          current_stream_handle()), "hps_maxabs")
+        self._maxabs(unew, guards[0])
         return unew
 
-    def _step_stage(self, t, u, guards):
+    def _step_stage(self, t, u, guards, out=None):
         """timestep.py:237-266 on the device."""
         pair, dt = self.pair, self.dt
         s, k, N, Lni = pair.s, u.shape[0], self.tree.N, self._dd.Lni
@@ -516,10 +704,10 @@ class TimeStepper:
                     terms.append((1.0, G))
                 if terms:
                     combine(terms, QG[i])
-                else:
+                elif not self._dry:
                     QG[i].zero_()
 
-        self._dd.eval(u, lu_int=Lu[0])
+        self._eval(u, lu_int=Lu[0])
         stage_q_g(0, t + pair.c[0] * dt, u)
         ui = u
         for i in range(1, s):
@@ -535,10 +723,9 @@ class TimeStepper:
             ui = U[i & 1]
             self._solve(self.ops, self._bc(ti), r, ui)
             if i < s - 1:
-                self._dd.eval(ui, lu_int=Lu[i], guard=guards[i - 1])
+                self._eval(ui, lu_int=Lu[i], guard=guards[i - 1])
             else:
-                _lib.check(_lib.load().hps_maxabs(k, N, ui.data_ptr(), N, guards[i - 1].data_ptr(),
-                                                  current_stream_handle()), "hps_maxabs")
+                self._maxabs(ui, guards[i - 1])
             stage_q_g(i, ti, ui)
         w = pair.bhat - Ah[s - 1]
         terms = [(1.0, ui)]
@@ -547,15 +734,11 @@ class TimeStepper:
         if qsep is not None:
             for m, phi in enumerate(qsep):
                 terms.append((sum(dt * w[j] * qfac[j][m] for j in range(s)), phi))
-        unew = torch.empty((k, N), dtype=torch.float64, device=self._dev)
+        # `out` may alias `u`: nothing below reads u
+        unew = torch.empty((k, N), dtype=torch.float64, device=self._dev) if out is None else out
         combine(terms, unew)
-        fb = self._bc(t + dt)
-        lib = _lib.load()
-        _lib.check(lib.hps_put_boundary(self._plan.handle, k, fb.data_ptr(),
-                                        0 if fb.shape[0] == 1 else fb.stride(0), unew.data_ptr(), N,
-                                        current_stream_handle()), "hps_put_boundary")
-        _lib.check(lib.hps_maxabs(k, N, unew.data_ptr(), N, guards[s - 1].data_ptr(),
-                                  current_stream_handle()), "hps_maxabs")
+        self._put_boundary(self._bc(t + dt), unew)
+        self._maxabs(unew, guards[s - 1])
         return unew
 
     # -- slope formulations (timestep.py:268-328) ----------------------------------------

@@ -44,10 +44,11 @@ def _c1_stepper(hb, separable, layout=None):
 
 
 @pytest.mark.parametrize("separable,layout", [(True, "shared"), (False, "shared"), (True, "per_node")])
-def test_c1_heat_matches_reference(golden, separable, layout):
+def test_c1_heat_matches_reference(golden, separable, layout, monkeypatch):
     hb = _hb()
     z = golden("step_c1")
     tree, st, uex = _c1_stepper(hb, separable, layout)
+    monkeypatch.setenv("HPSB_NO_GRAPH", "1")      # eager first step: record every stage solve
     stages = []
     orig = st.ops.solve_device
 
@@ -59,6 +60,7 @@ def test_c1_heat_matches_reference(golden, separable, layout):
     st.ops.solve_device = rec
     s = st.step(st.initial_state())
     st.ops.solve_device = orig
+    monkeypatch.delenv("HPSB_NO_GRAPH")           # the rest runs as replays of a captured step
     for i, (a, b) in enumerate(zip(stages, z["stages"])):
         assert rel_l2(a, b) < TOL, f"stage {i + 1}"
     assert isinstance(s.u, np.ndarray) and s.u.shape == (tree.N,)
@@ -179,3 +181,42 @@ def test_mismatched_shift_is_rejected():
         st.step(st.initial_state())
     st.set_dt(5e-3)
     st.step(st.initial_state())
+
+
+@pytest.mark.parametrize("layout", ["shared", "per_node"])
+def test_graph_replay_matches_eager_stepping(monkeypatch, layout):
+    """A captured step replayed with per-step coefficient tables gives the
+    same trajectory as eager launches (same kernels, same coefficients)."""
+    hb = _hb()
+    tree, st_g, uex = _c1_stepper(hb, True, layout)
+    s_g = st_g.run(st_g.initial_state(), 12, check_every=5)
+    assert st_g._graph is not None
+    monkeypatch.setenv("HPSB_NO_GRAPH", "1")
+    tree, st_e, _ = _c1_stepper(hb, True, layout)
+    s_e = st_e.run(st_e.initial_state(), 12)
+    assert abs(s_g.t - s_e.t) < 1e-15
+    assert rel_l2(s_g.u, s_e.u) < 1e-15
+    assert st_g._step_count == st_e._step_count == 12
+
+
+def test_graph_replay_nonlinear_and_backward_euler(golden):
+    hb = _hb()
+    z = golden("step_allen_cahn")
+    tree = hb.build_tree(UNIT, 8, 8, 12)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=0.01, c22=0.01),
+                               g=lambda t, u, ux, uy: u - u ** 3,
+                               u0=lambda pts: sine_field(z["modes"], pts), time_independent_bc=True)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=float(z["dt"]))
+    s = st.run(st.initial_state(), 10)          # 1 eager probe step, 9 replays
+    assert st._graph is not None
+    assert rel_l2(s.u, z["u10"]) < TOL
+    zb = golden("step_be")
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**lap_fields()),
+                               q=hb.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t)),
+                               f=hb.SeparableField.product(phi, np.cos), u0=lambda pts: uex(0.0, pts))
+    st = hb.TimeStepper(tree, prob, "BE", dt=float(zb["dt"]))
+    s = st.run(st.initial_state(), 3)
+    assert st._graph is not None
+    assert rel_l2(s.u, zb["u3"]) < TOL
