@@ -113,6 +113,14 @@ size_t hps_ops_device_bytes(const hps_ops* ops);
 int hps_ops_get_leaf(const hps_ops* ops, int which, int leaf, double* host_out);
 int hps_ops_get_merge(const hps_ops* ops, int level, int node, int which, double* host_out);
 
+/* Operator-set persistence (HpsOperatorSet.save / .load, solver.py:294-337):
+ * hps_ops_dump writes the operator set into a host buffer of
+ * hps_ops_dump_size(ops) bytes; hps_ops_load rebuilds it on the device for a
+ * plan of the same tree (no build). */
+long long hps_ops_dump_size(const hps_ops* ops);
+int hps_ops_dump(const hps_ops* ops, void* host, long long size);
+int hps_ops_load(const hps_plan* plan, const void* host, long long size, hps_ops** out);
+
 size_t hps_solve_workspace_bytes(const hps_plan* plan, int k);
 
 /* HpsOperatorSet._solve (solver.py:201-276) for k stacked right-hand sides:

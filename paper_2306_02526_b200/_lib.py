@@ -82,6 +82,10 @@ SIGNATURES = {
     "hps_ops_get_leaf": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_double_p]),
     "hps_ops_get_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          c_double_p]),
+    "hps_ops_dump_size": (ctypes.c_longlong, [ctypes.c_void_p]),
+    "hps_ops_dump": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]),
+    "hps_ops_load": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,
+                                    ctypes.POINTER(ctypes.c_void_p)]),
     "hps_solve_workspace_bytes": (ctypes.c_size_t, [ctypes.c_void_p, ctypes.c_int]),
     "hps_solve": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong,
                                  ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p,

@@ -208,6 +208,7 @@ static double* ops_alloc(Ops& O, size_t doubles, bool zero) {
   if (cudaMalloc(&p, doubles * 8) != cudaSuccess) return nullptr;
   if (zero) cudaMemset(p, 0, doubles * 8);
   O.allocs.push_back(p);
+  O.alloc_bytes.push_back(doubles * 8);
   O.bytes += doubles * 8;
   return p;
 }
@@ -550,6 +551,182 @@ int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const d
               size_t ws_bytes, void* stream) {
   if (!h || !fb || !u || !ws) { set_error("hps_solve: null argument"); return HPS_ERR_ARG; }
   return solve(h->O, k, fb, ld_f, g, ld_g, jump, ld_jump, inv_dt, u, ld_u, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Operator-set persistence (solver.py:294-337): the device buffers and the
+// structure that points into them, as one flat host byte stream.  Pointers are
+// stored as indices of the owning allocation.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr unsigned long long kDumpMagic = 0x31425350484244ULL;  // "DBHPSB1"
+
+struct Writer {
+  std::vector<unsigned char>* out;
+  template <class T>
+  void put(const T& v) {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+    out->insert(out->end(), p, p + sizeof(T));
+  }
+};
+
+struct Reader {
+  const unsigned char* p;
+  size_t left;
+  bool ok = true;
+  template <class T>
+  T get() {
+    T v{};
+    if (left < sizeof(T)) { ok = false; return v; }
+    memcpy(&v, p, sizeof(T));
+    p += sizeof(T);
+    left -= sizeof(T);
+    return v;
+  }
+};
+
+long long alloc_index(const Ops& O, const void* ptr) {
+  if (!ptr) return -1;
+  for (size_t i = 0; i < O.allocs.size(); ++i)
+    if (O.allocs[i] == ptr) return (long long)i;
+  return -2;
+}
+
+void put_panel(Writer& w, const Ops& O, const Panel& pn) {
+  w.put(pn.c); w.put(pn.R); w.put(pn.C); w.put(pn.TR); w.put(pn.TS); w.put(pn.ntiles);
+  w.put(alloc_index(O, pn.base));
+}
+
+void get_panel(Reader& r, Panel& pn, long long& idx) {
+  pn.c = r.get<int>(); pn.R = r.get<int>(); pn.C = r.get<int>(); pn.TR = r.get<int>(); pn.TS = r.get<int>();
+  pn.ntiles = r.get<int>();
+  idx = r.get<long long>();
+}
+
+// the structure (everything but the raw buffers)
+bool write_structure(const Ops& O, Writer& w) {
+  const Plan& P = *O.plan;
+  w.put(kDumpMagic);
+  w.put(O.sigma); w.put(O.dtg); w.put(O.shared_leaf); w.put(O.shared_levels); w.put(O.Lc);
+  w.put(P.depth); w.put(P.L); w.put(P.ni); w.put(P.nb); w.put(P.N);
+  std::vector<long long> ptrs = {alloc_index(O, O.Ainv), alloc_index(O, O.S_leaf), alloc_index(O, O.T_leaf),
+                                 alloc_index(O, O.D_bi), alloc_index(O, O.root_T), alloc_index(O, O.root_Tst)};
+  for (long long i : ptrs) { if (i == -2) return false; w.put(i); }
+  put_panel(w, O, O.pAinv);
+  put_panel(w, O, O.pSleaf);
+  for (const LevelOps& lo : O.lo) {
+    put_panel(w, O, lo.Up);
+    put_panel(w, O, lo.S);
+    for (const void* q : {(const void*)lo.Ush, (const void*)lo.Ssh, (const void*)lo.T}) {
+      long long i = alloc_index(O, q);
+      if (i == -2) return false;
+      w.put(i);
+    }
+  }
+  w.put((long long)O.allocs.size());
+  for (size_t b : O.alloc_bytes) w.put((unsigned long long)b);
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+long long hps_ops_dump_size(const hps_ops* h) {
+  if (!h) return -1;
+  std::vector<unsigned char> head;
+  Writer w{&head};
+  if (!write_structure(h->O, w)) return -1;
+  size_t n = head.size();
+  for (size_t b : h->O.alloc_bytes) n += b;
+  return (long long)n;
+}
+
+int hps_ops_dump(const hps_ops* h, void* host, long long size) {
+  if (!h || !host) { set_error("hps_ops_dump: null argument"); return HPS_ERR_ARG; }
+  std::vector<unsigned char> head;
+  Writer w{&head};
+  if (!write_structure(h->O, w)) { set_error("hps_ops_dump: unowned operator pointer"); return HPS_ERR_ARG; }
+  if (size < hps_ops_dump_size(h)) { set_error("hps_ops_dump: buffer too small"); return HPS_ERR_ARG; }
+  unsigned char* dst = (unsigned char*)host;
+  memcpy(dst, head.data(), head.size());
+  dst += head.size();
+  HPSB_CUDA(cudaDeviceSynchronize());
+  for (size_t i = 0; i < h->O.allocs.size(); ++i) {
+    HPSB_CUDA(cudaMemcpy(dst, h->O.allocs[i], h->O.alloc_bytes[i], cudaMemcpyDeviceToHost));
+    dst += h->O.alloc_bytes[i];
+  }
+  return HPS_OK;
+}
+
+int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops** out) {
+  *out = nullptr;
+  if (!hp || !host) { set_error("hps_ops_load: null argument"); return HPS_ERR_ARG; }
+  const Plan& P = hp->P;
+  Reader r{(const unsigned char*)host, (size_t)size};
+  if (r.get<unsigned long long>() != kDumpMagic) { set_error("hps_ops_load: not an operator dump"); return HPS_ERR_ARG; }
+  hps_ops* h = new hps_ops();
+  Ops& O = h->O;
+  O.plan = const_cast<Plan*>(&P);
+  O.sigma = r.get<double>(); O.dtg = r.get<double>(); O.shared_leaf = r.get<int>();
+  O.shared_levels = r.get<int>(); O.Lc = r.get<int>();
+  const int depth = r.get<int>(), L = r.get<int>(), ni = r.get<int>(), nb = r.get<int>();
+  const long long N = r.get<long long>();
+  if (!r.ok || depth != P.depth || L != P.L || ni != P.ni || nb != P.nb || N != P.N) {
+    delete h;
+    set_error("hps_ops_load: dump was made for a different tree");
+    return HPS_ERR_ARG;
+  }
+  long long ptr[6];
+  for (long long& i : ptr) i = r.get<long long>();
+  long long iA, iS;
+  get_panel(r, O.pAinv, iA);
+  get_panel(r, O.pSleaf, iS);
+  O.lo.resize(depth);
+  std::vector<long long> lidx((size_t)depth * 5);
+  for (int d = 0; d < depth; ++d) {
+    get_panel(r, O.lo[d].Up, lidx[5 * d]);
+    get_panel(r, O.lo[d].S, lidx[5 * d + 1]);
+    for (int j = 2; j < 5; ++j) lidx[5 * d + j] = r.get<long long>();
+  }
+  const long long na = r.get<long long>();
+  std::vector<size_t> sizes;
+  for (long long i = 0; i < na && r.ok; ++i) sizes.push_back((size_t)r.get<unsigned long long>());
+  size_t need = 0;
+  for (size_t b : sizes) need += b;
+  if (!r.ok || r.left < need) { delete h; set_error("hps_ops_load: truncated dump"); return HPS_ERR_ARG; }
+  for (size_t b : sizes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, b ? b : 8) != cudaSuccess) {
+      hps_ops_destroy(h);
+      set_error("hps_ops_load: out of device memory");
+      return HPS_ERR_CUDA;
+    }
+    O.allocs.push_back(p);
+    O.alloc_bytes.push_back(b);
+    O.bytes += b;
+    if (cudaMemcpy(p, r.p, b, cudaMemcpyHostToDevice) != cudaSuccess) {
+      hps_ops_destroy(h);
+      set_error("hps_ops_load: copy failed");
+      return HPS_ERR_CUDA;
+    }
+    r.p += b;
+    r.left -= b;
+  }
+  auto at = [&](long long i) -> double* { return i >= 0 && i < na ? (double*)O.allocs[(size_t)i] : nullptr; };
+  O.Ainv = at(ptr[0]); O.S_leaf = at(ptr[1]); O.T_leaf = at(ptr[2]); O.D_bi = at(ptr[3]);
+  O.root_T = at(ptr[4]); O.root_Tst = at(ptr[5]);
+  O.pAinv.base = at(iA); O.pSleaf.base = at(iS);
+  for (int d = 0; d < depth; ++d) {
+    LevelOps& lo = O.lo[d];
+    lo.Up.base = at(lidx[5 * d]); lo.S.base = at(lidx[5 * d + 1]);
+    lo.Ush = at(lidx[5 * d + 2]); lo.Ssh = at(lidx[5 * d + 3]); lo.T = at(lidx[5 * d + 4]);
+  }
+  *out = h;
+  return HPS_OK;
 }
 
 }  // extern "C"

@@ -113,6 +113,7 @@ struct Ops {
   double* root_Tst = nullptr;  // root Tstack, n12 x ld3 row-major (test hooks only)
   size_t bytes = 0;            // device bytes owned
   std::vector<void*> allocs;
+  std::vector<size_t> alloc_bytes;
 };
 
 int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st);

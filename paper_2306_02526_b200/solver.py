@@ -11,8 +11,8 @@ result copied back; torch CUDA tensors stay on the device.
 
 import ctypes
 import hashlib
+import json
 import os
-import pickle
 
 import numpy as np
 
@@ -331,6 +331,54 @@ class HpsOperatorSet:
         return self._merge_block(0, 0, 3) if self.tree.depth > 0 else None
 
     # -- persistence (reference solver.py:280-337) -----------------------------------
+    _DUMP_MAGIC = b"HPSB200OPS\n"
+
+    def save(self, path):
+        """Binary dump so repeated runs can skip the build (solver.py:294-306):
+        the versioned header, then the device operator set."""
+        lib = self._lib
+        n = int(lib.hps_ops_dump_size(self.handle))
+        if n < 0:
+            raise HpstepError("hps_ops_dump_size failed: " + _lib.last_error())
+        buf = np.empty(n, dtype=np.uint8)
+        _lib.check(lib.hps_ops_dump(self.handle, buf.ctypes.data_as(ctypes.c_void_p), n), "hps_ops_dump")
+        head = json.dumps({"header": _jsonable(self.header()), "layout": self.layout,
+                           "keep_dtn": self.keep_dtn}).encode()
+        with open(path, "wb") as fh:
+            fh.write(self._DUMP_MAGIC)
+            fh.write(len(head).to_bytes(8, "little"))
+            fh.write(head)
+            fh.write(buf.tobytes())
+
+    @classmethod
+    def load(cls, path, disc, sigma, dt_gamma):
+        """Load a dumped operator set, validating the versioned header
+        (solver.py:308-337): a dump made for another tree, coefficient field or
+        shift raises HpstepError."""
+        obj = cls.__new__(cls)
+        obj.disc, obj.tree = disc, disc.tree
+        obj.sigma, obj.dt_gamma = float(sigma), float(dt_gamma)
+        st = disc.stencil
+        obj.D_bi = st.D_bnd[:, :st.ni]
+        with open(path, "rb") as fh:
+            if fh.read(len(cls._DUMP_MAGIC)) != cls._DUMP_MAGIC:
+                raise HpstepError(f"{path} is not an operator dump of this package")
+            n = int.from_bytes(fh.read(8), "little")
+            meta = json.loads(fh.read(n).decode())
+            payload = np.frombuffer(fh.read(), dtype=np.uint8)
+        if meta["header"] != _jsonable(obj.header()):
+            raise HpstepError("operator dump does not match the requested configuration "
+                              f"(dump header {meta['header']})")
+        obj.layout, obj.keep_dtn = meta["layout"], bool(meta["keep_dtn"])
+        obj.plan = device_plan(obj.tree)
+        lib = obj.plan._lib
+        h = ctypes.c_void_p()
+        _lib.check(lib.hps_ops_load(obj.plan.handle, payload.ctypes.data_as(ctypes.c_void_p), payload.size,
+                                    ctypes.byref(h)), "hps_ops_load")
+        obj.handle, obj._lib = h, lib
+        obj.parent_order = [int(i) for lm in obj.tree.level_maps for i in lm.node_index]
+        return obj
+
     def header(self):
         tree = self.tree
         return {"version": FORMAT_VERSION, "dim": tree.dim, "bounds": tree.bounds, "n1": tree.n1,
@@ -356,6 +404,14 @@ class _LeafFactors:
 
     def __getitem__(self, i):
         return _InverseFactor(self._ops._leaf_block(0, i))
+
+
+def _jsonable(v):
+    if isinstance(v, dict):
+        return {k: _jsonable(x) for k, x in v.items()}
+    if isinstance(v, (list, tuple)):
+        return [_jsonable(x) for x in v]
+    return v
 
 
 def coefficient_hash(disc):

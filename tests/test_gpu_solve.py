@@ -82,3 +82,22 @@ def test_device_solve_is_bitwise_reproducible_and_multi_rhs_consistent(golden, l
     assert np.array_equal(a, b)
     loop = np.stack([ops.solve_with_body_load(z["f"][i], z["g"][i]) for i in range(3)])
     assert rel_l2(a, loop) < 1e-14
+
+
+@pytest.mark.parametrize("layout", ["per_node", "shared"])
+def test_operator_set_save_load_roundtrip(golden, tmp_path, layout):
+    """solver.py:294-337: a dumped operator set reloads without a build, solves
+    bitwise identically, and refuses a mismatched configuration."""
+    import paper_2306_02526_b200 as hb
+    z = golden("solve_c4var4x4p10" if layout == "per_node" else "solve_heat4x4p12k3")
+    name = "c4var4x4p10" if layout == "per_node" else "heat4x4p12k3"
+    tree, ops = _ops(z, name, keep_dtn=False, layout=layout)
+    path = tmp_path / "ops.bin"
+    ops.save(str(path))
+    ops2 = hb.HpsOperatorSet.load(str(path), ops.disc, ops.sigma, ops.dt_gamma)
+    a = ops.solve_with_body_load(z["f"], z["g"])
+    b = ops2.solve_with_body_load(z["f"], z["g"])
+    assert np.array_equal(a, b)
+    assert rel_l2(b, z["u"]) < TOL
+    with pytest.raises(hb.HpstepError):
+        hb.HpsOperatorSet.load(str(path), ops.disc, ops.sigma, 2 * ops.dt_gamma)
