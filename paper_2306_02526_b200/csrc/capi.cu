@@ -369,10 +369,9 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     double* R = talloc((size_t)ce * n3 * n12);
     double* lst = talloc(2 * (size_t)ce);
     const int nup = n3 + (l > 0 ? n12 : 0);
-    if (O.shared_levels && l >= P.dF) {  // fused levels: ONE node-aligned tile read by every subtree CTA
-      const int npn = 1 << (l - P.dF);
-      lo.Up = make_panel_nodes(npn, nup, n3, npn);
-      lo.S = make_panel_nodes(npn, n3, n12, npn);
+    if (O.shared_levels && l >= P.dF) {  // fused levels: ONE one-node tile read by every subtree CTA
+      lo.Up = make_panel_nodes(1, nup, n3, 1);
+      lo.S = make_panel_nodes(1, n3, n12, 1);
     } else if (O.shared_levels) {  // wide levels: one-node panels (or GEMM operands only)
       if (lv.c < kSharedGemmNodes) {
         lo.Up = make_panel(1, nup, n3);

@@ -48,25 +48,40 @@ struct SubArgs {
 
 // y(row) = sum_col M[col][row] x[node(row)][col] over the CTA's tile, then
 // out(j, row, kk, y) for every valid row; x is [node][KM][C] in shared memory.
-// When the tile has fewer row pairs than the CTA has threads, G threads share
-// a row pair, each streaming a contiguous column block; their partial sums
-// meet in shared memory (red, 2*NT*KM doubles) and are added in block order.
+// vn > 1: the tile holds ONE node's operator shared by vn nodes (shared
+// layout), row pair q = (node q / pairs, pair q % pairs).
+// When there are fewer row pairs than threads, G threads share a row pair,
+// each streaming a contiguous column block; their partial sums meet in shared
+// memory (red, 2*NT*KM doubles) and are added in block order.
 template <int KM, class Out>
 __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const double* xs, int xstride, double* red,
-                                           Out out) {
+                                           Out out, int vn = 1) {
   const int R = pn.R, C = pn.C, TR = pn.TR, TS = pn.TS;
   const double2* base = reinterpret_cast<const double2*>(pn.base + (size_t)tile * C * TS);
-  const int cs = TS / 2;
+  const int cs = TS / 2;          // stored row pairs
+  const int np = cs * vn;         // row pairs to compute
   int G = 1;
-  while (2 * G * cs <= NT && 2 * G * 4 <= C) G *= 2;
+  while (2 * G * np <= NT && 2 * G * 4 <= C) G *= 2;
   const int CKg = (C + G - 1) / G;
   const int t = threadIdx.x;
-  for (int rp = t % cs + (t / cs >= G ? NT : 0); rp < cs; rp += (G == 1 ? NT : cs)) {
-    const int g = G == 1 ? 0 : t / cs;
+  // (node, local row) of stored row r of pair q; valid = r < rows of that node
+  auto where = [&](int q, int h, int& j, int& row) -> bool {
+    if (vn > 1) {
+      j = q / cs;
+      row = 2 * (q % cs) + h;
+      return row < R;
+    }
+    const int r = 2 * q + h;
+    j = min(r, TR - 1) / R;
+    row = r - j * R;
+    return r < TR;
+  };
+  for (int q = t % np + (t / np >= G ? NT : 0); q < np; q += (G == 1 ? NT : np)) {
+    const int g = G == 1 ? 0 : t / np;
     const int c0 = g * CKg, c1 = min(C, c0 + CKg);
-    const int r0 = 2 * rp, r1 = r0 + 1;
-    const int ja = min(r0, TR - 1) / R, jb = min(r1, TR - 1) / R;
-    const double2* M = base + rp;
+    int ja, la, jb, lb;
+    const bool va = where(q, 0, ja, la), vb = where(q, 1, jb, lb);
+    const double2* M = base + (vn > 1 ? q % cs : q);
     double acc0[KM], acc1[KM];
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) { acc0[kk] = 0.0; acc1[kk] = 0.0; }
@@ -76,26 +91,27 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
     if (G == 1) {
 #pragma unroll
       for (int kk = 0; kk < KM; ++kk) {
-        if (r0 < TR) out(ja, r0 - ja * R, kk, acc0[kk]);
-        if (r1 < TR) out(jb, r1 - jb * R, kk, acc1[kk]);
+        if (va) out(ja, la, kk, acc0[kk]);
+        if (vb) out(jb, lb, kk, acc1[kk]);
       }
     } else {
 #pragma unroll
       for (int kk = 0; kk < KM; ++kk) {
-        red[(g * KM + kk) * TS + r0] = acc0[kk];
-        red[(g * KM + kk) * TS + r1] = acc1[kk];
+        red[(g * KM + kk) * 2 * np + 2 * q] = acc0[kk];
+        red[(g * KM + kk) * 2 * np + 2 * q + 1] = acc1[kk];
       }
     }
   }
   if (G > 1) {
     __syncthreads();
-    for (int r = t; r < TR; r += NT) {
-      const int j = r / R;
+    for (int i = t; i < 2 * np; i += NT) {
+      int j, row;
+      if (!where(i / 2, i % 2, j, row)) continue;
 #pragma unroll
       for (int kk = 0; kk < KM; ++kk) {
         double y = 0.0;
-        for (int g = 0; g < G; ++g) y += red[(g * KM + kk) * TS + r];
-        out(j, r - j * R, kk, y);
+        for (int g = 0; g < G; ++g) y += red[(g * KM + kk) * 2 * np + i];
+        out(j, row, kk, y);
       }
     }
     __syncthreads();
@@ -131,7 +147,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_up(SubArgs a) {
     }
     __syncthreads();
     // [w3; h - base] = [X33^-1; Tstack X33^-1] r3 for the subtree's nodes of this level
-    tile_apply<KM>(L.Up, L.Up.ntiles == 1 ? 0 : b, r3s, n3, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM>(L.Up, L.Up.c == 1 ? 0 : b, r3s, n3, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       if (row < n3) {
@@ -143,7 +159,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_up(SubArgs a) {
       const double h = base + y;
       Hn[(j * KM + kk) * n12 + r] = h;
       if (e == 0) a.H_dF[kg * a.H_k + (long long)(node0 + j) * n12 + r] = h;
-    });
+    }, L.Up.c == 1 ? npn : 1);
     __syncthreads();
     if (a.dF + e == 0) break;  // the root's outer flux is never consumed
     double* t = Hs; Hs = Hn; Hn = t;
@@ -167,13 +183,13 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
       xs[(j * KM + kk) * n12 + col] = kg < a.k ? a.u[kg * a.u_k + L.gidx[(long long)(node0 + j) * n12 + col]] : 0.0;
     }
     __syncthreads();
-    tile_apply<KM>(L.S, L.S.ntiles == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM>(L.S, L.S.c == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       const long long nd = (long long)(node0 + j) * n3 + row;
       if (a.has_w3) y = y + L.W3[kg * L.W3_k + nd];
       a.u[kg * a.u_k + L.j3[nd]] = y;
-    });
+    }, L.S.c == 1 ? npn : 1);
   }
 }
 
@@ -206,14 +222,14 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_down_local(SubArgs 
       xs[(j * KM + kk) * n12 + col] = uloc[kk * ns + sl[j * n12 + col]];
     }
     __syncthreads();
-    tile_apply<KM>(L.S, L.S.ntiles == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM>(L.S, L.S.c == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       const long long nd = (long long)(node0 + j) * n3 + row;
       if (a.has_w3) y = y + L.W3[kg * L.W3_k + nd];
       uloc[kk * ns + jb + j * n3 + row] = y;
       a.u[kg * a.u_k + L.j3[nd]] = y;
-    });
+    }, L.S.c == 1 ? npn : 1);
   }
 }
 
