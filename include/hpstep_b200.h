@@ -103,6 +103,14 @@ int hps_ops_build(const hps_plan* plan, const hps_build_desc* desc, void* stream
 void hps_ops_destroy(hps_ops* ops);
 size_t hps_ops_device_bytes(const hps_ops* ops);
 
+/* Enable the tensor-product leaf solve for a constant-coefficient operator
+ * set (leaf_fd.cu): host = Vx^-1, Vy^-T, Vx, Vy^T, rden (q x q each, row-major;
+ * rden[a][b] = 1 / (lx_a + ly_b + sigma + dtg c)), then the interior parts of the
+ * flux rows d1x[0], d1x[p-1], d1y[0], d1y[p-1] (q each); count = 5q^2 + 4q.
+ * host = NULL disables it.  Replaces the dense A_ii^-1 apply of
+ * solver.py:221-228 with the Kronecker-sum factorisation of A_ii. */
+int hps_ops_set_leaf_fd(hps_ops* ops, const double* host, int count);
+
 /* Copy one operator block to host memory (test hooks leaf_operators /
  * merge_operators, solver.py:339-348).  which: leaf 0=Ainv (ni x ni),
  * 1=S (ni x nb), 2=T (nb x nb, keep_dtn only); merge 0=Xinv (n3 x n3),

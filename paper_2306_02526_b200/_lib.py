@@ -82,6 +82,7 @@ SIGNATURES = {
     "hps_ops_get_leaf": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_double_p]),
     "hps_ops_get_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          c_double_p]),
+    "hps_ops_set_leaf_fd": (ctypes.c_int, [ctypes.c_void_p, c_double_p, ctypes.c_int]),
     "hps_ops_dump_size": (ctypes.c_longlong, [ctypes.c_void_p]),
     "hps_ops_dump": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]),
     "hps_ops_load": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong,

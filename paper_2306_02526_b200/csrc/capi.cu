@@ -612,7 +612,8 @@ bool write_structure(const Ops& O, Writer& w) {
   w.put(O.sigma); w.put(O.dtg); w.put(O.shared_leaf); w.put(O.shared_levels); w.put(O.Lc);
   w.put(P.depth); w.put(P.L); w.put(P.ni); w.put(P.nb); w.put(P.N);
   std::vector<long long> ptrs = {alloc_index(O, O.Ainv), alloc_index(O, O.S_leaf), alloc_index(O, O.T_leaf),
-                                 alloc_index(O, O.D_bi), alloc_index(O, O.root_T), alloc_index(O, O.root_Tst)};
+                                 alloc_index(O, O.D_bi), alloc_index(O, O.root_T), alloc_index(O, O.root_Tst),
+                                 alloc_index(O, O.fd)};
   for (long long i : ptrs) { if (i == -2) return false; w.put(i); }
   put_panel(w, O, O.pAinv);
   put_panel(w, O, O.pSleaf);
@@ -679,7 +680,7 @@ int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops**
     set_error("hps_ops_load: dump was made for a different tree");
     return HPS_ERR_ARG;
   }
-  long long ptr[6];
+  long long ptr[7];
   for (long long& i : ptr) i = r.get<long long>();
   long long iA, iS;
   get_panel(r, O.pAinv, iA);
@@ -717,7 +718,7 @@ int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops**
   }
   auto at = [&](long long i) -> double* { return i >= 0 && i < na ? (double*)O.allocs[(size_t)i] : nullptr; };
   O.Ainv = at(ptr[0]); O.S_leaf = at(ptr[1]); O.T_leaf = at(ptr[2]); O.D_bi = at(ptr[3]);
-  O.root_T = at(ptr[4]); O.root_Tst = at(ptr[5]);
+  O.root_T = at(ptr[4]); O.root_Tst = at(ptr[5]); O.fd = at(ptr[6]);
   O.pAinv.base = at(iA); O.pSleaf.base = at(iS);
   for (int d = 0; d < depth; ++d) {
     LevelOps& lo = O.lo[d];
@@ -729,3 +730,20 @@ int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops**
 }
 
 }  // extern "C"
+
+extern "C" int hps_ops_set_leaf_fd(hps_ops* h, const double* host, int count) {
+  if (!h) { set_error("hps_ops_set_leaf_fd: null ops"); return HPS_ERR_ARG; }
+  Ops& O = h->O;
+  const Plan& P = *O.plan;
+  if (!host) { O.fd = nullptr; return HPS_OK; }  // disable (the buffer stays owned)
+  const int q = P.q;
+  if (!O.shared_leaf || !leaf_fd_supported(q) || count != 5 * q * q + 4 * q) {
+    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in {8, 10, 14} and %d values", 5 * q * q + 4 * q);
+    return HPS_ERR_ARG;
+  }
+  double* d = ops_alloc(O, (size_t)count, false);
+  if (!d) { set_error("out of device memory"); return HPS_ERR_CUDA; }
+  HPSB_CUDA(cudaMemcpy(d, host, (size_t)count * 8, cudaMemcpyHostToDevice));
+  O.fd = d;
+  return HPS_OK;
+}

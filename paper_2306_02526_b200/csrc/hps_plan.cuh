@@ -106,6 +106,7 @@ struct Ops {
   double* Ainv = nullptr;      // shared leaf: [Ainv; D_bi Ainv], (ni+nb) x ldi row-major (GEMM operand)
   double* S_leaf = nullptr;    // shared leaf: ni x ldb row-major
   Panel pAinv, pSleaf;         // per-leaf operators (variable coefficients)
+  double* fd = nullptr;        // tensor-product leaf solve data (leaf_fd.cu), or null
   double* T_leaf = nullptr;    // Lc x nb x nb (kept only when keep_dtn)
   double* D_bi = nullptr;      // nb x ni (shared stencil rows)
   std::vector<LevelOps> lo;    // depth entries, root first
@@ -174,6 +175,10 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
                     long long Hc_s, const double* jump, long long ld_jump, double inv_dt, cudaStream_t st);
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
                       cudaStream_t st);
+
+// tensor-product leaf solve (leaf_fd.cu): [w | h] rows from the body load
+int leaf_fd(const Ops& ops, int k, const double* g, long long ld_g, double* WH, long long ld_wh, cudaStream_t st);
+bool leaf_fd_supported(int q);
 
 // solve entry (solve.cu)
 int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,

@@ -1,0 +1,294 @@
+// Tensor-product ("fast diagonalisation") leaf solve for constant coefficients.
+//
+// With constant coefficients the interior collocation block is a Kronecker
+// sum (operators.py:252-269 with x-major interior order):
+//     A_ii = Ax (x) I + I (x) Ay + s I,   Ax = dtg(-c11 d2x + c1 d1x)_int,
+//                                         Ay = dtg(-c22 d2y + c2 d1y)_int,
+//                                         s  = sigma + dtg c,
+// so with Ax = Vx Lx Vx^-1, Ay = Vy Ly Vy^-1 (real spectra, checked on the
+// host) the leaf particular solution w = A_ii^-1 r of solver.py:221-223 is
+//     W = Vx [ (Vx^-1 R Vy^-T) ./ (lx_a + ly_b + s) ] Vy^T     (R, W: q x q)
+// -- 8 q^3 flops per leaf instead of the dense inverse's 2 q^4 -- and the
+// leaf's outgoing flux h = D_bi w (solver.py:228) reads one grid line per
+// boundary point (2 q^2 flops instead of 8 q^3).  Results agree with the
+// LU-based reference to round-off times cond(V) (checked by the parity tests).
+//
+// One CTA works on LB leaves at a time (persistent over leaf groups); the
+// four q x q products run from shared memory, one output per thread-slot.
+#include <stdlib.h>
+
+#include "hps_plan.cuh"
+
+namespace hpsb {
+
+namespace {
+
+constexpr int NT = 256;
+
+struct FdArgs {
+  int L, k, nw;
+  const double* g; long long ld_g;   // body load rows (leaf l interior at l*ni)
+  double* WH; long long ld_wh;       // [w | h] rows of nw = ni + nb per leaf
+  const double* mats;                // Vxi, VyiT, Vx, VyT, den (q x q each), ex0, ex1, ey0, ey1 (q each)
+};
+
+template <int Q>
+__global__ void __launch_bounds__(NT) k_leaf_fd(FdArgs a) {
+  constexpr int QS = Q + 1, QQ = Q * QS, NI = Q * Q, NB = 4 * Q, P = Q + 2;
+  constexpr int LB = Q >= 12 ? 8 : 16;  // leaves per group (static smem < 48 KB)
+  __shared__ double M[5][QQ];
+  __shared__ double E[4][Q];
+  __shared__ double B0[LB][QQ], B1[LB][QQ];
+  const int tid = threadIdx.x, kk = blockIdx.y;
+  pdl_trigger();
+  for (int e = tid; e < 5 * NI; e += NT) M[e / NI][(e % NI) / Q * QS + e % Q] = a.mats[e];
+  for (int e = tid; e < 4 * Q; e += NT) E[e / Q][e % Q] = a.mats[5 * NI + e];
+  pdl_wait();
+  const double* g = a.g + kk * a.ld_g;
+  double* wh = a.WH + kk * a.ld_wh;
+  for (int l0 = blockIdx.x * LB; l0 < a.L; l0 += gridDim.x * LB) {
+    const int nl = min(LB, a.L - l0);
+    __syncthreads();
+    for (int e = tid; e < nl * NI; e += NT) B0[e / NI][(e % NI) / Q * QS + e % Q] = g[(long long)l0 * NI + e];
+    __syncthreads();
+    // B1 = Vx^-1 B0
+    for (int e = tid; e < nl * NI; e += NT) {
+      const int l = e / NI, i = (e % NI) / Q, j = e % Q;
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < Q; ++t) s = fma(M[0][i * QS + t], B0[l][t * QS + j], s);
+      B1[l][i * QS + j] = s;
+    }
+    __syncthreads();
+    // B0 = (B1 Vy^-T) ./ den
+    for (int e = tid; e < nl * NI; e += NT) {
+      const int l = e / NI, i = (e % NI) / Q, j = e % Q;
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < Q; ++t) s = fma(B1[l][i * QS + t], M[1][t * QS + j], s);
+      B0[l][i * QS + j] = s * M[4][i * QS + j];
+    }
+    __syncthreads();
+    // B1 = Vx B0
+    for (int e = tid; e < nl * NI; e += NT) {
+      const int l = e / NI, i = (e % NI) / Q, j = e % Q;
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < Q; ++t) s = fma(M[2][i * QS + t], B0[l][t * QS + j], s);
+      B1[l][i * QS + j] = s;
+    }
+    __syncthreads();
+    // w = B1 Vy^T  ->  B0 and the w part of the output rows
+    for (int e = tid; e < nl * NI; e += NT) {
+      const int l = e / NI, i = (e % NI) / Q, j = e % Q;
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < Q; ++t) s = fma(B1[l][i * QS + t], M[3][t * QS + j], s);
+      B0[l][i * QS + j] = s;
+      wh[(long long)(l0 + l) * a.nw + i * Q + j] = s;
+    }
+    __syncthreads();
+    // h = D_bi w: normal derivative along the grid line through each boundary point
+    for (int e = tid; e < nl * NB; e += NT) {
+      const int l = e / NB, b = e % NB;
+      double s = 0.0;
+      if (b < Q || b >= 3 * Q) {  // east (xi = 0) / west (xi = p-1): d/dx along row yi
+        const int yi = (b < Q ? b : b - 3 * Q);
+        const double* r = E[b < Q ? 0 : 1];
+#pragma unroll
+        for (int t = 0; t < Q; ++t) s = fma(r[t], B0[l][t * QS + yi], s);
+      } else {                    // north / south interleaved: d/dy along column xi
+        const int jj = b - Q, xi = jj / 2;
+        const double* r = E[(jj & 1) ? 3 : 2];
+#pragma unroll
+        for (int t = 0; t < Q; ++t) s = fma(r[t], B0[l][xi * QS + t], s);
+      }
+      wh[(long long)(l0 + l) * a.nw + NI + b] = s;
+    }
+  }
+  (void)P;
+}
+
+// DMMA variant: one warp per leaf, the q x q blocks zero-padded to 16 x 16 so
+// each of the four products is 2 x 2 output tiles x 4 k-steps of
+// mma.sync.m8n8k4.f64.  The four constant matrices and 1/den live in
+// registers as MMA fragments for the whole kernel; the leaf's blocks move
+// through two per-warp shared buffers whose strides make every fragment load
+// conflict-free (B-operand reads use stride 24, A-operand reads stride 20).
+constexpr int SB = 24, SA = 20;
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int Q>
+__global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
+  constexpr int NI = Q * Q, NB = 4 * Q;
+  extern __shared__ double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, kk = blockIdx.y;
+  double* bufB = sm + warp * 16 * (SB + SA);   // stride SB
+  double* bufA = bufB + 16 * SB;               // stride SA
+  const int gr = lane >> 2, gc = lane & 3;
+  pdl_trigger();
+  // constant fragments: A operands (Vx^-1, Vx) as [m tile][k step], B operands (Vy^-T, Vy^T) as [k step][n tile]
+  auto mat = [&](int m, int r, int c) -> double { return (r < Q && c < Q) ? a.mats[m * NI + r * Q + c] : 0.0; };
+  double fVxi[2][4], fVx[2][4], fVyit[4][2], fVyt[4][2], fR[2][2][2];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      fVxi[mi][k] = mat(0, mi * 8 + gr, k * 4 + gc);
+      fVx[mi][k] = mat(2, mi * 8 + gr, k * 4 + gc);
+    }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj) {
+      fVyit[k][nj] = mat(1, k * 4 + gc, nj * 8 + gr);
+      fVyt[k][nj] = mat(3, k * 4 + gc, nj * 8 + gr);
+    }
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) fR[mi][nj][h] = mat(4, mi * 8 + gr, nj * 8 + 2 * gc + h);
+  const double* E = a.mats + 5 * NI;
+  for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
+  __syncwarp();
+  pdl_wait();
+  const double* g = a.g + kk * a.ld_g;
+  double* wh = a.WH + kk * a.ld_wh;
+  const int nwarps = gridDim.x * 8;
+  constexpr int NR = (NI + 31) / 32;  // body-load values per lane
+  double nxt[NR];                     // next leaf's body load, prefetched during this leaf
+  auto fetch = [&](int leaf) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int e = lane + 32 * i;
+      nxt[i] = (leaf < a.L && e < NI) ? g[(long long)leaf * NI + e] : 0.0;
+    }
+  };
+  fetch(blockIdx.x * 8 + warp);
+  for (int l = blockIdx.x * 8 + warp; l < a.L; l += nwarps) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int e = lane + 32 * i;
+      if (e < NI) bufB[(e / Q) * SB + e % Q] = nxt[i];
+    }
+    fetch(l + nwarps);
+    __syncwarp();
+    double acc[2][2][2];
+    auto clear = [&]() {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) { acc[mi][nj][0] = 0.0; acc[mi][nj][1] = 0.0; }
+    };
+    auto store = [&](double* buf, int ld) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+          *reinterpret_cast<double2*>(buf + (mi * 8 + gr) * ld + nj * 8 + 2 * gc) =
+              make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+    };
+    // T1 = Vx^-1 R  (B operand from bufB)
+    clear();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) { dmma(acc[mi][0][0], acc[mi][0][1], fVxi[mi][k], b0); dmma(acc[mi][1][0], acc[mi][1][1], fVxi[mi][k], b1); }
+    }
+    store(bufA, SA);
+    __syncwarp();
+    // T2 = (T1 Vy^-T) .* rden  (A operand from bufA)
+    clear();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) { dmma(acc[0][nj][0], acc[0][nj][1], a0, fVyit[k][nj]); dmma(acc[1][nj][0], acc[1][nj][1], a1, fVyit[k][nj]); }
+    }
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[mi][nj][h] *= fR[mi][nj][h];
+    store(bufB, SB);
+    __syncwarp();
+    // T3 = Vx T2  (B operand from bufB)
+    clear();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) { dmma(acc[mi][0][0], acc[mi][0][1], fVx[mi][k], b0); dmma(acc[mi][1][0], acc[mi][1][1], fVx[mi][k], b1); }
+    }
+    store(bufA, SA);
+    __syncwarp();
+    // W = T3 Vy^T  (A operand from bufA)
+    clear();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) { dmma(acc[0][nj][0], acc[0][nj][1], a0, fVyt[k][nj]); dmma(acc[1][nj][0], acc[1][nj][1], a1, fVyt[k][nj]); }
+    }
+    store(bufB, SB);
+    __syncwarp();
+    double* out = wh + (long long)l * a.nw;
+    for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
+    // h = D_bi w along the grid line of each boundary point
+    for (int b = lane; b < NB; b += 32) {
+      double s = 0.0;
+      if (b < Q || b >= 3 * Q) {
+        const int yi = b < Q ? b : b - 3 * Q;
+        const double* rr = E + (b < Q ? 0 : Q);
+#pragma unroll
+        for (int t = 0; t < Q; ++t) s = fma(rr[t], bufB[t * SB + yi], s);
+      } else {
+        const int jj = b - Q, xi = jj / 2;
+        const double* rr = E + ((jj & 1) ? 3 : 2) * Q;
+#pragma unroll
+        for (int t = 0; t < Q; ++t) s = fma(rr[t], bufB[xi * SB + t], s);
+      }
+      out[NI + b] = s;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+int leaf_fd(const Ops& ops, int k, const double* g, long long ld_g, double* WH, long long ld_wh, cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  FdArgs a{};
+  a.L = P.L; a.k = k; a.nw = P.ni + P.nb;
+  a.g = g; a.ld_g = ld_g; a.WH = WH; a.ld_wh = ld_wh; a.mats = ops.fd;
+  const unsigned groups = (unsigned)std::min<long long>(cdiv(P.L, 8), (long long)kNumSMs * 4);
+  dim3 grid(groups, (unsigned)k);
+  if (!getenv("HPSB_FD_SIMT")) {  // tensor-core variant
+    const size_t smem = (size_t)8 * 16 * (SB + SA) * 8;
+    const unsigned warps = (unsigned)std::min<long long>(cdiv(P.L, 8), (long long)kNumSMs * 2);  // one wave
+    dim3 g2(warps, (unsigned)k);
+#define HPSB_FD2(QQ) \
+  if (P.q == QQ) { HPSB_CUDA(launch_pdl(k_leaf_fd_mma<QQ>, g2, dim3(256), smem, st, a)); HPSB_LAUNCH_CHECK(); return 0; }
+    HPSB_FD2(8) HPSB_FD2(10) HPSB_FD2(14)
+#undef HPSB_FD2
+  }
+#define HPSB_FD(QQ) \
+  if (P.q == QQ) { HPSB_CUDA(launch_pdl(k_leaf_fd<QQ>, grid, dim3(NT), 0, st, a)); HPSB_LAUNCH_CHECK(); return 0; }
+  HPSB_FD(8) HPSB_FD(10) HPSB_FD(14)
+#undef HPSB_FD
+  set_error("leaf_fd: no kernel for q = %d", P.q);
+  return -1;
+}
+
+bool leaf_fd_supported(int q) { return q == 8 || q == 10 || q == 14; }
+
+}  // namespace hpsb

@@ -133,7 +133,12 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
   const double* Hleaf = ws.Hleaf;
   // (2) leaf particular solutions and their fluxes (solver.py:219-230)
   if (g) {
-    if (ops.shared_leaf) {
+    if (ops.shared_leaf && ops.fd) {
+      // tensor-product leaf solve: same [W | H] rows, 5x fewer flops
+      if (int rc = leaf_fd(ops, k, g, ld_g, ws.W, (long long)P.L * nw, st)) return rc;
+      ldw = nw; sw = (long long)P.L * nw; hs = nw; sh = sw;
+      Hleaf = ws.W + P.ni;
+    } else if (ops.shared_leaf) {
       // [W | H] (L x (ni+nb)) = G_int (L x ni) * [Ainv; D_bi Ainv]^T, one GEMM per rhs
       GemmArgs a{};
       a.M = P.L; a.N = nw; a.K = P.ni; a.alpha = 1.0; a.beta = 0.0;

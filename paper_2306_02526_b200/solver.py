@@ -162,6 +162,12 @@ class HpsOperatorSet:
         self.handle = h
         self._lib = lib
         self.parent_order = [int(i) for lm in self.tree.level_maps for i in lm.node_index]
+        self.leaf_solve = "dense"  # "tensor": Kronecker-sum leaf solve (csrc/leaf_fd.cu)
+        fd = tensor_leaf_factors(disc, self.sigma, self.dt_gamma)
+        if fd is not None and os.environ.get("HPSB_NO_FD") != "1":
+            fd = np.ascontiguousarray(fd, dtype=float)
+            _lib.check(lib.hps_ops_set_leaf_fd(h, _lib.dbl_ptr(fd), fd.size), "hps_ops_set_leaf_fd")
+            self.leaf_solve = "tensor"
 
     def __del__(self):
         try:
@@ -404,6 +410,41 @@ class _LeafFactors:
 
     def __getitem__(self, i):
         return _InverseFactor(self._ops._leaf_block(0, i))
+
+
+def tensor_leaf_factors(disc, sigma, dt_gamma, cond_max=1e6):
+    """Kronecker-sum factorisation of the interior leaf block for constant
+    coefficients (see csrc/leaf_fd.cu): [Vx^-1, Vy^-T, Vx, Vy^T, 1/den] (q x q)
+    and the interior parts of the four flux rows, or None when the block is
+    not a Kronecker sum with a real, well-conditioned eigenbasis."""
+    cf, st, tree = disc.coeffs, disc.stencil, disc.tree
+    q = tree.q
+    if not cf.is_constant or q not in (8, 10, 14):
+        return None
+    v = lambda f: 0.0 if f is None else float(f)
+    c11, c22, c1, c2, c0 = v(cf.c11), v(cf.c22), v(cf.c1), v(cf.c2), v(cf.c)
+    i = slice(1, tree.p - 1)
+    Ax = dt_gamma * (-c11 * st.d2x[i, i] + c1 * st.d1x[i, i])
+    Ay = dt_gamma * (-c22 * st.d2y[i, i] + c2 * st.d1y[i, i])
+    out = []
+    for Amat in (Ax, Ay):
+        lam, V = np.linalg.eig(Amat)
+        scale = max(1.0, float(np.abs(lam).max()))
+        if np.abs(lam.imag).max() > 1e-12 * scale or np.abs(V.imag).max() > 1e-12:
+            return None
+        lam, V = lam.real, V.real
+        if np.linalg.cond(V) > cond_max:
+            return None
+        out.append((lam, V, np.linalg.inv(V)))
+    (lx, Vx, Vxi), (ly, Vy, Vyi) = out
+    den = lx[:, None] + ly[None, :] + (sigma + dt_gamma * c0)
+    if np.abs(den).min() <= 1e-13 * np.abs(den).max():
+        return None
+    den = 1.0 / den                      # the kernel multiplies
+    p = tree.p
+    edges = [st.d1x[0, i], st.d1x[p - 1, i], st.d1y[0, i], st.d1y[p - 1, i]]
+    return np.concatenate([Vxi.ravel(), Vyi.T.ravel(), Vx.ravel(), Vy.T.ravel(), den.ravel()]
+                          + [e.ravel() for e in edges])
 
 
 def _jsonable(v):

@@ -84,3 +84,40 @@ def test_product_has_no_cpu_fallback():
         t = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 6)
         with pytest.raises(hb.HpstepError):
             hb.build(t, hb.OperatorCoefficients(c11=1.0, c22=1.0))
+
+
+@pytest.mark.parametrize("p", [10, 12, 16])
+@pytest.mark.parametrize("dtg", [2.5e-5, 1e-2, 1.0])
+def test_tensor_leaf_factors_reproduce_dense_interior_solve(p, dtg):
+    """The Kronecker-sum factorisation used by the tensor-product leaf solve
+    (csrc/leaf_fd.cu) reproduces (sigma I + dtg A_ii)^-1 r and D_bi w."""
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.solver import tensor_leaf_factors
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, p)
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=0.7, c=0.3))
+    q, ni = tree.q, tree.ni
+    fd = tensor_leaf_factors(disc, 1.0, dtg)
+    assert fd is not None and fd.size == 5 * q * q + 4 * q
+    Aii, _ = disc.leaf_blocks(0)
+    r = np.random.default_rng(1).standard_normal(ni)
+    w_ref = np.linalg.solve(np.eye(ni) + dtg * Aii, r)
+    M = fd[:5 * ni].reshape(5, q, q)
+    W = M[2] @ (((M[0] @ r.reshape(q, q)) @ M[1]) * M[4]) @ M[3]
+    assert np.linalg.norm(W.ravel() - w_ref) / np.linalg.norm(w_ref) < 1e-13
+    E = fd[5 * ni:].reshape(4, q)
+    h = np.concatenate([E[0] @ W,                                    # east: d/dx, rows yi
+                        np.stack([W @ E[2], W @ E[3]], 1).ravel(),   # north/south interleaved
+                        E[1] @ W])                                   # west
+    D_bi = disc.stencil.D_bnd[:, :ni]
+    assert np.allclose(h, D_bi @ W.ravel(), rtol=1e-12, atol=1e-12 * np.abs(h).max())
+
+
+def test_tensor_leaf_factors_only_for_constant_coefficients():
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.solver import tensor_leaf_factors
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 10)
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=lambda x, y: 1 + x, c22=1.0))
+    assert tensor_leaf_factors(disc, 1.0, 0.1) is None
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 9)            # q = 7: no kernel
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0))
+    assert tensor_leaf_factors(disc, 1.0, 0.1) is None
