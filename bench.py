@@ -133,9 +133,14 @@ def solve_bytes_shared(tree, k):
 FP64_TFLOPS = 37.0   # measured DMMA peak on this pool's B200 (profiles/r01_fp64_peak.txt)
 
 
-def solve_flops(tree, k):
-    ni, nb, L = tree.ni, tree.nb, tree.L
-    e = L * (ni * ni + 2 * ni * nb)
+def solve_flops(tree, k, tensor_leaf=False):
+    """FP64 flops of one stage solve as executed: the dense leaf products, or
+    the tensor-product leaf solve (8 q^3 + 2 nb q per leaf) for the up pass."""
+    ni, nb, L, q = tree.ni, tree.nb, tree.L, tree.q
+    if tensor_leaf:
+        e = L * (4 * q ** 3 + nb * q + ni * nb)
+    else:
+        e = L * (ni * ni + 2 * ni * nb)
     for d, lm in enumerate(tree.level_maps):
         e += lm.count * (lm.n3 * lm.n3 + lm.n3 * lm.n12 + (lm.n12 * lm.n3 if d > 0 else 0))
     return 2 * k * e
@@ -208,6 +213,8 @@ def _kernels_per_step(st, state):
 
 
 def _time_solves(st, n):
+    """CUDA-event time of one stage solve (the stepper's body load, boundary
+    data and operators), replayed as a CUDA graph like inside the step."""
     import torch
     k = st._k
     r = st._bufs.get("r")
@@ -215,11 +222,16 @@ def _time_solves(st, n):
     fb = st._bc(0.0)
     st.ops.solve_device(fb, r, out)
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        st.ops.solve_device(fb, r, out)
+    g.replay()
+    torch.cuda.synchronize()
     times = []
     for _ in range(n):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st.ops.solve_device(fb, r, out)
+        g.replay()
         e1.record()
         times.append((e0, e1))
     torch.cuda.synchronize()
@@ -424,7 +436,7 @@ def main():
         b_op, b_vec = solve_bytes(tree, k, prob.coeffs.is_constant)
     avg_solve = statistics.mean(solve_ms)
     peak, src = peaks()
-    flops = solve_flops(tree, k)
+    flops = solve_flops(tree, k, tensor_leaf=getattr(st.ops, "leaf_solve", "dense") == "tensor")
     t_hbm = (b_op + b_vec) / (peak * 1e9)
     t_fp64 = flops / (FP64_TFLOPS * 1e12)
     traffic = profiled_traffic(f"{args.config}/{layout}")
@@ -436,7 +448,8 @@ def main():
                 "unit": "TFLOP/s", "peak_source": "measured FP64 DMMA (profiles/r01_fp64_peak.txt)"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof.update({"traffic": traffic, "kernel": "hps_solve (one stage solve: leaf GEMMs + level sweeps)",
-                 "layout": layout, "algorithmic_bytes_per_solve": b_op + b_vec,
+                 "layout": layout, "leaf_solve": getattr(st.ops, "leaf_solve", "dense"),
+                 "algorithmic_bytes_per_solve": b_op + b_vec,
                  "gflops_per_solve": flops / 1e9, "solve_ms": avg_solve, "solves_timed": len(solve_ms),
                  "frac_hbm": (b_op + b_vec) / (avg_solve * 1e-3) / (peak * 1e9),
                  "frac_fp64": flops / (avg_solve * 1e-3) / (FP64_TFLOPS * 1e12)})
