@@ -5,8 +5,11 @@
 A *step* is one ESDIRK4 (ARK4(3)6L[2]SA) time step of the configured problem
 through the drop-in ``TimeStepper`` -- 5 implicit HPS stage solves plus the
 device stage right-hand-side assembly -- with the state resident in HBM.
-``value`` = DOF*stages/s = N_dof * 5 * K / (device time of K steps), summed
-over ranks (each rank runs its own replica: ``scaling`` "weak").
+``value`` = DOF*stages/s = N_dof * 5 * K / (device time of K steps, max over
+ranks).  With N > 1 GPUs (torchrun) one problem is subtree-sharded over the
+ranks (level-log2(N) subtrees per GPU, an NCCL all-gather of
+the subtree-root fluxes per stage solve, ``scaling`` "strong"); the ensemble
+config shards members; ``--shard replicas`` runs one replica per GPU instead.
 ``e2e`` is the same metric through the public API with the state copied in
 from pinned host memory and the result read back every step.
 ``roofline`` is for the stage solve (the ~2*depth+5 level-batched kernels of
@@ -212,14 +215,28 @@ def _kernels_per_step(st, state):
     return lib.hps_launch_count() - n0
 
 
-def _time_solves(st, n):
+def _time_solves(st, n, sharded=False):
     """CUDA-event time of one stage solve (the stepper's body load, boundary
-    data and operators), replayed as a CUDA graph like inside the step."""
+    data and operators), replayed as a CUDA graph like inside the step.  A
+    subtree-sharded solve (collectives inside) is timed eagerly, every rank
+    in lockstep."""
     import torch
     k = st._k
     r = st._bufs.get("r")
     out = torch.empty((k, st.tree.N), dtype=torch.float64, device="cuda")
     fb = st._bc(0.0)
+    if sharded:
+        st._solve(st.ops, fb, r, out)
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st._solve(st.ops, fb, r, out)
+            e1.record()
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in times]
     st.ops.solve_device(fb, r, out)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
@@ -333,6 +350,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layout", default=None, choices=[None, "auto", "per_node", "shared"],
                     help="operator storage (default: shared for constant coefficients)")
+    ap.add_argument("--shard", default="auto", choices=["auto", "subtree", "replicas"],
+                    help="N > 1 GPUs: subtree-shard one problem (auto) or run replicas")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", "0"))
@@ -344,26 +363,37 @@ def main():
     import torch
     import torch.distributed as dist
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HPSB_BENCH_DEVICE / HPSB_BENCH_BACKEND: exercise the multi-rank code path on
+    # one GPU (gloo, host-staged exchanges) -- never for reported numbers
+    local = int(os.environ.get("HPSB_BENCH_DEVICE", local))
+    backend = os.environ.get("HPSB_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     distributed = "TORCHELASTIC_RUN_ID" in os.environ or world > 1   # launched by torchrun
     if distributed:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import paper_2306_02526_b200 as hb
     from paper_2306_02526_b200 import _lib
     from paper_2306_02526_b200.sharding import max_over_ranks as _max_over_ranks
-    from paper_2306_02526_b200.sharding import shard_problem
+    from paper_2306_02526_b200.sharding import ShardedTimeStepper, shard_problem
 
     lib = _lib.load()
     tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), cfg["n"], cfg["n"], cfg["p"])
     prob = hb.ParabolicProblem(**make_problem(hb, cfg))
-    # ensembles shard by member (strong scaling over the fixed ensemble);
-    # single problems run one replica per GPU (weak scaling)
+    # ensembles shard by member; a single problem is subtree-sharded (both
+    # strong scaling: fixed total work), or replicated with --shard replicas
     ensemble = prob.ncomp > 1
+    subtree = world > 1 and not ensemble and args.shard != "replicas"
     if ensemble and world > 1:
         prob = shard_problem(prob, rank, world)
-    scaling = "strong" if ensemble else "weak"
+    scaling = "strong" if (ensemble or subtree) else "weak"
     t0 = time.perf_counter()
-    st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"], layout=args.layout)
+    if subtree:
+        st = ShardedTimeStepper(tree, prob, "ARK4", dt=cfg["dt"], layout=args.layout)
+    else:
+        st = hb.TimeStepper(tree, prob, "ARK4", dt=cfg["dt"], layout=args.layout)
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     k = prob.ncomp
@@ -403,9 +433,10 @@ def main():
     ms = max_over_ranks(ms)
     # stage-solve time for the roofline: the same solve (operators, stage body
     # load, boundary data) timed with CUDA events, 5 per step as in the run
-    solve_ms = _time_solves(st, 5 * args.steps)
-    # whole-job throughput: replicas add up; a sharded ensemble counts each member once
-    units = tree.N * 5 * args.steps * (k_total if ensemble else k * world)
+    solve_ms = _time_solves(st, 5 * args.steps, sharded=subtree)
+    # whole-job throughput: replicas add up; a sharded problem / ensemble counts once
+    copies = k_total if ensemble else (k if subtree else k * world)
+    units = tree.N * 5 * args.steps * copies
     value = units / (ms * 1e-3)
 
     # e2e: public API with host state in / host result out every step
@@ -424,7 +455,7 @@ def main():
     e1.record()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-    e2e_val = tree.N * 5 * e2e_steps * (k_total if ensemble else k * world) / (e2e_ms * 1e-3)
+    e2e_val = tree.N * 5 * e2e_steps * copies / (e2e_ms * 1e-3)
     nbytes = uh.numel() * 8
 
     # roofline of the stage solve: HBM bytes actually required by the layout
@@ -434,9 +465,13 @@ def main():
         b_op, b_vec = solve_bytes_shared(tree, k)
     else:
         b_op, b_vec = solve_bytes(tree, k, prob.coeffs.is_constant)
-    avg_solve = statistics.mean(solve_ms)
+    avg_solve = max_over_ranks(statistics.mean(solve_ms))
+    if subtree:   # per-GPU share of the algorithmic bytes / flops (top levels counted once)
+        b_op, b_vec = b_op / world, b_vec / world
     peak, src = peaks()
     flops = solve_flops(tree, k, tensor_leaf=getattr(st.ops, "leaf_solve", "dense") == "tensor")
+    if subtree:
+        flops /= world
     t_hbm = (b_op + b_vec) / (peak * 1e9)
     t_fp64 = flops / (FP64_TFLOPS * 1e12)
     traffic = profiled_traffic(f"{args.config}/{layout}")
@@ -473,6 +508,8 @@ def main():
                                f"bench step (5 stage solves)",
                    "N_dof": tree.N, "layout": layout,
                    "parallelism": (f"ensemble members sharded over {world} GPU(s)" if ensemble
+                                   else f"subtree-sharded over {world} GPUs (level-{world.bit_length() - 1} "
+                                        f"subtrees, NCCL flux all-gather per stage solve)" if subtree
                                    else f"replicas x{world}"),
                    "l2": "inputs larger than L2 (operators %.2f GB)" % (b_op / 1e9)},
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes,

@@ -64,6 +64,9 @@ typedef struct {
   const int* leaf_bnd_gidx;                /* L x nb                          */
   const long long* leaf_node_index;        /* L                               */
   const int* boundary_ids;                 /* nbd, ascending                  */
+  int nparts;             /* subtree partition for multi-GPU solves (SURVEY.md
+                             8(e)): 0 or 1 = none, else 2^lstar parts = the
+                             subtrees of the lstar-th parent level, lstar < depth */
 } hps_plan_desc;
 
 /* Build inputs (host arrays, copied).  Replaces build_leaf / merge / _build
@@ -143,6 +146,38 @@ int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const
               long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
               long long ld_u, void* ws, size_t ws_bytes, void* stream);
 
+/* Subtree-sharded solve (the reference solves the whole tree
+ * in one call, solver.py:201-276).  With a plan created with nparts = 2^lstar,
+ * part r is the subtree of node r on parent level lstar.  Phases:
+ *   HPS_PHASE_UP    leaves + levels >= lstar of parts [part0, part1): leaf
+ *                   solves and upward merges; leaves the parts' level-lstar
+ *                   fluxes in the workspace's exchange block;
+ *   HPS_PHASE_TOP   Dirichlet data, then the levels < lstar up and down (needs
+ *                   every part's flux in the exchange block: all-gather it
+ *                   between the phases when the parts live on other GPUs);
+ *   HPS_PHASE_DOWN  levels >= lstar + leaf reconstruction of the parts.
+ * g is indexed from the first leaf of part0 (row stride ld_g) and only read
+ * by the UP phase; pass the same g / jump to every phase (its nullness selects
+ * the data flow).  u rows are global (N DOFs); a phase writes only the DOFs it
+ * owns: TOP the boundary and the interfaces of levels < lstar, DOWN the
+ * interfaces and leaf interiors inside its parts.  HPS_PHASE_ALL over all
+ * parts is hps_solve. */
+#define HPS_PHASE_UP 1
+#define HPS_PHASE_TOP 2
+#define HPS_PHASE_DOWN 4
+#define HPS_PHASE_ALL 7
+int hps_solve_phase(const hps_ops* ops, int phases, int part0, int part1, int k, const double* fb,
+                    long long ld_f, const double* g, long long ld_g, const double* jump,
+                    long long ld_jump, double inv_dt, double* u, long long ld_u, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* Partition of a plan: nparts, lstar, the level-lstar flux length n12 and the
+ * byte offset in a k-rhs workspace of the exchange block (k x nparts x n12
+ * doubles, part r's fluxes at [r*n12, (r+1)*n12) of each rhs row; -1 when
+ * nparts = 1). */
+int hps_plan_partition(const hps_plan* plan, int k, int* nparts, int* lstar, int* n12,
+                       long long* flux_offset);
+
 /* ------------------------------------------------------------------------
  * Stage right-hand-side assembly (timestep.py:237-266 and the leaf-local
  * evaluations of operators.py:276-346).
@@ -177,6 +212,16 @@ void hps_disc_destroy(hps_disc* disc);
 int hps_leaf_eval(const hps_disc* disc, int k, const double* u, long long ld_u, double* lu_int,
                   double* lu, double* ux, double* uy, double* jump, long long ld_o, double* guard,
                   void* stream);
+
+/* hps_leaf_eval over leaves [leaf0, leaf0 + nleaf) (a subtree part): lu_int
+ * rows are indexed from leaf0's first interior DOF, the other outputs are
+ * global N-DOF rows.  Edge DOFs receive only these leaves' contributions
+ * (the interface mean adds 1/2 of each abutting leaf), so an edge shared with
+ * leaves outside the range holds a partial sum the caller completes (e.g. an
+ * all-reduce over the GPUs of a sharded run). */
+int hps_leaf_eval_range(const hps_disc* disc, int leaf0, int nleaf, int k, const double* u,
+                        long long ld_u, double* lu_int, double* lu, double* ux, double* uy,
+                        double* jump, long long ld_o, double* guard, void* stream);
 
 /* out[r][0:n) = sum_t coefs[t] * vecs[t][r*lds[t] + (0:n)] for r < k
  * (lds[t] = 0 broadcasts one vector over the rows); at most 24 terms.

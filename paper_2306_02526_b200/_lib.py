@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libhpstep_b200.so")
 
 HPS_OK = 0
+HPS_PHASE_UP, HPS_PHASE_TOP, HPS_PHASE_DOWN, HPS_PHASE_ALL = 1, 2, 4, 7
 HPS_ERR_SINGULAR = -3
 
 c_int_p = ctypes.POINTER(ctypes.c_int)
@@ -34,6 +35,7 @@ class PlanDesc(ctypes.Structure):
         ("lvl_gidx_bnd", ctypes.POINTER(c_int_p)), ("lvl_j3", ctypes.POINTER(c_int_p)),
         ("lvl_node_index", ctypes.POINTER(c_ll_p)),
         ("leaf_bnd_gidx", c_int_p), ("leaf_node_index", c_ll_p), ("boundary_ids", c_int_p),
+        ("nparts", ctypes.c_int),
     ]
 
 
@@ -93,9 +95,13 @@ SIGNATURES = {
                                  ctypes.c_longlong, ctypes.c_double, ctypes.c_void_p,
                                  ctypes.c_longlong, ctypes.c_void_p, ctypes.c_size_t,
                                  ctypes.c_void_p]),
+    "hps_solve_phase": (_i, [_vp, _i, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _ll, ctypes.c_double,
+                             _vp, _ll, _vp, ctypes.c_size_t, _vp]),
+    "hps_plan_partition": (_i, [_vp, _i, c_int_p, c_int_p, c_int_p, c_ll_p]),
     "hps_disc_create": (_i, [_vp, ctypes.POINTER(DiscDesc), ctypes.POINTER(_vp)]),
     "hps_disc_destroy": (None, [_vp]),
     "hps_leaf_eval": (_i, [_vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp]),
+    "hps_leaf_eval_range": (_i, [_vp, _i, _i, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp]),
     "hps_combine": (_i, [_i, _ll, _i, c_double_p, ctypes.POINTER(_vp), c_ll_p, _vp, _ll, _vp,
                          _vp]),
     "hps_combine_dev": (_i, [_i, _ll, _i, _vp, ctypes.POINTER(_vp), c_ll_p, _vp, _ll, _vp, _vp]),

@@ -170,7 +170,16 @@ int hps_plan_create(const hps_plan_desc* d, hps_plan** out) {
     up(d->lvl_j3[l], (size_t)lv.c * lv.n3, &lv.j3);
     lv.node_index.assign(d->lvl_node_index[l], d->lvl_node_index[l] + lv.c);
   }
-  P.dF = fuse_level(P);
+  // subtree partition: nparts = 2^lstar parts below a parent level lstar; the
+  // fused subtree levels must lie inside one part
+  P.nparts = d->nparts > 1 ? d->nparts : 1;
+  while ((1 << P.lstar) < P.nparts) ++P.lstar;
+  if ((1 << P.lstar) != P.nparts || (P.nparts > 1 && P.lstar >= P.depth)) {
+    set_error("hps_plan_create: nparts = %d must be a power of two below 2^depth (depth %d)", d->nparts, P.depth);
+    hps_plan_destroy(h);
+    return HPS_ERR_ARG;
+  }
+  P.dF = std::max(fuse_level(P), P.lstar);
   if (!rc && P.dF < P.depth) {
     std::vector<int> s0, s1;
     std::vector<long long> o0, o1;
@@ -339,10 +348,10 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     O.Ainv = Ainv;
     O.S_leaf = Sl;
   } else {
-    O.pAinv = make_panel(P.L, ni, ni);
-    O.pSleaf = make_panel(P.L, ni, nb);
-    O.pAinv.base = ops_alloc(O, O.pAinv.doubles(), false);
-    O.pSleaf.base = ops_alloc(O, O.pSleaf.doubles(), false);
+    O.pAinv = make_panel(P.L, ni, ni, P.nparts);
+    O.pSleaf = make_panel(P.L, ni, nb, P.nparts);
+    O.pAinv.base = ops_alloc(O, O.pAinv.total(), false);
+    O.pSleaf.base = ops_alloc(O, O.pSleaf.total(), false);
     if (!O.pAinv.base || !O.pSleaf.base) { set_error("out of device memory (leaf panels)"); return fail(HPS_ERR_CUDA); }
     if (int rc = pack_panel(Ainv, (long long)ni * P.ldi, P.ldi, O.pAinv, st)) return fail(rc);
     if (int rc = pack_panel(Sl, (long long)ni * P.ldb, P.ldb, O.pSleaf, st)) return fail(rc);
@@ -381,12 +390,13 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
       const int npn = 1 << (l - P.dF);
       lo.Up = make_panel_nodes(lv.c, nup, n3, npn);
       lo.S = make_panel_nodes(lv.c, n3, n12, npn);
-    } else {
-      lo.Up = make_panel(lv.c, nup, n3);
-      lo.S = make_panel(lv.c, n3, n12);
+    } else {  // wide levels: below lstar every part gets its own tiles
+      const int parts = l >= P.lstar ? P.nparts : 1;
+      lo.Up = make_panel(lv.c, nup, n3, parts);
+      lo.S = make_panel(lv.c, n3, n12, parts);
     }
-    if (lo.Up.c) lo.Up.base = ops_alloc(O, lo.Up.doubles(), false);
-    if (lo.S.c) lo.S.base = ops_alloc(O, lo.S.doubles(), false);
+    if (lo.Up.c) lo.Up.base = ops_alloc(O, lo.Up.total(), false);
+    if (lo.S.c) lo.S.base = ops_alloc(O, lo.S.total(), false);
     if (O.shared_levels) {
       lo.Ush = ops_alloc(O, (size_t)nup * lv.ld3, true);
       lo.Ssh = ops_alloc(O, (size_t)n3 * lv.ld12, true);
@@ -549,7 +559,27 @@ int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const d
               const double* jump, long long ld_jump, double inv_dt, double* u, long long ld_u, void* ws,
               size_t ws_bytes, void* stream) {
   if (!h || !fb || !u || !ws) { set_error("hps_solve: null argument"); return HPS_ERR_ARG; }
-  return solve(h->O, k, fb, ld_f, g, ld_g, jump, ld_jump, inv_dt, u, ld_u, ws, ws_bytes, (cudaStream_t)stream);
+  return solve(h->O, SOLVE_ALL, 0, h->O.plan->nparts, k, fb, ld_f, g, ld_g, jump, ld_jump, inv_dt, u, ld_u, ws,
+               ws_bytes, (cudaStream_t)stream);
+}
+
+int hps_plan_partition(const hps_plan* h, int k, int* nparts, int* lstar, int* n12, long long* flux_offset) {
+  if (!h) { set_error("hps_plan_partition: null plan"); return HPS_ERR_ARG; }
+  const Plan& P = h->P;
+  if (nparts) *nparts = P.nparts;
+  if (lstar) *lstar = P.lstar;
+  if (n12) *n12 = P.nparts > 1 ? P.lv[P.lstar].n12 : 0;
+  if (flux_offset) *flux_offset = P.nparts > 1 && k > 0 ? (long long)exchange_offset(P, k) : -1;
+  return HPS_OK;
+}
+
+int hps_solve_phase(const hps_ops* h, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
+                    const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt,
+                    double* u, long long ld_u, void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !u || !ws || ((phases & SOLVE_TOP) && !fb)) { set_error("hps_solve_phase: null argument"); return HPS_ERR_ARG; }
+  if (phases <= 0 || phases > SOLVE_ALL) { set_error("hps_solve_phase: bad phase mask %d", phases); return HPS_ERR_ARG; }
+  return solve(h->O, phases, part0, part1, k, fb, ld_f, g, ld_g, jump, ld_jump, inv_dt, u, ld_u, ws, ws_bytes,
+               (cudaStream_t)stream);
 }
 
 }  // extern "C"
@@ -561,7 +591,7 @@ int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const d
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr unsigned long long kDumpMagic = 0x31425350484244ULL;  // "DBHPSB1"
+constexpr unsigned long long kDumpMagic = 0x32425350484244ULL;  // "DBHPSB2"
 
 struct Writer {
   std::vector<unsigned char>* out;
@@ -595,13 +625,13 @@ long long alloc_index(const Ops& O, const void* ptr) {
 }
 
 void put_panel(Writer& w, const Ops& O, const Panel& pn) {
-  w.put(pn.c); w.put(pn.R); w.put(pn.C); w.put(pn.TR); w.put(pn.TS); w.put(pn.ntiles);
+  w.put(pn.c); w.put(pn.R); w.put(pn.C); w.put(pn.TR); w.put(pn.TS); w.put(pn.ntiles); w.put(pn.parts);
   w.put(alloc_index(O, pn.base));
 }
 
 void get_panel(Reader& r, Panel& pn, long long& idx) {
   pn.c = r.get<int>(); pn.R = r.get<int>(); pn.C = r.get<int>(); pn.TR = r.get<int>(); pn.TS = r.get<int>();
-  pn.ntiles = r.get<int>();
+  pn.ntiles = r.get<int>(); pn.parts = r.get<int>();
   idx = r.get<long long>();
 }
 
@@ -610,7 +640,7 @@ bool write_structure(const Ops& O, Writer& w) {
   const Plan& P = *O.plan;
   w.put(kDumpMagic);
   w.put(O.sigma); w.put(O.dtg); w.put(O.shared_leaf); w.put(O.shared_levels); w.put(O.Lc);
-  w.put(P.depth); w.put(P.L); w.put(P.ni); w.put(P.nb); w.put(P.N);
+  w.put(P.depth); w.put(P.L); w.put(P.ni); w.put(P.nb); w.put(P.N); w.put(P.nparts);
   std::vector<long long> ptrs = {alloc_index(O, O.Ainv), alloc_index(O, O.S_leaf), alloc_index(O, O.T_leaf),
                                  alloc_index(O, O.D_bi), alloc_index(O, O.root_T), alloc_index(O, O.root_Tst),
                                  alloc_index(O, O.fd)};
@@ -675,7 +705,8 @@ int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops**
   O.shared_levels = r.get<int>(); O.Lc = r.get<int>();
   const int depth = r.get<int>(), L = r.get<int>(), ni = r.get<int>(), nb = r.get<int>();
   const long long N = r.get<long long>();
-  if (!r.ok || depth != P.depth || L != P.L || ni != P.ni || nb != P.nb || N != P.N) {
+  const int nparts = r.get<int>();
+  if (!r.ok || depth != P.depth || L != P.L || ni != P.ni || nb != P.nb || N != P.N || nparts != P.nparts) {
     delete h;
     set_error("hps_ops_load: dump was made for a different tree");
     return HPS_ERR_ARG;

@@ -188,7 +188,8 @@ int gs(const GsArgs& a, int k, cudaStream_t st) {
 }  // namespace
 
 int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const double* Hc, long long Hc_k,
-                    long long Hc_s, const double* jump, long long ld_jump, double inv_dt, cudaStream_t st) {
+                    long long Hc_s, const double* jump, long long ld_jump, double inv_dt, int n0, int n1,
+                    cudaStream_t st) {
   const Plan& P = *ops.plan;
   const Level& lv = P.lv[d];
   const LevelOps& lo = ops.lo[d];
@@ -199,19 +200,21 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
   g.i1a = lv.i1a; g.i3a = lv.i3a; g.i2b = lv.i2b; g.i3b = lv.i3b; g.n1a = lv.n1a; g.n12 = lv.n12;
   g.jump = jump; g.jump_k = ld_jump; g.inv_dt = inv_dt; g.j3 = lv.j3;
   g.Hout = d > 0 ? ws.H[d] : nullptr; g.Hout_k = (long long)lv.c * lv.n12;
+  g.mode = GEMV_UP;
   if (lv.c < kSharedGemmNodes) {
-    g.mode = GEMV_UP;
-    g.shared = lv.c;
-    return gemv_level(g, lo.Up, st);
+    g.shared = 1;
+    return gemv_nodes(g, lo.Up, n0, n1, st);
   }
   GsArgs a{};
-  a.M = lv.c; a.N = lv.n3 + (d > 0 ? lv.n12 : 0); a.K = lv.n3;
+  a.M = n1 - n0;
+  a.N = lv.n3 + (d > 0 ? lv.n12 : 0); a.K = lv.n3;
+  g = shift_nodes(g, n0);
   a.B = lo.Ush; a.ldb = lv.ld3; a.g = g;
   return gs<GS_UP>(a, k, st);
 }
 
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
-                      cudaStream_t st) {
+                      int n0, int n1, cudaStream_t st) {
   const Plan& P = *ops.plan;
   const Level& lv = P.lv[d];
   const LevelOps& lo = ops.lo[d];
@@ -219,13 +222,15 @@ int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool ha
   g.k = k; g.part = ws.part; g.cnt = ws.cnt;
   g.u = u; g.u_k = ld_u; g.gidx = lv.gidx_bnd; g.j3 = lv.j3; g.n3 = lv.n3; g.n12 = lv.n12;
   g.W3 = has_w3 ? ws.W3[d] : nullptr; g.W3_k = (long long)lv.c * lv.n3;
+  g.mode = GEMV_DOWN;
   if (lv.c < kSharedGemmNodes) {
-    g.mode = GEMV_DOWN;
-    g.shared = lv.c;
-    return gemv_level(g, lo.S, st);
+    g.shared = 1;
+    return gemv_nodes(g, lo.S, n0, n1, st);
   }
   GsArgs a{};
-  a.M = lv.c; a.N = lv.n3; a.K = lv.n12;
+  a.M = n1 - n0;
+  a.N = lv.n3; a.K = lv.n12;
+  g = shift_nodes(g, n0);
   a.B = lo.Ssh; a.ldb = lv.ld12; a.g = g;
   return gs<GS_DOWN>(a, k, st);
 }

@@ -46,6 +46,10 @@ struct Plan {
   std::vector<int> sub_j3_base;             // first slot of level e's interfaces
   int ldi = 0;                    // even-padded ni
   int ldb = 0;                    // even-padded nb
+  // subtree partition: the level-lstar nodes (nparts = 2^lstar)
+  // root independent subtrees; levels >= lstar and the leaves can be solved
+  // per contiguous part range, levels < lstar ("top") need every part's flux
+  int nparts = 1, lstar = 0;
 };
 
 // Streaming layout of one operator family of a level ("panel"): the level's
@@ -63,10 +67,19 @@ struct Panel {
   int TR = kPanelRows;  // logical rows per tile
   int TS = kPanelRows;  // stored rows per tile (even; > TR only for node-aligned tiles)
   int ntiles = 0;
-  size_t doubles() const { return (size_t)ntiles * C * TS; }
+  int parts = 1;        // > 1: c is the node count of one part; `parts` such panels back to back
+  size_t doubles() const { return (size_t)ntiles * C * TS; }    // one part
+  size_t total() const { return doubles() * parts; }
+  Panel part(int g) const {
+    Panel q = *this;
+    q.base = base ? base + (size_t)g * doubles() : nullptr;
+    q.parts = 1;
+    return q;
+  }
 };
-// wide levels: power-of-two tiles (TS = TR)
-Panel make_panel(int c, int R, int C);
+// wide levels: power-of-two tiles (TS = TR); parts > 1 tiles each of `parts`
+// equal node ranges separately (no tile straddles a part boundary)
+Panel make_panel(int c, int R, int C, int parts = 1);
 // fused (subtree) levels: one tile = the npn nodes of one subtree, so one
 // CTA finds all of its operator rows for a level in one contiguous tile
 Panel make_panel_nodes(int c, int R, int C, int npn);
@@ -162,28 +175,43 @@ struct GemvArgs {
   int shared;
 };
 int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st);
+// nodes [n0, n1) of a level: per-part panels are launched part by part (the
+// range must be part-aligned), one-node (shared) panels over the node range
+int gemv_nodes(const GemvArgs& a, const Panel& pn, int n0, int n1, cudaStream_t st);
+GemvArgs shift_nodes(GemvArgs a, long long n0);
 
 // fused subtree kernels (subtree.cu) for the narrow levels dF..depth-1
 int fuse_level(const Plan& P);
+// level-dF subtrees [b0, b1)
 int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, long long sh, long long hs,
-               const double* jump, long long ld_jump, double inv_dt, cudaStream_t st);
-int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u,
-                 cudaStream_t st);
+               const double* jump, long long ld_jump, double inv_dt, int b0, int b1, cudaStream_t st);
+int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u, int b0,
+                 int b1, cudaStream_t st);
 
 // shared-layout level applies (dedup.cu)
+// nodes [n0, n1) of level d
 int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const double* Hc, long long Hc_k,
-                    long long Hc_s, const double* jump, long long ld_jump, double inv_dt, cudaStream_t st);
+                    long long Hc_s, const double* jump, long long ld_jump, double inv_dt, int n0, int n1,
+                    cudaStream_t st);
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
-                      cudaStream_t st);
+                      int n0, int n1, cudaStream_t st);
 
 // tensor-product leaf solve (leaf_fd.cu): [w | h] rows from the body load
-int leaf_fd(const Ops& ops, int k, const double* g, long long ld_g, double* WH, long long ld_wh, cudaStream_t st);
+// nleaf leaves: g and WH point at the first one
+int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,
+            cudaStream_t st);
 bool leaf_fd_supported(int q);
 
-// solve entry (solve.cu)
-int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
-          const double* jump, long long ld_jump, double inv_dt, double* u, long long ld_u,
-          void* ws, size_t ws_bytes, cudaStream_t st);
+// solve entry (solve.cu).  phases: SOLVE_UP (leaves + levels >= lstar of parts
+// [part0, part1)), SOLVE_TOP (Dirichlet data, levels < lstar up and down),
+// SOLVE_DOWN (levels >= lstar + leaves of the parts); all three = the whole
+// solve.  g is indexed from the first leaf of part0.
+enum SolvePhase { SOLVE_UP = 1, SOLVE_TOP = 2, SOLVE_DOWN = 4, SOLVE_ALL = 7 };
+int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
+          const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
+          long long ld_u, void* ws, size_t ws_bytes, cudaStream_t st);
+// byte offset of level lstar's flux block (k x nparts x n12) in a workspace
+size_t exchange_offset(const Plan& P, int k);
 
 }  // namespace hpsb
 

@@ -265,16 +265,18 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
 
 }  // namespace
 
-int leaf_fd(const Ops& ops, int k, const double* g, long long ld_g, double* WH, long long ld_wh, cudaStream_t st) {
+int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,
+            cudaStream_t st) {
   const Plan& P = *ops.plan;
+  if (nleaf <= 0) return 0;
   FdArgs a{};
-  a.L = P.L; a.k = k; a.nw = P.ni + P.nb;
+  a.L = nleaf; a.k = k; a.nw = P.ni + P.nb;
   a.g = g; a.ld_g = ld_g; a.WH = WH; a.ld_wh = ld_wh; a.mats = ops.fd;
-  const unsigned groups = (unsigned)std::min<long long>(cdiv(P.L, 8), (long long)kNumSMs * 4);
+  const unsigned groups = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 4);
   dim3 grid(groups, (unsigned)k);
   if (!getenv("HPSB_FD_SIMT")) {  // tensor-core variant
     const size_t smem = (size_t)8 * 16 * (SB + SA) * 8;
-    const unsigned warps = (unsigned)std::min<long long>(cdiv(P.L, 8), (long long)kNumSMs * 2);  // one wave
+    const unsigned warps = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 2);  // one wave
     dim3 g2(warps, (unsigned)k);
 #define HPSB_FD2(QQ) \
   if (P.q == QQ) { HPSB_CUDA(launch_pdl(k_leaf_fd_mma<QQ>, g2, dim3(256), smem, st, a)); HPSB_LAUNCH_CHECK(); return 0; }

@@ -29,12 +29,13 @@ namespace hpsb {
 // few tiles to spread over the SMs, then down to 64 rows (one warp).  The
 // total thread count of a launch is (rows/2) x (column splits), whatever the
 // tile height; the height only sets how evenly the tiles land on the SMs.
-Panel make_panel(int c, int R, int C) {
+Panel make_panel(int c, int R, int C, int parts) {
   Panel p;
-  p.c = c; p.R = R; p.C = C;
-  const long long rows = (long long)c * R;
+  p.parts = std::max(1, parts);
+  p.c = c / p.parts; p.R = R; p.C = C;
+  const long long rows = (long long)p.c * R;
   p.TR = kPanelRows;
-  while (p.TR > 64 && cdiv(rows, p.TR) < 2LL * kNumSMs) p.TR /= 2;
+  while (p.TR > 64 && cdiv(rows, p.TR) * p.parts < 2LL * kNumSMs) p.TR /= 2;
   p.TS = p.TR;
   p.ntiles = (int)cdiv(rows, p.TR);
   return p;
@@ -283,8 +284,52 @@ int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
   }
 }
 
+// the node-indexed inputs / outputs of a launch shifted to start at node n0
+GemvArgs shift_nodes(GemvArgs a, long long n0) {
+  if (n0 == 0) return a;
+  if (a.mode == GEMV_UP) {
+    a.Hc += 2 * n0 * a.Hc_s;
+    a.W3 += n0 * a.n3;
+    if (a.Hout) a.Hout += n0 * a.n12;
+    if (a.j3) a.j3 += n0 * a.n3;
+  } else if (a.mode == GEMV_DOWN) {
+    a.gidx += n0 * a.n12;
+    a.j3 += n0 * a.n3;
+    if (a.W3) a.W3 += n0 * a.n3;
+  } else {
+    a.xin += n0 * a.xin_s;
+    a.yout += n0 * a.yout_s;
+    if (a.yadd) a.yadd += n0 * a.yadd_s;
+  }
+  return a;
+}
+
+int gemv_nodes(const GemvArgs& a, const Panel& pn, int n0, int n1, cudaStream_t st) {
+  if (n1 <= n0) return 0;
+  if (a.shared) {
+    GemvArgs b = shift_nodes(a, n0);
+    b.shared = n1 - n0;
+    return gemv_level(b, pn, st);
+  }
+  const int cp = pn.c;
+  if (n0 % cp || n1 % cp || n1 / cp > pn.parts) {
+    set_error("gemv: node range [%d, %d) is not aligned to the panel's parts (%d nodes each)", n0, n1, cp);
+    return -1;
+  }
+  for (int g = n0 / cp; g < n1 / cp; ++g)
+    if (int rc = gemv_level(shift_nodes(a, (long long)g * cp), pn.part(g), st)) return rc;
+  return 0;
+}
+
 int pack_panel2(const double* src1, long long s1, int ld1, int R1, const double* src2, long long s2, int ld2,
                 const Panel& pn, cudaStream_t st) {
+  if (pn.parts > 1) {
+    for (int g = 0; g < pn.parts; ++g) {
+      const long long o = (long long)g * pn.c;
+      if (int rc = pack_panel2(src1 + o * s1, s1, ld1, R1, src2 + o * s2, s2, ld2, pn.part(g), st)) return rc;
+    }
+    return 0;
+  }
   long long total = (long long)pn.ntiles * pn.C * pn.TS;
   if (total <= 0) return 0;
   unsigned blocks = (unsigned)std::min<long long>(cdiv(total, 256), (long long)kNumSMs * 32);
@@ -298,6 +343,7 @@ int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cud
 }
 
 int unpack_panel(const Panel& pn, int node, int row0, int nrows, double* dst, cudaStream_t st) {
+  if (pn.parts > 1) return unpack_panel(pn.part(node / pn.c), node % pn.c, row0, nrows, dst, st);
   long long n = (long long)nrows * pn.C;
   if (n <= 0) return 0;
   unsigned blocks = (unsigned)std::min<long long>(cdiv(n, 256), (long long)kNumSMs * 8);

@@ -18,15 +18,16 @@ __global__ void k_bnd_scatter(int k, int nbd, const int* __restrict__ ids, const
   u[kk * ld_u + ids[i]] = fb[kk * ld_f + i];
 }
 
-__global__ void k_leaf_gather(int k, int L, int nb, const int* __restrict__ lbg, const double* __restrict__ u,
-                              long long ld_u, double* __restrict__ ub) {
+// ub rows of nl leaves (rhs stride `per`); lbg and ub point at the first leaf
+__global__ void k_leaf_gather(int k, int nl, int nb, long long per, const int* __restrict__ lbg,
+                              const double* __restrict__ u, long long ld_u, double* __restrict__ ub) {
   pdl_trigger();
   pdl_wait();
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long per = (long long)L * nb;
-  if (e >= (long long)k * per) return;
-  int kk = (int)(e / per);
-  long long r = e % per;
+  const long long cnt = (long long)nl * nb;
+  if (e >= (long long)k * cnt) return;
+  int kk = (int)(e / cnt);
+  long long r = e % cnt;
   ub[kk * per + r] = u[kk * ld_u + lbg[r]];
 }
 
@@ -37,17 +38,19 @@ __global__ void k_leaf_gather(int k, int L, int nb, const int* __restrict__ lbg,
 // panels whose launches carry (nodes x rhs) right-hand sides
 static void solve_panels(const Plan& P, std::vector<std::pair<Panel, int>>& out) {
   out.clear();
-  out.push_back({make_panel(P.L, P.ni, P.ni), 1});
-  out.push_back({make_panel(P.L, P.ni, P.nb), 1});
+  out.push_back({make_panel(P.L, P.ni, P.ni, P.nparts), 1});
+  out.push_back({make_panel(P.L, P.ni, P.nb, P.nparts), 1});
   for (const Level& lv : P.lv)
-    if (lv.c < kSharedGemmNodes) {
-      out.push_back({make_panel(1, lv.n3 + lv.n12, lv.n3), lv.c});
-      out.push_back({make_panel(1, lv.n3, lv.n12), lv.c});
-    }
+    if (lv.c < kSharedGemmNodes)
+      for (int v = lv.c; v >= 1 && v >= lv.c / P.nparts; v /= 2) {  // node ranges of part ranges
+        out.push_back({make_panel(1, lv.n3 + lv.n12, lv.n3), v});
+        out.push_back({make_panel(1, lv.n3, lv.n12), v});
+      }
   for (int d = 0; d < P.dF; ++d) {  // wide levels only; fused levels use no split-K
     const Level& lv = P.lv[d];
-    out.push_back({make_panel(lv.c, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3), 1});
-    out.push_back({make_panel(lv.c, lv.n3, lv.n12), 1});
+    const int parts = d >= P.lstar ? P.nparts : 1;
+    out.push_back({make_panel(lv.c, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3, parts), 1});
+    out.push_back({make_panel(lv.c, lv.n3, lv.n12, parts), 1});
   }
 }
 
@@ -102,128 +105,176 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
   ws.cnt = (unsigned*)p;  // zeroed by the caller when the workspace is created
 }
 
-int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
-          const double* jump, long long ld_jump, double inv_dt, double* u, long long ld_u,
-          void* wsp, size_t ws_bytes, cudaStream_t st) {
+// one level's upward merge over nodes [n0, n1) (solver.py:243-256)
+static int level_up(const Ops& ops, const Workspace& ws, int d, int n0, int n1, int k, const double* Hleaf,
+                    long long sh, long long hs, const double* jump, long long ld_jump, double inv_dt,
+                    cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  const Level& lv = P.lv[d];
+  const bool leafc = d == P.depth - 1;
+  const double* Hc = leafc ? Hleaf : ws.H[d + 1];
+  const long long Hc_k = leafc ? sh : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
+  const long long Hc_s = leafc ? hs : lv.nbc;
+  if (ops.shared_levels)
+    return shared_level_up(ops, ws, d, k, Hc, Hc_k, Hc_s, jump, ld_jump, inv_dt, n0, n1, st);
+  GemvArgs a{};
+  a.k = k; a.part = ws.part; a.cnt = ws.cnt;
+  a.Hc = Hc; a.nbc = lv.nbc; a.Hc_k = Hc_k; a.Hc_s = Hc_s;
+  a.W3 = ws.W3[d]; a.n3 = lv.n3; a.W3_k = (long long)lv.c * lv.n3;
+  a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
+  a.n12 = lv.n12;
+  a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt; a.j3 = lv.j3;
+  a.mode = GEMV_UP;  // the root's panel has no flux rows (its outer flux is never consumed)
+  a.Hout = d > 0 ? ws.H[d] : nullptr; a.Hout_k = (long long)lv.c * lv.n12;
+  return gemv_nodes(a, ops.lo[d].Up, n0, n1, st);
+}
+
+// one level's downward sweep over nodes [n0, n1) (solver.py:258-268)
+static int level_down(const Ops& ops, const Workspace& ws, int d, int n0, int n1, int k, bool has_w3, double* u,
+                      long long ld_u, cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  const Level& lv = P.lv[d];
+  if (ops.shared_levels) return shared_level_down(ops, ws, d, k, has_w3, u, ld_u, n0, n1, st);
+  GemvArgs a{};
+  a.mode = GEMV_DOWN; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
+  a.u = u; a.u_k = ld_u; a.gidx = lv.gidx_bnd; a.j3 = lv.j3;
+  a.n3 = lv.n3; a.n12 = lv.n12;
+  a.W3 = has_w3 ? ws.W3[d] : nullptr; a.W3_k = (long long)lv.c * lv.n3;
+  return gemv_nodes(a, ops.lo[d].S, n0, n1, st);
+}
+
+size_t exchange_offset(const Plan& P, int k) {
+  Workspace ws;
+  carve_workspace(P, k, nullptr, ws);
+  return (size_t)(uintptr_t)ws.H[P.lstar];
+}
+
+// Phases of one solve over the parts [part0, part1) (SOLVE_ALL over every
+// part = the whole solve of solver.py:201-276).
+int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
+          const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
+          long long ld_u, void* wsp, size_t ws_bytes, cudaStream_t st) {
   const Plan& P = *ops.plan;
   if (k <= 0) return 0;
   if (ws_bytes < workspace_bytes(P, k)) {
     set_error("solve: workspace too small (%zu < %zu)", ws_bytes, workspace_bytes(P, k));
     return -1;
   }
+  const int NP = P.nparts, ls = P.lstar;
+  if (part0 < 0 || part1 > NP || part0 >= part1) {
+    set_error("solve: part range [%d, %d) outside [0, %d)", part0, part1, NP);
+    return -1;
+  }
   Workspace ws;
   carve_workspace(P, k, wsp, ws);
   const long long Lni = (long long)P.L * P.ni, Lnb = (long long)P.L * P.nb;
   const int T = 256;
-
-  // (1) Dirichlet data into u (solver.py:259-260)
-  {
-    long long n = (long long)k * P.nbd;
-    if (n > 0) {
-      HPSB_CUDA(launch_pdl(k_bnd_scatter, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.nbd, P.boundary_ids,
-                           fb, ld_f, u, ld_u));
-      HPSB_LAUNCH_CHECK();
-    }
-  }
+  const int lpp = P.L / NP, leaf0 = part0 * lpp, nleaf = (part1 - part0) * lpp;
+  auto range = [&](int d, int& n0, int& n1) {  // the parts' nodes on level d >= lstar
+    const int per = P.lv[d].c / NP;
+    n0 = part0 * per;
+    n1 = part1 * per;
+  };
 
   const bool up = (g != nullptr) || (jump != nullptr);
   const int nw = P.ni + P.nb;
   // leaf outputs: W (row stride ldw, rhs stride sw) and H (child stride hs, rhs stride sh)
   long long ldw = P.ni, sw = Lni, hs = P.nb, sh = Lnb;
   const double* Hleaf = ws.Hleaf;
-  // (2) leaf particular solutions and their fluxes (solver.py:219-230)
-  if (g) {
-    if (ops.shared_leaf && ops.fd) {
+  const bool stacked = g && ops.shared_leaf;  // [w | h] rows of one GEMM / the tensor-product solve
+  if (stacked) {
+    ldw = nw; sw = (long long)P.L * nw; hs = nw; sh = sw;
+    Hleaf = ws.W + P.ni;
+  }
+
+  if (phases & SOLVE_UP) {
+    // (2) leaf particular solutions and their fluxes (solver.py:219-230)
+    if (g && ops.shared_leaf && ops.fd) {
       // tensor-product leaf solve: same [W | H] rows, 5x fewer flops
-      if (int rc = leaf_fd(ops, k, g, ld_g, ws.W, (long long)P.L * nw, st)) return rc;
-      ldw = nw; sw = (long long)P.L * nw; hs = nw; sh = sw;
-      Hleaf = ws.W + P.ni;
-    } else if (ops.shared_leaf) {
+      if (int rc = leaf_fd(ops, k, nleaf, g, ld_g, ws.W + (long long)leaf0 * nw, sw, st)) return rc;
+    } else if (g && ops.shared_leaf) {
       // [W | H] (L x (ni+nb)) = G_int (L x ni) * [Ainv; D_bi Ainv]^T, one GEMM per rhs
       GemmArgs a{};
-      a.M = P.L; a.N = nw; a.K = P.ni; a.alpha = 1.0; a.beta = 0.0;
+      a.M = nleaf; a.N = nw; a.K = P.ni; a.alpha = 1.0; a.beta = 0.0;
       a.A = g; a.lda = P.ni; a.sA = ld_g; a.tA = 0;
       a.B = ops.Ainv; a.ldb = P.ldi; a.sB = 0; a.tB = 1;
-      a.C = ws.W; a.ldc = nw; a.sC = (long long)P.L * nw; a.batch = k;
+      a.C = ws.W + (long long)leaf0 * nw; a.ldc = nw; a.sC = sw; a.batch = k;
       if (int rc = gemm_nt(a, st)) return rc;
-      ldw = nw; sw = (long long)P.L * nw; hs = nw; sh = sw;
-      Hleaf = ws.W + P.ni;
-    } else {
+    } else if (g) {
       GemvArgs a{};
       a.mode = GEMV_LEAF; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
-      a.xin = g; a.xin_k = ld_g; a.xin_s = P.ni;
+      // xin is addressed by global leaf index: g's (virtual) leaf-0 origin
+      a.xin = (const double*)((uintptr_t)g - (uintptr_t)leaf0 * P.ni * sizeof(double));
+      a.xin_k = ld_g; a.xin_s = P.ni;
       a.yout = ws.W; a.yout_k = Lni; a.yout_s = P.ni;
-      if (int rc = gemv_level(a, ops.pAinv, st)) return rc;
-      // H (k*L x nb) = W (k*L x ni) * D_bi^T
+      if (int rc = gemv_nodes(a, ops.pAinv, leaf0, leaf0 + nleaf, st)) return rc;
+      // H (nleaf x nb) = W (nleaf x ni) * D_bi^T per rhs
       GemmArgs h{};
-      h.M = k * P.L; h.N = P.nb; h.K = P.ni; h.alpha = 1.0; h.beta = 0.0;
-      h.A = ws.W; h.lda = P.ni; h.sA = 0; h.tA = 0;
+      h.M = nleaf; h.N = P.nb; h.K = P.ni; h.alpha = 1.0; h.beta = 0.0;
+      h.A = ws.W + (long long)leaf0 * P.ni; h.lda = P.ni; h.sA = Lni; h.tA = 0;
       h.B = ops.D_bi; h.ldb = P.ni; h.sB = 0; h.tB = 1;
-      h.C = ws.Hleaf; h.ldc = P.nb; h.sC = 0; h.batch = 1;
+      h.C = ws.Hleaf + (long long)leaf0 * P.nb; h.ldc = P.nb; h.sC = Lnb; h.batch = k;
       if (int rc = gemm_nt(h, st)) return rc;
+    } else if (jump) {
+      for (int kk = 0; kk < k; ++kk)
+        HPSB_CUDA(cudaMemsetAsync(ws.Hleaf + kk * Lnb + (long long)leaf0 * P.nb, 0, (size_t)nleaf * P.nb * 8, st));
     }
-  } else if (jump) {
-    HPSB_CUDA(cudaMemsetAsync(ws.Hleaf, 0, (size_t)k * Lnb * 8, st));
-  }
-
-  // (3) upward merges, deepest level first (solver.py:243-256): the fused
-  // subtree levels in one launch, then one launch per family on wide levels
-  if (up) {
-    if (int rc = subtree_up(ops, ws, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
-    for (int d = P.dF - 1; d >= 0; --d) {
-      const Level& lv = P.lv[d];
-      const LevelOps& lo = ops.lo[d];
-      const bool leafc = d == P.depth - 1;
-      const double* Hc = leafc ? Hleaf : ws.H[d + 1];
-      const long long Hc_k = leafc ? sh : (long long)P.lv[d + 1].c * P.lv[d + 1].n12;
-      const long long Hc_s = leafc ? hs : lv.nbc;
-      if (ops.shared_levels) {
-        if (int rc = shared_level_up(ops, ws, d, k, Hc, Hc_k, Hc_s, jump, ld_jump, inv_dt, st)) return rc;
-        continue;
+    // (3) upward merges of the parts' levels, deepest first (solver.py:243-256):
+    // the fused subtree levels in one launch, then one launch per family
+    if (up) {
+      if (P.dF < P.depth) {
+        int b0, b1;
+        range(P.dF, b0, b1);
+        if (int rc = subtree_up(ops, ws, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, b0, b1, st)) return rc;
       }
-      GemvArgs a{};
-      a.k = k; a.part = ws.part; a.cnt = ws.cnt;
-      a.Hc = Hc; a.nbc = lv.nbc; a.Hc_k = Hc_k; a.Hc_s = Hc_s;
-      a.W3 = ws.W3[d]; a.n3 = lv.n3; a.W3_k = (long long)lv.c * lv.n3;
-      a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
-      a.n12 = lv.n12;
-      a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt; a.j3 = lv.j3;
-      a.mode = GEMV_UP;  // the root's panel has no flux rows (its outer flux is never consumed)
-      a.Hout = d > 0 ? ws.H[d] : nullptr; a.Hout_k = (long long)lv.c * lv.n12;
-      if (int rc = gemv_level(a, lo.Up, st)) return rc;
+      for (int d = P.dF - 1; d >= ls; --d) {
+        int n0, n1;
+        range(d, n0, n1);
+        if (int rc = level_up(ops, ws, d, n0, n1, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
+      }
     }
   }
 
-  // (4) downward sweep, root first (solver.py:258-268)
-  for (int d = 0; d < P.dF; ++d) {
-    const Level& lv = P.lv[d];
-    const LevelOps& lo = ops.lo[d];
-    if (ops.shared_levels) {
-      if (int rc = shared_level_down(ops, ws, d, k, up, u, ld_u, st)) return rc;
-      continue;
+  if (phases & SOLVE_TOP) {
+    // (1) Dirichlet data into u (solver.py:259-260)
+    long long n = (long long)k * P.nbd;
+    if (n > 0) {
+      HPSB_CUDA(launch_pdl(k_bnd_scatter, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.nbd, P.boundary_ids,
+                           fb, ld_f, u, ld_u));
+      HPSB_LAUNCH_CHECK();
     }
-    GemvArgs a{};
-    a.mode = GEMV_DOWN; a.k = k; a.part = ws.part; a.cnt = ws.cnt;
-    a.u = u; a.u_k = ld_u; a.gidx = lv.gidx_bnd; a.j3 = lv.j3;
-    a.n3 = lv.n3; a.n12 = lv.n12;
-    a.W3 = up ? ws.W3[d] : nullptr; a.W3_k = (long long)lv.c * lv.n3;
-    if (int rc = gemv_level(a, lo.S, st)) return rc;
+    if (up)
+      for (int d = ls - 1; d >= 0; --d)
+        if (int rc = level_up(ops, ws, d, 0, P.lv[d].c, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
+    // (4) downward sweep of the top levels, root first (solver.py:258-268)
+    for (int d = 0; d < ls; ++d)
+      if (int rc = level_down(ops, ws, d, 0, P.lv[d].c, k, up, u, ld_u, st)) return rc;
   }
-  if (int rc = subtree_down(ops, ws, k, up, u, ld_u, st)) return rc;
 
-  // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
-  {
-    long long n = (long long)k * Lnb;
-    HPSB_CUDA(launch_pdl(k_leaf_gather, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.L, P.nb,
-                         (const int*)P.leaf_bnd_gidx, (const double*)u, ld_u, ws.Ub));
+  if (phases & SOLVE_DOWN) {
+    for (int d = ls; d < P.dF; ++d) {
+      int n0, n1;
+      range(d, n0, n1);
+      if (int rc = level_down(ops, ws, d, n0, n1, k, up, u, ld_u, st)) return rc;
+    }
+    if (P.dF < P.depth) {
+      int b0, b1;
+      range(P.dF, b0, b1);
+      if (int rc = subtree_down(ops, ws, k, up, u, ld_u, b0, b1, st)) return rc;
+    }
+    // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
+    long long n = (long long)k * nleaf * P.nb;
+    HPSB_CUDA(launch_pdl(k_leaf_gather, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, nleaf, P.nb, Lnb,
+                         (const int*)(P.leaf_bnd_gidx + (long long)leaf0 * P.nb), (const double*)u, ld_u,
+                         ws.Ub + (long long)leaf0 * P.nb));
     HPSB_LAUNCH_CHECK();
     if (ops.shared_leaf) {
       GemmArgs a{};
-      a.M = P.L; a.N = P.ni; a.K = P.nb; a.alpha = 1.0;
-      a.A = ws.Ub; a.lda = P.nb; a.sA = Lnb; a.tA = 0;
+      a.M = nleaf; a.N = P.ni; a.K = P.nb; a.alpha = 1.0;
+      a.A = ws.Ub + (long long)leaf0 * P.nb; a.lda = P.nb; a.sA = Lnb; a.tA = 0;
       a.B = ops.S_leaf; a.ldb = P.ldb; a.sB = 0; a.tB = 1;
-      a.beta = g ? 1.0 : 0.0; a.D = g ? ws.W : nullptr; a.ldd = ldw; a.sD = sw;
-      a.C = u; a.ldc = P.ni; a.sC = ld_u; a.batch = k;
+      a.beta = g ? 1.0 : 0.0; a.D = g ? ws.W + (long long)leaf0 * ldw : nullptr; a.ldd = ldw; a.sD = sw;
+      a.C = u + (long long)leaf0 * P.ni; a.ldc = P.ni; a.sC = ld_u; a.batch = k;
       if (int rc = gemm_nt(a, st)) return rc;
     } else {
       GemvArgs a{};
@@ -231,7 +282,7 @@ int solve(const Ops& ops, int k, const double* fb, long long ld_f, const double*
       a.xin = ws.Ub; a.xin_k = Lnb; a.xin_s = P.nb;
       a.yout = u; a.yout_k = ld_u; a.yout_s = P.ni;
       a.yadd = g ? ws.W : nullptr; a.yadd_k = Lni; a.yadd_s = P.ni;
-      if (int rc = gemv_level(a, ops.pSleaf, st)) return rc;
+      if (int rc = gemv_nodes(a, ops.pSleaf, leaf0, leaf0 + nleaf, st)) return rc;
     }
   }
   return 0;

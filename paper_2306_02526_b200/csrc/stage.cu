@@ -48,6 +48,7 @@ struct EvalArgs {
   const double* u; long long ld_u;
   int L, p, q, ni, nb, m, lpb;
   long long N;
+  long long ioff;                   // first interior DOF of the leaf range (lbg / sign / coef start there)
   const int* lbg;                   // L x nb
   const signed char* sign;          // L x nb
   const double* mats;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
   // interior: one contiguous run of nl*ni values
   for (int e = tid; e < nl * a.ni; e += NT) {
     int ll = e / a.ni, i = e % a.ni;
-    double v = u[(long long)l0 * a.ni + e];
+    double v = u[a.ioff + (long long)l0 * a.ni + e];
     U[ll * pp + (i / q + 1) * PS + (i % q + 1)] = v;
     gacc(gmax, v);
   }
@@ -206,9 +207,9 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
     if (inner) {
       const long long gi = (long long)l * a.ni + t;
       if (a.lu_int) a.lu_int[ob + gi] = lop;
-      if (a.lu) a.lu[ob + gi] = lop;
-      if (a.ux) a.ux[ob + gi] = ux;
-      if (a.uy) a.uy[ob + gi] = uy;
+      if (a.lu) a.lu[ob + a.ioff + gi] = lop;
+      if (a.ux) a.ux[ob + a.ioff + gi] = ux;
+      if (a.uy) a.uy[ob + a.ioff + gi] = uy;
     } else {
       const int j = t - a.ni;
       const long long gi = a.lbg[(long long)l * a.nb + j];
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
     __syncthreads();
     for (int e = tid; e < nl * NI; e += NT) {
       int l2 = e / NI, i = e % NI;
-      double v = u[(long long)l0 * NI + e];
+      double v = u[a.ioff + (long long)l0 * NI + e];
       U[l2 * PP + (i / Q + 1) * PS + (i % Q + 1)] = v;
       gacc(gmax, v);
     }
@@ -431,10 +432,21 @@ void hps_disc_destroy(hps_disc* h) {
 
 int hps_leaf_eval(const hps_disc* h, int k, const double* u, long long ld_u, double* lu_int, double* lu,
                   double* ux, double* uy, double* jump, long long ld_o, double* guard, void* stream) {
+  if (!h) { set_error("hps_leaf_eval: null argument"); return HPS_ERR_ARG; }
+  return hps_leaf_eval_range(h, 0, h->D.L, k, u, ld_u, lu_int, lu, ux, uy, jump, ld_o, guard, stream);
+}
+
+int hps_leaf_eval_range(const hps_disc* h, int leaf0, int nleaf, int k, const double* u, long long ld_u,
+                        double* lu_int, double* lu, double* ux, double* uy, double* jump, long long ld_o,
+                        double* guard, void* stream) {
   if (!h || !u) { set_error("hps_leaf_eval: null argument"); return HPS_ERR_ARG; }
-  if (k <= 0) return HPS_OK;
   const Disc& D = h->D;
   const Plan& P = *D.P;
+  if (leaf0 < 0 || nleaf < 0 || leaf0 + nleaf > P.L) {
+    set_error("hps_leaf_eval: leaf range [%d, %d) outside [0, %d)", leaf0, leaf0 + nleaf, P.L);
+    return HPS_ERR_ARG;
+  }
+  if (k <= 0 || nleaf == 0) return HPS_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const long long Lni = (long long)P.L * P.ni;
   // averaged outputs accumulate at edge DOFs; the flux jump is zero off the edges
@@ -447,22 +459,23 @@ int hps_leaf_eval(const hps_disc* h, int k, const double* u, long long ld_u, dou
     for (int kk = 0; kk < k; ++kk) HPSB_CUDA(cudaMemsetAsync(jump + kk * ld_o, 0, (size_t)P.N * 8, st));
   EvalArgs a{};
   a.k = k; a.u = u; a.ld_u = ld_u;
-  a.L = P.L; a.p = D.p; a.q = D.q; a.ni = D.ni; a.nb = D.nb; a.m = D.m; a.N = P.N;
+  a.L = nleaf; a.p = D.p; a.q = D.q; a.ni = D.ni; a.nb = D.nb; a.m = D.m; a.N = P.N;
+  a.ioff = (long long)leaf0 * D.ni;
   a.lpb = std::max(1, NT / (D.p * D.p));
-  a.lbg = P.leaf_bnd_gidx; a.sign = D.sign; a.mats = D.mats;
-  a.Lc = D.Lc; a.coef = D.coef;
+  a.lbg = P.leaf_bnd_gidx + (long long)leaf0 * D.nb; a.sign = D.sign + (long long)leaf0 * D.nb; a.mats = D.mats;
+  a.Lc = D.Lc; a.coef = D.Lc > 1 ? D.coef + (long long)leaf0 * 5 * D.m : D.coef;
   for (int i = 0; i < 5; ++i) a.cc[i] = D.cc[i];
   a.has_c1 = D.has_c1; a.has_c2 = D.has_c2; a.has_c = D.has_c;
   a.lu_int = lu_int; a.lu = lu; a.ux = ux; a.uy = uy; a.jump = jump; a.ld_o = ld_o;
   a.guard = reinterpret_cast<unsigned long long*>(guard);
   const int PS = (D.p + 1) | 1, QS = (D.q + 1) | 1;
   const int pp = D.p * PS, qq = D.q * QS;
-  unsigned groups = (unsigned)cdiv(P.L, a.lpb);
+  unsigned groups = (unsigned)cdiv(nleaf, a.lpb);
   dim3 grid(std::min(groups, (unsigned)(kNumSMs * 8)), (unsigned)k);
   const bool int_only = lu_int && !lu && !ux && !uy && !jump;
   if (int_only && (D.p == 10 || D.p == 12 || D.p == 16)) {
     a.lpb = std::max(1, 2048 / (D.p * D.p));  // ~2K staged values per iteration
-    groups = (unsigned)cdiv(P.L, a.lpb);
+    groups = (unsigned)cdiv(nleaf, a.lpb);
     grid.x = std::min(groups, (unsigned)(kNumSMs * 8));
     size_t sm2 = (size_t)a.lpb * pp * 8;
     const bool g1 = D.has_c1 || D.has_c2;

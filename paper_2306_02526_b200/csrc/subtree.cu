@@ -44,6 +44,7 @@ struct SubArgs {
   // subtree-local numbering (Plan::sub_slots)
   const int* slots; long long slot_off[MAXF + 1]; int j3_base[MAXF]; int nslots;
   const int* gidx_root;                         // level-dF gidx_bnd
+  int b0;                                       // first subtree of the launch
 };
 
 // y(row) = sum_col M[col][row] x[node(row)][col] over the CTA's tile, then
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_up(SubArgs a) {
   double* Hn = Hs + KM * a.hcap;      // this level's fluxes [node][KM][n12]
   double* r3s = Hn + KM * a.hcap;     // [node][KM][n3]
   double* red = r3s + KM * a.rcap;    // 2 * NT * KM
-  const int b = blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x;
+  const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x;
   pdl_trigger();
   pdl_wait();
   for (int e = a.nf - 1; e >= 0; --e) {
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
   extern __shared__ double sm[];
   double* red = sm;                // 2 * NT * KM
   double* xs = sm + 2 * NT * KM;   // [node][KM][n12]
-  const int b = blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x;
+  const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x;
   pdl_trigger();
   pdl_wait();
   for (int e = 0; e < a.nf; ++e) {
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_down_local(SubArgs 
   double* red = sm;                        // 2 * NT * KM
   double* uloc = sm + 2 * NT * KM;         // [KM][nslots]
   double* xs = uloc + KM * a.nslots;       // [node][KM][n12]
-  const int b = blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x, ns = a.nslots;
+  const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x, ns = a.nslots;
   pdl_trigger();
   pdl_wait();
   {
@@ -269,7 +270,7 @@ void fill_args(const Ops& ops, const Workspace& ws, int k, SubArgs& a) {
 }
 
 template <class K>
-int launch_sub(K kern, const Plan& P, int KM, int k, size_t smem, const SubArgs& a, cudaStream_t st) {
+int launch_sub(K kern, int nsub, int KM, int k, size_t smem, const SubArgs& a, cudaStream_t st) {
   if (smem > 227 * 1024) {
     set_error("subtree kernel needs %zu bytes of shared memory", smem);
     return -1;
@@ -277,7 +278,8 @@ int launch_sub(K kern, const Plan& P, int KM, int k, size_t smem, const SubArgs&
   static bool attr = false;  // per instantiation
   (void)attr;
   HPSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)P.lv[P.dF].c, (unsigned)cdiv(k, KM));
+  if (nsub <= 0) return 0;
+  dim3 grid((unsigned)nsub, (unsigned)cdiv(k, KM));
   HPSB_CUDA(launch_pdl(kern, grid, dim3(NT), smem, st, a));
   HPSB_LAUNCH_CHECK();
   return 0;
@@ -306,25 +308,27 @@ int fuse_level(const Plan& P) {
 }
 
 int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, long long sh, long long hs,
-               const double* jump, long long ld_jump, double inv_dt, cudaStream_t st) {
+               const double* jump, long long ld_jump, double inv_dt, int b0, int b1, cudaStream_t st) {
   const Plan& P = *ops.plan;
   if (P.dF >= P.depth) return 0;
   SubArgs a{};
   fill_args(ops, ws, k, a);
+  a.b0 = b0;
   a.Hleaf = Hleaf; a.sh = sh; a.hs = hs;
   a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt;
   const int KM = k == 1 ? 1 : 4;
   const size_t smem = (size_t)KM * (2 * a.hcap + a.rcap + 2 * NT) * 8;
-  if (KM == 1) return launch_sub(k_sub_up<1>, P, 1, k, smem, a, st);
-  return launch_sub(k_sub_up<4>, P, 4, k, smem, a, st);
+  if (KM == 1) return launch_sub(k_sub_up<1>, b1 - b0, 1, k, smem, a, st);
+  return launch_sub(k_sub_up<4>, b1 - b0, 4, k, smem, a, st);
 }
 
-int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u,
-                 cudaStream_t st) {
+int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u, int b0,
+                 int b1, cudaStream_t st) {
   const Plan& P = *ops.plan;
   if (P.dF >= P.depth) return 0;
   SubArgs a{};
   fill_args(ops, ws, k, a);
+  a.b0 = b0;
   a.u = u; a.u_k = ld_u; a.has_w3 = has_w3 ? 1 : 0;
   const int KM = k == 1 ? 1 : 4;
   int xcap = 0;
@@ -332,13 +336,13 @@ int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double
   if (P.sub_local) {
     const size_t smem = (size_t)KM * (xcap + a.nslots + 2 * NT) * 8;
     if (smem <= 200 * 1024) {
-      if (KM == 1) return launch_sub(k_sub_down_local<1>, P, 1, k, smem, a, st);
-      return launch_sub(k_sub_down_local<4>, P, 4, k, smem, a, st);
+      if (KM == 1) return launch_sub(k_sub_down_local<1>, b1 - b0, 1, k, smem, a, st);
+      return launch_sub(k_sub_down_local<4>, b1 - b0, 4, k, smem, a, st);
     }
   }
   const size_t smem = (size_t)KM * (xcap + 2 * NT) * 8;
-  if (KM == 1) return launch_sub(k_sub_down<1>, P, 1, k, smem, a, st);
-  return launch_sub(k_sub_down<4>, P, 4, k, smem, a, st);
+  if (KM == 1) return launch_sub(k_sub_down<1>, b1 - b0, 1, k, smem, a, st);
+  return launch_sub(k_sub_down<4>, b1 - b0, 4, k, smem, a, st);
 }
 
 }  // namespace hpsb

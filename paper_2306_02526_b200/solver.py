@@ -25,9 +25,12 @@ FORMAT_VERSION = 1
 
 
 class DevicePlan:
-    """Device copy of the tree numbering (one per tree and device)."""
+    """Device copy of the tree numbering (one per tree, partition and device).
 
-    def __init__(self, tree):
+    ``nparts`` > 1 cuts the tree into the 2^lstar subtrees of parent level
+    lstar so a solve can run part by part (multi-GPU)."""
+
+    def __init__(self, tree, nparts=1):
         lib = _lib.load()
         cuda_device()  # raises without a GPU
         self.tree = tree
@@ -58,11 +61,16 @@ class DevicePlan:
         d.leaf_bnd_gidx = _lib.int_ptr(arr(tree.leaf_bnd_gidx))
         d.leaf_node_index = _lib.ll_ptr(arr(tree.leaves, np.int64))
         d.boundary_ids = _lib.int_ptr(arr(tree.boundary_ids))
+        d.nparts = int(nparts)
         h = ctypes.c_void_p()
         _lib.check(lib.hps_plan_create(ctypes.byref(d), ctypes.byref(h)), "hps_plan_create")
         self.handle = h
         self._lib = lib
         self._ws = {}
+        npt, ls, n12 = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(lib.hps_plan_partition(h, 1, ctypes.byref(npt), ctypes.byref(ls), ctypes.byref(n12), None),
+                   "hps_plan_partition")
+        self.nparts, self.lstar, self.flux_n12 = npt.value, ls.value, n12.value
         dev = cuda_device()
         self.boundary_ids = torch.as_tensor(tree.boundary_ids, device=dev)
 
@@ -74,6 +82,19 @@ class DevicePlan:
             self._ws[k] = ws
         return ws
 
+    def flux_block(self, k):
+        """(k, nparts, n12) view of the workspace's level-lstar flux block
+        (what the UP phase leaves for the TOP phase; all-gathered between
+        GPUs in a sharded solve)."""
+        off = ctypes.c_longlong()
+        _lib.check(self._lib.hps_plan_partition(self.handle, k, None, None, None, ctypes.byref(off)),
+                   "hps_plan_partition")
+        if off.value < 0:
+            raise HpstepError("plan has no subtree partition")
+        ws = self.workspace(k)
+        n = k * self.nparts * self.flux_n12
+        return ws[off.value:off.value + 8 * n].view(torch.float64).view(k, self.nparts, self.flux_n12)
+
     def __del__(self):
         try:
             if self.handle:
@@ -82,11 +103,13 @@ class DevicePlan:
             pass
 
 
-def device_plan(tree):
-    p = getattr(tree, "_device_plan", None)
+def device_plan(tree, nparts=1):
+    cache = getattr(tree, "_device_plans", None)
+    if cache is None:
+        cache = tree._device_plans = {}
+    p = cache.get(int(nparts))
     if p is None:
-        p = DevicePlan(tree)
-        tree._device_plan = p
+        p = cache[int(nparts)] = DevicePlan(tree, nparts)
     return p
 
 
@@ -118,7 +141,7 @@ class HpsOperatorSet:
     safe (each stream gets its own workspace).
     """
 
-    def __init__(self, disc, sigma, dt_gamma, keep_dtn=False, threads=None, layout=None):
+    def __init__(self, disc, sigma, dt_gamma, keep_dtn=False, threads=None, layout=None, nparts=1):
         self.disc = disc
         self.tree = disc.tree
         self.sigma = float(sigma)
@@ -127,7 +150,7 @@ class HpsOperatorSet:
         self.layout = resolve_layout(layout, disc.coeffs)
         st = disc.stencil
         self.D_bi = st.D_bnd[:, :st.ni]
-        self.plan = device_plan(self.tree)
+        self.plan = device_plan(self.tree, nparts)
         self._build()
 
     @property
@@ -276,6 +299,25 @@ class HpsOperatorSet:
         _lib.check(rc, "hps_solve")
         return out
 
+    def solve_phase(self, phases, part0, part1, fb, body, out, jump=None, inv_dt=None):
+        """One or more phases of a subtree-partitioned solve (hps_solve_phase):
+        ``_lib.HPS_PHASE_UP`` / ``TOP`` / ``DOWN`` over parts [part0, part1).
+        ``body`` rows start at the first leaf of part0 (or None); ``out`` (k, N)
+        rows are global."""
+        k = out.shape[0]
+        ld_f = 0 if fb.shape[0] == 1 else fb.stride(0)
+        ld_g = 0 if body is None or body.shape[0] == 1 else body.stride(0)
+        ld_j = 0 if jump is None or jump.shape[0] == 1 else jump.stride(0)
+        ws = self.plan.workspace(k)
+        rc = self._lib.hps_solve_phase(
+            self.handle, int(phases), int(part0), int(part1), k, fb.data_ptr(), ld_f,
+            None if body is None else body.data_ptr(), ld_g,
+            None if jump is None else jump.data_ptr(), ld_j,
+            0.0 if inv_dt is None else float(inv_dt), out.data_ptr(), out.stride(0),
+            ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_solve_phase")
+        return out
+
     # -- operator views (reference solver.py:339-348) ---------------------------------
     def _leaf_block(self, which, leaf):
         st = self.disc.stencil
@@ -349,7 +391,7 @@ class HpsOperatorSet:
         buf = np.empty(n, dtype=np.uint8)
         _lib.check(lib.hps_ops_dump(self.handle, buf.ctypes.data_as(ctypes.c_void_p), n), "hps_ops_dump")
         head = json.dumps({"header": _jsonable(self.header()), "layout": self.layout,
-                           "keep_dtn": self.keep_dtn}).encode()
+                           "keep_dtn": self.keep_dtn, "nparts": self.plan.nparts}).encode()
         with open(path, "wb") as fh:
             fh.write(self._DUMP_MAGIC)
             fh.write(len(head).to_bytes(8, "little"))
@@ -376,7 +418,7 @@ class HpsOperatorSet:
             raise HpstepError("operator dump does not match the requested configuration "
                               f"(dump header {meta['header']})")
         obj.layout, obj.keep_dtn = meta["layout"], bool(meta["keep_dtn"])
-        obj.plan = device_plan(obj.tree)
+        obj.plan = device_plan(obj.tree, meta.get("nparts", 1))
         lib = obj.plan._lib
         h = ctypes.c_void_p()
         _lib.check(lib.hps_ops_load(obj.plan.handle, payload.ctypes.data_as(ctypes.c_void_p), payload.size,
@@ -486,9 +528,10 @@ def resolve_layout(layout, coeffs):
     return layout
 
 
-def build(tree, coeffs, sigma=0.0, dt_gamma=1.0, disc=None, keep_dtn=False, threads=None, layout=None):
+def build(tree, coeffs, sigma=0.0, dt_gamma=1.0, disc=None, keep_dtn=False, threads=None, layout=None,
+          nparts=1):
     """Build the operator set for ``sigma*I + dt_gamma*A`` on the GPU."""
     if disc is None:
         disc = EllipticDiscretization(tree, coeffs)
     return HpsOperatorSet(disc, sigma=sigma, dt_gamma=dt_gamma, keep_dtn=keep_dtn, threads=threads,
-                          layout=layout)
+                          layout=layout, nparts=nparts)

@@ -162,15 +162,19 @@ class DeviceDiscretization:
         except Exception:
             pass
 
-    def eval(self, U, lu_int=None, lu=None, ux=None, uy=None, jump=None, guard=None, ld_o=None):
-        """One leaf pass over the (k, N) device tensor U (row stride U.stride(0))."""
+    def eval(self, U, lu_int=None, lu=None, ux=None, uy=None, jump=None, guard=None, ld_o=None,
+             leaves=None):
+        """One leaf pass over the (k, N) device tensor U (row stride U.stride(0)).
+        ``leaves = (leaf0, nleaf)`` restricts it to a leaf range (lu_int rows
+        then start at leaf0's interior; see hps_leaf_eval_range)."""
         outs = [lu_int, lu, ux, uy, jump]
         if ld_o is None:
             ld_o = next((o.stride(0) for o in outs if o is not None), 0)
         ptr = lambda o: None if o is None else o.data_ptr()
-        rc = self._lib.hps_leaf_eval(self.handle, U.shape[0], U.data_ptr(), U.stride(0),
-                                     *[ptr(o) for o in outs], ld_o, ptr(guard),
-                                     current_stream_handle())
+        leaf0, nleaf = (0, self.tree.L) if leaves is None else leaves
+        rc = self._lib.hps_leaf_eval_range(self.handle, leaf0, nleaf, U.shape[0], U.data_ptr(), U.stride(0),
+                                           *[ptr(o) for o in outs], ld_o, ptr(guard),
+                                           current_stream_handle())
         _lib.check(rc, "hps_leaf_eval")
 
     def _prep(self, u):
@@ -391,6 +395,10 @@ class TimeStepper:
                           self._dev)
         self._Q = _Field(problem.q, self._all_pts, k, self._dev)
         self._bufs = {}
+        # the leaf-interior DOF range this process steps (everything on one GPU;
+        # a subtree part range in sharding.ShardedTimeStepper)
+        self._ir = (0, self._dd.Lni)
+        self._nloc = self._dd.Lni
         self._dry = False          # dry pass: record combination coefficients only
         self._graph = None         # captured CUDA graph of one step (see _run_graph)
         self._graph_failed = False
@@ -413,7 +421,8 @@ class TimeStepper:
             return
         self.dt = float(dt)
         self.ops = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=self.dt * self.pair.gamma,
-                                  threads=self.threads, layout=self.layout)
+                                  threads=self.threads, layout=self.layout,
+                                  nparts=getattr(self, "_nparts", 1))
         if self.formulation != "stage" and self.ops_id is None:
             self.ops_id = HpsOperatorSet(self.disc, sigma=1.0, dt_gamma=0.0, threads=self.threads,
                                          layout=self.layout)
@@ -467,7 +476,7 @@ class TimeStepper:
             except _CaptureFailed:
                 pass
         new, guards = self._advance(state)
-        self._raise_if_diverged(guards, self._step_count)
+        self._raise_if_diverged(self._reduce_guards(guards), self._step_count)
         self._step_count += 1
         return new
 
@@ -535,18 +544,27 @@ class TimeStepper:
         finally:
             _CoefSink.current = None
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+
+        def body():
             _CoefSink.current = _CoefSink(dev=coef)
             try:
                 guards.zero_()
                 self._step_body(t, gin, guards, gin)
             finally:
                 _CoefSink.current = None
+
+        graph = self._capture_graph(body)
         ring = 4
         self._graph = dict(graph=graph, gin=gin, guards=guards, coef=coef, ncoef=len(vals), key=self._graph_key(gin),
                            pinned=[torch.zeros(len(vals) + 8, dtype=torch.float64).pin_memory() for _ in range(ring)],
                            events=[None] * ring, slot=0)
+
+    def _capture_graph(self, body):
+        """One CUDA graph of ``body`` (anything with ``replay()``)."""
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            body()
+        return graph
 
     def _graph_key(self, u):
         return (tuple(u.shape), self.dt, id(self.ops))
@@ -591,7 +609,7 @@ class TimeStepper:
             hist[(step - done) % hist.shape[0]].copy_(guards)
             t += self.dt
             if step + 1 - done == hist.shape[0] or step + 1 == nsteps:
-                host = hist[:step + 1 - done].cpu().numpy()
+                host = self._reduce_guards(hist[:step + 1 - done]).cpu().numpy()
                 for g in host:
                     self._raise_if_diverged(g, self._step_count, host_vals=True)
                     self._step_count += 1
@@ -602,7 +620,7 @@ class TimeStepper:
     def _drain(self, pending):
         if not pending:
             return
-        host = torch.stack(pending).cpu().numpy()
+        host = self._reduce_guards(torch.stack(pending)).cpu().numpy()
         for g in host:
             self._raise_if_diverged(g, self._step_count, host_vals=True)
             self._step_count += 1
@@ -640,6 +658,28 @@ class TimeStepper:
         if not self._dry:
             self._dd.eval(U, **kw)
 
+    # -- hooks over the DOFs this process owns (sharding.ShardedTimeStepper) ------------
+    def _iv(self, v):
+        """View of a full (rows, N) vector starting at this process's first
+        leaf-interior DOF (what combines over the local interior range read)."""
+        a = self._ir[0]
+        return v if a == 0 else v[:, a:]
+
+    def _eval_lu(self, U, out, guard=None):
+        """Stage history L u at the local leaf interiors."""
+        self._eval(U, lu_int=out, guard=guard)
+
+    def _owned_combine(self, terms, out):
+        """out = sum c v over every DOF this process owns."""
+        combine(terms, out)
+
+    def _owned_maxabs(self, x, guard):
+        self._maxabs(x, guard)
+
+    def _reduce_guards(self, g):
+        """Guard maxima over every process (identity on one GPU)."""
+        return g
+
     def _maxabs(self, x, guard):
         if not self._dry:
             k, n = x.shape
@@ -669,22 +709,24 @@ class TimeStepper:
     def _step_backward_euler(self, t, u, guards, out=None):
         dt, k, N = self.dt, u.shape[0], self.tree.N
         t1 = t + dt
-        r = self._buf("r", (k, self._dd.Lni))
-        terms = [(1.0, u)] + self._Q.terms(t1, dt)
+        iv = self._iv
+        r = self._buf("r", (k, self._nloc))
+        terms = [(1.0, iv(u))] + [(c, iv(v)) for c, v in self._Q.terms(t1, dt)]
         G = self._g(t, u)
         if G is not None:
-            terms.append((dt, G))
-        combine(terms, r, n=self._dd.Lni)
+            terms.append((dt, iv(G)))
+        combine(terms, r, n=self._nloc)
         unew = torch.empty((k, N), dtype=torch.float64, device=self._dev) if out is None else out
         self._solve(self.ops, self._bc(t1), r, unew)
-        self._maxabs(unew, guards[0])
+        self._owned_maxabs(unew, guards[0])
         return unew
 
     def _step_stage(self, t, u, guards, out=None):
         """timestep.py:237-266 on the device."""
         pair, dt = self.pair, self.dt
-        s, k, N, Lni = pair.s, u.shape[0], self.tree.N, self._dd.Lni
+        s, k, N, Lni = pair.s, u.shape[0], self.tree.N, self._nloc
         A, Ah = pair.A, pair.Ahat
+        iv = self._iv
         Lu = self._buf("Lu", (s, k, Lni))
         nonlin = self.problem.g is not None
         QG = self._buf("QG", (s, k, N)) if (nonlin or (self._Q.fn is not None and self._Q.sep is None)) \
@@ -703,29 +745,29 @@ class TimeStepper:
                 if G is not None:
                     terms.append((1.0, G))
                 if terms:
-                    combine(terms, QG[i])
+                    self._owned_combine(terms, QG[i])
                 elif not self._dry:
                     QG[i].zero_()
 
-        self._eval(u, lu_int=Lu[0])
+        self._eval_lu(u, Lu[0])
         stage_q_g(0, t + pair.c[0] * dt, u)
         ui = u
         for i in range(1, s):
             ti = t + pair.c[i] * dt
-            terms = [(1.0, u)]
+            terms = [(1.0, iv(u))]
             terms += [(dt * A[i, j], Lu[j]) for j in range(i)]
             if QG is not None:
-                terms += [(dt * Ah[i, j], QG[j]) for j in range(i)]
+                terms += [(dt * Ah[i, j], iv(QG[j])) for j in range(i)]
             if qsep is not None:
                 for m, phi in enumerate(qsep):
-                    terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), phi))
+                    terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), iv(phi)))
             combine(terms, r, n=Lni)
             ui = U[i & 1]
             self._solve(self.ops, self._bc(ti), r, ui)
             if i < s - 1:
-                self._eval(ui, lu_int=Lu[i], guard=guards[i - 1])
+                self._eval_lu(ui, Lu[i], guard=guards[i - 1])
             else:
-                self._maxabs(ui, guards[i - 1])
+                self._owned_maxabs(ui, guards[i - 1])
             stage_q_g(i, ti, ui)
         w = pair.bhat - Ah[s - 1]
         terms = [(1.0, ui)]
@@ -736,9 +778,9 @@ class TimeStepper:
                 terms.append((sum(dt * w[j] * qfac[j][m] for j in range(s)), phi))
         # `out` may alias `u`: nothing below reads u
         unew = torch.empty((k, N), dtype=torch.float64, device=self._dev) if out is None else out
-        combine(terms, unew)
+        self._owned_combine(terms, unew)
         self._put_boundary(self._bc(t + dt), unew)
-        self._maxabs(unew, guards[s - 1])
+        self._owned_maxabs(unew, guards[s - 1])
         return unew
 
     # -- slope formulations (timestep.py:268-328) ----------------------------------------

@@ -75,3 +75,160 @@ def test_gloo_two_ranks_gather_and_max():
         full, t = out[r]
         assert np.array_equal(np.array(full), np.arange(15.0).reshape(5, 3))
         assert t == 11.0
+
+
+# ---------------------------------------------------------------------------
+# subtree sharding: the partition, the per-stage flux
+# all-gather, the top-interface gradient completion and the final gather,
+# driven by a partitioned restatement of the oracle solve on 2 gloo ranks
+# ---------------------------------------------------------------------------
+
+def _partition_solve(ops, part, p0, p1, f, G, exchange, gather):
+    """The oracle solve (oracle/hps_oracle.py OHps.solve) split like
+    hps_solve_phase: UP over the parts' leaves and levels >= lstar, the flux
+    exchange, TOP, DOWN over the parts."""
+    tree, st = ops.tree, ops.disc.st
+    ni, ls, P = st.ni, part.lstar, part.nparts
+    k = G.shape[0]
+    fb = np.broadcast_to(ops.boundary_values(f), (k, tree.boundary_ids.size))
+    lid0, nl = part.leaves(p0, p1)
+    own_leaves = range(lid0, lid0 + nl)
+    lu = ops.leaf_lu[0]
+    w, hleaf = {}, {}
+    for l in own_leaves:
+        w[l] = lu.solve(G[:, tree.leaf_int_gidx[l]].T).T
+        hleaf[l] = w[l] @ ops.D_bi.T
+    H, W3 = {}, {}
+
+    def h(kk):
+        nd = tree.nodes[kk]
+        return hleaf[nd["lid"]] if nd["children"] is None else H[kk]
+
+    def up(kk):
+        nd = tree.nodes[kk]
+        S, f3, Tst = ops.merges[kk]
+        ha, hb = h(nd["children"][0]), h(nd["children"][1])
+        W3[kk] = f3.solve((hb[:, nd["i3b"]] - ha[:, nd["i3a"]]).T).T
+        H[kk] = np.concatenate([ha[:, nd["i1a"]], hb[:, nd["i2b"]]], axis=1) + W3[kk] @ Tst.T
+
+    def own_nodes(d):
+        lvl = [kk for kk in tree.levels[d] if tree.nodes[kk]["children"] is not None]
+        per = len(lvl) // P
+        return lvl[p0 * per:p1 * per]
+
+    for d in range(tree.depth - 2, ls - 1, -1):      # UP: the parts' levels, deepest first
+        for kk in own_nodes(d):
+            up(kk)
+    top_nodes = tree.levels[ls]
+    n12 = tree.nodes[top_nodes[0]]["bnd"].size
+    block = np.zeros((k, P, n12))
+    for g in range(p0, p1):
+        block[:, g] = H[top_nodes[g]]
+    block = exchange(block, p0, p1)                  # every part's level-lstar flux
+    for g in range(P):
+        H[top_nodes[g]] = block[:, g]
+    u = np.zeros((k, tree.N))
+    u[:, tree.boundary_ids] = fb
+    for d in range(ls - 1, -1, -1):                  # TOP
+        for kk in tree.levels[d]:
+            up(kk)
+
+    def down(kk):
+        nd = tree.nodes[kk]
+        u[:, nd["j3"]] = u[:, nd["bnd"]] @ ops.merges[kk][0].T + W3[kk]
+
+    for d in range(ls):
+        for kk in tree.levels[d]:
+            down(kk)
+    for d in range(ls, tree.depth - 1):              # DOWN
+        for kk in own_nodes(d):
+            down(kk)
+    for l in own_leaves:
+        u[:, tree.leaf_int_gidx[l]] = u[:, tree.leaf_bnd_gidx[l]] @ ops.S_leaf[0].T + w[l]
+    return gather(u)
+
+
+def _subtree_worker(rank, world, port, nparts, out):
+    import torch
+    import torch.distributed as dist
+    from oracle import hps_oracle as O
+    from paper_2306_02526_b200.sharding import (SubtreePartition, complete_edges, exchange_fluxes,
+                                                gather_owned)
+    from paper_2306_02526_b200.tree import build_tree
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, p, k = 8, 8, 2
+        ot = O.OTree(((0.0, 1.0), (0.0, 1.0)), n, n, p)
+        ops = O.OHps(O.ODisc(ot, O.OCoeffs(1.0, 1.0)), sigma=1.0, dt_gamma=0.01)
+        part = SubtreePartition(build_tree(((0.0, 1.0), (0.0, 1.0)), n, n, p), nparts)
+        p0, p1 = part.owner_parts(rank, world)
+        rng = np.random.default_rng(5)
+        G = rng.standard_normal((k, ot.N))
+        f = rng.standard_normal(ot.boundary_ids.size)
+        owned = torch.as_tensor(part.owned_ids(p0, p1, with_top=rank == 0))
+
+        def exchange(block, a, b):
+            t = torch.from_numpy(np.ascontiguousarray(block))
+            return exchange_fluxes(t, a, b).numpy()
+
+        def gather(u):
+            return gather_owned(torch.from_numpy(u), owned).numpy()
+
+        u = _partition_solve(ops, part, p0, p1, f, G, exchange, gather)
+        ref = ops.solve(np.broadcast_to(f, (k, f.size)), G)
+        # gradient partial sums of the own leaves, completed on the top interfaces
+        uu = rng.standard_normal((1, ot.N))
+        lid0, nl = part.leaves(p0, p1)
+        gi = ot.leaf_gidx[lid0:lid0 + nl]
+        vals = uu[:, gi] @ ops.disc.st.Ex1.T
+        part_ux = np.bincount(gi.ravel(), weights=vals[0].ravel(), minlength=ot.N) / np.maximum(ot.mult, 1)
+        ux = torch.from_numpy(part_ux[None].copy())
+        complete_edges([ux], torch.as_tensor(part.top_ids))
+        full_ux = ops.disc.gradient(uu[0])[0]
+        check = np.concatenate([part.owned_ids(p0, p1, with_top=False), part.top_ids])
+        out[rank] = dict(err=float(np.abs(u - ref).max() / np.abs(ref).max()),
+                         gerr=float(np.abs(ux.numpy()[0, check] - full_ux[check]).max()),
+                         owned=part.owned_ids(p0, p1, with_top=rank == 0).tolist())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nparts", [2, 4])
+def test_gloo_two_ranks_subtree_partitioned_solve(nparts):
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_subtree_worker, args=(world, port, nparts, out), nprocs=world, join=True)
+    owned = []
+    for r in range(world):
+        assert out[r]["err"] < 1e-13
+        assert out[r]["gerr"] < 1e-13
+        owned += out[r]["owned"]
+    # the ranks' owned DOFs partition the global vector
+    from paper_2306_02526_b200.tree import build_tree
+    N = build_tree(((0.0, 1.0), (0.0, 1.0)), 8, 8, 8).N
+    assert sorted(owned) == list(range(N))
+
+
+def test_subtree_partition_ranges():
+    from paper_2306_02526_b200.sharding import SubtreePartition
+    from paper_2306_02526_b200.tree import build_tree
+    from paper_2306_02526_b200.errors import UnsupportedConfigurationError
+    tree = build_tree(((0.0, 1.0), (0.0, 1.0)), 8, 8, 6)
+    part = SubtreePartition(tree, 4)
+    assert part.lstar == 2 and part.lpp == 16
+    assert part.owner_parts(1, 2) == (2, 4)
+    assert part.leaves(2, 4) == (32, 32)
+    assert part.interior_range(0, 1) == (0, 16 * tree.ni)
+    # top interfaces = j3 of the two top parent levels
+    lms = tree.level_maps
+    assert part.top_ids.size == lms[0].n3 + 2 * lms[1].n3
+    allids = np.concatenate([part.owned_ids(g, g + 1, with_top=g == 0) for g in range(4)])
+    assert np.array_equal(np.sort(allids), np.arange(tree.N))
+    for bad in (3, 128):
+        with pytest.raises(UnsupportedConfigurationError):
+            SubtreePartition(tree, bad)
+    with pytest.raises(UnsupportedConfigurationError):
+        part.owner_parts(0, 3)
