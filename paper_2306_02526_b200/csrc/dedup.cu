@@ -27,7 +27,8 @@ constexpr int BM = 64;  // nodes per CTA tile (2 warps of 32 rows)
 enum GsMode { GS_UP = 0, GS_DOWN = 1 };
 
 struct GsArgs {
-  int M, N, K;                 // nodes, operator rows, operator columns
+  int M, N, K;                 // nodes x rhs (row m: node m % nodes, rhs m / nodes), operator rows, columns
+  int nodes;
   const double* B; int ldb;    // operator, N x K row-major
   GemvArgs g;                  // gathers / scatters (same fields as the streaming kernels)
 };
@@ -70,6 +71,8 @@ __device__ __forceinline__ void gs_out(const GemvArgs& a, int node, int r, int k
   }
 }
 
+// Every (node, rhs) pair is one row of the GEMM: the multi-rhs (ensemble)
+// level apply is one tensor-core GEMM over nodes x rhs.
 template <int MODE, int WN>
 __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
   constexpr int BN = 32 * WN, NT = 64 * WN;
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
   double* As = sm;                  // [2][BM][SROW]
   double* Bs = sm + 2 * BM * SROW;  // [2][BN][SROW]
   const int tm = blockIdx.x / tilesN, tn = blockIdx.x % tilesN;
-  const int m0 = tm * BM, n0 = tn * BN, kg = blockIdx.y;
+  const int m0 = tm * BM, n0 = tn * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WN, wn = warp % WN;
   const int nk = (a.K + BK - 1) / BK;
@@ -98,7 +101,7 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
     for (int i = 0; i < AE; ++i) {
       const int e = tid + NT * i, r = e / BK, c = e % BK;
       const int gm = m0 + r, gk = kt * BK + c;
-      ra[i] = (gm < a.M && gk < a.K) ? gs_x<MODE>(a.g, gm, kg, gk) : 0.0;
+      ra[i] = (gm < a.M && gk < a.K) ? gs_x<MODE>(a.g, gm % a.nodes, gm / a.nodes, gk) : 0.0;
     }
   };
   auto store = [&](int buf) {
@@ -148,8 +151,9 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
 
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int node = m0 + wm * 32 + i * 8 + (lane >> 2);
-    if (node >= a.M) continue;
+    const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+    if (m >= a.M) continue;
+    const int node = m % a.nodes, kg = m / a.nodes;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -170,7 +174,7 @@ int launch_gs(const GsArgs& a, int k, cudaStream_t st) {
     attr = true;
   }
   const int tilesM = (int)cdiv(a.M, BM), tilesN = (int)cdiv(a.N, BN);
-  dim3 grid((unsigned)(tilesM * tilesN), (unsigned)k);
+  dim3 grid((unsigned)(tilesM * tilesN));
   HPSB_CUDA(launch_pdl(k_gs<MODE, WN>, grid, dim3(64 * WN), smem, st, a, tilesN));
   HPSB_LAUNCH_CHECK();
   return 0;
@@ -179,13 +183,21 @@ int launch_gs(const GsArgs& a, int k, cudaStream_t st) {
 template <int MODE>
 int gs(const GsArgs& a, int k, cudaStream_t st) {
   // operator rows per CTA tile: enough tiles to fill the SMs, little padding waste
-  const long long tilesM = cdiv(a.M, BM) * (long long)k;
+  const long long tilesM = cdiv(a.M, BM);
   if (a.N <= 32 || tilesM * cdiv(a.N, 64) < 2 * kNumSMs) return launch_gs<MODE, 1>(a, k, st);
   if (a.N <= 64 || tilesM * cdiv(a.N, 128) < 2 * kNumSMs) return launch_gs<MODE, 2>(a, k, st);
   return launch_gs<MODE, 4>(a, k, st);
 }
 
 }  // namespace
+
+// the level apply as a DMMA GEMM over (node, rhs) rows: many nodes, or a
+// multi-rhs solve (the streaming kernel otherwise); levels whose one-node
+// panel is node-aligned (fused subtree levels) always take the GEMM
+bool shared_gemm(const Plan& P, int d, int nodes, int k) {
+  if (d >= P.dF) return true;
+  return (long long)nodes * k >= kSharedGemmNodes || (k >= kSharedGemmRhs && (long long)nodes * k >= 256);
+}
 
 int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const double* Hc, long long Hc_k,
                     long long Hc_s, const double* jump, long long ld_jump, double inv_dt, int n0, int n1,
@@ -201,12 +213,13 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
   g.jump = jump; g.jump_k = ld_jump; g.inv_dt = inv_dt; g.j3 = lv.j3;
   g.Hout = d > 0 ? ws.H[d] : nullptr; g.Hout_k = (long long)lv.c * lv.n12;
   g.mode = GEMV_UP;
-  if (lv.c < kSharedGemmNodes) {
+  if (!shared_gemm(P, d, n1 - n0, k)) {
     g.shared = 1;
     return gemv_nodes(g, lo.Up, n0, n1, st);
   }
   GsArgs a{};
-  a.M = n1 - n0;
+  a.nodes = n1 - n0;
+  a.M = a.nodes * k;
   a.N = lv.n3 + (d > 0 ? lv.n12 : 0); a.K = lv.n3;
   g = shift_nodes(g, n0);
   a.B = lo.Ush; a.ldb = lv.ld3; a.g = g;
@@ -223,12 +236,13 @@ int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool ha
   g.u = u; g.u_k = ld_u; g.gidx = lv.gidx_bnd; g.j3 = lv.j3; g.n3 = lv.n3; g.n12 = lv.n12;
   g.W3 = has_w3 ? ws.W3[d] : nullptr; g.W3_k = (long long)lv.c * lv.n3;
   g.mode = GEMV_DOWN;
-  if (lv.c < kSharedGemmNodes) {
+  if (!shared_gemm(P, d, n1 - n0, k)) {
     g.shared = 1;
     return gemv_nodes(g, lo.S, n0, n1, st);
   }
   GsArgs a{};
-  a.M = n1 - n0;
+  a.nodes = n1 - n0;
+  a.M = a.nodes * k;
   a.N = lv.n3; a.K = lv.n12;
   g = shift_nodes(g, n0);
   a.B = lo.Ssh; a.ldb = lv.ld12; a.g = g;

@@ -151,7 +151,8 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
 
 // level GEMV launcher (see level_gemv.cu)
 enum GemvMode { GEMV_UP = 0, GEMV_DOWN = 2, GEMV_LEAF = 3 };
-constexpr int kSharedGemmNodes = 1024;  // shared layout: levels with at least this many nodes use the GEMM
+constexpr int kSharedGemmNodes = 1024;  // shared layout: levels with at least this many (node, rhs) rows use the GEMM
+constexpr int kSharedGemmRhs = 16;      // ... and multi-rhs solves from this many rhs on (fused subtree kernels off)
 
 struct GemvArgs {
   int mode;
@@ -195,6 +196,7 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
                     cudaStream_t st);
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
                       int n0, int n1, cudaStream_t st);
+bool shared_gemm(const Plan& P, int d, int nodes, int k);
 
 // tensor-product leaf solve (leaf_fd.cu): [w | h] rows from the body load
 // nleaf leaves: g and WH point at the first one

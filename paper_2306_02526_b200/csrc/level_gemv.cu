@@ -211,6 +211,89 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
   }
 }
 
+// Shared-layout levels with many nodes (the mid levels of the tree): the
+// level's single operator (one-node panel, TR-row tiles) is applied to NB
+// nodes per CTA.  The CTA stages the NB nodes' whole input vectors in shared
+// memory (one gather pass), its 256 threads are G = 256/(TR/2) column groups
+// of TR/2 threads (two rows each) streaming K/G columns of the tile from L2,
+// the groups' partial sums meet in shared memory (in group order: bitwise
+// reproducible) and the TR x NB outputs are spread over all threads for the
+// epilogue.  No split-K through global memory, no semaphores: the latency
+// chain is gather -> short stream -> reduce -> scatter.
+constexpr int kVnThreads = 256;
+
+template <int MODE, int NB, int U>
+__global__ void __launch_bounds__(kVnThreads) k_vn(GemvArgs a, Panel pn, int XS) {
+  extern __shared__ double sm[];
+  double* xs = sm;                    // [NB][XS] input slots
+  double* red = sm + NB * XS;         // [G][NB][TR] partial sums
+  const int TR = pn.TR, C = pn.C, P2 = TR / 2, G = kVnThreads / P2;
+  const int tile = blockIdx.x, tid = threadIdx.x, g = tid / P2, q = tid % P2;
+  const int slot0 = blockIdx.y * NB, nslots = a.shared * a.k;
+  const int CKg = (C + G - 1) / G, c0 = min(C, g * CKg), c1 = min(C, c0 + CKg);
+  const double2* M = reinterpret_cast<const double2*>(pn.base + (size_t)tile * C * TR) + q;
+  pdl_trigger();
+  double2 A[U];
+  if (c1 - c0 >= U) load_batch<U>(A, M, P2, c0);  // operator: independent of the previous kernel
+  pdl_wait();
+  for (int e = tid; e < NB * C; e += kVnThreads) {
+    const int j = e / C, col = e % C, s = slot0 + j;
+    xs[j * XS + col] = s < nslots ? xval<MODE>(a, s / a.k, s % a.k, col) : 0.0;
+  }
+  __syncthreads();
+  double acc0[NB], acc1[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
+  stream_cols<NB, U>(A, M, P2, c0, c1, xs, 0, 0, XS, acc0, acc1);
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    red[(g * NB + j) * TR + 2 * q] = acc0[j];
+    red[(g * NB + j) * TR + 2 * q + 1] = acc1[j];
+  }
+  __syncthreads();
+  for (int e = tid; e < NB * TR; e += kVnThreads) {
+    const int j = e / TR, r = e % TR, row = tile * TR + r, s = slot0 + j;
+    if (row >= pn.R || s >= nslots) continue;
+    double y = 0.0;
+    for (int gg = 0; gg < G; ++gg) y += red[(gg * NB + j) * TR + r];
+    epilogue<MODE>(a, s / a.k, row, s % a.k, y);
+  }
+}
+
+constexpr int kVnNB = 4;
+constexpr int kVnMinNodes = 32;      // fewer nodes: the operator stream dominates (panel kernel)
+constexpr size_t kVnMaxSmem = 96 * 1024;
+constexpr int kVnMaxCols = 64;
+
+size_t vn_smem(const Panel& pn, int& XS) {
+  XS = pn.C | 1;
+  return ((size_t)kVnNB * XS + (size_t)kVnNB * 2 * kVnThreads) * 8;
+}
+
+template <int MODE>
+int launch_vn(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
+  int XS;
+  const size_t smem = vn_smem(pn, XS);
+  static bool attr_set = false;
+  if (!attr_set) {
+    HPSB_CUDA(cudaFuncSetAttribute(k_vn<MODE, kVnNB, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)kVnMaxSmem));
+    attr_set = true;
+  }
+  dim3 grid((unsigned)pn.ntiles, (unsigned)cdiv((long long)a.shared * a.k, kVnNB));
+  HPSB_CUDA(launch_pdl(k_vn<MODE, kVnNB, 4>, grid, dim3(kVnThreads), smem, st, a, pn, XS));
+  HPSB_LAUNCH_CHECK();
+  return 0;
+}
+
+bool vn_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_VN");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 template <int MODE, int KM, int U>
 int launch(const GemvArgs& a, const Panel& pn, const PanelSplit& sp, cudaStream_t st) {
   static bool attr_set = false;
@@ -271,6 +354,19 @@ int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
   if (pn.TS != pn.TR) {
     set_error("gemv: node-aligned panel passed to the level kernel");
     return -1;
+  }
+  // (the column chain of one thread, C/G, must stay short: long-K levels
+  // -- the down sweep's S -- keep the split-K panel kernel)
+  if (a.shared >= kVnMinNodes && pn.c == 1 && pn.TR <= 2 * kVnThreads && vn_enabled() &&
+      cdiv(pn.C, kVnThreads / (pn.TR / 2)) <= kVnMaxCols) {
+    int XS;
+    if (vn_smem(pn, XS) <= kVnMaxSmem) {
+      switch (a.mode) {
+        case GEMV_UP: return launch_vn<GEMV_UP>(a, pn, st);
+        case GEMV_DOWN: return launch_vn<GEMV_DOWN>(a, pn, st);
+        default: return launch_vn<GEMV_LEAF>(a, pn, st);
+      }
+    }
   }
   const PanelSplit sp = panel_split(pn, a.k, a.shared ? a.shared : 1);
   if (sp.nsplit > 1 && (!a.part || !a.cnt)) {

@@ -178,6 +178,11 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
 
   const bool up = (g != nullptr) || (jump != nullptr);
   const int nw = P.ni + P.nb;
+  // fused subtree kernels for the deep levels, except for many-rhs solves on
+  // shared operators: there every level is one tensor-core GEMM over
+  // (node, rhs) rows (dedup.cu)
+  const bool fused = P.dF < P.depth && !(ops.shared_levels && k >= kSharedGemmRhs);
+  const int dW = fused ? P.dF : P.depth;  // levels [lstar, dW) run level by level
   // leaf outputs: W (row stride ldw, rhs stride sw) and H (child stride hs, rhs stride sh)
   long long ldw = P.ni, sw = Lni, hs = P.nb, sh = Lnb;
   const double* Hleaf = ws.Hleaf;
@@ -222,12 +227,12 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
     // (3) upward merges of the parts' levels, deepest first (solver.py:243-256):
     // the fused subtree levels in one launch, then one launch per family
     if (up) {
-      if (P.dF < P.depth) {
+      if (fused) {
         int b0, b1;
         range(P.dF, b0, b1);
         if (int rc = subtree_up(ops, ws, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, b0, b1, st)) return rc;
       }
-      for (int d = P.dF - 1; d >= ls; --d) {
+      for (int d = dW - 1; d >= ls; --d) {
         int n0, n1;
         range(d, n0, n1);
         if (int rc = level_up(ops, ws, d, n0, n1, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
@@ -252,12 +257,12 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   }
 
   if (phases & SOLVE_DOWN) {
-    for (int d = ls; d < P.dF; ++d) {
+    for (int d = ls; d < dW; ++d) {
       int n0, n1;
       range(d, n0, n1);
       if (int rc = level_down(ops, ws, d, n0, n1, k, up, u, ld_u, st)) return rc;
     }
-    if (P.dF < P.depth) {
+    if (fused) {
       int b0, b1;
       range(P.dF, b0, b1);
       if (int rc = subtree_down(ops, ws, k, up, u, ld_u, b0, b1, st)) return rc;

@@ -101,3 +101,25 @@ def test_operator_set_save_load_roundtrip(golden, tmp_path, layout):
     assert rel_l2(b, z["u"]) < TOL
     with pytest.raises(hb.HpstepError):
         hb.HpsOperatorSet.load(str(path), ops.disc, ops.sigma, 2 * ops.dt_gamma)
+
+
+@pytest.mark.parametrize("layout,nparts", [("shared", 1), ("per_node", 1), ("shared", 2)])
+def test_many_rhs_solve_matches_oracle(layout, nparts):
+    """k = 20 right-hand sides: on shared operators every level (fused ones
+    included) runs as one tensor-core GEMM over (node, rhs) rows."""
+    import paper_2306_02526_b200 as hb
+    from oracle import hps_oracle as O
+    n, p, k = 8, 12, 20
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), n, n, p)
+    ops = hb.build(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0), sigma=1.0, dt_gamma=1e-3, layout=layout,
+                   nparts=nparts)
+    ot = O.OTree(((0.0, 1.0), (0.0, 1.0)), n, n, p)
+    oops = O.OHps(O.ODisc(ot, O.OCoeffs(1.0, 1.0)), sigma=1.0, dt_gamma=1e-3)
+    rng = np.random.default_rng(9)
+    g = rng.standard_normal((k, tree.N))
+    f = rng.standard_normal((k, tree.boundary_ids.size))
+    u = ops.solve_with_body_load(f, g)
+    ref = oops.solve(f, g)
+    assert rel_l2(u, ref) < TOL
+    single = ops.solve_with_body_load(f[3], g[3])
+    assert rel_l2(single, ref[3]) < TOL
