@@ -29,6 +29,8 @@ enum GsMode { GS_UP = 0, GS_DOWN = 1 };
 struct GsArgs {
   int M, N, K;                 // nodes x rhs (row m: node m % nodes, rhs m / nodes), operator rows, columns
   int nodes;
+  int nsplit, KC;              // split-K: CTA column range [split * KC, +KC) (KC a multiple of BK)
+  double* part; unsigned* cnt; // split-K partials (nsplit x M x N) and per-tile semaphores
   const double* B; int ldb;    // operator, N x K row-major
   GemvArgs g;                  // gathers / scatters (same fields as the streaming kernels)
 };
@@ -78,13 +80,16 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
   constexpr int BN = 32 * WN, NT = 64 * WN;
   constexpr int AE = BM * BK / NT, BE = BN * BK / NT;  // staged elements per thread
   extern __shared__ double sm[];
+  __shared__ unsigned s_last;
   double* As = sm;                  // [2][BM][SROW]
   double* Bs = sm + 2 * BM * SROW;  // [2][BN][SROW]
-  const int tm = blockIdx.x / tilesN, tn = blockIdx.x % tilesN;
+  const int tile = blockIdx.x / a.nsplit, split = blockIdx.x % a.nsplit;
+  const int tm = tile / tilesN, tn = tile % tilesN;
   const int m0 = tm * BM, n0 = tn * BN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / WN, wn = warp % WN;
-  const int nk = (a.K + BK - 1) / BK;
+  const int kb = split * a.KC / BK;                                   // first k-step of this CTA
+  const int nk = (min(a.K, (split + 1) * a.KC) - split * a.KC + BK - 1) / BK;
   pdl_trigger();
 
   double ra[AE], rb[BE];
@@ -92,7 +97,7 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
 #pragma unroll
     for (int i = 0; i < BE; ++i) {
       const int e = tid + NT * i, r = e / BK, c = e % BK;
-      const int gn = n0 + r, gk = kt * BK + c;
+      const int gn = n0 + r, gk = (kb + kt) * BK + c;
       rb[i] = (gn < a.N && gk < a.K) ? a.B[(long long)gn * a.ldb + gk] : 0.0;
     }
   };
@@ -100,7 +105,7 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
 #pragma unroll
     for (int i = 0; i < AE; ++i) {
       const int e = tid + NT * i, r = e / BK, c = e % BK;
-      const int gm = m0 + r, gk = kt * BK + c;
+      const int gm = m0 + r, gk = (kb + kt) * BK + c;
       ra[i] = (gm < a.M && gk < a.K) ? gs_x<MODE>(a.g, gm % a.nodes, gm / a.nodes, gk) : 0.0;
     }
   };
@@ -149,6 +154,41 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
     __syncthreads();
   }
 
+  if (a.nsplit > 1) {  // partial tile to the workspace; the last CTA of the tile sums in split order
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+          if (m < a.M && r < a.N) a.part[((size_t)split * a.M + m) * a.N + r] = acc[i][j][h];
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.cnt + tile, 1u) == (unsigned)a.nsplit - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+          double y = 0.0;
+          if (m < a.M && r < a.N)
+            for (int sp = 0; sp < a.nsplit; ++sp) y += __ldcg(a.part + ((size_t)sp * a.M + m) * a.N + r);
+          acc[i][j][h] = y;
+        }
+    }
+    if (tid == 0) a.cnt[tile] = 0u;
+  }
+
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
@@ -165,7 +205,7 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
 }
 
 template <int MODE, int WN>
-int launch_gs(const GsArgs& a, int k, cudaStream_t st) {
+int launch_gs(GsArgs a, const GsSplit& sp, cudaStream_t st) {
   constexpr int BN = 32 * WN;
   const size_t smem = (size_t)2 * (BM + BN) * SROW * 8;
   static bool attr = false;
@@ -173,23 +213,52 @@ int launch_gs(const GsArgs& a, int k, cudaStream_t st) {
     HPSB_CUDA(cudaFuncSetAttribute(k_gs<MODE, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
-  const int tilesM = (int)cdiv(a.M, BM), tilesN = (int)cdiv(a.N, BN);
-  dim3 grid((unsigned)(tilesM * tilesN));
+  a.nsplit = sp.nsplit;
+  a.KC = sp.KC;
+  const int tilesN = (int)cdiv(a.N, BN);
+  dim3 grid((unsigned)(sp.tiles * sp.nsplit));
   HPSB_CUDA(launch_pdl(k_gs<MODE, WN>, grid, dim3(64 * WN), smem, st, a, tilesN));
   HPSB_LAUNCH_CHECK();
   return 0;
 }
 
 template <int MODE>
-int gs(const GsArgs& a, int k, cudaStream_t st) {
-  // operator rows per CTA tile: enough tiles to fill the SMs, little padding waste
-  const long long tilesM = cdiv(a.M, BM);
-  if (a.N <= 32 || tilesM * cdiv(a.N, 64) < 2 * kNumSMs) return launch_gs<MODE, 1>(a, k, st);
-  if (a.N <= 64 || tilesM * cdiv(a.N, 128) < 2 * kNumSMs) return launch_gs<MODE, 2>(a, k, st);
-  return launch_gs<MODE, 4>(a, k, st);
+int gs(const GsArgs& a, const Workspace& ws, cudaStream_t st) {
+  const GsSplit sp = gs_split(a.M, a.N, a.K);
+  if (sp.nsplit > 1 && (!ws.part || !ws.cnt)) {
+    set_error("gs: split-K needs workspace");
+    return -1;
+  }
+  GsArgs b = a;
+  b.part = ws.part;
+  b.cnt = ws.cnt;
+  if (sp.WN == 1) return launch_gs<MODE, 1>(b, sp, st);
+  if (sp.WN == 2) return launch_gs<MODE, 2>(b, sp, st);
+  return launch_gs<MODE, 4>(b, sp, st);
 }
 
 }  // namespace
+
+// tile width (operator rows per CTA: enough tiles to fill the SMs, little
+// padding waste) and split-K (short column chains when the tiles are few)
+GsSplit gs_split(long long M, int N, int K) {
+  GsSplit s;
+  const long long tilesM = cdiv(M, BM);
+  if (N <= 32 || tilesM * cdiv(N, 64) < 2 * kNumSMs) s.WN = 1;
+  else if (N <= 64 || tilesM * cdiv(N, 128) < 2 * kNumSMs) s.WN = 2;
+  else s.WN = 4;
+  s.tiles = (int)(tilesM * cdiv(N, 32 * s.WN));
+  const int ksteps = (int)cdiv(K, BK);
+  int ns = (int)std::min<long long>(cdiv(2LL * kNumSMs, s.tiles), 16);
+  ns = std::max(1, std::min(ns, ksteps / 4));          // >= 4 k-steps per CTA
+  s.KC = (int)cdiv(ksteps, ns) * BK;
+  s.nsplit = (int)cdiv(K, s.KC);
+  if (s.nsplit > 1) {
+    s.part_doubles = (size_t)s.nsplit * M * N;
+    s.counters = s.tiles;
+  }
+  return s;
+}
 
 // the level apply as a DMMA GEMM over (node, rhs) rows: many nodes, or a
 // multi-rhs solve (the streaming kernel otherwise); levels whose one-node
@@ -223,7 +292,7 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
   a.N = lv.n3 + (d > 0 ? lv.n12 : 0); a.K = lv.n3;
   g = shift_nodes(g, n0);
   a.B = lo.Ush; a.ldb = lv.ld3; a.g = g;
-  return gs<GS_UP>(a, k, st);
+  return gs<GS_UP>(a, ws, st);
 }
 
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
@@ -246,7 +315,7 @@ int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool ha
   a.N = lv.n3; a.K = lv.n12;
   g = shift_nodes(g, n0);
   a.B = lo.Ssh; a.ldb = lv.ld12; a.g = g;
-  return gs<GS_DOWN>(a, k, st);
+  return gs<GS_DOWN>(a, ws, st);
 }
 
 }  // namespace hpsb

@@ -197,6 +197,12 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
                       int n0, int n1, cudaStream_t st);
 bool shared_gemm(const Plan& P, int d, int nodes, int k);
+struct GsSplit {
+  int WN = 1, tiles = 0, nsplit = 1, KC = 0;
+  size_t part_doubles = 0;
+  int counters = 0;
+};
+GsSplit gs_split(long long M, int N, int K);  // (node, rhs) rows x operator rows x operator columns
 
 // tensor-product leaf solve (leaf_fd.cu): [w | h] rows from the body load
 // nleaf leaves: g and WH point at the first one

@@ -63,6 +63,17 @@ static void scratch_sizes(const Plan& P, int k, size_t& part, size_t& cnt) {
     part = std::max(part, sp.part_doubles);
     cnt = std::max(cnt, (size_t)sp.counters);
   }
+  // shared-layout GEMM level applies (dedup.cu) over every part range
+  for (int d = 0; d < P.depth; ++d) {
+    const Level& lv = P.lv[d];
+    for (int np = 1; np <= (d >= P.lstar ? P.nparts : 1); np *= 2) {
+      const long long M = (long long)(lv.c / np) * k;
+      for (const GsSplit& sp : {gs_split(M, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3), gs_split(M, lv.n3, lv.n12)}) {
+        part = std::max(part, sp.part_doubles);
+        cnt = std::max(cnt, (size_t)sp.counters);
+      }
+    }
+  }
 }
 
 size_t workspace_bytes(const Plan& P, int k) {
