@@ -141,7 +141,9 @@ size_t hps_solve_workspace_bytes(const hps_plan* plan, int k);
  *   jump device interface flux jumps (row stride ld_jump) or NULL; with
  *        inv_dt = 1/dt this is solve_penalized (solver.py:188-199, 249-250)
  *   u    device k x N output (row stride ld_u), every DOF written
- *   ws   device workspace of >= hps_solve_workspace_bytes(plan, k) bytes */
+ *   ws   device workspace of >= hps_solve_workspace_bytes(plan, k) bytes,
+ *        256-byte aligned and zero-filled before its first use (its
+ *        semaphores and completion counters return to zero after every solve) */
 int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
               long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
               long long ld_u, void* ws, size_t ws_bytes, void* stream);
