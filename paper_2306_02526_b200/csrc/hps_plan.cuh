@@ -145,6 +145,8 @@ struct Workspace {
   std::vector<double*> W3;  // per level: k x c x n3
   double* part = nullptr;   // split-K partials
   unsigned* cnt = nullptr;  // split-K semaphores (zero between launches)
+  unsigned* mega_cnt = nullptr;  // persistent level kernel: completion counters (zero between launches)
+  double* mega_part = nullptr;   // ... and its split partials
 };
 size_t workspace_bytes(const Plan& P, int k);
 void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
@@ -209,6 +211,15 @@ GsSplit gs_split(long long M, int N, int K);  // (node, rhs) rows x operator row
 int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,
             cudaStream_t st);
 bool leaf_fd_supported(int q);
+
+// persistent dataflow kernel for wide shared-layout levels (mega.cu): up
+// levels [u0, u1) deepest first, then down levels [d0, d1) root first, over
+// the parts' nodes on levels >= lstar; returns 1 when not eligible
+bool mega_enabled();
+void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles);
+int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int d1, int part0, int part1,
+                const double* Hleaf, long long hs, const double* jump, double inv_dt, bool has_w3, double* u,
+                cudaStream_t st);
 
 // solve entry (solve.cu).  phases: SOLVE_UP (leaves + levels >= lstar of parts
 // [part0, part1)), SOLVE_TOP (Dirichlet data, levels < lstar up and down),

@@ -57,7 +57,14 @@ constexpr int NT = 256;
 // 16-byte loads in flight, cover HBM latency under full load
 constexpr int kTargetThreads = kNumSMs * 1024;
 constexpr size_t kMaxStage = 64 * 1024;
-constexpr int kMaxSplit = 32;  // bounds the serial partial-sum tail of the last CTA
+constexpr int kMaxSplitDefault = 32;  // bounds the serial partial-sum tail of the last CTA
+int max_split() {
+  static const int v = [] {
+    const char* e = getenv("HPSB_MAXSPLIT");
+    return e ? std::max(1, atoi(e)) : kMaxSplitDefault;
+  }();
+  return v;
+}
 
 }  // namespace
 
@@ -69,7 +76,7 @@ PanelSplit panel_split(const Panel& pn, int k, int vnodes) {
   long long base = (long long)pn.ntiles * vnodes * s.kgroups;
   int ns = (int)std::max<long long>(1, cdiv(kTargetThreads, base * (pn.TR / 2)));
   ns = std::min(ns, std::max(1, pn.C / 16));
-  ns = std::min(ns, kMaxSplit);
+  ns = std::min(ns, max_split());
   int CK = (int)cdiv(pn.C, ns);
   auto xs = [](int ck) { return ck | 1; };
   long long cap = (long long)(kMaxStage / 8) / ((long long)s.nodes * s.KM);

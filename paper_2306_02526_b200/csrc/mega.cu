@@ -1,0 +1,385 @@
+// Persistent dataflow kernel for the wide levels of a shared-layout solve.
+//
+// The wide levels (0..dF-1) of the up and down sweeps (solver.py:243-268)
+// are ~2*dF dependent level applies; as one launch each, every level pays a
+// kernel drain + fill and the slowest CTA of the level (the split-K
+// reducers).  Here one persistent launch runs all of them as a task list:
+//
+//   task = (segment = (pass, level), node group of NB nodes, 64-row block,
+//           column split)
+//
+// in topological order (deepest level first for the up pass, root first for
+// the down pass).  A task waits only for what it reads -- the up pass for the
+// two children of each of its nodes, the down pass for the parents and for its
+// own nodes' up results -- through per-node completion counters (one count per
+// finished row block).  CTAs take tasks round-robin in increasing order; every
+// task depends only on lower-numbered ones and all CTAs are resident (the grid
+// is sized by occupancy), so the lowest unfinished task can always run.
+//
+// Within a task the CTA is 8 column groups x 32 threads; a thread owns two
+// adjacent rows of the block and walks its group's columns of the split
+// (16-byte loads of the column-major one-node panel), the groups' sums meet in
+// shared memory in group order, and a split > 1 goes through workspace
+// partials summed in split order by the last CTA (semaphore) -- outputs are
+// bitwise reproducible.  Data produced inside the launch are read with
+// ld.global.cg (L2; L1 is not coherent).  The last CTA to exit resets every
+// counter for the next solve.
+#include <stdio.h>
+
+#include "hps_plan.cuh"
+#include "stream.cuh"
+
+namespace hpsb {
+
+namespace {
+
+constexpr int MT = 256;        // threads per CTA
+constexpr int MRB = 64;        // rows per row block
+constexpr int MGRP = 8;        // column groups (MT / (MRB / 2))
+constexpr int MNB = 4;         // nodes per group
+constexpr int MKC = 256;       // max operator columns per task (32 per thread)
+constexpr int MAXSEG = 24;
+constexpr int MXS = MKC + 1;
+constexpr int MU = 4;          // 16-byte operator loads per batch (two batches in flight)
+
+struct MSeg {
+  int up;                      // 1 = up pass, 0 = down pass
+  int n0, nn;                  // node range [n0, n0 + nn)
+  int R, K;                    // operator rows / columns
+  const double* op; int TR;    // one-node panel (tiles of TR rows, column-major)
+  int RB, NG, S, KC;           // row blocks, node groups, splits, columns per split
+  int task0, ntasks;
+  // gathers / epilogue (global node numbering; k = 1)
+  const double* Hc; long long Hc_s; const int *i1a, *i3a, *i2b, *i3b; int n1a, n3, n12;
+  const double* jump; double inv_dt; const int* j3; const int* gidx;
+  double* W3; double* Hout; double* u;
+  // dataflow
+  unsigned* done;              // [nodes of the level] row blocks finished
+  const unsigned* wchild; int wchild_t;   // up: children's counters (level d+1), target
+  const unsigned* wpar; int wpar_t;       // down: parents' counters (level d-1)
+  const unsigned* wup; int wup_t;         // down: own nodes' up counters
+  double* part; unsigned* sem; // split partials [S][NG*NB][R], semaphores [NG*RB]
+};
+
+struct MProg {
+  int nseg, ntasks;
+  unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / end, ns
+  unsigned* reset; int nreset;  // counters to zero at exit (incl. the exit counter at the end)
+  MSeg s[MAXSEG];
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
+  long long spins = 0;
+  while (ld_acquire(p) < target) {
+    __nanosleep(32);
+    if (++spins > (1LL << 24)) __trap();  // a lost dependency must fail, not hang the GPU
+  }
+}
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
+  __shared__ double xs[MNB][MXS];              // the task's inputs
+  __shared__ double red[MGRP][MNB][MRB];       // column-group partial sums
+  __shared__ int sidx[MNB][MKC];               // gather indices (down: per node; up: i3a / i3b rows 0 / 1)
+  __shared__ unsigned s_last;
+  const int tid = threadIdx.x, grp = tid >> 5, q = tid & 31;
+  pdl_wait();
+  for (int t = blockIdx.x; t < p.ntasks; t += gridDim.x) {
+    int si = 0;
+    while (t >= p.s[si].task0 + p.s[si].ntasks) ++si;
+    const MSeg& g = p.s[si];
+    int local = t - g.task0;
+    const int split = local % g.S;
+    local /= g.S;
+    const int rb = local % g.RB, ng = local / g.RB;
+    const int node0 = g.n0 + ng * MNB, nv = min(MNB, g.n0 + g.nn - node0);
+    if (p.trace && tid == 0) p.trace[3 * t] = gtime();
+    // ---- nothing below depends on the inputs: the operator's first batch,
+    // the gather indices and this thread's epilogue index are in flight while
+    // the task waits for its inputs
+    const int c0 = split * g.KC, cw = min(g.KC, g.K - c0);
+    const int cg = (cw + MGRP - 1) / MGRP, a0 = min(cw, grp * cg), a1 = min(cw, a0 + cg);
+    const int row = rb * MRB + 2 * q;  // rows row, row + 1 (R and TR are even: both valid or both padding)
+    const bool rows_ok = row < g.R;
+    const int cs = g.TR / 2;           // column stride in double2
+    const int rowc = min(row, g.R - 2);
+    const double2* M =
+        reinterpret_cast<const double2*>(g.op + (size_t)(rowc / g.TR) * g.K * g.TR + rowc % g.TR) + (size_t)c0 * cs;
+    double2 A[MU];
+    if (rows_ok && a1 - a0 >= MU) load_batch<MU>(A, M, cs, a0);
+    if (g.up) {
+      for (int i = tid; i < 2 * cw; i += MT) sidx[i / cw][i % cw] = (i < cw ? g.i3a : g.i3b)[c0 + i % cw];
+    } else {
+      for (int i = tid; i < nv * cw; i += MT) sidx[i / cw][i % cw] = g.gidx[(long long)(node0 + i / cw) * g.n12 + c0 + i % cw];
+    }
+    const int oj = tid / MRB, orow = rb * MRB + tid % MRB;  // MT = MNB * MRB: one output per thread
+    const bool ovalid = oj < nv && orow < g.R;
+    int oidx = 0;  // epilogue index: up -> child flux position (flux rows), down -> global DOF
+    if (ovalid) {
+      if (g.up) {
+        const int r = orow - g.n3;
+        if (r >= 0) oidx = r < g.n1a ? g.i1a[r] : g.i2b[r - g.n1a];
+      } else {
+        oidx = g.j3[(long long)(node0 + oj) * g.n3 + orow];
+      }
+    }
+    // ---- dependencies
+    if (g.up) {
+      if (g.wchild && tid < 2 * nv) wait_count(g.wchild + 2 * node0 + tid, g.wchild_t);
+    } else {
+      if (g.wpar && tid < nv) wait_count(g.wpar + (node0 + tid) / 2, g.wpar_t);
+      if (g.wup && tid >= 32 && tid < 32 + nv) wait_count(g.wup + node0 + tid - 32, g.wup_t);
+    }
+    __syncthreads();
+    if (p.trace && tid == 0) p.trace[3 * t + 1] = gtime();
+    // ---- stage the group's inputs for this split's columns
+    for (int e = tid; e < MNB * cw; e += MT) {
+      const int j = e / cw, col = e % cw;
+      double v = 0.0;
+      if (j < nv) {
+        const int node = node0 + j;
+        if (g.up) {
+          const double* Ha = g.Hc + (long long)(2 * node) * g.Hc_s;
+          v = __ldcg(Ha + g.Hc_s + sidx[1][col]) - __ldcg(Ha + sidx[0][col]);
+          if (g.jump) v = v - g.inv_dt * g.jump[g.j3[(long long)node * g.n3 + c0 + col]];
+        } else {
+          v = __ldcg(g.u + sidx[j][col]);
+        }
+      }
+      xs[j][col] = v;
+    }
+    __syncthreads();
+    // ---- stream: group grp walks columns [a0, a1) of the split for rows 2q, 2q+1 of the block
+    double acc0[MNB], acc1[MNB];
+#pragma unroll
+    for (int j = 0; j < MNB; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
+    if (rows_ok) stream_cols<MNB, MU>(A, M, cs, a0, a1, &xs[0][0], 0, 0, MXS, acc0, acc1);
+#pragma unroll
+    for (int j = 0; j < MNB; ++j) {
+      red[grp][j][2 * q] = acc0[j];
+      red[grp][j][2 * q + 1] = acc1[j];
+    }
+    __syncthreads();
+    // ---- group sums (in group order), then split partials or the epilogue
+    const int r = tid % MRB;
+    double y = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < MGRP; ++gg) y += red[gg][oj][r];
+    bool emit_now = true;
+    if (g.S > 1) {
+      const size_t slot = (size_t)(ng * MNB + oj) * g.R + orow;
+      const size_t pstride = (size_t)g.NG * MNB * g.R;
+      if (ovalid) g.part[(size_t)split * pstride + slot] = y;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) s_last = atomicAdd(g.sem + ng * g.RB + rb, 1u) == (unsigned)g.S - 1;
+      __syncthreads();
+      emit_now = s_last;
+      if (emit_now) {
+        __threadfence();
+        y = 0.0;
+        if (ovalid)
+          for (int s = 0; s < g.S; ++s) y += __ldcg(g.part + (size_t)s * pstride + slot);
+      }
+    }
+    if (emit_now) {
+      if (ovalid) {
+        const int node = node0 + oj;
+        if (g.up) {
+          if (orow < g.n3) {
+            g.W3[(long long)node * g.n3 + orow] = y;
+          } else {
+            const int rr = orow - g.n3;
+            const double* Ha = g.Hc + (long long)(2 * node) * g.Hc_s;
+            const double base = rr < g.n1a ? __ldcg(Ha + oidx) : __ldcg(Ha + g.Hc_s + oidx);
+            g.Hout[(long long)node * g.n12 + rr] = base + y;
+          }
+        } else {
+          if (g.W3) y = y + __ldcg(g.W3 + (long long)node * g.n3 + orow);
+          g.u[oidx] = y;
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (tid < nv) atomicAdd(g.done + node0 + tid, 1u);
+    }
+    __syncthreads();  // xs / red / sidx are reused by the next task
+    if (p.trace && tid == 0) p.trace[3 * t + 2] = gtime();
+  }
+  // the last CTA out resets the counters for the next solve
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    s_last = atomicAdd(exit_count, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    for (int i = tid; i < p.nreset; i += MT) p.reset[i] = 0u;
+    __syncthreads();
+    if (tid == 0) *exit_count = 0u;
+  }
+}
+
+}  // namespace
+
+bool mega_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_MEGA");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// Counter / partial space of the workspace's mega region for one plan: every
+// wide level's nodes twice (up, down), semaphores and split partials of every
+// possible segment.  Sized generously from the plan alone.
+static void mega_dims(const Level& lv, bool root, bool up, int nn, int& RB, int& NG, int& S, int& KC, int& R,
+                      int& K) {
+  R = up ? lv.n3 + (root ? 0 : lv.n12) : lv.n3;
+  K = up ? lv.n3 : lv.n12;
+  RB = (R + MRB - 1) / MRB;
+  NG = (nn + MNB - 1) / MNB;
+  S = std::max(1, (K + MKC - 1) / MKC);
+  KC = (K + S - 1) / S;
+  S = (K + KC - 1) / KC;
+}
+
+void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles) {
+  counters = 1;  // exit counter
+  part_doubles = 0;
+  for (int d = 0; d < P.depth; ++d) {
+    const Level& lv = P.lv[d];
+    counters += 2 * (size_t)lv.c;
+    for (int up = 0; up < 2; ++up) {
+      int RB, NG, S, KC, R, K;
+      mega_dims(lv, d == 0, up, lv.c, RB, NG, S, KC, R, K);
+      counters += (size_t)RB * NG;
+      if (S > 1) part_doubles += (size_t)S * NG * MNB * R;
+    }
+  }
+}
+
+// Runs the up levels [u0, u1) (deepest first) and the down levels [d0, d1)
+// (root first) of nodes range(level) as one launch.  Returns 1 when the
+// levels are not eligible (caller falls back to per-level launches).
+int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int d1, int part0, int part1,
+                const double* Hleaf, long long hs, const double* jump, double inv_dt, bool has_w3, double* u,
+                cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  if (!mega_enabled() || !ops.shared_levels || !ws.mega_cnt) return 1;
+  MProg p{};
+  // counter carve: [exit][per level: up nodes, down nodes][sems...]
+  unsigned* cnt = ws.mega_cnt;
+  unsigned* exit_count = cnt;
+  std::vector<unsigned*> dup(P.depth), ddn(P.depth);
+  unsigned* c = cnt + 1;
+  for (int d = 0; d < P.depth; ++d) { dup[d] = c; c += P.lv[d].c; ddn[d] = c; c += P.lv[d].c; }
+  double* part = ws.mega_part;
+  int task = 0;
+  auto add = [&](int d, bool up) -> bool {
+    if (p.nseg >= MAXSEG) return false;
+    const Level& lv = P.lv[d];
+    const LevelOps& lo = ops.lo[d];
+    const Panel& pn = up ? lo.Up : lo.S;
+    if (!pn.base || pn.c != 1 || pn.TS != pn.TR || (pn.TR & 1)) return false;
+    MSeg& g = p.s[p.nseg];
+    int n0 = 0, n1 = lv.c;  // levels >= lstar: the parts' nodes
+    if (d >= P.lstar) { n0 = part0 * (lv.c / P.nparts); n1 = part1 * (lv.c / P.nparts); }
+    g.up = up;
+    g.n0 = n0; g.nn = n1 - n0;
+    mega_dims(lv, d == 0, up, g.nn, g.RB, g.NG, g.S, g.KC, g.R, g.K);
+    if (g.R != pn.R || g.K != pn.C || g.KC > MKC) return false;
+    g.op = pn.base; g.TR = pn.TR;
+    g.task0 = task; g.ntasks = g.RB * g.NG * g.S;
+    task += g.ntasks;
+    const bool leafc = d == P.depth - 1;
+    g.Hc = leafc ? Hleaf : ws.H[d + 1];
+    g.Hc_s = leafc ? hs : lv.nbc;
+    g.i1a = lv.i1a; g.i3a = lv.i3a; g.i2b = lv.i2b; g.i3b = lv.i3b; g.n1a = lv.n1a; g.n3 = lv.n3; g.n12 = lv.n12;
+    g.jump = jump; g.inv_dt = inv_dt; g.j3 = lv.j3; g.gidx = lv.gidx_bnd;
+    g.W3 = (up || has_w3) ? ws.W3[d] : nullptr;
+    g.Hout = d > 0 ? ws.H[d] : nullptr;
+    g.u = u;
+    g.done = up ? dup[d] : ddn[d];
+    g.sem = c; c += (size_t)g.RB * g.NG;
+    if (g.S > 1) { g.part = part; part += (size_t)g.S * g.NG * MNB * g.R; }
+    // dependencies inside this launch
+    if (up) {
+      const bool child_here = d + 1 < u1;
+      g.wchild = child_here ? dup[d + 1] : nullptr;
+      int RBc = 0, NGc, Sc, KCc, Rc, Kc;
+      if (child_here) mega_dims(P.lv[d + 1], false, true, 1, RBc, NGc, Sc, KCc, Rc, Kc);
+      g.wchild_t = RBc;
+    } else {
+      const bool par_here = d - 1 >= d0 && d > 0;
+      g.wpar = par_here ? ddn[d - 1] : nullptr;
+      int RBp = 0, x1, x2, x3, x4, x5;
+      if (par_here) mega_dims(P.lv[d - 1], d - 1 == 0, false, 1, RBp, x1, x2, x3, x4, x5);
+      g.wpar_t = RBp;
+      const bool up_here = d >= u0 && d < u1;
+      g.wup = up_here && has_w3 ? dup[d] : nullptr;
+      int RBu = 0;
+      if (up_here) mega_dims(lv, d == 0, true, 1, RBu, x1, x2, x3, x4, x5);
+      g.wup_t = RBu;
+    }
+    ++p.nseg;
+    return true;
+  };
+  for (int d = u1 - 1; d >= u0; --d)
+    if (!add(d, true)) return 1;
+  for (int d = d0; d < d1; ++d)
+    if (!add(d, false)) return 1;
+  if (p.nseg == 0) return 0;
+  p.ntasks = task;
+  p.reset = cnt + 1;
+  p.nreset = (int)(c - (cnt + 1));
+  static int max_ctas = 0;
+  if (!max_ctas) {
+    int per_sm = 0;
+    HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mega, MT, 0));
+    int dev = 0, sms = kNumSMs;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    max_ctas = std::max(1, per_sm) * sms;
+  }
+  const int grid = std::min(max_ctas, p.ntasks);
+  const char* tr = getenv("HPSB_MEGA_TRACE");  // debug: per-task timeline appended to this file
+  unsigned long long* dtrace = nullptr;
+  if (tr) {
+    HPSB_CUDA(cudaMalloc(&dtrace, (size_t)3 * p.ntasks * 8));
+    HPSB_CUDA(cudaMemsetAsync(dtrace, 0, (size_t)3 * p.ntasks * 8, st));
+    p.trace = dtrace;
+  }
+  HPSB_CUDA(launch_pdl(k_mega, dim3(grid), dim3(MT), 0, st, p, exit_count));
+  HPSB_LAUNCH_CHECK();
+  if (tr) {
+    std::vector<unsigned long long> h((size_t)3 * p.ntasks);
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    HPSB_CUDA(cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost));
+    cudaFree(dtrace);
+    if (FILE* f = fopen(tr, "a")) {
+      fprintf(f, "launch grid=%d tasks=%d segs=%d\n", grid, p.ntasks, p.nseg);
+      for (int i = 0; i < p.nseg; ++i) {
+        const MSeg& g = p.s[i];
+        fprintf(f, "seg %d up=%d nodes=%d R=%d K=%d RB=%d NG=%d S=%d tasks=%d:%d\n", i, g.up, g.nn, g.R, g.K, g.RB,
+                g.NG, g.S, g.task0, g.ntasks);
+      }
+      for (int t = 0; t < p.ntasks; ++t) fprintf(f, "%d %llu %llu %llu\n", t, h[3 * t], h[3 * t + 1], h[3 * t + 2]);
+      fclose(f);
+    }
+  }
+  return 0;
+}
+
+}  // namespace hpsb

@@ -90,6 +90,10 @@ size_t workspace_bytes(const Plan& P, int k) {
   scratch_sizes(P, k, part, cnt);
   n += (part * 8 + 255) & ~(size_t)255;
   n += (cnt * 4 + 255) & ~(size_t)255;
+  size_t mc, mp;
+  mega_scratch(P, mc, mp);
+  n += (mc * 4 + 255) & ~(size_t)255;
+  n += (mp * 8 + 255) & ~(size_t)255;
   return n + 256;
 }
 
@@ -114,6 +118,12 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
   ws.part = (double*)p;
   p += (part * 8 + 255) & ~(size_t)255;
   ws.cnt = (unsigned*)p;  // zeroed by the caller when the workspace is created
+  p += (cnt * 4 + 255) & ~(size_t)255;
+  size_t mc, mp;
+  mega_scratch(P, mc, mp);
+  ws.mega_cnt = (unsigned*)p;  // zeroed likewise
+  p += (mc * 4 + 255) & ~(size_t)255;
+  ws.mega_part = (double*)p;
 }
 
 // one level's upward merge over nodes [n0, n1) (solver.py:243-256)
@@ -235,44 +245,47 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
       for (int kk = 0; kk < k; ++kk)
         HPSB_CUDA(cudaMemsetAsync(ws.Hleaf + kk * Lnb + (long long)leaf0 * P.nb, 0, (size_t)nleaf * P.nb * 8, st));
     }
-    // (3) upward merges of the parts' levels, deepest first (solver.py:243-256):
-    // the fused subtree levels in one launch, then one launch per family
-    if (up) {
-      if (fused) {
-        int b0, b1;
-        range(P.dF, b0, b1);
-        if (int rc = subtree_up(ops, ws, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, b0, b1, st)) return rc;
-      }
-      for (int d = dW - 1; d >= ls; --d) {
-        int n0, n1;
-        range(d, n0, n1);
-        if (int rc = level_up(ops, ws, d, n0, n1, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
-      }
+    // (3) upward merges of the fused subtree levels in one launch (solver.py:243-256)
+    if (up && fused) {
+      int b0, b1;
+      range(P.dF, b0, b1);
+      if (int rc = subtree_up(ops, ws, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, b0, b1, st)) return rc;
     }
   }
-
   if (phases & SOLVE_TOP) {
-    // (1) Dirichlet data into u (solver.py:259-260)
+    // (1) Dirichlet data into u (solver.py:259-260); the up sweep never reads u
     long long n = (long long)k * P.nbd;
     if (n > 0) {
       HPSB_CUDA(launch_pdl(k_bnd_scatter, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.nbd, P.boundary_ids,
                            fb, ld_f, u, ld_u));
       HPSB_LAUNCH_CHECK();
     }
-    if (up)
-      for (int d = ls - 1; d >= 0; --d)
-        if (int rc = level_up(ops, ws, d, 0, P.lv[d].c, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
-    // (4) downward sweep of the top levels, root first (solver.py:258-268)
-    for (int d = 0; d < ls; ++d)
-      if (int rc = level_down(ops, ws, d, 0, P.lv[d].c, k, up, u, ld_u, st)) return rc;
+  }
+  // (3, 4) the wide levels: up [uA, uB) deepest first, then down [dA, dB) root
+  // first (solver.py:243-268) -- the parts' nodes on levels >= lstar, every
+  // node above.  Shared operators, one rhs: one persistent dataflow launch
+  // (mega.cu); otherwise one launch per level and pass.
+  const int uA = (phases & SOLVE_TOP) ? 0 : ls, uB = up ? ((phases & SOLVE_UP) ? dW : ls) : uA;
+  const int dA = (phases & SOLVE_TOP) ? 0 : ls, dB = (phases & SOLVE_DOWN) ? dW : ls;
+  int rc_mega = 1;
+  if (k == 1 && (uB > uA || dB > dA))
+    rc_mega = mega_levels(ops, ws, uA, std::max(uA, uB), dA, std::max(dA, dB), part0, part1, Hleaf, hs, jump,
+                          inv_dt, up, u, st);
+  if (rc_mega < 0) return rc_mega;
+  if (rc_mega == 1) {
+    for (int d = uB - 1; d >= uA; --d) {
+      int n0 = 0, n1 = P.lv[d].c;
+      if (d >= ls) range(d, n0, n1);
+      if (int rc = level_up(ops, ws, d, n0, n1, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
+    }
+    for (int d = dA; d < dB; ++d) {
+      int n0 = 0, n1 = P.lv[d].c;
+      if (d >= ls) range(d, n0, n1);
+      if (int rc = level_down(ops, ws, d, n0, n1, k, up, u, ld_u, st)) return rc;
+    }
   }
 
   if (phases & SOLVE_DOWN) {
-    for (int d = ls; d < dW; ++d) {
-      int n0, n1;
-      range(d, n0, n1);
-      if (int rc = level_down(ops, ws, d, n0, n1, k, up, u, ld_u, st)) return rc;
-    }
     if (fused) {
       int b0, b1;
       range(P.dF, b0, b1);
