@@ -15,6 +15,8 @@ from .tableaux import ButcherPair, available_tableaux, load_tableau
 from .timestep import (ParabolicProblem, SeparableField, StepperState, TimeStepper,
                        evaluate_nonlinear)
 from .tree import DomainTree, TreeNode, build_tree
+from .stability import StepMapSpectrum, analyze, assemble_step_map
+from .sharding import ShardedTimeStepper
 
 __version__ = "0.1.0"
 
@@ -25,4 +27,5 @@ __all__ = [
     "OperatorCoefficients", "shift_reaction", "HpsOperatorSet", "build", "DomainTree",
     "TreeNode", "build_tree", "ButcherPair", "available_tableaux", "load_tableau",
     "ParabolicProblem", "SeparableField", "StepperState", "TimeStepper", "evaluate_nonlinear",
+    "StepMapSpectrum", "analyze", "assemble_step_map", "ShardedTimeStepper",
 ]

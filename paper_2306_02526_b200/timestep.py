@@ -29,6 +29,7 @@ formulations (timestep.py:268-328) reuse the same device pieces.
 """
 
 import ctypes
+import gc
 import os
 
 import numpy as np
@@ -553,7 +554,14 @@ class TimeStepper:
             finally:
                 _CoefSink.current = None
 
-        graph = self._capture_graph(body)
+        # a finalizer that frees device memory (an operator set or plan collected
+        # by the GC) would invalidate the capture: collect now, none during it
+        gc.collect()
+        gc.disable()
+        try:
+            graph = self._capture_graph(body)
+        finally:
+            gc.enable()
         ring = 4
         self._graph = dict(graph=graph, gin=gin, guards=guards, coef=coef, ncoef=len(vals), key=self._graph_key(gin),
                            pinned=[torch.zeros(len(vals) + 8, dtype=torch.float64).pin_memory() for _ in range(ring)],

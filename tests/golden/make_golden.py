@@ -234,6 +234,26 @@ def slope_cases():
     save("step_slope", modes=coef, **out, ac_pen=s.u.copy())
 
 
+def stability_case():
+    """Step-map assembly (stability.py:57-85) and its spectrum at 4x4 p=6,
+    homogeneous heat (and variable coefficients for BE): ARK4 stage / slope, BE."""
+    from hpstep.stability import analyze, assemble_step_map
+    tree = build_tree(UNIT, 4, 4, 6)
+    out = {}
+    for key, coeffs, tab, form, dt in (("ark4", OperatorCoefficients(c11=1.0, c22=1.0, dim=2), "ARK4", "stage", 1e-2),
+                                       ("ark4_slope", OperatorCoefficients(c11=1.0, c22=1.0, dim=2), "ARK4", "slope",
+                                        1e-2),
+                                       ("be_var", coeffs_var_test(), "BE", "stage", 5e-2)):
+        prob = ParabolicProblem(coeffs=coeffs, u0=lambda pts: np.zeros(pts.shape[0]), time_independent_bc=True)
+        M = assemble_step_map(tree, prob, tab, dt, formulation=form)
+        spec = analyze(M, dt=dt, scheme=tab, formulation=form)
+        out[key + "_M"] = M
+        out[key + "_eig"] = spec.eigenvalues
+        out[key + "_rho"] = spec.spectral_radius
+        out[key + "_zeros"] = spec.zero_count
+    save("stability_4x4p6", **out)
+
+
 def main():
     if "--only" in sys.argv:
         for name in sys.argv[sys.argv.index("--only") + 1:]:
@@ -258,6 +278,7 @@ def main():
     burgers_var_case()
     ensemble_case()
     be_case()
+    stability_case()
     evals_case()
     slope_cases()
 

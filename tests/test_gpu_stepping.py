@@ -220,3 +220,22 @@ def test_graph_replay_nonlinear_and_backward_euler(golden):
     s = st.run(st.initial_state(), 3)
     assert st._graph is not None
     assert rel_l2(s.u, zb["u3"]) < TOL
+
+
+@pytest.mark.parametrize("key,tab,form,dt", [("ark4", "ARK4", "stage", 1e-2), ("ark4_slope", "ARK4", "slope", 1e-2),
+                                             ("be_var", "BE", "stage", 5e-2)])
+def test_step_map_assembly_matches_reference(golden, key, tab, form, dt):
+    """stability.py:59-85 on the device: 64 basis fields per multi-rhs step."""
+    hb = _hb()
+    from paper_2306_02526_b200.stability import analyze, assemble_step_map
+    z = golden("stability_4x4p6")
+    tree = hb.build_tree(UNIT, 4, 4, 6)
+    coeffs = hb.OperatorCoefficients(**(var_test_fields() if key == "be_var" else lap_fields()))
+    prob = hb.ParabolicProblem(coeffs=coeffs, u0=lambda pts: np.zeros(pts.shape[0]), time_independent_bc=True)
+    M = assemble_step_map(tree, prob, tab, dt, formulation=form)
+    assert rel_l2(M, z[key + "_M"]) < TOL
+    spec = analyze(M, dt=dt, scheme=tab, formulation=form)
+    assert abs(spec.spectral_radius - float(z[key + "_rho"])) < 1e-10
+    assert spec.zero_count == int(z[key + "_zeros"])
+    with pytest.raises(hb.UnsupportedConfigurationError):
+        assemble_step_map(tree, hb.ParabolicProblem(coeffs=coeffs, g=lambda t, u, ux, uy: u), tab, dt)

@@ -121,3 +121,17 @@ def test_tensor_leaf_factors_only_for_constant_coefficients():
     tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 9)            # q = 7: no kernel
     disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0))
     assert tensor_leaf_factors(disc, 1.0, 0.1) is None
+
+
+def test_step_map_analysis_matches_reference(golden):
+    """stability.analyze on the reference's assembled maps reproduces the
+    reference's spectrum, spectral radius and zero count (host only)."""
+    from paper_2306_02526_b200.stability import analyze, spectrum_csv_lines
+    z = golden("stability_4x4p6")
+    for key in ("ark4", "ark4_slope", "be_var"):
+        spec = analyze(z[key + "_M"], dt=0.01, scheme="ARK4")
+        assert abs(spec.spectral_radius - float(z[key + "_rho"])) < 1e-12
+        assert spec.zero_count == int(z[key + "_zeros"])
+        assert np.allclose(np.sort_complex(spec.eigenvalues), np.sort_complex(z[key + "_eig"]), atol=1e-10)
+    lines = spectrum_csv_lines(spec)
+    assert lines[1] == "re,im,modulus" and len(lines) == 2 + spec.eigenvalues.size
