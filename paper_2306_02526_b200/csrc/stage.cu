@@ -268,23 +268,51 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
     ryy[s] = mats[3 * P * P + yi * P + s];
   }
   double gmax = 0.0;
-  for (int l0 = blockIdx.x * lpb; l0 < a.L; l0 += gridDim.x * lpb) {
-    const int nl = min(lpb, a.L - l0);
-    __syncthreads();
-    for (int e = tid; e < nl * NI; e += NT) {
-      int l2 = e / NI, i = e % NI;
-      double v = u[a.ioff + (long long)l0 * NI + e];
-      U[l2 * PP + (i / Q + 1) * PS + (i % Q + 1)] = v;
-      gacc(gmax, v);
+  // the next leaf group's values are loaded into registers while the current
+  // group is computed from shared memory (lpb must equal LPB, set by the host)
+  constexpr int LPB = 2048 / (P * P), KI = (LPB * NI + NT - 1) / NT, KB = (LPB * NB + NT - 1) / NT;
+  double pi[KI], pb[KB];
+  auto fetch = [&](int l0) {
+    const int nl = min(LPB, a.L - l0);
+#pragma unroll
+    for (int i = 0; i < KI; ++i) {
+      const int e = tid + i * NT;
+      pi[i] = e < nl * NI ? u[a.ioff + (long long)l0 * NI + e] : 0.0;
     }
-    for (int e = tid; e < nl * NB; e += NT) {
-      int l2 = e / NB, j = e % NB, x, y;
-      edge_xy(j, P, Q, x, y);
-      double v = u[a.lbg[(long long)l0 * NB + e]];
-      U[l2 * PP + x * PS + y] = v;
-      gacc(gmax, v);
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const int e = tid + i * NT;
+      pb[i] = e < nl * NB ? u[a.lbg[(long long)l0 * NB + e]] : 0.0;
+    }
+  };
+  const int step = gridDim.x * LPB;
+  int l0 = blockIdx.x * LPB;
+  if (l0 < a.L) fetch(l0);
+  for (; l0 < a.L; l0 += step) {
+    const int nl = min(LPB, a.L - l0);
+    __syncthreads();  // the previous group is consumed
+#pragma unroll
+    for (int i = 0; i < KI; ++i) {
+      const int e = tid + i * NT;
+      if (e < nl * NI) {
+        const int l2 = e / NI, ii = e % NI;
+        U[l2 * PP + (ii / Q + 1) * PS + (ii % Q + 1)] = pi[i];
+        gacc(gmax, pi[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const int e = tid + i * NT;
+      if (e < nl * NB) {
+        const int l2 = e / NB, j = e % NB;
+        int x, y;
+        edge_xy(j, P, Q, x, y);
+        U[l2 * PP + x * PS + y] = pb[i];
+        gacc(gmax, pb[i]);
+      }
     }
     __syncthreads();
+    if (l0 + step < a.L) fetch(l0 + step);
     if (!active) continue;
     for (int ll = lane0; ll < nl; ll += LANES) {
       const double* G = U + ll * PP;
@@ -337,11 +365,57 @@ __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
   const long long stride = (long long)gridDim.x * NT;
   for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < a.n; e += stride) {
     double s = 0.0;
-    for (int t = 0; t < a.nt; ++t) s = fma(a.dc ? __ldg(a.dc + t) : a.c[t], __ldcs(a.v[t] + kk * a.ld[t] + e), s);
+    for (int t0 = 0; t0 < a.nt; t0 += 4) {
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = t0 + u < a.nt ? __ldcs(a.v[t0 + u] + kk * a.ld[t0 + u] + e) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t0 + u >= a.nt) break;
+        s = fma(a.dc ? __ldg(a.dc + t0 + u) : a.c[t0 + u], v[u], s);
+      }
+    }
     a.out[kk * a.ld_out + e] = s;
     gacc(gmax, s);
   }
   if (a.guard) guard_max(a.guard, gmax);
+}
+
+// 16-byte variant: every term pointer / row stride and the output 16-byte
+// aligned (even offsets), n even; two DOFs per thread and iteration, all
+// term loads issued before the sums
+__global__ void __launch_bounds__(NT) k_combine2(CombineArgs a) {
+  const int kk = blockIdx.y;
+  double gmax = 0.0;
+  const long long n2 = a.n / 2, stride = (long long)gridDim.x * NT;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < n2; e += stride) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int t0 = 0; t0 < a.nt; t0 += 4) {  // four independent loads in flight, then the fmas in term order
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = t0 + u < a.nt ? __ldcs(reinterpret_cast<const double2*>(a.v[t0 + u] + kk * a.ld[t0 + u]) + e)
+                             : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t0 + u >= a.nt) break;
+        const double c = a.dc ? __ldg(a.dc + t0 + u) : a.c[t0 + u];
+        s.x = fma(c, v[u].x, s.x);
+        s.y = fma(c, v[u].y, s.y);
+      }
+    }
+    reinterpret_cast<double2*>(a.out + kk * a.ld_out)[e] = s;
+    gacc(gmax, s.x);
+    gacc(gmax, s.y);
+  }
+  if (a.guard) guard_max(a.guard, gmax);
+}
+
+bool combine_vec_ok(const CombineArgs& a) {
+  if (a.n & 1 || ((uintptr_t)a.out & 15) || (a.ld_out & 1)) return false;
+  for (int t = 0; t < a.nt; ++t)
+    if (((uintptr_t)a.v[t] & 15) || (a.ld[t] & 1)) return false;
+  return true;
 }
 
 __global__ void __launch_bounds__(NT) k_maxabs(int k, long long n, const double* x, long long ld,
@@ -503,8 +577,13 @@ int hps_combine(int k, long long n, int nterms, const double* coefs, const doubl
   a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out;
   for (int t = 0; t < nterms; ++t) { a.c[t] = coefs[t]; a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
   a.guard = reinterpret_cast<unsigned long long*>(guard);
-  dim3 grid(stream_blocks(n), (unsigned)k);
-  k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  if (combine_vec_ok(a)) {
+    dim3 grid(stream_blocks(n / 2), (unsigned)k);
+    k_combine2<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  } else {
+    dim3 grid(stream_blocks(n), (unsigned)k);
+    k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  }
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
 }
@@ -517,8 +596,13 @@ int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const 
   a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out; a.dc = dcoefs;
   for (int t = 0; t < nterms; ++t) { a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
   a.guard = reinterpret_cast<unsigned long long*>(guard);
-  dim3 grid(stream_blocks(n), (unsigned)k);
-  k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  if (combine_vec_ok(a)) {
+    dim3 grid(stream_blocks(n / 2), (unsigned)k);
+    k_combine2<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  } else {
+    dim3 grid(stream_blocks(n), (unsigned)k);
+    k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+  }
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
 }
