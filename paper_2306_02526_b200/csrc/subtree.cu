@@ -20,7 +20,7 @@ namespace hpsb {
 
 namespace {
 
-constexpr int NT = 128;          // 512 subtree CTAs of 128 threads fit one wave on 148 SMs
+constexpr int NT = 256;          // 512 subtree CTAs of 256 threads (64 registers) fit one wave on 148 SMs
 constexpr int MAXF = 10;          // fused levels
 constexpr int kMaxRows = 2048;    // operator rows of one CTA on one level
 constexpr int U = 4;
@@ -120,7 +120,7 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
 }
 
 template <int KM>
-__global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_up(SubArgs a) {
+__global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
   extern __shared__ double sm[];
   double* Hs = sm;                    // children's fluxes of the current level [child][KM][nbc]
   double* Hn = Hs + KM * a.hcap;      // this level's fluxes [node][KM][n12]
@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
 // boundary is read from u once, every interface value this CTA produces is
 // kept (and written through to u) so lower levels gather from shared memory.
 template <int KM>
-__global__ void __launch_bounds__(NT, KM == 1 ? 6 : 1) k_sub_down_local(SubArgs a) {
+__global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_down_local(SubArgs a) {
   extern __shared__ double sm[];
   double* red = sm;                        // 2 * NT * KM
   double* uloc = sm + 2 * NT * KM;         // [KM][nslots]
