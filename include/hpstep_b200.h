@@ -109,7 +109,10 @@ size_t hps_ops_device_bytes(const hps_ops* ops);
 /* Enable the tensor-product leaf solve for a constant-coefficient operator
  * set (leaf_fd.cu): host = Vx^-1, Vy^-T, Vx, Vy^T, rden (q x q each, row-major;
  * rden[a][b] = 1 / (lx_a + ly_b + sigma + dtg c)), then the interior parts of the
- * flux rows d1x[0], d1x[p-1], d1y[0], d1y[p-1] (q each); count = 5q^2 + 4q.
+ * flux rows d1x[0], d1x[p-1], d1y[0], d1y[p-1] (q each), then the couplings of
+ * the interior points to the boundary, dtg(-c11 d2x + c1 d1x)[1..p-2][0],
+ * ...[1..p-2][p-1], dtg(-c22 d2y + c2 d1y)[1..p-2][0], ...[1..p-2][p-1]
+ * (q each); count = 5q^2 + 8q.
  * host = NULL disables it.  Replaces the dense A_ii^-1 apply of
  * solver.py:221-228 with the Kronecker-sum factorisation of A_ii. */
 int hps_ops_set_leaf_fd(hps_ops* ops, const double* host, int count);

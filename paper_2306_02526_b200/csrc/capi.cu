@@ -768,8 +768,8 @@ extern "C" int hps_ops_set_leaf_fd(hps_ops* h, const double* host, int count) {
   const Plan& P = *O.plan;
   if (!host) { O.fd = nullptr; return HPS_OK; }  // disable (the buffer stays owned)
   const int q = P.q;
-  if (!O.shared_leaf || !leaf_fd_supported(q) || count != 5 * q * q + 4 * q) {
-    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in {8, 10, 14} and %d values", 5 * q * q + 4 * q);
+  if (!O.shared_leaf || !leaf_fd_supported(q) || count != 5 * q * q + 8 * q) {
+    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in {8, 10, 14} and %d values", 5 * q * q + 8 * q);
     return HPS_ERR_ARG;
   }
   double* d = ops_alloc(O, (size_t)count, false);

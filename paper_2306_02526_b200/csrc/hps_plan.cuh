@@ -211,6 +211,13 @@ GsSplit gs_split(long long M, int N, int K);  // (node, rhs) rows x operator row
 int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,
             cudaStream_t st);
 bool leaf_fd_supported(int q);
+// tensor-product leaf solve split over the two sweeps: the up sweep writes only
+// the fluxes h, the down sweep solves u_int = A_ii^-1 (r - A_ib u_b) directly
+bool leaf_fd_down_enabled();
+int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* H, long long ld_h,
+                 cudaStream_t st);
+int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, const int* lbg, const double* u,
+                 long long ld_u, double* uint, long long ld_uint, cudaStream_t st);
 
 // persistent dataflow kernel for wide shared-layout levels (mega.cu): up
 // levels [u0, u1) deepest first, then down levels [d0, d1) root first, over

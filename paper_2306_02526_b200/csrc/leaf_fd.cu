@@ -27,10 +27,18 @@ constexpr int NT = 256;
 
 struct FdArgs {
   int L, k, nw;
-  const double* g; long long ld_g;   // body load rows (leaf l interior at l*ni)
-  double* WH; long long ld_wh;       // [w | h] rows of nw = ni + nb per leaf
-  const double* mats;                // Vxi, VyiT, Vx, VyT, den (q x q each), ex0, ex1, ey0, ey1 (q each)
+  const double* g; long long ld_g;   // body load rows (leaf l interior at l*ni); null = zero
+  double* WH; long long ld_wh;       // FD_UP_WH: [w | h] rows of nw = ni + nb per leaf
+  double* H; long long ld_h;         // FD_UP_H: h rows of nb per leaf
+  const int* lbg;                    // FD_DOWN: leaf boundary DOF ids (L x nb, first leaf of the range)
+  const double* u; long long ld_u;   // FD_DOWN: solution rows (boundary values read through lbg)
+  double* uint; long long ld_uint;   // FD_DOWN: interior output (leaf l at l*ni)
+  const double* mats;                // Vxi, VyiT, Vx, VyT, den (q x q each), flux rows ex0, ex1, ey0, ey1,
+                                     // then the interior-boundary couplings bx0, bx1, by0, by1 (q each)
 };
+
+// modes of the tensor-core kernel
+enum FdMode { FD_UP_WH = 0, FD_UP_H = 1, FD_DOWN = 2 };
 
 template <int Q>
 __global__ void __launch_bounds__(NT) k_leaf_fd(FdArgs a) {
@@ -123,13 +131,21 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-template <int Q>
+// FD_DOWN is the leaf half of the downward sweep without storing w:
+//     u_int = A_ii^-1 (r - A_ib u_b)   (= S_leaf u_b + w, solver.py:269-276)
+// where A_ib u_b at interior point (x, y) couples only the four boundary
+// points on its grid lines: bx0[x] u(0,y) + bx1[x] u(p-1,y) + by0[y] u(x,0)
+// + by1[y] u(x,p-1).
+template <int Q, int MODE>
 __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
-  constexpr int NI = Q * Q, NB = 4 * Q;
+  constexpr int NI = Q * Q, NB = 4 * Q, UBS = 4 * Q + 8;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, kk = blockIdx.y;
-  double* bufB = sm + warp * 16 * (SB + SA);   // stride SB
-  double* bufA = bufB + 16 * SB;               // stride SA
+  double* bufB = sm + warp * (16 * (SB + SA) + UBS);   // stride SB
+  double* bufA = bufB + 16 * SB;                       // stride SA
+  double* ub = bufA + 16 * SA;                         // FD_DOWN: the leaf's boundary values
+  double* cst = sm + 8 * (16 * (SB + SA) + UBS);       // flux rows + couplings (8q), shared by the CTA
+  for (int e = threadIdx.x; e < 8 * Q; e += 256) cst[e] = a.mats[5 * NI + e];
   const int gr = lane >> 2, gc = lane & 3;
   pdl_trigger();
   // constant fragments: A operands (Vx^-1, Vx) as [m tile][k step], B operands (Vy^-T, Vy^T) as [k step][n tile]
@@ -155,28 +171,57 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     for (int nj = 0; nj < 2; ++nj)
 #pragma unroll
       for (int h = 0; h < 2; ++h) fR[mi][nj][h] = mat(4, mi * 8 + gr, nj * 8 + 2 * gc + h);
-  const double* E = a.mats + 5 * NI;
+  const double* E = cst;
+  const double* Bc = cst + 4 * Q;
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
-  __syncwarp();
+  __syncthreads();
   pdl_wait();
-  const double* g = a.g + kk * a.ld_g;
-  double* wh = a.WH + kk * a.ld_wh;
+  const double* g = a.g ? a.g + kk * a.ld_g : nullptr;
   const int nwarps = gridDim.x * 8;
   constexpr int NR = (NI + 31) / 32;  // body-load values per lane
+  constexpr int NU = (NB + 31) / 32;  // boundary values per lane (FD_DOWN)
   double nxt[NR];                     // next leaf's body load, prefetched during this leaf
+  double nub[MODE == FD_DOWN ? NU : 1];
   auto fetch = [&](int leaf) {
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
       const int e = lane + 32 * i;
-      nxt[i] = (leaf < a.L && e < NI) ? g[(long long)leaf * NI + e] : 0.0;
+      nxt[i] = (g && leaf < a.L && e < NI) ? g[(long long)leaf * NI + e] : 0.0;
+    }
+    if (MODE == FD_DOWN) {
+      const double* u = a.u + kk * a.ld_u;
+#pragma unroll
+      for (int i = 0; i < NU; ++i) {
+        const int b = lane + 32 * i;
+        nub[i] = (leaf < a.L && b < NB) ? u[a.lbg[(long long)leaf * NB + b]] : 0.0;
+      }
     }
   };
   fetch(blockIdx.x * 8 + warp);
   for (int l = blockIdx.x * 8 + warp; l < a.L; l += nwarps) {
+    if (MODE == FD_DOWN) {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      const int e = lane + 32 * i;
-      if (e < NI) bufB[(e / Q) * SB + e % Q] = nxt[i];
+      for (int i = 0; i < NU; ++i) {
+        const int b = lane + 32 * i;
+        if (b < NB) ub[b] = nub[i];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int e = lane + 32 * i;
+        if (e < NI) {
+          const int x = e / Q, y = e % Q;
+          const double cpl = Bc[x] * ub[y] + Bc[Q + x] * ub[3 * Q + y] + Bc[2 * Q + y] * ub[Q + 2 * x] +
+                             Bc[3 * Q + y] * ub[Q + 2 * x + 1];
+          bufB[x * SB + y] = nxt[i] - cpl;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        const int e = lane + 32 * i;
+        if (e < NI) bufB[(e / Q) * SB + e % Q] = nxt[i];
+      }
     }
     fetch(l + nwarps);
     __syncwarp();
@@ -241,8 +286,16 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     }
     store(bufB, SB);
     __syncwarp();
-    double* out = wh + (long long)l * a.nw;
-    for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
+    if (MODE == FD_DOWN) {
+      double* out = a.uint + kk * a.ld_uint + (long long)l * NI;
+      for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
+      __syncwarp();
+      continue;
+    }
+    double* out = MODE == FD_UP_WH ? a.WH + kk * a.ld_wh + (long long)l * a.nw
+                                   : a.H + kk * a.ld_h + (long long)l * NB - NI;  // h at out[NI + b]
+    if (MODE == FD_UP_WH)
+      for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
     // h = D_bi w along the grid line of each boundary point
     for (int b = lane; b < NB; b += 32) {
       double s = 0.0;
@@ -265,6 +318,48 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
 
 }  // namespace
 
+template <int MODE>
+static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaStream_t st) {
+  const size_t smem = ((size_t)8 * (16 * (SB + SA) + 4 * P.q + 8) + 8 * P.q) * 8;
+  const unsigned warps = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 2);  // one wave
+  dim3 g2(warps, (unsigned)k);
+#define HPSB_FD2(QQ)                                                                                   \
+  if (P.q == QQ) {                                                                                     \
+    static bool attr = false;                                                                          \
+    if (!attr) {                                                                                       \
+      HPSB_CUDA(cudaFuncSetAttribute(k_leaf_fd_mma<QQ, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     64 * 1024));                                                      \
+      attr = true;                                                                                     \
+    }                                                                                                  \
+    HPSB_CUDA(launch_pdl(k_leaf_fd_mma<QQ, MODE>, g2, dim3(256), smem, st, a));                        \
+    HPSB_LAUNCH_CHECK();                                                                               \
+    return 0;                                                                                          \
+  }
+  HPSB_FD2(8) HPSB_FD2(10) HPSB_FD2(14)
+#undef HPSB_FD2
+  set_error("leaf_fd: no kernel for q = %d", P.q);
+  return -1;
+}
+
+bool leaf_fd_down_enabled() { return !getenv("HPSB_FD_SIMT") && !getenv("HPSB_NO_FD_DOWN"); }
+
+int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* H, long long ld_h,
+                 cudaStream_t st) {
+  if (nleaf <= 0) return 0;
+  FdArgs a{};
+  a.L = nleaf; a.k = k; a.g = g; a.ld_g = ld_g; a.H = H; a.ld_h = ld_h; a.mats = ops.fd;
+  return launch_fd_mma<FD_UP_H>(*ops.plan, a, nleaf, k, st);
+}
+
+int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, const int* lbg, const double* u,
+                 long long ld_u, double* uint, long long ld_uint, cudaStream_t st) {
+  if (nleaf <= 0) return 0;
+  FdArgs a{};
+  a.L = nleaf; a.k = k; a.g = g; a.ld_g = ld_g; a.lbg = lbg; a.u = u; a.ld_u = ld_u;
+  a.uint = uint; a.ld_uint = ld_uint; a.mats = ops.fd;
+  return launch_fd_mma<FD_DOWN>(*ops.plan, a, nleaf, k, st);
+}
+
 int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,
             cudaStream_t st) {
   const Plan& P = *ops.plan;
@@ -274,15 +369,7 @@ int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, d
   a.g = g; a.ld_g = ld_g; a.WH = WH; a.ld_wh = ld_wh; a.mats = ops.fd;
   const unsigned groups = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 4);
   dim3 grid(groups, (unsigned)k);
-  if (!getenv("HPSB_FD_SIMT")) {  // tensor-core variant
-    const size_t smem = (size_t)8 * 16 * (SB + SA) * 8;
-    const unsigned warps = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 2);  // one wave
-    dim3 g2(warps, (unsigned)k);
-#define HPSB_FD2(QQ) \
-  if (P.q == QQ) { HPSB_CUDA(launch_pdl(k_leaf_fd_mma<QQ>, g2, dim3(256), smem, st, a)); HPSB_LAUNCH_CHECK(); return 0; }
-    HPSB_FD2(8) HPSB_FD2(10) HPSB_FD2(14)
-#undef HPSB_FD2
-  }
+  if (!getenv("HPSB_FD_SIMT")) return launch_fd_mma<FD_UP_WH>(P, a, nleaf, k, st);  // tensor-core variant
 #define HPSB_FD(QQ) \
   if (P.q == QQ) { HPSB_CUDA(launch_pdl(k_leaf_fd<QQ>, grid, dim3(NT), 0, st, a)); HPSB_LAUNCH_CHECK(); return 0; }
   HPSB_FD(8) HPSB_FD(10) HPSB_FD(14)

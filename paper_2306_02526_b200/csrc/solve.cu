@@ -207,7 +207,9 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   // leaf outputs: W (row stride ldw, rhs stride sw) and H (child stride hs, rhs stride sh)
   long long ldw = P.ni, sw = Lni, hs = P.nb, sh = Lnb;
   const double* Hleaf = ws.Hleaf;
-  const bool stacked = g && ops.shared_leaf;  // [w | h] rows of one GEMM / the tensor-product solve
+  // tensor-product leaves: h only on the way up, u_int = A_ii^-1 (r - A_ib u_b) on the way down
+  const bool fd_down = ops.shared_leaf && ops.fd && leaf_fd_down_enabled();
+  const bool stacked = g && ops.shared_leaf && !fd_down;  // [w | h] rows of one GEMM / the tensor-product solve
   if (stacked) {
     ldw = nw; sw = (long long)P.L * nw; hs = nw; sh = sw;
     Hleaf = ws.W + P.ni;
@@ -215,7 +217,9 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
 
   if (phases & SOLVE_UP) {
     // (2) leaf particular solutions and their fluxes (solver.py:219-230)
-    if (g && ops.shared_leaf && ops.fd) {
+    if (g && fd_down) {
+      if (int rc = leaf_fd_up_h(ops, k, nleaf, g, ld_g, ws.Hleaf + (long long)leaf0 * P.nb, Lnb, st)) return rc;
+    } else if (g && ops.shared_leaf && ops.fd) {
       // tensor-product leaf solve: same [W | H] rows, 5x fewer flops
       if (int rc = leaf_fd(ops, k, nleaf, g, ld_g, ws.W + (long long)leaf0 * nw, sw, st)) return rc;
     } else if (g && ops.shared_leaf) {
@@ -292,6 +296,9 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
       if (int rc = subtree_down(ops, ws, k, up, u, ld_u, b0, b1, st)) return rc;
     }
     // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
+    if (fd_down)
+      return leaf_fd_down(ops, k, nleaf, g, ld_g, P.leaf_bnd_gidx + (long long)leaf0 * P.nb, u, ld_u,
+                          u + (long long)leaf0 * P.ni, ld_u, st);
     long long n = (long long)k * nleaf * P.nb;
     HPSB_CUDA(launch_pdl(k_leaf_gather, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, nleaf, P.nb, Lnb,
                          (const int*)(P.leaf_bnd_gidx + (long long)leaf0 * P.nb), (const double*)u, ld_u,

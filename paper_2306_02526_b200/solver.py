@@ -485,8 +485,13 @@ def tensor_leaf_factors(disc, sigma, dt_gamma, cond_max=1e6):
     den = 1.0 / den                      # the kernel multiplies
     p = tree.p
     edges = [st.d1x[0, i], st.d1x[p - 1, i], st.d1y[0, i], st.d1y[p - 1, i]]
+    # interior -> boundary couplings of the shifted operator (A_ib of solver.py:53-64)
+    cpl = [dt_gamma * (-c11 * st.d2x[i, 0] + c1 * st.d1x[i, 0]),
+           dt_gamma * (-c11 * st.d2x[i, p - 1] + c1 * st.d1x[i, p - 1]),
+           dt_gamma * (-c22 * st.d2y[i, 0] + c2 * st.d1y[i, 0]),
+           dt_gamma * (-c22 * st.d2y[i, p - 1] + c2 * st.d1y[i, p - 1])]
     return np.concatenate([Vxi.ravel(), Vyi.T.ravel(), Vx.ravel(), Vy.T.ravel(), den.ravel()]
-                          + [e.ravel() for e in edges])
+                          + [e.ravel() for e in edges] + [c.ravel() for c in cpl])
 
 
 def _jsonable(v):

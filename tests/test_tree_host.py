@@ -94,22 +94,29 @@ def test_tensor_leaf_factors_reproduce_dense_interior_solve(p, dtg):
     import paper_2306_02526_b200 as hb
     from paper_2306_02526_b200.solver import tensor_leaf_factors
     tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, p)
-    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=0.7, c=0.3))
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=0.7, c1=0.4, c2=-0.2, c=0.3))
     q, ni = tree.q, tree.ni
     fd = tensor_leaf_factors(disc, 1.0, dtg)
-    assert fd is not None and fd.size == 5 * q * q + 4 * q
-    Aii, _ = disc.leaf_blocks(0)
+    assert fd is not None and fd.size == 5 * q * q + 8 * q
+    Aii, Aib = disc.leaf_blocks(0)
     r = np.random.default_rng(1).standard_normal(ni)
     w_ref = np.linalg.solve(np.eye(ni) + dtg * Aii, r)
     M = fd[:5 * ni].reshape(5, q, q)
     W = M[2] @ (((M[0] @ r.reshape(q, q)) @ M[1]) * M[4]) @ M[3]
     assert np.linalg.norm(W.ravel() - w_ref) / np.linalg.norm(w_ref) < 1e-13
-    E = fd[5 * ni:].reshape(4, q)
+    E = fd[5 * ni:5 * ni + 4 * q].reshape(4, q)
     h = np.concatenate([E[0] @ W,                                    # east: d/dx, rows yi
                         np.stack([W @ E[2], W @ E[3]], 1).ravel(),   # north/south interleaved
                         E[1] @ W])                                   # west
     D_bi = disc.stencil.D_bnd[:, :ni]
     assert np.allclose(h, D_bi @ W.ravel(), rtol=1e-12, atol=1e-12 * np.abs(h).max())
+    # interior -> boundary couplings used by the down sweep: dtg A_ib u_b
+    B = fd[5 * ni + 4 * q:].reshape(4, q)
+    ub = np.random.default_rng(2).standard_normal(4 * q)
+    x, y = np.divmod(np.arange(ni), q)
+    cpl = B[0][x] * ub[y] + B[1][x] * ub[3 * q + y] + B[2][y] * ub[q + 2 * x] + B[3][y] * ub[q + 2 * x + 1]
+    ref = dtg * (Aib @ ub)
+    assert np.allclose(cpl, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
 
 
 def test_tensor_leaf_factors_only_for_constant_coefficients():
