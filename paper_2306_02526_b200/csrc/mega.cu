@@ -59,10 +59,19 @@ struct MSeg {
   const unsigned* wpar; int wpar_t;       // down: parents' counters (level d-1)
   const unsigned* wup; int wup_t;         // down: own nodes' up counters
   double* part; unsigned* sem; // split partials [S][NG*NB][R], semaphores [NG*RB]
+  // root pair: the root's down product S u_bnd needs only the Dirichlet data,
+  // so its tasks run at the head of the list, concurrently with the up sweep;
+  // the root's up tasks (w3 = X33^-1 r3) and down tasks share one semaphore per
+  // row block and the last arriver writes u3 = S u_bnd + w3 = sum of both
+  // partial sets (down splits first, then up splits)
+  int pair;
+  const double *pdn, *pup; int Sdn, Sup;
 };
 
 struct MProg {
   int nseg, ntasks;
+  int head, dedicated;          // the first `head` tasks (the root's down product) run on the last
+                                // `dedicated` CTAs only, every other task on the remaining CTAs
   unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / end, ns
   unsigned* reset; int nreset;  // counters to zero at exit (incl. the exit counter at the end)
   MSeg s[MAXSEG];
@@ -95,7 +104,11 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
   __shared__ unsigned s_last;
   const int tid = threadIdx.x, grp = tid >> 5, q = tid & 31;
   pdl_wait();
-  for (int t = blockIdx.x; t < p.ntasks; t += gridDim.x) {
+  const int G = gridDim.x, KR = p.dedicated;
+  const bool ded = KR > 0 && (int)blockIdx.x >= G - KR;
+  const int tfirst = ded ? (int)blockIdx.x - (G - KR) : p.head + (int)blockIdx.x;
+  const int tstep = ded ? KR : G - KR, tend = ded ? p.head : p.ntasks;
+  for (int t = tfirst; t < tend; t += tstep) {
     int si = 0;
     while (t >= p.s[si].task0 + p.s[si].ntasks) ++si;
     const MSeg& g = p.s[si];
@@ -177,23 +190,32 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
 #pragma unroll
     for (int gg = 0; gg < MGRP; ++gg) y += red[gg][oj][r];
     bool emit_now = true;
-    if (g.S > 1) {
+    if (g.S > 1 || g.pair) {
       const size_t slot = (size_t)(ng * MNB + oj) * g.R + orow;
       const size_t pstride = (size_t)g.NG * MNB * g.R;
       if (ovalid) g.part[(size_t)split * pstride + slot] = y;
       __threadfence();
       __syncthreads();
-      if (tid == 0) s_last = atomicAdd(g.sem + ng * g.RB + rb, 1u) == (unsigned)g.S - 1;
+      const unsigned total = g.pair ? (unsigned)(g.Sdn + g.Sup) : (unsigned)g.S;
+      if (tid == 0) s_last = atomicAdd(g.sem + ng * g.RB + rb, 1u) == total - 1;
       __syncthreads();
       emit_now = s_last;
       if (emit_now) {
         __threadfence();
         y = 0.0;
-        if (ovalid)
-          for (int s = 0; s < g.S; ++s) y += __ldcg(g.part + (size_t)s * pstride + slot);
+        if (ovalid) {
+          if (g.pair) {
+            for (int s = 0; s < g.Sdn; ++s) y += __ldcg(g.pdn + (size_t)s * pstride + slot);
+            for (int s = 0; s < g.Sup; ++s) y += __ldcg(g.pup + (size_t)s * pstride + slot);
+          } else {
+            for (int s = 0; s < g.S; ++s) y += __ldcg(g.part + (size_t)s * pstride + slot);
+          }
+        }
       }
     }
-    if (emit_now) {
+    if (emit_now && g.pair) {
+      if (ovalid) g.u[g.j3[(long long)(node0 + oj) * g.n3 + orow]] = y;
+    } else if (emit_now) {
       if (ovalid) {
         const int node = node0 + oj;
         if (g.up) {
@@ -210,6 +232,8 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
           g.u[oidx] = y;
         }
       }
+    }
+    if (emit_now) {
       __threadfence();
       __syncthreads();
       if (tid < nv) atomicAdd(g.done + node0 + tid, 1u);
@@ -233,6 +257,14 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
 }
 
 }  // namespace
+
+static bool pair_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_ROOT_PAIR");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
 
 bool mega_enabled() {
   static const bool on = [] {
@@ -266,7 +298,7 @@ void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles) {
       int RB, NG, S, KC, R, K;
       mega_dims(lv, d == 0, up, lv.c, RB, NG, S, KC, R, K);
       counters += (size_t)RB * NG;
-      if (S > 1) part_doubles += (size_t)S * NG * MNB * R;
+      if (S > 1 || d == 0) part_doubles += (size_t)S * NG * MNB * R;  // the root pair always uses partials
     }
   }
 }
@@ -337,10 +369,34 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     ++p.nseg;
     return true;
   };
+  // the root pair: the root's down product first (no inputs from this launch)
+  const bool pair = u0 == 0 && u1 > 0 && d0 == 0 && d1 > 0 && has_w3 && !jump && pair_enabled();
+  int iroot_dn = -1;
+  if (pair) {
+    iroot_dn = p.nseg;
+    if (!add(0, false)) return 1;
+  }
   for (int d = u1 - 1; d >= u0; --d)
     if (!add(d, true)) return 1;
-  for (int d = d0; d < d1; ++d)
+  for (int d = pair ? 1 : d0; d < d1; ++d)
     if (!add(d, false)) return 1;
+  if (pair) {
+    MSeg& dn = p.s[iroot_dn];
+    MSeg* upp = nullptr;
+    for (int i = 0; i < p.nseg; ++i)
+      if (p.s[i].up && p.s[i].Hout == nullptr) upp = &p.s[i];  // the root's up segment (no flux rows)
+    if (!upp || upp->RB != dn.RB || upp->NG != dn.NG || upp->R != dn.R) return 1;
+    for (MSeg* g : {&dn, upp}) {
+      g->pair = 1;
+      g->Sdn = dn.S; g->Sup = upp->S;
+      g->wup = nullptr;
+      g->done = dn.done;             // level 1's down tasks wait on the root's u3
+      g->sem = dn.sem;               // one semaphore per row block for both
+      if (!g->part) { g->part = part; part += (size_t)g->S * g->NG * MNB * g->R; }
+    }
+    dn.pdn = upp->pdn = dn.part;
+    dn.pup = upp->pup = upp->part;
+  }
   if (p.nseg == 0) return 0;
   p.ntasks = task;
   p.reset = cnt + 1;
@@ -353,7 +409,12 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     max_ctas = std::max(1, per_sm) * sms;
   }
-  const int grid = std::min(max_ctas, p.ntasks);
+  int grid = std::min(max_ctas, p.ntasks);
+  if (pair) {  // a quarter of the CTAs stream the root's down product while the up sweep climbs
+    grid = max_ctas;
+    p.head = p.s[iroot_dn].ntasks;
+    p.dedicated = std::max(1, grid / 4);
+  }
   const char* tr = getenv("HPSB_MEGA_TRACE");  // debug: per-task timeline appended to this file
   unsigned long long* dtrace = nullptr;
   if (tr) {
