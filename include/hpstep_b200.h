@@ -112,7 +112,9 @@ size_t hps_ops_device_bytes(const hps_ops* ops);
  * flux rows d1x[0], d1x[p-1], d1y[0], d1y[p-1] (q each), then the couplings of
  * the interior points to the boundary, dtg(-c11 d2x + c1 d1x)[1..p-2][0],
  * ...[1..p-2][p-1], dtg(-c22 d2y + c2 d1y)[1..p-2][0], ...[1..p-2][p-1]
- * (q each); count = 5q^2 + 8q.
+ * (q each), then Mx = c11 d2x - c1 d1x and My = c22 d2y - c2 d1y (p x p
+ * zero-padded to 16 x 16, row-major) and c -- the interior L u of the stage
+ * history is Mx G + G My^T - c G on the leaf grid G; count = 5q^2 + 8q + 513.
  * host = NULL disables it.  Replaces the dense A_ii^-1 apply of
  * solver.py:221-228 with the Kronecker-sum factorisation of A_ii. */
 int hps_ops_set_leaf_fd(hps_ops* ops, const double* host, int count);
@@ -150,6 +152,18 @@ size_t hps_solve_workspace_bytes(const hps_plan* plan, int k);
 int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
               long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
               long long ld_u, void* ws, size_t ws_bytes, void* stream);
+
+/* Fused ARK stage (timestep.py:259-261 after solver.py:201-276): hps_solve
+ * of the stage body load, plus the next stage's history L u at the leaf
+ * interiors (lu_int, k x L*ni rows of stride ld_lu, operators.py:276-301 at
+ * interior points) and guard = max(guard, max |u|) over the leaves' grids
+ * (timestep.py:198-203), computed by the leaf kernel of the downward sweep
+ * while the leaf's grid is on chip.  Constant coefficients with the
+ * tensor-product leaf solve only (HPS_ERR_ARG otherwise: use hps_solve +
+ * hps_leaf_eval). */
+int hps_solve_stage(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
+                    long long ld_g, double* u, long long ld_u, double* lu_int, long long ld_lu,
+                    double* guard, void* ws, size_t ws_bytes, void* stream);
 
 /* Subtree-sharded solve (the reference solves the whole tree
  * in one call, solver.py:201-276).  With a plan created with nparts = 2^lstar,

@@ -563,6 +563,19 @@ int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const d
                ws_bytes, (cudaStream_t)stream);
 }
 
+int hps_solve_stage(const hps_ops* h, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
+                    double* u, long long ld_u, double* lu_int, long long ld_lu, double* guard, void* ws,
+                    size_t ws_bytes, void* stream) {
+  if (!h || !fb || !u || !ws || !lu_int) { set_error("hps_solve_stage: null argument"); return HPS_ERR_ARG; }
+  const Ops& O = h->O;
+  if (!(O.shared_leaf && O.fd && leaf_fd_down_enabled())) {
+    set_error("hps_solve_stage: needs the tensor-product leaf solve (constant coefficients)");
+    return HPS_ERR_ARG;
+  }
+  return solve(O, SOLVE_ALL, 0, O.plan->nparts, k, fb, ld_f, g, ld_g, nullptr, 0, 0.0, u, ld_u, ws, ws_bytes,
+               (cudaStream_t)stream, lu_int, ld_lu, guard);
+}
+
 int hps_plan_partition(const hps_plan* h, int k, int* nparts, int* lstar, int* n12, long long* flux_offset) {
   if (!h) { set_error("hps_plan_partition: null plan"); return HPS_ERR_ARG; }
   const Plan& P = h->P;
@@ -768,8 +781,9 @@ extern "C" int hps_ops_set_leaf_fd(hps_ops* h, const double* host, int count) {
   const Plan& P = *O.plan;
   if (!host) { O.fd = nullptr; return HPS_OK; }  // disable (the buffer stays owned)
   const int q = P.q;
-  if (!O.shared_leaf || !leaf_fd_supported(q) || count != 5 * q * q + 8 * q) {
-    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in {8, 10, 14} and %d values", 5 * q * q + 8 * q);
+  if (!O.shared_leaf || !leaf_fd_supported(q) || count != 5 * q * q + 8 * q + 513) {
+    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in {8, 10, 14} and %d values",
+              5 * q * q + 8 * q + 513);
     return HPS_ERR_ARG;
   }
   double* d = ops_alloc(O, (size_t)count, false);

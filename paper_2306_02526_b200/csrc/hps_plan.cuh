@@ -217,7 +217,8 @@ bool leaf_fd_down_enabled();
 int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* H, long long ld_h,
                  cudaStream_t st);
 int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, const int* lbg, const double* u,
-                 long long ld_u, double* uint, long long ld_uint, cudaStream_t st);
+                 long long ld_u, double* uint, long long ld_uint, double* lu, long long ld_lu, double* guard,
+                 cudaStream_t st);
 
 // persistent dataflow kernel for wide shared-layout levels (mega.cu): up
 // levels [u0, u1) deepest first, then down levels [d0, d1) root first, over
@@ -235,7 +236,8 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
 enum SolvePhase { SOLVE_UP = 1, SOLVE_TOP = 2, SOLVE_DOWN = 4, SOLVE_ALL = 7 };
 int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
           const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
-          long long ld_u, void* ws, size_t ws_bytes, cudaStream_t st);
+          long long ld_u, void* ws, size_t ws_bytes, cudaStream_t st, double* lu = nullptr, long long ld_lu = 0,
+          double* guard = nullptr);
 // byte offset of level lstar's flux block (k x nparts x n12) in a workspace
 size_t exchange_offset(const Plan& P, int k);
 

@@ -33,8 +33,12 @@ struct FdArgs {
   const int* lbg;                    // FD_DOWN: leaf boundary DOF ids (L x nb, first leaf of the range)
   const double* u; long long ld_u;   // FD_DOWN: solution rows (boundary values read through lbg)
   double* uint; long long ld_uint;   // FD_DOWN: interior output (leaf l at l*ni)
+  double* lu; long long ld_lu;       // FD_DOWN, optional: L u at the interiors (the stage history)
+  unsigned long long* guard;         // ... and max |u| over the leaves' grids (bits, NaN sticky)
   const double* mats;                // Vxi, VyiT, Vx, VyT, den (q x q each), flux rows ex0, ex1, ey0, ey1,
-                                     // then the interior-boundary couplings bx0, bx1, by0, by1 (q each)
+                                     // then the interior-boundary couplings bx0, bx1, by0, by1 (q each),
+                                     // then Mx = c11 d2x - c1 d1x, My = c22 d2y - c2 d1y (16 x 16, zero
+                                     // padded) and c: L u = Mx G + G My^T - c G on the leaf grid G
 };
 
 // modes of the tensor-core kernel
@@ -145,7 +149,11 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   double* bufA = bufB + 16 * SB;                       // stride SA
   double* ub = bufA + 16 * SA;                         // FD_DOWN: the leaf's boundary values
   double* cst = sm + 8 * (16 * (SB + SA) + UBS);       // flux rows + couplings (8q), shared by the CTA
-  for (int e = threadIdx.x; e < 8 * Q; e += 256) cst[e] = a.mats[5 * NI + e];
+  constexpr int NCST = 8 * Q + (MODE == FD_DOWN ? 513 : 0);
+  for (int e = threadIdx.x; e < NCST; e += 256) cst[e] = a.mats[5 * NI + e];
+  const double* Mx = cst + 8 * Q;                      // FD_DOWN with L u: [x][s], 16 x 16
+  const double* My = Mx + 256;                         // [y][s]
+  double gmax = 0.0;
   const int gr = lane >> 2, gc = lane & 3;
   pdl_trigger();
   // constant fragments: A operands (Vx^-1, Vx) as [m tile][k step], B operands (Vy^-T, Vy^T) as [k step][n tile]
@@ -289,6 +297,59 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     if (MODE == FD_DOWN) {
       double* out = a.uint + kk * a.ld_uint + (long long)l * NI;
       for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
+      if (a.lu) {
+        // the leaf grid G (p x p in 16 x 16, zero padded) in both operand layouts:
+        // bufA (A operand, stride SA) and bufB (B operand, stride SB)
+        __syncwarp();
+        for (int e = lane; e < 256; e += 32) {
+          const int x = e >> 4, y = e & 15;
+          double v = 0.0;
+          if (x >= 1 && x <= Q && y >= 1 && y <= Q) v = bufB[(x - 1) * SB + (y - 1)];
+          else if (x == 0 && y >= 1 && y <= Q) v = ub[y - 1];
+          else if (x == Q + 1 && y >= 1 && y <= Q) v = ub[3 * Q + y - 1];
+          else if (y == 0 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1)];
+          else if (y == Q + 1 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1) + 1];
+          bufA[x * SA + y] = v;
+          const double av = fabs(v);
+          gmax = (av > gmax || av != av) ? av : gmax;
+        }
+        __syncwarp();
+        for (int e = lane; e < 256; e += 32) bufB[(e >> 4) * SB + (e & 15)] = bufA[(e >> 4) * SA + (e & 15)];
+        __syncwarp();
+        clear();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // Mx G
+          const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            const double am = Mx[(mi * 8 + gr) * 16 + k * 4 + gc];
+            dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
+            dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // + G My^T
+          const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) {
+            const double bm = My[(nj * 8 + gr) * 16 + k * 4 + gc];
+            dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
+            dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
+          }
+        }
+        double* lo = a.lu + kk * a.ld_lu + (long long)l * NI;
+        const double c0 = Mx[512];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int x = mi * 8 + gr, y = nj * 8 + 2 * gc + h;
+              if (x >= 1 && x <= Q && y >= 1 && y <= Q)
+                lo[(x - 1) * Q + (y - 1)] = acc[mi][nj][h] - c0 * bufA[x * SA + y];
+            }
+      }
       __syncwarp();
       continue;
     }
@@ -314,13 +375,21 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     }
     __syncwarp();
   }
+  if (MODE == FD_DOWN && a.guard) {  // max |u| over the staged grids (NaN sorts above inf)
+    unsigned long long bits = __double_as_longlong(gmax);
+    for (int off = 16; off > 0; off >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(0xffffffffu, bits, off);
+      bits = o > bits ? o : bits;
+    }
+    if (lane == 0 && bits && bits > __ldcg(a.guard)) atomicMax(a.guard, bits);
+  }
 }
 
 }  // namespace
 
 template <int MODE>
 static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaStream_t st) {
-  const size_t smem = ((size_t)8 * (16 * (SB + SA) + 4 * P.q + 8) + 8 * P.q) * 8;
+  const size_t smem = ((size_t)8 * (16 * (SB + SA) + 4 * P.q + 8) + 8 * P.q + 513) * 8;
   const unsigned warps = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 2);  // one wave
   dim3 g2(warps, (unsigned)k);
 #define HPSB_FD2(QQ)                                                                                   \
@@ -352,11 +421,13 @@ int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld
 }
 
 int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, const int* lbg, const double* u,
-                 long long ld_u, double* uint, long long ld_uint, cudaStream_t st) {
+                 long long ld_u, double* uint, long long ld_uint, double* lu, long long ld_lu, double* guard,
+                 cudaStream_t st) {
   if (nleaf <= 0) return 0;
   FdArgs a{};
   a.L = nleaf; a.k = k; a.g = g; a.ld_g = ld_g; a.lbg = lbg; a.u = u; a.ld_u = ld_u;
   a.uint = uint; a.ld_uint = ld_uint; a.mats = ops.fd;
+  a.lu = lu; a.ld_lu = ld_lu; a.guard = reinterpret_cast<unsigned long long*>(guard);
   return launch_fd_mma<FD_DOWN>(*ops.plan, a, nleaf, k, st);
 }
 

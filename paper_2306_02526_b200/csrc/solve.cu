@@ -174,7 +174,8 @@ size_t exchange_offset(const Plan& P, int k) {
 // part = the whole solve of solver.py:201-276).
 int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
           const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
-          long long ld_u, void* wsp, size_t ws_bytes, cudaStream_t st) {
+          long long ld_u, void* wsp, size_t ws_bytes, cudaStream_t st, double* lu, long long ld_lu,
+          double* guard) {
   const Plan& P = *ops.plan;
   if (k <= 0) return 0;
   if (ws_bytes < workspace_bytes(P, k)) {
@@ -298,7 +299,11 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
     // (5) leaf interiors: u_int = S_leaf u_bnd + w (solver.py:269-276)
     if (fd_down)
       return leaf_fd_down(ops, k, nleaf, g, ld_g, P.leaf_bnd_gidx + (long long)leaf0 * P.nb, u, ld_u,
-                          u + (long long)leaf0 * P.ni, ld_u, st);
+                          u + (long long)leaf0 * P.ni, ld_u, lu, ld_lu, guard, st);
+    if (lu) {
+      set_error("solve: the fused stage history needs the tensor-product leaf solve");
+      return -1;
+    }
     long long n = (long long)k * nleaf * P.nb;
     HPSB_CUDA(launch_pdl(k_leaf_gather, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, nleaf, P.nb, Lnb,
                          (const int*)(P.leaf_bnd_gidx + (long long)leaf0 * P.nb), (const double*)u, ld_u,

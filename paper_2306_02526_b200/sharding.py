@@ -341,6 +341,9 @@ class ShardedTimeStepper(TimeStepper):
     def _eval_lu(self, U, out, guard=None):
         self._eval(U, lu_int=out, guard=guard, leaves=self._leaves)
 
+    def _fused_stage(self, fb, body, out, lu, guard):
+        return False                      # the sharded solve runs in phases with an exchange
+
     def _ranges(self):
         return (self._ir, self._edges)
 

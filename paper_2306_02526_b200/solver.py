@@ -299,6 +299,27 @@ class HpsOperatorSet:
         _lib.check(rc, "hps_solve")
         return out
 
+    @property
+    def fuses_stage_history(self):
+        """Whether ``solve_stage_device`` can return the stage history L u
+        (tensor-product leaf solve, constant coefficients)."""
+        return self.leaf_solve == "tensor" and os.environ.get("HPSB_NO_FUSED_LU") != "1" \
+            and os.environ.get("HPSB_NO_FD_DOWN") is None and os.environ.get("HPSB_FD_SIMT") is None
+
+    def solve_stage_device(self, fb, body, out, lu, guard):
+        """``solve_device`` plus the interior L u of the solution into ``lu``
+        (k, >= L*ni) and max |u| into ``guard`` (hps_solve_stage)."""
+        k = out.shape[0]
+        ld_f = 0 if fb.shape[0] == 1 else fb.stride(0)
+        ld_g = 0 if body is None or body.shape[0] == 1 else body.stride(0)
+        ws = self.plan.workspace(k)
+        rc = self._lib.hps_solve_stage(
+            self.handle, k, fb.data_ptr(), ld_f, None if body is None else body.data_ptr(), ld_g,
+            out.data_ptr(), out.stride(0), lu.data_ptr(), lu.stride(0),
+            None if guard is None else guard.data_ptr(), ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_solve_stage")
+        return out
+
     def solve_phase(self, phases, part0, part1, fb, body, out, jump=None, inv_dt=None):
         """One or more phases of a subtree-partitioned solve (hps_solve_phase):
         ``_lib.HPS_PHASE_UP`` / ``TOP`` / ``DOWN`` over parts [part0, part1).
@@ -490,8 +511,14 @@ def tensor_leaf_factors(disc, sigma, dt_gamma, cond_max=1e6):
            dt_gamma * (-c11 * st.d2x[i, p - 1] + c1 * st.d1x[i, p - 1]),
            dt_gamma * (-c22 * st.d2y[i, 0] + c2 * st.d1y[i, 0]),
            dt_gamma * (-c22 * st.d2y[i, p - 1] + c2 * st.d1y[i, p - 1])]
+    # interior L u of the stage history on the leaf grid G: Mx G + G My^T - c G
+    Mx = np.zeros((16, 16))
+    My = np.zeros((16, 16))
+    Mx[:p, :p] = c11 * st.d2x - c1 * st.d1x
+    My[:p, :p] = c22 * st.d2y - c2 * st.d1y
     return np.concatenate([Vxi.ravel(), Vyi.T.ravel(), Vx.ravel(), Vy.T.ravel(), den.ravel()]
-                          + [e.ravel() for e in edges] + [c.ravel() for c in cpl])
+                          + [e.ravel() for e in edges] + [c.ravel() for c in cpl]
+                          + [Mx.ravel(), My.ravel(), [c0]])
 
 
 def _jsonable(v):

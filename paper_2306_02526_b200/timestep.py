@@ -673,6 +673,15 @@ class TimeStepper:
         a = self._ir[0]
         return v if a == 0 else v[:, a:]
 
+    def _fused_stage(self, fb, body, out, lu, guard):
+        """Stage solve with the history L u and the guard from the leaf kernel
+        of the downward sweep (hps_solve_stage); False when not available."""
+        if not self.ops.fuses_stage_history or self.solve_timer is not None:
+            return False
+        if not self._dry:
+            self.ops.solve_stage_device(fb, body, out, lu, guard)
+        return True
+
     def _eval_lu(self, U, out, guard=None):
         """Stage history L u at the local leaf interiors."""
         self._eval(U, lu_int=out, guard=guard)
@@ -771,10 +780,13 @@ class TimeStepper:
                     terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), iv(phi)))
             combine(terms, r, n=Lni)
             ui = U[i & 1]
-            self._solve(self.ops, self._bc(ti), r, ui)
-            if i < s - 1:
+            if i < s - 1 and self._fused_stage(self._bc(ti), r, ui, Lu[i], guards[i - 1]):
+                pass                                 # solve + history L u_i + guard in one pass
+            elif i < s - 1:
+                self._solve(self.ops, self._bc(ti), r, ui)
                 self._eval_lu(ui, Lu[i], guard=guards[i - 1])
             else:
+                self._solve(self.ops, self._bc(ti), r, ui)
                 self._owned_maxabs(ui, guards[i - 1])
             stage_q_g(i, ti, ui)
         w = pair.bhat - Ah[s - 1]

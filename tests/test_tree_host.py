@@ -97,7 +97,7 @@ def test_tensor_leaf_factors_reproduce_dense_interior_solve(p, dtg):
     disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=0.7, c1=0.4, c2=-0.2, c=0.3))
     q, ni = tree.q, tree.ni
     fd = tensor_leaf_factors(disc, 1.0, dtg)
-    assert fd is not None and fd.size == 5 * q * q + 8 * q
+    assert fd is not None and fd.size == 5 * q * q + 8 * q + 513
     Aii, Aib = disc.leaf_blocks(0)
     r = np.random.default_rng(1).standard_normal(ni)
     w_ref = np.linalg.solve(np.eye(ni) + dtg * Aii, r)
@@ -111,12 +111,23 @@ def test_tensor_leaf_factors_reproduce_dense_interior_solve(p, dtg):
     D_bi = disc.stencil.D_bnd[:, :ni]
     assert np.allclose(h, D_bi @ W.ravel(), rtol=1e-12, atol=1e-12 * np.abs(h).max())
     # interior -> boundary couplings used by the down sweep: dtg A_ib u_b
-    B = fd[5 * ni + 4 * q:].reshape(4, q)
+    B = fd[5 * ni + 4 * q:5 * ni + 8 * q].reshape(4, q)
     ub = np.random.default_rng(2).standard_normal(4 * q)
     x, y = np.divmod(np.arange(ni), q)
     cpl = B[0][x] * ub[y] + B[1][x] * ub[3 * q + y] + B[2][y] * ub[q + 2 * x] + B[3][y] * ub[q + 2 * x + 1]
     ref = dtg * (Aib @ ub)
     assert np.allclose(cpl, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    # stage history on the leaf grid: Mx G + G My^T - c G = L u at the interiors
+    o = 5 * ni + 8 * q
+    Mx, My, c0 = fd[o:o + 256].reshape(16, 16), fd[o + 256:o + 512].reshape(16, 16), fd[o + 512]
+    ui = np.random.default_rng(3).standard_normal(ni)
+    G = np.zeros((16, 16))
+    G[1:p - 1, 1:p - 1] = ui.reshape(q, q)
+    G[0, 1:p - 1], G[p - 1, 1:p - 1] = ub[:q], ub[3 * q:]
+    G[1:p - 1, 0], G[1:p - 1, p - 1] = ub[q:3 * q:2], ub[q + 1:3 * q:2]
+    lop = (Mx @ G + G @ My.T - c0 * G)[1:p - 1, 1:p - 1].ravel()
+    ref = -(Aii @ ui + Aib @ ub)          # L = -A at the interior points
+    assert np.allclose(lop, ref, rtol=1e-11, atol=1e-11 * np.abs(ref).max())
 
 
 def test_tensor_leaf_factors_only_for_constant_coefficients():
