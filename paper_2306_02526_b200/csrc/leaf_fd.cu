@@ -140,6 +140,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // where A_ib u_b at interior point (x, y) couples only the four boundary
 // points on its grid lines: bx0[x] u(0,y) + bx1[x] u(p-1,y) + by0[y] u(x,0)
 // + by1[y] u(x,p-1).
+// Constant operands live in shared memory (one copy per CTA) in strides that
+// make every fragment load conflict-free: A-type (row-indexed by the lane's
+// group) stride CSA = 20, B-type stride CSB = 24.
+constexpr int CSA = 20, CSB = 24;
+constexpr int kFdCst = 5 * 16 * CSA + 2 * 16 * CSB;  // Vxi, Vx, Mx, My, 1/den | VyiT, VyT
+
 template <int Q, int MODE>
 __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   constexpr int NI = Q * Q, NB = 4 * Q, UBS = 4 * Q + 8;
@@ -149,36 +155,34 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   double* bufA = bufB + 16 * SB;                       // stride SA
   double* ub = bufA + 16 * SA;                         // FD_DOWN: the leaf's boundary values
   double* cst = sm + 8 * (16 * (SB + SA) + UBS);       // flux rows + couplings (8q), shared by the CTA
-  constexpr int NCST = 8 * Q + (MODE == FD_DOWN ? 513 : 0);
-  for (int e = threadIdx.x; e < NCST; e += 256) cst[e] = a.mats[5 * NI + e];
-  const double* Mx = cst + 8 * Q;                      // FD_DOWN with L u: [x][s], 16 x 16
-  const double* My = Mx + 256;                         // [y][s]
+  double* cm = cst + 8 * Q + 1;                        // constant matrices (kFdCst)
+  double* cVxi = cm;
+  double* cVx = cVxi + 16 * CSA;
+  double* cMx = cVx + 16 * CSA;
+  double* cMy = cMx + 16 * CSA;
+  double* cR = cMy + 16 * CSA;
+  double* cVyit = cR + 16 * CSA;
+  double* cVyt = cVyit + 16 * CSB;
+  for (int e = threadIdx.x; e < 8 * Q; e += 256) cst[e] = a.mats[5 * NI + e];
+  if (threadIdx.x == 0) cst[8 * Q] = MODE == FD_DOWN ? a.mats[5 * NI + 8 * Q + 512] : 0.0;  // c
+  for (int e = threadIdx.x; e < 256; e += 256) {
+    const int r = e >> 4, c = e & 15;
+    auto mat = [&](int m) -> double { return (r < Q && c < Q) ? a.mats[m * NI + r * Q + c] : 0.0; };
+    cVxi[r * CSA + c] = mat(0);
+    cVyit[r * CSB + c] = mat(1);
+    cVx[r * CSA + c] = mat(2);
+    cVyt[r * CSB + c] = mat(3);
+    cR[r * CSA + c] = mat(4);
+    if (MODE == FD_DOWN) {
+      cMx[r * CSA + c] = a.mats[5 * NI + 8 * Q + e];
+      cMy[r * CSA + c] = a.mats[5 * NI + 8 * Q + 256 + e];
+    }
+  }
+  const double* Mx = cMx;                              // FD_DOWN with L u: [x][s]
+  const double* My = cMy;                              // [y][s]
   double gmax = 0.0;
   const int gr = lane >> 2, gc = lane & 3;
   pdl_trigger();
-  // constant fragments: A operands (Vx^-1, Vx) as [m tile][k step], B operands (Vy^-T, Vy^T) as [k step][n tile]
-  auto mat = [&](int m, int r, int c) -> double { return (r < Q && c < Q) ? a.mats[m * NI + r * Q + c] : 0.0; };
-  double fVxi[2][4], fVx[2][4], fVyit[4][2], fVyt[4][2], fR[2][2][2];
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      fVxi[mi][k] = mat(0, mi * 8 + gr, k * 4 + gc);
-      fVx[mi][k] = mat(2, mi * 8 + gr, k * 4 + gc);
-    }
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int nj = 0; nj < 2; ++nj) {
-      fVyit[k][nj] = mat(1, k * 4 + gc, nj * 8 + gr);
-      fVyt[k][nj] = mat(3, k * 4 + gc, nj * 8 + gr);
-    }
-#pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-    for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) fR[mi][nj][h] = mat(4, mi * 8 + gr, nj * 8 + 2 * gc + h);
   const double* E = cst;
   const double* Bc = cst + 4 * Q;
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
@@ -254,7 +258,11 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     for (int k = 0; k < 4; ++k) {
       double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) { dmma(acc[mi][0][0], acc[mi][0][1], fVxi[mi][k], b0); dmma(acc[mi][1][0], acc[mi][1][1], fVxi[mi][k], b1); }
+      for (int mi = 0; mi < 2; ++mi) {
+        const double am = cVxi[(mi * 8 + gr) * CSA + k * 4 + gc];
+        dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
+        dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
+      }
     }
     store(bufA, SA);
     __syncwarp();
@@ -264,14 +272,18 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     for (int k = 0; k < 4; ++k) {
       double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
-      for (int nj = 0; nj < 2; ++nj) { dmma(acc[0][nj][0], acc[0][nj][1], a0, fVyit[k][nj]); dmma(acc[1][nj][0], acc[1][nj][1], a1, fVyit[k][nj]); }
+      for (int nj = 0; nj < 2; ++nj) {
+        const double bm = cVyit[(k * 4 + gc) * CSB + nj * 8 + gr];
+        dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
+        dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
+      }
     }
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) acc[mi][nj][h] *= fR[mi][nj][h];
+        for (int h = 0; h < 2; ++h) acc[mi][nj][h] *= cR[(mi * 8 + gr) * CSA + nj * 8 + 2 * gc + h];
     store(bufB, SB);
     __syncwarp();
     // T3 = Vx T2  (B operand from bufB)
@@ -280,7 +292,11 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     for (int k = 0; k < 4; ++k) {
       double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) { dmma(acc[mi][0][0], acc[mi][0][1], fVx[mi][k], b0); dmma(acc[mi][1][0], acc[mi][1][1], fVx[mi][k], b1); }
+      for (int mi = 0; mi < 2; ++mi) {
+        const double am = cVx[(mi * 8 + gr) * CSA + k * 4 + gc];
+        dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
+        dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
+      }
     }
     store(bufA, SA);
     __syncwarp();
@@ -290,7 +306,11 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     for (int k = 0; k < 4; ++k) {
       double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
-      for (int nj = 0; nj < 2; ++nj) { dmma(acc[0][nj][0], acc[0][nj][1], a0, fVyt[k][nj]); dmma(acc[1][nj][0], acc[1][nj][1], a1, fVyt[k][nj]); }
+      for (int nj = 0; nj < 2; ++nj) {
+        const double bm = cVyt[(k * 4 + gc) * CSB + nj * 8 + gr];
+        dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
+        dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
+      }
     }
     store(bufB, SB);
     __syncwarp();
@@ -322,7 +342,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
           const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) {
-            const double am = Mx[(mi * 8 + gr) * 16 + k * 4 + gc];
+            const double am = Mx[(mi * 8 + gr) * CSA + k * 4 + gc];
             dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
             dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
           }
@@ -332,13 +352,13 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
           const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
           for (int nj = 0; nj < 2; ++nj) {
-            const double bm = My[(nj * 8 + gr) * 16 + k * 4 + gc];
+            const double bm = My[(nj * 8 + gr) * CSA + k * 4 + gc];
             dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
             dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
           }
         }
         double* lo = a.lu + kk * a.ld_lu + (long long)l * NI;
-        const double c0 = Mx[512];
+        const double c0 = cst[8 * Q];
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -389,7 +409,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
 
 template <int MODE>
 static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaStream_t st) {
-  const size_t smem = ((size_t)8 * (16 * (SB + SA) + 4 * P.q + 8) + 8 * P.q + 513) * 8;
+  const size_t smem = ((size_t)8 * (16 * (SB + SA) + 4 * P.q + 8) + 8 * P.q + 1 + kFdCst) * 8;
   const unsigned warps = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 2);  // one wave
   dim3 g2(warps, (unsigned)k);
 #define HPSB_FD2(QQ)                                                                                   \
@@ -397,7 +417,7 @@ static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaS
     static bool attr = false;                                                                          \
     if (!attr) {                                                                                       \
       HPSB_CUDA(cudaFuncSetAttribute(k_leaf_fd_mma<QQ, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     64 * 1024));                                                      \
+                                     (int)smem));                                                       \
       attr = true;                                                                                     \
     }                                                                                                  \
     HPSB_CUDA(launch_pdl(k_leaf_fd_mma<QQ, MODE>, g2, dim3(256), smem, st, a));                        \
