@@ -91,6 +91,19 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
   }
 }
 
+// sum of n split partials p[s * stride] in split order, eight loads in flight
+__device__ __forceinline__ double sum_splits(const double* p, size_t stride, int n, double y) {
+  for (int s0 = 0; s0 < n; s0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = s0 + u < n ? __ldcg(p + (size_t)(s0 + u) * stride) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (s0 + u < n) y += v[u];
+  }
+  return y;
+}
+
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -156,6 +169,21 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     __syncthreads();
     if (p.trace && tid == 0) p.trace[3 * t + 1] = gtime();
+    // the epilogue's additive term (child flux / w3) is ready now: load it
+    // while the inputs are gathered and the columns streamed
+    double oadd = 0.0;
+    if (ovalid && !g.pair) {
+      const int node = node0 + oj;
+      if (g.up) {
+        const int rr = orow - g.n3;
+        if (rr >= 0) {
+          const double* Ha = g.Hc + (long long)(2 * node) * g.Hc_s;
+          oadd = rr < g.n1a ? __ldcg(Ha + oidx) : __ldcg(Ha + g.Hc_s + oidx);
+        }
+      } else if (g.W3) {
+        oadd = __ldcg(g.W3 + (long long)node * g.n3 + orow);
+      }
+    }
     // ---- stage the group's inputs for this split's columns
     for (int e = tid; e < MNB * cw; e += MT) {
       const int j = e / cw, col = e % cw;
@@ -205,10 +233,10 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
         y = 0.0;
         if (ovalid) {
           if (g.pair) {
-            for (int s = 0; s < g.Sdn; ++s) y += __ldcg(g.pdn + (size_t)s * pstride + slot);
-            for (int s = 0; s < g.Sup; ++s) y += __ldcg(g.pup + (size_t)s * pstride + slot);
+            y = sum_splits(g.pdn + slot, pstride, g.Sdn, y);
+            y = sum_splits(g.pup + slot, pstride, g.Sup, y);
           } else {
-            for (int s = 0; s < g.S; ++s) y += __ldcg(g.part + (size_t)s * pstride + slot);
+            y = sum_splits(g.part + slot, pstride, g.S, y);
           }
         }
       }
@@ -222,14 +250,10 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
           if (orow < g.n3) {
             g.W3[(long long)node * g.n3 + orow] = y;
           } else {
-            const int rr = orow - g.n3;
-            const double* Ha = g.Hc + (long long)(2 * node) * g.Hc_s;
-            const double base = rr < g.n1a ? __ldcg(Ha + oidx) : __ldcg(Ha + g.Hc_s + oidx);
-            g.Hout[(long long)node * g.n12 + rr] = base + y;
+            g.Hout[(long long)node * g.n12 + orow - g.n3] = oadd + y;
           }
         } else {
-          if (g.W3) y = y + __ldcg(g.W3 + (long long)node * g.n3 + orow);
-          g.u[oidx] = y;
+          g.u[oidx] = y + oadd;
         }
       }
     }
