@@ -181,8 +181,18 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
         for (int h = 0; h < 2; ++h) {
           const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
           double y = 0.0;
-          if (m < a.M && r < a.N)
-            for (int sp = 0; sp < a.nsplit; ++sp) y += __ldcg(a.part + ((size_t)sp * a.M + m) * a.N + r);
+          if (m < a.M && r < a.N) {
+            const double* pp = a.part + (size_t)m * a.N + r;
+            const size_t ps = (size_t)a.M * a.N;
+            for (int s0 = 0; s0 < a.nsplit; s0 += 4) {  // four loads in flight, summed in split order
+              double v[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[u] = s0 + u < a.nsplit ? __ldcg(pp + (size_t)(s0 + u) * ps) : 0.0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (s0 + u < a.nsplit) y += v[u];
+            }
+          }
           acc[i][j][h] = y;
         }
     }
