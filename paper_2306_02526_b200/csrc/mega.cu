@@ -71,7 +71,8 @@ struct MSeg {
 struct MProg {
   int nseg, ntasks;
   int head, dedicated;          // the first `head` tasks (the root's down product) run on the last
-                                // `dedicated` CTAs only, every other task on the remaining CTAs
+                                // `dedicated` CTAs first; every other task is taken by ticket
+  unsigned* ticket;             // next task after the head (reset at exit)
   unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / end, ns
   unsigned* reset; int nreset;  // counters to zero at exit (incl. the exit counter at the end)
   MSeg s[MAXSEG];
@@ -119,9 +120,19 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
   pdl_wait();
   const int G = gridDim.x, KR = p.dedicated;
   const bool ded = KR > 0 && (int)blockIdx.x >= G - KR;
-  const int tfirst = ded ? (int)blockIdx.x - (G - KR) : p.head + (int)blockIdx.x;
-  const int tstep = ded ? KR : G - KR, tend = ded ? p.head : p.ntasks;
-  for (int t = tfirst; t < tend; t += tstep) {
+  // the dedicated CTAs first take the head tasks round-robin, then every CTA
+  // takes the remaining tasks in list order from a ticket counter (each task
+  // depends only on lower-numbered ones, all taken by resident CTAs)
+  __shared__ int s_ticket;
+  int t = ded ? (int)blockIdx.x - (G - KR) : p.ntasks;
+  for (;;) {
+    if (!(ded && t < p.head)) {
+      __syncthreads();
+      if (tid == 0) s_ticket = p.head + (int)atomicAdd(p.ticket, 1u);
+      __syncthreads();
+      t = s_ticket;
+      if (t >= p.ntasks) break;
+    }
     int si = 0;
     while (t >= p.s[si].task0 + p.s[si].ntasks) ++si;
     const MSeg& g = p.s[si];
@@ -264,6 +275,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     __syncthreads();  // xs / red / sidx are reused by the next task
     if (p.trace && tid == 0) p.trace[3 * t + 2] = gtime();
+    if (ded && t < p.head) t += KR;
   }
   // the last CTA out resets the counters for the next solve
   __syncthreads();
@@ -313,7 +325,7 @@ static void mega_dims(const Level& lv, bool root, bool up, int nn, int& RB, int&
 }
 
 void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles) {
-  counters = 1;  // exit counter
+  counters = 2;  // exit counter, task ticket
   part_doubles = 0;
   for (int d = 0; d < P.depth; ++d) {
     const Level& lv = P.lv[d];
@@ -423,6 +435,7 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   }
   if (p.nseg == 0) return 0;
   p.ntasks = task;
+  p.ticket = c++;
   p.reset = cnt + 1;
   p.nreset = (int)(c - (cnt + 1));
   static int max_ctas = 0;
