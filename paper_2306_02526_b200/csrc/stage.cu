@@ -347,6 +347,111 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
   if (a.guard) guard_max(a.guard, gmax);
 }
 
+// Interface-averaged gradient only (the nonlinear g of timestep.py:192-196):
+// thread <-> one grid point of the leaf slot (interior or edge), its two line
+// rows held in registers for the whole kernel -- the normal / interior rows
+// are the full p-point derivative rows, the tangential rows at edge points
+// are the edge-local (p-2)-point rows placed at grid positions 1..p-2 (zeros
+// elsewhere, and the grid's unused corners are kept at zero) -- so every
+// point is the same two p-term sums.  Interior values are stored, edge values
+// accumulate w * value (w = 1/2 on interfaces) as in k_leaf_eval.  The next
+// leaf group is loaded into registers while the current one is computed.
+template <int P>
+__global__ void __launch_bounds__(NT) k_leaf_grad(EvalArgs a) {
+  extern __shared__ double U[];  // LPB x P x PS
+  constexpr int Q = P - 2, NI = Q * Q, NB = 4 * Q, M = NI + NB, PS = (P + 1) | 1, PP = P * PS;
+  constexpr int LANES = NT / M > 0 ? NT / M : 1;
+  constexpr int LPB = 2048 / (P * P), KI = (LPB * NI + NT - 1) / NT, KB = (LPB * NB + NT - 1) / NT;
+  const int tid = threadIdx.x, kk = blockIdx.y;
+  const double* u = a.u + kk * a.ld_u;
+  const long long ob = kk * a.ld_o;
+  const bool active = tid < LANES * M;
+  const int t = tid % M, lane0 = tid / M;
+  const bool inner = t < NI;
+  int xi, yi;
+  if (inner) { xi = t / Q + 1; yi = t % Q + 1; }
+  else edge_xy(t - NI, P, Q, xi, yi);
+  const bool vert = !inner && (xi == 0 || xi == P - 1), horz = !inner && !vert;
+  const double* mats = a.mats;
+  const double* ex1 = mats + 4 * P * P;
+  const double* ey1 = ex1 + 2 * Q * Q;
+  double rA[P], rB[P];
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const bool mid = s >= 1 && s <= Q;
+    rA[s] = horz ? (mid ? ex1[(xi - 1) * Q + s - 1] : 0.0) : mats[xi * P + s];
+    rB[s] = vert ? (mid ? ey1[(yi - 1) * Q + s - 1] : 0.0) : mats[2 * P * P + yi * P + s];
+  }
+  for (int e = tid; e < LPB * PP; e += NT) U[e] = 0.0;  // corners stay zero
+  double gmax = 0.0;
+  double pi[KI], pb[KB];
+  auto fetch = [&](int l0) {
+    const int nl = min(LPB, a.L - l0);
+#pragma unroll
+    for (int i = 0; i < KI; ++i) {
+      const int e = tid + i * NT;
+      pi[i] = e < nl * NI ? u[a.ioff + (long long)l0 * NI + e] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const int e = tid + i * NT;
+      pb[i] = e < nl * NB ? u[a.lbg[(long long)l0 * NB + e]] : 0.0;
+    }
+  };
+  const int step = gridDim.x * LPB;
+  int l0 = blockIdx.x * LPB;
+  if (l0 < a.L) fetch(l0);
+  for (; l0 < a.L; l0 += step) {
+    const int nl = min(LPB, a.L - l0);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < KI; ++i) {
+      const int e = tid + i * NT;
+      if (e < nl * NI) {
+        const int l2 = e / NI, ii = e % NI;
+        U[l2 * PP + (ii / Q + 1) * PS + (ii % Q + 1)] = pi[i];
+        gacc(gmax, pi[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const int e = tid + i * NT;
+      if (e < nl * NB) {
+        const int l2 = e / NB, j = e % NB;
+        int x, y;
+        edge_xy(j, P, Q, x, y);
+        U[l2 * PP + x * PS + y] = pb[i];
+        gacc(gmax, pb[i]);
+      }
+    }
+    __syncthreads();
+    if (l0 + step < a.L) fetch(l0 + step);
+    if (!active) continue;
+    for (int ll = lane0; ll < nl; ll += LANES) {
+      const double* G = U + ll * PP;
+      double ux = 0.0, uy = 0.0;
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        ux = fma(rA[s], G[s * PS + yi], ux);
+        uy = fma(rB[s], G[xi * PS + s], uy);
+      }
+      const int l = l0 + ll;
+      if (inner) {
+        const long long gi = ob + a.ioff + (long long)l * NI + t;
+        a.ux[gi] = ux;
+        a.uy[gi] = uy;
+      } else {
+        const int j = t - NI;
+        const long long gi = ob + a.lbg[(long long)l * NB + j];
+        const double w = a.sign[(long long)l * NB + j] ? 0.5 : 1.0;
+        atomicAdd(a.ux + gi, w * ux);
+        atomicAdd(a.uy + gi, w * uy);
+      }
+    }
+  }
+  if (a.guard) guard_max(a.guard, gmax);
+}
+
 constexpr int MAXT = 24;
 struct CombineArgs {
   int nt, k;
@@ -436,6 +541,14 @@ __global__ void k_bnd_put(int k, int nbd, const int* __restrict__ ids, const dou
   if (e >= (long long)k * nbd) return;
   int kk = (int)(e / nbd), i = (int)(e % nbd);
   u[kk * ld_u + ids[i]] = fb[kk * ld_f + i];
+}
+
+bool grad_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_GRAD");
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 unsigned stream_blocks(long long n) {
@@ -560,6 +673,18 @@ int hps_leaf_eval_range(const hps_disc* h, int leaf0, int nleaf, int k, const do
     }
     HPSB_LOP(10) HPSB_LOP(12) HPSB_LOP(16)
 #undef HPSB_LOP
+    HPSB_LAUNCH_CHECK();
+    return HPS_OK;
+  }
+  const bool grad_only = ux && uy && !lu && !lu_int && !jump;
+  if (grad_only && (D.p == 10 || D.p == 12 || D.p == 16) && grad_enabled()) {
+    a.lpb = std::max(1, 2048 / (D.p * D.p));
+    groups = (unsigned)cdiv(nleaf, a.lpb);
+    grid.x = std::min(groups, (unsigned)(kNumSMs * 8));
+    const size_t sm2 = (size_t)a.lpb * pp * 8;
+    if (D.p == 10) k_leaf_grad<10><<<grid, NT, sm2, st>>>(a);
+    if (D.p == 12) k_leaf_grad<12><<<grid, NT, sm2, st>>>(a);
+    if (D.p == 16) k_leaf_grad<16><<<grid, NT, sm2, st>>>(a);
     HPSB_LAUNCH_CHECK();
     return HPS_OK;
   }

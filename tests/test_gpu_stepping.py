@@ -248,3 +248,18 @@ def test_step_map_assembly_matches_reference(golden, key, tab, form, dt):
     assert spec.zero_count == int(z[key + "_zeros"])
     with pytest.raises(hb.UnsupportedConfigurationError):
         assemble_step_map(tree, hb.ParabolicProblem(coeffs=coeffs, g=lambda t, u, ux, uy: u), tab, dt)
+
+
+@pytest.mark.parametrize("p", [10, 12, 16])
+def test_gradient_kernel_matches_oracle(p):
+    """The register-row gradient kernel (stage.cu k_leaf_grad) against the
+    oracle's interface-averaged gradient (operators.py:303-317)."""
+    hb = _hb()
+    from oracle import hps_oracle as O
+    tree = hb.build_tree(UNIT, 4, 4, p)
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(**var_test_fields()))
+    od = O.ODisc(O.OTree(UNIT, 4, 4, p), O.OCoeffs(**var_test_fields()))
+    u = np.random.default_rng(p).standard_normal((3, tree.N))
+    ux, uy = disc.gradient(u)
+    rx, ry = od.gradient(u)
+    assert rel_l2(ux, rx) < 1e-13 and rel_l2(uy, ry) < 1e-13
