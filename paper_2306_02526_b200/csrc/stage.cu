@@ -314,8 +314,24 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
     __syncthreads();
     if (l0 + step < a.L) fetch(l0 + step);
     if (!active) continue;
-    for (int ll = lane0; ll < nl; ll += LANES) {
+    constexpr int PER = (LPB + LANES - 1) / LANES;  // leaf slots per thread and group
+#pragma unroll
+    for (int it = 0; it < PER; ++it) {
+      const int ll = lane0 + it * LANES;
+      if (ll >= nl) continue;
       const double* G = U + ll * PP;
+      const int l = l0 + ll;
+      // variable coefficients: only the fields present, loaded before the line
+      // sums so the loads are in flight while they run
+      double c11, c22, c1 = 0.0, c2 = 0.0, c0 = 0.0;
+      if (a.Lc == 1) { c11 = a.cc[0]; c22 = a.cc[1]; c1 = a.cc[2]; c2 = a.cc[3]; c0 = a.cc[4]; }
+      else {
+        const double* cv = a.coef + (long long)l * 5 * a.m;
+        c11 = __ldcs(cv + t); c22 = __ldcs(cv + a.m + t);
+        if (a.has_c1) c1 = __ldcs(cv + 2 * a.m + t);
+        if (a.has_c2) c2 = __ldcs(cv + 3 * a.m + t);
+        if (a.has_c) c0 = __ldcs(cv + 4 * a.m + t);
+      }
       double ux = 0.0, uxx = 0.0, uy = 0.0, uyy = 0.0;
 #pragma unroll
       for (int s = 0; s < P; ++s) {
@@ -328,13 +344,6 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
         const double v = G[xi * PS + s];
         uyy = fma(ryy[s], v, uyy);
         if (G1) uy = fma(ry[G1 ? s : 0], v, uy);
-      }
-      const int l = l0 + ll;
-      double c11, c22, c1, c2, c0;
-      if (a.Lc == 1) { c11 = a.cc[0]; c22 = a.cc[1]; c1 = a.cc[2]; c2 = a.cc[3]; c0 = a.cc[4]; }
-      else {
-        const double* cv = a.coef + (long long)l * 5 * a.m;
-        c11 = cv[t]; c22 = cv[a.m + t]; c1 = cv[2 * a.m + t]; c2 = cv[3 * a.m + t]; c0 = cv[4 * a.m + t];
       }
       double lop = __dmul_rn(c11, uxx);
       lop = __dadd_rn(lop, __dmul_rn(c22, uyy));
