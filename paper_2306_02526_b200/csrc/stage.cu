@@ -436,7 +436,11 @@ __global__ void __launch_bounds__(NT) k_leaf_grad(EvalArgs a) {
     __syncthreads();
     if (l0 + step < a.L) fetch(l0 + step);
     if (!active) continue;
-    for (int ll = lane0; ll < nl; ll += LANES) {
+    constexpr int PER = (LPB + LANES - 1) / LANES;
+#pragma unroll
+    for (int it = 0; it < PER; ++it) {
+      const int ll = lane0 + it * LANES;
+      if (ll >= nl) continue;
       const double* G = U + ll * PP;
       double ux = 0.0, uy = 0.0;
 #pragma unroll
