@@ -123,3 +123,33 @@ def test_many_rhs_solve_matches_oracle(layout, nparts):
     assert rel_l2(u, ref) < TOL
     single = ops.solve_with_body_load(f[3], g[3])
     assert rel_l2(single, ref[3]) < TOL
+
+
+@pytest.mark.parametrize("p", [10, 12, 16])
+def test_fused_stage_matches_solve_then_eval(p):
+    """hps_solve_stage (solve + interior L u + guard from the leaf kernel of the
+    down sweep) equals hps_solve followed by hps_leaf_eval."""
+    import torch
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.timestep import device_discretization
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 8, 8, p)
+    coeffs = hb.OperatorCoefficients(c11=1.0, c22=0.7, c1=0.3, c2=-0.2, c=0.1)
+    disc = hb.EllipticDiscretization(tree, coeffs)
+    ops = hb.HpsOperatorSet(disc, sigma=1.0, dt_gamma=1e-3, layout="shared")
+    assert ops.fuses_stage_history
+    k = 2
+    rng = np.random.default_rng(p)
+    body = torch.as_tensor(rng.standard_normal((k, tree.N)), device="cuda")
+    fb = torch.as_tensor(rng.standard_normal((k, tree.boundary_ids.size)), device="cuda")
+    u1 = torch.empty((k, tree.N), dtype=torch.float64, device="cuda")
+    u2 = torch.empty_like(u1)
+    lu1 = torch.empty((k, tree.L * tree.ni), dtype=torch.float64, device="cuda")
+    lu2 = torch.empty_like(lu1)
+    g1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.solve_stage_device(fb, body, u1, lu1, g1)
+    ops.solve_device(fb, body, u2)
+    device_discretization(disc).eval(u2, lu_int=lu2, guard=g2)
+    assert torch.equal(u1, u2)
+    assert rel_l2(lu1.cpu().numpy(), lu2.cpu().numpy()) < 1e-13
+    assert g1.item() == g2.item() and g1.item() > 0
