@@ -250,6 +250,7 @@ __global__ void __launch_bounds__(NT) k_leaf_eval(EvalArgs a) {
 template <int P, bool G1>
 __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
   extern __shared__ double U[];  // lpb x P x PS
+  pdl_trigger();
   constexpr int Q = P - 2, NI = Q * Q, PS = (P + 1) | 1, PP = P * PS, NB = 4 * Q;
   constexpr int LANES = NT / NI;  // threads sharing one interior point (over leaves)
   const int tid = threadIdx.x, lpb = a.lpb;
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
   };
   const int step = gridDim.x * LPB;
   int l0 = blockIdx.x * LPB;
+  pdl_wait();  // the vector below is produced by the previous kernel
   if (l0 < a.L) fetch(l0);
   for (; l0 < a.L; l0 += step) {
     const int nl = min(LPB, a.L - l0);
@@ -368,6 +370,7 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
 template <int P>
 __global__ void __launch_bounds__(NT) k_leaf_grad(EvalArgs a) {
   extern __shared__ double U[];  // LPB x P x PS
+  pdl_trigger();
   constexpr int Q = P - 2, NI = Q * Q, NB = 4 * Q, M = NI + NB, PS = (P + 1) | 1, PP = P * PS;
   constexpr int LANES = NT / M > 0 ? NT / M : 1;
   constexpr int LPB = 2048 / (P * P), KI = (LPB * NI + NT - 1) / NT, KB = (LPB * NB + NT - 1) / NT;
@@ -409,6 +412,7 @@ __global__ void __launch_bounds__(NT) k_leaf_grad(EvalArgs a) {
   };
   const int step = gridDim.x * LPB;
   int l0 = blockIdx.x * LPB;
+  pdl_wait();  // the vector below is produced by the previous kernel
   if (l0 < a.L) fetch(l0);
   for (; l0 < a.L; l0 += step) {
     const int nl = min(LPB, a.L - l0);
@@ -478,6 +482,8 @@ struct CombineArgs {
 };
 
 __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int kk = blockIdx.y;
   double gmax = 0.0;
   const long long stride = (long long)gridDim.x * NT;
@@ -503,6 +509,8 @@ __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
 // aligned (even offsets), n even; two DOFs per thread and iteration, all
 // term loads issued before the sums
 __global__ void __launch_bounds__(NT) k_combine2(CombineArgs a) {
+  pdl_trigger();
+  pdl_wait();
   const int kk = blockIdx.y;
   double gmax = 0.0;
   const long long n2 = a.n / 2, stride = (long long)gridDim.x * NT;
@@ -538,6 +546,8 @@ bool combine_vec_ok(const CombineArgs& a) {
 
 __global__ void __launch_bounds__(NT) k_maxabs(int k, long long n, const double* x, long long ld,
                                                 unsigned long long* guard) {
+  pdl_trigger();
+  pdl_wait();
   const int kk = blockIdx.y;
   double gmax = 0.0;
   const long long stride = (long long)gridDim.x * NT;
@@ -550,6 +560,8 @@ __global__ void __launch_bounds__(NT) k_maxabs(int k, long long n, const double*
 
 __global__ void k_bnd_put(int k, int nbd, const int* __restrict__ ids, const double* __restrict__ fb,
                           long long ld_f, double* __restrict__ u, long long ld_u) {
+  pdl_trigger();
+  pdl_wait();
   long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= (long long)k * nbd) return;
   int kk = (int)(e / nbd), i = (int)(e % nbd);
@@ -681,8 +693,8 @@ int hps_leaf_eval_range(const hps_disc* h, int leaf0, int nleaf, int k, const do
     const bool g1 = D.has_c1 || D.has_c2;
 #define HPSB_LOP(PP)                                                        \
     if (D.p == PP) {                                                        \
-      if (g1) k_leaf_lop_int<PP, true><<<grid, NT, sm2, st>>>(a);           \
-      else k_leaf_lop_int<PP, false><<<grid, NT, sm2, st>>>(a);             \
+      if (g1) HPSB_CUDA(launch_pdl(k_leaf_lop_int<PP, true>, grid, dim3(NT), sm2, st, a));  \
+      else HPSB_CUDA(launch_pdl(k_leaf_lop_int<PP, false>, grid, dim3(NT), sm2, st, a));    \
     }
     HPSB_LOP(10) HPSB_LOP(12) HPSB_LOP(16)
 #undef HPSB_LOP
@@ -695,9 +707,9 @@ int hps_leaf_eval_range(const hps_disc* h, int leaf0, int nleaf, int k, const do
     groups = (unsigned)cdiv(nleaf, a.lpb);
     grid.x = std::min(groups, (unsigned)(kNumSMs * 8));
     const size_t sm2 = (size_t)a.lpb * pp * 8;
-    if (D.p == 10) k_leaf_grad<10><<<grid, NT, sm2, st>>>(a);
-    if (D.p == 12) k_leaf_grad<12><<<grid, NT, sm2, st>>>(a);
-    if (D.p == 16) k_leaf_grad<16><<<grid, NT, sm2, st>>>(a);
+    if (D.p == 10) HPSB_CUDA(launch_pdl(k_leaf_grad<10>, grid, dim3(NT), sm2, st, a));
+    if (D.p == 12) HPSB_CUDA(launch_pdl(k_leaf_grad<12>, grid, dim3(NT), sm2, st, a));
+    if (D.p == 16) HPSB_CUDA(launch_pdl(k_leaf_grad<16>, grid, dim3(NT), sm2, st, a));
     HPSB_LAUNCH_CHECK();
     return HPS_OK;
   }
@@ -717,10 +729,10 @@ int hps_combine(int k, long long n, int nterms, const double* coefs, const doubl
   a.guard = reinterpret_cast<unsigned long long*>(guard);
   if (combine_vec_ok(a)) {
     dim3 grid(stream_blocks(n / 2), (unsigned)k);
-    k_combine2<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+    HPSB_CUDA(launch_pdl(k_combine2, grid, dim3(NT), 0, (cudaStream_t)stream, a));
   } else {
     dim3 grid(stream_blocks(n), (unsigned)k);
-    k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+    HPSB_CUDA(launch_pdl(k_combine, grid, dim3(NT), 0, (cudaStream_t)stream, a));
   }
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
@@ -736,10 +748,10 @@ int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const 
   a.guard = reinterpret_cast<unsigned long long*>(guard);
   if (combine_vec_ok(a)) {
     dim3 grid(stream_blocks(n / 2), (unsigned)k);
-    k_combine2<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+    HPSB_CUDA(launch_pdl(k_combine2, grid, dim3(NT), 0, (cudaStream_t)stream, a));
   } else {
     dim3 grid(stream_blocks(n), (unsigned)k);
-    k_combine<<<grid, NT, 0, (cudaStream_t)stream>>>(a);
+    HPSB_CUDA(launch_pdl(k_combine, grid, dim3(NT), 0, (cudaStream_t)stream, a));
   }
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
@@ -748,7 +760,8 @@ int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const 
 int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard, void* stream) {
   if (k <= 0 || n <= 0) return HPS_OK;
   dim3 grid(stream_blocks(n), (unsigned)k);
-  k_maxabs<<<grid, NT, 0, (cudaStream_t)stream>>>(k, n, x, ld, reinterpret_cast<unsigned long long*>(guard));
+  HPSB_CUDA(launch_pdl(k_maxabs, grid, dim3(NT), 0, (cudaStream_t)stream, k, n, x, ld,
+                       reinterpret_cast<unsigned long long*>(guard)));
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
 }
@@ -759,7 +772,8 @@ int hps_put_boundary(const hps_plan* pv, int k, const double* fb, long long ld_f
   const Plan& P = pv->P;
   long long n = (long long)k * P.nbd;
   if (n <= 0) return HPS_OK;
-  k_bnd_put<<<(unsigned)cdiv(n, NT), NT, 0, (cudaStream_t)stream>>>(k, P.nbd, P.boundary_ids, fb, ld_f, u, ld_u);
+  HPSB_CUDA(launch_pdl(k_bnd_put, dim3((unsigned)cdiv(n, NT)), dim3(NT), 0, (cudaStream_t)stream, k, P.nbd,
+                       (const int*)P.boundary_ids, fb, ld_f, u, ld_u));
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
 }
