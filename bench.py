@@ -10,8 +10,11 @@ ranks).  With N > 1 GPUs (torchrun) one problem is subtree-sharded over the
 ranks (level-log2(N) subtrees per GPU, an NCCL all-gather of
 the subtree-root fluxes per stage solve, ``scaling`` "strong"); the ensemble
 config shards members; ``--shard replicas`` runs one replica per GPU instead.
-``e2e`` is the same metric through the public API with the state copied in
-from pinned host memory and the result read back every step.
+``e2e`` is the same metric through the public API with host-resident
+states: every step copies its input state in from pinned host memory and its
+result back out (``TimeStepper.step_host``; the steps are independent requests
+on the same input, so one step's copies overlap its neighbours' compute on
+separate copy streams).
 ``roofline`` is for the stage solve (the ~2*depth+5 level-batched kernels of
 ``hps_solve``): algorithmic bytes per solve over
 the CUDA-event duration of the solves inside the timed region.
@@ -444,15 +447,30 @@ def main():
     uh = torch.empty((k, tree.N) if k > 1 else (tree.N,), dtype=torch.float64).pin_memory()
     uh.copy_(state.u_device.cpu())
     out = torch.empty_like(uh).pin_memory()
-    s = hb.StepperState(state.t, uh)
-    s = st.step(s)            # warm
+    t_e2e = state.t
+    if subtree:   # the sharded stepper: synchronous public step with host state
+        def e2e_step():
+            s = st.step(hb.StepperState(t_e2e, uh))
+            out.copy_(s.u_device, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            return ev
+    else:         # step_host: every step copies its input in and its result out;
+        def e2e_step():   # the copies of neighbouring (independent) steps overlap
+            return st.step_host(t_e2e, uh, out)
+    e2e_step()              # warm
+    if not subtree:
+        st.sync_host()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    last = None
     for _ in range(e2e_steps):
-        s = st.step(hb.StepperState(s.t, uh))
-        out.copy_(s.u_device, non_blocking=True)
+        last = e2e_step()
+    torch.cuda.current_stream().wait_event(last)
     e1.record()
+    if not subtree:
+        st.sync_host()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_val = tree.N * 5 * e2e_steps * copies / (e2e_ms * 1e-3)

@@ -625,6 +625,90 @@ class TimeStepper:
         u = gin.clone()
         return StepperState(t, u[0] if squeeze else u)
 
+    # -- host-resident states: copies overlapped with the neighbouring steps ---------------
+    def step_host(self, t, u_in, u_out, check_every=32):
+        """One step of the host state ``u_in`` at time ``t`` into the host
+        tensor ``u_out`` (both pinned for asynchrony), enqueued without host
+        synchronisation: the input copy runs on a copy stream, the step (one
+        CUDA-graph replay) on the current stream, the result copy on a second
+        copy stream, ordered by events -- so consecutive calls on independent
+        states overlap one call's copies with the neighbouring calls' compute.
+        Returns the event that completes the result copy.  The divergence guard
+        is checked every ``check_every`` calls and by ``sync_host()``."""
+        uin = torch.atleast_2d(u_in)
+        uout = torch.atleast_2d(u_out)
+        if not self._graph_eligible():
+            s = self.step(StepperState(t, u_in))
+            uout.copy_(torch.atleast_2d(s.u_device))
+            ev = torch.cuda.Event()
+            ev.record()
+            return ev
+        G = self._graph
+        if G is None or G["key"] != self._graph_key(uin):
+            self._run_graph(StepperState(t, uin.to(self._dev)), 1, 1)   # capture (synchronous once)
+            G = self._graph
+        io = getattr(self, "_io", None)
+        if io is None or io["shape"] != tuple(uin.shape):
+            dev = self._dev
+            io = self._io = dict(shape=tuple(uin.shape), h2d=torch.cuda.Stream(), d2h=torch.cuda.Stream(),
+                                 din=[torch.empty(uin.shape, dtype=torch.float64, device=dev) for _ in range(2)],
+                                 dout=[torch.empty(uin.shape, dtype=torch.float64, device=dev) for _ in range(2)],
+                                 in_free=[None, None], out_free=[None, None], slot=0, pending=[])
+        cs = torch.cuda.current_stream()
+        slot = io["slot"]
+        io["slot"] ^= 1
+        with torch.cuda.stream(io["h2d"]):
+            if io["in_free"][slot] is not None:
+                io["h2d"].wait_event(io["in_free"][slot])
+            io["din"][slot].copy_(uin, non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(io["h2d"])
+        cs.wait_event(ev_in)
+        gin, guards, coef = G["gin"], G["guards"], G["coef"]
+        gin.copy_(io["din"][slot])
+        free = torch.cuda.Event()
+        free.record(cs)
+        io["in_free"][slot] = free
+        vals = self._dry_coefs(t, gin, guards)
+        if len(vals) != G["ncoef"]:
+            raise HpstepError("captured step and coefficient pass disagree")
+        cslot = G["slot"]
+        G["slot"] = (cslot + 1) % len(G["pinned"])
+        if G["events"][cslot] is not None:
+            G["events"][cslot].synchronize()
+        buf = G["pinned"][cslot]
+        buf[:len(vals)] = torch.as_tensor(vals, dtype=torch.float64)
+        coef.copy_(buf, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        G["events"][cslot] = ev
+        G["graph"].replay()
+        io["pending"].append(guards.clone())
+        if io["out_free"][slot] is not None:
+            cs.wait_event(io["out_free"][slot])
+        io["dout"][slot].copy_(gin)
+        done = torch.cuda.Event()
+        done.record(cs)
+        with torch.cuda.stream(io["d2h"]):
+            io["d2h"].wait_event(done)
+            uout.copy_(io["dout"][slot], non_blocking=True)
+            ev_out = torch.cuda.Event()
+            ev_out.record(io["d2h"])
+        io["out_free"][slot] = ev_out
+        if len(io["pending"]) >= check_every:
+            self.sync_host()
+        return ev_out
+
+    def sync_host(self):
+        """Wait for every ``step_host`` call and check their divergence guards."""
+        io = getattr(self, "_io", None)
+        if io is None:
+            return
+        torch.cuda.current_stream().synchronize()
+        io["h2d"].synchronize()
+        io["d2h"].synchronize()
+        self._drain(io["pending"])
+
     def _drain(self, pending):
         if not pending:
             return

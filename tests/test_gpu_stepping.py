@@ -263,3 +263,20 @@ def test_gradient_kernel_matches_oracle(p):
     ux, uy = disc.gradient(u)
     rx, ry = od.gradient(u)
     assert rel_l2(ux, rx) < 1e-13 and rel_l2(uy, ry) < 1e-13
+
+
+def test_step_host_overlapped_copies_match_step():
+    """TimeStepper.step_host (host state in, host result out, copies on their
+    own streams) gives the same states as step()."""
+    import torch
+    hb = _hb()
+    tree, st, uex = _c1_stepper(hb, True)
+    s0 = st.initial_state()
+    u0 = torch.as_tensor(np.asarray(s0.u), dtype=torch.float64).pin_memory()
+    ref = st.step(hb.StepperState(0.0, u0.clone())).u
+    outs = [torch.empty_like(u0).pin_memory() for _ in range(3)]
+    for o in outs:
+        st.step_host(0.0, u0, o)
+    st.sync_host()
+    for o in outs:
+        assert np.array_equal(o.numpy(), ref)
