@@ -153,3 +153,16 @@ def test_fused_stage_matches_solve_then_eval(p):
     assert torch.equal(u1, u2)
     assert rel_l2(lu1.cpu().numpy(), lu2.cpu().numpy()) < 1e-13
     assert g1.item() == g2.item() and g1.item() > 0
+
+
+def test_timing_harness_rows(tmp_path):
+    """run_timing (drivers.py:160-204) on the device: one row per size with
+    the reference's columns, build and median solve times, CSV written."""
+    from paper_2306_02526_b200.timing import COLUMNS, run_timing
+    path = tmp_path / "timing.csv"
+    rows = run_timing(sizes=(2, 4), p=11, out_path=str(path))
+    assert [r["n_side"] for r in rows] == [2, 4]
+    for r in rows:
+        assert r["N"] == (r["n_side"] * 10 + 1) ** 2
+        assert r["build_seconds"] > 0 and r["per_step_solve_seconds"] > 0
+    assert path.read_text().splitlines()[0] == ",".join(COLUMNS)

@@ -153,3 +153,9 @@ def test_step_map_analysis_matches_reference(golden):
         assert np.allclose(np.sort_complex(spec.eigenvalues), np.sort_complex(z[key + "_eig"]), atol=1e-10)
     lines = spectrum_csv_lines(spec)
     assert lines[1] == "re,im,modulus" and len(lines) == 2 + spec.eigenvalues.size
+
+
+def test_loglog_slope():
+    from paper_2306_02526_b200.timing import loglog_slope
+    xs = np.array([1e3, 1e4, 1e5, 1e6])
+    assert abs(loglog_slope(xs, 3.0 * xs ** 1.1) - 1.1) < 1e-12
