@@ -149,6 +149,9 @@ constexpr int kFdCst = 5 * 16 * CSA + 2 * 16 * CSB;  // Vxi, Vx, Mx, My, 1/den |
 template <int Q, int MODE>
 __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   constexpr int NI = Q * Q, NB = 4 * Q, UBS = 4 * Q + 8;
+  // k-steps of 4 that cover the q (leaf solve) / p (stage history) columns:
+  // the zero padding beyond them is never multiplied
+  constexpr int KS = (Q + 3) / 4, KSL = (Q + 2 + 3) / 4;
   extern __shared__ double sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, kk = blockIdx.y;
   double* bufB = sm + warp * (16 * (SB + SA) + UBS);   // stride SB
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     // T1 = Vx^-1 R  (B operand from bufB)
     clear();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KS; ++k) {
       double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     // T2 = (T1 Vy^-T) .* rden  (A operand from bufA)
     clear();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KS; ++k) {
       double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) {
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     // T3 = Vx T2  (B operand from bufB)
     clear();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KS; ++k) {
       double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
@@ -303,7 +306,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     // W = T3 Vy^T  (A operand from bufA)
     clear();
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < KS; ++k) {
       double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) {
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         __syncwarp();
         clear();
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // Mx G
+        for (int k = 0; k < KSL; ++k) {  // Mx G
           const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi) {
@@ -348,7 +351,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
           }
         }
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // + G My^T
+        for (int k = 0; k < KSL; ++k) {  // + G My^T
           const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
           for (int nj = 0; nj < 2; ++nj) {
