@@ -72,7 +72,7 @@ __device__ __forceinline__ void gacc(double& g, double v) {
 // maximum already covers it (thousands of blocks would otherwise serialise
 // on one address)
 __device__ __forceinline__ void guard_max(unsigned long long* slot, double v) {
-  __shared__ unsigned long long s_w[NT / 32];
+  __shared__ unsigned long long s_w[32];  // up to 1024 threads
   // |v| as an unsigned bit pattern orders like the value; NaN sorts above inf
   unsigned long long b = __double_as_longlong(fabs(v));
   for (int off = 16; off > 0; off >>= 1) {
@@ -367,8 +367,16 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
 // point is the same two p-term sums.  Interior values are stored, edge values
 // accumulate w * value (w = 1/2 on interfaces) as in k_leaf_eval.  The next
 // leaf group is loaded into registers while the current one is computed.
+// block size: 288 threads for p = 10 (3 x 96 grid points, no idle lanes);
+// 256 otherwise (p = 12 at 288 would drop to one CTA per SM by registers)
 template <int P>
-__global__ void __launch_bounds__(NT) k_leaf_grad(EvalArgs a) {
+struct GradThreads {
+  static constexpr int value = P == 10 ? 288 : 256;
+};
+
+template <int P>
+__global__ void __launch_bounds__(GradThreads<P>::value) k_leaf_grad(EvalArgs a) {
+  constexpr int NT = GradThreads<P>::value;  // a multiple of 32 covering whole grid points
   extern __shared__ double U[];  // LPB x P x PS
   pdl_trigger();
   constexpr int Q = P - 2, NI = Q * Q, NB = 4 * Q, M = NI + NB, PS = (P + 1) | 1, PP = P * PS;
@@ -707,9 +715,9 @@ int hps_leaf_eval_range(const hps_disc* h, int leaf0, int nleaf, int k, const do
     groups = (unsigned)cdiv(nleaf, a.lpb);
     grid.x = std::min(groups, (unsigned)(kNumSMs * 8));
     const size_t sm2 = (size_t)a.lpb * pp * 8;
-    if (D.p == 10) HPSB_CUDA(launch_pdl(k_leaf_grad<10>, grid, dim3(NT), sm2, st, a));
-    if (D.p == 12) HPSB_CUDA(launch_pdl(k_leaf_grad<12>, grid, dim3(NT), sm2, st, a));
-    if (D.p == 16) HPSB_CUDA(launch_pdl(k_leaf_grad<16>, grid, dim3(NT), sm2, st, a));
+    if (D.p == 10) HPSB_CUDA(launch_pdl(k_leaf_grad<10>, grid, dim3(GradThreads<10>::value), sm2, st, a));
+    if (D.p == 12) HPSB_CUDA(launch_pdl(k_leaf_grad<12>, grid, dim3(GradThreads<12>::value), sm2, st, a));
+    if (D.p == 16) HPSB_CUDA(launch_pdl(k_leaf_grad<16>, grid, dim3(GradThreads<16>::value), sm2, st, a));
     HPSB_LAUNCH_CHECK();
     return HPS_OK;
   }
