@@ -367,15 +367,15 @@ __global__ void __launch_bounds__(NT) k_leaf_lop_int(EvalArgs a) {
 // point is the same two p-term sums.  Interior values are stored, edge values
 // accumulate w * value (w = 1/2 on interfaces) as in k_leaf_eval.  The next
 // leaf group is loaded into registers while the current one is computed.
-// block size: 288 threads for p = 10 (3 x 96 grid points, no idle lanes);
-// 256 otherwise (p = 12 at 288 would drop to one CTA per SM by registers)
+// block size: 288 threads for p = 10 / 12 (3 x 96 / 2 x 140 grid points, no
+// idle lanes), 256 for p = 16 (252 points); two CTAs per SM
 template <int P>
 struct GradThreads {
-  static constexpr int value = P == 10 ? 288 : 256;
+  static constexpr int value = P == 16 ? 256 : 288;
 };
 
 template <int P>
-__global__ void __launch_bounds__(GradThreads<P>::value) k_leaf_grad(EvalArgs a) {
+__global__ void __launch_bounds__(GradThreads<P>::value, 2) k_leaf_grad(EvalArgs a) {
   constexpr int NT = GradThreads<P>::value;  // a multiple of 32 covering whole grid points
   extern __shared__ double U[];  // LPB x P x PS
   pdl_trigger();
