@@ -152,3 +152,14 @@ def test_sharded_stepper_two_gloo_ranks_match_stepper(kind):
     mp.spawn(_two_rank_worker, args=(2, _free_port(), kind, out), nprocs=2, join=True)
     for r in range(2):
         assert rel_l2(np.array(out[r]), ref) < 1e-12
+
+
+def test_sharded_backward_euler_matches_stepper():
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.sharding import ShardedTimeStepper
+    tree, prob = _heat(hb, 8, 12)
+    ref = hb.TimeStepper(tree, prob, "BE", dt=1e-2)
+    r = ref.run(ref.initial_state(), 4)
+    sh = ShardedTimeStepper(tree, prob, "BE", dt=1e-2, nparts=4)
+    s = sh.run(sh.initial_state(), 4)
+    assert rel_l2(s.u, r.u) < 1e-12
