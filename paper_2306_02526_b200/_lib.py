@@ -13,7 +13,8 @@ import numpy as np
 from .errors import HpstepError, SingularMatrixError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libhpstep_b200.so")
+# HPSB_LIB: an alternative build of the same library (A/B timing of two builds)
+LIB_PATH = os.environ.get("HPSB_LIB") or os.path.join(_HERE, "lib", "libhpstep_b200.so")
 
 HPS_OK = 0
 HPS_PHASE_UP, HPS_PHASE_TOP, HPS_PHASE_DOWN, HPS_PHASE_ALL = 1, 2, 4, 7

@@ -220,10 +220,11 @@ int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld
                  long long ld_u, double* uint, long long ld_uint, double* lu, long long ld_lu, double* guard,
                  cudaStream_t st);
 
-// persistent dataflow kernel for wide shared-layout levels (mega.cu): up
+// persistent dataflow kernel for the wide levels (mega.cu): up
 // levels [u0, u1) deepest first, then down levels [d0, d1) root first, over
 // the parts' nodes on levels >= lstar; returns 1 when not eligible
 bool mega_enabled();
+int mega_depth(const Ops& ops);  // levels [0, mega_depth) are eligible
 void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles);
 int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int d1, int part0, int part1,
                 const double* Hleaf, long long hs, const double* jump, double inv_dt, bool has_w3, double* u,

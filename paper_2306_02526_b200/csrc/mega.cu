@@ -58,6 +58,7 @@ struct MSeg {
   const unsigned* wchild; int wchild_t;   // up: children's counters (level d+1), target
   const unsigned* wpar; int wpar_t;       // down: parents' counters (level d-1)
   const unsigned* wup; int wup_t;         // down: own nodes' up counters
+  int Rc, Rp, Ru;              // pn: rows per node of the waited-on segments (targets vary per node)
   double* part; unsigned* sem; // split partials [S][NG*NB][R], semaphores [NG*RB]
   // root pair: the root's down product S u_bnd needs only the Dirichlet data,
   // so its tasks run at the head of the list, concurrently with the up sweep;
@@ -105,12 +106,20 @@ __device__ __forceinline__ double sum_splits(const double* p, size_t stride, int
   return y;
 }
 
+// pn: number of 64-row blocks of a row space of R rows per node that touch node n
+__device__ __forceinline__ unsigned blocks_of(int n, int R) {
+  return (unsigned)(((n + 1) * R - 1) / MRB - (n * R) / MRB + 1);
+}
+
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 
+// PN: per-node operators -- a task's 64 rows tile the level's row space
+// (node * R + r) and may span up to MNB nodes; NG = 1
+template <bool PN>
 __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
   __shared__ double xs[MNB][MXS];              // the task's inputs
   __shared__ double red[MGRP][MNB][MRB];       // column-group partial sums
@@ -140,7 +149,18 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     const int split = local % g.S;
     local /= g.S;
     const int rb = local % g.RB, ng = local / g.RB;
-    const int node0 = g.n0 + ng * MNB, nv = min(MNB, g.n0 + g.nn - node0);
+    // rows of the task: shared -> rows of the one-node operator for MNB nodes;
+    // pn -> 64 rows of the level's row space, nodes [node0, node0 + nv)
+    const int nrows = PN ? g.nn * g.R : g.R;
+    int node0, nv;
+    if (PN) {
+      const int r0 = rb * MRB, r1 = min(r0 + MRB, nrows) - 1;
+      node0 = g.n0 + r0 / g.R;
+      nv = r1 / g.R - r0 / g.R + 1;
+    } else {
+      node0 = g.n0 + ng * MNB;
+      nv = min(MNB, g.n0 + g.nn - node0);
+    }
     if (p.trace && tid == 0) p.trace[3 * t] = gtime();
     // ---- nothing below depends on the inputs: the operator's first batch,
     // the gather indices and this thread's epilogue index are in flight while
@@ -148,9 +168,10 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     const int c0 = split * g.KC, cw = min(g.KC, g.K - c0);
     const int cg = (cw + MGRP - 1) / MGRP, a0 = min(cw, grp * cg), a1 = min(cw, a0 + cg);
     const int row = rb * MRB + 2 * q;  // rows row, row + 1 (R and TR are even: both valid or both padding)
-    const bool rows_ok = row < g.R;
+    const bool rows_ok = row < nrows;
     const int cs = g.TR / 2;           // column stride in double2
-    const int rowc = min(row, g.R - 2);
+    const int rowc = min(row, nrows - 2);
+    const int jn = PN ? g.n0 + rowc / g.R - node0 : 0;  // pn: the node of both rows (R even)
     const double2* M =
         reinterpret_cast<const double2*>(g.op + (size_t)(rowc / g.TR) * g.K * g.TR + rowc % g.TR) + (size_t)c0 * cs;
     double2 A[MU];
@@ -160,8 +181,19 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     } else {
       for (int i = tid; i < nv * cw; i += MT) sidx[i / cw][i % cw] = g.gidx[(long long)(node0 + i / cw) * g.n12 + c0 + i % cw];
     }
-    const int oj = tid / MRB, orow = rb * MRB + tid % MRB;  // MT = MNB * MRB: one output per thread
-    const bool ovalid = oj < nv && orow < g.R;
+    // one output per thread (shared: MT = MNB * MRB); pn: the block's 64 rows
+    int oj, orow;
+    bool ovalid;
+    if (PN) {
+      const int gr = min(rb * MRB + tid, nrows - 1);
+      oj = g.n0 + gr / g.R - node0;
+      orow = gr % g.R;
+      ovalid = tid < MRB && rb * MRB + tid < nrows;
+    } else {
+      oj = tid / MRB;
+      orow = rb * MRB + tid % MRB;
+      ovalid = oj < nv && orow < g.R;
+    }
     int oidx = 0;  // epilogue index: up -> child flux position (flux rows), down -> global DOF
     if (ovalid) {
       if (g.up) {
@@ -173,10 +205,19 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     // ---- dependencies
     if (g.up) {
-      if (g.wchild && tid < 2 * nv) wait_count(g.wchild + 2 * node0 + tid, g.wchild_t);
+      if (g.wchild && tid < 2 * nv) {
+        const int ch = 2 * node0 + tid;
+        wait_count(g.wchild + ch, PN ? blocks_of(ch, g.Rc) : g.wchild_t);
+      }
     } else {
-      if (g.wpar && tid < nv) wait_count(g.wpar + (node0 + tid) / 2, g.wpar_t);
-      if (g.wup && tid >= 32 && tid < 32 + nv) wait_count(g.wup + node0 + tid - 32, g.wup_t);
+      if (g.wpar && tid < nv) {
+        const int pa = (node0 + tid) / 2;
+        wait_count(g.wpar + pa, PN ? blocks_of(pa, g.Rp) : g.wpar_t);
+      }
+      if (g.wup && tid >= 32 && tid < 32 + nv) {
+        const int nd = node0 + tid - 32;
+        wait_count(g.wup + nd, PN ? blocks_of(nd, g.Ru) : g.wup_t);
+      }
     }
     __syncthreads();
     if (p.trace && tid == 0) p.trace[3 * t + 1] = gtime();
@@ -213,25 +254,32 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     __syncthreads();
     // ---- stream: group grp walks columns [a0, a1) of the split for rows 2q, 2q+1 of the block
-    double acc0[MNB], acc1[MNB];
+    if (PN) {
+      double acc0[1] = {0.0}, acc1[1] = {0.0};
+      if (rows_ok) stream_cols<1, MU>(A, M, cs, a0, a1, &xs[0][0], jn * MXS, jn * MXS, MXS, acc0, acc1);
+      red[grp][0][2 * q] = acc0[0];
+      red[grp][0][2 * q + 1] = acc1[0];
+    } else {
+      double acc0[MNB], acc1[MNB];
 #pragma unroll
-    for (int j = 0; j < MNB; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
-    if (rows_ok) stream_cols<MNB, MU>(A, M, cs, a0, a1, &xs[0][0], 0, 0, MXS, acc0, acc1);
+      for (int j = 0; j < MNB; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
+      if (rows_ok) stream_cols<MNB, MU>(A, M, cs, a0, a1, &xs[0][0], 0, 0, MXS, acc0, acc1);
 #pragma unroll
-    for (int j = 0; j < MNB; ++j) {
-      red[grp][j][2 * q] = acc0[j];
-      red[grp][j][2 * q + 1] = acc1[j];
+      for (int j = 0; j < MNB; ++j) {
+        red[grp][j][2 * q] = acc0[j];
+        red[grp][j][2 * q + 1] = acc1[j];
+      }
     }
     __syncthreads();
     // ---- group sums (in group order), then split partials or the epilogue
-    const int r = tid % MRB;
+    const int r = tid % MRB, rj = PN ? 0 : oj;
     double y = 0.0;
 #pragma unroll
-    for (int gg = 0; gg < MGRP; ++gg) y += red[gg][oj][r];
+    for (int gg = 0; gg < MGRP; ++gg) y += red[gg][rj][r];
     bool emit_now = true;
     if (g.S > 1 || g.pair) {
-      const size_t slot = (size_t)(ng * MNB + oj) * g.R + orow;
-      const size_t pstride = (size_t)g.NG * MNB * g.R;
+      const size_t slot = PN ? (size_t)rb * MRB + r : (size_t)(ng * MNB + oj) * g.R + orow;
+      const size_t pstride = PN ? (size_t)g.RB * MRB : (size_t)g.NG * MNB * g.R;
       if (ovalid) g.part[(size_t)split * pstride + slot] = y;
       __threadfence();
       __syncthreads();
@@ -310,15 +358,38 @@ bool mega_enabled() {
   return on;
 }
 
+// Levels [0, mega_depth) may run in the persistent launch.  Shared operators:
+// all.  Per-node operators: the persistent kernel streams ~8% below the
+// per-level panel kernel but saves a level's drain / fill (~5 us), which pays
+// only while a level's operators are small; levels from the first one whose
+// up or down operators exceed HPSB_PN_MEGA_MB (default 256 MB) down to the
+// leaves run as per-level launches.
+int mega_depth(const Ops& ops) {
+  const Plan& P = *ops.plan;
+  if (ops.shared_levels) return P.depth;
+  static const double cap = [] {
+    const char* e = getenv("HPSB_PN_MEGA_MB");
+    return (e ? atof(e) : 256.0) * 1048576.0;
+  }();
+  int d = 0;
+  for (; d < P.depth; ++d) {
+    const Level& lv = P.lv[d];
+    const double up = (double)lv.c * (lv.n3 + (d ? lv.n12 : 0)) * lv.n3 * 8.0;
+    const double dn = (double)lv.c * lv.n3 * lv.n12 * 8.0;
+    if (std::max(up, dn) > cap) break;
+  }
+  return d;
+}
+
 // Counter / partial space of the workspace's mega region for one plan: every
 // wide level's nodes twice (up, down), semaphores and split partials of every
 // possible segment.  Sized generously from the plan alone.
 static void mega_dims(const Level& lv, bool root, bool up, int nn, int& RB, int& NG, int& S, int& KC, int& R,
-                      int& K) {
+                      int& K, bool pn = false) {
   R = up ? lv.n3 + (root ? 0 : lv.n12) : lv.n3;
   K = up ? lv.n3 : lv.n12;
-  RB = (R + MRB - 1) / MRB;
-  NG = (nn + MNB - 1) / MNB;
+  RB = pn ? (int)(((long long)nn * R + MRB - 1) / MRB) : (R + MRB - 1) / MRB;
+  NG = pn ? 1 : (nn + MNB - 1) / MNB;
   S = std::max(1, (K + MKC - 1) / MKC);
   KC = (K + S - 1) / S;
   S = (K + KC - 1) / KC;
@@ -333,8 +404,12 @@ void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles) {
     for (int up = 0; up < 2; ++up) {
       int RB, NG, S, KC, R, K;
       mega_dims(lv, d == 0, up, lv.c, RB, NG, S, KC, R, K);
-      counters += (size_t)RB * NG;
-      if (S > 1 || d == 0) part_doubles += (size_t)S * NG * MNB * R;  // the root pair always uses partials
+      size_t sems = (size_t)RB * NG, parts = (size_t)S * NG * MNB * R;
+      mega_dims(lv, d == 0, up, lv.c, RB, NG, S, KC, R, K, true);  // per-node row blocks
+      sems = std::max(sems, (size_t)RB);
+      parts = std::max(parts, (size_t)S * RB * MRB);
+      counters += sems;
+      if (S > 1 || d == 0) part_doubles += parts;  // the root pair always uses partials
     }
   }
 }
@@ -346,7 +421,8 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
                 const double* Hleaf, long long hs, const double* jump, double inv_dt, bool has_w3, double* u,
                 cudaStream_t st) {
   const Plan& P = *ops.plan;
-  if (!mega_enabled() || !ops.shared_levels || !ws.mega_cnt) return 1;
+  if (!mega_enabled() || !ws.mega_cnt) return 1;
+  const bool pnm = !ops.shared_levels;  // per-node operators
   MProg p{};
   // counter carve: [exit][per level: up nodes, down nodes][sems...]
   unsigned* cnt = ws.mega_cnt;
@@ -361,14 +437,19 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     const Level& lv = P.lv[d];
     const LevelOps& lo = ops.lo[d];
     const Panel& pn = up ? lo.Up : lo.S;
-    if (!pn.base || pn.c != 1 || pn.TS != pn.TR || (pn.TR & 1)) return false;
+    if (!pn.base || pn.c != (pnm ? lv.c : 1) || pn.parts != 1 || pn.TS != pn.TR || (pn.TR & 1) ||
+        (pnm && pn.TR % MRB))
+      return false;
     MSeg& g = p.s[p.nseg];
     int n0 = 0, n1 = lv.c;  // levels >= lstar: the parts' nodes
     if (d >= P.lstar) { n0 = part0 * (lv.c / P.nparts); n1 = part1 * (lv.c / P.nparts); }
+    if (pnm && n0 != 0) return false;  // per-node panels of a part range: per-level launches
     g.up = up;
     g.n0 = n0; g.nn = n1 - n0;
-    mega_dims(lv, d == 0, up, g.nn, g.RB, g.NG, g.S, g.KC, g.R, g.K);
+    mega_dims(lv, d == 0, up, g.nn, g.RB, g.NG, g.S, g.KC, g.R, g.K, pnm);
     if (g.R != pn.R || g.K != pn.C || g.KC > MKC) return false;
+    // pn: both rows of a thread in one node (R even), a row block spans <= MNB nodes
+    if (pnm && ((g.R & 1) || (MRB - 2) / g.R + 2 > MNB)) return false;
     g.op = pn.base; g.TR = pn.TR;
     g.task0 = task; g.ntasks = g.RB * g.NG * g.S;
     task += g.ntasks;
@@ -382,7 +463,8 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     g.u = u;
     g.done = up ? dup[d] : ddn[d];
     g.sem = c; c += (size_t)g.RB * g.NG;
-    if (g.S > 1) { g.part = part; part += (size_t)g.S * g.NG * MNB * g.R; }
+    const size_t seg_part = pnm ? (size_t)g.S * g.RB * MRB : (size_t)g.S * g.NG * MNB * g.R;
+    if (g.S > 1) { g.part = part; part += seg_part; }
     // dependencies inside this launch
     if (up) {
       const bool child_here = d + 1 < u1;
@@ -390,17 +472,20 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
       int RBc = 0, NGc, Sc, KCc, Rc, Kc;
       if (child_here) mega_dims(P.lv[d + 1], false, true, 1, RBc, NGc, Sc, KCc, Rc, Kc);
       g.wchild_t = RBc;
+      g.Rc = child_here ? Rc : 0;
     } else {
       const bool par_here = d - 1 >= d0 && d > 0;
       g.wpar = par_here ? ddn[d - 1] : nullptr;
-      int RBp = 0, x1, x2, x3, x4, x5;
+      int RBp = 0, x1, x2, x3, x4 = 0, x5;
       if (par_here) mega_dims(P.lv[d - 1], d - 1 == 0, false, 1, RBp, x1, x2, x3, x4, x5);
       g.wpar_t = RBp;
+      g.Rp = par_here ? x4 : 0;
       const bool up_here = d >= u0 && d < u1;
       g.wup = up_here && has_w3 ? dup[d] : nullptr;
       int RBu = 0;
       if (up_here) mega_dims(lv, d == 0, true, 1, RBu, x1, x2, x3, x4, x5);
       g.wup_t = RBu;
+      g.Ru = up_here ? x4 : 0;
     }
     ++p.nseg;
     return true;
@@ -428,7 +513,10 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
       g->wup = nullptr;
       g->done = dn.done;             // level 1's down tasks wait on the root's u3
       g->sem = dn.sem;               // one semaphore per row block for both
-      if (!g->part) { g->part = part; part += (size_t)g->S * g->NG * MNB * g->R; }
+      if (!g->part) {
+        g->part = part;
+        part += pnm ? (size_t)g->S * g->RB * MRB : (size_t)g->S * g->NG * MNB * g->R;
+      }
     }
     dn.pdn = upp->pdn = dn.part;
     dn.pup = upp->pup = upp->part;
@@ -438,10 +526,11 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   p.ticket = c++;
   p.reset = cnt + 1;
   p.nreset = (int)(c - (cnt + 1));
-  static int max_ctas = 0;
+  static int max_ctas_pn[2] = {0, 0};
+  int& max_ctas = max_ctas_pn[pnm];
   if (!max_ctas) {
     int per_sm = 0;
-    HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_mega, MT, 0));
+    HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pnm ? k_mega<true> : k_mega<false>, MT, 0));
     int dev = 0, sms = kNumSMs;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     max_ctas = std::max(1, per_sm) * sms;
@@ -459,7 +548,10 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     HPSB_CUDA(cudaMemsetAsync(dtrace, 0, (size_t)3 * p.ntasks * 8, st));
     p.trace = dtrace;
   }
-  HPSB_CUDA(launch_pdl(k_mega, dim3(grid), dim3(MT), 0, st, p, exit_count));
+  if (pnm)
+    HPSB_CUDA(launch_pdl(k_mega<true>, dim3(grid), dim3(MT), 0, st, p, exit_count));
+  else
+    HPSB_CUDA(launch_pdl(k_mega<false>, dim3(grid), dim3(MT), 0, st, p, exit_count));
   HPSB_LAUNCH_CHECK();
   if (tr) {
     std::vector<unsigned long long> h((size_t)3 * p.ntasks);

@@ -272,23 +272,36 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   // (mega.cu); otherwise one launch per level and pass.
   const int uA = (phases & SOLVE_TOP) ? 0 : ls, uB = up ? ((phases & SOLVE_UP) ? dW : ls) : uA;
   const int dA = (phases & SOLVE_TOP) ? 0 : ls, dB = (phases & SOLVE_DOWN) ? dW : ls;
-  int rc_mega = 1;
-  if (k == 1 && (uB > uA || dB > dA))
-    rc_mega = mega_levels(ops, ws, uA, std::max(uA, uB), dA, std::max(dA, dB), part0, part1, Hleaf, hs, jump,
-                          inv_dt, up, u, st);
-  if (rc_mega < 0) return rc_mega;
-  if (rc_mega == 1) {
-    for (int d = uB - 1; d >= uA; --d) {
+  // levels >= dm (large per-node operators) always run per level
+  const int dm = k == 1 && mega_enabled() ? mega_depth(ops) : 0;
+  auto ups = [&](int d1, int d0) -> int {  // per-level up merges d1 - 1 .. d0
+    for (int d = d1 - 1; d >= d0; --d) {
       int n0 = 0, n1 = P.lv[d].c;
       if (d >= ls) range(d, n0, n1);
       if (int rc = level_up(ops, ws, d, n0, n1, k, Hleaf, sh, hs, jump, ld_jump, inv_dt, st)) return rc;
     }
-    for (int d = dA; d < dB; ++d) {
+    return 0;
+  };
+  auto downs = [&](int d0, int d1) -> int {
+    for (int d = d0; d < d1; ++d) {
       int n0 = 0, n1 = P.lv[d].c;
       if (d >= ls) range(d, n0, n1);
       if (int rc = level_down(ops, ws, d, n0, n1, k, up, u, ld_u, st)) return rc;
     }
+    return 0;
+  };
+  if (int rc = ups(uB, std::max(uA, dm))) return rc;
+  const int mu1 = std::min(uB, dm), md1 = std::min(dB, dm);
+  int rc_mega = 1;
+  if (mu1 > uA || md1 > dA)
+    rc_mega = mega_levels(ops, ws, uA, std::max(uA, mu1), dA, std::max(dA, md1), part0, part1, Hleaf, hs, jump,
+                          inv_dt, up, u, st);
+  if (rc_mega < 0) return rc_mega;
+  if (rc_mega == 1) {
+    if (int rc = ups(std::max(uA, mu1), uA)) return rc;
+    if (int rc = downs(dA, std::max(dA, md1))) return rc;
   }
+  if (int rc = downs(std::max(dA, dm), dB)) return rc;
 
   if (phases & SOLVE_DOWN) {
     if (fused) {
