@@ -40,6 +40,7 @@ constexpr int MNB = 4;         // nodes per group
 constexpr int MKC = 256;       // max operator columns per task (32 per thread)
 constexpr int MAXSEG = 24;
 constexpr int MXS = MKC + 1;
+constexpr int MTS = 6;         // trace stamps per task
 constexpr int MU = 4;          // 16-byte operator loads per batch (two batches in flight)
 
 struct MSeg {
@@ -74,7 +75,8 @@ struct MProg {
   int head, dedicated;          // the first `head` tasks (the root's down product) run on the last
                                 // `dedicated` CTAs first; every other task is taken by ticket
   unsigned* ticket;             // next task after the head (reset at exit)
-  unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / end, ns
+  unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / staged /
+                                // streamed / emitted / end, ns (MTS stamps)
   unsigned* reset; int nreset;  // counters to zero at exit (incl. the exit counter at the end)
   MSeg s[MAXSEG];
 };
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       node0 = g.n0 + ng * MNB;
       nv = min(MNB, g.n0 + g.nn - node0);
     }
-    if (p.trace && tid == 0) p.trace[3 * t] = gtime();
+    if (p.trace && tid == 0) p.trace[MTS * t] = gtime();
     // ---- nothing below depends on the inputs: the operator's first batch,
     // the gather indices and this thread's epilogue index are in flight while
     // the task waits for its inputs
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       }
     }
     __syncthreads();
-    if (p.trace && tid == 0) p.trace[3 * t + 1] = gtime();
+    if (p.trace && tid == 0) p.trace[MTS * t + 1] = gtime();
     // the epilogue's additive term (child flux / w3) is ready now: load it
     // while the inputs are gathered and the columns streamed
     double oadd = 0.0;
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       xs[j][col] = v;
     }
     __syncthreads();
+    if (p.trace && tid == 0) p.trace[MTS * t + 2] = gtime();
     // ---- stream: group grp walks columns [a0, a1) of the split for rows 2q, 2q+1 of the block
     if (PN) {
       double acc0[1] = {0.0}, acc1[1] = {0.0};
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       }
     }
     __syncthreads();
+    if (p.trace && tid == 0) p.trace[MTS * t + 3] = gtime();
     // ---- group sums (in group order), then split partials or the epilogue
     const int r = tid % MRB, rj = PN ? 0 : oj;
     double y = 0.0;
@@ -320,9 +324,10 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       __threadfence();
       __syncthreads();
       if (tid < nv) atomicAdd(g.done + node0 + tid, 1u);
+      if (p.trace && tid == 0) p.trace[MTS * t + 4] = gtime();
     }
     __syncthreads();  // xs / red / sidx are reused by the next task
-    if (p.trace && tid == 0) p.trace[3 * t + 2] = gtime();
+    if (p.trace && tid == 0) p.trace[MTS * t + 5] = gtime();
     if (ded && t < p.head) t += KR;
   }
   // the last CTA out resets the counters for the next solve
@@ -544,8 +549,8 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   const char* tr = getenv("HPSB_MEGA_TRACE");  // debug: per-task timeline appended to this file
   unsigned long long* dtrace = nullptr;
   if (tr) {
-    HPSB_CUDA(cudaMalloc(&dtrace, (size_t)3 * p.ntasks * 8));
-    HPSB_CUDA(cudaMemsetAsync(dtrace, 0, (size_t)3 * p.ntasks * 8, st));
+    HPSB_CUDA(cudaMalloc(&dtrace, (size_t)MTS * p.ntasks * 8));
+    HPSB_CUDA(cudaMemsetAsync(dtrace, 0, (size_t)MTS * p.ntasks * 8, st));
     p.trace = dtrace;
   }
   if (pnm)
@@ -554,7 +559,7 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     HPSB_CUDA(launch_pdl(k_mega<false>, dim3(grid), dim3(MT), 0, st, p, exit_count));
   HPSB_LAUNCH_CHECK();
   if (tr) {
-    std::vector<unsigned long long> h((size_t)3 * p.ntasks);
+    std::vector<unsigned long long> h((size_t)MTS * p.ntasks);
     HPSB_CUDA(cudaStreamSynchronize(st));
     HPSB_CUDA(cudaMemcpy(h.data(), dtrace, h.size() * 8, cudaMemcpyDeviceToHost));
     cudaFree(dtrace);
@@ -565,7 +570,11 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
         fprintf(f, "seg %d up=%d nodes=%d R=%d K=%d RB=%d NG=%d S=%d tasks=%d:%d\n", i, g.up, g.nn, g.R, g.K, g.RB,
                 g.NG, g.S, g.task0, g.ntasks);
       }
-      for (int t = 0; t < p.ntasks; ++t) fprintf(f, "%d %llu %llu %llu\n", t, h[3 * t], h[3 * t + 1], h[3 * t + 2]);
+      for (int t = 0; t < p.ntasks; ++t) {
+        fprintf(f, "%d", t);
+        for (int i = 0; i < MTS; ++i) fprintf(f, " %llu", h[(size_t)MTS * t + i]);
+        fprintf(f, "\n");
+      }
       fclose(f);
     }
   }

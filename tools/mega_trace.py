@@ -1,7 +1,8 @@
-"""Summarise an HPSB_MEGA_TRACE file: per segment first start / last end /
-mean task time / mean wait, relative to the launch's first task start (us)."""
+"""Summarise an HPSB_MEGA_TRACE file: per segment first start / last end and
+the mean task phases (us): wait for inputs, stage (gather), stream (columns),
+finish (group sums, split partials, epilogue; emitting tasks only), relative
+to the launch's first task start."""
 import sys
-from collections import defaultdict
 
 
 def main(path):
@@ -21,17 +22,21 @@ def main(path):
             i += 1
         rows = []
         while i < len(lines) and lines[i] and lines[i][0].isdigit():
-            t, s, w, e = map(int, lines[i].split())
-            rows.append((t, s, w, e))
+            rows.append(list(map(int, lines[i].split())))
             i += 1
         t0 = min(r[1] for r in rows if r[1])
         for desc, a, b in segs:
             rs = [r for r in rows if a <= r[0] < a + b]
             st = min(r[1] for r in rs) - t0
-            en = max(r[3] for r in rs) - t0
-            dur = sum(r[3] - r[1] for r in rs) / len(rs)
-            wt = sum(r[2] - r[1] for r in rs) / len(rs)
-            print(f"{desc:70s} start {st / 1e3:7.1f} end {en / 1e3:7.1f} task {dur / 1e3:6.2f} wait {wt / 1e3:6.2f} us")
+            en = max(r[-1] for r in rs) - t0
+            n = len(rs)
+            mean = lambda j, k, sel=rs: sum(r[k] - r[j] for r in sel) / max(1, len(sel)) / 1e3
+            em = [r for r in rs if len(r) > 6 and r[5]]
+            if len(rs[0]) > 6:
+                print(f"{desc[:60]:60s} {st / 1e3:6.1f}-{en / 1e3:6.1f} wait {mean(1, 2):5.2f} stage {mean(2, 3):5.2f}"
+                      f" stream {mean(3, 4):5.2f} finish {mean(4, 5, em):5.2f} (emit {len(em)}/{n}) us")
+            else:
+                print(f"{desc[:60]:60s} {st / 1e3:6.1f}-{en / 1e3:6.1f} task {mean(1, 3):6.2f} wait {mean(1, 2):6.2f} us")
 
 
 if __name__ == "__main__":
