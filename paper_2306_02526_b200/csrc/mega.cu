@@ -285,14 +285,19 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       const size_t slot = PN ? (size_t)rb * MRB + r : (size_t)(ng * MNB + oj) * g.R + orow;
       const size_t pstride = PN ? (size_t)g.RB * MRB : (size_t)g.NG * MNB * g.R;
       if (ovalid) g.part[(size_t)split * pstride + slot] = y;
-      __threadfence();
+      // barrier + one thread's fence + atomic publishes the CTA's partials
+      // (the cooperative-groups grid barrier pattern); the last arriver's
+      // fence after the atomic orders the CTA's partial reads after it
       __syncthreads();
       const unsigned total = g.pair ? (unsigned)(g.Sdn + g.Sup) : (unsigned)g.S;
-      if (tid == 0) s_last = atomicAdd(g.sem + ng * g.RB + rb, 1u) == total - 1;
+      if (tid == 0) {
+        __threadfence();
+        s_last = atomicAdd(g.sem + ng * g.RB + rb, 1u) == total - 1;
+        if (s_last) __threadfence();
+      }
       __syncthreads();
       emit_now = s_last;
       if (emit_now) {
-        __threadfence();
         y = 0.0;
         if (ovalid) {
           if (g.pair) {
@@ -321,9 +326,11 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       }
     }
     if (emit_now) {
-      __threadfence();
       __syncthreads();
-      if (tid < nv) atomicAdd(g.done + node0 + tid, 1u);
+      if (tid < 32) {
+        __threadfence();
+        if (tid < nv) atomicAdd(g.done + node0 + tid, 1u);
+      }
       if (p.trace && tid == 0) p.trace[MTS * t + 4] = gtime();
     }
     __syncthreads();  // xs / red / sidx are reused by the next task
