@@ -185,15 +185,15 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
       double2 v = make_double2(acc0[kk], acc1[kk]);
       *reinterpret_cast<double2*>(part + ((long long)kk * sp.nsplit + split) * Pp + pv) = v;
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();  // barrier + one thread's fence + atomic (see mega.cu)
     if (tid == 0) {
+      __threadfence();
       unsigned old = atomicAdd(a.cnt + cidx, 1u);
       s_last = (old == (unsigned)sp.nsplit - 1);
+      if (s_last) __threadfence();
     }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) {
       double s0 = 0.0, s1 = 0.0;
