@@ -180,6 +180,8 @@ int hps_plan_create(const hps_plan_desc* d, hps_plan** out) {
     return HPS_ERR_ARG;
   }
   P.dF = std::max(fuse_level(P), P.lstar);
+  if (const char* e = getenv("HPSB_FUSE_LEVEL"))  // A/B: first fused level (depth = none)
+    P.dF = std::min(P.depth, std::max(P.lstar, atoi(e)));
   if (!rc && P.dF < P.depth) {
     std::vector<int> s0, s1;
     std::vector<long long> o0, o1;

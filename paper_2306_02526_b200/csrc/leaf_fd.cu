@@ -144,7 +144,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // make every fragment load conflict-free: A-type (row-indexed by the lane's
 // group) stride CSA = 20, B-type stride CSB = 24.
 constexpr int CSA = 20, CSB = 24;
-constexpr int kFdCst = 5 * 16 * CSA + 2 * 16 * CSB;  // Vxi, Vx, Mx, My, 1/den | VyiT, VyT
+constexpr int kFdCst = 5 * 16 * CSA + 2 * 16 * CSB + 8 * CSA + 16 * 8;  // Vxi, Vx, Mx, My, 1/den | VyiT, VyT |
+                                                                        // flux projections (FD_UP_H)
 
 template <int Q, int MODE>
 __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
@@ -166,6 +167,8 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   double* cR = cMy + 16 * CSA;
   double* cVyit = cR + 16 * CSA;
   double* cVyt = cVyit + 16 * CSB;
+  double* cAew = cVyt + 16 * CSB;                      // FD_UP_H: rows Vx^T e_east, Vx^T e_west (A type, 8 rows)
+  double* cBns = cAew + 8 * CSA;                       // FD_UP_H: cols Vy^T e_n0, Vy^T e_n1 (B type, 16 x 8)
   for (int e = threadIdx.x; e < 8 * Q; e += 256) cst[e] = a.mats[5 * NI + e];
   if (threadIdx.x == 0) cst[8 * Q] = MODE == FD_DOWN ? a.mats[5 * NI + 8 * Q + 512] : 0.0;  // c
   for (int e = threadIdx.x; e < 256; e += 256) {
@@ -179,6 +182,26 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     if (MODE == FD_DOWN) {
       cMx[r * CSA + c] = a.mats[5 * NI + 8 * Q + e];
       cMy[r * CSA + c] = a.mats[5 * NI + 8 * Q + 256 + e];
+    }
+  }
+  if (MODE == FD_UP_H) {
+    __syncthreads();
+    // the fluxes of w = Vx T2 Vy^T need only projections of T2:
+    //   east / west (d/dx rows E0, E1):  h[y] = sum_r (a^T T2)[r] Vy[y][r],  a = Vx^T E
+    //   north / south (d/dy rows E2, E3): h[x] = sum_s Vx[x][s] (T2 b)[s],   b = Vy^T E
+    for (int e = threadIdx.x; e < 8 * CSA + 16 * 8; e += 256) {
+      double v = 0.0;
+      if (e < 8 * CSA) {
+        const int r = e / CSA, c = e % CSA;
+        if (r < 2 && c < Q)
+          for (int t = 0; t < Q; ++t) v = fma(a.mats[5 * NI + r * Q + t], cVx[t * CSA + c], v);
+        cAew[e] = v;
+      } else {
+        const int f = e - 8 * CSA, r = f >> 3, n = f & 7;
+        if (n < 2 && r < Q)
+          for (int t = 0; t < Q; ++t) v = fma(a.mats[5 * NI + (2 + n) * Q + t], cVyt[r * CSB + t], v);
+        cBns[f] = v;
+      }
     }
   }
   const double* Mx = cMx;                              // FD_DOWN with L u: [x][s]
@@ -289,6 +312,70 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         for (int h = 0; h < 2; ++h) acc[mi][nj][h] *= cR[(mi * 8 + gr) * CSA + nj * 8 + 2 * gc + h];
     store(bufB, SB);
     __syncwarp();
+    if (MODE == FD_UP_H) {
+      // fluxes of w = Vx T2 Vy^T without forming w (4 small DMMA products):
+      //   east / west rows:  h_ew = (A_ew T2) Vy^T,  A_ew = [e_east; e_west] Vx (2 of 8 rows)
+      //   north / south:     h_ns = Vx (T2 B_ns),    B_ns = Vy^T [e_n0 e_n1] (2 of 8 columns)
+      store(bufA, SA);  // T2 again, as an A operand
+      __syncwarp();
+      double pe[2][2], qn[2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) { pe[i][0] = pe[i][1] = 0.0; qn[i][0] = qn[i][1] = 0.0; }
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const double am = cAew[gr * CSA + k * 4 + gc];
+        const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
+        dmma(pe[0][0], pe[0][1], am, b0);
+        dmma(pe[1][0], pe[1][1], am, b1);
+        const double bq = cBns[(k * 4 + gc) * 8 + gr];
+        const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
+        dmma(qn[0][0], qn[0][1], a0, bq);
+        dmma(qn[1][0], qn[1][1], a1, bq);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        *reinterpret_cast<double2*>(bufA + gr * SA + i * 8 + 2 * gc) = make_double2(pe[i][0], pe[i][1]);
+        *reinterpret_cast<double2*>(bufB + (i * 8 + gr) * 8 + 2 * gc) = make_double2(qn[i][0], qn[i][1]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < 2; ++i) { pe[i][0] = pe[i][1] = 0.0; qn[i][0] = qn[i][1] = 0.0; }
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const double am = bufA[gr * SA + k * 4 + gc];
+        const double b0 = cVyt[(k * 4 + gc) * CSB + gr], b1 = cVyt[(k * 4 + gc) * CSB + 8 + gr];
+        dmma(pe[0][0], pe[0][1], am, b0);
+        dmma(pe[1][0], pe[1][1], am, b1);
+        const double bq = bufB[(k * 4 + gc) * 8 + gr];
+        const double a0 = cVx[gr * CSA + k * 4 + gc], a1 = cVx[(8 + gr) * CSA + k * 4 + gc];
+        dmma(qn[0][0], qn[0][1], a0, bq);
+        dmma(qn[1][0], qn[1][1], a1, bq);
+      }
+      // boundary order of the D_bi rows: east y (0..q), north / south interleaved by x, west y
+      double* out = a.H + kk * a.ld_h + (long long)l * NB;
+      if (gr < 2) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int yi = i * 8 + 2 * gc + h;
+            if (yi < Q) out[(gr == 0 ? 0 : 3 * Q) + yi] = pe[i][h];
+          }
+      }
+      if (gc == 0) {
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int xi = i * 8 + gr;
+          if (xi < Q) {
+            out[Q + 2 * xi] = qn[i][0];
+            out[Q + 2 * xi + 1] = qn[i][1];
+          }
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     // T3 = Vx T2  (B operand from bufB)
     clear();
 #pragma unroll
