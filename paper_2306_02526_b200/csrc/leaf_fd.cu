@@ -215,6 +215,9 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   __syncthreads();
   pdl_wait();
   const double* g = a.g ? a.g + kk * a.ld_g : nullptr;
+  // FD_DOWN: 16-byte stores of u_int pairs (every leaf block starts at an even offset when Q is even)
+  const bool vec = MODE == FD_DOWN && Q % 2 == 0 &&
+                   (reinterpret_cast<uintptr_t>(a.uint + (long long)kk * a.ld_uint) & 15) == 0;
   const int nwarps = gridDim.x * 8;
   constexpr int NR = (NI + 31) / 32;  // body-load values per lane
   constexpr int NU = (NB + 31) / 32;  // boundary values per lane (FD_DOWN)
@@ -244,21 +247,26 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         if (b < NB) ub[b] = nub[i];
       }
       __syncwarp();
+      int x = lane / Q, y = lane % Q;  // grid point of element lane + 32 i, advanced incrementally
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
-        const int e = lane + 32 * i;
-        if (e < NI) {
-          const int x = e / Q, y = e % Q;
+        if (x < Q) {
           const double cpl = Bc[x] * ub[y] + Bc[Q + x] * ub[3 * Q + y] + Bc[2 * Q + y] * ub[Q + 2 * x] +
                              Bc[3 * Q + y] * ub[Q + 2 * x + 1];
           bufB[x * SB + y] = nxt[i] - cpl;
         }
+        x += 32 / Q;
+        y += 32 % Q;
+        if (y >= Q) { y -= Q; ++x; }
       }
     } else {
+      int x = lane / Q, y = lane % Q;
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
-        const int e = lane + 32 * i;
-        if (e < NI) bufB[(e / Q) * SB + e % Q] = nxt[i];
+        if (x < Q) bufB[x * SB + y] = nxt[i];
+        x += 32 / Q;
+        y += 32 % Q;
+        if (y >= Q) { y -= Q; ++x; }
       }
     }
     fetch(l + nwarps);
@@ -402,14 +410,27 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
       }
     }
-    store(bufB, SB);
-    __syncwarp();
     if (MODE == FD_DOWN) {
+      // u_int straight from the accumulator fragments: row x = mi * 8 + gr, columns y, y + 1
       double* out = a.uint + kk * a.ld_uint + (long long)l * NI;
-      for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) {
+          const int x = mi * 8 + gr, y = nj * 8 + 2 * gc;
+          if (x < Q && y < Q) {
+            if (vec && y + 1 < Q) {
+              *reinterpret_cast<double2*>(out + x * Q + y) = make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+            } else {
+              out[x * Q + y] = acc[mi][nj][0];
+              if (y + 1 < Q) out[x * Q + y + 1] = acc[mi][nj][1];
+            }
+          }
+        }
       if (a.lu) {
         // the leaf grid G (p x p in 16 x 16, zero padded) in both operand layouts:
         // bufA (A operand, stride SA) and bufB (B operand, stride SB)
+        store(bufB, SB);
         __syncwarp();
         for (int e = lane; e < 256; e += 32) {
           const int x = e >> 4, y = e & 15;
@@ -463,6 +484,8 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       __syncwarp();
       continue;
     }
+    store(bufB, SB);
+    __syncwarp();
     double* out = MODE == FD_UP_WH ? a.WH + kk * a.ld_wh + (long long)l * a.nw
                                    : a.H + kk * a.ld_h + (long long)l * NB - NI;  // h at out[NI + b]
     if (MODE == FD_UP_WH)
