@@ -239,20 +239,32 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       }
     }
     // ---- stage the group's inputs for this split's columns
-    for (int e = tid; e < MNB * cw; e += MT) {
-      const int j = e / cw, col = e % cw;
-      double v = 0.0;
-      if (j < nv) {
-        const int node = node0 + j;
-        if (g.up) {
-          const double* Ha = g.Hc + (long long)(2 * node) * g.Hc_s;
-          v = __ldcg(Ha + g.Hc_s + sidx[1][col]) - __ldcg(Ha + sidx[0][col]);
-          if (g.jump) v = v - g.inv_dt * g.jump[g.j3[(long long)node * g.n3 + c0 + col]];
-        } else {
-          v = __ldcg(g.u + sidx[j][col]);
+    {  // every thread's loads issued before any is consumed
+      constexpr int GE = MNB * MKC / MT;
+      double va[GE], vb[GE];
+#pragma unroll
+      for (int u = 0; u < GE; ++u) {
+        const int e = tid + u * MT, j = e / cw, col = e - j * cw;
+        va[u] = 0.0; vb[u] = 0.0;
+        if (e < MNB * cw && j < nv) {
+          if (g.up) {
+            const double* Ha = g.Hc + (long long)(2 * (node0 + j)) * g.Hc_s;
+            vb[u] = __ldcg(Ha + g.Hc_s + sidx[1][col]);
+            va[u] = __ldcg(Ha + sidx[0][col]);
+          } else {
+            vb[u] = __ldcg(g.u + sidx[j][col]);
+          }
         }
       }
-      xs[j][col] = v;
+#pragma unroll
+      for (int u = 0; u < GE; ++u) {
+        const int e = tid + u * MT, j = e / cw, col = e - j * cw;
+        if (e < MNB * cw) {
+          double v = vb[u] - va[u];
+          if (g.up && g.jump && j < nv) v = v - g.inv_dt * g.jump[g.j3[(long long)(node0 + j) * g.n3 + c0 + col]];
+          xs[j][col] = v;
+        }
+      }
     }
     __syncthreads();
     if (p.trace && tid == 0) p.trace[MTS * t + 2] = gtime();

@@ -10,7 +10,9 @@ COLS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+        "lts__t_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct"]
 
 
 def main(rep):
@@ -23,7 +25,7 @@ def main(rep):
         vals = []
         for c in COLS:
             if c in idx:
-                vals.append(f"{c.split('__')[1][:18]}={row[idx[c]]}{units[idx[c]][:6]}")
+                vals.append(f"{c.split('__')[0][:4]}.{c.split('__')[1][:18]}={row[idx[c]]}{units[idx[c]][:6]}")
         st = []
         tot = 0.0
         for s in STALLS:
