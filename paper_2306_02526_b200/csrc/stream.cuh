@@ -54,4 +54,45 @@ __device__ __forceinline__ void stream_cols(double2 (&A)[U], const double2* __re
   }
 }
 
+// Both rows of the thread apply to ONE input vector x (a shared operator:
+// the row pair belongs to one node): x is read two columns at a time
+// (16-byte shared loads; x 16-byte aligned), operator addresses advance by a
+// pointer increment.  Columns [0, n) of x and of the panel starting at M.
+__device__ __forceinline__ void stream_pairs(const double2* __restrict__ M, int cs, int n, const double* x,
+                                             double& acc0, double& acc1) {
+  constexpr int U = 4;
+  const double2* p = M;
+  double2 A[U], B[U];
+  auto ld = [&](double2 (&m)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) { m[u] = __ldcs(p); p += cs; }
+  };
+  auto fma4 = [&](const double2 (&m)[U], int col) {
+#pragma unroll
+    for (int u = 0; u < U; u += 2) {
+      const double2 xv = *reinterpret_cast<const double2*>(x + col + u);
+      acc0 = fma(m[u].x, xv.x, acc0);
+      acc1 = fma(m[u].y, xv.x, acc1);
+      acc0 = fma(m[u + 1].x, xv.y, acc0);
+      acc1 = fma(m[u + 1].y, xv.y, acc1);
+    }
+  };
+  const int nfull = n / U;
+  if (nfull > 0) ld(A);
+  int b = 0;
+  for (; b + 1 < nfull; b += 2) {
+    ld(B);
+    fma4(A, b * U);
+    if (b + 2 < nfull) ld(A);
+    fma4(B, (b + 1) * U);
+  }
+  if (b < nfull) fma4(A, b * U);
+  for (int col = nfull * U; col < n; ++col) {
+    const double2 m = __ldcs(p);
+    p += cs;
+    acc0 = fma(m.x, x[col], acc0);
+    acc1 = fma(m.y, x[col], acc1);
+  }
+}
+
 }  // namespace hpsb

@@ -13,6 +13,8 @@
 // The operator rows a CTA needs for one level are one contiguous node-aligned
 // panel tile (make_panel_nodes), streamed column by column with the same
 // two-rows-per-thread, software-pipelined 16-byte loads as level_gemv.cu.
+#include <stdlib.h>
+
 #include "hps_plan.cuh"
 #include "stream.cuh"
 
@@ -54,7 +56,7 @@ struct SubArgs {
 // When there are fewer row pairs than threads, G threads share a row pair,
 // each streaming a contiguous column block; their partial sums meet in shared
 // memory (red, 2*NT*KM doubles) and are added in block order.
-template <int KM, class Out>
+template <int KM, bool SH, class Out>
 __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const double* xs, int xstride, double* red,
                                            Out out, int vn = 1) {
   const int R = pn.R, C = pn.C, TR = pn.TR, TS = pn.TS;
@@ -63,7 +65,7 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
   const int np = cs * vn;         // row pairs to compute
   int G = 1;
   while (2 * G * np <= NT && 2 * G * 4 <= C) G *= 2;
-  const int CKg = (C + G - 1) / G;
+  const int CKg = SH ? (((C + G - 1) / G + 1) & ~1) : (C + G - 1) / G;  // SH: even column blocks (16-byte x loads)
   const int t = threadIdx.x;
   // (node, local row) of stored row r of pair q; valid = r < rows of that node
   auto where = [&](int q, int h, int& j, int& row) -> bool {
@@ -86,9 +88,16 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
     double acc0[KM], acc1[KM];
 #pragma unroll
     for (int kk = 0; kk < KM; ++kk) { acc0[kk] = 0.0; acc1[kk] = 0.0; }
-    double2 A[U];
-    if (c1 - c0 >= U) load_batch<U>(A, M, cs, c0);
-    stream_cols<KM, U>(A, M, cs, c0, c1, xs, ja * KM * xstride, jb * KM * xstride, xstride, acc0, acc1);
+    const double* xa = xs + ja * KM * xstride + c0;
+    if (SH && KM == 1) {
+      // shared operator: both rows belong to node ja (= jb); x rows are 16-byte
+      // aligned (even strides and offsets, see the kernels' shared-memory carve)
+      stream_pairs(M + (size_t)c0 * cs, cs, c1 - c0, xa, acc0[0], acc1[0]);
+    } else {
+      double2 A[U];
+      if (c1 - c0 >= U) load_batch<U>(A, M, cs, c0);
+      stream_cols<KM, U>(A, M, cs, c0, c1, xs, ja * KM * xstride, jb * KM * xstride, xstride, acc0, acc1);
+    }
     if (G == 1) {
 #pragma unroll
       for (int kk = 0; kk < KM; ++kk) {
@@ -119,7 +128,7 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
   }
 }
 
-template <int KM>
+template <int KM, bool SH = false>
 __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
   extern __shared__ double sm[];
   double* Hs = sm;                    // children's fluxes of the current level [child][KM][nbc]
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
   pdl_wait();
   for (int e = a.nf - 1; e >= 0; --e) {
     const FLevel& L = a.lv[e];
-    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, nbc = L.nbc;
+    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, nbc = L.nbc, n3s = (n3 + 1) & ~1;
     const bool leafc = e == a.nf - 1;
     auto child = [&](int j, int kk, int which) -> const double* {  // which: 0 = alpha, 1 = beta
       if (leafc) return a.Hleaf + (kg0 + kk) * a.sh + (2LL * (node0 + j) + which) * a.hs;
@@ -144,11 +153,11 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
         v = child(j, kk, 1)[L.i3b[col]] - child(j, kk, 0)[L.i3a[col]];
         if (a.jump) v = v - a.inv_dt * a.jump[kg * a.jump_k + L.j3[(long long)(node0 + j) * n3 + col]];
       }
-      r3s[(j * KM + kk) * n3 + col] = v;
+      r3s[(j * KM + kk) * n3s + col] = v;
     }
     __syncthreads();
     // [w3; h - base] = [X33^-1; Tstack X33^-1] r3 for the subtree's nodes of this level
-    tile_apply<KM>(L.Up, L.Up.c == 1 ? 0 : b, r3s, n3, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM, SH>(L.Up, L.Up.c == 1 ? 0 : b, r3s, n3s, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       if (row < n3) {
@@ -167,7 +176,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
   }
 }
 
-template <int KM>
+template <int KM, bool SH = false>
 __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
   extern __shared__ double sm[];
   double* red = sm;                // 2 * NT * KM
@@ -177,14 +186,14 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
   pdl_wait();
   for (int e = 0; e < a.nf; ++e) {
     const FLevel& L = a.lv[e];
-    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12;
+    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, n12s = (n12 + 1) & ~1;
     if (e > 0) __syncthreads();  // this CTA's writes one level up are visible from here on
     for (int idx = tid; idx < npn * KM * n12; idx += NT) {
       const int col = idx % n12, t2 = idx / n12, kk = t2 % KM, j = t2 / KM, kg = kg0 + kk;
-      xs[(j * KM + kk) * n12 + col] = kg < a.k ? a.u[kg * a.u_k + L.gidx[(long long)(node0 + j) * n12 + col]] : 0.0;
+      xs[(j * KM + kk) * n12s + col] = kg < a.k ? a.u[kg * a.u_k + L.gidx[(long long)(node0 + j) * n12 + col]] : 0.0;
     }
     __syncthreads();
-    tile_apply<KM>(L.S, L.S.c == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM, SH>(L.S, L.S.c == 1 ? 0 : b, xs, n12s, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       const long long nd = (long long)(node0 + j) * n3 + row;
@@ -197,12 +206,12 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
 // Down sweep with the subtree's DOFs held in shared memory: the root
 // boundary is read from u once, every interface value this CTA produces is
 // kept (and written through to u) so lower levels gather from shared memory.
-template <int KM>
+template <int KM, bool SH = false>
 __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_down_local(SubArgs a) {
   extern __shared__ double sm[];
   double* red = sm;                        // 2 * NT * KM
   double* uloc = sm + 2 * NT * KM;         // [KM][nslots]
-  double* xs = uloc + KM * a.nslots;       // [node][KM][n12]
+  double* xs = uloc + ((KM * a.nslots + 1) & ~1);  // [node][KM][n12 rounded up to even]
   const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x, ns = a.nslots;
   pdl_trigger();
   pdl_wait();
@@ -215,15 +224,15 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_down_local(SubArgs 
   }
   for (int e = 0; e < a.nf; ++e) {
     const FLevel& L = a.lv[e];
-    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, jb = a.j3_base[e];
+    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, jb = a.j3_base[e], n12s = (n12 + 1) & ~1;
     const int* sl = a.slots + a.slot_off[e];
     __syncthreads();
     for (int idx = tid; idx < npn * KM * n12; idx += NT) {
       const int col = idx % n12, t2 = idx / n12, kk = t2 % KM, j = t2 / KM;
-      xs[(j * KM + kk) * n12 + col] = uloc[kk * ns + sl[j * n12 + col]];
+      xs[(j * KM + kk) * n12s + col] = uloc[kk * ns + sl[j * n12 + col]];
     }
     __syncthreads();
-    tile_apply<KM>(L.S, L.S.c == 1 ? 0 : b, xs, n12, red, [&](int j, int row, int kk, double y) {
+    tile_apply<KM, SH>(L.S, L.S.c == 1 ? 0 : b, xs, n12s, red, [&](int j, int row, int kk, double y) {
       const int kg = kg0 + kk;
       if (kg >= a.k) return;
       const long long nd = (long long)(node0 + j) * n3 + row;
@@ -252,9 +261,9 @@ void fill_args(const Ops& ops, const Workspace& ws, int k, SubArgs& a) {
     L.W3_k = (long long)lv.c * lv.n3;
     const int npn = 1 << e;
     hcap = std::max(hcap, npn * lv.n12);  // children's fluxes of level e are level e+1's
-    rcap = std::max(rcap, npn * lv.n3);
+    rcap = std::max(rcap, npn * ((lv.n3 + 1) & ~1));
   }
-  a.hcap = hcap;
+  a.hcap = (hcap + 1) & ~1;  // even: the r3 block after the two flux blocks starts 16-byte aligned
   a.rcap = rcap;
   if (P.sub_local) {
     a.slots = P.sub_slots;
@@ -267,6 +276,18 @@ void fill_args(const Ops& ops, const Workspace& ws, int k, SubArgs& a) {
     a.H_dF = ws.H[P.dF];
     a.H_k = (long long)P.lv[P.dF].c * P.lv[P.dF].n12;
   }
+}
+
+// every fused level holds one (shared) operator tile: row pairs never straddle nodes
+bool shared_sub(const SubArgs& a) {
+  static const bool off = [] {
+    const char* e = getenv("HPSB_NO_SUB_SH");
+    return e && e[0] == '1';
+  }();
+  if (off) return false;
+  for (int e = 0; e < a.nf; ++e)
+    if (a.lv[e].Up.c != 1 || a.lv[e].S.c != 1) return false;
+  return true;
 }
 
 template <class K>
@@ -318,6 +339,7 @@ int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, 
   a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt;
   const int KM = k == 1 ? 1 : 4;
   const size_t smem = (size_t)KM * (2 * a.hcap + a.rcap + 2 * NT) * 8;
+  if (KM == 1 && shared_sub(a)) return launch_sub(k_sub_up<1, true>, b1 - b0, 1, k, smem, a, st);
   if (KM == 1) return launch_sub(k_sub_up<1>, b1 - b0, 1, k, smem, a, st);
   return launch_sub(k_sub_up<4>, b1 - b0, 4, k, smem, a, st);
 }
@@ -332,15 +354,17 @@ int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double
   a.u = u; a.u_k = ld_u; a.has_w3 = has_w3 ? 1 : 0;
   const int KM = k == 1 ? 1 : 4;
   int xcap = 0;
-  for (int e = 0; e < a.nf; ++e) xcap = std::max(xcap, (1 << e) * a.lv[e].n12);
+  for (int e = 0; e < a.nf; ++e) xcap = std::max(xcap, (1 << e) * ((a.lv[e].n12 + 1) & ~1));
   if (P.sub_local) {
-    const size_t smem = (size_t)KM * (xcap + a.nslots + 2 * NT) * 8;
+    const size_t smem = (size_t)(KM * (xcap + 2 * NT) + ((KM * a.nslots + 1) & ~1)) * 8;
     if (smem <= 200 * 1024) {
+      if (KM == 1 && shared_sub(a)) return launch_sub(k_sub_down_local<1, true>, b1 - b0, 1, k, smem, a, st);
       if (KM == 1) return launch_sub(k_sub_down_local<1>, b1 - b0, 1, k, smem, a, st);
       return launch_sub(k_sub_down_local<4>, b1 - b0, 4, k, smem, a, st);
     }
   }
   const size_t smem = (size_t)KM * (xcap + 2 * NT) * 8;
+  if (KM == 1 && shared_sub(a)) return launch_sub(k_sub_down<1, true>, b1 - b0, 1, k, smem, a, st);
   if (KM == 1) return launch_sub(k_sub_down<1>, b1 - b0, 1, k, smem, a, st);
   return launch_sub(k_sub_down<4>, b1 - b0, 4, k, smem, a, st);
 }
