@@ -39,7 +39,7 @@ constexpr int MGRP = 8;        // column groups (MT / (MRB / 2))
 constexpr int MNB = 4;         // nodes per group
 constexpr int MKC = 256;       // max operator columns per task (32 per thread)
 constexpr int MAXSEG = 24;
-constexpr int MXS = MKC + 1;
+constexpr int MXS = MKC + 2;   // even: 16-byte x loads (every lane of a group reads the same x: broadcasts)
 constexpr int MTS = 6;         // trace stamps per task
 constexpr int MU = 4;          // 16-byte operator loads per batch (two batches in flight)
 
@@ -123,7 +123,7 @@ __device__ __forceinline__ unsigned long long gtime() {
 // (node * R + r) and may span up to MNB nodes; NG = 1
 template <bool PN>
 __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
-  __shared__ double xs[MNB][MXS];              // the task's inputs
+  __shared__ __align__(16) double xs[MNB][MXS];              // the task's inputs
   __shared__ double red[MGRP][MNB][MRB];       // column-group partial sums
   __shared__ int sidx[MNB][MKC];               // gather indices (down: per node; up: i3a / i3b rows 0 / 1)
   __shared__ unsigned s_last;
@@ -168,7 +168,8 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     // the gather indices and this thread's epilogue index are in flight while
     // the task waits for its inputs
     const int c0 = split * g.KC, cw = min(g.KC, g.K - c0);
-    const int cg = (cw + MGRP - 1) / MGRP, a0 = min(cw, grp * cg), a1 = min(cw, a0 + cg);
+    // column groups of an even width (16-byte x loads in the shared-operator stream)
+    const int cg = ((cw + MGRP - 1) / MGRP + 1) & ~1, a0 = min(cw, grp * cg), a1 = min(cw, a0 + cg);
     const int row = rb * MRB + 2 * q;  // rows row, row + 1 (R and TR are even: both valid or both padding)
     const bool rows_ok = row < nrows;
     const int cs = g.TR / 2;           // column stride in double2
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       double acc0[MNB], acc1[MNB];
 #pragma unroll
       for (int j = 0; j < MNB; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
-      if (rows_ok) stream_cols<MNB, MU>(A, M, cs, a0, a1, &xs[0][0], 0, 0, MXS, acc0, acc1);
+      if (rows_ok) stream_pairs_nb<MNB, MU>(A, M + (size_t)a0 * cs, cs, a1 - a0, &xs[0][a0], MXS, acc0, acc1);
 #pragma unroll
       for (int j = 0; j < MNB; ++j) {
         red[grp][j][2 * q] = acc0[j];

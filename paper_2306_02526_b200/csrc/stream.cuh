@@ -95,4 +95,49 @@ __device__ __forceinline__ void stream_pairs(const double2* __restrict__ M, int 
   }
 }
 
+// NB input vectors at x + j * XS (16-byte aligned rows, XS even) share one
+// operator (row pair of a one-node panel): acc{0,1}[j] += M[col].{x,y} x[j][col]
+// over columns [0, n).  A must already hold columns [0, U) when n >= U.
+template <int NB, int U>
+__device__ __forceinline__ void stream_pairs_nb(double2 (&A)[U], const double2* __restrict__ M, int cs, int n,
+                                                const double* x, int XS, double (&acc0)[NB], double (&acc1)[NB]) {
+  static_assert(U % 2 == 0, "column pairs");
+  const int nfull = n / U;
+  const double2* p = M + (size_t)(nfull > 0 ? U : 0) * cs;
+  double2 B[U];
+  auto ld = [&](double2 (&m)[U]) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) { m[u] = __ldcs(p); p += cs; }
+  };
+  auto fma4 = [&](const double2 (&m)[U], int col) {
+#pragma unroll
+    for (int u = 0; u < U; u += 2)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const double2 xv = *reinterpret_cast<const double2*>(x + j * XS + col + u);
+        acc0[j] = fma(m[u].x, xv.x, acc0[j]);
+        acc1[j] = fma(m[u].y, xv.x, acc1[j]);
+        acc0[j] = fma(m[u + 1].x, xv.y, acc0[j]);
+        acc1[j] = fma(m[u + 1].y, xv.y, acc1[j]);
+      }
+  };
+  int b = 0;
+  for (; b + 1 < nfull; b += 2) {
+    ld(B);
+    fma4(A, b * U);
+    if (b + 2 < nfull) ld(A);
+    fma4(B, (b + 1) * U);
+  }
+  if (b < nfull) fma4(A, b * U);
+  for (int col = nfull * U; col < n; ++col) {
+    const double2 m = __ldcs(p);
+    p += cs;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      acc0[j] = fma(m.x, x[j * XS + col], acc0[j]);
+      acc1[j] = fma(m.y, x[j * XS + col], acc1[j]);
+    }
+  }
+}
+
 }  // namespace hpsb
