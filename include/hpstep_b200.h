@@ -165,6 +165,16 @@ int hps_solve_stage(const hps_ops* ops, int k, const double* fb, long long ld_f,
                     long long ld_g, double* u, long long ld_u, double* lu_int, long long ld_lu,
                     double* guard, void* ws, size_t ws_bytes, void* stream);
 
+/* Stage history of an explicit stage (timestep.py:259-261, the first ARK
+ * stage's L u_n): lu_int = L u at the interiors of leaves [leaf0, leaf0 +
+ * nleaf) (operators.py:276-301 at interior points; rows start at leaf0's
+ * interior) and guard = max(guard, max |u|) over those leaves' grids
+ * (guard may be NULL).  The same leaf-grid products as hps_solve_stage,
+ * without the solve.  Constant coefficients with the tensor-product leaf
+ * solve only (HPS_ERR_ARG otherwise: use hps_leaf_eval_range). */
+int hps_leaf_lu(const hps_ops* ops, int leaf0, int nleaf, int k, const double* u, long long ld_u,
+                double* lu_int, long long ld_lu, double* guard, void* stream);
+
 /* Subtree-sharded solve (the reference solves the whole tree
  * in one call, solver.py:201-276).  With a plan created with nparts = 2^lstar,
  * part r is the subtree of node r on parent level lstar.  Phases:

@@ -100,6 +100,7 @@ SIGNATURES = {
                              _vp, _ll, _vp, ctypes.c_size_t, _vp]),
     "hps_plan_partition": (_i, [_vp, _i, c_int_p, c_int_p, c_int_p, c_ll_p]),
     "hps_solve_stage": (_i, [_vp, _i, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _ll, _vp, _vp, ctypes.c_size_t, _vp]),
+    "hps_leaf_lu": (_i, [_vp, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),
     "hps_disc_create": (_i, [_vp, ctypes.POINTER(DiscDesc), ctypes.POINTER(_vp)]),
     "hps_disc_destroy": (None, [_vp]),
     "hps_leaf_eval": (_i, [_vp, _i, _vp, _ll, _vp, _vp, _vp, _vp, _vp, _ll, _vp, _vp]),

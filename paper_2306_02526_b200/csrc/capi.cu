@@ -578,6 +578,25 @@ int hps_solve_stage(const hps_ops* h, int k, const double* fb, long long ld_f, c
                (cudaStream_t)stream, lu_int, ld_lu, guard);
 }
 
+int hps_leaf_lu(const hps_ops* h, int leaf0, int nleaf, int k, const double* u, long long ld_u, double* lu_int,
+                long long ld_lu, double* guard, void* stream) {
+  if (!h || !u || !lu_int) { set_error("hps_leaf_lu: null argument"); return HPS_ERR_ARG; }
+  const Ops& O = h->O;
+  const Plan& P = *O.plan;
+  if (!(O.shared_leaf && O.fd)) {
+    set_error("hps_leaf_lu: needs the tensor-product leaf solve (constant coefficients)");
+    return HPS_ERR_ARG;
+  }
+  if (leaf0 < 0 || nleaf < 0 || leaf0 + nleaf > P.L || k <= 0) {
+    set_error("hps_leaf_lu: leaf range [%d, %d) of %d, k = %d", leaf0, leaf0 + nleaf, P.L, k);
+    return HPS_ERR_ARG;
+  }
+  if (leaf_fd_lu(O, k, nleaf, P.leaf_bnd_gidx + (long long)leaf0 * P.nb, u, ld_u, u + (long long)leaf0 * P.ni,
+                 lu_int, ld_lu, guard, (cudaStream_t)stream))
+    return HPS_ERR_CUDA;
+  return HPS_OK;
+}
+
 int hps_plan_partition(const hps_plan* h, int k, int* nparts, int* lstar, int* n12, long long* flux_offset) {
   if (!h) { set_error("hps_plan_partition: null plan"); return HPS_ERR_ARG; }
   const Plan& P = h->P;

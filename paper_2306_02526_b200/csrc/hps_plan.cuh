@@ -219,6 +219,10 @@ int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld
 int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, const int* lbg, const double* u,
                  long long ld_u, double* uint, long long ld_uint, double* lu, long long ld_lu, double* guard,
                  cudaStream_t st);
+// L u at the interiors of nleaf leaves of a given state (the leaf grid's two
+// DMMA products of the fused stage, without the solve); lbg / uint / lu at the first leaf
+int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u, long long ld_u, const double* uint,
+               double* lu, long long ld_lu, double* guard, cudaStream_t st);
 
 // persistent dataflow kernel for the wide levels (mega.cu): up
 // levels [u0, u1) deepest first, then down levels [d0, d1) root first, over

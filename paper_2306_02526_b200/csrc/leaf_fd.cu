@@ -42,7 +42,9 @@ struct FdArgs {
 };
 
 // modes of the tensor-core kernel
-enum FdMode { FD_UP_WH = 0, FD_UP_H = 1, FD_DOWN = 2 };
+// FD_LU: L u at the interiors of a given state (interiors from a.uint, boundary
+// values through lbg), the stage history of an explicit stage
+enum FdMode { FD_UP_WH = 0, FD_UP_H = 1, FD_DOWN = 2, FD_LU = 3 };
 
 template <int Q>
 __global__ void __launch_bounds__(NT) k_leaf_fd(FdArgs a) {
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   double* cAew = cVyt + 16 * CSB;                      // FD_UP_H: rows Vx^T e_east, Vx^T e_west (A type, 8 rows)
   double* cBns = cAew + 8 * CSA;                       // FD_UP_H: cols Vy^T e_n0, Vy^T e_n1 (B type, 16 x 8)
   for (int e = threadIdx.x; e < 8 * Q; e += 256) cst[e] = a.mats[5 * NI + e];
-  if (threadIdx.x == 0) cst[8 * Q] = MODE == FD_DOWN ? a.mats[5 * NI + 8 * Q + 512] : 0.0;  // c
+  if (threadIdx.x == 0) cst[8 * Q] = MODE >= FD_DOWN ? a.mats[5 * NI + 8 * Q + 512] : 0.0;  // c
   for (int e = threadIdx.x; e < 256; e += 256) {
     const int r = e >> 4, c = e & 15;
     auto mat = [&](int m) -> double { return (r < Q && c < Q) ? a.mats[m * NI + r * Q + c] : 0.0; };
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     cVx[r * CSA + c] = mat(2);
     cVyt[r * CSB + c] = mat(3);
     cR[r * CSA + c] = mat(4);
-    if (MODE == FD_DOWN) {
+    if (MODE >= FD_DOWN) {
       cMx[r * CSA + c] = a.mats[5 * NI + 8 * Q + e];
       cMy[r * CSA + c] = a.mats[5 * NI + 8 * Q + 256 + e];
     }
@@ -222,14 +224,14 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   constexpr int NR = (NI + 31) / 32;  // body-load values per lane
   constexpr int NU = (NB + 31) / 32;  // boundary values per lane (FD_DOWN)
   double nxt[NR];                     // next leaf's body load, prefetched during this leaf
-  double nub[MODE == FD_DOWN ? NU : 1];
+  double nub[MODE >= FD_DOWN ? NU : 1];
   auto fetch = [&](int leaf) {
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
       const int e = lane + 32 * i;
       nxt[i] = (g && leaf < a.L && e < NI) ? g[(long long)leaf * NI + e] : 0.0;
     }
-    if (MODE == FD_DOWN) {
+    if (MODE >= FD_DOWN) {
       const double* u = a.u + kk * a.ld_u;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
@@ -240,6 +242,13 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   };
   fetch(blockIdx.x * 8 + warp);
   for (int l = blockIdx.x * 8 + warp; l < a.L; l += nwarps) {
+    if (MODE == FD_LU) {
+#pragma unroll
+      for (int i = 0; i < NU; ++i) {
+        const int b = lane + 32 * i;
+        if (b < NB) ub[b] = nub[i];
+      }
+    }
     if (MODE == FD_DOWN) {
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
@@ -286,6 +295,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
           *reinterpret_cast<double2*>(buf + (mi * 8 + gr) * ld + nj * 8 + 2 * gc) =
               make_double2(acc[mi][nj][0], acc[mi][nj][1]);
     };
+    if (MODE != FD_LU) {
     // T1 = Vx^-1 R  (B operand from bufB)
     clear();
 #pragma unroll
@@ -427,88 +437,93 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
             }
           }
         }
-      if (a.lu) {
-        // the leaf grid G (p x p in 16 x 16, zero padded) in both operand layouts:
-        // bufA (A operand, stride SA) and bufB (B operand, stride SB)
-        store(bufB, SB);
+      if (!a.lu) {
         __syncwarp();
-        for (int e = lane; e < 256; e += 32) {
-          const int x = e >> 4, y = e & 15;
-          double v = 0.0;
-          if (x >= 1 && x <= Q && y >= 1 && y <= Q) v = bufB[(x - 1) * SB + (y - 1)];
-          else if (x == 0 && y >= 1 && y <= Q) v = ub[y - 1];
-          else if (x == Q + 1 && y >= 1 && y <= Q) v = ub[3 * Q + y - 1];
-          else if (y == 0 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1)];
-          else if (y == Q + 1 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1) + 1];
-          bufA[x * SA + y] = v;
-          const double av = fabs(v);
-          gmax = (av > gmax || av != av) ? av : gmax;
+        continue;
+      }
+      store(bufB, SB);  // u_int: the interior of the leaf grid
+      __syncwarp();
+    } else {
+      store(bufB, SB);
+      __syncwarp();
+      double* out = MODE == FD_UP_WH ? a.WH + kk * a.ld_wh + (long long)l * a.nw
+                                     : a.H + kk * a.ld_h + (long long)l * NB - NI;  // h at out[NI + b]
+      if (MODE == FD_UP_WH)
+        for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
+      // h = D_bi w along the grid line of each boundary point
+      for (int b = lane; b < NB; b += 32) {
+        double s = 0.0;
+        if (b < Q || b >= 3 * Q) {
+          const int yi = b < Q ? b : b - 3 * Q;
+          const double* rr = E + (b < Q ? 0 : Q);
+#pragma unroll
+          for (int t = 0; t < Q; ++t) s = fma(rr[t], bufB[t * SB + yi], s);
+        } else {
+          const int jj = b - Q, xi = jj / 2;
+          const double* rr = E + ((jj & 1) ? 3 : 2) * Q;
+#pragma unroll
+          for (int t = 0; t < Q; ++t) s = fma(rr[t], bufB[xi * SB + t], s);
         }
-        __syncwarp();
-        for (int e = lane; e < 256; e += 32) bufB[(e >> 4) * SB + (e & 15)] = bufA[(e >> 4) * SA + (e & 15)];
-        __syncwarp();
-        clear();
-#pragma unroll
-        for (int k = 0; k < KSL; ++k) {  // Mx G
-          const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
-#pragma unroll
-          for (int mi = 0; mi < 2; ++mi) {
-            const double am = Mx[(mi * 8 + gr) * CSA + k * 4 + gc];
-            dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
-            dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < KSL; ++k) {  // + G My^T
-          const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
-#pragma unroll
-          for (int nj = 0; nj < 2; ++nj) {
-            const double bm = My[(nj * 8 + gr) * CSA + k * 4 + gc];
-            dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
-            dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
-          }
-        }
-        double* lo = a.lu + kk * a.ld_lu + (long long)l * NI;
-        const double c0 = cst[8 * Q];
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int nj = 0; nj < 2; ++nj)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int x = mi * 8 + gr, y = nj * 8 + 2 * gc + h;
-              if (x >= 1 && x <= Q && y >= 1 && y <= Q)
-                lo[(x - 1) * Q + (y - 1)] = acc[mi][nj][h] - c0 * bufA[x * SA + y];
-            }
+        out[NI + b] = s;
       }
       __syncwarp();
       continue;
     }
-    store(bufB, SB);
-    __syncwarp();
-    double* out = MODE == FD_UP_WH ? a.WH + kk * a.ld_wh + (long long)l * a.nw
-                                   : a.H + kk * a.ld_h + (long long)l * NB - NI;  // h at out[NI + b]
-    if (MODE == FD_UP_WH)
-      for (int e = lane; e < NI; e += 32) out[e] = bufB[(e / Q) * SB + e % Q];
-    // h = D_bi w along the grid line of each boundary point
-    for (int b = lane; b < NB; b += 32) {
-      double s = 0.0;
-      if (b < Q || b >= 3 * Q) {
-        const int yi = b < Q ? b : b - 3 * Q;
-        const double* rr = E + (b < Q ? 0 : Q);
-#pragma unroll
-        for (int t = 0; t < Q; ++t) s = fma(rr[t], bufB[t * SB + yi], s);
-      } else {
-        const int jj = b - Q, xi = jj / 2;
-        const double* rr = E + ((jj & 1) ? 3 : 2) * Q;
-#pragma unroll
-        for (int t = 0; t < Q; ++t) s = fma(rr[t], bufB[xi * SB + t], s);
-      }
-      out[NI + b] = s;
+    }  // MODE != FD_LU
+    // FD_DOWN with the stage history, FD_LU: bufB holds the leaf's interior values
+    // the leaf grid G (p x p in 16 x 16, zero padded) in both operand layouts:
+    // bufA (A operand, stride SA) and bufB (B operand, stride SB)
+    for (int e = lane; e < 256; e += 32) {
+      const int x = e >> 4, y = e & 15;
+      double v = 0.0;
+      if (x >= 1 && x <= Q && y >= 1 && y <= Q) v = bufB[(x - 1) * SB + (y - 1)];
+      else if (x == 0 && y >= 1 && y <= Q) v = ub[y - 1];
+      else if (x == Q + 1 && y >= 1 && y <= Q) v = ub[3 * Q + y - 1];
+      else if (y == 0 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1)];
+      else if (y == Q + 1 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1) + 1];
+      bufA[x * SA + y] = v;
+      const double av = fabs(v);
+      gmax = (av > gmax || av != av) ? av : gmax;
     }
     __syncwarp();
+    for (int e = lane; e < 256; e += 32) bufB[(e >> 4) * SB + (e & 15)] = bufA[(e >> 4) * SA + (e & 15)];
+    __syncwarp();
+    clear();
+#pragma unroll
+    for (int k = 0; k < KSL; ++k) {  // Mx G
+      const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const double am = Mx[(mi * 8 + gr) * CSA + k * 4 + gc];
+        dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
+        dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KSL; ++k) {  // + G My^T
+      const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj) {
+        const double bm = My[(nj * 8 + gr) * CSA + k * 4 + gc];
+        dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
+        dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
+      }
+    }
+    double* lo = a.lu + kk * a.ld_lu + (long long)l * NI;
+    const double c0 = cst[8 * Q];
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int x = mi * 8 + gr, y = nj * 8 + 2 * gc + h;
+          if (x >= 1 && x <= Q && y >= 1 && y <= Q)
+            lo[(x - 1) * Q + (y - 1)] = acc[mi][nj][h] - c0 * bufA[x * SA + y];
+        }
+    __syncwarp();
   }
-  if (MODE == FD_DOWN && a.guard) {  // max |u| over the staged grids (NaN sorts above inf)
+  if (MODE >= FD_DOWN && a.guard) {  // max |u| over the staged grids (NaN sorts above inf)
     unsigned long long bits = __double_as_longlong(gmax);
     for (int off = 16; off > 0; off >>= 1) {
       const unsigned long long o = __shfl_xor_sync(0xffffffffu, bits, off);
@@ -562,6 +577,15 @@ int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld
   a.uint = uint; a.ld_uint = ld_uint; a.mats = ops.fd;
   a.lu = lu; a.ld_lu = ld_lu; a.guard = reinterpret_cast<unsigned long long*>(guard);
   return launch_fd_mma<FD_DOWN>(*ops.plan, a, nleaf, k, st);
+}
+
+int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u, long long ld_u, const double* uint,
+               double* lu, long long ld_lu, double* guard, cudaStream_t st) {
+  if (nleaf <= 0) return 0;
+  FdArgs a{};
+  a.L = nleaf; a.k = k; a.g = uint; a.ld_g = ld_u; a.lbg = lbg; a.u = u; a.ld_u = ld_u; a.mats = ops.fd;
+  a.lu = lu; a.ld_lu = ld_lu; a.guard = reinterpret_cast<unsigned long long*>(guard);
+  return launch_fd_mma<FD_LU>(*ops.plan, a, nleaf, k, st);
 }
 
 int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,

@@ -320,6 +320,19 @@ class HpsOperatorSet:
         _lib.check(rc, "hps_solve_stage")
         return out
 
+    def leaf_lu_device(self, u, lu, guard=None, leaves=None):
+        """Interior L u of the (k, N) device state ``u`` into ``lu`` (rows from
+        the first leaf's interior) and max |u| into ``guard``, by the leaf-grid
+        products of the fused stage (hps_leaf_lu; needs ``fuses_stage_history``).
+        ``leaves = (leaf0, nleaf)`` restricts it to a leaf range."""
+        k = u.shape[0]
+        leaf0, nleaf = (0, self.tree.L) if leaves is None else leaves
+        rc = self._lib.hps_leaf_lu(self.handle, leaf0, nleaf, k, u.data_ptr(), u.stride(0), lu.data_ptr(),
+                                   lu.stride(0), None if guard is None else guard.data_ptr(),
+                                   current_stream_handle())
+        _lib.check(rc, "hps_leaf_lu")
+        return lu
+
     def solve_phase(self, phases, part0, part1, fb, body, out, jump=None, inv_dt=None):
         """One or more phases of a subtree-partitioned solve (hps_solve_phase):
         ``_lib.HPS_PHASE_UP`` / ``TOP`` / ``DOWN`` over parts [part0, part1).

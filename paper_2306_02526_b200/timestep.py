@@ -767,7 +767,13 @@ class TimeStepper:
         return True
 
     def _eval_lu(self, U, out, guard=None):
-        """Stage history L u at the local leaf interiors."""
+        """Stage history L u at the local leaf interiors: the leaf-grid DMMA
+        products of the fused stage when the operator set has them, else the
+        general leaf evaluation."""
+        if self.ops.fuses_stage_history and os.environ.get("HPSB_NO_FD_LU") != "1":
+            if not self._dry:
+                self.ops.leaf_lu_device(U, out, guard)
+            return
         self._eval(U, lu_int=out, guard=guard)
 
     def _owned_combine(self, terms, out):

@@ -155,6 +155,40 @@ def test_fused_stage_matches_solve_then_eval(p):
     assert g1.item() == g2.item() and g1.item() > 0
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [10, 12, 16])
+def test_leaf_lu_matches_leaf_eval(p):
+    """hps_leaf_lu (the explicit stage's L u_n by the leaf-grid DMMA products)
+    equals the general leaf evaluation at the interiors, on a full range and a
+    leaf sub-range, with the same guard."""
+    import torch
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.timestep import device_discretization
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 8, 8, p)
+    coeffs = hb.OperatorCoefficients(c11=1.0, c22=0.7, c1=0.3, c2=-0.2, c=0.1)
+    disc = hb.EllipticDiscretization(tree, coeffs)
+    ops = hb.HpsOperatorSet(disc, sigma=1.0, dt_gamma=1e-3, layout="shared")
+    assert ops.fuses_stage_history
+    k = 2
+    rng = np.random.default_rng(100 + p)
+    u = torch.as_tensor(rng.standard_normal((k, tree.N)), device="cuda")
+    lu1 = torch.empty((k, tree.L * tree.ni), dtype=torch.float64, device="cuda")
+    lu2 = torch.empty_like(lu1)
+    g1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    g2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    ops.leaf_lu_device(u, lu1, g1)
+    device_discretization(disc).eval(u, lu_int=lu2, guard=g2)
+    assert rel_l2(lu1.cpu().numpy(), lu2.cpu().numpy()) < 1e-13
+    assert g1.item() == g2.item() == float(u.abs().max())
+    # leaf sub-range: rows start at the first leaf's interior, nothing else written
+    leaf0, nleaf = 5, 17
+    lu3 = torch.full_like(lu1, 7.0)
+    ops.leaf_lu_device(u, lu3[:, leaf0 * tree.ni:], leaves=(leaf0, nleaf))
+    a, b = leaf0 * tree.ni, (leaf0 + nleaf) * tree.ni
+    assert rel_l2(lu3[:, a:b].cpu().numpy(), lu2[:, a:b].cpu().numpy()) < 1e-13
+    assert torch.all(lu3[:, :a] == 7.0) and torch.all(lu3[:, b:] == 7.0)
+
+
 def test_timing_harness_rows(tmp_path):
     """run_timing (drivers.py:160-204) on the device: one row per size with
     the reference's columns, build and median solve times, CSV written."""
