@@ -160,7 +160,7 @@ int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const
  * (timestep.py:198-203), computed by the leaf kernel of the downward sweep
  * while the leaf's grid is on chip.  Constant coefficients with the
  * tensor-product leaf solve only (HPS_ERR_ARG otherwise: use hps_solve +
- * hps_leaf_eval). */
+ * hps_leaf_eval).  lu_int may be NULL (the last stage: solve + guard only). */
 int hps_solve_stage(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
                     long long ld_g, double* u, long long ld_u, double* lu_int, long long ld_lu,
                     double* guard, void* ws, size_t ws_bytes, void* stream);
@@ -262,6 +262,13 @@ int hps_combine(int k, long long n, int nterms, const double* coefs, const doubl
  * (dcoefs[t]), so a captured CUDA graph replays with per-step coefficients. */
 int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const double* const* vecs,
                     const long long* lds, double* out, long long ld_out, double* guard, void* stream);
+
+/* As hps_combine_dev with per-row coefficients: row r of out takes
+ * dcoefs[r * ld_c + t] (the boundary data f(t_i) of every stage time of a
+ * step, timestep.py:245,265, in one launch). */
+int hps_combine_dev_rows(int k, long long n, int nterms, const double* dcoefs, long long ld_c,
+                         const double* const* vecs, const long long* lds, double* out, long long ld_out,
+                         double* guard, void* stream);
 
 /* guard = max(guard, max |x|) over k rows of n values. */
 int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard, void* stream);

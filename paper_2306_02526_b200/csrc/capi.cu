@@ -568,7 +568,7 @@ int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const d
 int hps_solve_stage(const hps_ops* h, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
                     double* u, long long ld_u, double* lu_int, long long ld_lu, double* guard, void* ws,
                     size_t ws_bytes, void* stream) {
-  if (!h || !fb || !u || !ws || !lu_int) { set_error("hps_solve_stage: null argument"); return HPS_ERR_ARG; }
+  if (!h || !fb || !u || !ws) { set_error("hps_solve_stage: null argument"); return HPS_ERR_ARG; }
   const Ops& O = h->O;
   if (!(O.shared_leaf && O.fd && leaf_fd_down_enabled())) {
     set_error("hps_solve_stage: needs the tensor-product leaf solve (constant coefficients)");

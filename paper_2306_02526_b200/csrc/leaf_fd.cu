@@ -438,6 +438,22 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
           }
         }
       if (!a.lu) {
+        if (a.guard) {  // max |u| over the leaf's grid: interior fragments and boundary values
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int x = mi * 8 + gr, y = nj * 8 + 2 * gc + h;
+                const double av = (x < Q && y < Q) ? fabs(acc[mi][nj][h]) : 0.0;
+                gmax = (av > gmax || av != av) ? av : gmax;
+              }
+          for (int b = lane; b < NB; b += 32) {
+            const double av = fabs(ub[b]);
+            gmax = (av > gmax || av != av) ? av : gmax;
+          }
+        }
         __syncwarp();
         continue;
       }

@@ -487,6 +487,7 @@ struct CombineArgs {
   double* out; long long ld_out;
   unsigned long long* guard;
   const double* dc;            // device coefficient table (graph replay), else c[]
+  long long ldc;               // row stride of dc (per-row coefficients; 0 = shared by the rows)
 };
 
 __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(NT) k_combine(CombineArgs a) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (t0 + u >= a.nt) break;
-        s = fma(a.dc ? __ldg(a.dc + t0 + u) : a.c[t0 + u], v[u], s);
+        s = fma(a.dc ? __ldg(a.dc + kk * a.ldc + t0 + u) : a.c[t0 + u], v[u], s);
       }
     }
     a.out[kk * a.ld_out + e] = s;
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(NT) k_combine2(CombineArgs a) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (t0 + u >= a.nt) break;
-        const double c = a.dc ? __ldg(a.dc + t0 + u) : a.c[t0 + u];
+        const double c = a.dc ? __ldg(a.dc + kk * a.ldc + t0 + u) : a.c[t0 + u];
         s.x = fma(c, v[u].x, s.x);
         s.y = fma(c, v[u].y, s.y);
       }
@@ -748,10 +749,16 @@ int hps_combine(int k, long long n, int nterms, const double* coefs, const doubl
 
 int hps_combine_dev(int k, long long n, int nterms, const double* dcoefs, const double* const* vecs,
                     const long long* lds, double* out, long long ld_out, double* guard, void* stream) {
+  return hps_combine_dev_rows(k, n, nterms, dcoefs, 0, vecs, lds, out, ld_out, guard, stream);
+}
+
+int hps_combine_dev_rows(int k, long long n, int nterms, const double* dcoefs, long long ld_c,
+                         const double* const* vecs, const long long* lds, double* out, long long ld_out,
+                         double* guard, void* stream) {
   if (k <= 0 || n <= 0) return HPS_OK;
   if (nterms < 0 || nterms > MAXT) { set_error("hps_combine_dev: %d terms (max %d)", nterms, MAXT); return HPS_ERR_ARG; }
   CombineArgs a{};
-  a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out; a.dc = dcoefs;
+  a.nt = nterms; a.k = k; a.n = n; a.out = out; a.ld_out = ld_out; a.dc = dcoefs; a.ldc = ld_c;
   for (int t = 0; t < nterms; ++t) { a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
   a.guard = reinterpret_cast<unsigned long long*>(guard);
   if (combine_vec_ok(a)) {

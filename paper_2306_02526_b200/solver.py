@@ -315,7 +315,7 @@ class HpsOperatorSet:
         ws = self.plan.workspace(k)
         rc = self._lib.hps_solve_stage(
             self.handle, k, fb.data_ptr(), ld_f, None if body is None else body.data_ptr(), ld_g,
-            out.data_ptr(), out.stride(0), lu.data_ptr(), lu.stride(0),
+            out.data_ptr(), out.stride(0), None if lu is None else lu.data_ptr(), 0 if lu is None else lu.stride(0),
             None if guard is None else guard.data_ptr(), ws.data_ptr(), ws.numel(), current_stream_handle())
         _lib.check(rc, "hps_solve_stage")
         return out

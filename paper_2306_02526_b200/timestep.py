@@ -272,6 +272,29 @@ def combine(terms, out, n=None, guard=None):
     return out
 
 
+def combine_rows(coefs, vecs, out):
+    """out[r] = sum_t coefs[r][t] * vecs[t] (single-row terms) for every row r
+    of ``out`` in one launch (hps_combine_dev_rows)."""
+    lib = _lib.load()
+    k, nt = out.shape[0], len(vecs)
+    flat = [float(c) for row in coefs for c in row]
+    sink = _CoefSink.current
+    if sink is not None:
+        dptr = sink.take(flat)
+        if sink.dry:
+            return out
+        dc = None
+    else:
+        dc = torch.tensor(flat, dtype=torch.float64, device=out.device)
+        dptr = dc.data_ptr()
+    vp = (ctypes.c_void_p * max(1, nt))(*[v.data_ptr() for v in vecs])
+    lds = (ctypes.c_longlong * max(1, nt))(*([0] * nt))
+    rc = lib.hps_combine_dev_rows(k, out.shape[1], nt, dptr, nt, vp, lds, out.data_ptr(), out.stride(0), None,
+                                  current_stream_handle())
+    _lib.check(rc, "hps_combine_dev_rows")
+    return out
+
+
 def evaluate_nonlinear(disc, problem, t, u):
     """Pointwise g with leaf-local spectral derivatives (timestep.py:64-78)."""
     as_numpy = not torch.is_tensor(u)
@@ -342,6 +365,14 @@ class _Field:
             return [(scale * f, phi) for f, phi in zip(self.fn.factors(t), self.sep)]
         return [(scale, self._stack(self.fn(t, self.pts)))]
 
+    def values(self, times):
+        """(len(times), n) tensor of F at each time in one launch, for a
+        separable F of single-row terms (None otherwise: use value)."""
+        if self.fn is None or self.sep is None or any(v.shape[0] != 1 for v in self.sep):
+            return None
+        out = torch.empty((len(times), self.n), dtype=torch.float64, device=self.dev)
+        return combine_rows([self.fn.factors(t) for t in times], self.sep, out)
+
     def value(self, t, out=None):
         """(k or 1, n) tensor of F(t)."""
         if self.fn is None:
@@ -392,6 +423,7 @@ class TimeStepper:
         k = problem.ncomp
         self._k = k
         self._F = _Field(problem.f, self._bnd_pts, k, self._dev)
+        self._bc_batch = os.environ.get("HPSB_NO_BC_BATCH") != "1"
         self._Ft = _Field(None if problem.time_independent_bc else problem.f_t, self._bnd_pts, k,
                           self._dev)
         self._Q = _Field(problem.q, self._all_pts, k, self._dev)
@@ -856,6 +888,10 @@ class TimeStepper:
                 elif not self._dry:
                     QG[i].zero_()
 
+        # boundary data of stages 1..s-1 and of t + dt, one launch when f is separable
+        bcs = self._F.values([t + pair.c[i] * dt for i in range(1, s)] + [t + dt]) \
+            if self._bc_batch else None
+        bc_at = lambda i, ti: self._bc(ti) if bcs is None else bcs[i - 1:i]
         self._eval_lu(u, Lu[0])
         stage_q_g(0, t + pair.c[0] * dt, u)
         ui = u
@@ -870,14 +906,14 @@ class TimeStepper:
                     terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), iv(phi)))
             combine(terms, r, n=Lni)
             ui = U[i & 1]
-            if i < s - 1 and self._fused_stage(self._bc(ti), r, ui, Lu[i], guards[i - 1]):
-                pass                                 # solve + history L u_i + guard in one pass
-            elif i < s - 1:
-                self._solve(self.ops, self._bc(ti), r, ui)
-                self._eval_lu(ui, Lu[i], guard=guards[i - 1])
-            else:
-                self._solve(self.ops, self._bc(ti), r, ui)
-                self._owned_maxabs(ui, guards[i - 1])
+            bc = bc_at(i, ti)
+            # solve + history L u_i (not needed after the last stage) + guard in one pass
+            if not self._fused_stage(bc, r, ui, Lu[i] if i < s - 1 else None, guards[i - 1]):
+                self._solve(self.ops, bc, r, ui)
+                if i < s - 1:
+                    self._eval_lu(ui, Lu[i], guard=guards[i - 1])
+                else:
+                    self._owned_maxabs(ui, guards[i - 1])
             stage_q_g(i, ti, ui)
         w = pair.bhat - Ah[s - 1]
         terms = [(1.0, ui)]
@@ -889,7 +925,7 @@ class TimeStepper:
         # `out` may alias `u`: nothing below reads u
         unew = torch.empty((k, N), dtype=torch.float64, device=self._dev) if out is None else out
         self._owned_combine(terms, unew)
-        self._put_boundary(self._bc(t + dt), unew)
+        self._put_boundary(bc_at(s, t + dt), unew)
         self._owned_maxabs(unew, guards[s - 1])
         return unew
 
