@@ -487,8 +487,8 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     }
     }  // MODE != FD_LU
     // FD_DOWN with the stage history, FD_LU: bufB holds the leaf's interior values
-    // the leaf grid G (p x p in 16 x 16, zero padded) in both operand layouts:
-    // bufA (A operand, stride SA) and bufB (B operand, stride SB)
+    // the leaf grid G (p x p in 16 x 16, zero padded) in bufA (stride SA), read
+    // as the B operand of Mx G and the A operand of G My^T
     for (int e = lane; e < 256; e += 32) {
       const int x = e >> 4, y = e & 15;
       double v = 0.0;
@@ -502,12 +502,10 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       gmax = (av > gmax || av != av) ? av : gmax;
     }
     __syncwarp();
-    for (int e = lane; e < 256; e += 32) bufB[(e >> 4) * SB + (e & 15)] = bufA[(e >> 4) * SA + (e & 15)];
-    __syncwarp();
     clear();
 #pragma unroll
-    for (int k = 0; k < KSL; ++k) {  // Mx G
-      const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
+    for (int k = 0; k < KSL; ++k) {  // Mx G (SA = 4 mod 16: conflict-free as a B operand too)
+      const double b0 = bufA[(k * 4 + gc) * SA + gr], b1 = bufA[(k * 4 + gc) * SA + 8 + gr];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
         const double am = Mx[(mi * 8 + gr) * CSA + k * 4 + gc];
