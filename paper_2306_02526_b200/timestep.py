@@ -481,18 +481,51 @@ class TimeStepper:
         return self._Ft.value(t)
 
     def _g(self, t, U, out=None):
-        """g(t, U) with the interface-averaged device gradient (timestep.py:192-196)."""
+        """g(t, U) with the interface-averaged device gradient (timestep.py:192-196).
+        The gradient is not evaluated for a g that reads neither component
+        (found by one probe per g, see _probe_grad_use)."""
         if self.problem.g is None:
             return None
         ux, uy = self._buf("gx", U.shape), self._buf("gy", U.shape)
         if self._dry:
             return ux
-        self._dd.eval(U, ux=ux, uy=uy)
-        r = _call_g(self.problem.g, t, U, ux, uy)
+        g = self.problem.g
+        use = getattr(g, "_hb_grad_use", None) if getattr(g, "_hb_torch", None) is True else None
+        if use is None or any(use):  # both components: one pass of the gradient kernel
+            self._dd.eval(U, ux=ux, uy=uy)
+        r = _call_g(g, t, U, ux, uy)
+        if use is None and getattr(g, "_hb_torch", None) is True and \
+                os.environ.get("HPSB_NO_GRAD_PROBE") != "1" and not torch.cuda.is_current_stream_capturing():
+            self._probe_grad_use(g, t, U, ux, uy, r)
         if out is not None:
             out.copy_(r)
             return out
         return r
+
+    @staticmethod
+    def _probe_grad_use(g, t, U, ux, uy, r):
+        """Whether g reads ux / uy: g must return bitwise the same result with
+        the component replaced by NaNs and by random values (a g that reads it
+        cannot); any failure or difference counts as a use."""
+        use = []
+        gen = torch.Generator(device=U.device).manual_seed(12345)
+        for i in range(2):
+            used = False
+            for fill in ("nan", "rand"):
+                d = torch.full_like(ux, float("nan")) if fill == "nan" else \
+                    torch.randn(ux.shape, generator=gen, dtype=ux.dtype, device=ux.device)
+                args = (d, uy) if i == 0 else (ux, d)
+                try:
+                    rr = g(t, U, *args)
+                    rr = torch.broadcast_to(rr.to(torch.float64), U.shape)
+                    used = used or not torch.equal(rr, r)
+                except Exception:
+                    used = True
+            use.append(used)
+        try:
+            g._hb_grad_use = tuple(use)
+        except AttributeError:
+            pass
 
     def initial_state(self):
         u0 = np.asarray(self.problem.u0(self._all_pts), dtype=float)
