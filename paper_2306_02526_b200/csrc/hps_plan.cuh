@@ -214,8 +214,10 @@ bool leaf_fd_supported(int q);
 // tensor-product leaf solve split over the two sweeps: the up sweep writes only
 // the fluxes h, the down sweep solves u_int = A_ii^-1 (r - A_ib u_b) directly
 bool leaf_fd_down_enabled();
+// (nbd > 0: also the Dirichlet data u[bids[i]] = fb[i], see FdArgs)
 int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* H, long long ld_h,
-                 cudaStream_t st);
+                 cudaStream_t st, int nbd = 0, const int* bids = nullptr, const double* fb = nullptr,
+                 long long ld_f = 0, double* u = nullptr, long long ld_u = 0);
 int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, const int* lbg, const double* u,
                  long long ld_u, double* uint, long long ld_uint, double* lu, long long ld_lu, double* guard,
                  cudaStream_t st);

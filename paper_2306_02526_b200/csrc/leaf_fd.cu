@@ -35,6 +35,9 @@ struct FdArgs {
   double* uint; long long ld_uint;   // FD_DOWN: interior output (leaf l at l*ni)
   double* lu; long long ld_lu;       // FD_DOWN, optional: L u at the interiors (the stage history)
   unsigned long long* guard;         // ... and max |u| over the leaves' grids (bits, NaN sticky)
+  // FD_UP_H, optional: the solve's Dirichlet data u[ids[i]] = fb[i] (solver.py:259-260), written by the
+  // CTAs after the dependency wait (the up sweep never reads u) -- one launch fewer per solve
+  int nbd; const int* bids; const double* fb; long long ld_f; double* ubnd; long long ld_ubnd;
   const double* mats;                // Vxi, VyiT, Vx, VyT, den (q x q each), flux rows ex0, ex1, ey0, ey1,
                                      // then the interior-boundary couplings bx0, bx1, by0, by1 (q each),
                                      // then Mx = c11 d2x - c1 d1x, My = c22 d2y - c2 d1y (16 x 16, zero
@@ -216,6 +219,10 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
   __syncthreads();
   pdl_wait();
+  if (MODE == FD_UP_H && a.nbd > 0) {
+    for (int i = blockIdx.x * 256 + threadIdx.x; i < a.nbd; i += gridDim.x * 256)
+      a.ubnd[kk * a.ld_ubnd + a.bids[i]] = a.fb[kk * a.ld_f + i];
+  }
   const double* g = a.g ? a.g + kk * a.ld_g : nullptr;
   // FD_DOWN: 16-byte stores of u_int pairs (every leaf block starts at an even offset when Q is even)
   const bool vec = MODE == FD_DOWN && Q % 2 == 0 &&
@@ -457,8 +464,6 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         __syncwarp();
         continue;
       }
-      store(bufB, SB);  // u_int: the interior of the leaf grid
-      __syncwarp();
     } else {
       store(bufB, SB);
       __syncwarp();
@@ -486,17 +491,44 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       continue;
     }
     }  // MODE != FD_LU
-    // FD_DOWN with the stage history, FD_LU: bufB holds the leaf's interior values
-    // the leaf grid G (p x p in 16 x 16, zero padded) in bufA (stride SA), read
-    // as the B operand of Mx G and the A operand of G My^T
-    for (int e = lane; e < 256; e += 32) {
-      const int x = e >> 4, y = e & 15;
-      double v = 0.0;
-      if (x >= 1 && x <= Q && y >= 1 && y <= Q) v = bufB[(x - 1) * SB + (y - 1)];
-      else if (x == 0 && y >= 1 && y <= Q) v = ub[y - 1];
-      else if (x == Q + 1 && y >= 1 && y <= Q) v = ub[3 * Q + y - 1];
-      else if (y == 0 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1)];
-      else if (y == Q + 1 && x >= 1 && x <= Q) v = ub[Q + 2 * (x - 1) + 1];
+    // FD_DOWN with the stage history (u_int in the accumulator fragments), FD_LU
+    // (the interior staged in bufB): the leaf grid G (p x p in 16 x 16) in bufA
+    // (stride SA), read as the B operand of Mx G and the A operand of G My^T.
+    // Interior and boundary ring are written here; the four corners and (for
+    // p < 16) the padding keep finite values from the products / the initial
+    // zeroing, and only reach outputs that are discarded (every interior
+    // output's sums run along one grid line).
+    __syncwarp();
+    if (MODE == FD_LU) {
+      for (int e = lane; e < NI; e += 32) {
+        const int x = e / Q, y = e - x * Q;
+        const double v = bufB[x * SB + y];
+        bufA[(x + 1) * SA + y + 1] = v;
+        const double av = fabs(v);
+        gmax = (av > gmax || av != av) ? av : gmax;
+      }
+    } else {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int x = mi * 8 + gr, y = nj * 8 + 2 * gc + h;
+            if (x < Q && y < Q) {
+              const double v = acc[mi][nj][h];
+              bufA[(x + 1) * SA + y + 1] = v;
+              const double av = fabs(v);
+              gmax = (av > gmax || av != av) ? av : gmax;
+            }
+          }
+    }
+    for (int b = lane; b < NB; b += 32) {  // boundary order: east y, north / south by x, west y
+      int x, y;
+      if (b < Q) { x = 0; y = b + 1; }
+      else if (b >= 3 * Q) { x = Q + 1; y = b - 3 * Q + 1; }
+      else { x = (b - Q) / 2 + 1; y = ((b - Q) & 1) ? Q + 1 : 0; }
+      const double v = ub[b];
       bufA[x * SA + y] = v;
       const double av = fabs(v);
       gmax = (av > gmax || av != av) ? av : gmax;
@@ -575,10 +607,12 @@ static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaS
 bool leaf_fd_down_enabled() { return !getenv("HPSB_FD_SIMT") && !getenv("HPSB_NO_FD_DOWN"); }
 
 int leaf_fd_up_h(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* H, long long ld_h,
-                 cudaStream_t st) {
+                 cudaStream_t st, int nbd, const int* bids, const double* fb, long long ld_f, double* u,
+                 long long ld_u) {
   if (nleaf <= 0) return 0;
   FdArgs a{};
   a.L = nleaf; a.k = k; a.g = g; a.ld_g = ld_g; a.H = H; a.ld_h = ld_h; a.mats = ops.fd;
+  a.nbd = nbd; a.bids = bids; a.fb = fb; a.ld_f = ld_f; a.ubnd = u; a.ld_ubnd = ld_u;
   return launch_fd_mma<FD_UP_H>(*ops.plan, a, nleaf, k, st);
 }
 

@@ -216,10 +216,16 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
     Hleaf = ws.W + P.ni;
   }
 
+  bool bnd_done = false;  // Dirichlet data already written by the leaf kernel
   if (phases & SOLVE_UP) {
     // (2) leaf particular solutions and their fluxes (solver.py:219-230)
     if (g && fd_down) {
-      if (int rc = leaf_fd_up_h(ops, k, nleaf, g, ld_g, ws.Hleaf + (long long)leaf0 * P.nb, Lnb, st)) return rc;
+      // a whole solve: the leaf kernel also writes the Dirichlet data (no separate scatter launch)
+      const bool bnd = (phases & SOLVE_TOP) && P.nbd > 0;
+      if (int rc = leaf_fd_up_h(ops, k, nleaf, g, ld_g, ws.Hleaf + (long long)leaf0 * P.nb, Lnb, st,
+                                bnd ? P.nbd : 0, P.boundary_ids, fb, ld_f, u, ld_u))
+        return rc;
+      bnd_done = bnd;
     } else if (g && ops.shared_leaf && ops.fd) {
       // tensor-product leaf solve: same [W | H] rows, 5x fewer flops
       if (int rc = leaf_fd(ops, k, nleaf, g, ld_g, ws.W + (long long)leaf0 * nw, sw, st)) return rc;
@@ -259,7 +265,7 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   }
   if (phases & SOLVE_TOP) {
     // (1) Dirichlet data into u (solver.py:259-260); the up sweep never reads u
-    long long n = (long long)k * P.nbd;
+    long long n = bnd_done ? 0 : (long long)k * P.nbd;
     if (n > 0) {
       HPSB_CUDA(launch_pdl(k_bnd_scatter, dim3((unsigned)cdiv(n, T)), dim3(T), 0, st, k, P.nbd, P.boundary_ids,
                            fb, ld_f, u, ld_u));
