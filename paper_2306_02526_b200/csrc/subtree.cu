@@ -47,6 +47,7 @@ struct SubArgs {
   const int* slots; long long slot_off[MAXF + 1]; int j3_base[MAXF]; int nslots;
   const int* gidx_root;                         // level-dF gidx_bnd
   int b0;                                       // first subtree of the launch
+  int fold;                                     // shared one-rhs apply: two nodes per thread
 };
 
 // y(row) = sum_col M[col][row] x[node(row)][col] over the CTA's tile, then
@@ -56,12 +57,101 @@ struct SubArgs {
 // When there are fewer row pairs than threads, G threads share a row pair,
 // each streaming a contiguous column block; their partial sums meet in shared
 // memory (red, 2*NT*KM doubles) and are added in block order.
+// partial-sum space of a CTA (doubles): 2 rows x KM rhs per thread, or 2 rows
+// x 2 nodes per (item, column block) in the shared one-rhs apply
+constexpr int red_doubles(int KM, bool SH) { return SH && KM == 1 ? 4 * NT : 2 * NT * KM; }
+
+// Shared operator, one rhs: a thread owns a row pair of the one-node operator
+// for TWO nodes, so each 16-byte operator load feeds four fmas (the subtree
+// levels are bound by the L1 traffic of the operator loads: every CTA re-reads
+// the level's tile once per node otherwise).  x rows 16-byte aligned.
+__device__ __forceinline__ void stream_pairs2(const double2* __restrict__ M, int cs, int n, const double* xa,
+                                              const double* xb, double (&acc)[4]) {
+  constexpr int SU = 4;
+  const double2* p = M;
+  double2 A[SU], B[SU];
+  auto ld = [&](double2 (&m)[SU]) {
+#pragma unroll
+    for (int u = 0; u < SU; ++u) { m[u] = __ldcs(p); p += cs; }
+  };
+  auto fma4 = [&](const double2 (&m)[SU], int col) {
+#pragma unroll
+    for (int u = 0; u < SU; u += 2) {
+      const double2 va = *reinterpret_cast<const double2*>(xa + col + u);
+      const double2 vb = *reinterpret_cast<const double2*>(xb + col + u);
+      acc[0] = fma(m[u].x, va.x, acc[0]); acc[1] = fma(m[u].y, va.x, acc[1]);
+      acc[2] = fma(m[u].x, vb.x, acc[2]); acc[3] = fma(m[u].y, vb.x, acc[3]);
+      acc[0] = fma(m[u + 1].x, va.y, acc[0]); acc[1] = fma(m[u + 1].y, va.y, acc[1]);
+      acc[2] = fma(m[u + 1].x, vb.y, acc[2]); acc[3] = fma(m[u + 1].y, vb.y, acc[3]);
+    }
+  };
+  const int nfull = n / SU;
+  if (nfull > 0) ld(A);
+  int b = 0;
+  for (; b + 1 < nfull; b += 2) {
+    ld(B);
+    fma4(A, b * SU);
+    if (b + 2 < nfull) ld(A);
+    fma4(B, (b + 1) * SU);
+  }
+  if (b < nfull) fma4(A, b * SU);
+  for (int col = nfull * SU; col < n; ++col) {
+    const double2 m = __ldcs(p);
+    p += cs;
+    acc[0] = fma(m.x, xa[col], acc[0]); acc[1] = fma(m.y, xa[col], acc[1]);
+    acc[2] = fma(m.x, xb[col], acc[2]); acc[3] = fma(m.y, xb[col], acc[3]);
+  }
+}
+
+template <class Out>
+__device__ __forceinline__ void apply_sh2(const double2* base, int R, int C, int cs, const double* xs, int xstride,
+                                          double* red, Out out, int vn) {
+  const int items = cs * ((vn + 1) / 2);
+  int G = 1;
+  while (2 * G * items <= NT && 2 * G * 4 <= C) G *= 2;  // then G * items <= NT: red holds 4 * NT doubles
+  const int CKg = ((C + G - 1) / G + 1) & ~1;
+  const int t = threadIdx.x;
+  for (int q = t % items + (t / items >= G ? NT : 0); q < items; q += (G == 1 ? NT : items)) {
+    const int g = G == 1 ? 0 : t / items;
+    const int c0 = min(C, g * CKg), c1 = min(C, c0 + CKg);
+    const int pr = q % cs, j0 = 2 * (q / cs), j1 = min(j0 + 1, vn - 1);  // node j0 + 1 past vn: results discarded
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    stream_pairs2(base + pr + (size_t)c0 * cs, cs, c1 - c0, xs + j0 * xstride + c0, xs + j1 * xstride + c0, acc);
+    if (G == 1) {
+      if (2 * pr < R) out(j0, 2 * pr, 0, acc[0]);
+      if (2 * pr + 1 < R) out(j0, 2 * pr + 1, 0, acc[1]);
+      if (j0 + 1 < vn) {
+        if (2 * pr < R) out(j0 + 1, 2 * pr, 0, acc[2]);
+        if (2 * pr + 1 < R) out(j0 + 1, 2 * pr + 1, 0, acc[3]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) red[(g * 4 + i) * items + q] = acc[i];
+    }
+  }
+  if (G > 1) {
+    __syncthreads();
+    for (int i = t; i < 4 * items; i += NT) {
+      const int q = i % items, w = i / items, pr = q % cs, node = 2 * (q / cs) + (w >> 1), row = 2 * pr + (w & 1);
+      if (node >= vn || row >= R) continue;
+      double y = 0.0;
+      for (int g = 0; g < G; ++g) y += red[(g * 4 + w) * items + q];
+      out(node, row, 0, y);
+    }
+    __syncthreads();
+  }
+}
+
 template <int KM, bool SH, class Out>
 __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const double* xs, int xstride, double* red,
-                                           Out out, int vn = 1) {
+                                           Out out, int vn = 1, int fold = 0) {
   const int R = pn.R, C = pn.C, TR = pn.TR, TS = pn.TS;
   const double2* base = reinterpret_cast<const double2*>(pn.base + (size_t)tile * C * TS);
   const int cs = TS / 2;          // stored row pairs
+  if constexpr (SH && KM == 1) {  // (one-node levels too: the second node's sums are discarded)
+    apply_sh2(base, R, C, cs, xs, xstride, red, out, vn);
+    return;
+  }
   const int np = cs * vn;         // row pairs to compute
   int G = 1;
   while (2 * G * np <= NT && 2 * G * 4 <= C) G *= 2;
@@ -134,7 +224,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
   double* Hs = sm;                    // children's fluxes of the current level [child][KM][nbc]
   double* Hn = Hs + KM * a.hcap;      // this level's fluxes [node][KM][n12]
   double* r3s = Hn + KM * a.hcap;     // [node][KM][n3]
-  double* red = r3s + KM * a.rcap;    // 2 * NT * KM
+  double* red = r3s + KM * a.rcap;    // red_doubles(KM, SH)
   const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x;
   pdl_trigger();
   pdl_wait();
@@ -169,7 +259,7 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
       const double h = base + y;
       Hn[(j * KM + kk) * n12 + r] = h;
       if (e == 0) a.H_dF[kg * a.H_k + (long long)(node0 + j) * n12 + r] = h;
-    }, L.Up.c == 1 ? npn : 1);
+    }, L.Up.c == 1 ? npn : 1, a.fold);
     __syncthreads();
     if (a.dF + e == 0) break;  // the root's outer flux is never consumed
     double* t = Hs; Hs = Hn; Hn = t;
@@ -179,8 +269,8 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_up(SubArgs a) {
 template <int KM, bool SH = false>
 __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
   extern __shared__ double sm[];
-  double* red = sm;                // 2 * NT * KM
-  double* xs = sm + 2 * NT * KM;   // [node][KM][n12]
+  double* red = sm;                          // red_doubles(KM, SH)
+  double* xs = sm + red_doubles(KM, SH);     // [node][KM][n12]
   const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x;
   pdl_trigger();
   pdl_wait();
@@ -199,7 +289,7 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
       const long long nd = (long long)(node0 + j) * n3 + row;
       if (a.has_w3) y = y + L.W3[kg * L.W3_k + nd];
       a.u[kg * a.u_k + L.j3[nd]] = y;
-    }, L.S.c == 1 ? npn : 1);
+    }, L.S.c == 1 ? npn : 1, a.fold);
   }
 }
 
@@ -209,8 +299,8 @@ __global__ void __launch_bounds__(NT) k_sub_down(SubArgs a) {
 template <int KM, bool SH = false>
 __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_down_local(SubArgs a) {
   extern __shared__ double sm[];
-  double* red = sm;                        // 2 * NT * KM
-  double* uloc = sm + 2 * NT * KM;         // [KM][nslots]
+  double* red = sm;                        // red_doubles(KM, SH)
+  double* uloc = sm + red_doubles(KM, SH); // [KM][nslots]
   double* xs = uloc + ((KM * a.nslots + 1) & ~1);  // [node][KM][n12 rounded up to even]
   const int b = a.b0 + blockIdx.x, kg0 = blockIdx.y * KM, tid = threadIdx.x, ns = a.nslots;
   pdl_trigger();
@@ -239,12 +329,17 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_down_local(SubArgs 
       if (a.has_w3) y = y + L.W3[kg * L.W3_k + nd];
       uloc[kk * ns + jb + j * n3 + row] = y;
       a.u[kg * a.u_k + L.j3[nd]] = y;
-    }, L.S.c == 1 ? npn : 1);
+    }, L.S.c == 1 ? npn : 1, a.fold);
   }
 }
 
 void fill_args(const Ops& ops, const Workspace& ws, int k, SubArgs& a) {
   const Plan& P = *ops.plan;
+  static const int fold = [] {
+    const char* e = getenv("HPSB_NO_SUB_FOLD");
+    return e && e[0] == '1' ? 0 : 1;
+  }();
+  a.fold = fold;
   a.nf = P.depth - P.dF;
   a.dF = P.dF;
   a.k = k;
@@ -338,8 +433,9 @@ int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, 
   a.Hleaf = Hleaf; a.sh = sh; a.hs = hs;
   a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt;
   const int KM = k == 1 ? 1 : 4;
-  const size_t smem = (size_t)KM * (2 * a.hcap + a.rcap + 2 * NT) * 8;
-  if (KM == 1 && shared_sub(a)) return launch_sub(k_sub_up<1, true>, b1 - b0, 1, k, smem, a, st);
+  const bool shm = KM == 1 && shared_sub(a);
+  const size_t smem = (size_t)(KM * (2 * a.hcap + a.rcap) + red_doubles(KM, shm)) * 8;
+  if (shm) return launch_sub(k_sub_up<1, true>, b1 - b0, 1, k, smem, a, st);
   if (KM == 1) return launch_sub(k_sub_up<1>, b1 - b0, 1, k, smem, a, st);
   return launch_sub(k_sub_up<4>, b1 - b0, 4, k, smem, a, st);
 }
@@ -355,16 +451,17 @@ int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double
   const int KM = k == 1 ? 1 : 4;
   int xcap = 0;
   for (int e = 0; e < a.nf; ++e) xcap = std::max(xcap, (1 << e) * ((a.lv[e].n12 + 1) & ~1));
+  const bool shm = KM == 1 && shared_sub(a);
   if (P.sub_local) {
-    const size_t smem = (size_t)(KM * (xcap + 2 * NT) + ((KM * a.nslots + 1) & ~1)) * 8;
+    const size_t smem = (size_t)(KM * xcap + red_doubles(KM, shm) + ((KM * a.nslots + 1) & ~1)) * 8;
     if (smem <= 200 * 1024) {
-      if (KM == 1 && shared_sub(a)) return launch_sub(k_sub_down_local<1, true>, b1 - b0, 1, k, smem, a, st);
+      if (shm) return launch_sub(k_sub_down_local<1, true>, b1 - b0, 1, k, smem, a, st);
       if (KM == 1) return launch_sub(k_sub_down_local<1>, b1 - b0, 1, k, smem, a, st);
       return launch_sub(k_sub_down_local<4>, b1 - b0, 4, k, smem, a, st);
     }
   }
-  const size_t smem = (size_t)KM * (xcap + 2 * NT) * 8;
-  if (KM == 1 && shared_sub(a)) return launch_sub(k_sub_down<1, true>, b1 - b0, 1, k, smem, a, st);
+  const size_t smem = (size_t)(KM * xcap + red_doubles(KM, shm)) * 8;
+  if (shm) return launch_sub(k_sub_down<1, true>, b1 - b0, 1, k, smem, a, st);
   if (KM == 1) return launch_sub(k_sub_down<1>, b1 - b0, 1, k, smem, a, st);
   return launch_sub(k_sub_down<4>, b1 - b0, 4, k, smem, a, st);
 }
