@@ -57,33 +57,44 @@ struct SubArgs {
 // When there are fewer row pairs than threads, G threads share a row pair,
 // each streaming a contiguous column block; their partial sums meet in shared
 // memory (red, 2*NT*KM doubles) and are added in block order.
+// nodes per thread of the shared one-rhs apply
+#ifndef HPSB_SUB_NODES
+#define HPSB_SUB_NODES 2
+#endif
+constexpr int SNF = HPSB_SUB_NODES;
+
 // partial-sum space of a CTA (doubles): 2 rows x KM rhs per thread, or 2 rows
-// x 2 nodes per (item, column block) in the shared one-rhs apply
-constexpr int red_doubles(int KM, bool SH) { return SH && KM == 1 ? 4 * NT : 2 * NT * KM; }
+// x SNF nodes per (item, column block) in the shared one-rhs apply
+constexpr int red_doubles(int KM, bool SH) { return SH && KM == 1 ? 2 * SNF * NT : 2 * NT * KM; }
 
 // Shared operator, one rhs: a thread owns a row pair of the one-node operator
-// for TWO nodes, so each 16-byte operator load feeds four fmas (the subtree
+// for SNF nodes, so each 16-byte operator load feeds 2 SNF fmas (the subtree
 // levels are bound by the L1 traffic of the operator loads: every CTA re-reads
 // the level's tile once per node otherwise).  x rows 16-byte aligned.
-__device__ __forceinline__ void stream_pairs2(const double2* __restrict__ M, int cs, int n, const double* xa,
-                                              const double* xb, double (&acc)[4]) {
+template <int NF>
+__device__ __forceinline__ void stream_nodes(const double2* __restrict__ M, int cs, int n, const double* x, int XS,
+                                             int nv, double (&acc)[2 * NF]) {
   constexpr int SU = 4;
   const double2* p = M;
   double2 A[SU], B[SU];
+  int xo[NF];  // node j's x row (nodes past nv read node nv - 1; their sums are discarded)
+#pragma unroll
+  for (int j = 0; j < NF; ++j) xo[j] = min(j, nv - 1) * XS;
   auto ld = [&](double2 (&m)[SU]) {
 #pragma unroll
     for (int u = 0; u < SU; ++u) { m[u] = __ldcs(p); p += cs; }
   };
   auto fma4 = [&](const double2 (&m)[SU], int col) {
 #pragma unroll
-    for (int u = 0; u < SU; u += 2) {
-      const double2 va = *reinterpret_cast<const double2*>(xa + col + u);
-      const double2 vb = *reinterpret_cast<const double2*>(xb + col + u);
-      acc[0] = fma(m[u].x, va.x, acc[0]); acc[1] = fma(m[u].y, va.x, acc[1]);
-      acc[2] = fma(m[u].x, vb.x, acc[2]); acc[3] = fma(m[u].y, vb.x, acc[3]);
-      acc[0] = fma(m[u + 1].x, va.y, acc[0]); acc[1] = fma(m[u + 1].y, va.y, acc[1]);
-      acc[2] = fma(m[u + 1].x, vb.y, acc[2]); acc[3] = fma(m[u + 1].y, vb.y, acc[3]);
-    }
+    for (int u = 0; u < SU; u += 2)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(x + xo[j] + col + u);
+        acc[2 * j] = fma(m[u].x, v.x, acc[2 * j]);
+        acc[2 * j + 1] = fma(m[u].y, v.x, acc[2 * j + 1]);
+        acc[2 * j] = fma(m[u + 1].x, v.y, acc[2 * j]);
+        acc[2 * j + 1] = fma(m[u + 1].y, v.y, acc[2 * j + 1]);
+      }
   };
   const int nfull = n / SU;
   if (nfull > 0) ld(A);
@@ -98,44 +109,49 @@ __device__ __forceinline__ void stream_pairs2(const double2* __restrict__ M, int
   for (int col = nfull * SU; col < n; ++col) {
     const double2 m = __ldcs(p);
     p += cs;
-    acc[0] = fma(m.x, xa[col], acc[0]); acc[1] = fma(m.y, xa[col], acc[1]);
-    acc[2] = fma(m.x, xb[col], acc[2]); acc[3] = fma(m.y, xb[col], acc[3]);
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      acc[2 * j] = fma(m.x, x[xo[j] + col], acc[2 * j]);
+      acc[2 * j + 1] = fma(m.y, x[xo[j] + col], acc[2 * j + 1]);
+    }
   }
 }
 
 template <class Out>
-__device__ __forceinline__ void apply_sh2(const double2* base, int R, int C, int cs, const double* xs, int xstride,
-                                          double* red, Out out, int vn) {
-  const int items = cs * ((vn + 1) / 2);
+__device__ __forceinline__ void apply_shared(const double2* base, int R, int C, int cs, const double* xs,
+                                             int xstride, double* red, Out out, int vn) {
+  const int items = cs * ((vn + SNF - 1) / SNF);
   int G = 1;
-  while (2 * G * items <= NT && 2 * G * 4 <= C) G *= 2;  // then G * items <= NT: red holds 4 * NT doubles
+  while (2 * G * items <= NT && 2 * G * 4 <= C) G *= 2;  // then G * items <= NT
   const int CKg = ((C + G - 1) / G + 1) & ~1;
   const int t = threadIdx.x;
   for (int q = t % items + (t / items >= G ? NT : 0); q < items; q += (G == 1 ? NT : items)) {
     const int g = G == 1 ? 0 : t / items;
     const int c0 = min(C, g * CKg), c1 = min(C, c0 + CKg);
-    const int pr = q % cs, j0 = 2 * (q / cs), j1 = min(j0 + 1, vn - 1);  // node j0 + 1 past vn: results discarded
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    stream_pairs2(base + pr + (size_t)c0 * cs, cs, c1 - c0, xs + j0 * xstride + c0, xs + j1 * xstride + c0, acc);
+    const int pr = q % cs, j0 = SNF * (q / cs);
+    double acc[2 * SNF];
+#pragma unroll
+    for (int i = 0; i < 2 * SNF; ++i) acc[i] = 0.0;
+    stream_nodes<SNF>(base + pr + (size_t)c0 * cs, cs, c1 - c0, xs + j0 * xstride + c0, xstride, vn - j0, acc);
     if (G == 1) {
-      if (2 * pr < R) out(j0, 2 * pr, 0, acc[0]);
-      if (2 * pr + 1 < R) out(j0, 2 * pr + 1, 0, acc[1]);
-      if (j0 + 1 < vn) {
-        if (2 * pr < R) out(j0 + 1, 2 * pr, 0, acc[2]);
-        if (2 * pr + 1 < R) out(j0 + 1, 2 * pr + 1, 0, acc[3]);
+#pragma unroll
+      for (int j = 0; j < SNF; ++j) {
+        if (j0 + j >= vn) break;
+        if (2 * pr < R) out(j0 + j, 2 * pr, 0, acc[2 * j]);
+        if (2 * pr + 1 < R) out(j0 + j, 2 * pr + 1, 0, acc[2 * j + 1]);
       }
     } else {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) red[(g * 4 + i) * items + q] = acc[i];
+      for (int i = 0; i < 2 * SNF; ++i) red[(g * 2 * SNF + i) * items + q] = acc[i];
     }
   }
   if (G > 1) {
     __syncthreads();
-    for (int i = t; i < 4 * items; i += NT) {
-      const int q = i % items, w = i / items, pr = q % cs, node = 2 * (q / cs) + (w >> 1), row = 2 * pr + (w & 1);
+    for (int i = t; i < 2 * SNF * items; i += NT) {
+      const int q = i % items, w = i / items, pr = q % cs, node = SNF * (q / cs) + (w >> 1), row = 2 * pr + (w & 1);
       if (node >= vn || row >= R) continue;
       double y = 0.0;
-      for (int g = 0; g < G; ++g) y += red[(g * 4 + w) * items + q];
+      for (int g = 0; g < G; ++g) y += red[(g * 2 * SNF + w) * items + q];
       out(node, row, 0, y);
     }
     __syncthreads();
@@ -149,7 +165,7 @@ __device__ __forceinline__ void tile_apply(const Panel& pn, int tile, const doub
   const double2* base = reinterpret_cast<const double2*>(pn.base + (size_t)tile * C * TS);
   const int cs = TS / 2;          // stored row pairs
   if constexpr (SH && KM == 1) {  // (one-node levels too: the second node's sums are discarded)
-    apply_sh2(base, R, C, cs, xs, xstride, red, out, vn);
+    apply_shared(base, R, C, cs, xs, xstride, red, out, vn);
     return;
   }
   const int np = cs * vn;         // row pairs to compute
