@@ -215,6 +215,18 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   const int gr = lane >> 2, gc = lane & 3;
   pdl_trigger();
   const double* E = cst;
+  // FD_UP_H: the first two products' constant fragments in registers (the
+  // kernel is bound by shared-memory traffic; it has registers to spare)
+  double rVxi[2][KS], rVyit[2][KS];
+  if (MODE == FD_UP_H) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        rVxi[i][k] = cVxi[(i * 8 + gr) * CSA + k * 4 + gc];
+        rVyit[i][k] = cVyit[(k * 4 + gc) * CSB + i * 8 + gr];
+      }
+  }
   const double* Bc = cst + 4 * Q;
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
   __syncthreads();
@@ -310,7 +322,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
-        const double am = cVxi[(mi * 8 + gr) * CSA + k * 4 + gc];
+        const double am = MODE == FD_UP_H ? rVxi[mi][k] : cVxi[(mi * 8 + gr) * CSA + k * 4 + gc];
         dmma(acc[mi][0][0], acc[mi][0][1], am, b0);
         dmma(acc[mi][1][0], acc[mi][1][1], am, b1);
       }
@@ -324,7 +336,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) {
-        const double bm = cVyit[(k * 4 + gc) * CSB + nj * 8 + gr];
+        const double bm = MODE == FD_UP_H ? rVyit[nj][k] : cVyit[(k * 4 + gc) * CSB + nj * 8 + gr];
         dmma(acc[0][nj][0], acc[0][nj][1], a0, bm);
         dmma(acc[1][nj][0], acc[1][nj][1], a1, bm);
       }
