@@ -160,10 +160,23 @@ int hps_solve(const hps_ops* ops, int k, const double* fb, long long ld_f, const
  * (timestep.py:198-203), computed by the leaf kernel of the downward sweep
  * while the leaf's grid is on chip.  Constant coefficients with the
  * tensor-product leaf solve only (HPS_ERR_ARG otherwise: use hps_solve +
- * hps_leaf_eval).  lu_int may be NULL (the last stage: solve + guard only). */
+ * hps_leaf_eval).  lu_int may be NULL (the last stage: solve + guard only).
+ * root_pre (k = 1, may be NULL): this solve's root Dirichlet product from
+ * hps_root_dirichlet. */
 int hps_solve_stage(const hps_ops* ops, int k, const double* fb, long long ld_f, const double* g,
                     long long ld_g, double* u, long long ld_u, double* lu_int, long long ld_lu,
-                    double* guard, void* ws, size_t ws_bytes, void* stream);
+                    double* guard, const double* root_pre, void* ws, size_t ws_bytes, void* stream);
+
+/* The root's Dirichlet product S_root u_bnd (solver.py:262-265 at the root,
+ * whose boundary is the domain boundary) for ns <= 8 rows of boundary data
+ * fb (nbd values each, row stride ld_f) in one pass over the root operator:
+ * out[s * ld_out + r], r < n3 of the root.  A step computes it once for all of
+ * its stage times and passes row s to hps_solve_stage as root_pre (k = 1), so
+ * the per-stage solves skip the root's down product.  scratch holds
+ * hps_root_dirichlet_scratch(ops, ns) bytes. */
+size_t hps_root_dirichlet_scratch(const hps_ops* ops, int ns);
+int hps_root_dirichlet(const hps_ops* ops, int ns, const double* fb, long long ld_f, double* out,
+                       long long ld_out, void* scratch, size_t scratch_bytes, void* stream);
 
 /* Stage history of an explicit stage (timestep.py:259-261, the first ARK
  * stage's L u_n): lu_int = L u at the interiors of leaves [leaf0, leaf0 +

@@ -201,6 +201,19 @@ int hps_plan_create(const hps_plan_desc* d, hps_plan** out) {
   }
   up(d->leaf_bnd_gidx, (size_t)P.L * P.nb, &P.leaf_bnd_gidx);
   up(d->boundary_ids, (size_t)P.nbd, &P.boundary_ids);
+  if (P.depth > 0 && P.nbd > 0) {  // the root's boundary is the domain boundary: its position in fb order
+    std::unordered_map<int, int> pos;
+    for (int i = 0; i < P.nbd; ++i) pos[d->boundary_ids[i]] = i;
+    const int n12 = P.lv[0].n12;
+    std::vector<int> bp(n12, -1);
+    bool all = true;
+    for (int c = 0; c < n12 && all; ++c) {
+      auto it = pos.find(d->lvl_gidx_bnd[0][c]);
+      if (it == pos.end()) all = false;
+      else bp[c] = it->second;
+    }
+    if (all) up(bp.data(), (size_t)n12, &P.root_bpos);
+  }
   P.leaf_node_index.assign(d->leaf_node_index, d->leaf_node_index + P.L);
   if (rc) { hps_plan_destroy(h); return rc; }
   *out = h;
@@ -566,16 +579,30 @@ int hps_solve(const hps_ops* h, int k, const double* fb, long long ld_f, const d
 }
 
 int hps_solve_stage(const hps_ops* h, int k, const double* fb, long long ld_f, const double* g, long long ld_g,
-                    double* u, long long ld_u, double* lu_int, long long ld_lu, double* guard, void* ws,
-                    size_t ws_bytes, void* stream) {
+                    double* u, long long ld_u, double* lu_int, long long ld_lu, double* guard,
+                    const double* root_pre, void* ws, size_t ws_bytes, void* stream) {
   if (!h || !fb || !u || !ws) { set_error("hps_solve_stage: null argument"); return HPS_ERR_ARG; }
   const Ops& O = h->O;
   if (!(O.shared_leaf && O.fd && leaf_fd_down_enabled())) {
     set_error("hps_solve_stage: needs the tensor-product leaf solve (constant coefficients)");
     return HPS_ERR_ARG;
   }
+  if (root_pre && k != 1) { set_error("hps_solve_stage: root_pre needs k = 1"); return HPS_ERR_ARG; }
   return solve(O, SOLVE_ALL, 0, O.plan->nparts, k, fb, ld_f, g, ld_g, nullptr, 0, 0.0, u, ld_u, ws, ws_bytes,
-               (cudaStream_t)stream, lu_int, ld_lu, guard);
+               (cudaStream_t)stream, lu_int, ld_lu, guard, root_pre);
+}
+
+size_t hps_root_dirichlet_scratch(const hps_ops* h, int ns) { return h ? root_dirichlet_scratch(*h->O.plan, ns) : 0; }
+
+int hps_root_dirichlet(const hps_ops* h, int ns, const double* fb, long long ld_f, double* out, long long ld_out,
+                       void* scratch, size_t scratch_bytes, void* stream) {
+  if (!h || !fb || !out || !scratch) { set_error("hps_root_dirichlet: null argument"); return HPS_ERR_ARG; }
+  if (scratch_bytes < root_dirichlet_scratch(*h->O.plan, ns)) {
+    set_error("hps_root_dirichlet: scratch too small");
+    return HPS_ERR_ARG;
+  }
+  if (root_dirichlet(h->O, ns, fb, ld_f, out, ld_out, (double*)scratch, (cudaStream_t)stream)) return HPS_ERR_ARG;
+  return HPS_OK;
 }
 
 int hps_leaf_lu(const hps_ops* h, int leaf0, int nleaf, int k, const double* u, long long ld_u, double* lu_int,

@@ -33,6 +33,7 @@ struct Plan {
   std::vector<Level> lv;          // depth entries, root first
   int* leaf_bnd_gidx = nullptr;   // device L x nb
   int* boundary_ids = nullptr;    // device nbd
+  int* root_bpos = nullptr;       // device lv[0].n12: fb position of each root boundary DOF (null: not all on the boundary)
   std::vector<long long> leaf_node_index;  // host
   int dF = 0;                     // levels d >= dF run as fused subtree kernels
   // subtree-local numbering of the DOFs a fused subtree touches (the same for
@@ -232,9 +233,16 @@ int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u
 bool mega_enabled();
 int mega_depth(const Ops& ops);  // levels [0, mega_depth) are eligible
 void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles);
+// root_pre: the root's Dirichlet product S u_bnd of this solve, precomputed
+// (root_dirichlet); the launch then has no root down tasks
 int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int d1, int part0, int part1,
                 const double* Hleaf, long long hs, const double* jump, double inv_dt, bool has_w3, double* u,
-                cudaStream_t st);
+                cudaStream_t st, const double* root_pre = nullptr);
+// S_root u_bnd for ns (<= 8) rows of boundary data (fb order), streaming the
+// root's down operator once for all of them (mega.cu); scratch >= root_dirichlet_scratch
+size_t root_dirichlet_scratch(const Plan& P, int ns);
+int root_dirichlet(const Ops& ops, int ns, const double* fb, long long ld_f, double* out, long long ld_out,
+                   double* scratch, cudaStream_t st);
 
 // solve entry (solve.cu).  phases: SOLVE_UP (leaves + levels >= lstar of parts
 // [part0, part1)), SOLVE_TOP (Dirichlet data, levels < lstar up and down),
@@ -244,7 +252,7 @@ enum SolvePhase { SOLVE_UP = 1, SOLVE_TOP = 2, SOLVE_DOWN = 4, SOLVE_ALL = 7 };
 int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
           const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
           long long ld_u, void* ws, size_t ws_bytes, cudaStream_t st, double* lu = nullptr, long long ld_lu = 0,
-          double* guard = nullptr);
+          double* guard = nullptr, const double* root_pre = nullptr);
 // byte offset of level lstar's flux block (k x nparts x n12) in a workspace
 size_t exchange_offset(const Plan& P, int k);
 

@@ -68,6 +68,9 @@ struct MSeg {
   // partial sets (down splits first, then up splits)
   int pair;
   const double *pdn, *pup; int Sdn, Sup;
+  // the root's up segment with the Dirichlet product S u_bnd precomputed for
+  // this solve (hps_root_dirichlet): the emitting task also writes u3 = w3 + pre
+  const double* rootpre;
 };
 
 struct MProg {
@@ -330,6 +333,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
         if (g.up) {
           if (orow < g.n3) {
             g.W3[(long long)node * g.n3 + orow] = y;
+            if (g.rootpre) g.u[g.j3[orow]] = y + g.rootpre[orow];
           } else {
             g.Hout[(long long)node * g.n12 + orow - g.n3] = oadd + y;
           }
@@ -366,6 +370,123 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
 }
 
 }  // namespace
+
+// ---- the root's Dirichlet product for several solves at once
+// Y[s][r] = sum_c S_root[r][c] fb_s[bpos[c]], s < ns <= RDN: the root's down
+// operator (the largest of the solve) streamed once per step instead of once
+// per stage solve.  Task = (64-row block, 256-column split): 8 column groups x
+// 32 lanes x two rows, ns accumulators per row; split partials summed in split
+// order by k_root_sum (bitwise reproducible).
+constexpr int RDN = 8;
+constexpr int RDK = 512;
+
+__global__ void __launch_bounds__(MT) k_root_dir(const double* __restrict__ S, int R, int C, int TR,
+                                                 const int* __restrict__ bpos, const double* __restrict__ fb,
+                                                 long long ld_f, int ns, double* __restrict__ part) {
+  static_assert(MGRP * MRB <= RDK, "the group sums reuse the x buffer");
+  __shared__ __align__(16) double buf[RDN * RDK];
+  double (*xs)[RDK] = reinterpret_cast<double (*)[RDK]>(buf);           // inputs, then ...
+  double (*red)[RDN][MRB] = reinterpret_cast<double (*)[RDN][MRB]>(buf);  // ... the group sums
+  const int rb = blockIdx.x, split = blockIdx.y, tid = threadIdx.x, grp = tid >> 5, q = tid & 31;
+  const int c0 = split * RDK, cw = min(RDK, C - c0);
+  for (int i = tid; i < ns * cw; i += MT) {
+    const int s = i / cw, c = i - s * cw;
+    xs[s][c] = fb[s * ld_f + bpos[c0 + c]];
+  }
+  __syncthreads();
+  const int cg = ((cw + MGRP - 1) / MGRP + 1) & ~1, a0 = min(cw, grp * cg), a1 = min(cw, a0 + cg);
+  const int row = rb * MRB + 2 * q, rowc = min(row, R - 2);
+  const double2* M = reinterpret_cast<const double2*>(S + (size_t)(rowc / TR) * C * TR + rowc % TR) +
+                     (size_t)(c0 + a0) * (TR / 2);
+  double acc0[RDN], acc1[RDN];
+#pragma unroll
+  for (int j = 0; j < RDN; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; }
+  if (row < R) {
+    int c = a0;
+    for (; c + 4 <= a1; c += 4) {  // four column loads in flight
+      double2 m[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { m[u] = __ldcs(M); M += TR / 2; }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int j = 0; j < RDN; ++j) {
+          if (j < ns) {
+            acc0[j] = fma(m[u].x, xs[j][c + u], acc0[j]);
+            acc1[j] = fma(m[u].y, xs[j][c + u], acc1[j]);
+          }
+        }
+    }
+    for (; c < a1; ++c) {
+      const double2 m = __ldcs(M);
+      M += TR / 2;
+#pragma unroll
+      for (int j = 0; j < RDN; ++j) {
+        if (j < ns) {
+          acc0[j] = fma(m.x, xs[j][c], acc0[j]);
+          acc1[j] = fma(m.y, xs[j][c], acc1[j]);
+        }
+      }
+    }
+  }
+  __syncthreads();  // every x read is done: the buffer takes the group sums
+#pragma unroll
+  for (int j = 0; j < RDN; ++j) {
+    red[grp][j][2 * q] = acc0[j];
+    red[grp][j][2 * q + 1] = acc1[j];
+  }
+  __syncthreads();
+  for (int i = tid; i < ns * MRB; i += MT) {
+    const int j = i / MRB, r = i - j * MRB;
+    double y = 0.0;
+#pragma unroll
+    for (int gg = 0; gg < MGRP; ++gg) y += red[gg][j][r];
+    if (rb * MRB + r < R) part[((size_t)split * ns + j) * R + rb * MRB + r] = y;
+  }
+}
+
+__global__ void k_root_sum(const double* __restrict__ part, int nsplit, int ns, int R, double* __restrict__ out,
+                           long long ld_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ns * R) return;
+  const int j = i / R, r = i - j * R;
+  double y = 0.0;
+  for (int s0 = 0; s0 < nsplit; s0 += 8) {  // eight loads in flight, summed in split order
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = s0 + u < nsplit ? part[((size_t)(s0 + u) * ns + j) * R + r] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (s0 + u < nsplit) y += v[u];
+  }
+  out[j * ld_out + r] = y;
+}
+
+size_t root_dirichlet_scratch(const Plan& P, int ns) {
+  if (P.depth == 0) return 0;
+  return (size_t)((P.lv[0].n12 + RDK - 1) / RDK) * ns * P.lv[0].n3 * 8;
+}
+
+int root_dirichlet(const Ops& ops, int ns, const double* fb, long long ld_f, double* out, long long ld_out,
+                   double* scratch, cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  if (P.depth == 0 || !P.root_bpos || ns <= 0 || ns > RDN) {
+    set_error("root_dirichlet: not available (depth %d, %d rows)", P.depth, ns);
+    return -1;
+  }
+  const Panel& pn = ops.lo[0].S;
+  if (!pn.base || pn.TS != pn.TR || (pn.TR & 1) || pn.R != P.lv[0].n3 || pn.C != P.lv[0].n12) {
+    set_error("root_dirichlet: unexpected root operator layout");
+    return -1;
+  }
+  const int R = pn.R, C = pn.C, nsplit = (C + RDK - 1) / RDK;
+  k_root_dir<<<dim3((unsigned)cdiv(R, MRB), (unsigned)nsplit), MT, 0, st>>>(pn.base, R, C, pn.TR, P.root_bpos, fb,
+                                                                         ld_f, ns, scratch);
+  HPSB_LAUNCH_CHECK();
+  k_root_sum<<<(unsigned)cdiv((long long)ns * R, 256), 256, 0, st>>>(scratch, nsplit, ns, R, out, ld_out);
+  HPSB_LAUNCH_CHECK();
+  return 0;
+}
 
 static bool pair_enabled() {
   static const bool on = [] {
@@ -444,9 +565,12 @@ void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles) {
 // levels are not eligible (caller falls back to per-level launches).
 int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int d1, int part0, int part1,
                 const double* Hleaf, long long hs, const double* jump, double inv_dt, bool has_w3, double* u,
-                cudaStream_t st) {
+                cudaStream_t st, const double* root_pre) {
   const Plan& P = *ops.plan;
   if (!mega_enabled() || !ws.mega_cnt) return 1;
+  // root_pre: the root's down product is precomputed, so the root's up tasks
+  // write its interface and level 1's down tasks wait on them (no root pair)
+  const bool rpre = root_pre && u0 == 0 && u1 > 0 && d0 == 0 && d1 > 0 && has_w3 && !jump;
   const bool pnm = !ops.shared_levels;  // per-node operators
   MProg p{};
   // counter carve: [exit][per level: up nodes, down nodes][sems...]
@@ -500,9 +624,10 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
       g.Rc = child_here ? Rc : 0;
     } else {
       const bool par_here = d - 1 >= d0 && d > 0;
-      g.wpar = par_here ? ddn[d - 1] : nullptr;
+      const bool from_up = rpre && d == 1;  // the root's interface comes from its up tasks
+      g.wpar = par_here ? (from_up ? dup[0] : ddn[d - 1]) : nullptr;
       int RBp = 0, x1, x2, x3, x4 = 0, x5;
-      if (par_here) mega_dims(P.lv[d - 1], d - 1 == 0, false, 1, RBp, x1, x2, x3, x4, x5);
+      if (par_here) mega_dims(P.lv[d - 1], d - 1 == 0, from_up, 1, RBp, x1, x2, x3, x4, x5);
       g.wpar_t = RBp;
       g.Rp = par_here ? x4 : 0;
       const bool up_here = d >= u0 && d < u1;
@@ -516,7 +641,7 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     return true;
   };
   // the root pair: the root's down product first (no inputs from this launch)
-  const bool pair = u0 == 0 && u1 > 0 && d0 == 0 && d1 > 0 && has_w3 && !jump && pair_enabled();
+  const bool pair = !rpre && u0 == 0 && u1 > 0 && d0 == 0 && d1 > 0 && has_w3 && !jump && pair_enabled();
   int iroot_dn = -1;
   if (pair) {
     iroot_dn = p.nseg;
@@ -524,7 +649,10 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   }
   for (int d = u1 - 1; d >= u0; --d)
     if (!add(d, true)) return 1;
-  for (int d = pair ? 1 : d0; d < d1; ++d)
+  if (rpre)
+    for (int i = 0; i < p.nseg; ++i)
+      if (p.s[i].up && p.s[i].Hout == nullptr) p.s[i].rootpre = root_pre;  // the root's up segment
+  for (int d = (pair || rpre) ? 1 : d0; d < d1; ++d)
     if (!add(d, false)) return 1;
   if (pair) {
     MSeg& dn = p.s[iroot_dn];

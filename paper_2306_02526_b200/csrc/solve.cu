@@ -175,7 +175,7 @@ size_t exchange_offset(const Plan& P, int k) {
 int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
           const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
           long long ld_u, void* wsp, size_t ws_bytes, cudaStream_t st, double* lu, long long ld_lu,
-          double* guard) {
+          double* guard, const double* root_pre) {
   const Plan& P = *ops.plan;
   if (k <= 0) return 0;
   if (ws_bytes < workspace_bytes(P, k)) {
@@ -301,7 +301,7 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   int rc_mega = 1;
   if (mu1 > uA || md1 > dA)
     rc_mega = mega_levels(ops, ws, uA, std::max(uA, mu1), dA, std::max(dA, md1), part0, part1, Hleaf, hs, jump,
-                          inv_dt, up, u, st);
+                          inv_dt, up, u, st, root_pre);
   if (rc_mega < 0) return rc_mega;
   if (rc_mega == 1) {
     if (int rc = ups(std::max(uA, mu1), uA)) return rc;

@@ -341,8 +341,11 @@ class ShardedTimeStepper(TimeStepper):
     def _eval_lu(self, U, out, guard=None):
         self._eval(U, lu_int=out, guard=guard, leaves=self._leaves)
 
-    def _fused_stage(self, fb, body, out, lu, guard):
+    def _fused_stage(self, fb, body, out, lu, guard, root_pre=None):
         return False                      # the sharded solve runs in phases with an exchange
+
+    def _root_batch(self):
+        return False
 
     def _ranges(self):
         return (self._ir, self._edges)

@@ -306,7 +306,7 @@ class HpsOperatorSet:
         return self.leaf_solve == "tensor" and os.environ.get("HPSB_NO_FUSED_LU") != "1" \
             and os.environ.get("HPSB_NO_FD_DOWN") is None and os.environ.get("HPSB_FD_SIMT") is None
 
-    def solve_stage_device(self, fb, body, out, lu, guard):
+    def solve_stage_device(self, fb, body, out, lu, guard, root_pre=None):
         """``solve_device`` plus the interior L u of the solution into ``lu``
         (k, >= L*ni) and max |u| into ``guard`` (hps_solve_stage)."""
         k = out.shape[0]
@@ -316,8 +316,28 @@ class HpsOperatorSet:
         rc = self._lib.hps_solve_stage(
             self.handle, k, fb.data_ptr(), ld_f, None if body is None else body.data_ptr(), ld_g,
             out.data_ptr(), out.stride(0), None if lu is None else lu.data_ptr(), 0 if lu is None else lu.stride(0),
-            None if guard is None else guard.data_ptr(), ws.data_ptr(), ws.numel(), current_stream_handle())
+            None if guard is None else guard.data_ptr(), None if root_pre is None else root_pre.data_ptr(),
+            ws.data_ptr(), ws.numel(), current_stream_handle())
         _lib.check(rc, "hps_solve_stage")
+        return out
+
+    @property
+    def root_dirichlet_ok(self):
+        """Whether the root's Dirichlet product can be batched over a step's
+        stages (hps_root_dirichlet: the root boundary is the domain boundary)."""
+        return self.tree.depth > 0 and self.plan.nparts == 1 and \
+            os.environ.get("HPSB_NO_ROOT_BATCH") != "1"
+
+    def root_dirichlet_device(self, fb_rows, out):
+        """S_root u_bnd for each row of boundary data (ns <= 8 rows, fb order)
+        into out (ns, n3_root): one pass over the root operator (hps_root_dirichlet)."""
+        ns = fb_rows.shape[0]
+        nbytes = self._lib.hps_root_dirichlet_scratch(self.handle, ns)
+        scratch = torch.empty(max(1, (nbytes + 7) // 8), dtype=torch.float64, device=out.device)
+        rc = self._lib.hps_root_dirichlet(self.handle, ns, fb_rows.data_ptr(), fb_rows.stride(0), out.data_ptr(),
+                                          out.stride(0), scratch.data_ptr(), scratch.numel() * 8,
+                                          current_stream_handle())
+        _lib.check(rc, "hps_root_dirichlet")
         return out
 
     def leaf_lu_device(self, u, lu, guard=None, leaves=None):

@@ -822,13 +822,16 @@ class TimeStepper:
         a = self._ir[0]
         return v if a == 0 else v[:, a:]
 
-    def _fused_stage(self, fb, body, out, lu, guard):
+    def _root_batch(self):
+        return self.ops.fuses_stage_history and self.ops.root_dirichlet_ok and self.solve_timer is None
+
+    def _fused_stage(self, fb, body, out, lu, guard, root_pre=None):
         """Stage solve with the history L u and the guard from the leaf kernel
         of the downward sweep (hps_solve_stage); False when not available."""
         if not self.ops.fuses_stage_history or self.solve_timer is not None:
             return False
         if not self._dry:
-            self.ops.solve_stage_device(fb, body, out, lu, guard)
+            self.ops.solve_stage_device(fb, body, out, lu, guard, root_pre=root_pre)
         return True
 
     def _eval_lu(self, U, out, guard=None):
@@ -925,6 +928,13 @@ class TimeStepper:
         bcs = self._F.values([t + pair.c[i] * dt for i in range(1, s)] + [t + dt]) \
             if self._bc_batch else None
         bc_at = lambda i, ti: self._bc(ti) if bcs is None else bcs[i - 1:i]
+        # the root's Dirichlet product of every stage solve in one pass over the
+        # root operator (k = 1; the fused stage solves then skip it)
+        rpre = None
+        if bcs is not None and k == 1 and s > 1 and self._root_batch():
+            rpre = self._buf("rootpre", (s - 1, self.tree.level_maps[0].n3))
+            if not self._dry:
+                self.ops.root_dirichlet_device(bcs[:s - 1], rpre)
         self._eval_lu(u, Lu[0])
         stage_q_g(0, t + pair.c[0] * dt, u)
         ui = u
@@ -941,7 +951,8 @@ class TimeStepper:
             ui = U[i & 1]
             bc = bc_at(i, ti)
             # solve + history L u_i (not needed after the last stage) + guard in one pass
-            if not self._fused_stage(bc, r, ui, Lu[i] if i < s - 1 else None, guards[i - 1]):
+            if not self._fused_stage(bc, r, ui, Lu[i] if i < s - 1 else None, guards[i - 1],
+                                     None if rpre is None else rpre[i - 1:i]):
                 self._solve(self.ops, bc, r, ui)
                 if i < s - 1:
                     self._eval_lu(ui, Lu[i], guard=guards[i - 1])

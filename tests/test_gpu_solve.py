@@ -189,6 +189,36 @@ def test_leaf_lu_matches_leaf_eval(p):
     assert torch.all(lu3[:, :a] == 7.0) and torch.all(lu3[:, b:] == 7.0)
 
 
+@pytest.mark.parametrize("n", [8, 32])
+def test_root_dirichlet_product_in_stage_solve(n):
+    """The root's Dirichlet product batched over several boundary-data rows
+    (hps_root_dirichlet) and handed to the fused stage solve (root_pre) gives
+    the solve without it (round-off: the root's sums are grouped differently)."""
+    import torch
+    import paper_2306_02526_b200 as hb
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), n, n, 16)
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0))
+    ops = hb.HpsOperatorSet(disc, sigma=1.0, dt_gamma=2.5e-4, layout="shared")
+    assert ops.root_dirichlet_ok
+    rng = np.random.default_rng(7 + n)
+    fb = torch.as_tensor(rng.standard_normal((3, tree.boundary_ids.size)), device="cuda")
+    body = torch.as_tensor(rng.standard_normal((1, tree.N)), device="cuda")
+    rp = torch.empty((3, tree.level_maps[0].n3), dtype=torch.float64, device="cuda")
+    ops.root_dirichlet_device(fb, rp)
+    for s_ in range(3):
+        u1 = torch.zeros((1, tree.N), dtype=torch.float64, device="cuda")
+        u2 = torch.zeros_like(u1)
+        lu1 = torch.empty((1, tree.L * tree.ni), dtype=torch.float64, device="cuda")
+        lu2 = torch.empty_like(lu1)
+        g1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        g2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ops.solve_stage_device(fb[s_:s_ + 1], body, u1, lu1, g1, root_pre=rp[s_:s_ + 1])
+        ops.solve_stage_device(fb[s_:s_ + 1], body, u2, lu2, g2)
+        assert rel_l2(u1.cpu().numpy(), u2.cpu().numpy()) < 1e-14
+        assert rel_l2(lu1.cpu().numpy(), lu2.cpu().numpy()) < 1e-12
+        assert abs(g1.item() - g2.item()) <= 1e-13 * g2.item()
+
+
 def test_timing_harness_rows(tmp_path):
     """run_timing (drivers.py:160-204) on the device: one row per size with
     the reference's columns, build and median solve times, CSV written."""

@@ -59,8 +59,8 @@ def test_c1_heat_matches_reference(golden, separable, layout, monkeypatch):
 
     orig_stage = st.ops.solve_stage_device
 
-    def rec_stage(fb, body, out, lu, guard):
-        r = orig_stage(fb, body, out, lu, guard)
+    def rec_stage(fb, body, out, lu, guard, **kw):
+        r = orig_stage(fb, body, out, lu, guard, **kw)
         stages.append(out[0].cpu().numpy().copy())
         return r
 
