@@ -708,58 +708,62 @@ class TimeStepper:
             ev = torch.cuda.Event()
             ev.record()
             return ev
-        G = self._graph
-        if G is None or G["key"] != self._graph_key(uin):
-            self._run_graph(StepperState(t, uin.to(self._dev)), 1, 1)   # capture (synchronous once)
-            G = self._graph
+        # two device buffers, each with its own captured step that runs in place
+        # on it: the input is copied straight into the buffer and the result
+        # straight out of it (no device-side copies on the compute stream)
         io = getattr(self, "_io", None)
-        if io is None or io["shape"] != tuple(uin.shape):
+        key = self._graph_key(uin)
+        if io is None or io["key"] != key:
             dev = self._dev
-            io = self._io = dict(shape=tuple(uin.shape), h2d=torch.cuda.Stream(), d2h=torch.cuda.Stream(),
-                                 din=[torch.empty(uin.shape, dtype=torch.float64, device=dev) for _ in range(2)],
-                                 dout=[torch.empty(uin.shape, dtype=torch.float64, device=dev) for _ in range(2)],
-                                 in_free=[None, None], out_free=[None, None], slot=0, pending=[])
+            io = self._io = dict(key=key, h2d=torch.cuda.Stream(), d2h=torch.cuda.Stream(),
+                                 buf=[torch.zeros(uin.shape, dtype=torch.float64, device=dev) for _ in range(2)],
+                                 G=[None, None], free=[None, None], slot=0, pending=[])
+            saved = self._graph
+            try:
+                for b in range(2):
+                    self._capture(t, io["buf"][b])
+                    io["G"][b] = self._graph
+            except Exception:  # e.g. an op in g that cannot be captured: step eagerly from now on
+                self._graph_failed, self._io = True, None
+                torch.cuda.synchronize()
+                return self.step_host(t, u_in, u_out, check_every)
+            finally:
+                self._graph = saved
         cs = torch.cuda.current_stream()
         slot = io["slot"]
         io["slot"] ^= 1
+        G, buf = io["G"][slot], io["buf"][slot]
         with torch.cuda.stream(io["h2d"]):
-            if io["in_free"][slot] is not None:
-                io["h2d"].wait_event(io["in_free"][slot])
-            io["din"][slot].copy_(uin, non_blocking=True)
+            if io["free"][slot] is not None:
+                io["h2d"].wait_event(io["free"][slot])   # the result copy that last read this buffer
+            buf.copy_(uin, non_blocking=True)
             ev_in = torch.cuda.Event()
             ev_in.record(io["h2d"])
         cs.wait_event(ev_in)
-        gin, guards, coef = G["gin"], G["guards"], G["coef"]
-        gin.copy_(io["din"][slot])
-        free = torch.cuda.Event()
-        free.record(cs)
-        io["in_free"][slot] = free
-        vals = self._dry_coefs(t, gin, guards)
+        guards, coef = G["guards"], G["coef"]
+        vals = self._dry_coefs(t, buf, guards)
         if len(vals) != G["ncoef"]:
             raise HpstepError("captured step and coefficient pass disagree")
         cslot = G["slot"]
         G["slot"] = (cslot + 1) % len(G["pinned"])
         if G["events"][cslot] is not None:
             G["events"][cslot].synchronize()
-        buf = G["pinned"][cslot]
-        buf[:len(vals)] = torch.as_tensor(vals, dtype=torch.float64)
-        coef.copy_(buf, non_blocking=True)
+        pin = G["pinned"][cslot]
+        pin[:len(vals)] = torch.as_tensor(vals, dtype=torch.float64)
+        coef.copy_(pin, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
         G["events"][cslot] = ev
         G["graph"].replay()
         io["pending"].append(guards.clone())
-        if io["out_free"][slot] is not None:
-            cs.wait_event(io["out_free"][slot])
-        io["dout"][slot].copy_(gin)
         done = torch.cuda.Event()
         done.record(cs)
         with torch.cuda.stream(io["d2h"]):
             io["d2h"].wait_event(done)
-            uout.copy_(io["dout"][slot], non_blocking=True)
+            uout.copy_(buf, non_blocking=True)
             ev_out = torch.cuda.Event()
             ev_out.record(io["d2h"])
-        io["out_free"][slot] = ev_out
+        io["free"][slot] = ev_out
         if len(io["pending"]) >= check_every:
             self.sync_host()
         return ev_out
