@@ -167,6 +167,17 @@ int hps_solve_stage(const hps_ops* ops, int k, const double* fb, long long ld_f,
                     long long ld_g, double* u, long long ld_u, double* lu_int, long long ld_lu,
                     double* guard, const double* root_pre, void* ws, size_t ws_bytes, void* stream);
 
+/* hps_solve_stage for one rhs (k = 1) with the stage body load given as its
+ * combination (timestep.py:255-257): r = sum_t dcoefs[t] vecs[t] over the
+ * leaf interiors [0, L*ni) (device coefficients, 1..8 terms, term order as
+ * hps_combine), formed by the upward sweep's leaf kernel -- no separate
+ * combination pass -- and written to r_out for the downward sweep.  lu_int
+ * and guard as hps_solve_stage (row strides N); root_pre as hps_solve_stage. */
+int hps_solve_stage_terms(const hps_ops* ops, const double* fb, int nterms, const double* dcoefs,
+                          const double* const* vecs, double* r_out, double* u, double* lu_int,
+                          double* guard, const double* root_pre, void* ws, size_t ws_bytes,
+                          void* stream);
+
 /* The root's Dirichlet product S_root u_bnd (solver.py:262-265 at the root,
  * whose boundary is the domain boundary) for ns <= 8 rows of boundary data
  * fb (nbd values each, row stride ld_f) in one pass over the root operator:

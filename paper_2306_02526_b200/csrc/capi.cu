@@ -592,6 +592,27 @@ int hps_solve_stage(const hps_ops* h, int k, const double* fb, long long ld_f, c
                (cudaStream_t)stream, lu_int, ld_lu, guard, root_pre);
 }
 
+int hps_solve_stage_terms(const hps_ops* h, const double* fb, int nterms, const double* dcoefs,
+                          const double* const* vecs, double* r_out, double* u, double* lu_int, double* guard,
+                          const double* root_pre, void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !fb || !u || !ws || !r_out || !dcoefs || !vecs) {
+    set_error("hps_solve_stage_terms: null argument");
+    return HPS_ERR_ARG;
+  }
+  const Ops& O = h->O;
+  if (!(O.shared_leaf && O.fd && leaf_fd_down_enabled())) {
+    set_error("hps_solve_stage_terms: needs the tensor-product leaf solve (constant coefficients)");
+    return HPS_ERR_ARG;
+  }
+  if (nterms < 1 || nterms > 8) { set_error("hps_solve_stage_terms: %d terms (1..8)", nterms); return HPS_ERR_ARG; }
+  StageTerms T;
+  T.nterm = nterms; T.tdc = dcoefs; T.rout = r_out;
+  for (int t = 0; t < nterms; ++t) T.tv[t] = vecs[t];
+  const long long N = h->O.plan->N;
+  return solve(O, SOLVE_ALL, 0, O.plan->nparts, 1, fb, 0, r_out, 0, nullptr, 0, 0.0, u, N, ws, ws_bytes,
+               (cudaStream_t)stream, lu_int, N, guard, root_pre, &T);
+}
+
 size_t hps_root_dirichlet_scratch(const hps_ops* h, int ns) { return h ? root_dirichlet_scratch(*h->O.plan, ns) : 0; }
 
 int hps_root_dirichlet(const hps_ops* h, int ns, const double* fb, long long ld_f, double* out, long long ld_out,

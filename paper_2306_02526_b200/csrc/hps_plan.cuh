@@ -227,6 +227,18 @@ int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld
 int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u, long long ld_u, const double* uint,
                double* lu, long long ld_lu, double* guard, cudaStream_t st);
 
+// the up sweep's leaf kernel forming the body load sum_t tdc[t] tv[t] (one rhs,
+// leaf interiors) itself and writing it to rout for the downward sweep
+int leaf_fd_up_terms(const Ops& ops, int nleaf, int nterm, const double* const* tv, const double* tdc, double* rout,
+                     double* H, long long ld_h, cudaStream_t st, int nbd, const int* bids, const double* fb,
+                     double* u);
+struct StageTerms {
+  int nterm = 0;
+  const double* tv[8] = {};
+  const double* tdc = nullptr;
+  double* rout = nullptr;
+};
+
 // persistent dataflow kernel for the wide levels (mega.cu): up
 // levels [u0, u1) deepest first, then down levels [d0, d1) root first, over
 // the parts' nodes on levels >= lstar; returns 1 when not eligible
@@ -252,7 +264,7 @@ enum SolvePhase { SOLVE_UP = 1, SOLVE_TOP = 2, SOLVE_DOWN = 4, SOLVE_ALL = 7 };
 int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
           const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
           long long ld_u, void* ws, size_t ws_bytes, cudaStream_t st, double* lu = nullptr, long long ld_lu = 0,
-          double* guard = nullptr, const double* root_pre = nullptr);
+          double* guard = nullptr, const double* root_pre = nullptr, const StageTerms* terms = nullptr);
 // byte offset of level lstar's flux block (k x nparts x n12) in a workspace
 size_t exchange_offset(const Plan& P, int k);
 

@@ -25,6 +25,8 @@ namespace {
 
 constexpr int NT = 256;
 
+constexpr int kFdTerms = 8;  // FD_UP_T: terms of the body load
+
 struct FdArgs {
   int L, k, nw;
   const double* g; long long ld_g;   // body load rows (leaf l interior at l*ni); null = zero
@@ -35,6 +37,8 @@ struct FdArgs {
   double* uint; long long ld_uint;   // FD_DOWN: interior output (leaf l at l*ni)
   double* lu; long long ld_lu;       // FD_DOWN, optional: L u at the interiors (the stage history)
   unsigned long long* guard;         // ... and max |u| over the leaves' grids (bits, NaN sticky)
+  int nterm; const double* tv[kFdTerms]; const double* tdc;  // FD_UP_T: body load = sum_t tdc[t] tv[t] ...
+  double* rout;                                              // ... written here (leaf l interior at l*ni)
   // FD_UP_H, optional: the solve's Dirichlet data u[ids[i]] = fb[i] (solver.py:259-260), written by the
   // CTAs after the dependency wait (the up sweep never reads u) -- one launch fewer per solve
   int nbd; const int* bids; const double* fb; long long ld_f; double* ubnd; long long ld_ubnd;
@@ -47,7 +51,9 @@ struct FdArgs {
 // modes of the tensor-core kernel
 // FD_LU: L u at the interiors of a given state (interiors from a.uint, boundary
 // values through lbg), the stage history of an explicit stage
-enum FdMode { FD_UP_WH = 0, FD_UP_H = 1, FD_DOWN = 2, FD_LU = 3 };
+// FD_UP_T: FD_UP_H with the body load formed from terms (sum_t c_t v_t, the
+// stage combination) and written out for the downward sweep
+enum FdMode { FD_UP_WH = 0, FD_UP_H = 1, FD_DOWN = 2, FD_LU = 3, FD_UP_T = 4 };
 
 template <int Q>
 __global__ void __launch_bounds__(NT) k_leaf_fd(FdArgs a) {
@@ -154,6 +160,8 @@ constexpr int kFdCst = 5 * 16 * CSA + 2 * 16 * CSB + 8 * CSA + 16 * 8;  // Vxi, 
 
 template <int Q, int MODE>
 __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
+  constexpr bool DOWNLIKE = MODE == FD_DOWN || MODE == FD_LU;   // leaf grid + boundary values
+  constexpr bool UPH = MODE == FD_UP_H || MODE == FD_UP_T;       // fluxes only on the way up
   constexpr int NI = Q * Q, NB = 4 * Q, UBS = 4 * Q + 8;
   // k-steps of 4 that cover the q (leaf solve) / p (stage history) columns:
   // the zero padding beyond them is never multiplied
@@ -175,7 +183,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   double* cAew = cVyt + 16 * CSB;                      // FD_UP_H: rows Vx^T e_east, Vx^T e_west (A type, 8 rows)
   double* cBns = cAew + 8 * CSA;                       // FD_UP_H: cols Vy^T e_n0, Vy^T e_n1 (B type, 16 x 8)
   for (int e = threadIdx.x; e < 8 * Q; e += 256) cst[e] = a.mats[5 * NI + e];
-  if (threadIdx.x == 0) cst[8 * Q] = MODE >= FD_DOWN ? a.mats[5 * NI + 8 * Q + 512] : 0.0;  // c
+  if (threadIdx.x == 0) cst[8 * Q] = DOWNLIKE ? a.mats[5 * NI + 8 * Q + 512] : 0.0;  // c
   for (int e = threadIdx.x; e < 256; e += 256) {
     const int r = e >> 4, c = e & 15;
     auto mat = [&](int m) -> double { return (r < Q && c < Q) ? a.mats[m * NI + r * Q + c] : 0.0; };
@@ -184,12 +192,12 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     cVx[r * CSA + c] = mat(2);
     cVyt[r * CSB + c] = mat(3);
     cR[r * CSA + c] = mat(4);
-    if (MODE >= FD_DOWN) {
+    if (DOWNLIKE) {
       cMx[r * CSA + c] = a.mats[5 * NI + 8 * Q + e];
       cMy[r * CSA + c] = a.mats[5 * NI + 8 * Q + 256 + e];
     }
   }
-  if (MODE == FD_UP_H) {
+  if (UPH) {
     __syncthreads();
     // the fluxes of w = Vx T2 Vy^T need only projections of T2:
     //   east / west (d/dx rows E0, E1):  h[y] = sum_r (a^T T2)[r] Vy[y][r],  a = Vx^T E
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
   __syncthreads();
   pdl_wait();
-  if (MODE == FD_UP_H && a.nbd > 0) {
+  if (UPH && a.nbd > 0) {
     for (int i = blockIdx.x * 256 + threadIdx.x; i < a.nbd; i += gridDim.x * 256)
       a.ubnd[kk * a.ld_ubnd + a.bids[i]] = a.fb[kk * a.ld_f + i];
   }
@@ -243,14 +251,50 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   constexpr int NR = (NI + 31) / 32;  // body-load values per lane
   constexpr int NU = (NB + 31) / 32;  // boundary values per lane (FD_DOWN)
   double nxt[NR];                     // next leaf's body load, prefetched during this leaf
-  double nub[MODE >= FD_DOWN ? NU : 1];
+  double nub[DOWNLIKE ? NU : 1];
   auto fetch = [&](int leaf) {
+    if (MODE == FD_UP_T) {
+      // the stage combination in term order (the fma order of k_combine), the
+      // next term's loads in flight while one is summed
+      double va[NR], vb[NR];
+      auto ldt = [&](double (&v)[NR], int t) {
+        const double* src = a.tv[t] + (long long)leaf * NI;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          const int e = lane + 32 * i;
+          v[i] = (leaf < a.L && e < NI) ? __ldcs(src + e) : 0.0;
+        }
+      };
+#pragma unroll
+      for (int i = 0; i < NR; ++i) nxt[i] = 0.0;
+      ldt(va, 0);
+      for (int t = 0; t < a.nterm; t += 2) {
+        if (t + 1 < a.nterm) ldt(vb, t + 1);
+        const double c0 = __ldg(a.tdc + t);
+#pragma unroll
+        for (int i = 0; i < NR; ++i) nxt[i] = fma(c0, va[i], nxt[i]);
+        if (t + 1 >= a.nterm) break;
+        if (t + 2 < a.nterm) ldt(va, t + 2);
+        const double c1 = __ldg(a.tdc + t + 1);
+#pragma unroll
+        for (int i = 0; i < NR; ++i) nxt[i] = fma(c1, vb[i], nxt[i]);
+      }
+      if (leaf < a.L) {
+        double* ro = a.rout + (long long)leaf * NI;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          const int e = lane + 32 * i;
+          if (e < NI) ro[e] = nxt[i];
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int i = 0; i < NR; ++i) {
       const int e = lane + 32 * i;
       nxt[i] = (g && leaf < a.L && e < NI) ? g[(long long)leaf * NI + e] : 0.0;
     }
-    if (MODE >= FD_DOWN) {
+    if (DOWNLIKE) {
       const double* u = a.u + kk * a.ld_u;
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
@@ -349,7 +393,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         for (int h = 0; h < 2; ++h) acc[mi][nj][h] *= cR[(mi * 8 + gr) * CSA + nj * 8 + 2 * gc + h];
     store(bufB, SB);
     __syncwarp();
-    if (MODE == FD_UP_H) {
+    if (UPH) {
       // fluxes of w = Vx T2 Vy^T without forming w (4 small DMMA products):
       //   east / west rows:  h_ew = (A_ew T2) Vy^T,  A_ew = [e_east; e_west] Vx (2 of 8 rows)
       //   north / south:     h_ns = Vx (T2 B_ns),    B_ns = Vy^T [e_n0 e_n1] (2 of 8 columns)
@@ -581,7 +625,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         }
     __syncwarp();
   }
-  if (MODE >= FD_DOWN && a.guard) {  // max |u| over the staged grids (NaN sorts above inf)
+  if (DOWNLIKE && a.guard) {  // max |u| over the staged grids (NaN sorts above inf)
     unsigned long long bits = __double_as_longlong(gmax);
     for (int off = 16; off > 0; off >>= 1) {
       const unsigned long long o = __shfl_xor_sync(0xffffffffu, bits, off);
@@ -646,6 +690,19 @@ int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u
   a.L = nleaf; a.k = k; a.g = uint; a.ld_g = ld_u; a.lbg = lbg; a.u = u; a.ld_u = ld_u; a.mats = ops.fd;
   a.lu = lu; a.ld_lu = ld_lu; a.guard = reinterpret_cast<unsigned long long*>(guard);
   return launch_fd_mma<FD_LU>(*ops.plan, a, nleaf, k, st);
+}
+
+int leaf_fd_up_terms(const Ops& ops, int nleaf, int nterm, const double* const* tv, const double* tdc, double* rout,
+                     double* H, long long ld_h, cudaStream_t st, int nbd, const int* bids, const double* fb,
+                     double* u) {
+  if (nleaf <= 0) return 0;
+  if (nterm <= 0 || nterm > kFdTerms) { set_error("leaf_fd_up_terms: %d terms (1..%d)", nterm, kFdTerms); return -1; }
+  FdArgs a{};
+  a.L = nleaf; a.k = 1; a.H = H; a.ld_h = ld_h; a.mats = ops.fd;
+  a.nterm = nterm; a.tdc = tdc; a.rout = rout;
+  for (int t = 0; t < nterm; ++t) a.tv[t] = tv[t];
+  a.nbd = nbd; a.bids = bids; a.fb = fb; a.ld_f = 0; a.ubnd = u; a.ld_ubnd = 0;
+  return launch_fd_mma<FD_UP_T>(*ops.plan, a, nleaf, 1, st);
 }
 
 int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,

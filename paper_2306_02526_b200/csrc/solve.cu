@@ -175,7 +175,7 @@ size_t exchange_offset(const Plan& P, int k) {
 int solve(const Ops& ops, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
           const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt, double* u,
           long long ld_u, void* wsp, size_t ws_bytes, cudaStream_t st, double* lu, long long ld_lu,
-          double* guard, const double* root_pre) {
+          double* guard, const double* root_pre, const StageTerms* terms) {
   const Plan& P = *ops.plan;
   if (k <= 0) return 0;
   if (ws_bytes < workspace_bytes(P, k)) {
@@ -219,7 +219,16 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   bool bnd_done = false;  // Dirichlet data already written by the leaf kernel
   if (phases & SOLVE_UP) {
     // (2) leaf particular solutions and their fluxes (solver.py:219-230)
-    if (g && fd_down) {
+    if (terms && fd_down && k == 1) {
+      // the stage combination formed by the leaf kernel (no combination pass), written out for the
+      // downward sweep; the Dirichlet data too
+      const bool bnd = (phases & SOLVE_TOP) && P.nbd > 0;
+      if (int rc = leaf_fd_up_terms(ops, nleaf, terms->nterm, terms->tv, terms->tdc,
+                                    terms->rout + (long long)leaf0 * P.ni, ws.Hleaf + (long long)leaf0 * P.nb, Lnb,
+                                    st, bnd ? P.nbd : 0, P.boundary_ids, fb, u))
+        return rc;
+      bnd_done = bnd;
+    } else if (g && fd_down) {
       // a whole solve: the leaf kernel also writes the Dirichlet data (no separate scatter launch)
       const bool bnd = (phases & SOLVE_TOP) && P.nbd > 0;
       if (int rc = leaf_fd_up_h(ops, k, nleaf, g, ld_g, ws.Hleaf + (long long)leaf0 * P.nb, Lnb, st,
@@ -309,6 +318,7 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   }
   if (int rc = downs(std::max(dA, dm), dB)) return rc;
 
+  if (terms && fd_down && k == 1) { g = terms->rout; ld_g = 0; }  // the formed body load
   if (phases & SOLVE_DOWN) {
     if (fused) {
       int b0, b1;

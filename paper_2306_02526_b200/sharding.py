@@ -347,6 +347,9 @@ class ShardedTimeStepper(TimeStepper):
     def _root_batch(self):
         return False
 
+    def _fused_stage_terms(self, fb, terms, r, out, lu, guard, root_pre):
+        return False
+
     def _ranges(self):
         return (self._ir, self._edges)
 

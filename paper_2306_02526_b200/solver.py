@@ -321,6 +321,20 @@ class HpsOperatorSet:
         _lib.check(rc, "hps_solve_stage")
         return out
 
+    def solve_stage_terms_device(self, fb, dcoef_ptr, vecs, rout, out, lu, guard, root_pre=None):
+        """The fused stage solve (one rhs) with its body load given as the
+        combination sum_t c_t vecs[t] over the leaf interiors (coefficients in
+        device memory at ``dcoef_ptr``), formed by the upward sweep's leaf
+        kernel and written to ``rout`` (hps_solve_stage_terms)."""
+        ws = self.plan.workspace(1)
+        vp = (ctypes.c_void_p * len(vecs))(*[v.data_ptr() for v in vecs])
+        rc = self._lib.hps_solve_stage_terms(
+            self.handle, fb.data_ptr(), len(vecs), dcoef_ptr, vp, rout.data_ptr(), out.data_ptr(),
+            None if lu is None else lu.data_ptr(), None if guard is None else guard.data_ptr(),
+            None if root_pre is None else root_pre.data_ptr(), ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_solve_stage_terms")
+        return out
+
     @property
     def root_dirichlet_ok(self):
         """Whether the root's Dirichlet product can be batched over a step's

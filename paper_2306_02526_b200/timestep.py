@@ -826,6 +826,34 @@ class TimeStepper:
         a = self._ir[0]
         return v if a == 0 else v[:, a:]
 
+    def _fused_stage_terms(self, fb, terms, r, out, lu, guard, root_pre):
+        """hps_solve_stage_terms when the stage's combination fits it (one rhs,
+        at most 8 single-row terms, the whole tree); False otherwise."""
+        if not (self._k == 1 and 0 < len(terms) <= 8 and self.ops.fuses_stage_history and
+                self.solve_timer is None and self._ir[0] == 0 and
+                os.environ.get("HPSB_NO_STAGE_TERMS") != "1"):
+            return False
+        if any(v.shape[0] != 1 for _, v in terms):
+            return False
+        dptr = self._coef_ptr([c for c, _ in terms])
+        if not self._dry:
+            self.ops.solve_stage_terms_device(fb, dptr, [v for _, v in terms], r, out, lu, guard, root_pre)
+        return True
+
+    def _coef_ptr(self, vals):
+        """Device address of ``vals`` (float64): a slot range of the captured
+        step's coefficient table, or a fresh device array when stepping eagerly
+        (kept alive until the next step)."""
+        sink = _CoefSink.current
+        if sink is not None:
+            return sink.take([float(v) for v in vals])
+        t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=self._dev)
+        keep = getattr(self, "_coef_keep", None)
+        if keep is None or keep[0] is not self._step_token:
+            keep = self._coef_keep = (self._step_token, [])
+        keep[1].append(t)
+        return t.data_ptr()
+
     def _root_batch(self):
         return self.ops.fuses_stage_history and self.ops.root_dirichlet_ok and self.solve_timer is None
 
@@ -906,6 +934,7 @@ class TimeStepper:
         s, k, N, Lni = pair.s, u.shape[0], self.tree.N, self._nloc
         A, Ah = pair.A, pair.Ahat
         iv = self._iv
+        self._step_token = object()          # eager coefficient arrays live until the next step
         Lu = self._buf("Lu", (s, k, Lni))
         nonlin = self.problem.g is not None
         QG = self._buf("QG", (s, k, N)) if (nonlin or (self._Q.fn is not None and self._Q.sep is None)) \
@@ -951,12 +980,16 @@ class TimeStepper:
             if qsep is not None:
                 for m, phi in enumerate(qsep):
                     terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), iv(phi)))
-            combine(terms, r, n=Lni)
             ui = U[i & 1]
             bc = bc_at(i, ti)
-            # solve + history L u_i (not needed after the last stage) + guard in one pass
-            if not self._fused_stage(bc, r, ui, Lu[i] if i < s - 1 else None, guards[i - 1],
-                                     None if rpre is None else rpre[i - 1:i]):
+            rp = None if rpre is None else rpre[i - 1:i]
+            # the combination formed by the solve's leaf kernel; solve + history L u_i (not
+            # needed after the last stage) + guard in one pass
+            if self._fused_stage_terms(bc, terms, r, ui, Lu[i] if i < s - 1 else None, guards[i - 1], rp):
+                stage_q_g(i, ti, ui)
+                continue
+            combine(terms, r, n=Lni)
+            if not self._fused_stage(bc, r, ui, Lu[i] if i < s - 1 else None, guards[i - 1], rp):
                 self._solve(self.ops, bc, r, ui)
                 if i < s - 1:
                     self._eval_lu(ui, Lu[i], guard=guards[i - 1])

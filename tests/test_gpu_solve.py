@@ -219,6 +219,38 @@ def test_root_dirichlet_product_in_stage_solve(n):
         assert abs(g1.item() - g2.item()) <= 1e-13 * g2.item()
 
 
+@pytest.mark.parametrize("p", [12, 16])
+def test_stage_terms_match_combine_then_stage(p):
+    """hps_solve_stage_terms (the body load formed from its terms by the up
+    sweep's leaf kernel and written out) equals hps_combine + hps_solve_stage:
+    the same body load bitwise (same fma order), the same solution."""
+    import torch
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.timestep import combine
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 16, 16, p)
+    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0))
+    ops = hb.HpsOperatorSet(disc, sigma=1.0, dt_gamma=2.5e-4, layout="shared")
+    rng = np.random.default_rng(p)
+    Lni = tree.L * tree.ni
+    vecs = [torch.as_tensor(rng.standard_normal((1, Lni)), device="cuda") for _ in range(7)]
+    coefs = [1.0, -0.3, 2.5e-4, 0.125, -7.0, 1e-3, 0.5]
+    dc = torch.tensor(coefs, dtype=torch.float64, device="cuda")
+    fb = torch.as_tensor(rng.standard_normal((1, tree.boundary_ids.size)), device="cuda")
+    for nt in (1, 2, 7):
+        r1 = torch.empty((1, Lni), dtype=torch.float64, device="cuda")
+        u1 = torch.zeros((1, tree.N), dtype=torch.float64, device="cuda")
+        u2 = torch.zeros_like(u1)
+        lu1, lu2 = torch.empty_like(r1), torch.empty_like(r1)
+        g1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        g2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+        ops.solve_stage_terms_device(fb, dc.data_ptr(), vecs[:nt], r1, u1, lu1, g1)
+        r2 = combine(list(zip(coefs[:nt], vecs[:nt])), torch.empty_like(r1))
+        ops.solve_stage_device(fb, r2, u2, lu2, g2)
+        assert torch.equal(r1, r2), nt
+        assert torch.equal(u1, u2), nt
+        assert torch.equal(lu1, lu2) and g1.item() == g2.item(), nt
+
+
 def test_timing_harness_rows(tmp_path):
     """run_timing (drivers.py:160-204) on the device: one row per size with
     the reference's columns, build and median solve times, CSV written."""

@@ -64,11 +64,20 @@ def test_c1_heat_matches_reference(golden, separable, layout, monkeypatch):
         stages.append(out[0].cpu().numpy().copy())
         return r
 
+    orig_terms = st.ops.solve_stage_terms_device
+
+    def rec_terms(fb, dptr, vecs, rout, out, lu, guard, *a, **kw):
+        r = orig_terms(fb, dptr, vecs, rout, out, lu, guard, *a, **kw)
+        stages.append(out[0].cpu().numpy().copy())
+        return r
+
     st.ops.solve_device = rec
     st.ops.solve_stage_device = rec_stage
+    st.ops.solve_stage_terms_device = rec_terms
     s = st.step(st.initial_state())
     st.ops.solve_device = orig
     st.ops.solve_stage_device = orig_stage
+    st.ops.solve_stage_terms_device = orig_terms
     monkeypatch.delenv("HPSB_NO_GRAPH")           # the rest runs as replays of a captured step
     for i, (a, b) in enumerate(zip(stages, z["stages"])):
         assert rel_l2(a, b) < TOL, f"stage {i + 1}"
