@@ -169,7 +169,7 @@ int hps_solve_stage(const hps_ops* ops, int k, const double* fb, long long ld_f,
 
 /* hps_solve_stage for one rhs (k = 1) with the stage body load given as its
  * combination (timestep.py:255-257): r = sum_t dcoefs[t] vecs[t] over the
- * leaf interiors [0, L*ni) (device coefficients, 1..8 terms, term order as
+ * leaf interiors [0, L*ni) (device coefficients, 1..12 terms, term order as
  * hps_combine), formed by the upward sweep's leaf kernel -- no separate
  * combination pass -- and written to r_out for the downward sweep.  lu_int
  * and guard as hps_solve_stage (row strides N); root_pre as hps_solve_stage. */

@@ -604,7 +604,7 @@ int hps_solve_stage_terms(const hps_ops* h, const double* fb, int nterms, const 
     set_error("hps_solve_stage_terms: needs the tensor-product leaf solve (constant coefficients)");
     return HPS_ERR_ARG;
   }
-  if (nterms < 1 || nterms > 8) { set_error("hps_solve_stage_terms: %d terms (1..8)", nterms); return HPS_ERR_ARG; }
+  if (nterms < 1 || nterms > 12) { set_error("hps_solve_stage_terms: %d terms (1..12)", nterms); return HPS_ERR_ARG; }
   StageTerms T;
   T.nterm = nterms; T.tdc = dcoefs; T.rout = r_out;
   for (int t = 0; t < nterms; ++t) T.tv[t] = vecs[t];

@@ -234,7 +234,7 @@ int leaf_fd_up_terms(const Ops& ops, int nleaf, int nterm, const double* const* 
                      double* u);
 struct StageTerms {
   int nterm = 0;
-  const double* tv[8] = {};
+  const double* tv[12] = {};
   const double* tdc = nullptr;
   double* rout = nullptr;
 };

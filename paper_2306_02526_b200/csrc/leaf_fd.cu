@@ -25,7 +25,7 @@ namespace {
 
 constexpr int NT = 256;
 
-constexpr int kFdTerms = 8;  // FD_UP_T: terms of the body load
+constexpr int kFdTerms = 12;  // FD_UP_T: terms of the body load
 
 struct FdArgs {
   int L, k, nw;

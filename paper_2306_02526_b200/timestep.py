@@ -828,8 +828,8 @@ class TimeStepper:
 
     def _fused_stage_terms(self, fb, terms, r, out, lu, guard, root_pre):
         """hps_solve_stage_terms when the stage's combination fits it (one rhs,
-        at most 8 single-row terms, the whole tree); False otherwise."""
-        if not (self._k == 1 and 0 < len(terms) <= 8 and self.ops.fuses_stage_history and
+        at most 12 single-row terms, the whole tree); False otherwise."""
+        if not (self._k == 1 and 0 < len(terms) <= 12 and self.ops.fuses_stage_history and
                 self.solve_timer is None and self._ir[0] == 0 and
                 os.environ.get("HPSB_NO_STAGE_TERMS") != "1"):
             return False
