@@ -297,6 +297,14 @@ int hps_combine_dev_rows(int k, long long n, int nterms, const double* dcoefs, l
 /* guard = max(guard, max |x|) over k rows of n values. */
 int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard, void* stream);
 
+/* The step's final combination with the Dirichlet data and the guard in one
+ * pass (timestep.py:263-266): out[k][e] = sum_t c_t vecs[t][k][e] over all N
+ * DOFs, then fb at the domain-boundary DOFs, guard = max(guard, max |out|).
+ * Coefficients from the host (coefs) or device memory (dcoefs, graph replay). */
+int hps_combine_bnd(const hps_plan* plan, int k, int nterms, const double* coefs, const double* dcoefs,
+                    const double* const* vecs, const long long* lds, const double* fb, long long ld_f,
+                    double* out, long long ld_out, double* guard, void* stream);
+
 /* u[r][boundary_ids] = fb[r] (timestep.py:265). */
 int hps_put_boundary(const hps_plan* plan, int k, const double* fb, long long ld_f, double* u,
                      long long ld_u, void* stream);

@@ -115,6 +115,8 @@ SIGNATURES = {
     "hps_combine_dev": (_i, [_i, _ll, _i, _vp, ctypes.POINTER(_vp), c_ll_p, _vp, _ll, _vp, _vp]),
     "hps_combine_dev_rows": (_i, [_i, _ll, _i, _vp, _ll, ctypes.POINTER(_vp), c_ll_p, _vp, _ll, _vp, _vp]),
     "hps_maxabs": (_i, [_i, _ll, _vp, _ll, _vp, _vp]),
+    "hps_combine_bnd": (_i, [_vp, _i, _i, c_double_p, _vp, ctypes.POINTER(_vp), c_ll_p, _vp, _ll, _vp, _ll, _vp,
+                             _vp]),
     "hps_put_boundary": (_i, [_vp, _i, _vp, _ll, _vp, _ll, _vp]),
 }
 

@@ -214,6 +214,17 @@ int hps_plan_create(const hps_plan_desc* d, hps_plan** out) {
     }
     if (all) up(bp.data(), (size_t)n12, &P.root_bpos);
   }
+  {  // boundary position of every edge DOF (the final stage combination writes the Dirichlet data itself)
+    const long long e0 = (long long)P.L * P.ni, ne = P.N - e0;
+    std::vector<int> eb((size_t)std::max(0LL, ne), -1);
+    bool ok = true;
+    for (int i = 0; i < P.nbd && ok; ++i) {
+      const long long g = d->boundary_ids[i] - e0;
+      if (g < 0 || g >= ne) ok = false;
+      else eb[(size_t)g] = i;
+    }
+    if (ok && ne > 0) up(eb.data(), (size_t)ne, &P.edge_bpos);
+  }
   P.leaf_node_index.assign(d->leaf_node_index, d->leaf_node_index + P.L);
   if (rc) { hps_plan_destroy(h); return rc; }
   *out = h;

@@ -34,6 +34,7 @@ struct Plan {
   int* leaf_bnd_gidx = nullptr;   // device L x nb
   int* boundary_ids = nullptr;    // device nbd
   int* root_bpos = nullptr;       // device lv[0].n12: fb position of each root boundary DOF (null: not all on the boundary)
+  int* edge_bpos = nullptr;       // device N - L*ni: fb position of each edge DOF, -1 off the domain boundary
   std::vector<long long> leaf_node_index;  // host
   int dF = 0;                     // levels d >= dF run as fused subtree kernels
   // subtree-local numbering of the DOFs a fused subtree touches (the same for

@@ -546,6 +546,39 @@ __global__ void __launch_bounds__(NT) k_combine2(CombineArgs a) {
   if (a.guard) guard_max(a.guard, gmax);
 }
 
+// The step's final combination with the Dirichlet overwrite and the guard in
+// one pass (timestep.py:263-266): out = sum c v, then fb at the boundary DOFs
+// (edge DOFs e >= e0 with ebp[e - e0] >= 0), guard over the final values.
+__global__ void __launch_bounds__(NT) k_combine_bnd(CombineArgs a, long long e0, const int* __restrict__ ebp,
+                                                    const double* __restrict__ fb, long long ld_f) {
+  pdl_trigger();
+  pdl_wait();
+  const int kk = blockIdx.y;
+  double gmax = 0.0;
+  const long long stride = (long long)gridDim.x * NT;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < a.n; e += stride) {
+    double s = 0.0;
+    const int bp = e >= e0 ? __ldg(ebp + (e - e0)) : -1;
+    if (bp >= 0) {
+      s = fb[kk * ld_f + bp];
+    } else {
+      for (int t0 = 0; t0 < a.nt; t0 += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = t0 + u < a.nt ? __ldcs(a.v[t0 + u] + kk * a.ld[t0 + u] + e) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (t0 + u >= a.nt) break;
+          s = fma(a.dc ? __ldg(a.dc + kk * a.ldc + t0 + u) : a.c[t0 + u], v[u], s);
+        }
+      }
+    }
+    a.out[kk * a.ld_out + e] = s;
+    gacc(gmax, s);
+  }
+  if (a.guard) guard_max(a.guard, gmax);
+}
+
 bool combine_vec_ok(const CombineArgs& a) {
   if (a.n & 1 || ((uintptr_t)a.out & 15) || (a.ld_out & 1)) return false;
   for (int t = 0; t < a.nt; ++t)
@@ -777,6 +810,25 @@ int hps_maxabs(int k, long long n, const double* x, long long ld, double* guard,
   dim3 grid(stream_blocks(n), (unsigned)k);
   HPSB_CUDA(launch_pdl(k_maxabs, grid, dim3(NT), 0, (cudaStream_t)stream, k, n, x, ld,
                        reinterpret_cast<unsigned long long*>(guard)));
+  HPSB_LAUNCH_CHECK();
+  return HPS_OK;
+}
+
+int hps_combine_bnd(const hps_plan* pv, int k, int nterms, const double* coefs, const double* dcoefs,
+                    const double* const* vecs, const long long* lds, const double* fb, long long ld_f, double* out,
+                    long long ld_out, double* guard, void* stream) {
+  if (!pv || !fb || !out || (!coefs && !dcoefs)) { set_error("hps_combine_bnd: null argument"); return HPS_ERR_ARG; }
+  const Plan& P = pv->P;
+  if (!P.edge_bpos) { set_error("hps_combine_bnd: boundary DOFs outside the edge range"); return HPS_ERR_ARG; }
+  if (nterms < 0 || nterms > MAXT) { set_error("hps_combine_bnd: %d terms (max %d)", nterms, MAXT); return HPS_ERR_ARG; }
+  if (k <= 0) return HPS_OK;
+  CombineArgs a{};
+  a.nt = nterms; a.k = k; a.n = P.N; a.out = out; a.ld_out = ld_out; a.dc = dcoefs;
+  for (int t = 0; t < nterms; ++t) { if (coefs) a.c[t] = coefs[t]; a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
+  a.guard = reinterpret_cast<unsigned long long*>(guard);
+  dim3 grid(stream_blocks(P.N), (unsigned)k);
+  HPSB_CUDA(launch_pdl(k_combine_bnd, grid, dim3(NT), 0, (cudaStream_t)stream, a, (long long)P.L * P.ni,
+                       (const int*)P.edge_bpos, fb, ld_f));
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
 }

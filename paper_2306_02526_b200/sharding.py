@@ -347,6 +347,11 @@ class ShardedTimeStepper(TimeStepper):
     def _root_batch(self):
         return False
 
+    def _final_combine(self, terms, fb, unew, guard):
+        self._owned_combine(terms, unew)
+        self._put_boundary(fb, unew)
+        self._owned_maxabs(unew, guard)
+
     def _fused_stage_terms(self, fb, terms, r, out, lu, guard, root_pre):
         return False
 

@@ -272,6 +272,26 @@ def combine(terms, out, n=None, guard=None):
     return out
 
 
+def combine_bnd(plan, terms, fb, out, guard):
+    """out = sum c * v over all DOFs, the Dirichlet data fb at the boundary
+    DOFs and guard = max(guard, max |out|), one pass (hps_combine_bnd)."""
+    lib = _lib.load()
+    sink = _CoefSink.current
+    terms = [(float(c), v) for c, v in terms]
+    nt = len(terms)
+    dptr = sink.take([c for c, _ in terms]) if sink is not None else None
+    if sink is not None and sink.dry:
+        return out
+    vecs = (ctypes.c_void_p * max(1, nt))(*[v.data_ptr() for _, v in terms])
+    lds = (ctypes.c_longlong * max(1, nt))(*[0 if v.shape[0] == 1 else v.stride(0) for _, v in terms])
+    coefs = (ctypes.c_double * max(1, nt))(*[c for c, _ in terms]) if sink is None else None
+    rc = lib.hps_combine_bnd(plan.handle, out.shape[0], nt, coefs, dptr, vecs, lds, fb.data_ptr(),
+                             0 if fb.shape[0] == 1 else fb.stride(0), out.data_ptr(), out.stride(0),
+                             None if guard is None else guard.data_ptr(), current_stream_handle())
+    _lib.check(rc, "hps_combine_bnd")
+    return out
+
+
 def combine_rows(coefs, vecs, out):
     """out[r] = sum_t coefs[r][t] * vecs[t] (single-row terms) for every row r
     of ``out`` in one launch (hps_combine_dev_rows)."""
@@ -854,6 +874,16 @@ class TimeStepper:
         keep[1].append(t)
         return t.data_ptr()
 
+    def _final_combine(self, terms, fb, unew, guard):
+        """unew = the final combination, its boundary DOFs set to f(t + dt), and
+        the step's guard (timestep.py:263-266): one fused pass."""
+        if os.environ.get("HPSB_NO_COMBINE_BND") == "1":
+            self._owned_combine(terms, unew)
+            self._put_boundary(fb, unew)
+            self._owned_maxabs(unew, guard)
+            return
+        combine_bnd(self._plan, terms, fb, unew, guard)
+
     def _root_batch(self):
         return self.ops.fuses_stage_history and self.ops.root_dirichlet_ok and self.solve_timer is None
 
@@ -1005,9 +1035,7 @@ class TimeStepper:
                 terms.append((sum(dt * w[j] * qfac[j][m] for j in range(s)), phi))
         # `out` may alias `u`: nothing below reads u
         unew = torch.empty((k, N), dtype=torch.float64, device=self._dev) if out is None else out
-        self._owned_combine(terms, unew)
-        self._put_boundary(bc_at(s, t + dt), unew)
-        self._owned_maxabs(unew, guards[s - 1])
+        self._final_combine(terms, bc_at(s, t + dt), unew, guards[s - 1])
         return unew
 
     # -- slope formulations (timestep.py:268-328) ----------------------------------------

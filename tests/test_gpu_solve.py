@@ -251,6 +251,36 @@ def test_stage_terms_match_combine_then_stage(p):
         assert torch.equal(lu1, lu2) and g1.item() == g2.item(), nt
 
 
+def test_combine_bnd_matches_combine_put_maxabs():
+    """hps_combine_bnd (final combination + Dirichlet data + guard, one pass)
+    equals hps_combine, hps_put_boundary and hps_maxabs in sequence."""
+    import torch
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200 import _lib
+    from paper_2306_02526_b200.device import current_stream_handle
+    from paper_2306_02526_b200.solver import device_plan
+    from paper_2306_02526_b200.timestep import combine, combine_bnd
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 8, 4, 12)
+    plan = device_plan(tree)
+    rng = np.random.default_rng(3)
+    k, N = 2, tree.N
+    v = [torch.as_tensor(rng.standard_normal((k, N)), device="cuda") for _ in range(3)]
+    v.append(torch.as_tensor(rng.standard_normal((1, N)), device="cuda"))
+    terms = [(1.0, v[0]), (-0.5, v[1]), (0.25, v[2]), (3.0, v[3])]
+    fb = torch.as_tensor(rng.standard_normal((k, tree.boundary_ids.size)), device="cuda")
+    out1 = torch.empty((k, N), dtype=torch.float64, device="cuda")
+    g1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    combine_bnd(plan, terms, fb, out1, g1)
+    out2 = combine(terms, torch.empty_like(out1))
+    lib = _lib.load()
+    _lib.check(lib.hps_put_boundary(plan.handle, k, fb.data_ptr(), fb.stride(0), out2.data_ptr(), out2.stride(0),
+                                    current_stream_handle()), "put")
+    g2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.check(lib.hps_maxabs(k, N, out2.data_ptr(), out2.stride(0), g2.data_ptr(), current_stream_handle()), "max")
+    assert torch.equal(out1, out2)
+    assert g1.item() == g2.item() == float(out2.abs().max())
+
+
 def test_timing_harness_rows(tmp_path):
     """run_timing (drivers.py:160-204) on the device: one row per size with
     the reference's columns, build and median solve times, CSV written."""
