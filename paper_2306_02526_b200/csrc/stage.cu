@@ -579,6 +579,42 @@ __global__ void __launch_bounds__(NT) k_combine_bnd(CombineArgs a, long long e0,
   if (a.guard) guard_max(a.guard, gmax);
 }
 
+// 16-byte variant of k_combine_bnd (pairs of DOFs; e0 even)
+__global__ void __launch_bounds__(NT) k_combine_bnd2(CombineArgs a, long long e0, const int* __restrict__ ebp,
+                                                     const double* __restrict__ fb, long long ld_f) {
+  pdl_trigger();
+  pdl_wait();
+  const int kk = blockIdx.y;
+  double gmax = 0.0;
+  const long long n2 = a.n / 2, stride = (long long)gridDim.x * NT;
+  for (long long e = blockIdx.x * (long long)NT + threadIdx.x; e < n2; e += stride) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int t0 = 0; t0 < a.nt; t0 += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = t0 + u < a.nt ? __ldcs(reinterpret_cast<const double2*>(a.v[t0 + u] + kk * a.ld[t0 + u]) + e)
+                             : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t0 + u >= a.nt) break;
+        const double c = a.dc ? __ldg(a.dc + kk * a.ldc + t0 + u) : a.c[t0 + u];
+        s.x = fma(c, v[u].x, s.x);
+        s.y = fma(c, v[u].y, s.y);
+      }
+    }
+    if (2 * e >= e0) {  // edge DOFs: the Dirichlet data where they lie on the domain boundary
+      const int2 bp = __ldg(reinterpret_cast<const int2*>(ebp + (2 * e - e0)));
+      if (bp.x >= 0) s.x = fb[kk * ld_f + bp.x];
+      if (bp.y >= 0) s.y = fb[kk * ld_f + bp.y];
+    }
+    reinterpret_cast<double2*>(a.out + kk * a.ld_out)[e] = s;
+    gacc(gmax, s.x);
+    gacc(gmax, s.y);
+  }
+  if (a.guard) guard_max(a.guard, gmax);
+}
+
 bool combine_vec_ok(const CombineArgs& a) {
   if (a.n & 1 || ((uintptr_t)a.out & 15) || (a.ld_out & 1)) return false;
   for (int t = 0; t < a.nt; ++t)
@@ -826,9 +862,16 @@ int hps_combine_bnd(const hps_plan* pv, int k, int nterms, const double* coefs, 
   a.nt = nterms; a.k = k; a.n = P.N; a.out = out; a.ld_out = ld_out; a.dc = dcoefs;
   for (int t = 0; t < nterms; ++t) { if (coefs) a.c[t] = coefs[t]; a.v[t] = vecs[t]; a.ld[t] = lds[t]; }
   a.guard = reinterpret_cast<unsigned long long*>(guard);
-  dim3 grid(stream_blocks(P.N), (unsigned)k);
-  HPSB_CUDA(launch_pdl(k_combine_bnd, grid, dim3(NT), 0, (cudaStream_t)stream, a, (long long)P.L * P.ni,
-                       (const int*)P.edge_bpos, fb, ld_f));
+  const long long e0 = (long long)P.L * P.ni;
+  if (combine_vec_ok(a) && !(e0 & 1) && !((uintptr_t)P.edge_bpos & 7)) {
+    dim3 grid(stream_blocks(P.N / 2), (unsigned)k);
+    HPSB_CUDA(launch_pdl(k_combine_bnd2, grid, dim3(NT), 0, (cudaStream_t)stream, a, e0, (const int*)P.edge_bpos,
+                         fb, ld_f));
+  } else {
+    dim3 grid(stream_blocks(P.N), (unsigned)k);
+    HPSB_CUDA(launch_pdl(k_combine_bnd, grid, dim3(NT), 0, (cudaStream_t)stream, a, e0, (const int*)P.edge_bpos,
+                         fb, ld_f));
+  }
   HPSB_LAUNCH_CHECK();
   return HPS_OK;
 }
