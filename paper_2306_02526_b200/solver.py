@@ -343,15 +343,18 @@ class HpsOperatorSet:
             os.environ.get("HPSB_NO_ROOT_BATCH") != "1"
 
     def root_dirichlet_device(self, fb_rows, out):
-        """S_root u_bnd for each row of boundary data (ns <= 8 rows, fb order)
-        into out (ns, n3_root): one pass over the root operator (hps_root_dirichlet)."""
+        """S_root u_bnd for each row of boundary data (fb order) into out
+        (ns, n3_root): one pass over the root operator per 8 rows
+        (hps_root_dirichlet)."""
         ns = fb_rows.shape[0]
-        nbytes = self._lib.hps_root_dirichlet_scratch(self.handle, ns)
+        nbytes = self._lib.hps_root_dirichlet_scratch(self.handle, min(ns, 8))
         scratch = torch.empty(max(1, (nbytes + 7) // 8), dtype=torch.float64, device=out.device)
-        rc = self._lib.hps_root_dirichlet(self.handle, ns, fb_rows.data_ptr(), fb_rows.stride(0), out.data_ptr(),
-                                          out.stride(0), scratch.data_ptr(), scratch.numel() * 8,
-                                          current_stream_handle())
-        _lib.check(rc, "hps_root_dirichlet")
+        for r0 in range(0, ns, 8):  # eight rows per pass (tableaus with more stages: several passes)
+            m = min(8, ns - r0)
+            rc = self._lib.hps_root_dirichlet(self.handle, m, fb_rows[r0].data_ptr(), fb_rows.stride(0),
+                                              out[r0].data_ptr(), out.stride(0), scratch.data_ptr(),
+                                              scratch.numel() * 8, current_stream_handle())
+            _lib.check(rc, "hps_root_dirichlet")
         return out
 
     def leaf_lu_device(self, u, lu, guard=None, leaves=None):
