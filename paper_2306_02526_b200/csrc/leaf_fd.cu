@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   // the zero padding beyond them is never multiplied
   constexpr int KS = (Q + 3) / 4, KSL = (Q + 2 + 3) / 4;
   extern __shared__ double sm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, kk = blockIdx.y;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* bufB = sm + warp * (16 * (SB + SA) + UBS);   // stride SB
   double* bufA = bufB + 16 * SB;                       // stride SA
   double* ub = bufA + 16 * SA;                         // FD_DOWN: the leaf's boundary values
@@ -239,6 +239,8 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
   __syncthreads();
   pdl_wait();
+  // rhs rows kk of this CTA: the constant staging above is paid once for all of them
+  for (int kk = blockIdx.y; kk < a.k; kk += gridDim.y) {
   if (UPH && a.nbd > 0) {
     for (int i = blockIdx.x * 256 + threadIdx.x; i < a.nbd; i += gridDim.x * 256)
       a.ubnd[kk * a.ld_ubnd + a.bids[i]] = a.fb[kk * a.ld_f + i];
@@ -625,6 +627,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         }
     __syncwarp();
   }
+  }  // rhs rows
   if (DOWNLIKE && a.guard) {  // max |u| over the staged grids (NaN sorts above inf)
     unsigned long long bits = __double_as_longlong(gmax);
     for (int off = 16; off > 0; off >>= 1) {
@@ -641,7 +644,7 @@ template <int MODE>
 static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaStream_t st) {
   const size_t smem = ((size_t)8 * (16 * (SB + SA) + 4 * P.q + 8) + 8 * P.q + 1 + kFdCst) * 8;
   const unsigned warps = (unsigned)std::min<long long>(cdiv(nleaf, 8), (long long)kNumSMs * 2);  // one wave
-  dim3 g2(warps, (unsigned)k);
+  dim3 g2(warps, (unsigned)std::min(k, 8));  // each CTA loops over rhs rows blockIdx.y + 8 i
 #define HPSB_FD2(QQ)                                                                                   \
   if (P.q == QQ) {                                                                                     \
     static bool attr = false;                                                                          \
