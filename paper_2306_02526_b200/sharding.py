@@ -347,6 +347,9 @@ class ShardedTimeStepper(TimeStepper):
     def _root_batch(self):
         return False
 
+    def _qg_alias_ok(self):
+        return False                      # only the owned DOFs of the history are written
+
     def _final_combine(self, terms, fb, unew, guard):
         self._owned_combine(terms, unew)
         self._put_boundary(fb, unew)

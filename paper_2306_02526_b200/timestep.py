@@ -884,6 +884,11 @@ class TimeStepper:
             return
         combine_bnd(self._plan, terms, fb, unew, guard)
 
+    def _qg_alias_ok(self):
+        """Whether g's result may serve as the QG history entry itself (one
+        process: every DOF of it is owned)."""
+        return True
+
     def _root_batch(self):
         return self.ops.fuses_stage_history and self.ops.root_dirichlet_ok and self.solve_timer is None
 
@@ -969,6 +974,7 @@ class TimeStepper:
         nonlin = self.problem.g is not None
         QG = self._buf("QG", (s, k, N)) if (nonlin or (self._Q.fn is not None and self._Q.sep is None)) \
             else None
+        QGl = [None] * s                     # the history entries (QG rows, or g's own result tensors)
         qsep = self._Q.sep
         qfac = []                                    # per stage: separable q time factors
         r = self._buf("r", (k, Lni))
@@ -982,10 +988,21 @@ class TimeStepper:
                 G = self._g(ti, ui)
                 if G is not None:
                     terms.append((1.0, G))
-                if terms:
+                if len(terms) == 1 and terms[0][0] == 1.0 and self._qg_alias_ok():
+                    G = terms[0][1]
+                    if G.shape == QG[i].shape and G.is_contiguous():
+                        QGl[i] = G                   # g's result as the history itself (no copy)
+                    else:
+                        QGl[i] = QG[i]
+                        if not self._dry:
+                            QG[i].copy_(G)
+                elif terms:
+                    QGl[i] = QG[i]
                     self._owned_combine(terms, QG[i])
-                elif not self._dry:
-                    QG[i].zero_()
+                else:
+                    QGl[i] = QG[i]
+                    if not self._dry:
+                        QG[i].zero_()
 
         # boundary data of stages 1..s-1 and of t + dt, one launch when f is separable
         bcs = self._F.values([t + pair.c[i] * dt for i in range(1, s)] + [t + dt]) \
@@ -1006,7 +1023,7 @@ class TimeStepper:
             terms = [(1.0, iv(u))]
             terms += [(dt * A[i, j], Lu[j]) for j in range(i)]
             if QG is not None:
-                terms += [(dt * Ah[i, j], iv(QG[j])) for j in range(i)]
+                terms += [(dt * Ah[i, j], iv(QGl[j])) for j in range(i)]
             if qsep is not None:
                 for m, phi in enumerate(qsep):
                     terms.append((sum(dt * Ah[i, j] * qfac[j][m] for j in range(i)), iv(phi)))
@@ -1029,7 +1046,7 @@ class TimeStepper:
         w = pair.bhat - Ah[s - 1]
         terms = [(1.0, ui)]
         if QG is not None:
-            terms += [(dt * w[j], QG[j]) for j in range(s)]
+            terms += [(dt * w[j], QGl[j]) for j in range(s)]
         if qsep is not None:
             for m, phi in enumerate(qsep):
                 terms.append((sum(dt * w[j] * qfac[j][m] for j in range(s)), phi))
