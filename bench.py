@@ -92,12 +92,14 @@ def make_problem(mod, cfg):
     if kind == "allen_cahn":
         coef = sine_modes(0)
         return dict(coeffs=mod.OperatorCoefficients(c11=0.01, c22=0.01),
-                    g=lambda t, u, ux, uy: u - u ** 3, u0=lambda pts: sine_field(coef, pts),
+                    g=mod.declare_nonlinear(lambda t, u, ux, uy: u - u ** 3, ux=False, uy=False, pure=True),
+                    u0=lambda pts: sine_field(coef, pts),
                     time_independent_bc=True)
     if kind == "burgers_var":
         coef = sine_modes(1)
         return dict(coeffs=mod.OperatorCoefficients(**c4_fields()),
-                    g=lambda t, u, ux, uy: -u * ux, u0=lambda pts: sine_field(coef, pts),
+                    g=mod.declare_nonlinear(lambda t, u, ux, uy: -u * ux, ux=True, uy=False, pure=True),
+                    u0=lambda pts: sine_field(coef, pts),
                     time_independent_bc=True)
     if kind == "ensemble":
         coef = sine_modes(2, k=cfg["k"])
@@ -240,11 +242,13 @@ def _time_solves(st, n, sharded=False):
             times.append((e0, e1))
         torch.cuda.synchronize()
         return [a.elapsed_time(b) for a, b in times]
-    st.ops.solve_device(fb, r, out)
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    from paper_2306_02526_b200.solver import graph_workspace
+    with graph_workspace("bench-solve"):     # the graph's workspace, allocated by the warm solve
         st.ops.solve_device(fb, r, out)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            st.ops.solve_device(fb, r, out)
     g.replay()
     torch.cuda.synchronize()
     times = []
@@ -281,10 +285,11 @@ def profiled_traffic(config):
 # CPU oracle timing (cpu_baseline and --impl reference)
 # ---------------------------------------------------------------------------
 
-def cpu_oracle_sample(cfg, steps, warmup):
-    """Times the oracle port on the SAMPLE_N x SAMPLE_N subtree of the config."""
+def oracle_stepper(cfg, n=None, record=False):
+    """The CPU oracle's stepper of the config (n x n leaves; default the
+    config's own n): (tree, stepper, initial state).  Checker / CPU baseline only."""
     from oracle import hps_oracle as O  # checker / CPU baseline only
-    n = min(SAMPLE_N, cfg["n"])
+    n = cfg["n"] if n is None else n
     tree = O.OTree(((0.0, 1.0), (0.0, 1.0)), n, n, cfg["p"])
     kind = cfg["kind"]
     kw = {}
@@ -305,7 +310,14 @@ def cpu_oracle_sample(cfg, steps, warmup):
         coef = sine_modes(2, k=cfg["k"])
         kw = dict(q=lambda t, pts: sine_field(coef, pts), ncomp=cfg["k"])
         u = np.zeros((cfg["k"], tree.N))
-    st = O.OStepper(tree, coeffs, O.ark4_tableau(), cfg["dt"], **kw)
+    st = O.OStepper(tree, coeffs, O.ark4_tableau(), cfg["dt"], record=record, **kw)
+    return tree, st, u
+
+
+def cpu_oracle_sample(cfg, steps, warmup):
+    """Times the oracle port on the SAMPLE_N x SAMPLE_N subtree of the config."""
+    n = min(SAMPLE_N, cfg["n"])
+    tree, st, u = oracle_stepper(cfg, n)
     t = 0.0
     for _ in range(warmup):
         t, u = st.run(t, u, 1)

@@ -13,7 +13,7 @@ from .operators import EllipticDiscretization, LeafStencil, OperatorCoefficients
 from .solver import HpsOperatorSet, build
 from .tableaux import ButcherPair, available_tableaux, load_tableau
 from .timestep import (ParabolicProblem, SeparableField, StepperState, TimeStepper,
-                       evaluate_nonlinear)
+                       declare_nonlinear, evaluate_nonlinear, gradient_use, is_pure)
 from .tree import DomainTree, TreeNode, build_tree
 from .stability import StepMapSpectrum, analyze, assemble_step_map
 from .sharding import ShardedTimeStepper
@@ -27,5 +27,6 @@ __all__ = [
     "OperatorCoefficients", "shift_reaction", "HpsOperatorSet", "build", "DomainTree",
     "TreeNode", "build_tree", "ButcherPair", "available_tableaux", "load_tableau",
     "ParabolicProblem", "SeparableField", "StepperState", "TimeStepper", "evaluate_nonlinear",
+    "declare_nonlinear", "gradient_use", "is_pure",
     "StepMapSpectrum", "analyze", "assemble_step_map", "ShardedTimeStepper",
 ]

@@ -75,9 +75,10 @@ struct MSeg {
 
 struct MProg {
   int nseg, ntasks;
-  int head, dedicated;          // the first `head` tasks (the root's down product) run on the last
-                                // `dedicated` CTAs first; every other task is taken by ticket
-  unsigned* ticket;             // next task after the head (reset at exit)
+  int head, ratio;              // the first `head` tasks (the root's down product, no inputs) are
+                                // interleaved with the others in ticket order: one head task after
+                                // every `ratio` others until the head is exhausted (see task_of)
+  unsigned* ticket;             // next ticket (reset at exit)
   unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / staged /
                                 // streamed / emitted / end, ns (MTS stamps)
   unsigned* reset; int nreset;  // counters to zero at exit (incl. the exit counter at the end)
@@ -122,6 +123,19 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+// Ticket -> task.  Every CTA takes tickets in increasing order, so a task
+// must depend only on tasks with lower tickets: then the lowest unfinished
+// ticket is always held by a running CTA whose inputs are complete, and the
+// launch makes progress whatever subset of its CTAs is resident (a kernel on
+// another stream may hold SMs).  The head tasks depend on nothing; the host
+// picks `ratio` so that every head ticket precedes the first task that reads
+// the head's results.
+__device__ __forceinline__ int task_of(int x, int head, int ratio) {
+  const int per = ratio + 1;
+  if (x >= per * head) return x;
+  return x % per == ratio ? x / per : head + x - x / per;
+}
+
 // PN: per-node operators -- a task's 64 rows tile the level's row space
 // (node * R + r) and may span up to MNB nodes; NG = 1
 template <bool PN>
@@ -132,21 +146,13 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
   __shared__ unsigned s_last;
   const int tid = threadIdx.x, grp = tid >> 5, q = tid & 31;
   pdl_wait();
-  const int G = gridDim.x, KR = p.dedicated;
-  const bool ded = KR > 0 && (int)blockIdx.x >= G - KR;
-  // the dedicated CTAs first take the head tasks round-robin, then every CTA
-  // takes the remaining tasks in list order from a ticket counter (each task
-  // depends only on lower-numbered ones, all taken by resident CTAs)
   __shared__ int s_ticket;
-  int t = ded ? (int)blockIdx.x - (G - KR) : p.ntasks;
   for (;;) {
-    if (!(ded && t < p.head)) {
-      __syncthreads();
-      if (tid == 0) s_ticket = p.head + (int)atomicAdd(p.ticket, 1u);
-      __syncthreads();
-      t = s_ticket;
-      if (t >= p.ntasks) break;
-    }
+    __syncthreads();
+    if (tid == 0) s_ticket = (int)atomicAdd(p.ticket, 1u);
+    __syncthreads();
+    if (s_ticket >= p.ntasks) break;
+    const int t = task_of(s_ticket, p.head, p.ratio);
     int si = 0;
     while (t >= p.s[si].task0 + p.s[si].ntasks) ++si;
     const MSeg& g = p.s[si];
@@ -352,7 +358,6 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     __syncthreads();  // xs / red / sidx are reused by the next task
     if (p.trace && tid == 0) p.trace[MTS * t + 5] = gtime();
-    if (ded && t < p.head) t += KR;
   }
   // the last CTA out resets the counters for the next solve
   __syncthreads();
@@ -513,10 +518,8 @@ bool mega_enabled() {
 int mega_depth(const Ops& ops) {
   const Plan& P = *ops.plan;
   if (ops.shared_levels) return P.depth;
-  static const double cap = [] {
-    const char* e = getenv("HPSB_PN_MEGA_MB");
-    return (e ? atof(e) : 256.0) * 1048576.0;
-  }();
+  const char* e = getenv("HPSB_PN_MEGA_MB");  // read per call: tests lower it to exercise k_panel
+  const double cap = (e ? atof(e) : 256.0) * 1048576.0;
   int d = 0;
   for (; d < P.depth; ++d) {
     const Level& lv = P.lv[d];
@@ -689,10 +692,15 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     max_ctas = std::max(1, per_sm) * sms;
   }
   int grid = std::min(max_ctas, p.ntasks);
-  if (pair) {  // a quarter of the CTAs stream the root's down product while the up sweep climbs
+  if (pair) {  // about a quarter of the tickets stream the root's down product while the up sweep climbs
     grid = max_ctas;
     p.head = p.s[iroot_dn].ntasks;
-    p.dedicated = std::max(1, grid / 4);
+    // the first task reading the head's results: level 1's down segment (or the
+    // end of the list); every head ticket must precede it
+    int first_dep = p.ntasks;
+    for (int i = 0; i < p.nseg; ++i)
+      if (!p.s[i].up && p.s[i].wpar == p.s[iroot_dn].done && i != iroot_dn) first_dep = std::min(first_dep, p.s[i].task0);
+    p.ratio = std::min(3, (first_dep - p.head) / std::max(1, p.head));
   }
   const char* tr = getenv("HPSB_MEGA_TRACE");  // debug: per-task timeline appended to this file
   unsigned long long* dtrace = nullptr;

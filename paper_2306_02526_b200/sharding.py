@@ -25,7 +25,7 @@ GPUs; gloo for the CPU tests, staging CUDA tensors through the host).
 import numpy as np
 
 from .errors import UnsupportedConfigurationError
-from .timestep import ParabolicProblem, SeparableField, TimeStepper, _call_g
+from .timestep import ParabolicProblem, SeparableField, TimeStepper, _call_g, gradient_use, is_pure
 
 
 def member_slice(k, rank, world):
@@ -237,22 +237,6 @@ def reduce_max(t, group=None):
     return work.to(t.device) if staged else work
 
 
-class _SegmentedGraph:
-    """A captured step cut at its collectives: graph segments replayed in
-    order with each cut's collective issued eagerly in between (the
-    collectives run on NCCL's own streams, ordered after the segment before
-    and before the segment after by the current stream)."""
-
-    def __init__(self):
-        self.parts = []          # (CUDAGraph, collective or None)
-
-    def replay(self):
-        for g, fn in self.parts:
-            g.replay()
-            if fn is not None:
-                fn()
-
-
 class ShardedTimeStepper(TimeStepper):
     """The stage-formulation (and backward-Euler) stepper of one problem
     sharded by subtrees over the ranks of a process group, one GPU each
@@ -289,44 +273,6 @@ class ShardedTimeStepper(TimeStepper):
         self._top_ids = torch.as_tensor(P.top_ids, dtype=torch.long, device=self._dev)
         self._owned = torch.as_tensor(P.owned_ids(*self._parts, with_top=self._rank == 0), dtype=torch.long,
                                       device=self._dev)
-
-    # -- capture with the collectives between graph segments ------------------------------
-    _seg = None
-
-    def _capture_graph(self, body):
-        import torch
-        seg = _SegmentedGraph()
-        stream = torch.cuda.Stream()
-        stream.wait_stream(torch.cuda.current_stream())
-        self._seg = dict(graph=seg, pool=torch.cuda.graph_pool_handle(), cur=None)
-        try:
-            with torch.cuda.stream(stream):
-                self._seg_begin()
-                body()
-                self._seg_end(None)
-        finally:
-            self._seg = None
-            torch.cuda.current_stream().wait_stream(stream)
-        return seg
-
-    def _seg_begin(self):
-        import torch
-        g = torch.cuda.CUDAGraph()
-        g.capture_begin(pool=self._seg["pool"])
-        self._seg["cur"] = g
-
-    def _seg_end(self, fn):
-        g = self._seg["cur"]
-        g.capture_end()
-        self._seg["graph"].parts.append((g, fn))
-
-    def _collective(self, fn):
-        """Run ``fn`` now, or while a step is being captured, cut the graph there."""
-        if self._seg is None:
-            fn()
-        else:
-            self._seg_end(fn)
-            self._seg_begin()
 
     # buffers start at zero: DOFs other ranks own are never written here and
     # must stay finite for the (range-wise) combinations and guards
@@ -381,11 +327,19 @@ class ShardedTimeStepper(TimeStepper):
         res = out if out is not None else self._buf("gval", U.shape)
         if self._dry:
             return res
-        self._dd.eval(U, ux=ux, uy=uy, leaves=self._leaves)
-        if self._world > 1:
-            self._collective(lambda: complete_edges([ux, uy], self._top_ids, self._group))
-        for a, b in self._ranges():
-            res[:, a:b].copy_(_call_g(self.problem.g, t, U[:, a:b], ux[:, a:b], uy[:, a:b]))
+        g = self.problem.g
+        if any(gradient_use(g)):
+            self._dd.eval(U, ux=ux, uy=uy, leaves=self._leaves)
+            if self._world > 1:
+                self._eager(lambda: complete_edges([ux, uy], self._top_ids, self._group))
+
+        def fill(tt):
+            for a, b in self._ranges():
+                res[:, a:b].copy_(_call_g(g, tt, U[:, a:b], ux[:, a:b], uy[:, a:b]))
+        if self._seg is not None and not is_pure(g):   # cut: g runs at every replay
+            self._eager(lambda tc=t: fill(self._replay_t + tc))
+        else:
+            fill(t)
         return res
 
     def _solve(self, ops, fb, body, out, jump=None, inv_dt=None):
@@ -403,7 +357,7 @@ class ShardedTimeStepper(TimeStepper):
         ops.solve_phase(_lib.HPS_PHASE_UP, p0, p1, fb, body, out)
         if self._world > 1:
             block = ops.plan.flux_block(out.shape[0])
-            self._collective(lambda: exchange_fluxes(block, p0, p1, self._group))
+            self._eager(lambda: exchange_fluxes(block, p0, p1, self._group))
         ops.solve_phase(_lib.HPS_PHASE_TOP | _lib.HPS_PHASE_DOWN, p0, p1, fb, body, out)
         if tm is not None:
             e1.record()

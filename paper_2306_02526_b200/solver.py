@@ -9,10 +9,12 @@ the GPU (no CPU fallback): numpy inputs are copied to the device and the
 result copied back; torch CUDA tensors stay on the device.
 """
 
+import contextlib
 import ctypes
 import hashlib
 import json
 import os
+import threading
 
 import numpy as np
 
@@ -22,6 +24,34 @@ from .errors import HpstepError, InvalidStepError
 from .operators import EllipticDiscretization
 
 FORMAT_VERSION = 1
+
+# Solve workspaces (level fluxes, w3, split partials, dataflow counters) are
+# per plan and per stream, so solves on different streams never share one
+# (solver.py:84-89: solves are re-entrant and concurrent-safe).  A captured
+# CUDA graph owns its own workspace instead: it replays on whatever stream
+# the caller uses, so its key is the capturing owner's token
+# (graph_workspace), set for the warm pass that precedes the capture (which
+# allocates it outside the capture) and for the capture itself.
+_tls = threading.local()
+
+
+@contextlib.contextmanager
+def graph_workspace(token):
+    prev = getattr(_tls, "graph", None)
+    _tls.graph = ("graph", token)
+    try:
+        yield
+    finally:
+        _tls.graph = prev
+
+
+def _workspace_key(k):
+    tok = getattr(_tls, "graph", None)
+    if tok is not None:
+        return (k, tok)
+    if torch.cuda.is_current_stream_capturing():
+        return (k, ("graph", None))
+    return (k, current_stream_handle())
 
 
 class DevicePlan:
@@ -75,11 +105,14 @@ class DevicePlan:
         self.boundary_ids = torch.as_tensor(tree.boundary_ids, device=dev)
 
     def workspace(self, k):
-        ws = self._ws.get(k)
+        """The solve workspace of ``k`` right-hand sides for the current
+        stream (or the graph being captured / warmed, see graph_workspace)."""
+        key = _workspace_key(k)
+        ws = self._ws.get(key)
         if ws is None:
             nbytes = self._lib.hps_solve_workspace_bytes(self.handle, k)
             ws = torch.zeros(nbytes, dtype=torch.uint8, device=cuda_device())  # split-K semaphores start at 0
-            self._ws[k] = ws
+            self._ws[key] = ws
         return ws
 
     def flux_block(self, k):
@@ -138,7 +171,7 @@ class HpsOperatorSet:
     """Per-node HPS operators of ``sigma*I + dt_gamma*A``, resident on the GPU.
 
     Read-only after construction; concurrent solves on different streams are
-    safe (each stream gets its own workspace).
+    safe (each stream gets its own workspace, ``DevicePlan.workspace``).
     """
 
     def __init__(self, disc, sigma, dt_gamma, keep_dtn=False, threads=None, layout=None, nparts=1):

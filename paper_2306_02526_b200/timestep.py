@@ -31,6 +31,7 @@ formulations (timestep.py:268-328) reuse the same device pieces.
 import ctypes
 import gc
 import os
+import sys
 
 import numpy as np
 
@@ -38,7 +39,7 @@ from . import _lib
 from .device import cuda_device, current_stream_handle, torch
 from .errors import DivergenceError, HpstepError, UnsupportedConfigurationError
 from .operators import EllipticDiscretization
-from .solver import HpsOperatorSet, device_plan
+from .solver import HpsOperatorSet, device_plan, graph_workspace
 from .tableaux import ButcherPair, load_tableau
 
 DIVERGENCE_LIMIT = 1e12
@@ -331,6 +332,48 @@ def evaluate_nonlinear(disc, problem, t, u):
     return out.cpu().numpy() if as_numpy else out
 
 
+def gradient_use(g):
+    """Which gradient components ``g(t, u, u_x, u_y)`` reads: ``(True, True)``
+    unless ``g`` declares otherwise through :func:`declare_nonlinear`."""
+    use = getattr(g, "grad_use", None)
+    return (True, True) if use is None else (bool(use[0]), bool(use[1]))
+
+
+def is_pure(g):
+    """Whether ``g`` is declared a pure device function (see declare_nonlinear)."""
+    return bool(getattr(g, "pure", False))
+
+
+def declare_nonlinear(g, ux=True, uy=True, pure=False):
+    """Declare properties of a nonlinear term ``g(t, u, u_x, u_y)`` that the
+    device stepper may exploit (an extension of the reference API, which
+    always evaluates both gradient components, timestep.py:192-196, and
+    calls g afresh every stage).  Returns ``g``, so it can wrap a lambda.
+
+    * ``ux`` / ``uy`` False: that gradient component is never read; it is
+      not computed and ``g`` receives a buffer of unspecified contents.
+    * ``pure`` True: ``g`` is a fixed composition of torch operations on its
+      device tensor arguments -- independent of ``t``, of host state and of
+      data-dependent Python control flow -- so the step's CUDA graph may
+      capture it.  Undeclared terms are called eagerly at every stage (the
+      captured step is cut around them), with the stage time of that step.
+
+    A declaration is the caller's promise for every (t, u)."""
+    try:
+        g.grad_use = (bool(ux), bool(uy))
+        g.pure = bool(pure)
+    except AttributeError as e:
+        raise TypeError(f"cannot attach a declaration to {g!r}") from e
+    return g
+
+
+def _is_fresh(r, refs):
+    """Whether the tensor ``r`` a call returned owns fresh storage.  ``refs``
+    counts the references to ``r`` including the caller's own: a cast copies;
+    otherwise ``r`` must not be a view and nobody else may hold it."""
+    return r.dtype != torch.float64 or (refs <= 1 and r._base is None)
+
+
 def _call_g(g, t, U, ux, uy):
     """g on device tensors when it accepts them, else on host copies."""
     if getattr(g, "_hb_torch", True):
@@ -341,7 +384,15 @@ def _call_g(g, t, U, ux, uy):
                     g._hb_torch = True
                 except AttributeError:
                     pass
-                return torch.broadcast_to(r.to(torch.float64), U.shape)
+                # a tensor nobody else references that is not a view of other
+                # storage is g's own fresh result: it may serve as stage-history
+                # storage (no copy); anything else (u, u_x, a persistent out=
+                # buffer, a view) is copied by the caller
+                refs = sys.getrefcount(r) - 1     # alone in a statement: no stack reference
+                fresh = _is_fresh(r, refs)
+                out = torch.broadcast_to(r.to(torch.float64), U.shape)
+                out._hb_fresh = fresh
+                return out
         except Exception:
             pass
         try:
@@ -358,6 +409,21 @@ def _call_g(g, t, U, ux, uy):
 
 class _CaptureFailed(Exception):
     pass
+
+
+class _SegmentedGraph:
+    """A captured step cut at its host work: graph segments replayed in order
+    with each cut's host function (a nonlinear term, a field evaluation, a
+    collective) run eagerly in between, on the replaying stream."""
+
+    def __init__(self):
+        self.parts = []          # (CUDAGraph, host function or None)
+
+    def replay(self):
+        for g, fn in self.parts:
+            g.replay()
+            if fn is not None:
+                fn()
 
 
 class _Field:
@@ -377,13 +443,26 @@ class _Field:
         a = a.reshape(self.k, self.n) if (a.ndim > 1 or self.k == 1) else a.reshape(1, self.n)
         return torch.as_tensor(np.ascontiguousarray(a), device=self.dev)
 
+    stepper = None     # the TimeStepper whose step may be captured (host evaluations become cuts)
+
+    def _host_value(self, t):
+        """F(t) of a non-separable F: evaluated on the host now, or -- while a
+        step is captured -- at this point of every replay, with the replayed
+        step's time (the captured step is cut here)."""
+        st = self.stepper
+        if st is not None and st._dry:
+            return st._dummy((1, self.n))
+        if st is not None and st._seg is not None:
+            return st._cut_field(self, t)
+        return self._stack(self.fn(t, self.pts))
+
     def terms(self, t, scale=1.0):
         """(coef, tensor) terms of scale*F(t); evaluates non-separable F now."""
         if self.fn is None:
             return []
         if self.sep is not None:
             return [(scale * f, phi) for f, phi in zip(self.fn.factors(t), self.sep)]
-        return [(scale, self._stack(self.fn(t, self.pts)))]
+        return [(scale, self._host_value(t))]
 
     def values(self, times):
         """(len(times), n) tensor of F at each time in one launch, for a
@@ -402,7 +481,7 @@ class _Field:
             out = torch.empty((rows, self.n), dtype=torch.float64, device=self.dev) \
                 if out is None else out
             return combine(self.terms(t), out)
-        return self._stack(self.fn(t, self.pts))
+        return self._host_value(t)
 
 
 class TimeStepper:
@@ -447,7 +526,12 @@ class TimeStepper:
         self._Ft = _Field(None if problem.time_independent_bc else problem.f_t, self._bnd_pts, k,
                           self._dev)
         self._Q = _Field(problem.q, self._all_pts, k, self._dev)
+        for F in (self._F, self._Ft, self._Q):
+            F.stepper = self
         self._bufs = {}
+        self._seg = None           # while a step is captured: the graph segments (see _eager)
+        self._replay_t = 0.0       # time of the step being replayed (host work at the cuts)
+        self._cut_bufs = []
         # the leaf-interior DOF range this process steps (everything on one GPU;
         # a subtree part range in sharding.ShardedTimeStepper)
         self._ir = (0, self._dd.Lni)
@@ -502,50 +586,55 @@ class TimeStepper:
 
     def _g(self, t, U, out=None):
         """g(t, U) with the interface-averaged device gradient (timestep.py:192-196).
-        The gradient is not evaluated for a g that reads neither component
-        (found by one probe per g, see _probe_grad_use)."""
+        The gradient is always evaluated, as the reference does, unless g
+        declares that it reads neither component (:func:`declare_nonlinear`).
+        While a step is captured, a g not declared pure is cut out of the graph:
+        it runs at every replay with that step's stage time, into ``out`` (or a
+        buffer of its own)."""
         if self.problem.g is None:
             return None
         ux, uy = self._buf("gx", U.shape), self._buf("gy", U.shape)
         if self._dry:
-            return ux
+            return ux if out is None else out
         g = self.problem.g
-        use = getattr(g, "_hb_grad_use", None) if getattr(g, "_hb_torch", None) is True else None
-        if use is None or any(use):  # both components: one pass of the gradient kernel
+        if any(gradient_use(g)):  # both components: one pass of the gradient kernel
             self._dd.eval(U, ux=ux, uy=uy)
+        if self._seg is not None and not is_pure(g):
+            tgt = out if out is not None else self._cut_buf(tuple(U.shape))
+            self._eager(lambda tc=t: tgt.copy_(_call_g(g, self._replay_t + tc, U, ux, uy)))
+            return tgt
         r = _call_g(g, t, U, ux, uy)
-        if use is None and getattr(g, "_hb_torch", None) is True and \
-                os.environ.get("HPSB_NO_GRAD_PROBE") != "1" and not torch.cuda.is_current_stream_capturing():
-            self._probe_grad_use(g, t, U, ux, uy, r)
         if out is not None:
             out.copy_(r)
             return out
         return r
 
-    @staticmethod
-    def _probe_grad_use(g, t, U, ux, uy, r):
-        """Whether g reads ux / uy: g must return bitwise the same result with
-        the component replaced by NaNs and by random values (a g that reads it
-        cannot); any failure or difference counts as a use."""
-        use = []
-        gen = torch.Generator(device=U.device).manual_seed(12345)
-        for i in range(2):
-            used = False
-            for fill in ("nan", "rand"):
-                d = torch.full_like(ux, float("nan")) if fill == "nan" else \
-                    torch.randn(ux.shape, generator=gen, dtype=ux.dtype, device=ux.device)
-                args = (d, uy) if i == 0 else (ux, d)
-                try:
-                    rr = g(t, U, *args)
-                    rr = torch.broadcast_to(rr.to(torch.float64), U.shape)
-                    used = used or not torch.equal(rr, r)
-                except Exception:
-                    used = True
-            use.append(used)
-        try:
-            g._hb_grad_use = tuple(use)
-        except AttributeError:
-            pass
+    # -- host work inside a captured step: the graph is cut there ------------------------
+    def _eager(self, fn):
+        """Run ``fn`` now; while a step is being captured, cut the graph here
+        and run ``fn`` at this point of every replay instead."""
+        if self._seg is None:
+            fn()
+        else:
+            self._seg_end(fn)
+            self._seg_begin()
+
+    def _cut_buf(self, shape):
+        """A persistent buffer for the result of one cut (allocated from the
+        capture's pool; lives as long as the stepper)."""
+        b = torch.empty(shape, dtype=torch.float64, device=self._dev)
+        self._cut_bufs.append(b)
+        return b
+
+    def _cut_field(self, F, t):
+        a = np.asarray(F.fn(t, F.pts), dtype=float)      # shape only (host)
+        rows = F.k if (a.ndim > 1 or F.k == 1) else 1
+        tgt = self._cut_buf((rows, F.n))
+        self._eager(lambda tc=t: tgt.copy_(F._stack(F.fn(self._replay_t + tc, F.pts))))
+        return tgt
+
+    def _dummy(self, shape):
+        return self._buf("dummy%dx%d" % shape, shape)
 
     def initial_state(self):
         u0 = np.asarray(self.problem.u0(self._all_pts), dtype=float)
@@ -570,7 +659,7 @@ class TimeStepper:
         """``nsteps`` steps; the divergence guard is read back once per
         ``check_every`` steps (the first failing step is reported exactly)."""
         g = self.problem.g
-        if nsteps > 1 and g is not None and getattr(g, "_hb_torch", None) is None and \
+        if nsteps > 1 and g is not None and is_pure(g) and getattr(g, "_hb_torch", None) is None and \
                 self._graph_eligible(probe=True):
             state = self.step(state)           # one eager step probes g on device tensors
             nsteps -= 1
@@ -590,18 +679,17 @@ class TimeStepper:
 
     # -- CUDA-graph stepping -------------------------------------------------------------
     def _graph_eligible(self, probe=False):
-        """One step is captured once and replayed when every field is device
-        resident (SeparableField or None), g runs on device tensors (probed by
-        an eager step), and the formulation is the stage one or BE."""
+        """One step is captured once and replayed for the stage formulation and
+        BE.  Field callables other than SeparableField and a g not declared
+        pure run on the host / eagerly at cuts of the captured step; a g
+        declared pure is captured and must run on device tensors (probed by an
+        eager step)."""
         if os.environ.get("HPSB_NO_GRAPH") == "1" or self.solve_timer is not None or self._graph_failed:
             return False
         if self.pair.s > 1 and self.formulation != "stage":
             return False
-        for F in (self._F, self._Q):
-            if F.fn is not None and F.sep is None:
-                return False
         g = self.problem.g
-        return g is None or probe or getattr(g, "_hb_torch", None) is True
+        return g is None or not is_pure(g) or probe or getattr(g, "_hb_torch", None) is True
 
     def _step_body(self, t, u, guards, out):
         if self.pair.s == 1:
@@ -622,42 +710,79 @@ class TimeStepper:
         vals = self._dry_coefs(t, gin, guards)
         coef = torch.zeros(len(vals) + 8, dtype=torch.float64, device=dev)
         coef[:len(vals)] = torch.as_tensor(vals, dtype=torch.float64)
-        # warm the captured code path once (kernel attributes, workspaces) on scratch data
+        # warm the captured code path once (kernel attributes, workspaces) on scratch
+        # data; the warm pass and the capture use this stepper's graph workspaces
+        # (allocated here, outside the capture)
         scratch = gin.clone()
-        _CoefSink.current = _CoefSink(dev=coef)
-        try:
-            self._step_body(t, scratch, guards, scratch)
-        finally:
-            _CoefSink.current = None
-        torch.cuda.synchronize()
-
-        def body():
+        with graph_workspace(id(self)):
             _CoefSink.current = _CoefSink(dev=coef)
             try:
-                guards.zero_()
-                self._step_body(t, gin, guards, gin)
+                self._step_body(t, scratch, guards, scratch)
             finally:
                 _CoefSink.current = None
+            torch.cuda.synchronize()
 
-        # a finalizer that frees device memory (an operator set or plan collected
-        # by the GC) would invalidate the capture: collect now, none during it
-        gc.collect()
-        gc.disable()
-        try:
-            graph = self._capture_graph(body)
-        finally:
-            gc.enable()
+            def body():
+                # captured at t = 0: the time enters only through the coefficient
+                # table (recomputed per replay) and the cuts, which evaluate at
+                # replay time t_step + (stage offset), the reference's t + c_i dt
+                _CoefSink.current = _CoefSink(dev=coef)
+                try:
+                    guards.zero_()
+                    self._step_body(0.0, gin, guards, gin)
+                finally:
+                    _CoefSink.current = None
+
+            # a finalizer that frees device memory (an operator set or plan collected
+            # by the GC) would invalidate the capture: collect now, none during it
+            gc.collect()
+            gc.disable()
+            try:
+                graph = self._capture_graph(body)
+            finally:
+                gc.enable()
         ring = 4
         self._graph = dict(graph=graph, gin=gin, guards=guards, coef=coef, ncoef=len(vals), key=self._graph_key(gin),
                            pinned=[torch.zeros(len(vals) + 8, dtype=torch.float64).pin_memory() for _ in range(ring)],
                            events=[None] * ring, slot=0)
 
     def _capture_graph(self, body):
-        """One CUDA graph of ``body`` (anything with ``replay()``)."""
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            body()
-        return graph
+        """``body`` captured as CUDA-graph segments cut at its host work
+        (``_eager``: a nonlinear term not declared pure, a field callable, a
+        collective); returns an object whose ``replay()`` replays the segments
+        in order with the host work in between."""
+        seg = _SegmentedGraph()
+        stream = torch.cuda.Stream()
+        stream.wait_stream(torch.cuda.current_stream())
+        self._seg = dict(graph=seg, pool=torch.cuda.graph_pool_handle(), cur=None)
+        try:
+            with torch.cuda.stream(stream):
+                self._seg_begin()
+                body()
+                self._seg_end(None)
+        except Exception:
+            cur = self._seg["cur"]
+            if cur is not None:
+                try:
+                    cur.capture_end()
+                except Exception:
+                    pass
+            raise
+        finally:
+            self._seg = None
+            torch.cuda.current_stream().wait_stream(stream)
+        return seg
+
+    def _seg_begin(self):
+        g = torch.cuda.CUDAGraph()
+        g.capture_begin(pool=self._seg["pool"])
+        self._seg["cur"] = g
+
+    def _seg_end(self, fn):
+        g = self._seg["cur"]
+        self._seg["cur"] = None
+        g.capture_end()
+        self._seg["graph"].parts.append((g, fn))
 
     def _graph_key(self, u):
         return (tuple(u.shape), self.dt, id(self.ops))
@@ -698,6 +823,7 @@ class TimeStepper:
             ev = torch.cuda.Event()
             ev.record()
             G["events"][slot] = ev
+            self._replay_t = t
             G["graph"].replay()
             hist[(step - done) % hist.shape[0]].copy_(guards)
             t += self.dt
@@ -774,6 +900,7 @@ class TimeStepper:
         ev = torch.cuda.Event()
         ev.record()
         G["events"][cslot] = ev
+        self._replay_t = t
         G["graph"].replay()
         io["pending"].append(guards.clone())
         done = torch.cuda.Event()
@@ -983,26 +1110,33 @@ class TimeStepper:
         def stage_q_g(i, ti, ui):
             if qsep is not None:
                 qfac.append(self._Q.fn.factors(ti))
-            if QG is not None:
-                terms = [] if qsep is not None else self._Q.terms(ti)
-                G = self._g(ti, ui)
-                if G is not None:
-                    terms.append((1.0, G))
-                if len(terms) == 1 and terms[0][0] == 1.0 and self._qg_alias_ok():
-                    G = terms[0][1]
-                    if G.shape == QG[i].shape and G.is_contiguous():
-                        QGl[i] = G                   # g's result as the history itself (no copy)
-                    else:
-                        QGl[i] = QG[i]
-                        if not self._dry:
-                            QG[i].copy_(G)
-                elif terms:
-                    QGl[i] = QG[i]
-                    self._owned_combine(terms, QG[i])
+            if QG is None:
+                return
+            terms = [] if qsep is not None else self._Q.terms(ti)
+            # g alone: written straight into the history row when it runs at a
+            # cut of the captured step; otherwise its own fresh result may serve
+            # as the row (no copy) -- storage g reuses (u, u_x, an out= buffer)
+            # is overwritten by later stages and is copied
+            G = self._g(ti, ui, out=QG[i] if not terms and self._seg is not None else None)
+            if G is not None:
+                terms.append((1.0, G))
+            if len(terms) == 1 and terms[0][0] == 1.0 and G is not None:
+                if G is QG[i]:
+                    QGl[i] = G
+                elif self._qg_alias_ok() and getattr(G, "_hb_fresh", False) and G.shape == QG[i].shape \
+                        and G.is_contiguous():
+                    QGl[i] = G
                 else:
                     QGl[i] = QG[i]
                     if not self._dry:
-                        QG[i].zero_()
+                        QG[i].copy_(G)
+            elif terms:
+                QGl[i] = QG[i]
+                self._owned_combine(terms, QG[i])
+            else:
+                QGl[i] = QG[i]
+                if not self._dry:
+                    QG[i].zero_()
 
         # boundary data of stages 1..s-1 and of t + dt, one launch when f is separable
         bcs = self._F.values([t + pair.c[i] * dt for i in range(1, s)] + [t + dt]) \

@@ -1,0 +1,112 @@
+"""Parity at the benchmarked configurations (BASELINE.json C2-C5), through the
+exact code path ``bench.py`` times, against the CPU oracle run on the box.
+
+* C2 at full size (128x128 leaves, p=16, N = 3,673,600): every stage solve
+  of the first ARK4 step (the fused stage solves forming their body load
+  from the stage terms, the per-step root Dirichlet product, the dataflow
+  kernel with its full node groups and splits) and the state after a
+  captured-graph step, against the oracle (reference solver.py:201-276,
+  timestep.py:237-266);
+* C3's recipe (Allen-Cahn, pure g without gradient) at 64x64 p=12;
+* C4's recipe (variable coefficients, per-node operators, Burgers g) at
+  64x64 p=10, once with the default wide-level dataflow kernel and once with
+  the per-level split-K panel launches forced (HPSB_PN_MEGA_MB), the path
+  C4's full size takes;
+* C5's recipe (64 members, multi-rhs level GEMMs) at 16x16 p=16.
+Tolerance: the north-star 1e-10 relative L2, per stage and per step.
+Needs a B200 (and a few minutes of host time for the C2 oracle)."""
+
+import numpy as np
+import pytest
+
+import bench
+from tests.problems import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10
+
+
+def _record_stages(st, stages):
+    """Hook the operator set's stage-solve entry points: every stage solve's
+    output is appended to ``stages`` (eager stepping only)."""
+    ops = st.ops
+    names = ("solve_device", "solve_stage_device", "solve_stage_terms_device")
+    orig = {n: getattr(ops, n) for n in names}
+
+    def wrap(name, out_pos):
+        def f(*a, **kw):
+            r = orig[name](*a, **kw)
+            stages.append(a[out_pos].cpu().numpy().copy())
+            return r
+        return f
+    ops.solve_device = wrap("solve_device", 2)
+    ops.solve_stage_device = wrap("solve_stage_device", 2)
+    ops.solve_stage_terms_device = wrap("solve_stage_terms_device", 4)
+
+    def restore():
+        for n in names:
+            setattr(ops, n, orig[n])
+    return restore
+
+
+def _gpu_stepper(cfg, n):
+    import paper_2306_02526_b200 as hb
+    c = dict(cfg, n=n)
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), n, n, c["p"])
+    prob = hb.ParabolicProblem(**bench.make_problem(hb, c))
+    return tree, hb.TimeStepper(tree, prob, "ARK4", dt=c["dt"])
+
+
+def _run_config(cfg, n, steps, monkeypatch, check_stages=True):
+    import paper_2306_02526_b200 as hb
+    tree, st = _gpu_stepper(cfg, n)
+    _, ost, u0 = bench.oracle_stepper(cfg, n, record=True)
+    s0 = st.initial_state()
+    assert rel_l2(np.asarray(s0.u), u0) == 0.0 or rel_l2(np.asarray(s0.u), u0) < 1e-15
+    # step 1 eagerly with every stage solve recorded, then the captured graph
+    monkeypatch.setenv("HPSB_NO_GRAPH", "1")
+    stages = []
+    restore = _record_stages(st, stages)
+    s = st.step(s0)
+    restore()
+    monkeypatch.delenv("HPSB_NO_GRAPH")
+    t, u = 0.0, u0
+    t, u = ost.run(t, u, 1)
+    if check_stages:
+        assert len(stages) == len(ost.stages) == 5
+        for i, (a, b) in enumerate(zip(stages, ost.stages)):
+            assert rel_l2(a, np.asarray(b).reshape(a.shape)) < TOL, f"stage {i + 1}"
+    assert rel_l2(s.u, u) < TOL, "step 1"
+    if steps > 1:
+        s = st.run(hb.StepperState(s.t, s.u_device), steps - 1)
+        assert st._graph is not None
+        t, u = ost.run(t, u, steps - 1)
+        assert abs(s.t - t) < 1e-15
+        assert rel_l2(s.u, u) < TOL, f"step {steps}"
+    return st
+
+
+def test_c2_full_scale_parity(monkeypatch):
+    st = _run_config(bench.CONFIGS["C2"], 128, 2, monkeypatch)
+    # the bench's path: shared layout, tensor-product leaves, fused stage terms, root batch
+    assert st.ops.layout == "shared" and st.ops.leaf_solve == "tensor"
+    assert st.ops.fuses_stage_history and st._root_batch()
+
+
+def test_c3_recipe_parity(monkeypatch):
+    _run_config(bench.CONFIGS["C3"], 64, 3, monkeypatch)
+
+
+@pytest.mark.parametrize("panel_levels", [False, True])
+def test_c4_recipe_parity(monkeypatch, panel_levels):
+    if panel_levels:   # every wide level as a per-level k_panel launch (as C4's >256 MB levels)
+        monkeypatch.setenv("HPSB_PN_MEGA_MB", "0.01")
+    st = _run_config(bench.CONFIGS["C4"], 64, 2, monkeypatch)
+    assert st.ops.layout == "per_node"
+
+
+def test_c5_recipe_parity(monkeypatch):
+    cfg = bench.CONFIGS["C5"]
+    assert cfg["k"] == 64
+    _run_config(cfg, 16, 2, monkeypatch, check_stages=True)

@@ -1,21 +1,53 @@
 """Host-side stepping logic that needs no GPU."""
+import sys
+
+import pytest
 import torch
 
-from paper_2306_02526_b200.timestep import TimeStepper
+from paper_2306_02526_b200 import declare_nonlinear, gradient_use, is_pure
+from paper_2306_02526_b200.timestep import _is_fresh
 
 
-def test_gradient_use_probe():
-    """The stepper skips the device gradient only for a g that reads neither
-    component; reads through arithmetic or through comparisons are detected."""
-    gen = torch.Generator().manual_seed(0)
-    U, ux, uy = (torch.randn((1, 64), generator=gen, dtype=torch.float64) for _ in range(3))
+def test_gradient_use_defaults_to_both():
+    """The reference always evaluates the gradient (timestep.py:192-196): an
+    undeclared g gets both components, whatever it reads (no probing)."""
+    for g in (lambda t, u, gx, gy: u - u ** 3,
+              lambda t, u, gx, gy: torch.where(u > 5, gx, 0 * u),
+              lambda t, u, gx, gy: gx if t > 1 else u):
+        assert gradient_use(g) == (True, True)
+
+
+def test_gradient_use_declaration():
+    g = declare_nonlinear(lambda t, u, gx, gy: -u * gx, ux=True, uy=False)
+    assert gradient_use(g) == (True, False) and not is_pure(g)
+    h = declare_nonlinear(lambda t, u, gx, gy: u - u ** 3, ux=False, uy=False, pure=True)
+    assert gradient_use(h) == (False, False) and is_pure(h)
+    assert not is_pure(lambda t, u, gx, gy: u)
+    with pytest.raises(TypeError):
+        declare_nonlinear(len)          # builtins take no attributes
+
+
+def _refs_after_call(fn, *a):
+    r = fn(*a)
+    refs = sys.getrefcount(r) - 1           # as _call_g counts them
+    return r, refs
+
+
+def test_fresh_result_detection():
+    """Only g's own fresh result may serve as stage-history storage; a g that
+    returns its input, a gradient buffer, a persistent out= buffer or a view
+    must be copied (history aliasing)."""
+    U = torch.randn(1, 64, dtype=torch.float64)
+    ux = torch.randn(1, 64, dtype=torch.float64)
+    keep = torch.empty(1, 64, dtype=torch.float64)
     cases = {
-        "allen_cahn": (lambda t, u, gx, gy: u - u ** 3, (False, False)),
-        "burgers": (lambda t, u, gx, gy: -u * gx, (True, False)),
-        "switch_y": (lambda t, u, gx, gy: torch.where(gy > 0, u, -u), (False, True)),
-        "both": (lambda t, u, gx, gy: gx * gx + gy * gy, (True, True)),
+        "fresh": (lambda t, u, gx, gy: u - u ** 3, True),
+        "returns_u": (lambda t, u, gx, gy: u, False),
+        "returns_ux": (lambda t, u, gx, gy: gx, False),
+        "out_buffer": (lambda t, u, gx, gy: torch.mul(u, u, out=keep), False),
+        "view": (lambda t, u, gx, gy: (u * 2).view(1, 64), False),
+        "cast": (lambda t, u, gx, gy: (u * 2).float(), True),
     }
     for name, (g, want) in cases.items():
-        r = g(0.0, U, ux, uy)
-        TimeStepper._probe_grad_use(g, 0.0, U, ux, uy, r)
-        assert g._hb_grad_use == want, name
+        r, refs = _refs_after_call(g, 0.0, U, ux, ux)
+        assert _is_fresh(r, refs) == want, name
