@@ -119,6 +119,19 @@ size_t hps_ops_device_bytes(const hps_ops* ops);
  * solver.py:221-228 with the Kronecker-sum factorisation of A_ii. */
 int hps_ops_set_leaf_fd(hps_ops* ops, const double* host, int count);
 
+/* merge(T_alpha, T_beta, node) (solver.py:67-81) on the device for one node:
+ * Tc = [T_alpha; T_beta], two nbc x nbc row-major DtN maps (a smaller child's
+ * map zero-padded), i1a/i3a/i2b/i3b the node's child-local index maps (device
+ * int arrays).  Forms X33 = T_a33 - T_b33, inverts it by pivoted Gauss-Jordan
+ * under the reference's singularity rule (linalg.py:17,36-42: min pivot <=
+ * 1e-13 max pivot -> HPS_ERR_SINGULAR naming "merge node <node_index>"), and
+ * writes Xinv (n3 x n3), S = X33^-1 [-T_a31 | T_b32] (n3 x n12), Tstack
+ * (n12 x n3) and T = blkdiag(T_a11, T_b22) + Tstack S (n12 x n12), all
+ * row-major device arrays.  Synchronises the stream (the pivot check). */
+int hps_merge_node(int nbc, const double* Tc, int n1a, int n2b, int n3, const int* i1a, const int* i3a,
+                   const int* i2b, const int* i3b, long long node_index, double* Xinv, double* S,
+                   double* Tstack, double* T, void* stream);
+
 /* Copy one operator block to host memory (test hooks leaf_operators /
  * merge_operators, solver.py:339-348).  which: leaf 0=Ainv (ni x ni),
  * 1=S (ni x nb), 2=T (nb x nb, keep_dtn only); merge 0=Xinv (n3 x n3),

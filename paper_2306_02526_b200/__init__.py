@@ -9,11 +9,13 @@ path: tree numbering, coefficients / discretization, the HPS operator set
 from .chebyshev import ChebGrid1D, cheb_nodes, diff_matrix
 from .errors import (ConfigError, DivergenceError, HpstepError, InvalidStepError,
                      SingularMatrixError, UnknownTableauError, UnsupportedConfigurationError)
-from .operators import EllipticDiscretization, LeafStencil, OperatorCoefficients, shift_reaction
-from .solver import HpsOperatorSet, build
+from .operators import (EllipticDiscretization, LeafStencil, OperatorCoefficients, leaf_matrix,
+                        shift_reaction)
+from .solver import HpsOperatorSet, build, build_leaf, merge
 from .tableaux import ButcherPair, available_tableaux, load_tableau
 from .timestep import (ParabolicProblem, SeparableField, StepperState, TimeStepper,
-                       declare_nonlinear, evaluate_nonlinear, gradient_use, is_pure)
+                       declare_nonlinear, evaluate_nonlinear, gradient_use, is_pure,
+                       scalar_stability_function)
 from .tree import DomainTree, TreeNode, build_tree
 from .stability import StepMapSpectrum, analyze, assemble_step_map
 from .sharding import ShardedTimeStepper
@@ -24,7 +26,8 @@ __all__ = [
     "ChebGrid1D", "cheb_nodes", "diff_matrix", "ConfigError", "DivergenceError", "HpstepError",
     "InvalidStepError", "SingularMatrixError", "UnknownTableauError",
     "UnsupportedConfigurationError", "EllipticDiscretization", "LeafStencil",
-    "OperatorCoefficients", "shift_reaction", "HpsOperatorSet", "build", "DomainTree",
+    "OperatorCoefficients", "leaf_matrix", "shift_reaction", "HpsOperatorSet", "build",
+    "build_leaf", "merge", "scalar_stability_function", "DomainTree",
     "TreeNode", "build_tree", "ButcherPair", "available_tableaux", "load_tableau",
     "ParabolicProblem", "SeparableField", "StepperState", "TimeStepper", "evaluate_nonlinear",
     "declare_nonlinear", "gradient_use", "is_pure",

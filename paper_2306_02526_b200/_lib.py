@@ -81,6 +81,7 @@ SIGNATURES = {
     "hps_ops_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BuildDesc), ctypes.c_void_p,
                                      ctypes.POINTER(ctypes.c_void_p)]),
     "hps_ops_destroy": (None, [ctypes.c_void_p]),
+    "hps_merge_node": (_i, [_i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp]),
     "hps_ops_device_bytes": (ctypes.c_size_t, [ctypes.c_void_p]),
     "hps_ops_get_leaf": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_double_p]),
     "hps_ops_get_merge": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,

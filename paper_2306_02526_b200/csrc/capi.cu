@@ -130,6 +130,46 @@ using namespace hpsb;
 extern "C" {
 
 int hps_version(void) { return 1; }
+
+int hps_merge_node(int nbc, const double* Tc, int n1a, int n2b, int n3, const int* i1a, const int* i3a,
+                   const int* i2b, const int* i3b, long long node_index, double* Xinv, double* S,
+                   double* Tstack, double* T, void* stream) {
+  if (nbc <= 0 || n3 <= 0 || n1a < 0 || n2b < 0 || !Tc || !i3a || !i3b || !Xinv || !S || !Tstack || !T) {
+    set_error("hps_merge_node: bad arguments");
+    return HPS_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n12 = n1a + n2b;
+  double *X33 = nullptr, *R = nullptr, *stats = nullptr;
+  auto done = [&](int rc) {
+    cudaFree(X33); cudaFree(R); cudaFree(stats);
+    return rc;
+  };
+  if (cudaMalloc(&X33, (size_t)n3 * n3 * 8) != cudaSuccess || cudaMalloc(&R, (size_t)n3 * n12 * 8 + 8) != cudaSuccess ||
+      cudaMalloc(&stats, 16) != cudaSuccess) {
+    set_error("hps_merge_node: out of device memory");
+    return done(HPS_ERR_CUDA);
+  }
+  // X33, [-T_a31 | T_b32], Tstack and the block diagonal of T (build.cu k_merge_gather, one node)
+  if (int rc = merge_gather(1, n3, n1a, n2b, nbc, Tc, (long long)nbc * nbc, i1a, i3a, i2b, i3b, X33, R, Tstack,
+                            n3, T, st))
+    return done(rc);
+  if (int rc = gj_invert(n3, 1, X33, Xinv, n3, (long long)n3 * n3, stats, st)) return done(rc);
+  std::vector<double> hs;
+  const int bad = check_pivots(stats, 1, n3, hs, st);
+  if (bad == -2) { set_error("cuda error during merge"); return done(HPS_ERR_CUDA); }
+  if (bad >= 0) return done(singular(n3, hs[0], hs[1], "merge", node_index));
+  GemmArgs a{};  // S = Xinv [-T_a31 | T_b32]
+  a.M = n3; a.N = n12; a.K = n3; a.alpha = 1.0; a.beta = 0.0;
+  a.A = Xinv; a.lda = n3; a.B = R; a.ldb = n12; a.C = S; a.ldc = n12; a.batch = 1;
+  if (int rc = gemm(a, st)) return done(rc);
+  GemmArgs t{};  // T = blkdiag + Tstack S
+  t.M = n12; t.N = n12; t.K = n3; t.alpha = 1.0; t.beta = 1.0;
+  t.A = Tstack; t.lda = n3; t.B = S; t.ldb = n12; t.D = T; t.ldd = n12; t.C = T; t.ldc = n12; t.batch = 1;
+  if (int rc = gemm(t, st)) return done(rc);
+  if (cudaStreamSynchronize(st) != cudaSuccess) { set_error("cuda error during merge"); return done(HPS_ERR_CUDA); }
+  return done(0);
+}
 long long hps_launch_count(void) { return g_launches.load(); }
 const char* hps_last_error(void) { return g_err; }
 long long hps_last_error_node(void) { return g_err_node; }

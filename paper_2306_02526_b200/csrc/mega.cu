@@ -12,9 +12,12 @@
 // the down pass).  A task waits only for what it reads -- the up pass for the
 // two children of each of its nodes, the down pass for the parents and for its
 // own nodes' up results -- through per-node completion counters (one count per
-// finished row block).  CTAs take tasks round-robin in increasing order; every
-// task depends only on lower-numbered ones and all CTAs are resident (the grid
-// is sized by occupancy), so the lowest unfinished task can always run.
+// finished row block).  CTAs take tasks in increasing order from a ticket
+// counter and every task depends only on lower-numbered ones, so the lowest
+// unfinished task is always held by a running CTA and can run, whichever of
+// the CTAs are resident (another stream's kernel may hold SMs).  The one
+// exception is opt-in (HPSB_MEGA_DEDICATED=1, an exclusive GPU): the root
+// pair's head tasks bound to the last CTAs of the grid.
 //
 // Within a task the CTA is 8 column groups x 32 threads; a thread owns two
 // adjacent rows of the block and walks its group's columns of the split
@@ -62,7 +65,7 @@ struct MSeg {
   int Rc, Rp, Ru;              // pn: rows per node of the waited-on segments (targets vary per node)
   double* part; unsigned* sem; // split partials [S][NG*NB][R], semaphores [NG*RB]
   // root pair: the root's down product S u_bnd needs only the Dirichlet data,
-  // so its tasks run at the head of the list, concurrently with the up sweep;
+  // so its tasks run at the head of the list;
   // the root's up tasks (w3 = X33^-1 r3) and down tasks share one semaphore per
   // row block and the last arriver writes u3 = S u_bnd + w3 = sum of both
   // partial sets (down splits first, then up splits)
@@ -75,10 +78,10 @@ struct MSeg {
 
 struct MProg {
   int nseg, ntasks;
-  int head, ratio;              // the first `head` tasks (the root's down product, no inputs) are
-                                // interleaved with the others in ticket order: one head task after
-                                // every `ratio` others until the head is exhausted (see task_of)
-  unsigned* ticket;             // next ticket (reset at exit)
+  int head, dedicated;          // opt-in (mega_dedicated): the first `head` tasks (the root's down
+                                // product) run on the last `dedicated` CTAs; every other task is
+                                // taken by ticket.  Default 0 / 0: every task by ticket
+  unsigned* ticket;             // next task after the head (reset at exit)
   unsigned long long* trace;    // debug (HPSB_MEGA_TRACE): per task start / inputs ready / staged /
                                 // streamed / emitted / end, ns (MTS stamps)
   unsigned* reset; int nreset;  // counters to zero at exit (incl. the exit counter at the end)
@@ -123,19 +126,6 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-// Ticket -> task.  Every CTA takes tickets in increasing order, so a task
-// must depend only on tasks with lower tickets: then the lowest unfinished
-// ticket is always held by a running CTA whose inputs are complete, and the
-// launch makes progress whatever subset of its CTAs is resident (a kernel on
-// another stream may hold SMs).  The head tasks depend on nothing; the host
-// picks `ratio` so that every head ticket precedes the first task that reads
-// the head's results.
-__device__ __forceinline__ int task_of(int x, int head, int ratio) {
-  const int per = ratio + 1;
-  if (x >= per * head) return x;
-  return x % per == ratio ? x / per : head + x - x / per;
-}
-
 // PN: per-node operators -- a task's 64 rows tile the level's row space
 // (node * R + r) and may span up to MNB nodes; NG = 1
 template <bool PN>
@@ -146,13 +136,21 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
   __shared__ unsigned s_last;
   const int tid = threadIdx.x, grp = tid >> 5, q = tid & 31;
   pdl_wait();
+  const int G = gridDim.x, KR = p.dedicated;
+  const bool ded = KR > 0 && (int)blockIdx.x >= G - KR;
+  // the dedicated CTAs first take the head tasks round-robin, then every CTA
+  // takes the remaining tasks in list order from a ticket counter (each task
+  // depends only on lower-numbered ones, all taken by resident CTAs)
   __shared__ int s_ticket;
+  int t = ded ? (int)blockIdx.x - (G - KR) : p.ntasks;
   for (;;) {
-    __syncthreads();
-    if (tid == 0) s_ticket = (int)atomicAdd(p.ticket, 1u);
-    __syncthreads();
-    if (s_ticket >= p.ntasks) break;
-    const int t = task_of(s_ticket, p.head, p.ratio);
+    if (!(ded && t < p.head)) {
+      __syncthreads();
+      if (tid == 0) s_ticket = p.head + (int)atomicAdd(p.ticket, 1u);
+      __syncthreads();
+      t = s_ticket;
+      if (t >= p.ntasks) break;
+    }
     int si = 0;
     while (t >= p.s[si].task0 + p.s[si].ntasks) ++si;
     const MSeg& g = p.s[si];
@@ -358,6 +356,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     __syncthreads();  // xs / red / sidx are reused by the next task
     if (p.trace && tid == 0) p.trace[MTS * t + 5] = gtime();
+    if (ded && t < p.head) t += KR;
   }
   // the last CTA out resets the counters for the next solve
   __syncthreads();
@@ -497,6 +496,19 @@ static bool pair_enabled() {
   static const bool on = [] {
     const char* e = getenv("HPSB_NO_ROOT_PAIR");
     return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// The root pair's head tasks on dedicated CTAs stream the root's down product
+// beside the up sweep (12 us per plain C2 solve faster), but a level-1 down
+// task then spins on work bound to specific CTAs, which needs every CTA of the
+// grid resident at once: only on an exclusive GPU, by opt-in.  By default the
+// head tasks are simply the first tickets (deadlock-free on a shared GPU).
+static bool mega_dedicated() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_MEGA_DEDICATED");
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -692,15 +704,10 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     max_ctas = std::max(1, per_sm) * sms;
   }
   int grid = std::min(max_ctas, p.ntasks);
-  if (pair) {  // about a quarter of the tickets stream the root's down product while the up sweep climbs
+  if (pair && mega_dedicated()) {  // a quarter of the CTAs stream the root's down product while the up sweep climbs
     grid = max_ctas;
     p.head = p.s[iroot_dn].ntasks;
-    // the first task reading the head's results: level 1's down segment (or the
-    // end of the list); every head ticket must precede it
-    int first_dep = p.ntasks;
-    for (int i = 0; i < p.nseg; ++i)
-      if (!p.s[i].up && p.s[i].wpar == p.s[iroot_dn].done && i != iroot_dn) first_dep = std::min(first_dep, p.s[i].task0);
-    p.ratio = std::min(3, (first_dep - p.head) / std::max(1, p.head));
+    p.dedicated = std::max(1, grid / 4);
   }
   const char* tr = getenv("HPSB_MEGA_TRACE");  // debug: per-task timeline appended to this file
   unsigned long long* dtrace = nullptr;

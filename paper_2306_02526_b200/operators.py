@@ -164,10 +164,20 @@ class EllipticDiscretization:
         return self._samples
 
     def leaf_interior_rows(self, leaf_id):
-        """Host copy of the collocated interior rows (ni x m); diagnostics only."""
+        """Host copy of the collocated interior rows (ni x m); diagnostics only.
+        Constant coefficients: one cached copy serves every leaf (reference
+        operators.py:238-262)."""
         st = self.stencil
         s = self.coefficient_samples()
-        v = s[0 if s.shape[0] == 1 else leaf_id][:, :st.ni]
+        if s.shape[0] == 1:
+            rows = self._device.get("rows0")
+            if rows is None:
+                rows = self._device["rows0"] = self._interior_rows(s[0][:, :st.ni])
+            return rows
+        return self._interior_rows(s[leaf_id][:, :st.ni])
+
+    def _interior_rows(self, v):
+        st = self.stencil
         ii = slice(0, st.ni)
         rows = -v[0][:, None] * st.D2x[ii]
         rows = rows - v[1][:, None] * st.D2y[ii]
@@ -196,6 +206,17 @@ class EllipticDiscretization:
     def flux_jump(self, u):
         from .timestep import device_discretization
         return device_discretization(self).flux_jump(u)
+
+
+def leaf_matrix(disc, leaf_id):
+    """The leaf's full local collocation system (m x m, reference
+    operators.py:265-274): the interior rows of ``A``, then identity rows for
+    the edge points (Dirichlet data)."""
+    st = disc.stencil
+    A = np.zeros((st.m, st.m))
+    A[:st.ni] = disc.leaf_interior_rows(leaf_id)
+    A[st.ni:, st.ni:] = np.eye(st.nb)
+    return A
 
 
 def shift_reaction(coeffs, sigma, dt_gamma):

@@ -51,7 +51,7 @@ def _workspace_key(k):
         return (k, tok)
     if torch.cuda.is_current_stream_capturing():
         return (k, ("graph", None))
-    return (k, current_stream_handle())
+    return (k, torch.cuda.current_stream().cuda_stream)
 
 
 class DevicePlan:
@@ -165,6 +165,44 @@ class LeafOperators:
 class MergeOperators:
     def __init__(self, S, X33_factor, Tstack, T=None):
         self.S, self.X33_factor, self.Tstack, self.T = S, X33_factor, Tstack, T
+
+
+def build_leaf(disc, leaf_id, sigma=0.0, dt_gamma=1.0):
+    """One leaf's operators S = -A_ii^-1 A_ib, T = D_bi S + D_bb (reference
+    solver.py:53-64), from a device build of the operator set (the leaf build
+    is batched over every leaf); SingularMatrixError names "leaf node {i}"."""
+    ops = build(disc.tree, disc.coeffs, sigma=sigma, dt_gamma=dt_gamma, disc=disc, keep_dtn=True)
+    return ops.leaf_operators(leaf_id)
+
+
+def merge(T_alpha, T_beta, node):
+    """Merge two children's DtN maps across their interface (reference
+    solver.py:67-81) on the device (``hps_merge_node``): the same X33 / S /
+    Tstack / T and the same singularity rule, raising SingularMatrixError
+    naming "merge node {node.index}"."""
+    lib = _lib.load()
+    dev = cuda_device()
+    Ta = np.asarray(T_alpha, dtype=float)
+    Tb = np.asarray(T_beta, dtype=float)
+    nbc = max(Ta.shape[0], Tb.shape[0])
+    Tc = np.zeros((2, nbc, nbc))
+    Tc[0, :Ta.shape[0], :Ta.shape[1]] = Ta
+    Tc[1, :Tb.shape[0], :Tb.shape[1]] = Tb
+    maps = [torch.as_tensor(np.ascontiguousarray(getattr(node, k), dtype=np.int32), device=dev)
+            for k in ("i1a", "i3a", "i2b", "i3b")]
+    n1a, n3, n2b = maps[0].numel(), maps[1].numel(), maps[2].numel()
+    n12 = n1a + n2b
+    dTc = torch.as_tensor(Tc, device=dev)
+    Xinv = torch.empty((n3, n3), dtype=torch.float64, device=dev)
+    S = torch.empty((n3, n12), dtype=torch.float64, device=dev)
+    Tst = torch.empty((n12, n3), dtype=torch.float64, device=dev)
+    T = torch.empty((n12, n12), dtype=torch.float64, device=dev)
+    rc = lib.hps_merge_node(nbc, dTc.data_ptr(), n1a, n2b, n3, *[m.data_ptr() for m in maps],
+                            int(node.index), Xinv.data_ptr(), S.data_ptr(), Tst.data_ptr(), T.data_ptr(),
+                            current_stream_handle())
+    _lib.check(rc, "hps_merge_node")
+    return MergeOperators(S=S.cpu().numpy(), X33_factor=_InverseFactor(Xinv.cpu().numpy()),
+                          Tstack=Tst.cpu().numpy(), T=T.cpu().numpy())
 
 
 class HpsOperatorSet:

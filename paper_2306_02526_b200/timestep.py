@@ -316,6 +316,12 @@ def combine_rows(coefs, vecs, out):
     return out
 
 
+def scalar_stability_function(pair, z):
+    """Amplification factor of the implicit half on u' = lambda u (reference
+    timestep.py:331-333)."""
+    return pair.stability_function(z)
+
+
 def evaluate_nonlinear(disc, problem, t, u):
     """Pointwise g with leaf-local spectral derivatives (timestep.py:64-78)."""
     as_numpy = not torch.is_tensor(u)

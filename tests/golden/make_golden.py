@@ -190,6 +190,40 @@ def ensemble_case():
     save("step_ensemble", modes=coef, u3=s.u, dt=1e-3)
 
 
+def ark5_case():
+    """ARK5(4)8L[2]SA (reference tableaux.py:157-221): its coefficient arrays;
+    the C1 heat recipe at 4x4 p=10 (stages of step 1, u after 1 and 5 steps)
+    and the Allen-Cahn recipe at 4x4 p=10 (u after 3 steps)."""
+    from hpstep.tableaux import load_tableau
+    tab = load_tableau("ARK5")
+    tree = build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    prob = ParabolicProblem(coeffs=OperatorCoefficients(c11=1.0, c22=1.0, dim=2), q=q,
+                            f=uex, u0=lambda pts: uex(0.0, pts))
+    st = TimeStepper(tree, prob, "ARK5", dt=2e-3)
+    stages = []
+    orig = st.ops.solve_with_body_load
+
+    def rec(f, g):
+        u = orig(f, g)
+        stages.append(np.array(u))
+        return u
+
+    st.ops.solve_with_body_load = rec
+    s = st.step(st.initial_state())
+    st.ops.solve_with_body_load = orig
+    u1 = s.u.copy()
+    s = st.run(s, 4)
+    coef = sine_modes(0)
+    ac = ParabolicProblem(coeffs=OperatorCoefficients(c11=0.01, c22=0.01, dim=2),
+                          g=lambda t, u, ux, uy: u - u ** 3,
+                          u0=lambda pts: sine_field(coef, pts), time_independent_bc=True)
+    sa = TimeStepper(tree, ac, "ARK5", dt=1e-2)
+    a3 = sa.run(sa.initial_state(), 3)
+    save("step_ark5", A=tab.A, Ahat=tab.Ahat, b=tab.b, c=tab.c, b_emb=tab.b_emb, gamma=tab.gamma,
+         stages=np.array(stages)[:, 0], u1=u1, u5=s.u, dt=2e-3, ac_modes=coef, ac_u3=a3.u, ac_dt=1e-2)
+
+
 def be_case():
     tree = build_tree(UNIT, 4, 4, 10)
     phi, uex, q = heat_manufactured()
@@ -278,6 +312,7 @@ def main():
     burgers_var_case()
     ensemble_case()
     be_case()
+    ark5_case()
     stability_case()
     evals_case()
     slope_cases()

@@ -289,3 +289,52 @@ def test_step_host_overlapped_copies_match_step():
     st.sync_host()
     for o in outs:
         assert np.array_equal(o.numpy(), ref)
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_ark5_matches_reference(golden, graph, monkeypatch):
+    """ARK5(4)8L[2]SA (reference tableaux.py:157-221): 7 implicit stages per
+    step, stage right-hand sides of up to 15 terms (past the fused
+    stage-terms kernel's 12: the combination fallback), the root Dirichlet
+    product of 8 boundary-data rows per step; per stage and per step."""
+    hb = _hb()
+    z = golden("step_ark5")
+    if not graph:
+        monkeypatch.setenv("HPSB_NO_GRAPH", "1")
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**lap_fields()),
+                               q=hb.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t)),
+                               f=hb.SeparableField.product(phi, np.cos), u0=lambda pts: uex(0.0, pts))
+    st = hb.TimeStepper(tree, prob, "ARK5", dt=float(z["dt"]))
+    assert st.pair.s == 8
+    s = st.step(st.initial_state())
+    assert rel_l2(s.u, z["u1"]) < TOL
+    s = st.run(s, 4)
+    assert rel_l2(s.u, z["u5"]) < TOL
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=0.01, c22=0.01),
+                               g=lambda t, u, ux, uy: u - u ** 3,
+                               u0=lambda pts: sine_field(z["ac_modes"], pts), time_independent_bc=True)
+    st = hb.TimeStepper(tree, prob, "ARK5", dt=float(z["ac_dt"]))
+    s = st.run(st.initial_state(), 3)
+    assert rel_l2(s.u, z["ac_u3"]) < TOL
+
+
+def test_ark5_stages_match_reference(golden, monkeypatch):
+    hb = _hb()
+    z = golden("step_ark5")
+    monkeypatch.setenv("HPSB_NO_GRAPH", "1")
+    from tests.test_gpu_scale import _record_stages
+    tree = hb.build_tree(UNIT, 4, 4, 10)
+    phi, uex, q = heat_manufactured()
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(**lap_fields()), q=q, f=uex,
+                               u0=lambda pts: uex(0.0, pts))
+    st = hb.TimeStepper(tree, prob, "ARK5", dt=float(z["dt"]))
+    stages = []
+    restore = _record_stages(st, stages)
+    s = st.step(st.initial_state())
+    restore()
+    assert len(stages) == 7
+    for i, (a, b) in enumerate(zip(stages, z["stages"])):
+        assert rel_l2(a[0], b) < TOL, f"stage {i + 1}"
+    assert rel_l2(s.u, z["u1"]) < TOL

@@ -132,3 +132,41 @@ def test_oracle_leaf_evaluations_match_reference(golden):
     ux, uy = disc.gradient(z["u"])
     assert rel_l2(ux, z["ux"]) < 1e-13 and rel_l2(uy, z["uy"]) < 1e-13
     assert rel_l2(disc.flux_jump(z["u"]), z["jump"]) < 1e-13
+
+
+def _golden_tableau(z):
+    return dict(A=z["A"], Ahat=z["Ahat"], b=z["b"], bhat=z["b"], c=z["c"], gamma=float(z["gamma"]),
+                s=int(z["b"].size))
+
+
+def test_ark5_tableau_matches_reference(golden):
+    """The drop-in's ARK5(4)8L[2]SA arrays are bitwise the reference's
+    (tableaux.py:157-221); alias and registry as the reference."""
+    from paper_2306_02526_b200.tableaux import available_tableaux, load_tableau
+    z = golden("step_ark5")
+    p = load_tableau("ARK5")
+    assert p.name == "ARK5(4)8L[2]SA" and p.s == 8 and p.order == 5 and p.embedded_order == 4
+    for key in ("A", "Ahat", "b", "c", "b_emb"):
+        assert np.array_equal(getattr(p, key), z[key]), key
+    assert np.array_equal(p.bhat, z["b"]) and p.gamma == float(z["gamma"])
+    assert "ARK5(4)8L[2]SA" in available_tableaux()
+
+
+def test_oracle_ark5_stepping_matches_reference(golden):
+    """The oracle's stage stepper with the 8-stage pair (every stage has more
+    than the 6-stage pair's terms) against the reference run."""
+    z = golden("step_ark5")
+    tab = _golden_tableau(z)
+    phi, uex, q = heat_manufactured()
+    tree = O.OTree(UNIT, 4, 4, 10)
+    st = O.OStepper(tree, O.OCoeffs(c11=1.0, c22=1.0), tab, float(z["dt"]), q=q, f=uex, record=True)
+    t, u = st.run(0.0, uex(0.0, tree.points), 1)
+    for i, (a, b) in enumerate(zip(st.stages, z["stages"])):
+        assert rel_l2(a[0], b) < 1e-13, f"stage {i + 1}"
+    assert rel_l2(u, z["u1"]) < 1e-13
+    t, u = st.run(t, u, 4)
+    assert rel_l2(u, z["u5"]) < 1e-13
+    ac = O.OStepper(tree, O.OCoeffs(c11=0.01, c22=0.01), tab, float(z["ac_dt"]),
+                    g=lambda t, u, ux, uy: u - u ** 3)
+    _, a3 = ac.run(0.0, sine_field(z["ac_modes"], tree.points), 3)
+    assert rel_l2(a3, z["ac_u3"]) < 1e-13
