@@ -7,22 +7,34 @@ through the drop-in ``TimeStepper`` -- 5 implicit HPS stage solves plus the
 device stage right-hand-side assembly -- with the state resident in HBM.
 ``value`` = DOF*stages/s = N_dof * 5 * K / (device time of K steps, max over
 ranks).  With N > 1 GPUs (torchrun) one problem is subtree-sharded over the
-ranks (level-log2(N) subtrees per GPU, an NCCL all-gather of
-the subtree-root fluxes per stage solve, ``scaling`` "strong"); the ensemble
-config shards members; ``--shard replicas`` runs one replica per GPU instead.
-``e2e`` is the same metric through the public API with host-resident
-states: every step copies its input state in from pinned host memory and its
-result back out (``TimeStepper.step_host``; the steps are independent requests
-on the same input, so one step's copies overlap its neighbours' compute on
-separate copy streams).
-``roofline`` is for the stage solve (the ~2*depth+5 level-batched kernels of
-``hps_solve``): algorithmic bytes per solve over
-the CUDA-event duration of the solves inside the timed region.
+ranks; the ensemble config shards members; ``--shard
+replicas`` runs one replica per GPU instead.
+
+``e2e`` is the same metric through the public API with host-resident states:
+every step copies its input state in from pinned host memory and its result
+back out (``TimeStepper.step_host``; independent requests on the same input,
+so one step's copies overlap its neighbours' compute).  ``e2e_dependent``:
+a trajectory whose every step starts from the previous step's host result
+(copies serialised with the compute).
+
+``kernels``: per-kernel CUDA-event durations of the step's kernels (a
+separate pass of eager steps with every launch bracketed by events,
+``hps_ktimer_*``), each with its share of the step and its algorithmic HBM
+bytes per launch.  ``roofline`` is
+the dominant kernel's entry; ``traffic`` is its ncu dram bytes per launch from
+the committed capture (profiles/traffic_kernels.json).  ``solve`` keeps the
+whole-solve figures (plain solve, CUDA graph).
+
+``parity``: the bench checks its own output -- C2's final state against the
+manufactured solution, and one GPU step of the 64x64-leaf sample against the
+CPU oracle's step from the same initial state (north-star bar 1e-10).
+
 ``cpu_baseline`` times the CPU oracle port (numpy/scipy, all host cores) on a
-bounded sample: the 64x64-leaf subtree of the same problem (same p, dt), one
-step, build excluded.
-``--impl reference`` times that CPU path alone (the reference is pure Python
-and cannot be installed on the GPU box).
+bounded sample: the 64x64-leaf version of the problem (same p, dt), one step,
+build excluded.  ``--impl reference`` times the oracle port on the full
+configuration (C2: 128x128 leaves, p=16), build outside the timed region, on
+all host cores (the reference is pure Python and does not travel to the GPU
+box).
 """
 
 import argparse
@@ -45,11 +57,11 @@ TWO_PI = 2 * np.pi
 
 # BASELINE.json configs (single-GPU workloads); C2 is the metric's config
 CONFIGS = {
-    "C1": dict(n=8, p=12, dt=1e-3, kind="heat", k=1),
-    "C2": dict(n=128, p=16, dt=1e-4, kind="heat", k=1),
-    "C3": dict(n=256, p=12, dt=1e-3, kind="allen_cahn", k=1),
-    "C4": dict(n=512, p=10, dt=1e-5, kind="burgers_var", k=1),
-    "C5": dict(n=128, p=16, dt=1e-4, kind="ensemble", k=64),
+    "C1": dict(name="C1", n=8, p=12, dt=1e-3, kind="heat", k=1),
+    "C2": dict(name="C2", n=128, p=16, dt=1e-4, kind="heat", k=1),
+    "C3": dict(name="C3", n=256, p=12, dt=1e-3, kind="allen_cahn", k=1),
+    "C4": dict(name="C4", n=512, p=10, dt=1e-5, kind="burgers_var", k=1),
+    "C5": dict(name="C5", n=128, p=16, dt=1e-4, kind="ensemble", k=64),
 }
 SAMPLE_N = 64      # CPU sample: the 64x64-leaf subtree of the configured problem
 
@@ -152,6 +164,70 @@ def solve_flops(tree, k, tensor_leaf=False):
     for d, lm in enumerate(tree.level_maps):
         e += lm.count * (lm.n3 * lm.n3 + lm.n3 * lm.n12 + (lm.n12 * lm.n3 if d > 0 else 0))
     return 2 * k * e
+
+
+def level_shapes(n, p):
+    """(count, n3, n12) of every parent level, root first, of an n x n-leaf
+    tree with p nodes per leaf side (SURVEY.md 8(a) closed form: x-splits of
+    m x m boxes have n3 = m q, n12 = 4 m q; y-splits of (m/2) x m boxes
+    n3 = m q / 2, n12 = 3 m q)."""
+    q = p - 2
+    out, m, c = [], n, 1
+    while m > 1:
+        out.append((c, m * q, 4 * m * q))               # x-split of an m x m box
+        out.append((2 * c, m * q // 2, 3 * m * q))      # y-split of an (m/2) x m box
+        m //= 2
+        c *= 4
+    return out
+
+
+def config_block(cfg):
+    """The config dict both arms print (same workload)."""
+    n, p = cfg["n"], cfg["p"]
+    q = p - 2
+    L, ni = n * n, q * q
+    N = q * (p * L + 2 * n)
+    ops = sum(n3 * n3 + 2 * n3 * n12 for _, n3, n12 in level_shapes(n, p)) * 8
+    return {"workload": f"{cfg['name']}: {n}x{n} leaves, p={p}, {cfg['kind']}, ARK4 dt={cfg['dt']}, "
+                        f"k={cfg['k']}, one ARK4 step per bench step (5 stage solves)",
+            "N_dof": N,
+            "l2": ("inputs larger than L2, no flush (level operators streamed per stage solve %.2f GB "
+                   "> 126 MB L2; state %.1f MB)" % (ops / 1e9, 8e-6 * N * cfg["k"])) if ops > 126e6 else
+                  "working set fits the 126 MB L2 (a latency-bound configuration; no flush)"}
+
+
+def kernel_bytes(shapes, dF, L, ni, nb, nbd, N, k=1):
+    """Algorithmic HBM bytes per launch of the stage-path kernels (shared
+    layout): every vector byte a kernel must read or write once,
+    every operator byte once per launch.  Up-level node: children's flux
+    entries 2 n3 + n12 in, w3 n3 + flux n12 out, operator (n3 + n12) n3 (root
+    n3 n3); down-level node: boundary values n12 + w3 n3 in, u3 n3 out,
+    operator n3 n12 (root: precomputed by k_root_dir in the stage path).
+    Returns {category: bytes or fn(nterms)}."""
+    def up(lv, root):
+        c, n3, n12 = lv
+        return 8 * (k * c * (3 * n3 + 2 * n12 - (n12 if root else 0)) + (n3 + (0 if root else n12)) * n3)
+
+    def dn(lv, root):
+        c, n3, n12 = lv
+        return 8 * (k * c * (n12 + 2 * n3) + (0 if root else n3 * n12))
+
+    wide = range(0, dF)
+    fused = range(dF, len(shapes))
+    c0, n3r, n12r = shapes[0]
+    return {
+        "k_mega": sum(up(shapes[d], d == 0) + dn(shapes[d], d == 0) for d in wide),
+        "k_sub_up": sum(up(shapes[d], False) for d in fused) + 8 * k * L * nb,
+        "k_sub_down": sum(dn(shapes[d], False) for d in fused),
+        # leaf up: the stage terms in, the formed body load and the leaf fluxes out, Dirichlet data
+        "leaf_up_terms": lambda nt: 8 * k * ((nt + 1) * L * ni + L * nb + nbd),
+        # leaf down: body load + boundary values in, u_int and the L u history out
+        "leaf_down": 8 * k * (L * ni + L * nb + 2 * L * ni),
+        "leaf_lu": 8 * k * (L * ni + L * nb + L * ni),
+        # the root's Dirichlet product of ns boundary-data rows: S_root once
+        "root_dir": lambda ns: 8 * (n3r * n12r + ns * (n12r + n3r)),
+        "combine_bnd": lambda nt: 8 * k * (nt + 1) * N,
+    }
 
 
 class ClockSampler:
@@ -314,39 +390,73 @@ def oracle_stepper(cfg, n=None, record=False):
     return tree, st, u
 
 
-def cpu_oracle_sample(cfg, steps, warmup):
-    """Times the oracle port on the SAMPLE_N x SAMPLE_N subtree of the config."""
+def cpu_oracle_sample(cfg, steps, warmup, keep_state=False):
+    """Times the oracle port on the SAMPLE_N x SAMPLE_N-leaf version of the
+    config (build excluded).  keep_state: also return the state after the
+    first step from the initial data (the GPU parity check)."""
     n = min(SAMPLE_N, cfg["n"])
     tree, st, u = oracle_stepper(cfg, n)
     t = 0.0
+    first = None
     for _ in range(warmup):
         t, u = st.run(t, u, 1)
+        first = u if first is None else first
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
         t, u = st.run(t, u, 1)
         times.append(time.perf_counter() - t0)
+        first = u if first is None else first
     k = cfg["k"]
     val = tree.N * k * 5 * len(times) / sum(times)
-    sample = (f"{n}x{n}-leaf subtree, p={cfg['p']}, k={k}, {len(times)} ARK4 step(s) "
+    sample = (f"{n}x{n}-leaf version of the config, p={cfg['p']}, k={k}, {len(times)} ARK4 step(s) "
               f"({5 * len(times)} stage solves + RHS), N={tree.N}, build excluded")
+    if keep_state:
+        return val, sample, times, first
     return val, sample, times
 
 
 def run_reference(args, cfg, rank):
+    """The reference arm: the CPU oracle port (a restatement of the reference
+    hpstep algorithm; the reference itself is pure Python and cannot travel to
+    the GPU box) on the FULL configuration -- C2: 128 x 128 leaves, p = 16,
+    N = 3,673,600 -- with all host cores (numpy/scipy's OpenBLAS threads).
+    The operator build is outside the timed region; W untimed steps, then K
+    timed ARK4 steps from the configuration's initial data."""
     if rank != 0:
         return
-    val, sample, times = cpu_oracle_sample(cfg, max(1, args.steps), max(0, args.warmup))
+    t0 = time.perf_counter()
+    tree, st, u = oracle_stepper(cfg)
+    build_s = time.perf_counter() - t0
+    t = 0.0
+    for _ in range(args.warmup):
+        t, u = st.run(t, u, 1)
+    times = []
+    for _ in range(max(1, args.steps)):
+        t1 = time.perf_counter()
+        t, u = st.run(t, u, 1)
+        times.append(time.perf_counter() - t1)
+    k = cfg["k"]
+    val = tree.N * k * 5 * len(times) / sum(times)
     cores = os.cpu_count()
+    threads = os.environ.get("OPENBLAS_NUM_THREADS") or os.environ.get("OMP_NUM_THREADS") or str(cores)
+    sample = (f"full configuration ({cfg['n']}x{cfg['n']} leaves, p={cfg['p']}, N={tree.N}), "
+              f"{len(times)} timed ARK4 steps after {args.warmup} untimed, build {build_s:.1f} s excluded, "
+              f"BLAS threads {threads}")
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} (CPU sample)", "sample": sample},
+            "config": config_block(cfg),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "build_s": build_s}
+    if cfg["kind"] == "heat":
+        uex = phi(tree.points) * np.cos(t)
+        line["parity"] = {"manufactured_max_rel": float(np.abs(u - uex).max() / np.abs(uex).max()),
+                          "manufactured_t": t}
     print(json.dumps(line), flush=True)
 
 
@@ -446,13 +556,36 @@ def main():
         launches = _kernels_per_step(st, state) * args.steps
     ms = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms)
-    # stage-solve time for the roofline: the same solve (operators, stage body
-    # load, boundary data) timed with CUDA events, 5 per step as in the run
-    solve_ms = _time_solves(st, 5 * args.steps, sharded=subtree)
-    # whole-job throughput: replicas add up; a sharded problem / ensemble counts once
     copies = k_total if ensemble else (k if subtree else k * world)
     units = tree.N * 5 * args.steps * copies
     value = units / (ms * 1e-3)
+    final = state
+
+    # parity of the timed run itself: C2 / C1 have a manufactured solution
+    parity = {}
+    if cfg["kind"] == "heat" and not subtree:
+        uf = final.u_device.reshape(-1)
+        uex = torch.as_tensor(phi(tree.points) * np.cos(final.t), device=uf.device)
+        parity["manufactured_max_rel"] = float((uf - uex).abs().max() / uex.abs().max())
+        parity["manufactured_t"] = final.t
+
+    # whole-solve figures (plain solve replayed as a graph) for reference
+    solve_ms = _time_solves(st, 5 * args.steps, sharded=subtree)
+
+    # per-kernel CUDA-event durations of the step (eager steps, every launch bracketed)
+    kt_steps = 3
+    kernels = None
+    if not subtree:
+        kstate = state
+        kstate, _ = st._advance(kstate)           # warm the eager path
+        torch.cuda.synchronize()
+        _lib.kernel_times()                        # clear
+        lib.hps_ktimer_enable(1)
+        for _ in range(kt_steps):
+            kstate, _ = st._advance(kstate)
+        lib.hps_ktimer_enable(0)
+        kt = _lib.kernel_times()
+        kernels = kernel_table(kt, kt_steps, tree, lib, st, k)
 
     # e2e: public API with host state in / host result out every step
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
@@ -461,15 +594,15 @@ def main():
     out = torch.empty_like(uh).pin_memory()
     t_e2e = state.t
     if subtree:   # the sharded stepper: synchronous public step with host state
-        def e2e_step():
-            s = st.step(hb.StepperState(t_e2e, uh))
-            out.copy_(s.u_device, non_blocking=True)
+        def e2e_step(src=uh, dst=out):
+            s = st.step(hb.StepperState(t_e2e, src))
+            dst.copy_(s.u_device, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
             return ev
     else:         # step_host: every step copies its input in and its result out;
-        def e2e_step():   # the copies of neighbouring (independent) steps overlap
-            return st.step_host(t_e2e, uh, out)
+        def e2e_step(src=uh, dst=out):   # the copies of neighbouring (independent) steps overlap
+            return st.step_host(t_e2e, src, dst)
     e2e_step()              # warm
     if not subtree:
         st.sync_host()
@@ -487,9 +620,21 @@ def main():
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
     e2e_val = tree.N * 5 * e2e_steps * copies / (e2e_ms * 1e-3)
     nbytes = uh.numel() * 8
+    # dependent trajectory: each step starts from the previous step's host result
+    dep = None
+    if not subtree:
+        bufs = [uh, out]
+        barrier()
+        t0w = time.perf_counter()
+        for i in range(e2e_steps):
+            ev = st.step_host(t_e2e, bufs[i & 1], bufs[(i + 1) & 1])
+            ev.synchronize()
+        st.sync_host()
+        dep_s = time.perf_counter() - t0w
+        dep = {"value": tree.N * 5 * e2e_steps * copies / dep_s, "unit": UNIT,
+               "ms_per_step": 1e3 * dep_s / e2e_steps, "clock": "host wall clock (each step waits for its result)"}
 
-    # roofline of the stage solve: HBM bytes actually required by the layout
-    # in use vs FP64 work; the bound is whichever takes longer at its peak
+    # whole-solve roofline (plain solve): HBM bytes the layout requires vs FP64 work
     layout = st.ops.layout
     if layout == "shared":
         b_op, b_vec = solve_bytes_shared(tree, k)
@@ -502,50 +647,68 @@ def main():
     flops = solve_flops(tree, k, tensor_leaf=getattr(st.ops, "leaf_solve", "dense") == "tensor")
     if subtree:
         flops /= world
-    t_hbm = (b_op + b_vec) / (peak * 1e9)
-    t_fp64 = flops / (FP64_TFLOPS * 1e12)
-    traffic = profiled_traffic(f"{args.config}/{layout}")
-    if t_hbm >= t_fp64:
+    solve = {"solve_ms": avg_solve, "solves_timed": len(solve_ms), "layout": layout,
+             "leaf_solve": getattr(st.ops, "leaf_solve", "dense"),
+             "algorithmic_bytes_per_solve": b_op + b_vec, "gflops_per_solve": flops / 1e9,
+             "frac_hbm": (b_op + b_vec) / (avg_solve * 1e-3) / (peak * 1e9),
+             "frac_fp64": flops / (avg_solve * 1e-3) / (FP64_TFLOPS * 1e12),
+             "traffic": profiled_traffic(f"{args.config}/{layout}")}
+
+    # roofline: the dominant kernel of the step (largest share of the step time)
+    if kernels:
+        top = max(kernels, key=lambda r: r["share_of_step"])
+        traffic = profiled_kernel_traffic(args.config, top["kernel"])
+        roof = {"bound": "hbm", "achieved": top["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                "peak_source": src, "frac": top["achieved_gbs"] / peak, "traffic": traffic,
+                "kernel": top["kernel"], "us_per_launch": top["us_per_launch"],
+                "algorithmic_bytes_per_launch": top["bytes_per_launch"],
+                "share_of_step": top["share_of_step"]}
+    else:   # sharded: the whole stage solve
         roof = {"bound": "hbm", "achieved": (b_op + b_vec) / (avg_solve * 1e-3) / 1e9, "peak": peak,
-                "unit": "GB/s", "peak_source": src}
-    else:
-        roof = {"bound": "tensor", "achieved": flops / (avg_solve * 1e-3) / 1e12, "peak": FP64_TFLOPS,
-                "unit": "TFLOP/s", "peak_source": "measured FP64 DMMA (profiles/r01_fp64_peak.txt)"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof.update({"traffic": traffic, "kernel": "hps_solve (one stage solve: leaf GEMMs + level sweeps)",
-                 "layout": layout, "leaf_solve": getattr(st.ops, "leaf_solve", "dense"),
-                 "algorithmic_bytes_per_solve": b_op + b_vec,
-                 "gflops_per_solve": flops / 1e9, "solve_ms": avg_solve, "solves_timed": len(solve_ms),
-                 "frac_hbm": (b_op + b_vec) / (avg_solve * 1e-3) / (peak * 1e9),
-                 "frac_fp64": flops / (avg_solve * 1e-3) / (FP64_TFLOPS * 1e12)})
+                "unit": "GB/s", "peak_source": src, "traffic": None, "kernel": "hps_solve_phase (stage solve)"}
+        roof["frac"] = roof["achieved"] / peak
+
+    # the bench's own 64x64 sample: one GPU step against the CPU oracle's step
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, sample, _, ostate = cpu_oracle_sample(cfg, 1, 0, keep_state=True)
+        cpu = {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": sample}
+        n_s = min(SAMPLE_N, cfg["n"])
+        c_s = dict(cfg, n=n_s)
+        tree_s = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), n_s, n_s, cfg["p"])
+        st_s = hb.TimeStepper(tree_s, hb.ParabolicProblem(**make_problem(hb, c_s)), "ARK4", dt=cfg["dt"],
+                              layout=args.layout)
+        u_s = st_s.step(st_s.initial_state()).u
+        parity["sample"] = f"{n_s}x{n_s} leaves, p={cfg['p']}, one ARK4 step vs the CPU oracle"
+        parity["sample_rel_l2"] = float(np.linalg.norm(u_s - ostate) / np.linalg.norm(ostate))
+    if parity:
+        vals = [v for key, v in parity.items() if key in ("sample_rel_l2",)]
+        parity["tolerance"] = 1e-10
+        parity["ok"] = all(v <= 1e-10 for v in vals) and parity.get("manufactured_max_rel", 0.0) <= 1e-8
 
     if rank != 0:
         if distributed:
             dist.destroy_process_group()
         return
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        val, sample, _ = cpu_oracle_sample(cfg, 1, 0)
-        cpu = {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-               "sample": sample}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (manufactured / seeded analytic fields; no dataset)",
-        "config": {"workload": f"{args.config}: {cfg['n']}x{cfg['n']} leaves, p={cfg['p']}, "
-                               f"{cfg['kind']}, ARK4 dt={cfg['dt']}, k={k}, one ARK4 step per "
-                               f"bench step (5 stage solves)",
-                   "N_dof": tree.N, "layout": layout,
-                   "parallelism": (f"ensemble members sharded over {world} GPU(s)" if ensemble
-                                   else f"subtree-sharded over {world} GPUs (level-{world.bit_length() - 1} "
-                                        f"subtrees, NCCL flux all-gather per stage solve)" if subtree
-                                   else f"replicas x{world}"),
-                   "l2": "inputs larger than L2 (operators %.2f GB)" % (b_op / 1e9)},
+        "config": config_block(cfg),
+        "parallelism": (f"ensemble members sharded over {world} GPU(s)" if ensemble
+                        else f"subtree-sharded over {world} GPUs (level-{world.bit_length() - 1} "
+                             f"subtrees, NCCL flux all-gather per stage solve)" if subtree
+                        else f"replicas x{world}"),
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                 "d2h_bytes_per_step": nbytes},
+        "e2e_dependent": dep,
         "gpu_launches": int(launches),
         "roofline": roof,
+        "kernels": kernels,
+        "solve": solve,
+        "parity": parity or None,
         "clocks": clk.summary(),
         "build_s": build_s,
         "cpu_baseline": cpu,
@@ -553,6 +716,64 @@ def main():
     print(json.dumps(line), flush=True)
     if distributed:
         dist.destroy_process_group()
+
+
+def profiled_kernel_traffic(config, kernel):
+    """ncu dram bytes (read + write) per launch of ``kernel`` from the
+    committed capture summary, if any (profiles/traffic_kernels.json)."""
+    path = os.path.join(ROOT, "profiles", "traffic_kernels.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh).get(config, {})
+    except (OSError, ValueError):
+        return None
+    for name, v in d.items():
+        if name == kernel or kernel.startswith(name):
+            return v
+    return None
+
+
+def kernel_table(kt, nsteps, tree, lib, st, k):
+    """Per-kernel rows {kernel, launches_per_step, us_per_launch,
+    share_of_step, bytes_per_launch, achieved_gbs, frac} from the event
+    timings of ``nsteps`` eager steps (kernel_bytes gives the algorithmic
+    bytes; None for kernels without a byte model)."""
+    peak, _ = peaks()
+    shapes = [(lm.count, lm.n3, lm.n12) for lm in tree.level_maps]
+    dF = lib.hps_plan_fused_level(st.ops.plan.handle)
+    nbd = tree.boundary_ids.size
+    kb = kernel_bytes(shapes, dF, tree.L, tree.ni, tree.nb, nbd, tree.N, k)
+    s = st.pair.s
+    total = sum(v[0] for v in kt.values())
+    # stage terms of the fused leaf-up kernel, stage i (1..s-1): u, L u_0..u_{i-1}, q's spatial parts
+    nq = len(st._Q.sep) if st._Q.sep is not None else 0
+    nqg = 1 if st.problem.g is not None else 0
+    up_terms = [1 + i + nq + nqg * i for i in range(1, s)]
+    rows = []
+    for name, (tot_ms, cnt) in sorted(kt.items(), key=lambda kv: -kv[1][0]):
+        per = tot_ms / cnt
+        b = None
+        if name.startswith("k_mega"):
+            b = kb["k_mega"]
+        elif name.startswith("k_sub_up"):
+            b = kb["k_sub_up"]
+        elif name.startswith("k_sub_down"):
+            b = kb["k_sub_down"]
+        elif name.startswith("k_leaf_fd_mma") and name.endswith(", 4>"):
+            b = statistics.mean(kb["leaf_up_terms"](nt) for nt in up_terms)
+        elif name.startswith("k_leaf_fd_mma") and name.endswith(", 2>"):
+            b = kb["leaf_down"]
+        elif name.startswith("k_leaf_fd_mma") and name.endswith(", 3>"):
+            b = kb["leaf_lu"]
+        elif name.startswith("k_root_dir"):
+            b = kb["root_dir"](s - 1)
+        row = {"kernel": name, "launches_per_step": cnt / nsteps, "us_per_launch": 1e3 * per,
+               "share_of_step": tot_ms / total if total else None, "bytes_per_launch": b}
+        if b:
+            row["achieved_gbs"] = b / (per * 1e-3) / 1e9
+            row["frac"] = row["achieved_gbs"] / peak
+        rows.append(row)
+    return rows
 
 
 if __name__ == "__main__":

@@ -119,6 +119,16 @@ size_t hps_ops_device_bytes(const hps_ops* ops);
  * solver.py:221-228 with the Kronecker-sum factorisation of A_ii. */
 int hps_ops_set_leaf_fd(hps_ops* ops, const double* host, int count);
 
+/* Measurement hooks (bench.py): per-kernel CUDA-event timing of this
+ * library's launches on streams that are not being captured.  While enabled,
+ * each launch is bracketed by two events (this serialises the programmatic-
+ * dependent-launch overlap of neighbouring kernels).  hps_ktimer_collect
+ * synchronises the device and returns the number of distinct kernels (<= max):
+ * names ('\n'-separated, mangled), total milliseconds and launch counts,
+ * then clears the records. */
+void hps_ktimer_enable(int on);
+int hps_ktimer_collect(char* names, int names_len, double* ms, long long* counts, int max);
+
 /* merge(T_alpha, T_beta, node) (solver.py:67-81) on the device for one node:
  * Tc = [T_alpha; T_beta], two nbc x nbc row-major DtN maps (a smaller child's
  * map zero-padded), i1a/i3a/i2b/i3b the node's child-local index maps (device
@@ -243,6 +253,11 @@ int hps_solve_phase(const hps_ops* ops, int phases, int part0, int part1, int k,
  * nparts = 1). */
 int hps_plan_partition(const hps_plan* plan, int k, int* nparts, int* lstar, int* n12,
                        long long* flux_offset);
+
+/* The first parent level the fused subtree kernels run (levels >= it);
+ * levels above run in the wide-level dataflow kernel / per-level launches.
+ * Measurement only (bench.py's per-kernel algorithmic bytes). */
+int hps_plan_fused_level(const hps_plan* plan);
 
 /* ------------------------------------------------------------------------
  * Stage right-hand-side assembly (timestep.py:237-266 and the leaf-local

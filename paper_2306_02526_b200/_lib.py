@@ -81,6 +81,9 @@ SIGNATURES = {
     "hps_ops_build": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(BuildDesc), ctypes.c_void_p,
                                      ctypes.POINTER(ctypes.c_void_p)]),
     "hps_ops_destroy": (None, [ctypes.c_void_p]),
+    "hps_ktimer_enable": (None, [_i]),
+    "hps_plan_fused_level": (_i, [_vp]),
+    "hps_ktimer_collect": (_i, [ctypes.c_char_p, _i, c_double_p, c_ll_p, _i]),
     "hps_merge_node": (_i, [_i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp]),
     "hps_ops_device_bytes": (ctypes.c_size_t, [ctypes.c_void_p]),
     "hps_ops_get_leaf": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, c_double_p]),
@@ -172,3 +175,30 @@ def dbl_ptr(a):
 
 def as_i32(a):
     return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def kernel_times(max_kernels=64):
+    """{kernel name: (total ms, launches)} of the launches timed since
+    hps_ktimer_enable(1) (hps_ktimer_collect; synchronises the device)."""
+    import subprocess
+    lib = load()
+    names = ctypes.create_string_buffer(1 << 16)
+    ms = (ctypes.c_double * max_kernels)()
+    cnt = (ctypes.c_longlong * max_kernels)()
+    n = lib.hps_ktimer_collect(names, len(names), ms, cnt, max_kernels)
+    if n < 0:
+        check(n, "hps_ktimer_collect")
+    raw = names.value.decode().split("\n")[:n]
+    try:
+        dem = subprocess.run(["c++filt"], input="\n".join(raw), capture_output=True, text=True,
+                             timeout=10).stdout.split("\n")[:n]
+    except (OSError, subprocess.SubprocessError):
+        dem = raw
+    out = {}
+    for i, name in enumerate(dem if len(dem) == n else raw):
+        name = name.replace("hpsb::", "").replace("(anonymous namespace)::", "")
+        name = name.split("(")[0].replace("void ", "").strip()
+        a, c = out.get(name, (0.0, 0))
+        out[name] = (a + ms[i], c + cnt[i])
+    return out
+

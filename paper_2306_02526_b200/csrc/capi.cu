@@ -5,6 +5,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <unordered_map>
 #include <vector>
 
@@ -14,6 +16,37 @@
 namespace hpsb {
 
 std::atomic<long long> g_launches{0};
+std::atomic<int> g_ktimer_on{0};
+
+// ---- per-kernel event timing (hps_ktimer_*)
+struct KRec { cudaEvent_t a, b; const void* fn; };
+static std::mutex g_kt_mu;
+static std::vector<KRec> g_kt_recs;
+static std::vector<cudaEvent_t> g_kt_pool;
+
+static cudaEvent_t kt_event() {
+  if (!g_kt_pool.empty()) { cudaEvent_t e = g_kt_pool.back(); g_kt_pool.pop_back(); return e; }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+cudaEvent_t ktimer_begin(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  cudaEvent_t a = kt_event();
+  if (a) cudaEventRecord(a, st);
+  return a;
+}
+
+void ktimer_end(cudaEvent_t a, const void* fn, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_kt_mu);
+  cudaEvent_t b = kt_event();
+  if (!b) return;
+  cudaEventRecord(b, st);
+  g_kt_recs.push_back({a, b, fn});
+}
 static thread_local char g_err[1024] = {0};
 static thread_local long long g_err_node = -1;
 
@@ -122,6 +155,62 @@ static int singular(int n, double pmin, double pmax, const char* kind, long long
   return HPS_ERR_SINGULAR;
 }
 
+// Accuracy of the explicit inverses the solve applies.  Gauss-Jordan gives
+// X ~ A^-1 with a relative residual of ~kappa*eps; the solves chain these
+// products through every level of the tree and the time stepper applies the
+// same operators thousands of times, so a residual that is systematic (the
+// same every step) accumulates linearly.  One Newton step
+// X <- X + X (I - A X) squares the residual; the products that use X in the
+// build (S = X R) get one step of residual correction S <- S + X (R - A S).
+// HPSB_NO_REFINE=1 skips both (A/B).
+static bool refine_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_REFINE");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
+// X (n x n per batch entry, ld ldx, stride sX) <- X + X (I - A X); A n x n dense (stride sA), batch entries.
+// tmp: 2 * batch * n * n doubles; ident: n * n identity.
+static int newton_inverse(int n, int batch, const double* A, long long sA, double* X, int ldx, long long sX,
+                          double* tmp, const double* ident, cudaStream_t st) {
+  double* E = tmp;
+  double* Xn = tmp + (size_t)batch * n * n;
+  GemmArgs r{};  // E = I - A X
+  r.M = n; r.N = n; r.K = n; r.alpha = -1.0; r.beta = 1.0;
+  r.A = A; r.lda = n; r.sA = sA; r.B = X; r.ldb = ldx; r.sB = sX;
+  r.D = ident; r.ldd = n; r.sD = 0; r.C = E; r.ldc = n; r.sC = (long long)n * n; r.batch = batch;
+  if (int rc = gemm(r, st)) return rc;
+  GemmArgs u{};  // Xn = X + X E
+  u.M = n; u.N = n; u.K = n; u.alpha = 1.0; u.beta = 1.0;
+  u.A = X; u.lda = ldx; u.sA = sX; u.B = E; u.ldb = n; u.sB = (long long)n * n;
+  u.D = X; u.ldd = ldx; u.sD = sX; u.C = Xn; u.ldc = n; u.sC = (long long)n * n; u.batch = batch;
+  if (int rc = gemm(u, st)) return rc;
+  HPSB_CUDA(cudaMemcpy2DAsync(X, (size_t)ldx * 8, Xn, (size_t)n * 8, (size_t)n * 8, (size_t)batch * n,
+                              cudaMemcpyDeviceToDevice, st));
+  (void)sX;
+  return 0;
+}
+
+// S (M x N, ld lds, stride sS) = alpha X R refined once: S <- S + alpha X (R - A S / alpha) where X ~ A^-1.
+// Implemented for the two uses: S = X R (alpha 1) and S = -X R (alpha -1).  tmp: batch * M * N doubles.
+static int refine_solve(int M, int N, int batch, double alpha, const double* A, long long sA, const double* X,
+                        int ldx, long long sX, const double* R, int ldr, long long sR, double* S, int lds,
+                        long long sS, double* tmp, cudaStream_t st) {
+  // residual of X^-1 S = alpha R:  Res = alpha R - A S
+  GemmArgs r{};
+  r.M = M; r.N = N; r.K = M; r.alpha = -1.0; r.beta = alpha;
+  r.A = A; r.lda = M; r.sA = sA; r.B = S; r.ldb = lds; r.sB = sS;
+  r.D = R; r.ldd = ldr; r.sD = sR; r.C = tmp; r.ldc = N; r.sC = (long long)M * N; r.batch = batch;
+  if (int rc = gemm(r, st)) return rc;
+  GemmArgs u{};  // S = S + X Res
+  u.M = M; u.N = N; u.K = M; u.alpha = 1.0; u.beta = 1.0;
+  u.A = X; u.lda = ldx; u.sA = sX; u.B = tmp; u.ldb = N; u.sB = (long long)M * N;
+  u.D = S; u.ldd = lds; u.sD = sS; u.C = S; u.ldc = lds; u.sC = sS; u.batch = batch;
+  return gemm(u, st);
+}
+
 }  // namespace hpsb
 
 using namespace hpsb;
@@ -130,6 +219,45 @@ using namespace hpsb;
 extern "C" {
 
 int hps_version(void) { return 1; }
+
+void hps_ktimer_enable(int on) { g_ktimer_on.store(on ? 1 : 0); }
+
+int hps_ktimer_collect(char* names, int names_len, double* ms, long long* counts, int max) {
+  if (cudaDeviceSynchronize() != cudaSuccess) { set_error("hps_ktimer_collect: device error"); return HPS_ERR_CUDA; }
+  std::map<std::string, std::pair<double, long long>> agg;
+  {
+    std::lock_guard<std::mutex> lk(g_kt_mu);
+    for (const KRec& r : g_kt_recs) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      const char* nm = nullptr;
+      if (cudaFuncGetName(&nm, r.fn) != cudaSuccess || !nm) nm = "?";
+      auto& v = agg[nm];
+      v.first += t;
+      v.second += 1;
+      g_kt_pool.push_back(r.a);
+      g_kt_pool.push_back(r.b);
+    }
+    g_kt_recs.clear();
+  }
+  // names: '\n'-separated, in the same order as ms / counts
+  int n = 0;
+  std::string all;
+  for (auto& kv : agg) {
+    if (n >= max) break;
+    if (ms) ms[n] = kv.second.first;
+    if (counts) counts[n] = kv.second.second;
+    all += kv.first;
+    all += '\n';
+    ++n;
+  }
+  if (names && names_len > 0) {
+    const size_t m = std::min((size_t)names_len - 1, all.size());
+    memcpy(names, all.data(), m);
+    names[m] = 0;
+  }
+  return n;
+}
 
 int hps_merge_node(int nbc, const double* Tc, int n1a, int n2b, int n3, const int* i1a, const int* i3a,
                    const int* i2b, const int* i3b, long long node_index, double* Xinv, double* S,
@@ -334,6 +462,15 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     auto it = std::find(tmp.begin(), tmp.end(), (void*)p);
     if (it != tmp.end()) { cudaFree(p); tmp.erase(it); }
   };
+  // an n x n identity (Newton refinement of the explicit inverses)
+  auto ident = [&](int n) -> double* {
+    std::vector<double> h((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) h[(size_t)i * n + i] = 1.0;
+    double* p = talloc((size_t)n * n);
+    if (p && cudaMemcpy(p, h.data(), h.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return p;
+  };
+  const bool refine = refine_enabled();
   // stencil rows, coefficients
   double *dD2x, *dD2y, *dD1x, *dD1y, *dcoef;
   std::vector<double> Dbi((size_t)nb * ni), Dbb((size_t)nb * nb);
@@ -382,12 +519,25 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   if (int rc = leaf_assemble(Lc, ni, nb, dcoef, d->has_c1, d->has_c2, d->has_c, dD2x, dD2y, dD1x, dD1y,
                              d->sigma, d->dt_gamma, Aii, Aib, st))
     return fail(rc);
+  double* Aii0 = refine ? talloc((size_t)Lc * ni * ni) : nullptr;  // A_ii (Gauss-Jordan overwrites it)
+  if (refine) {
+    if (!Aii0) { set_error("out of device memory (leaf build)"); return fail(HPS_ERR_CUDA); }
+    HPSB_CUDA(cudaMemcpyAsync(Aii0, Aii, (size_t)Lc * ni * ni * 8, cudaMemcpyDeviceToDevice, st));
+  }
   if (int rc = gj_invert(ni, Lc, Aii, Ainv, P.ldi, (long long)ni * P.ldi, stats, st)) return fail(rc);
   {
     std::vector<double> hs;
     int bad = check_pivots(stats, Lc, ni, hs, st);
     if (bad == -2) { set_error("cuda error during leaf build"); return fail(HPS_ERR_CUDA); }
     if (bad >= 0) return fail(singular(ni, hs[2 * bad], hs[2 * bad + 1], "leaf", P.leaf_node_index[bad]));
+  }
+  if (refine) {
+    double* I = ident(ni);
+    double* tmp = talloc(2 * (size_t)Lc * ni * std::max(ni, nb));
+    if (!I || !tmp) { set_error("out of device memory (leaf refinement)"); return fail(HPS_ERR_CUDA); }
+    if (int rc = newton_inverse(ni, Lc, Aii0, (long long)ni * ni, Ainv, P.ldi, (long long)ni * P.ldi, tmp, I, st))
+      return fail(rc);
+    tfree(tmp); tfree(I);
   }
   {
     GemmArgs a{};  // S = -Ainv A_ib
@@ -396,6 +546,14 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     a.B = Aib; a.ldb = nb; a.sB = (long long)ni * nb; a.tB = 0;
     a.C = Sl; a.ldc = P.ldb; a.sC = (long long)ni * P.ldb; a.batch = Lc;
     if (int rc = gemm(a, st)) return fail(rc);
+    if (refine) {
+      double* tmp = talloc((size_t)Lc * ni * nb);
+      if (!tmp) { set_error("out of device memory (leaf refinement)"); return fail(HPS_ERR_CUDA); }
+      if (int rc = refine_solve(ni, nb, Lc, -1.0, Aii0, (long long)ni * ni, Ainv, P.ldi, (long long)ni * P.ldi, Aib,
+                                nb, (long long)ni * nb, Sl, P.ldb, (long long)ni * P.ldb, tmp, st))
+        return fail(rc);
+      tfree(tmp);
+    }
     GemmArgs t{};  // T = D_bi S + D_bb
     t.M = nb; t.N = nb; t.K = ni; t.alpha = 1.0; t.beta = 1.0;
     t.A = O.D_bi; t.lda = ni; t.sA = 0; t.tA = 0;
@@ -424,7 +582,7 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     tfree(Ainv);
     tfree(Sl);
   }
-  tfree(Aii); tfree(Aib); tfree(stats);
+  tfree(Aii); tfree(Aib); tfree(stats); tfree(Aii0);
 
   // ---- merges, deepest level first (solver.py:127-155)
   double* Tchild = Tleaf;
@@ -480,6 +638,11 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     if (int rc = merge_gather(ce, n3, lv.n1a, lv.n2b, lv.nbc, Tchild, sTchild, lv.i1a, lv.i3a, lv.i2b, lv.i3b,
                               X33, R, Tst, lv.ld3, Tnew, st))
       return fail(rc);
+    double* X330 = refine ? talloc((size_t)ce * n3 * n3) : nullptr;  // X33 (Gauss-Jordan overwrites it)
+    if (refine) {
+      if (!X330) { set_error("out of device memory (merge level %d)", l); return fail(HPS_ERR_CUDA); }
+      HPSB_CUDA(cudaMemcpyAsync(X330, X33, (size_t)ce * n3 * n3 * 8, cudaMemcpyDeviceToDevice, st));
+    }
     if (int rc = gj_invert(n3, ce, X33, Xinv, lv.ld3, (long long)n3 * lv.ld3, lst, st)) return fail(rc);
     {
       std::vector<double> hs;
@@ -487,12 +650,29 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
       if (bad == -2) { set_error("cuda error during merge build"); return fail(HPS_ERR_CUDA); }
       if (bad >= 0) return fail(singular(n3, hs[2 * bad], hs[2 * bad + 1], "merge", lv.node_index[bad]));
     }
+    if (refine) {
+      double* I = ident(n3);
+      double* tmp = talloc(2 * (size_t)ce * n3 * n3);
+      if (!I || !tmp) { set_error("out of device memory (merge level %d)", l); return fail(HPS_ERR_CUDA); }
+      if (int rc = newton_inverse(n3, ce, X330, (long long)n3 * n3, Xinv, lv.ld3, (long long)n3 * lv.ld3, tmp, I, st))
+        return fail(rc);
+      tfree(tmp); tfree(I);
+    }
     GemmArgs a{};  // S = Xinv [-Ta31 | Tb32]
     a.M = n3; a.N = n12; a.K = n3; a.alpha = 1.0; a.beta = 0.0;
     a.A = Xinv; a.lda = lv.ld3; a.sA = (long long)n3 * lv.ld3; a.tA = 0;
     a.B = R; a.ldb = n12; a.sB = (long long)n3 * n12; a.tB = 0;
     a.C = S; a.ldc = lv.ld12; a.sC = (long long)n3 * lv.ld12; a.batch = ce;
     if (int rc = gemm(a, st)) return fail(rc);
+    if (refine) {
+      double* tmp = talloc((size_t)ce * n3 * n12);
+      if (!tmp) { set_error("out of device memory (merge level %d)", l); return fail(HPS_ERR_CUDA); }
+      if (int rc = refine_solve(n3, n12, ce, 1.0, X330, (long long)n3 * n3, Xinv, lv.ld3, (long long)n3 * lv.ld3, R,
+                                n12, (long long)n3 * n12, S, lv.ld12, (long long)n3 * lv.ld12, tmp, st))
+        return fail(rc);
+      tfree(tmp);
+      tfree(X330);
+    }
     {
       GemmArgs t{};  // T = blkdiag + Tstack S
       t.M = n12; t.N = n12; t.K = n3; t.alpha = 1.0; t.beta = 1.0;
@@ -705,6 +885,8 @@ int hps_plan_partition(const hps_plan* h, int k, int* nparts, int* lstar, int* n
   if (flux_offset) *flux_offset = P.nparts > 1 && k > 0 ? (long long)exchange_offset(P, k) : -1;
   return HPS_OK;
 }
+
+int hps_plan_fused_level(const hps_plan* h) { return h ? h->P.dF : -1; }
 
 int hps_solve_phase(const hps_ops* h, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
                     const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt,

@@ -54,16 +54,21 @@ __host__ __device__ inline long long cdiv(long long a, long long b) { return (a 
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-// bulk L2 prefetch of [p, p + bytes) (16-byte aligned, bytes a multiple of 16)
-__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 
 bool pdl_enabled();  // HPSB_NO_PDL=1 disables
 
+// Per-kernel CUDA-event timing (hps_ktimer_enable): while on, every launch
+// through launch_pdl / launch_plain on a stream that is not being captured is
+// bracketed by two events on its stream; hps_ktimer_collect sums the elapsed
+// times per kernel.  The events serialise the PDL overlap of neighbouring
+// kernels, so this is a measurement pass, not the timed one.
+extern std::atomic<int> g_ktimer_on;
+cudaEvent_t ktimer_begin(cudaStream_t st);           // nullptr unless timing this launch
+void ktimer_end(cudaEvent_t a, const void* fn, cudaStream_t st);
+
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
+cudaError_t launch_kernel(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                          Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -71,10 +76,27 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl && pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  cudaEvent_t ev = g_ktimer_on.load(std::memory_order_relaxed) ? ktimer_begin(st) : nullptr;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (ev) ktimer_end(ev, (const void*)kern, st);
+  return e;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  return launch_kernel(true, kern, grid, block, smem, st, std::forward<Args>(args)...);
+}
+
+// no programmatic dependency (a kernel that reads its predecessor's output
+// from its first instruction)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_plain(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                         Args&&... args) {
+  return launch_kernel(false, kern, grid, block, smem, st, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------------------------

@@ -484,10 +484,11 @@ int root_dirichlet(const Ops& ops, int ns, const double* fb, long long ld_f, dou
     return -1;
   }
   const int R = pn.R, C = pn.C, nsplit = (C + RDK - 1) / RDK;
-  k_root_dir<<<dim3((unsigned)cdiv(R, MRB), (unsigned)nsplit), MT, 0, st>>>(pn.base, R, C, pn.TR, P.root_bpos, fb,
-                                                                         ld_f, ns, scratch);
+  HPSB_CUDA(launch_plain(k_root_dir, dim3((unsigned)cdiv(R, MRB), (unsigned)nsplit), dim3(MT), 0, st, pn.base, R,
+                         C, pn.TR, (const int*)P.root_bpos, fb, ld_f, ns, scratch));
   HPSB_LAUNCH_CHECK();
-  k_root_sum<<<(unsigned)cdiv((long long)ns * R, 256), 256, 0, st>>>(scratch, nsplit, ns, R, out, ld_out);
+  HPSB_CUDA(launch_plain(k_root_sum, dim3((unsigned)cdiv((long long)ns * R, 256)), dim3(256), 0, st,
+                         (const double*)scratch, nsplit, ns, R, out, ld_out));
   HPSB_LAUNCH_CHECK();
   return 0;
 }
