@@ -727,8 +727,9 @@ def profiled_kernel_traffic(config, kernel):
             d = json.load(fh).get(config, {})
     except (OSError, ValueError):
         return None
+    norm = lambda n: n.replace("true", "1").replace("false", "0").replace(" ", "")
     for name, v in d.items():
-        if name == kernel or kernel.startswith(name):
+        if norm(name) == norm(kernel):
             return v
     return None
 
