@@ -94,6 +94,19 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+// release / acquire counters (the CUTLASS semaphore pattern): a CTA's writes,
+// ordered before one thread by a barrier, are published by that thread's
+// release atomic; the consumer's acquire load plus a barrier orders its reads
+// after them.  Cheaper than __threadfence (MEMBAR.SC + an L1 invalidate).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
   long long spins = 0;
   while (ld_acquire(p) < target) {
@@ -305,16 +318,11 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
       const size_t slot = PN ? (size_t)rb * MRB + r : (size_t)(ng * MNB + oj) * g.R + orow;
       const size_t pstride = PN ? (size_t)g.RB * MRB : (size_t)g.NG * MNB * g.R;
       if (ovalid) g.part[(size_t)split * pstride + slot] = y;
-      // barrier + one thread's fence + atomic publishes the CTA's partials
-      // (the cooperative-groups grid barrier pattern); the last arriver's
-      // fence after the atomic orders the CTA's partial reads after it
+      // barrier + one thread's acq_rel atomic publishes the CTA's partials; the
+      // last arriver's barrier after it orders the CTA's partial reads after them
       __syncthreads();
       const unsigned total = g.pair ? (unsigned)(g.Sdn + g.Sup) : (unsigned)g.S;
-      if (tid == 0) {
-        __threadfence();
-        s_last = atomicAdd(g.sem + ng * g.RB + rb, 1u) == total - 1;
-        if (s_last) __threadfence();
-      }
+      if (tid == 0) s_last = atom_add_acq_rel(g.sem + ng * g.RB + rb, 1u) == total - 1;
       __syncthreads();
       emit_now = s_last;
       if (emit_now) {
@@ -348,10 +356,7 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     if (emit_now) {
       __syncthreads();
-      if (tid < 32) {
-        __threadfence();
-        if (tid < nv) atomicAdd(g.done + node0 + tid, 1u);
-      }
+      if (tid < nv) red_add_release(g.done + node0 + tid, 1u);
       if (p.trace && tid == 0) p.trace[MTS * t + 4] = gtime();
     }
     __syncthreads();  // xs / red / sidx are reused by the next task

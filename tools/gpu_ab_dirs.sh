@@ -5,7 +5,7 @@ for i in 1 2 3; do
   for v in A B; do
     if [ $v = A ]; then d=ab; else d=.; fi
     (cd $d && env ${AB_ENV} timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline ${BENCH_ARGS}) > gpurun_out/bench_$v.log 2>&1
-    tail -1 gpurun_out/bench_$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), 'solve', round(d['roofline']['solve_ms'],4), 'e2e', '%.3e'%d['e2e']['value'])" >> $out 2>&1 || tail -3 gpurun_out/bench_$v.log >> $out
+    tail -1 gpurun_out/bench_$v.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['ms_per_step'],4), 'solve', round(d['solve']['solve_ms'],4), 'mega', round(d['roofline']['us_per_launch'],1), 'e2e', '%.3e'%d['e2e']['value'])" >> $out 2>&1 || tail -3 gpurun_out/bench_$v.log >> $out
   done
 done
 cat $out
