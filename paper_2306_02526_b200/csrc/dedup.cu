@@ -166,12 +166,8 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
           if (m < a.M && r < a.N) a.part[((size_t)split * a.M + m) * a.N + r] = acc[i][j][h];
         }
     }
-    __syncthreads();  // barrier + one thread's fence + atomic (see mega.cu)
-    if (tid == 0) {
-      __threadfence();
-      s_last = atomicAdd(a.cnt + tile, 1u) == (unsigned)a.nsplit - 1;
-      if (s_last) __threadfence();
-    }
+    __syncthreads();  // barrier + one thread's acq_rel atomic (hps_common.cuh)
+    if (tid == 0) s_last = atom_add_acq_rel(a.cnt + tile, 1u) == (unsigned)a.nsplit - 1;
     __syncthreads();
     if (!s_last) return;
 #pragma unroll

@@ -55,6 +55,19 @@ __host__ __device__ inline long long cdiv(long long a, long long b) { return (a 
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// release / acquire counters (the CUTLASS semaphore pattern): a CTA's writes,
+// ordered before one thread by a barrier, are published by that thread's
+// release atomic; the consumer's acquire load plus a barrier orders its reads
+// after them.  Cheaper than __threadfence (MEMBAR.SC + an L1 invalidate).
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 bool pdl_enabled();  // HPSB_NO_PDL=1 disables
 
 // Per-kernel CUDA-event timing (hps_ktimer_enable): while on, every launch

@@ -185,13 +185,8 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
       double2 v = make_double2(acc0[kk], acc1[kk]);
       *reinterpret_cast<double2*>(part + ((long long)kk * sp.nsplit + split) * Pp + pv) = v;
     }
-    __syncthreads();  // barrier + one thread's fence + atomic (see mega.cu)
-    if (tid == 0) {
-      __threadfence();
-      unsigned old = atomicAdd(a.cnt + cidx, 1u);
-      s_last = (old == (unsigned)sp.nsplit - 1);
-      if (s_last) __threadfence();
-    }
+    __syncthreads();  // barrier + one thread's acq_rel atomic (hps_common.cuh)
+    if (tid == 0) s_last = atom_add_acq_rel(a.cnt + cidx, 1u) == (unsigned)sp.nsplit - 1;
     __syncthreads();
     if (!s_last) return;
 #pragma unroll

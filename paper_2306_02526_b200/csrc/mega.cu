@@ -94,19 +94,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
-// release / acquire counters (the CUTLASS semaphore pattern): a CTA's writes,
-// ordered before one thread by a barrier, are published by that thread's
-// release atomic; the consumer's acquire load plus a barrier orders its reads
-// after them.  Cheaper than __threadfence (MEMBAR.SC + an L1 invalidate).
-__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
-  unsigned old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
   long long spins = 0;
   while (ld_acquire(p) < target) {
@@ -365,13 +352,9 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
   }
   // the last CTA out resets the counters for the next solve
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(exit_count, 1u) == gridDim.x - 1;
-  }
+  if (tid == 0) s_last = atom_add_acq_rel(exit_count, 1u) == gridDim.x - 1;
   __syncthreads();
   if (s_last) {
-    __threadfence();
     for (int i = tid; i < p.nreset; i += MT) p.reset[i] = 0u;
     __syncthreads();
     if (tid == 0) *exit_count = 0u;
