@@ -655,18 +655,26 @@ def main():
              "traffic": profiled_traffic(f"{args.config}/{layout}")}
 
     # roofline: the dominant kernel of the step (largest share of the step time)
-    if kernels:
-        top = max(kernels, key=lambda r: r["share_of_step"])
+    top = max(kernels, key=lambda r: r["share_of_step"]) if kernels else None
+    if top is not None and top.get("achieved_gbs"):
         traffic = profiled_kernel_traffic(args.config, top["kernel"])
         roof = {"bound": "hbm", "achieved": top["achieved_gbs"], "peak": peak, "unit": "GB/s",
                 "peak_source": src, "frac": top["achieved_gbs"] / peak, "traffic": traffic,
                 "kernel": top["kernel"], "us_per_launch": top["us_per_launch"],
                 "algorithmic_bytes_per_launch": top["bytes_per_launch"],
                 "share_of_step": top["share_of_step"]}
-    else:   # sharded: the whole stage solve
-        roof = {"bound": "hbm", "achieved": (b_op + b_vec) / (avg_solve * 1e-3) / 1e9, "peak": peak,
-                "unit": "GB/s", "peak_source": src, "traffic": None, "kernel": "hps_solve_phase (stage solve)"}
-        roof["frac"] = roof["achieved"] / peak
+    else:   # no byte model for the dominant kernel (sharded solve, multi-rhs GEMMs): the whole stage solve
+        t_hbm = (b_op + b_vec) / (peak * 1e9)
+        t_fp64 = flops / (FP64_TFLOPS * 1e12)
+        if t_hbm >= t_fp64:
+            roof = {"bound": "hbm", "achieved": (b_op + b_vec) / (avg_solve * 1e-3) / 1e9, "peak": peak,
+                    "unit": "GB/s", "peak_source": src}
+        else:
+            roof = {"bound": "tensor", "achieved": flops / (avg_solve * 1e-3) / 1e12, "peak": FP64_TFLOPS,
+                    "unit": "TFLOP/s", "peak_source": "measured FP64 DMMA (profiles/r01_fp64_peak.txt)"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof.update({"traffic": solve["traffic"], "kernel": "stage solve (hps_solve%s)" % ("_phase" if subtree else ""),
+                     "dominant_kernel": None if top is None else top["kernel"]})
 
     # the bench's own 64x64 sample: one GPU step against the CPU oracle's step
     cpu = None

@@ -14,6 +14,8 @@
 // nodes (the top of the tree: few nodes, operators up to hundreds of MB) use
 // the streaming panel kernel on a one-node panel, one virtual tile per
 // (node, tile): the operator is read from HBM once and re-read from L2.
+#include <stdlib.h>
+
 #include "hps_plan.cuh"
 
 namespace hpsb {
@@ -32,6 +34,7 @@ struct GsArgs {
   int nsplit, KC;              // split-K: CTA column range [split * KC, +KC) (KC a multiple of BK)
   double* part; unsigned* cnt; // split-K partials (nsplit x M x N) and per-tile semaphores
   const double* B; int ldb;    // operator, N x K row-major
+  const double* X;             // non-null: the gathered inputs, M x K row-major (k_gs_gather)
   GemvArgs g;                  // gathers / scatters (same fields as the streaming kernels)
 };
 
@@ -73,6 +76,21 @@ __device__ __forceinline__ void gs_out(const GemvArgs& a, int node, int r, int k
   }
 }
 
+// The (node, rhs) x K input matrix of a level GEMM gathered once: every
+// N-tile of the GEMM reads it (the top levels have few (node, rhs) rows but
+// thousands of operator rows, i.e. tens of N-tiles that would each repeat the
+// index-chasing gathers).
+template <int MODE>
+__global__ void k_gs_gather(GsArgs a) {
+  const long long n = (long long)a.M * a.K;
+  pdl_trigger();
+  pdl_wait();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(e / a.K), col = (int)(e % a.K);
+    const_cast<double*>(a.X)[e] = gs_x<MODE>(a.g, m % a.nodes, m / a.nodes, col);
+  }
+}
+
 // Every (node, rhs) pair is one row of the GEMM: the multi-rhs (ensemble)
 // level apply is one tensor-core GEMM over nodes x rhs.
 template <int MODE, int WN>
@@ -106,7 +124,8 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
     for (int i = 0; i < AE; ++i) {
       const int e = tid + NT * i, r = e / BK, c = e % BK;
       const int gm = m0 + r, gk = (kb + kt) * BK + c;
-      ra[i] = (gm < a.M && gk < a.K) ? gs_x<MODE>(a.g, gm % a.nodes, gm / a.nodes, gk) : 0.0;
+      ra[i] = (gm < a.M && gk < a.K) ? (a.X ? a.X[(long long)gm * a.K + gk] : gs_x<MODE>(a.g, gm % a.nodes, gm / a.nodes, gk))
+                                     : 0.0;
     }
   };
   auto store = [&](int buf) {
@@ -230,6 +249,14 @@ int launch_gs(GsArgs a, const GsSplit& sp, cudaStream_t st) {
   return 0;
 }
 
+static bool gs_gather_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_GS_GATHER");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 template <int MODE>
 int gs(const GsArgs& a, const Workspace& ws, cudaStream_t st) {
   const GsSplit sp = gs_split(a.M, a.N, a.K);
@@ -240,6 +267,14 @@ int gs(const GsArgs& a, const Workspace& ws, cudaStream_t st) {
   GsArgs b = a;
   b.part = ws.part;
   b.cnt = ws.cnt;
+  b.X = nullptr;
+  if (sp.gather_doubles && ws.xg && gs_gather_enabled()) {
+    b.X = ws.xg;
+    const long long n = (long long)a.M * a.K;
+    HPSB_CUDA(launch_pdl(k_gs_gather<MODE>, dim3((unsigned)std::min<long long>(cdiv(n, 256), 148LL * 16)), dim3(256), 0,
+                         st, b));
+    HPSB_LAUNCH_CHECK();
+  }
   if (sp.WN == 1) return launch_gs<MODE, 1>(b, sp, st);
   if (sp.WN == 2) return launch_gs<MODE, 2>(b, sp, st);
   return launch_gs<MODE, 4>(b, sp, st);
@@ -265,6 +300,7 @@ GsSplit gs_split(long long M, int N, int K) {
     s.part_doubles = (size_t)s.nsplit * M * N;
     s.counters = s.tiles;
   }
+  if (cdiv(N, 32 * s.WN) >= 4) s.gather_doubles = (size_t)M * K;  // many N-tiles re-read the inputs
   return s;
 }
 

@@ -149,6 +149,7 @@ struct Workspace {
   unsigned* cnt = nullptr;  // split-K semaphores (zero between launches)
   unsigned* mega_cnt = nullptr;  // persistent level kernel: completion counters (zero between launches)
   double* mega_part = nullptr;   // ... and its split partials
+  double* xg = nullptr;          // shared-layout GEMMs: the gathered (node, rhs) x K inputs (GsSplit)
 };
 size_t workspace_bytes(const Plan& P, int k);
 void carve_workspace(const Plan& P, int k, void* base, Workspace& ws);
@@ -205,6 +206,7 @@ struct GsSplit {
   int WN = 1, tiles = 0, nsplit = 1, KC = 0;
   size_t part_doubles = 0;
   int counters = 0;
+  size_t gather_doubles = 0;  // > 0: the (node, rhs) x K input matrix is gathered once up front
 };
 GsSplit gs_split(long long M, int N, int K);  // (node, rhs) rows x operator rows x operator columns
 

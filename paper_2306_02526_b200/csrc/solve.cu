@@ -2,6 +2,8 @@
 // launches on one stream: boundary scatter, leaf upward pass, level upward
 // merges (deepest first), level downward sweep (root first), leaf downward
 // reconstruction.  No host synchronisation; capturable in a CUDA graph.
+#include <stdlib.h>
+
 #include "hps_plan.cuh"
 
 namespace hpsb {
@@ -54,7 +56,7 @@ static void solve_panels(const Plan& P, std::vector<std::pair<Panel, int>>& out)
   }
 }
 
-static void scratch_sizes(const Plan& P, int k, size_t& part, size_t& cnt) {
+static void scratch_sizes(const Plan& P, int k, size_t& part, size_t& cnt, size_t* xg = nullptr) {
   std::vector<std::pair<Panel, int>> pns;
   solve_panels(P, pns);
   part = 0; cnt = 0;
@@ -71,6 +73,7 @@ static void scratch_sizes(const Plan& P, int k, size_t& part, size_t& cnt) {
       for (const GsSplit& sp : {gs_split(M, lv.n3 + (d > 0 ? lv.n12 : 0), lv.n3), gs_split(M, lv.n3, lv.n12)}) {
         part = std::max(part, sp.part_doubles);
         cnt = std::max(cnt, (size_t)sp.counters);
+        if (xg) *xg = std::max(*xg, sp.gather_doubles);
       }
     }
   }
@@ -86,14 +89,15 @@ size_t workspace_bytes(const Plan& P, int k) {
     if (d >= 1) add((long long)P.lv[d].c * P.lv[d].n12);
     add((long long)P.lv[d].c * P.lv[d].n3);
   }
-  size_t part, cnt;
-  scratch_sizes(P, k, part, cnt);
+  size_t part, cnt, xg = 0;
+  scratch_sizes(P, k, part, cnt, &xg);
   n += (part * 8 + 255) & ~(size_t)255;
   n += (cnt * 4 + 255) & ~(size_t)255;
   size_t mc, mp;
   mega_scratch(P, mc, mp);
   n += (mc * 4 + 255) & ~(size_t)255;
   n += (mp * 8 + 255) & ~(size_t)255;
+  n += (xg * 8 + 255) & ~(size_t)255;
   return n + 256;
 }
 
@@ -113,8 +117,8 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
     if (d >= 1) ws.H[d] = take((long long)P.lv[d].c * P.lv[d].n12);
     ws.W3[d] = take((long long)P.lv[d].c * P.lv[d].n3);
   }
-  size_t part, cnt;
-  scratch_sizes(P, k, part, cnt);
+  size_t part, cnt, xg = 0;
+  scratch_sizes(P, k, part, cnt, &xg);
   ws.part = (double*)p;
   p += (part * 8 + 255) & ~(size_t)255;
   ws.cnt = (unsigned*)p;  // zeroed by the caller when the workspace is created
@@ -124,6 +128,8 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
   ws.mega_cnt = (unsigned*)p;  // zeroed likewise
   p += (mc * 4 + 255) & ~(size_t)255;
   ws.mega_part = (double*)p;
+  p += (mp * 8 + 255) & ~(size_t)255;
+  ws.xg = xg ? (double*)p : nullptr;
 }
 
 // one level's upward merge over nodes [n0, n1) (solver.py:243-256)
@@ -203,7 +209,11 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   // fused subtree kernels for the deep levels, except for many-rhs solves on
   // shared operators: there every level is one tensor-core GEMM over
   // (node, rhs) rows (dedup.cu)
-  const bool fused = P.dF < P.depth && !(ops.shared_levels && k >= kSharedGemmRhs);
+  static const int sub_rhs_max = [] {  // A/B: HPSB_SUB_RHS_MAX=n fuses the deep levels up to n rhs
+    const char* e = getenv("HPSB_SUB_RHS_MAX");
+    return e ? atoi(e) : kSharedGemmRhs - 1;
+  }();
+  const bool fused = P.dF < P.depth && !(ops.shared_levels && k > sub_rhs_max);
   const int dW = fused ? P.dF : P.depth;  // levels [lstar, dW) run level by level
   // leaf outputs: W (row stride ldw, rhs stride sw) and H (child stride hs, rhs stride sh)
   long long ldw = P.ni, sw = Lni, hs = P.nb, sh = Lnb;
