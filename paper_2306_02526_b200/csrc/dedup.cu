@@ -309,7 +309,11 @@ GsSplit gs_split(long long M, int N, int K) {
 // panel is node-aligned (fused subtree levels) always take the GEMM
 bool shared_gemm(const Plan& P, int d, int nodes, int k) {
   if (d >= P.dF) return true;
-  return (long long)nodes * k >= kSharedGemmNodes || (k >= kSharedGemmRhs && (long long)nodes * k >= 256);
+  static const long long min_rows = [] {  // A/B: HPSB_GS_MIN_ROWS
+    const char* e = getenv("HPSB_GS_MIN_ROWS");
+    return e ? atoll(e) : 64LL;
+  }();
+  return (long long)nodes * k >= kSharedGemmNodes || (k >= kSharedGemmRhs && (long long)nodes * k >= min_rows);
 }
 
 int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const double* Hc, long long Hc_k,

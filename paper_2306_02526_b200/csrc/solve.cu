@@ -206,14 +206,18 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
 
   const bool up = (g != nullptr) || (jump != nullptr);
   const int nw = P.ni + P.nb;
-  // fused subtree kernels for the deep levels, except for many-rhs solves on
+  bool mb_applies(const Ops& ops, int k);
+
+// fused subtree kernels for the deep levels, except for many-rhs solves on
   // shared operators: there every level is one tensor-core GEMM over
   // (node, rhs) rows (dedup.cu)
   static const int sub_rhs_max = [] {  // A/B: HPSB_SUB_RHS_MAX=n fuses the deep levels up to n rhs
     const char* e = getenv("HPSB_SUB_RHS_MAX");
     return e ? atoi(e) : kSharedGemmRhs - 1;
   }();
-  const bool fused = P.dF < P.depth && !(ops.shared_levels && k > sub_rhs_max);
+  // ... unless the member-blocked subtree kernels take them (member_subtree.cu)
+  const bool many = ops.shared_levels && k > sub_rhs_max;
+  const bool fused = P.dF < P.depth && (!many || (!jump && k >= kSharedGemmRhs && mb_applies(ops, k)));
   const int dW = fused ? P.dF : P.depth;  // levels [lstar, dW) run level by level
   // leaf outputs: W (row stride ldw, rhs stride sw) and H (child stride hs, rhs stride sh)
   long long ldw = P.ni, sw = Lni, hs = P.nb, sh = Lnb;

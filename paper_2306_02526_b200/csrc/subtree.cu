@@ -439,10 +439,19 @@ int fuse_level(const Plan& P) {
   return best;
 }
 
+int mb_subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, long long sh, long long hs,
+                  int b0, int b1, cudaStream_t st);
+int mb_subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u, int b0,
+                    int b1, cudaStream_t st);
+
 int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, long long sh, long long hs,
                const double* jump, long long ld_jump, double inv_dt, int b0, int b1, cudaStream_t st) {
   const Plan& P = *ops.plan;
   if (P.dF >= P.depth) return 0;
+  if (ops.shared_levels && k >= kSharedGemmRhs && !jump) {  // many rhs: member-blocked kernels
+    const int rc = mb_subtree_up(ops, ws, k, Hleaf, sh, hs, b0, b1, st);
+    if (rc != 1) return rc;
+  }
   SubArgs a{};
   fill_args(ops, ws, k, a);
   a.b0 = b0;
@@ -460,6 +469,10 @@ int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double
                  int b1, cudaStream_t st) {
   const Plan& P = *ops.plan;
   if (P.dF >= P.depth) return 0;
+  if (ops.shared_levels && k >= kSharedGemmRhs) {
+    const int rc = mb_subtree_down(ops, ws, k, has_w3, u, ld_u, b0, b1, st);
+    if (rc != 1) return rc;
+  }
   SubArgs a{};
   fill_args(ops, ws, k, a);
   a.b0 = b0;
