@@ -1123,7 +1123,9 @@ class TimeStepper:
             # cut of the captured step; otherwise its own fresh result may serve
             # as the row (no copy) -- storage g reuses (u, u_x, an out= buffer)
             # is overwritten by later stages and is copied
-            G = self._g(ti, ui, out=QG[i] if not terms and self._seg is not None else None)
+            g = self.problem.g
+            cut = self._seg is not None and g is not None and not is_pure(g)   # g runs at a graph cut
+            G = self._g(ti, ui, out=QG[i] if not terms and cut else None)
             if G is not None:
                 terms.append((1.0, G))
             if len(terms) == 1 and terms[0][0] == 1.0 and G is not None:

@@ -25,11 +25,13 @@ from paper_2306_02526_b200.sharding import ShardedTimeStepper  # noqa: E402
 
 
 def graph_time(fn, reps=20):
-    fn()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    from paper_2306_02526_b200.solver import graph_workspace
+    with graph_workspace("probe"):      # the graph's workspace, allocated by the warm call
         fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
     g.replay()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
