@@ -259,6 +259,23 @@ int hps_plan_partition(const hps_plan* plan, int k, int* nparts, int* lstar, int
  * Measurement only (bench.py's per-kernel algorithmic bytes). */
 int hps_plan_fused_level(const hps_plan* plan);
 
+/* Row-sharded top levels of a subtree-sharded solve (the
+ * levels < lstar, which every rank would otherwise run whole).  Between the
+ * UP phase (+ the level-lstar flux all-gather) and the DOWN phase, each rank
+ * runs, for level = lstar-1 .. 0, hps_top_level(level, down = 0): its share
+ * rank/nranks of the level's up operator tiles for every node, writing w3 and
+ * flux rows into the workspace's level blocks (zeroed first, so a sum over
+ * the ranks completes them -- hps_workspace_level gives their byte offsets),
+ * then for level = 0 .. lstar-1 hps_top_level(level, down = 1): its share of
+ * the S tiles, u3 = S u_bnd + w3 rows into `stage` (k x c x n3, zeroed
+ * first), to be summed over the ranks and scattered to u[j3] of the level.
+ * u must hold the Dirichlet data (hps_put_boundary) and every interface value
+ * of the levels above.  Replaces HPS_PHASE_TOP (solver.py:243-268 for the top
+ * levels) with 1/nranks of its operator traffic per rank. */
+int hps_workspace_level(const hps_plan* plan, int k, int level, long long* w3_off, long long* h_off);
+int hps_top_level(const hps_ops* ops, int level, int down, int rank, int nranks, int k, double* u, long long ld_u,
+                  double* stage, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------
  * Stage right-hand-side assembly (timestep.py:237-266 and the leaf-local
  * evaluations of operators.py:276-346).

@@ -83,6 +83,8 @@ SIGNATURES = {
     "hps_ops_destroy": (None, [ctypes.c_void_p]),
     "hps_ktimer_enable": (None, [_i]),
     "hps_plan_fused_level": (_i, [_vp]),
+    "hps_workspace_level": (_i, [_vp, _i, _i, c_ll_p, c_ll_p]),
+    "hps_top_level": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _ll, _vp, _vp, ctypes.c_size_t, _vp]),
     "hps_ktimer_collect": (_i, [ctypes.c_char_p, _i, c_double_p, c_ll_p, _i]),
     "hps_merge_node": (_i, [_i, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _ll, _vp, _vp, _vp, _vp, _vp]),
     "hps_ops_device_bytes": (ctypes.c_size_t, [ctypes.c_void_p]),

@@ -888,6 +888,24 @@ int hps_plan_partition(const hps_plan* h, int k, int* nparts, int* lstar, int* n
 
 int hps_plan_fused_level(const hps_plan* h) { return h ? h->P.dF : -1; }
 
+int hps_workspace_level(const hps_plan* h, int k, int level, long long* w3_off, long long* h_off) {
+  if (!h || k <= 0 || level < 0 || level >= h->P.depth) {
+    set_error("hps_workspace_level: bad arguments");
+    return HPS_ERR_ARG;
+  }
+  long long w = -1, f = -1;
+  level_offsets(h->P, k, level, w, f);
+  if (w3_off) *w3_off = w;
+  if (h_off) *h_off = f;
+  return HPS_OK;
+}
+
+int hps_top_level(const hps_ops* h, int level, int down, int rank, int nranks, int k, double* u, long long ld_u,
+                  double* stage, void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !u || !ws) { set_error("hps_top_level: null argument"); return HPS_ERR_ARG; }
+  return top_level(h->O, level, down != 0, rank, nranks, k, u, ld_u, stage, ws, ws_bytes, (cudaStream_t)stream);
+}
+
 int hps_solve_phase(const hps_ops* h, int phases, int part0, int part1, int k, const double* fb, long long ld_f,
                     const double* g, long long ld_g, const double* jump, long long ld_jump, double inv_dt,
                     double* u, long long ld_u, void* ws, size_t ws_bytes, void* stream) {

@@ -179,6 +179,11 @@ struct GemvArgs {
   // shared layout: the one-node panel is applied to `shared` nodes (virtual
   // tiles = node x tile); 0 = per-node panels
   int shared;
+  // row-sharded launches (top levels over several GPUs): the panel passed is a
+  // view starting at tile t0 of the level's panel; prow0 = t0 * TR is its
+  // first row in the level's row space.  DOWN with yout set: u3 goes to
+  // yout[kg * yout_k + node * n3 + r] (a staging vector) instead of u[j3].
+  long long prow0;
 };
 int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st);
 // nodes [n0, n1) of a level: per-part panels are launched part by part (the
@@ -270,6 +275,9 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
           double* guard = nullptr, const double* root_pre = nullptr, const StageTerms* terms = nullptr);
 // byte offset of level lstar's flux block (k x nparts x n12) in a workspace
 size_t exchange_offset(const Plan& P, int k);
+void level_offsets(const Plan& P, int k, int d, long long& w3, long long& h);
+int top_level(const Ops& ops, int d, bool down, int rank, int nranks, int k, double* u, long long ld_u,
+              double* stage, void* wsp, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace hpsb
 

@@ -124,7 +124,9 @@ __device__ __forceinline__ void epilogue(const GemvArgs& a, int node, int r, int
   } else if (MODE == GEMV_DOWN) {
     double v = y;
     if (a.W3) v = v + a.W3[kg * a.W3_k + (long long)node * a.n3 + r];
-    a.u[kg * a.u_k + a.j3[(long long)node * a.n3 + r]] = v;
+    const long long nr = (long long)node * a.n3 + r;
+    if (a.yout) a.yout[kg * a.yout_k + nr] = v;   // staging output (row-sharded top levels)
+    else a.u[kg * a.u_k + a.j3[nr]] = v;
   } else {
     double v = y;
     if (a.yadd) v = v + a.yadd[kg * a.yadd_k + (long long)node * a.yadd_s + r];
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
   const int kg0 = blockIdx.y * KM;
   const int R = pn.R, TR = pn.TR;
   const long long P = (long long)pn.c * R;
-  const long long p0 = (long long)tile * TR;
+  const long long p0 = (long long)tile * TR + a.prow0;
   const int n0 = (int)(p0 / R);
   const int nn = (int)((std::min(P, p0 + TR) - 1) / R) - n0 + 1;
   const int c0 = split * sp.CK, cw = min(sp.CK, pn.C - c0);
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(NT) k_panel(GemvArgs a, Panel pn, PanelSplit s
 
   if (sp.nsplit > 1) {
     const long long Pp = (long long)pn.ntiles * TR * (a.shared ? a.shared : 1);
-    const long long pv = pa + (long long)vnode * pn.ntiles * TR;  // row in the (virtual) row space
+    const long long pv = pa - a.prow0 + (long long)vnode * pn.ntiles * TR;  // row in the (virtual) row space of the view
     const size_t cidx = ((size_t)vnode * pn.ntiles + tile) * gridDim.y + blockIdx.y;
     double* part = a.part + ((long long)blockIdx.y * KM * sp.nsplit) * Pp;
 #pragma unroll
@@ -359,7 +361,7 @@ int gemv_level(const GemvArgs& a, const Panel& pn, cudaStream_t st) {
   }
   // (the column chain of one thread, C/G, must stay short: long-K levels
   // -- the down sweep's S -- keep the split-K panel kernel)
-  if (a.shared >= kVnMinNodes && pn.c == 1 && pn.TR <= 2 * kVnThreads && vn_enabled() &&
+  if (a.prow0 == 0 && a.shared >= kVnMinNodes && pn.c == 1 && pn.TR <= 2 * kVnThreads && vn_enabled() &&
       cdiv(pn.C, kVnThreads / (pn.TR / 2)) <= kVnMaxCols) {
     int XS;
     if (vn_smem(pn, XS) <= kVnMaxSmem) {

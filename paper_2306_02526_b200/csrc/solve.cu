@@ -170,6 +170,70 @@ static int level_down(const Ops& ops, const Workspace& ws, int d, int n0, int n1
   return gemv_nodes(a, ops.lo[d].S, n0, n1, st);
 }
 
+// byte offsets of level d's w3 and flux blocks in a k-rhs workspace (-1: none)
+void level_offsets(const Plan& P, int k, int d, long long& w3, long long& h) {
+  Workspace ws;
+  carve_workspace(P, k, nullptr, ws);
+  w3 = (long long)(uintptr_t)ws.W3[d];
+  h = d >= 1 ? (long long)(uintptr_t)ws.H[d] : -1;
+}
+
+// One top level (d < lstar) of a subtree-sharded solve, row-sharded over
+// nranks GPUs: this rank applies its contiguous share of the level's operator
+// tiles (up: [X33^-1; Tstack X33^-1], down: S) for every node of the level.
+// Up: w3 / flux rows into the workspace's level-d blocks, zeroed first, so a
+// sum over the ranks completes them; down: u3 rows into `stage` (k x c x n3,
+// zeroed first), summed over the ranks and scattered to u[j3] by the caller.
+int top_level(const Ops& ops, int d, bool down, int rank, int nranks, int k, double* u, long long ld_u,
+              double* stage, void* wsp, size_t ws_bytes, cudaStream_t st) {
+  const Plan& P = *ops.plan;
+  if (d < 0 || d >= P.lstar || rank < 0 || rank >= nranks || k <= 0) {
+    set_error("top_level: level %d (lstar %d), rank %d of %d", d, P.lstar, rank, nranks);
+    return -1;
+  }
+  if (ws_bytes < workspace_bytes(P, k)) {
+    set_error("top_level: workspace too small");
+    return -1;
+  }
+  Workspace ws;
+  carve_workspace(P, k, wsp, ws);
+  const Level& lv = P.lv[d];
+  const LevelOps& lo = ops.lo[d];
+  const Panel& full = down ? lo.S : lo.Up;
+  if (!full.base || full.parts != 1 || full.TS != full.TR || (ops.shared_levels && full.c != 1)) {
+    set_error("top_level: level %d has no streaming panel", d);
+    return -1;
+  }
+  const int T = full.ntiles, t0 = (int)((long long)T * rank / nranks), t1 = (int)((long long)T * (rank + 1) / nranks);
+  Panel view = full;
+  view.base = full.base + (size_t)t0 * full.C * full.TS;
+  view.ntiles = t1 - t0;
+  GemvArgs a{};
+  a.k = k; a.part = ws.part; a.cnt = ws.cnt;
+  a.prow0 = (long long)t0 * full.TR;
+  a.shared = ops.shared_levels ? lv.c : 0;
+  a.n3 = lv.n3; a.n12 = lv.n12;
+  a.W3 = ws.W3[d]; a.W3_k = (long long)lv.c * lv.n3;
+  if (!down) {
+    HPSB_CUDA(cudaMemsetAsync(ws.W3[d], 0, (size_t)k * lv.c * lv.n3 * 8, st));
+    if (d > 0) HPSB_CUDA(cudaMemsetAsync(ws.H[d], 0, (size_t)k * lv.c * lv.n12 * 8, st));
+    a.mode = GEMV_UP;
+    a.Hc = ws.H[d + 1]; a.nbc = lv.nbc;
+    a.Hc_k = (long long)P.lv[d + 1].c * P.lv[d + 1].n12; a.Hc_s = lv.nbc;
+    a.i1a = lv.i1a; a.i3a = lv.i3a; a.i2b = lv.i2b; a.i3b = lv.i3b; a.n1a = lv.n1a;
+    a.j3 = lv.j3;
+    a.Hout = d > 0 ? ws.H[d] : nullptr; a.Hout_k = (long long)lv.c * lv.n12;
+  } else {
+    if (!stage) { set_error("top_level: down pass needs a staging vector"); return -1; }
+    HPSB_CUDA(cudaMemsetAsync(stage, 0, (size_t)k * lv.c * lv.n3 * 8, st));
+    a.mode = GEMV_DOWN;
+    a.u = u; a.u_k = ld_u; a.gidx = lv.gidx_bnd; a.j3 = lv.j3;
+    a.yout = stage; a.yout_k = (long long)lv.c * lv.n3;  // u3 to the staging vector
+  }
+  if (view.ntiles <= 0) return 0;
+  return gemv_level(a, view, st);
+}
+
 size_t exchange_offset(const Plan& P, int k) {
   Workspace ws;
   carve_workspace(P, k, nullptr, ws);

@@ -22,6 +22,8 @@ Everything that talks to torch.distributed works on any backend (NCCL on the
 GPUs; gloo for the CPU tests, staging CUDA tensors through the host).
 """
 
+import os
+
 import numpy as np
 
 from .errors import UnsupportedConfigurationError
@@ -212,6 +214,27 @@ def complete_edges(vecs, top_ids, group=None):
     return vecs
 
 
+def allreduce_sum(tensors, group=None):
+    """Sum each tensor over the ranks in place (one collective on a flat
+    buffer; gloo stages through the host)."""
+    import torch
+    dist = _dist()
+    if dist is None or dist.get_world_size(group) == 1 or not tensors:
+        return tensors
+    flat = torch.cat([t.reshape(-1) for t in tensors])
+    staged = _staged(flat, group)
+    work = flat.cpu() if staged else flat
+    dist.all_reduce(work, op=dist.ReduceOp.SUM, group=group)
+    if staged:
+        flat.copy_(work)
+    o = 0
+    for t in tensors:
+        n = t.numel()
+        t.copy_(flat[o:o + n].view(t.shape))
+        o += n
+    return tensors
+
+
 def gather_owned(u, owned_ids, group=None):
     """Full (k, N) vector on every rank from each rank's owned DOFs (the owned
     sets partition [0, N); a sum with zeros elsewhere is exact)."""
@@ -358,11 +381,54 @@ class ShardedTimeStepper(TimeStepper):
         if self._world > 1:
             block = ops.plan.flux_block(out.shape[0])
             self._eager(lambda: exchange_fluxes(block, p0, p1, self._group))
-        ops.solve_phase(_lib.HPS_PHASE_TOP | _lib.HPS_PHASE_DOWN, p0, p1, fb, body, out)
+        if self._top_rows(ops):
+            self._top_row_sharded(ops, fb, out)
+            ops.solve_phase(_lib.HPS_PHASE_DOWN, p0, p1, fb, body, out)
+        else:
+            ops.solve_phase(_lib.HPS_PHASE_TOP | _lib.HPS_PHASE_DOWN, p0, p1, fb, body, out)
         if tm is not None:
             e1.record()
             tm.append((e0, e1))
         return out
+
+    # -- row-sharded top levels -------------------------------------------
+    def _top_rows(self, ops):
+        """Whether the levels above lstar run row-sharded over the ranks
+        (HPSB_TOP_ROWS=1/0 forces it): each rank then streams 1/world of their
+        operators at the price of 2 lstar - 1 small all-reduces per solve.
+        That pays for per-node operators (C4: the replicated top levels
+        stream ~0.4 ms of operators per solve at 8 ranks); the shared layout's
+        top levels are latency-bound and run replicated."""
+        e = os.environ.get("HPSB_TOP_ROWS")
+        if e is not None:
+            return e == "1" and ops.plan.lstar > 0
+        return ops.plan.lstar > 0 and ops.layout == "per_node" and self._world > 1
+
+    def _top_row_sharded(self, ops, fb, out):
+        """Levels lstar-1 .. 0 up, then 0 .. lstar-1 down, each rank applying
+        its share of every level's operator rows; one all-reduce (sum) per
+        level completes the level's w3 / fluxes (up) or interface values
+        (down) on every rank."""
+        import torch
+        k, plan, world, rank = out.shape[0], ops.plan, self._world, self._rank
+        lms = self.tree.level_maps
+        self._put_boundary(fb, out)                        # the Dirichlet data (what TOP wrote)
+        for d in reversed(range(plan.lstar)):
+            ops.top_level(d, False, rank, world, out)
+            if world > 1:
+                blocks = [b for b in plan.level_blocks(k, d) if b is not None]
+                self._eager(lambda blocks=blocks: allreduce_sum(blocks, self._group))
+        for d in range(plan.lstar):
+            lm = lms[d]
+            stage = self._buf(f"top_stage{d}", (k, lm.count * lm.n3))
+            ops.top_level(d, True, rank, world, out, stage)
+            if world > 1:
+                self._eager(lambda stage=stage: allreduce_sum([stage], self._group))
+            idx = self._bufs.get(f"top_j3_{d}")
+            if idx is None:
+                idx = self._bufs[f"top_j3_{d}"] = torch.as_tensor(np.asarray(lm.j3).ravel(), dtype=torch.long,
+                                                                  device=self._dev)
+            out.index_copy_(1, idx, stage)
 
     def gather(self, state):
         """The state with every DOF exact on every rank."""

@@ -115,6 +115,19 @@ class DevicePlan:
             self._ws[key] = ws
         return ws
 
+    def level_blocks(self, k, level):
+        """(k, c * n3) view of level ``level``'s w3 block and (k, c * n12) view
+        of its flux block (None for the root) in the current workspace."""
+        w3, h = ctypes.c_longlong(), ctypes.c_longlong()
+        _lib.check(self._lib.hps_workspace_level(self.handle, k, int(level), ctypes.byref(w3), ctypes.byref(h)),
+                   "hps_workspace_level")
+        lm = self.tree.level_maps[level]
+        ws = self.workspace(k)
+
+        def view(off, n):
+            return ws[off:off + 8 * k * n].view(torch.float64).view(k, n)
+        return view(w3.value, lm.count * lm.n3), (None if h.value < 0 else view(h.value, lm.count * lm.n12))
+
     def flux_block(self, k):
         """(k, nparts, n12) view of the workspace's level-lstar flux block
         (what the UP phase leaves for the TOP phase; all-gathered between
@@ -459,6 +472,19 @@ class HpsOperatorSet:
             ws.data_ptr(), ws.numel(), current_stream_handle())
         _lib.check(rc, "hps_solve_phase")
         return out
+
+    def top_level(self, level, down, rank, nranks, out, stage=None):
+        """This rank's share of one top level (< lstar) of a row-sharded
+        subtree-partitioned solve (hps_top_level): up -> w3 / flux rows into
+        the workspace's level blocks (``plan.level_blocks``), down -> u3 rows
+        into ``stage`` (k, c * n3); the caller sums both over the ranks."""
+        k = out.shape[0]
+        ws = self.plan.workspace(k)
+        rc = self._lib.hps_top_level(self.handle, int(level), 1 if down else 0, int(rank), int(nranks), k,
+                                     out.data_ptr(), out.stride(0), None if stage is None else stage.data_ptr(),
+                                     ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_top_level")
+        return stage
 
     # -- operator views (reference solver.py:339-348) ---------------------------------
     def _leaf_block(self, which, leaf):

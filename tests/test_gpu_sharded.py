@@ -163,3 +163,81 @@ def test_sharded_backward_euler_matches_stepper():
     sh = ShardedTimeStepper(tree, prob, "BE", dt=1e-2, nparts=4)
     s = sh.run(sh.initial_state(), 4)
     assert rel_l2(s.u, r.u) < 1e-12
+
+
+@pytest.mark.parametrize("layout", ["per_node", "shared"])
+@pytest.mark.parametrize("name,nparts", [("heat8x8p16", 8), ("c4var4x4p10", 4), ("heat4x4p12k3", 2)])
+@pytest.mark.parametrize("nranks", [1, 3])
+def test_row_sharded_top_levels_match_reference(golden, name, nparts, layout, nranks):
+    """The top levels (< lstar) row-sharded over `nranks` ranks (hps_top_level),
+    the ranks' shares run one after another on this GPU and summed on the
+    host side -- what the per-level all-reduce does -- then the parts' DOWN
+    phases: the reference solution."""
+    import torch
+    from paper_2306_02526_b200 import _lib
+    z = golden("solve_" + name)
+    tree, ops = _ops(z, name, layout, nparts)
+    plan = ops.plan
+    G = torch.as_tensor(np.atleast_2d(z["g"]), device="cuda").contiguous()
+    k = G.shape[0]
+    fb = ops._boundary_values(z["f"], G.device)
+    out = torch.zeros((k, tree.N), dtype=torch.float64, device="cuda")
+    lpp = tree.L // nparts
+    for g in range(nparts):
+        ops.solve_phase(_lib.HPS_PHASE_UP, g, g + 1, fb, G[:, g * lpp * tree.ni:], out)
+    bid = torch.as_tensor(tree.boundary_ids, device="cuda")
+    out[:, bid] = fb.expand(k, -1) if fb.shape[0] == 1 else fb
+    for d in reversed(range(plan.lstar)):
+        acc = None
+        for r in range(nranks):
+            ops.top_level(d, False, r, nranks, out)
+            blocks = [b.clone() for b in plan.level_blocks(k, d) if b is not None]
+            acc = blocks if acc is None else [a + b for a, b in zip(acc, blocks)]
+        for b, a in zip([b for b in plan.level_blocks(k, d) if b is not None], acc):
+            b.copy_(a)
+    for d in range(plan.lstar):
+        lm = tree.level_maps[d]
+        tot = torch.zeros((k, lm.count * lm.n3), dtype=torch.float64, device="cuda")
+        for r in range(nranks):
+            stage = torch.empty_like(tot)
+            ops.top_level(d, True, r, nranks, out, stage)
+            tot += stage
+        out[:, torch.as_tensor(np.asarray(lm.j3).ravel(), device="cuda")] = tot
+    for g in range(nparts):
+        ops.solve_phase(_lib.HPS_PHASE_DOWN, g, g + 1, fb, G[:, g * lpp * tree.ni:], out)
+    ph = out.cpu().numpy()
+    ph = ph[0] if np.ndim(z["u"]) == 1 else ph
+    assert rel_l2(ph, z["u"]) < TOL
+
+
+@pytest.mark.parametrize("layout", ["per_node", "shared"])
+def test_sharded_stepper_row_sharded_top_single_rank(layout, monkeypatch):
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.sharding import ShardedTimeStepper
+    monkeypatch.setenv("HPSB_TOP_ROWS", "1")
+    tree, prob = _heat(hb, 8, 12)
+    ref = hb.TimeStepper(tree, prob, "ARK4", dt=1e-3, layout=layout)
+    r = ref.run(ref.initial_state(), 5)
+    sh = ShardedTimeStepper(tree, prob, "ARK4", dt=1e-3, nparts=4, layout=layout)
+    s = sh.run(sh.initial_state(), 5)
+    assert rel_l2(s.u, r.u) < 1e-12
+
+
+def _two_rank_rows_worker(rank, world, port, out):
+    os.environ["HPSB_TOP_ROWS"] = "1"
+    _two_rank_worker(rank, world, port, "burgers", out)
+
+
+def test_sharded_stepper_row_sharded_top_two_gloo_ranks():
+    """Row-sharded top levels over two gloo ranks sharing the GPU (per-level
+    host-staged all-reduces between launches; no kernel waits on another rank)."""
+    import torch.multiprocessing as mp
+    import paper_2306_02526_b200 as hb
+    tree, prob = _burgers(hb, 8, 10, _modes())
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=2e-3)
+    ref = st.run(st.initial_state(), 4).u
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_two_rank_rows_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        assert rel_l2(np.array(out[r]), ref) < 1e-12

@@ -83,7 +83,7 @@ def test_gloo_two_ranks_gather_and_max():
 # driven by a partitioned restatement of the oracle solve on 2 gloo ranks
 # ---------------------------------------------------------------------------
 
-def _partition_solve(ops, part, p0, p1, f, G, exchange, gather):
+def _partition_solve(ops, part, p0, p1, f, G, exchange, gather, rows=None):
     """The oracle solve (oracle/hps_oracle.py OHps.solve) split like
     hps_solve_phase: UP over the parts' leaves and levels >= lstar, the flux
     exchange, TOP, DOWN over the parts."""
@@ -129,17 +129,62 @@ def _partition_solve(ops, part, p0, p1, f, G, exchange, gather):
         H[top_nodes[g]] = block[:, g]
     u = np.zeros((k, tree.N))
     u[:, tree.boundary_ids] = fb
-    for d in range(ls - 1, -1, -1):                  # TOP
-        for kk in tree.levels[d]:
-            up(kk)
 
     def down(kk):
         nd = tree.nodes[kk]
         u[:, nd["j3"]] = u[:, nd["bnd"]] @ ops.merges[kk][0].T + W3[kk]
 
-    for d in range(ls):
-        for kk in tree.levels[d]:
-            down(kk)
+    if rows is None:
+        for d in range(ls - 1, -1, -1):              # TOP, every level on every rank
+            for kk in tree.levels[d]:
+                up(kk)
+        for d in range(ls):
+            for kk in tree.levels[d]:
+                down(kk)
+    else:
+        # TOP row-sharded (hps_top_level): rank r keeps its contiguous share of
+        # the level's row space (node-major, R rows per node), zeros elsewhere,
+        # and one sum over the ranks per level completes it
+        rank, world, allreduce = rows
+
+        def share(nrows):
+            m = np.zeros(nrows, dtype=bool)
+            m[nrows * rank // world:nrows * (rank + 1) // world] = True
+            return m
+
+        for d in range(ls - 1, -1, -1):
+            nodes = tree.levels[d]
+            for kk in nodes:
+                up(kk)
+            n3 = W3[nodes[0]].shape[1]
+            nh = H[nodes[0]].shape[1] if d > 0 else 0
+            R = n3 + nh
+            mask = share(len(nodes) * R).reshape(len(nodes), R)
+            blk = np.zeros((k, len(nodes), R))
+            for j, kk in enumerate(nodes):
+                blk[:, j, :n3] = W3[kk]
+                if nh:
+                    base = np.concatenate([h(tree.nodes[kk]["children"][0])[:, tree.nodes[kk]["i1a"]],
+                                           h(tree.nodes[kk]["children"][1])[:, tree.nodes[kk]["i2b"]]], axis=1)
+                    blk[:, j, n3:] = H[kk] - base      # the rank's rows of Tstack X33^-1 r3
+            blk = allreduce(np.where(mask[None], blk, 0.0))
+            for j, kk in enumerate(nodes):
+                W3[kk] = blk[:, j, :n3]
+                if nh:
+                    base = np.concatenate([h(tree.nodes[kk]["children"][0])[:, tree.nodes[kk]["i1a"]],
+                                           h(tree.nodes[kk]["children"][1])[:, tree.nodes[kk]["i2b"]]], axis=1)
+                    H[kk] = base + blk[:, j, n3:]
+        for d in range(ls):
+            nodes = tree.levels[d]
+            n3 = W3[nodes[0]].shape[1]
+            mask = share(len(nodes) * n3).reshape(len(nodes), n3)
+            stage = np.zeros((k, len(nodes), n3))
+            for j, kk in enumerate(nodes):
+                nd = tree.nodes[kk]
+                stage[:, j] = u[:, nd["bnd"]] @ ops.merges[kk][0].T + W3[kk]
+            stage = allreduce(np.where(mask[None], stage, 0.0))
+            for j, kk in enumerate(nodes):
+                u[:, tree.nodes[kk]["j3"]] = stage[:, j]
     for d in range(ls, tree.depth - 1):              # DOWN
         for kk in own_nodes(d):
             down(kk)
@@ -152,8 +197,8 @@ def _subtree_worker(rank, world, port, nparts, out):
     import torch
     import torch.distributed as dist
     from oracle import hps_oracle as O
-    from paper_2306_02526_b200.sharding import (SubtreePartition, complete_edges, exchange_fluxes,
-                                                gather_owned)
+    from paper_2306_02526_b200.sharding import (SubtreePartition, allreduce_sum, complete_edges,
+                                                exchange_fluxes, gather_owned)
     from paper_2306_02526_b200.tree import build_tree
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -177,6 +222,13 @@ def _subtree_worker(rank, world, port, nparts, out):
 
         u = _partition_solve(ops, part, p0, p1, f, G, exchange, gather)
         ref = ops.solve(np.broadcast_to(f, (k, f.size)), G)
+
+        def allreduce(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            allreduce_sum([t])
+            return t.numpy()
+
+        u_rows = _partition_solve(ops, part, p0, p1, f, G, exchange, gather, rows=(rank, world, allreduce))
         # gradient partial sums of the own leaves, completed on the top interfaces
         uu = rng.standard_normal((1, ot.N))
         lid0, nl = part.leaves(p0, p1)
@@ -188,6 +240,7 @@ def _subtree_worker(rank, world, port, nparts, out):
         full_ux = ops.disc.gradient(uu[0])[0]
         check = np.concatenate([part.owned_ids(p0, p1, with_top=False), part.top_ids])
         out[rank] = dict(err=float(np.abs(u - ref).max() / np.abs(ref).max()),
+                         err_rows=float(np.abs(u_rows - ref).max() / np.abs(ref).max()),
                          gerr=float(np.abs(ux.numpy()[0, check] - full_ux[check]).max()),
                          owned=part.owned_ids(p0, p1, with_top=rank == 0).tolist())
     finally:
@@ -204,6 +257,7 @@ def test_gloo_two_ranks_subtree_partitioned_solve(nparts):
     owned = []
     for r in range(world):
         assert out[r]["err"] < 1e-13
+        assert out[r]["err_rows"] < 1e-13      # row-sharded top levels
         assert out[r]["gerr"] < 1e-13
         owned += out[r]["owned"]
     # the ranks' owned DOFs partition the global vector

@@ -81,9 +81,20 @@ def main():
         up = lambda: ops.solve_phase(_lib.HPS_PHASE_UP, 0, 1, fb, body, out)
         top = lambda: ops.solve_phase(_lib.HPS_PHASE_TOP, 0, 1, fb, body, out)
         down = lambda: ops.solve_phase(_lib.HPS_PHASE_DOWN, 0, 1, fb, body, out)
+        ls = ops.plan.lstar
+        stages = [torch.zeros((k, tree.level_maps[d].count * tree.level_maps[d].n3), dtype=torch.float64,
+                              device="cuda") for d in range(ls)]
+
+        def top_rows():   # rank 0's share of the row-sharded top levels (the all-reduces excluded)
+            for d in reversed(range(ls)):
+                ops.top_level(d, False, 0, P, out)
+            for d in range(ls):
+                ops.top_level(d, True, 0, P, out, stages[d])
         r = {"up_ms": graph_time(up), "top_ms": graph_time(top), "down_ms": graph_time(down),
+             "top_rows_ms": graph_time(top_rows), "top_allreduces": 2 * ls - 1,
              "full_solve_partitioned_plan_ms": graph_time(lambda: ops.solve_device(fb, body, out))}
         r["rank_solve_ms"] = r["up_ms"] + r["top_ms"] + r["down_ms"]
+        r["rank_solve_rows_ms"] = r["up_ms"] + r["top_rows_ms"] + r["down_ms"]
         s2 = sh.run(sh.initial_state(), 2)          # numerically meaningless (one part), timing only
         s2 = hb.StepperState(s2.t, s2.u_device)
         e0.record()
@@ -92,6 +103,7 @@ def main():
         torch.cuda.synchronize()
         r["rank_step_ms"] = e0.elapsed_time(e1) / a.steps
         r["speedup_solve"] = res["solve_ms_1gpu"] / r["rank_solve_ms"]
+        r["speedup_solve_rows"] = res["solve_ms_1gpu"] / r["rank_solve_rows_ms"]
         r["speedup_step"] = res["step_ms_1gpu"] / r["rank_step_ms"]
         res[f"P{P}"] = r
         del sh
