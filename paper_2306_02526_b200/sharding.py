@@ -166,6 +166,16 @@ def _dist():
     return dist if dist.is_available() and dist.is_initialized() else None
 
 
+def _force():
+    """HPSB_FORCE_COLLECTIVES=1: issue the collectives even on a one-rank
+    group (tests of the collective / graph-capture paths on one GPU)."""
+    return os.environ.get("HPSB_FORCE_COLLECTIVES") == "1"
+
+
+def _solo(dist, group):
+    return dist is None or (dist.get_world_size(group) == 1 and not _force())
+
+
 def _staged(t, group):
     """gloo collectives run on host tensors: stage CUDA tensors through the CPU."""
     dist = _dist()
@@ -177,7 +187,7 @@ def exchange_fluxes(block, part0, part1, group=None):
     rank's parts [part0, part1) on entry and every part on exit."""
     import torch
     dist = _dist()
-    if dist is None or dist.get_world_size(group) == 1:
+    if _solo(dist, group):
         return block
     world = dist.get_world_size(group)
     k, P, n12 = block.shape
@@ -201,7 +211,7 @@ def complete_edges(vecs, top_ids, group=None):
     sum the single-GPU kernel forms."""
     import torch
     dist = _dist()
-    if dist is None or dist.get_world_size(group) == 1 or top_ids.numel() == 0:
+    if _solo(dist, group) or top_ids.numel() == 0:
         return vecs
     buf = torch.stack([v[:, top_ids] for v in vecs])
     staged = _staged(buf, group)
@@ -219,7 +229,7 @@ def allreduce_sum(tensors, group=None):
     buffer; gloo stages through the host)."""
     import torch
     dist = _dist()
-    if dist is None or dist.get_world_size(group) == 1 or not tensors:
+    if _solo(dist, group) or not tensors:
         return tensors
     flat = torch.cat([t.reshape(-1) for t in tensors])
     staged = _staged(flat, group)
@@ -281,6 +291,7 @@ class ShardedTimeStepper(TimeStepper):
         self._group = group
         self._world = 1 if dist is None else dist.get_world_size(group)
         self._rank = 0 if dist is None else dist.get_rank(group)
+        self._multi = self._world > 1 or _force()      # collectives are issued
         nparts = self._world if nparts is None else int(nparts)
         self._partition = SubtreePartition(tree, nparts)
         self._nparts = nparts
@@ -353,8 +364,8 @@ class ShardedTimeStepper(TimeStepper):
         g = self.problem.g
         if any(gradient_use(g)):
             self._dd.eval(U, ux=ux, uy=uy, leaves=self._leaves)
-            if self._world > 1:
-                self._eager(lambda: complete_edges([ux, uy], self._top_ids, self._group))
+            if self._multi:
+                self._collective(lambda: complete_edges([ux, uy], self._top_ids, self._group))
 
         def fill(tt):
             for a, b in self._ranges():
@@ -378,9 +389,9 @@ class ShardedTimeStepper(TimeStepper):
             e0.record()
         p0, p1 = self._parts
         ops.solve_phase(_lib.HPS_PHASE_UP, p0, p1, fb, body, out)
-        if self._world > 1:
+        if self._multi:
             block = ops.plan.flux_block(out.shape[0])
-            self._eager(lambda: exchange_fluxes(block, p0, p1, self._group))
+            self._collective(lambda: exchange_fluxes(block, p0, p1, self._group))
         if self._top_rows(ops):
             self._top_row_sharded(ops, fb, out)
             ops.solve_phase(_lib.HPS_PHASE_DOWN, p0, p1, fb, body, out)
@@ -390,6 +401,21 @@ class ShardedTimeStepper(TimeStepper):
             e1.record()
             tm.append((e0, e1))
         return out
+
+    # -- collectives inside the captured step ----------------------------------------------
+    def _collective(self, fn):
+        """A collective of the stage solve.  With NCCL it is captured into the
+        step's CUDA graph with the kernels around it (NCCL collectives are
+        graph-capturable; no host round trip per collective at replay);
+        HPSB_GRAPH_COLLECTIVES=0, or a host-staged backend (gloo), cuts the
+        graph there instead and issues it eagerly between the segments."""
+        dist = _dist()
+        captured = (self._seg is not None and dist is not None and dist.get_backend(self._group) == "nccl"
+                    and os.environ.get("HPSB_GRAPH_COLLECTIVES", "1") != "0")
+        if captured:
+            fn()
+        else:
+            self._eager(fn)
 
     # -- row-sharded top levels (SURVEY.md 8(e)) -------------------------------------------
     def _top_rows(self, ops):
@@ -415,15 +441,15 @@ class ShardedTimeStepper(TimeStepper):
         self._put_boundary(fb, out)                        # the Dirichlet data (what TOP wrote)
         for d in reversed(range(plan.lstar)):
             ops.top_level(d, False, rank, world, out)
-            if world > 1:
+            if self._multi:
                 blocks = [b for b in plan.level_blocks(k, d) if b is not None]
-                self._eager(lambda blocks=blocks: allreduce_sum(blocks, self._group))
+                self._collective(lambda blocks=blocks: allreduce_sum(blocks, self._group))
         for d in range(plan.lstar):
             lm = lms[d]
             stage = self._buf(f"top_stage{d}", (k, lm.count * lm.n3))
             ops.top_level(d, True, rank, world, out, stage)
-            if world > 1:
-                self._eager(lambda stage=stage: allreduce_sum([stage], self._group))
+            if self._multi:
+                self._collective(lambda stage=stage: allreduce_sum([stage], self._group))
             idx = self._bufs.get(f"top_j3_{d}")
             if idx is None:
                 idx = self._bufs[f"top_j3_{d}"] = torch.as_tensor(np.asarray(lm.j3).ravel(), dtype=torch.long,

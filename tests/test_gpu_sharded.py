@@ -241,3 +241,48 @@ def test_sharded_stepper_row_sharded_top_two_gloo_ranks():
     mp.spawn(_two_rank_rows_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     for r in range(2):
         assert rel_l2(np.array(out[r]), ref) < 1e-12
+
+
+def _nccl_one_rank_worker(rank, world, port, mode, out):
+    """One NCCL rank on this GPU with the collectives forced (a one-rank group
+    makes them no-op copies, but they are issued and captured like at N > 1)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.sharding import ShardedTimeStepper
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), HPSB_FORCE_COLLECTIVES="1")
+    if mode == "cut":
+        os.environ["HPSB_GRAPH_COLLECTIVES"] = "0"
+    if mode == "rows":
+        os.environ["HPSB_TOP_ROWS"] = "1"
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        tree, prob = _burgers(hb, 8, 10, _modes())
+        sh = ShardedTimeStepper(tree, prob, "ARK4", dt=2e-3, nparts=4)
+        s = sh.run(sh.initial_state(), 4)
+        out["u"] = s.u.tolist()
+        out["graph"] = sh._graph is not None
+        out["segments"] = len(sh._graph["graph"].parts) if sh._graph is not None else -1
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["captured", "cut", "rows"])
+def test_sharded_stepper_nccl_collectives_in_graph(mode):
+    """The stage solve's collectives issued through NCCL: captured into the
+    step's CUDA graph (default; one graph segment per step besides the cuts
+    around g), or cut out of it (HPSB_GRAPH_COLLECTIVES=0); same trajectory
+    as the single-GPU stepper."""
+    import torch.multiprocessing as mp
+    import paper_2306_02526_b200 as hb
+    tree, prob = _burgers(hb, 8, 10, _modes())
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=2e-3)
+    ref = st.run(st.initial_state(), 4).u
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_nccl_one_rank_worker, args=(1, _free_port(), mode, out), nprocs=1, join=True)
+    assert out["graph"]
+    assert rel_l2(np.array(out["u"]), ref) < 1e-12
+    if mode == "cut":
+        assert out["segments"] > 6          # cut at every collective (and around g)
