@@ -231,6 +231,177 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
   }
 }
 
+// The same GEMM with its operands streamed by a GS_STAGES-deep cp.async
+// pipeline (16-byte copies, zero-filled past K) instead of one register-staged
+// k-tile: the top levels of a many-rhs solve (X gathered up front, thousands
+// of operator rows and columns, few (node, rhs) row tiles) are long k-loops
+// whose global latency the two-stage register path leaves exposed.
+constexpr int GS_STAGES = 4;
+
+__device__ __forceinline__ void cp16_zfill(double* dst, const double* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+template <int MODE, int WN>
+__global__ void __launch_bounds__(64 * WN) k_gsp(GsArgs a, int tilesN) {
+  constexpr int BN = 32 * WN, NT = 64 * WN;
+  constexpr int ACH = BM * BK / 2 / NT, BCH = BN * BK / 2 / NT;  // 16-byte chunks per thread and stage
+  extern __shared__ double sm[];
+  __shared__ unsigned s_last;
+  double* As = sm;                           // [GS_STAGES][BM][SROW]
+  double* Bs = sm + GS_STAGES * BM * SROW;   // [GS_STAGES][BN][SROW]
+  const int tile = blockIdx.x / a.nsplit, split = blockIdx.x % a.nsplit;
+  const int tm = tile / tilesN, tn = tile % tilesN;
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const int kb = split * a.KC / BK;
+  const int kend = min(a.K, (split + 1) * a.KC);
+  const int nk = (kend - split * a.KC + BK - 1) / BK;
+  pdl_trigger();
+  auto load_b = [&](int kt, int buf) {  // the operator does not depend on the previous kernel
+#pragma unroll
+    for (int i = 0; i < BCH; ++i) {
+      const int e = tid + NT * i, r = e / (BK / 2), c = 2 * (e % (BK / 2));
+      const int gn = n0 + r, gk = (kb + kt) * BK + c;
+      const bool ok = gn < a.N && gk < kend;
+      cp16_zfill(Bs + (buf * BN + r) * SROW + c, ok ? a.B + (long long)gn * a.ldb + gk : a.B, ok);
+    }
+  };
+  auto load_a = [&](int kt, int buf) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i) {
+      const int e = tid + NT * i, r = e / (BK / 2), c = 2 * (e % (BK / 2));
+      const int gm = m0 + r, gk = (kb + kt) * BK + c;
+      const bool ok = gm < a.M && gk < kend;
+      cp16_zfill(As + (buf * BM + r) * SROW + c, ok ? a.X + (long long)gm * a.K + gk : a.X, ok);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+  // prologue: the operator's first stages before the dependency wait, the inputs after
+#pragma unroll
+  for (int s = 0; s < GS_STAGES - 1; ++s)
+    if (s < nk) load_b(s, s);
+  pdl_wait();
+#pragma unroll
+  for (int s = 0; s < GS_STAGES - 1; ++s) {
+    if (s < nk) load_a(s, s);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt % GS_STAGES;
+    asm volatile("cp.async.wait_group %0;" ::"n"(GS_STAGES - 2) : "memory");
+    __syncthreads();  // stage kt landed for every thread; stage kt - 1 is consumed by all
+    if (kt + GS_STAGES - 1 < nk) {
+      load_b(kt + GS_STAGES - 1, (kt + GS_STAGES - 1) % GS_STAGES);
+      load_a(kt + GS_STAGES - 1, (kt + GS_STAGES - 1) % GS_STAGES);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const double* Ab = As + (buf * BM + wm * 32 + (lane >> 2)) * SROW + (lane & 3);
+    const double* Bb = Bs + (buf * BN + wn * 32 + (lane >> 2)) * SROW + (lane & 3);
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Ab[i * 8 * SROW + kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bb[j * 8 * SROW + kk];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+
+  if (a.nsplit > 1) {  // partial tile to the workspace; the last CTA of the tile sums in split order
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+          if (m < a.M && r < a.N) a.part[((size_t)split * a.M + m) * a.N + r] = acc[i][j][h];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) s_last = atom_add_acq_rel(a.cnt + tile, 1u) == (unsigned)a.nsplit - 1;
+    __syncthreads();
+    if (!s_last) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+          double y = 0.0;
+          if (m < a.M && r < a.N) {
+            const double* pp = a.part + (size_t)m * a.N + r;
+            const size_t ps = (size_t)a.M * a.N;
+            for (int s0 = 0; s0 < a.nsplit; s0 += 4) {
+              double v[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[u] = s0 + u < a.nsplit ? __ldcg(pp + (size_t)(s0 + u) * ps) : 0.0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (s0 + u < a.nsplit) y += v[u];
+            }
+          }
+          acc[i][j][h] = y;
+        }
+    }
+    if (tid == 0) a.cnt[tile] = 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
+    if (m >= a.M) continue;
+    const int node = m % a.nodes, kg = m / a.nodes;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
+        if (r < a.N) gs_out<MODE>(a.g, node, r, kg, acc[i][j][h]);
+      }
+  }
+}
+
+template <int MODE, int WN>
+int launch_gsp(GsArgs a, const GsSplit& sp, cudaStream_t st) {
+  constexpr int BN = 32 * WN;
+  const size_t smem = (size_t)GS_STAGES * (BM + BN) * SROW * 8;
+  static bool attr = false;
+  if (!attr) {
+    HPSB_CUDA(cudaFuncSetAttribute(k_gsp<MODE, WN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  a.nsplit = sp.nsplit;
+  a.KC = sp.KC;
+  const int tilesN = (int)cdiv(a.N, BN);
+  dim3 grid((unsigned)(sp.tiles * sp.nsplit));
+  HPSB_CUDA(launch_pdl(k_gsp<MODE, WN>, grid, dim3(64 * WN), smem, st, a, tilesN));
+  HPSB_LAUNCH_CHECK();
+  return 0;
+}
+
+static bool gs_pipe_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HPSB_NO_GS_PIPE");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 template <int MODE, int WN>
 int launch_gs(GsArgs a, const GsSplit& sp, cudaStream_t st) {
   constexpr int BN = 32 * WN;
@@ -274,6 +445,14 @@ int gs(const GsArgs& a, const Workspace& ws, cudaStream_t st) {
     HPSB_CUDA(launch_pdl(k_gs_gather<MODE>, dim3((unsigned)std::min<long long>(cdiv(n, 256), 148LL * 16)), dim3(256), 0,
                          st, b));
     HPSB_LAUNCH_CHECK();
+  }
+  // pipelined path: gathered inputs and 16-byte aligned rows of X and of the operator
+  // (long k-loops only: with a few k-steps the 2-CTA/SM register path wins)
+  if (b.X && gs_pipe_enabled() && sp.KC >= 8 * BK && a.K % 2 == 0 && a.ldb % 2 == 0 && ((uintptr_t)a.B & 15) == 0 &&
+      ((uintptr_t)b.X & 15) == 0) {
+    if (sp.WN == 1) return launch_gsp<MODE, 1>(b, sp, st);
+    if (sp.WN == 2) return launch_gsp<MODE, 2>(b, sp, st);
+    return launch_gsp<MODE, 4>(b, sp, st);
   }
   if (sp.WN == 1) return launch_gs<MODE, 1>(b, sp, st);
   if (sp.WN == 2) return launch_gs<MODE, 2>(b, sp, st);
@@ -340,6 +519,8 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
   a.N = lv.n3 + (d > 0 ? lv.n12 : 0); a.K = lv.n3;
   g = shift_nodes(g, n0);
   a.B = lo.Ush; a.ldb = lv.ld3; a.g = g;
+  const int rc = deep_level(g, true, a.nodes, k, a.N, a.K, lo.Ush, lv.ld3, st);  // many rhs, deep levels
+  if (rc != 1) return rc;
   return gs<GS_UP>(a, ws, st);
 }
 
@@ -363,6 +544,8 @@ int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool ha
   a.N = lv.n3; a.K = lv.n12;
   g = shift_nodes(g, n0);
   a.B = lo.Ssh; a.ldb = lv.ld12; a.g = g;
+  const int rc = deep_level(g, false, a.nodes, k, a.N, a.K, lo.Ssh, lv.ld12, st);
+  if (rc != 1) return rc;
   return gs<GS_DOWN>(a, ws, st);
 }
 

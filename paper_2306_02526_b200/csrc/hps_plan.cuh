@@ -207,6 +207,10 @@ int shared_level_up(const Ops& ops, const Workspace& ws, int d, int k, const dou
 int shared_level_down(const Ops& ops, const Workspace& ws, int d, int k, bool has_w3, double* u, long long ld_u,
                       int n0, int n1, cudaStream_t st);
 bool shared_gemm(const Plan& P, int d, int nodes, int k);
+// many-rhs deep levels (deep.cu): staged contiguous inputs, DMMA product; 1 = not eligible
+bool deep_enabled();
+int deep_level(const GemvArgs& g, bool up, int nodes, int k, int R, int K, const double* op, int ldo,
+               cudaStream_t st);
 struct GsSplit {
   int WN = 1, tiles = 0, nsplit = 1, KC = 0;
   size_t part_doubles = 0;
