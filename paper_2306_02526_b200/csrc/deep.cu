@@ -124,7 +124,13 @@ __global__ void __launch_bounds__(DT) k_deep(DeepArgs a) {
     }
   } else {
     const int* isrc = g.gidx + (long long)nb0 * g.n12;
-    for (int e = tid; e < nv * g.n12; e += DT) idx[e] = isrc[e];
+    if ((g.n12 & 3) == 0 && (reinterpret_cast<uintptr_t>(isrc) & 15) == 0) {  // one contiguous block
+      for (int e = 4 * tid; e < nv * g.n12; e += 4 * DT)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(idx + e)), "l"(isrc + e) : "memory");
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    } else {
+      for (int e = tid; e < nv * g.n12; e += DT) idx[e] = isrc[e];
+    }
     __syncthreads();
     const double* u = g.u + kg * g.u_k;
     // boundary values in pairs: one 16-byte copy where the two DOFs are
