@@ -1102,7 +1102,7 @@ extern "C" int hps_ops_set_leaf_fd(hps_ops* h, const double* host, int count) {
   if (!host) { O.fd = nullptr; return HPS_OK; }  // disable (the buffer stays owned)
   const int q = P.q;
   if (!O.shared_leaf || !leaf_fd_supported(q) || count != 5 * q * q + 8 * q + 513) {
-    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in {8, 10, 14} and %d values",
+    set_error("hps_ops_set_leaf_fd: needs constant coefficients, q in [4, 14] and %d values",
               5 * q * q + 8 * q + 513);
     return HPS_ERR_ARG;
   }

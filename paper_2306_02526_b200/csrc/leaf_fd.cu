@@ -657,7 +657,8 @@ static int launch_fd_mma(const Plan& P, const FdArgs& a, int nleaf, int k, cudaS
     HPSB_LAUNCH_CHECK();                                                                               \
     return 0;                                                                                          \
   }
-  HPSB_FD2(8) HPSB_FD2(10) HPSB_FD2(14)
+  HPSB_FD2(4) HPSB_FD2(5) HPSB_FD2(6) HPSB_FD2(7) HPSB_FD2(8) HPSB_FD2(9) HPSB_FD2(10) HPSB_FD2(11) HPSB_FD2(12)
+  HPSB_FD2(13) HPSB_FD2(14)
 #undef HPSB_FD2
   set_error("leaf_fd: no kernel for q = %d", P.q);
   return -1;
@@ -720,12 +721,14 @@ int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, d
   if (!getenv("HPSB_FD_SIMT")) return launch_fd_mma<FD_UP_WH>(P, a, nleaf, k, st);  // tensor-core variant
 #define HPSB_FD(QQ) \
   if (P.q == QQ) { HPSB_CUDA(launch_pdl(k_leaf_fd<QQ>, grid, dim3(NT), 0, st, a)); HPSB_LAUNCH_CHECK(); return 0; }
-  HPSB_FD(8) HPSB_FD(10) HPSB_FD(14)
+  HPSB_FD(4) HPSB_FD(5) HPSB_FD(6) HPSB_FD(7) HPSB_FD(8) HPSB_FD(9) HPSB_FD(10) HPSB_FD(11) HPSB_FD(12) HPSB_FD(13)
+  HPSB_FD(14)
 #undef HPSB_FD
   set_error("leaf_fd: no kernel for q = %d", P.q);
   return -1;
 }
 
-bool leaf_fd_supported(int q) { return q == 8 || q == 10 || q == 14; }
+// every leaf order p = q + 2 from 6 to 16 (the leaf grid fits one 16 x 16 DMMA tile)
+bool leaf_fd_supported(int q) { return q >= 4 && q <= 14; }
 
 }  // namespace hpsb

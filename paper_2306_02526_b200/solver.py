@@ -675,7 +675,7 @@ def tensor_leaf_factors(disc, sigma, dt_gamma, cond_max=1e6):
     not a Kronecker sum with a real, well-conditioned eigenbasis."""
     cf, st, tree = disc.coeffs, disc.stencil, disc.tree
     q = tree.q
-    if not cf.is_constant or q not in (8, 10, 14):
+    if not cf.is_constant or not 4 <= q <= 14:
         return None
     v = lambda f: 0.0 if f is None else float(f)
     c11, c22, c1, c2, c0 = v(cf.c11), v(cf.c22), v(cf.c1), v(cf.c2), v(cf.c)

@@ -292,3 +292,35 @@ def test_timing_harness_rows(tmp_path):
         assert r["N"] == (r["n_side"] * 10 + 1) ** 2
         assert r["build_seconds"] > 0 and r["per_step_solve_seconds"] > 0
     assert path.read_text().splitlines()[0] == ",".join(COLUMNS)
+
+
+@pytest.mark.parametrize("p", list(range(6, 17)))
+def test_tensor_leaf_solve_every_order(p):
+    """The tensor-product (Kronecker-sum) leaf kernels take every leaf order
+    p = 6..16 (q = p - 2 interior points): plain solves and one fused ARK4
+    step agree with the CPU oracle to the north-star tolerance."""
+    import paper_2306_02526_b200 as hb
+    from oracle import hps_oracle as O
+    unit = ((0.0, 1.0), (0.0, 1.0))
+    rng = np.random.default_rng(p)
+    tree = hb.build_tree(unit, 4, 4, p)
+    ops = hb.build(tree, hb.OperatorCoefficients(c11=1.0, c22=0.5, c1=0.3), sigma=1.0, dt_gamma=2e-3)
+    assert ops.leaf_solve == "tensor", p
+    f = rng.standard_normal(tree.boundary_ids.size)
+    g = rng.standard_normal(tree.N)
+    ot = O.OTree(unit, 4, 4, p)
+    ref = O.OHps(O.ODisc(ot, O.OCoeffs(c11=1.0, c22=0.5, c1=0.3)), 1.0, 2e-3).solve_with_body_load(f, g)
+    assert rel_l2(ops.solve_with_body_load(f, g), ref) < TOL, p
+    two_pi = 2 * np.pi
+    phi = lambda pts: np.sin(two_pi * pts[:, 0]) * np.sin(two_pi * pts[:, 1])
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0),
+                               q=hb.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t)),
+                               f=hb.SeparableField.product(phi, np.cos), u0=phi)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=1e-3)
+    assert st.ops.leaf_solve == "tensor", p
+    s = st.run(st.initial_state(), 2)
+    ost = O.OStepper(ot, O.OCoeffs(c11=1.0, c22=1.0), O.ark4_tableau(), 1e-3,
+                     q=lambda t, pts: phi(pts) * (-np.sin(t) + 8 * np.pi ** 2 * np.cos(t)),
+                     f=lambda t, pts: phi(pts) * np.cos(t))
+    _, uref = ost.run(0.0, phi(ot.points), 2)
+    assert rel_l2(s.u, uref) < TOL, p
