@@ -57,23 +57,59 @@ __device__ __forceinline__ double gs_x(const GemvArgs& a, int node, int kg, int 
   }
 }
 
+// The epilogue in two halves, so that it issues every load of a row group
+// (pass-through flux entries / w3, target indices) before its first store --
+// the stores may alias the loaded arrays as far as the compiler knows, so a
+// fused load-store per output serialises the loads
 template <int MODE>
-__device__ __forceinline__ void gs_out(const GemvArgs& a, int node, int r, int kg, double y) {
+__device__ __forceinline__ void gs_pre(const GemvArgs& a, int node, int r, int kg, double& base, int& t) {
   if (MODE == GS_UP) {
-    if (r < a.n3) {
-      a.W3[kg * a.W3_k + (long long)node * a.n3 + r] = y;
-    } else {
+    base = 0.0;
+    t = 0;
+    if (r >= a.n3) {
       r -= a.n3;
       const double* Ha = a.Hc + kg * a.Hc_k + (long long)(2 * node) * a.Hc_s;
-      const double* Hb = Ha + a.Hc_s;
-      const double base = (r < a.n1a) ? Ha[a.i1a[r]] : Hb[a.i2b[r - a.n1a]];
-      a.Hout[kg * a.Hout_k + (long long)node * a.n12 + r] = base + y;
+      base = (r < a.n1a) ? Ha[a.i1a[r]] : Ha[a.Hc_s + a.i2b[r - a.n1a]];
     }
   } else {
-    double v = y;
-    if (a.W3) v = v + a.W3[kg * a.W3_k + (long long)node * a.n3 + r];
-    a.u[kg * a.u_k + a.j3[(long long)node * a.n3 + r]] = v;
+    base = a.W3 ? a.W3[kg * a.W3_k + (long long)node * a.n3 + r] : 0.0;
+    t = a.j3[(long long)node * a.n3 + r];
   }
+}
+
+template <int MODE>
+__device__ __forceinline__ void gs_put(const GemvArgs& a, int node, int r, int kg, double v, int t) {
+  if (MODE == GS_UP) {
+    if (r < a.n3) a.W3[kg * a.W3_k + (long long)node * a.n3 + r] = v;
+    else a.Hout[kg * a.Hout_k + (long long)node * a.n12 + r - a.n3] = v;
+  } else {
+    a.u[kg * a.u_k + t] = v;
+  }
+}
+
+// epilogue of one 8-row group of a warp tile: loads first, then the stores
+template <int MODE>
+__device__ __forceinline__ void gs_epilogue_row(const GsArgs& a, int m, int rbase, const double (&acc)[4][2]) {
+  if (m >= a.M) return;
+  const int node = m % a.nodes, kg = m / a.nodes;
+  double base[4][2];
+  int t[4][2];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = rbase + j * 8 + h;
+      base[j][h] = 0.0;
+      t[j][h] = 0;
+      if (r < a.N) gs_pre<MODE>(a.g, node, r, kg, base[j][h], t[j][h]);
+    }
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = rbase + j * 8 + h;
+      if (r < a.N) gs_put<MODE>(a.g, node, r, kg, acc[j][h] + base[j][h], t[j][h]);
+    }
 }
 
 // The (node, rhs) x K input matrix of a level GEMM gathered once: every
@@ -217,18 +253,8 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
   }
 
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
-    if (m >= a.M) continue;
-    const int node = m % a.nodes, kg = m / a.nodes;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
-        if (r < a.N) gs_out<MODE>(a.g, node, r, kg, acc[i][j][h]);
-      }
-  }
+  for (int i = 0; i < 4; ++i)
+    gs_epilogue_row<MODE>(a, m0 + wm * 32 + i * 8 + (lane >> 2), n0 + wn * 32 + 2 * (lane & 3), acc[i]);
 }
 
 // The same GEMM with its operands streamed by a GS_STAGES-deep cp.async
@@ -362,18 +388,8 @@ __global__ void __launch_bounds__(64 * WN) k_gsp(GsArgs a, int tilesN) {
     if (tid == 0) a.cnt[tile] = 0u;
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
-    if (m >= a.M) continue;
-    const int node = m % a.nodes, kg = m / a.nodes;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = n0 + wn * 32 + j * 8 + 2 * (lane & 3) + h;
-        if (r < a.N) gs_out<MODE>(a.g, node, r, kg, acc[i][j][h]);
-      }
-  }
+  for (int i = 0; i < 4; ++i)
+    gs_epilogue_row<MODE>(a, m0 + wm * 32 + i * 8 + (lane >> 2), n0 + wn * 32 + 2 * (lane & 3), acc[i]);
 }
 
 template <int MODE, int WN>
