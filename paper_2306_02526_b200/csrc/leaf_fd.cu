@@ -396,64 +396,68 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     store(bufB, SB);
     __syncwarp();
     if (UPH) {
-      // fluxes of w = Vx T2 Vy^T without forming w (4 small DMMA products):
-      //   east / west rows:  h_ew = (A_ew T2) Vy^T,  A_ew = [e_east; e_west] Vx (2 of 8 rows)
-      //   north / south:     h_ns = Vx (T2 B_ns),    B_ns = Vy^T [e_n0 e_n1] (2 of 8 columns)
-      store(bufA, SA);  // T2 again, as an A operand
+      // fluxes of w = Vx T2 Vy^T without forming w, as line sums (as DMMA
+      // products they would pad 2 useful rows / columns to 8):
+      //   east / west:   pe_r = a_r^T T2 (a_r = Vx^T e_r),  h_r[y] = sum_s pe_r[s] Vy[y][s]
+      //   north / south: qn_n = T2 b_n   (b_n = Vy^T e_n),  h_n[x] = sum_s Vx[x][s] qn_n[s]
+      // lanes 0..q-1 take the east / west rows (column y of T2, conflict-free
+      // in bufB), lanes 16..16+q-1 the north / south ones (row x of T2 read
+      // as column x of its transpose, stored to bufA from the accumulators)
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) bufA[(nj * 8 + 2 * gc + h) * SA + mi * 8 + gr] = acc[mi][nj][h];
       __syncwarp();
-      double pe[2][2], qn[2][2];
+      const int li = lane & 15;
+      const bool ew = lane < 16;
+      double p0 = 0.0, p1 = 0.0;
+      if (li < Q) {
+        if (ew) {
 #pragma unroll
-      for (int i = 0; i < 2; ++i) { pe[i][0] = pe[i][1] = 0.0; qn[i][0] = qn[i][1] = 0.0; }
+          for (int x = 0; x < Q; ++x) {
+            const double t = bufB[x * SB + li];
+            p0 = fma(cAew[x], t, p0);
+            p1 = fma(cAew[CSA + x], t, p1);
+          }
+        } else {
 #pragma unroll
-      for (int k = 0; k < KS; ++k) {
-        const double am = cAew[gr * CSA + k * 4 + gc];
-        const double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
-        dmma(pe[0][0], pe[0][1], am, b0);
-        dmma(pe[1][0], pe[1][1], am, b1);
-        const double bq = cBns[(k * 4 + gc) * 8 + gr];
-        const double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
-        dmma(qn[0][0], qn[0][1], a0, bq);
-        dmma(qn[1][0], qn[1][1], a1, bq);
+          for (int y = 0; y < Q; ++y) {
+            const double t = bufA[y * SA + li];
+            p0 = fma(cBns[y * 8], t, p0);
+            p1 = fma(cBns[y * 8 + 1], t, p1);
+          }
+        }
       }
       __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        *reinterpret_cast<double2*>(bufA + gr * SA + i * 8 + 2 * gc) = make_double2(pe[i][0], pe[i][1]);
-        *reinterpret_cast<double2*>(bufB + (i * 8 + gr) * 8 + 2 * gc) = make_double2(qn[i][0], qn[i][1]);
+      double* pq = bufA + 16 * SA;  // the warp's ub scratch (4q + 8): pe_0, pe_1, qn_0, qn_1 (q each)
+      if (li < Q) {
+        pq[(ew ? 0 : 2 * Q) + li] = p0;
+        pq[(ew ? Q : 3 * Q) + li] = p1;
       }
       __syncwarp();
-#pragma unroll
-      for (int i = 0; i < 2; ++i) { pe[i][0] = pe[i][1] = 0.0; qn[i][0] = qn[i][1] = 0.0; }
-#pragma unroll
-      for (int k = 0; k < KS; ++k) {
-        const double am = bufA[gr * SA + k * 4 + gc];
-        const double b0 = cVyt[(k * 4 + gc) * CSB + gr], b1 = cVyt[(k * 4 + gc) * CSB + 8 + gr];
-        dmma(pe[0][0], pe[0][1], am, b0);
-        dmma(pe[1][0], pe[1][1], am, b1);
-        const double bq = bufB[(k * 4 + gc) * 8 + gr];
-        const double a0 = cVx[gr * CSA + k * 4 + gc], a1 = cVx[(8 + gr) * CSA + k * 4 + gc];
-        dmma(qn[0][0], qn[0][1], a0, bq);
-        dmma(qn[1][0], qn[1][1], a1, bq);
-      }
-      // boundary order of the D_bi rows: east y (0..q), north / south interleaved by x, west y
       double* out = a.H + kk * a.ld_h + (long long)l * NB;
-      if (gr < 2) {
+      if (li < Q) {
+        double h0 = 0.0, h1 = 0.0;
+        if (ew) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int yi = i * 8 + 2 * gc + h;
-            if (yi < Q) out[(gr == 0 ? 0 : 3 * Q) + yi] = pe[i][h];
+          for (int s2 = 0; s2 < Q; ++s2) {
+            const double v = cVyt[s2 * CSB + li];
+            h0 = fma(pq[s2], v, h0);
+            h1 = fma(pq[Q + s2], v, h1);
           }
-      }
-      if (gc == 0) {
+          out[li] = h0;
+          out[3 * Q + li] = h1;
+        } else {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int xi = i * 8 + gr;
-          if (xi < Q) {
-            out[Q + 2 * xi] = qn[i][0];
-            out[Q + 2 * xi + 1] = qn[i][1];
+          for (int s2 = 0; s2 < Q; ++s2) {
+            const double v = cVx[li * CSA + s2];
+            h0 = fma(v, pq[2 * Q + s2], h0);
+            h1 = fma(v, pq[3 * Q + s2], h1);
           }
+          out[Q + 2 * li] = h0;
+          out[Q + 2 * li + 1] = h1;
         }
       }
       __syncwarp();
