@@ -201,6 +201,15 @@ int hps_solve_stage_terms(const hps_ops* ops, const double* fb, int nterms, cons
                           double* guard, const double* root_pre, void* ws, size_t ws_bytes,
                           void* stream);
 
+/* hps_solve_stage_terms for k rhs rows (an ensemble stage, timestep.py:255-257
+ * over the stacked members): term t has row stride vec_ld[t] (0 = one row
+ * shared by every rhs), r_out / u / lu_int rows of stride ld_r / ld_u / ld_lu,
+ * fb rows of stride ld_f; no root_pre. */
+int hps_solve_stage_terms_k(const hps_ops* ops, int k, const double* fb, long long ld_f, int nterms,
+                            const double* dcoefs, const double* const* vecs, const long long* vec_ld,
+                            double* r_out, long long ld_r, double* u, long long ld_u, double* lu_int,
+                            long long ld_lu, double* guard, void* ws, size_t ws_bytes, void* stream);
+
 /* The root's Dirichlet product S_root u_bnd (solver.py:262-265 at the root,
  * whose boundary is the domain boundary) for ns <= 8 rows of boundary data
  * fb (nbd values each, row stride ld_f) in one pass over the root operator:

@@ -109,6 +109,8 @@ SIGNATURES = {
                              _vp]),
     "hps_solve_stage_terms": (_i, [_vp, _vp, _i, _vp, ctypes.POINTER(_vp), _vp, _vp, _vp, _vp, _vp, _vp,
                                    ctypes.c_size_t, _vp]),
+    "hps_solve_stage_terms_k": (_i, [_vp, _i, _vp, _ll, _i, _vp, ctypes.POINTER(_vp), ctypes.POINTER(_ll), _vp, _ll,
+                                     _vp, _ll, _vp, _ll, _vp, _vp, ctypes.c_size_t, _vp]),
     "hps_root_dirichlet_scratch": (ctypes.c_size_t, [_vp, _i]),
     "hps_root_dirichlet": (_i, [_vp, _i, _vp, _ll, _vp, _ll, _vp, ctypes.c_size_t, _vp]),
     "hps_leaf_lu": (_i, [_vp, _i, _i, _i, _vp, _ll, _vp, _ll, _vp, _vp]),

@@ -840,8 +840,30 @@ int hps_solve_stage_terms(const hps_ops* h, const double* fb, int nterms, const 
   T.nterm = nterms; T.tdc = dcoefs; T.rout = r_out;
   for (int t = 0; t < nterms; ++t) T.tv[t] = vecs[t];
   const long long N = h->O.plan->N;
+  T.ld_rout = N;
   return solve(O, SOLVE_ALL, 0, O.plan->nparts, 1, fb, 0, r_out, 0, nullptr, 0, 0.0, u, N, ws, ws_bytes,
                (cudaStream_t)stream, lu_int, N, guard, root_pre, &T);
+}
+
+int hps_solve_stage_terms_k(const hps_ops* h, int k, const double* fb, long long ld_f, int nterms,
+                            const double* dcoefs, const double* const* vecs, const long long* vec_ld, double* r_out,
+                            long long ld_r, double* u, long long ld_u, double* lu_int, long long ld_lu, double* guard,
+                            void* ws, size_t ws_bytes, void* stream) {
+  if (!h || !fb || !u || !ws || !r_out || !dcoefs || !vecs || !vec_ld || k <= 0) {
+    set_error("hps_solve_stage_terms_k: null argument or k <= 0");
+    return HPS_ERR_ARG;
+  }
+  const Ops& O = h->O;
+  if (!(O.shared_leaf && O.fd && leaf_fd_down_enabled())) {
+    set_error("hps_solve_stage_terms_k: needs the tensor-product leaf solve (constant coefficients)");
+    return HPS_ERR_ARG;
+  }
+  if (nterms < 1 || nterms > 12) { set_error("hps_solve_stage_terms_k: %d terms (1..12)", nterms); return HPS_ERR_ARG; }
+  StageTerms T;
+  T.nterm = nterms; T.tdc = dcoefs; T.rout = r_out; T.ld_rout = ld_r;
+  for (int t = 0; t < nterms; ++t) { T.tv[t] = vecs[t]; T.tld[t] = vec_ld[t]; }
+  return solve(O, SOLVE_ALL, 0, O.plan->nparts, k, fb, ld_f, r_out, ld_r, nullptr, 0, 0.0, u, ld_u, ws, ws_bytes,
+               (cudaStream_t)stream, lu_int, ld_lu, guard, nullptr, &T);
 }
 
 size_t hps_root_dirichlet_scratch(const hps_ops* h, int ns) { return h ? root_dirichlet_scratch(*h->O.plan, ns) : 0; }

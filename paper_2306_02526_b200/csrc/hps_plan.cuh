@@ -239,16 +239,19 @@ int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld
 int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u, long long ld_u, const double* uint,
                double* lu, long long ld_lu, double* guard, cudaStream_t st);
 
-// the up sweep's leaf kernel forming the body load sum_t tdc[t] tv[t] (one rhs,
-// leaf interiors) itself and writing it to rout for the downward sweep
-int leaf_fd_up_terms(const Ops& ops, int nleaf, int nterm, const double* const* tv, const double* tdc, double* rout,
-                     double* H, long long ld_h, cudaStream_t st, int nbd, const int* bids, const double* fb,
-                     double* u);
+// the up sweep's leaf kernel forming the body load sum_t tdc[t] tv[t] (leaf
+// interiors; k rhs rows, term t's row stride tld[t], 0 = one row for every rhs)
+// itself and writing it to rout (row stride ld_rout) for the downward sweep
+int leaf_fd_up_terms(const Ops& ops, int k, int nleaf, int nterm, const double* const* tv, const long long* tld,
+                     const double* tdc, double* rout, long long ld_rout, double* H, long long ld_h, cudaStream_t st,
+                     int nbd, const int* bids, const double* fb, long long ld_f, double* u, long long ld_u);
 struct StageTerms {
   int nterm = 0;
   const double* tv[12] = {};
+  long long tld[12] = {};   // rhs row strides (0: one row shared by every rhs)
   const double* tdc = nullptr;
   double* rout = nullptr;
+  long long ld_rout = 0;
 };
 
 // persistent dataflow kernel for the wide levels (mega.cu): up

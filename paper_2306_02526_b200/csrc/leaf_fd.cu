@@ -38,7 +38,8 @@ struct FdArgs {
   double* lu; long long ld_lu;       // FD_DOWN, optional: L u at the interiors (the stage history)
   unsigned long long* guard;         // ... and max |u| over the leaves' grids (bits, NaN sticky)
   int nterm; const double* tv[kFdTerms]; const double* tdc;  // FD_UP_T: body load = sum_t tdc[t] tv[t] ...
-  double* rout;                                              // ... written here (leaf l interior at l*ni)
+  long long tld[kFdTerms];                                   // (rhs row strides of the terms, 0 = shared row)
+  double* rout; long long ld_rout;                           // ... written here (leaf l interior at l*ni)
   // FD_UP_H, optional: the solve's Dirichlet data u[ids[i]] = fb[i] (solver.py:259-260), written by the
   // CTAs after the dependency wait (the up sweep never reads u) -- one launch fewer per solve
   int nbd; const int* bids; const double* fb; long long ld_f; double* ubnd; long long ld_ubnd;
@@ -260,7 +261,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       // next term's loads in flight while one is summed
       double va[NR], vb[NR];
       auto ldt = [&](double (&v)[NR], int t) {
-        const double* src = a.tv[t] + (long long)leaf * NI;
+        const double* src = a.tv[t] + kk * a.tld[t] + (long long)leaf * NI;
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
           const int e = lane + 32 * i;
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         for (int i = 0; i < NR; ++i) nxt[i] = fma(c1, vb[i], nxt[i]);
       }
       if (leaf < a.L) {
-        double* ro = a.rout + (long long)leaf * NI;
+        double* ro = a.rout + kk * a.ld_rout + (long long)leaf * NI;
 #pragma unroll
         for (int i = 0; i < NR; ++i) {
           const int e = lane + 32 * i;
@@ -700,17 +701,17 @@ int leaf_fd_lu(const Ops& ops, int k, int nleaf, const int* lbg, const double* u
   return launch_fd_mma<FD_LU>(*ops.plan, a, nleaf, k, st);
 }
 
-int leaf_fd_up_terms(const Ops& ops, int nleaf, int nterm, const double* const* tv, const double* tdc, double* rout,
-                     double* H, long long ld_h, cudaStream_t st, int nbd, const int* bids, const double* fb,
-                     double* u) {
+int leaf_fd_up_terms(const Ops& ops, int k, int nleaf, int nterm, const double* const* tv, const long long* tld,
+                     const double* tdc, double* rout, long long ld_rout, double* H, long long ld_h, cudaStream_t st,
+                     int nbd, const int* bids, const double* fb, long long ld_f, double* u, long long ld_u) {
   if (nleaf <= 0) return 0;
   if (nterm <= 0 || nterm > kFdTerms) { set_error("leaf_fd_up_terms: %d terms (1..%d)", nterm, kFdTerms); return -1; }
   FdArgs a{};
-  a.L = nleaf; a.k = 1; a.H = H; a.ld_h = ld_h; a.mats = ops.fd;
-  a.nterm = nterm; a.tdc = tdc; a.rout = rout;
-  for (int t = 0; t < nterm; ++t) a.tv[t] = tv[t];
-  a.nbd = nbd; a.bids = bids; a.fb = fb; a.ld_f = 0; a.ubnd = u; a.ld_ubnd = 0;
-  return launch_fd_mma<FD_UP_T>(*ops.plan, a, nleaf, 1, st);
+  a.L = nleaf; a.k = k; a.H = H; a.ld_h = ld_h; a.mats = ops.fd;
+  a.nterm = nterm; a.tdc = tdc; a.rout = rout; a.ld_rout = ld_rout;
+  for (int t = 0; t < nterm; ++t) { a.tv[t] = tv[t]; a.tld[t] = tld ? tld[t] : 0; }
+  a.nbd = nbd; a.bids = bids; a.fb = fb; a.ld_f = ld_f; a.ubnd = u; a.ld_ubnd = ld_u;
+  return launch_fd_mma<FD_UP_T>(*ops.plan, a, nleaf, k, st);
 }
 
 int leaf_fd(const Ops& ops, int k, int nleaf, const double* g, long long ld_g, double* WH, long long ld_wh,

@@ -297,13 +297,14 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   bool bnd_done = false;  // Dirichlet data already written by the leaf kernel
   if (phases & SOLVE_UP) {
     // (2) leaf particular solutions and their fluxes (solver.py:219-230)
-    if (terms && fd_down && k == 1) {
+    if (terms && fd_down) {
       // the stage combination formed by the leaf kernel (no combination pass), written out for the
       // downward sweep; the Dirichlet data too
       const bool bnd = (phases & SOLVE_TOP) && P.nbd > 0;
-      if (int rc = leaf_fd_up_terms(ops, nleaf, terms->nterm, terms->tv, terms->tdc,
-                                    terms->rout + (long long)leaf0 * P.ni, ws.Hleaf + (long long)leaf0 * P.nb, Lnb,
-                                    st, bnd ? P.nbd : 0, P.boundary_ids, fb, u))
+      if (int rc = leaf_fd_up_terms(ops, k, nleaf, terms->nterm, terms->tv, terms->tld, terms->tdc,
+                                    terms->rout + (long long)leaf0 * P.ni, terms->ld_rout,
+                                    ws.Hleaf + (long long)leaf0 * P.nb, Lnb, st, bnd ? P.nbd : 0, P.boundary_ids,
+                                    fb, ld_f, u, ld_u))
         return rc;
       bnd_done = bnd;
     } else if (g && fd_down) {
@@ -396,7 +397,7 @@ int solve(const Ops& ops, int phases, int part0, int part1, int k, const double*
   }
   if (int rc = downs(std::max(dA, dm), dB)) return rc;
 
-  if (terms && fd_down && k == 1) { g = terms->rout; ld_g = 0; }  // the formed body load
+  if (terms && fd_down) { g = terms->rout; ld_g = terms->ld_rout; }  // the formed body load
   if (phases & SOLVE_DOWN) {
     if (fused) {
       int b0, b1;

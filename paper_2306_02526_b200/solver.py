@@ -419,6 +419,21 @@ class HpsOperatorSet:
         _lib.check(rc, "hps_solve_stage_terms")
         return out
 
+    def solve_stage_terms_k_device(self, fb, dcoef_ptr, vecs, rout, out, lu, guard):
+        """solve_stage_terms_device for k rhs rows (hps_solve_stage_terms_k):
+        vecs are (rows, N) views with rows 1 (shared by every rhs) or k."""
+        k = out.shape[0]
+        ws = self.plan.workspace(k)
+        vp = (ctypes.c_void_p * len(vecs))(*[v.data_ptr() for v in vecs])
+        lds = (ctypes.c_longlong * len(vecs))(*[0 if v.shape[0] == 1 else v.stride(0) for v in vecs])
+        rc = self._lib.hps_solve_stage_terms_k(
+            self.handle, k, fb.data_ptr(), fb.stride(0) if fb.shape[0] > 1 else 0, len(vecs), dcoef_ptr, vp, lds,
+            rout.data_ptr(), rout.stride(0), out.data_ptr(), out.stride(0),
+            None if lu is None else lu.data_ptr(), 0 if lu is None else lu.stride(0),
+            None if guard is None else guard.data_ptr(), ws.data_ptr(), ws.numel(), current_stream_handle())
+        _lib.check(rc, "hps_solve_stage_terms_k")
+        return out
+
     @property
     def root_dirichlet_ok(self):
         """Whether the root's Dirichlet product can be batched over a step's

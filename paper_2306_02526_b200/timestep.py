@@ -980,17 +980,21 @@ class TimeStepper:
         return v if a == 0 else v[:, a:]
 
     def _fused_stage_terms(self, fb, terms, r, out, lu, guard, root_pre):
-        """hps_solve_stage_terms when the stage's combination fits it (one rhs,
-        at most 12 single-row terms, the whole tree); False otherwise."""
-        if not (self._k == 1 and 0 < len(terms) <= 12 and self.ops.fuses_stage_history and
+        """hps_solve_stage_terms(_k) when the stage's combination fits it (at
+        most 12 terms of one row or k rows, the whole tree); False otherwise."""
+        k = self._k
+        if not (0 < len(terms) <= 12 and self.ops.fuses_stage_history and
                 self.solve_timer is None and self._ir[0] == 0 and
                 os.environ.get("HPSB_NO_STAGE_TERMS") != "1"):
             return False
-        if any(v.shape[0] != 1 for _, v in terms):
+        if any(v.shape[0] not in (1, k) for _, v in terms) or (k > 1 and root_pre is not None):
             return False
         dptr = self._coef_ptr([c for c, _ in terms])
         if not self._dry:
-            self.ops.solve_stage_terms_device(fb, dptr, [v for _, v in terms], r, out, lu, guard, root_pre)
+            if k == 1:
+                self.ops.solve_stage_terms_device(fb, dptr, [v for _, v in terms], r, out, lu, guard, root_pre)
+            else:
+                self.ops.solve_stage_terms_k_device(fb, dptr, [v for _, v in terms], r, out, lu, guard)
         return True
 
     def _coef_ptr(self, vals):

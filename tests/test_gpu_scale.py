@@ -31,7 +31,7 @@ def _record_stages(st, stages):
     """Hook the operator set's stage-solve entry points: every stage solve's
     output is appended to ``stages`` (eager stepping only)."""
     ops = st.ops
-    names = ("solve_device", "solve_stage_device", "solve_stage_terms_device")
+    names = ("solve_device", "solve_stage_device", "solve_stage_terms_device", "solve_stage_terms_k_device")
     orig = {n: getattr(ops, n) for n in names}
 
     def wrap(name, out_pos):
@@ -43,6 +43,7 @@ def _record_stages(st, stages):
     ops.solve_device = wrap("solve_device", 2)
     ops.solve_stage_device = wrap("solve_stage_device", 2)
     ops.solve_stage_terms_device = wrap("solve_stage_terms_device", 4)
+    ops.solve_stage_terms_k_device = wrap("solve_stage_terms_k_device", 4)
 
     def restore():
         for n in names:

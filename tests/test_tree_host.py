@@ -136,9 +136,10 @@ def test_tensor_leaf_factors_only_for_constant_coefficients():
     tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 10)
     disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=lambda x, y: 1 + x, c22=1.0))
     assert tensor_leaf_factors(disc, 1.0, 0.1) is None
-    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, 9)            # q = 7: no kernel
-    disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0))
-    assert tensor_leaf_factors(disc, 1.0, 0.1) is None
+    for p, ok in ((5, False), (6, True), (9, True), (16, True), (17, False)):  # kernels for q = p - 2 in [4, 14]
+        tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 2, 2, p)
+        disc = hb.EllipticDiscretization(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0))
+        assert (tensor_leaf_factors(disc, 1.0, 0.1) is not None) == ok, p
 
 
 def test_step_map_analysis_matches_reference(golden):
