@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(64 * WN) k_gs(GsArgs a, int tilesN) {
 // k-tile: the top levels of a many-rhs solve (X gathered up front, thousands
 // of operator rows and columns, few (node, rhs) row tiles) are long k-loops
 // whose global latency the two-stage register path leaves exposed.
-constexpr int GS_STAGES = 4;
+constexpr int GS_STAGES = 3;
 
 __device__ __forceinline__ void cp16_zfill(double* dst, const double* src, bool ok) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
