@@ -495,7 +495,8 @@ GsSplit gs_split(long long M, int N, int K) {
     s.part_doubles = (size_t)s.nsplit * M * N;
     s.counters = s.tiles;
   }
-  if (cdiv(N, 32 * s.WN) >= 4) s.gather_doubles = (size_t)M * K;  // many N-tiles re-read the inputs
+  // many N-tiles re-read the inputs, or a long k-loop (the pipelined GEMM streams gathered inputs)
+  if (cdiv(N, 32 * s.WN) >= 4 || K >= 256) s.gather_doubles = (size_t)M * K;
   return s;
 }
 
