@@ -22,8 +22,10 @@
 //   (DMMA m8n8k4), the operator fragments from L1 / L2 (every CTA reads the
 //   same operator) one k-step ahead: wide operators (the up pass, R = n3 +
 //   n12) as 32-column chunks per warp over all m-tiles (each operator
-//   fragment serves BMN / 8 tiles), short ones (the down pass, R = n3) as
-//   m-tiles spread over the warps;
+//   fragment serves BMN / 8 tiles), short ones (the down pass, R = n3, K =
+//   n12 long) split-K over the warps with all BMN / 8 x R / 8 tiles per warp
+//   (independent accumulator chains), the warps' partials summed in warp
+//   order through shared memory;
 // * outputs: w3 and flux rows are contiguous per node (16-byte stores of the
 //   accumulator pairs), u3 goes to u[j3] (+ w3).
 // Summation order per output is fixed (k-steps in order): bitwise
@@ -91,7 +93,7 @@ __device__ __forceinline__ void deep_out(const DeepArgs& a, const double* blk, i
   }
 }
 
-template <int MODE, int BMN, bool WIDE>
+template <int MODE, int BMN, int NT8>  // NT8 = 0: wide operators; else the n-tiles of a short one
 __global__ void __launch_bounds__(DT) k_deep(DeepArgs a) {
   constexpr int MT = BMN / 8;   // m-tiles of 8 nodes
   extern __shared__ __align__(16) double dsm[];
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(DT) k_deep(DeepArgs a) {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   }
   __syncthreads();
-  if (WIDE) {
+  if (NT8 == 0) {
     // wide operators (R > 64): warp w takes operator rows [32 (w + DW it), +32) for all MT
     // m-tiles (4 x MT tiles per fragment pair: each operator fragment serves MT tiles)
     const int ksteps = (a.K + 3) / 4;
@@ -202,64 +204,93 @@ __global__ void __launch_bounds__(DT) k_deep(DeepArgs a) {
     }
     return;
   }
-  // Y (BMN x R) = X Op^T in 8 x 8 DMMA tiles: warp w takes m-tile w % MT and
-  // the 32-column chunks ch = w / MT, w / MT + DW / MT, ... of the operator
-  // rows (n-tiles past R skipped: the short down operators, R = n3, keep
-  // every warp busy)
+  // short operators (the down pass, R = n3 <= 8 NT8): split-K over the warps
+  // -- warp w takes k-steps [w K4 / DW, (w + 1) K4 / DW) for all MT x NT8
+  // tiles (MT NT8 independent accumulator chains, each operator fragment
+  // serving MT tiles); the warps' partial tiles meet in shared memory (the
+  // staged inputs' space) and are summed in warp order
+  constexpr int NTA = NT8 > 0 ? NT8 : 1;  // (NT8 = 0 returned above)
   const int ksteps = (a.K + 3) / 4;
-  const int mi = warp % MT;
-  const int n = mi * 8 + gr;  // this lane's output node (row of Y)
-  for (int r0 = (warp / MT) * 32; r0 < a.R; r0 += 32 * (DW / MT)) {
-    const int ntv = min(4, (a.R - r0 + 7) / 8);  // valid n-tiles of the chunk
-    double acc[4][2];
+  const int ks0 = warp * ksteps / DW, ks1 = (warp + 1) * ksteps / DW;
+  double acc[MT][NTA][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { acc[j][0] = 0.0; acc[j][1] = 0.0; }
-    const double* orow[4];
-    bool rok[4];
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int r = r0 + j * 8 + gr;
-      rok[j] = r < a.R;
-      orow[j] = a.op + (long long)(rok[j] ? r : 0) * a.ldo;
+    for (int j = 0; j < NT8; ++j) { acc[i][j][0] = 0.0; acc[i][j][1] = 0.0; }
+  const double* orow[NTA];
+  bool rok[NTA];
+#pragma unroll
+  for (int j = 0; j < NT8; ++j) {
+    const int r = j * 8 + gr;
+    rok[j] = r < a.R;
+    orow[j] = a.op + (long long)(rok[j] ? r : 0) * a.ldo;
+  }
+  double bn[NTA];
+  {
+    const int k = ks0 * 4 + gc;
+#pragma unroll
+    for (int j = 0; j < NT8; ++j) bn[j] = (ks0 < ks1 && rok[j] && k < a.K) ? __ldg(orow[j] + k) : 0.0;
+  }
+  for (int ks = ks0; ks < ks1; ++ks) {
+    const int k = ks * 4 + gc;
+    double bf[NTA];
+#pragma unroll
+    for (int j = 0; j < NT8; ++j) bf[j] = bn[j];
+    if (ks + 1 < ks1) {  // next k-step's operator fragments in flight
+#pragma unroll
+      for (int j = 0; j < NT8; ++j) bn[j] = (rok[j] && k + 4 < a.K) ? __ldg(orow[j] + k + 4) : 0.0;
     }
-    double bn[4];
+    double af[MT];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bn[j] = (j < ntv && rok[j] && gc < a.K) ? __ldg(orow[j] + gc) : 0.0;
-    const double* xr = X + n * a.xs;
-    for (int ks = 0; ks < ksteps; ++ks) {
-      const int k = ks * 4 + gc;
-      double bf[4];
+    for (int i = 0; i < MT; ++i) af[i] = k < a.K ? X[(i * 8 + gr) * a.xs + k] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bn[j];
-      if (ks + 1 < ksteps) {  // next k-step's operator fragments in flight
+    for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bn[j] = (j < ntv && rok[j] && k + 4 < a.K) ? __ldg(orow[j] + k + 4) : 0.0;
-      }
-      const double af = k < a.K ? xr[k] : 0.0;
+      for (int j = 0; j < NT8; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+  __syncthreads();  // every warp is done with X: it takes the partial tiles [DW][BMN][R]
+  double* red = X;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < ntv) dmma(acc[j][0], acc[j][1], af, bf[j]);
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT8; ++j) {
+      const int r = j * 8 + 2 * gc;
+      if (r < a.R)
+        *reinterpret_cast<double2*>(red + ((long long)warp * BMN + i * 8 + gr) * a.R + r) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
     }
+  __syncthreads();
+  const int hr = a.R / 2;
+  for (int o = tid; o < BMN * hr; o += DT) {
+    const int n = o / hr, r = 2 * (o - n * hr);
+    double y0 = 0.0, y1 = 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < ntv) deep_out<MODE>(a, blk, nb0, nv, kg, n, r0 + j * 8 + 2 * gc, acc[j][0], acc[j][1]);
+    for (int w = 0; w < DW; ++w) {
+      const double2 v = *reinterpret_cast<const double2*>(red + ((long long)w * BMN + n) * a.R + r);
+      y0 += v.x;
+      y1 += v.y;
+    }
+    deep_out<MODE>(a, blk, nb0, nv, kg, n, r, y0, y1);
   }
 }
 
-template <int MODE, int BMN, bool WIDE>
+template <int MODE, int BMN, int NT8>
 int launch_deep1(const DeepArgs& a, size_t smem, cudaStream_t st) {
-  HPSB_CUDA(cudaFuncSetAttribute(k_deep<MODE, BMN, WIDE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  HPSB_CUDA(cudaFuncSetAttribute(k_deep<MODE, BMN, NT8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)cdiv(a.nodes, BMN), (unsigned)a.k);
-  HPSB_CUDA(launch_pdl(k_deep<MODE, BMN, WIDE>, grid, dim3(DT), smem, st, a));
+  HPSB_CUDA(launch_pdl(k_deep<MODE, BMN, NT8>, grid, dim3(DT), smem, st, a));
   HPSB_LAUNCH_CHECK();
   return 0;
 }
 
 template <int MODE, int BMN>
 int launch_deep(const DeepArgs& a, size_t smem, cudaStream_t st) {
-  // wide operators (the up pass: R = n3 + n12) reuse each operator fragment over all m-tiles;
-  // short ones (the down pass: R = n3) spread the m-tiles over the warps
-  return a.R > 64 ? launch_deep1<MODE, BMN, true>(a, smem, st) : launch_deep1<MODE, BMN, false>(a, smem, st);
+  // wide operators (the up pass: R = n3 + n12) as column chunks over the warps; short ones (the
+  // down pass: R = n3) split-K over the warps with all tiles per warp
+  if (a.R > 64) return launch_deep1<MODE, BMN, 0>(a, smem, st);
+  if (a.R <= 16) return launch_deep1<MODE, BMN, 2>(a, smem, st);
+  if (a.R <= 32) return launch_deep1<MODE, BMN, 4>(a, smem, st);
+  return launch_deep1<MODE, BMN, 8>(a, smem, st);
 }
 
 }  // namespace
@@ -282,6 +313,7 @@ int deep_level(const GemvArgs& g, bool up, int nodes, int k, int R, int K, const
   a.nodes = nodes; a.k = k; a.R = R; a.K = K; a.op = op; a.ldo = ldo; a.g = g;
   a.xs = K + 2 - (K & 1);  // even (16-byte rows), offset from multiples of 32 doubles
   if (a.xs % 32 == 0) a.xs += 2;
+  if (R <= 64) a.xs = std::max(a.xs, DW * R);  // the split-K partials reuse the staged inputs' space
   if (up) {
     if ((g.Hc_s & 1) || (g.Hc_k & 1) || (reinterpret_cast<uintptr_t>(g.Hc) & 15) || !g.Hout) return 1;
     for (int bmn : {32, 16}) {
