@@ -111,3 +111,30 @@ def test_c5_recipe_parity(monkeypatch):
     cfg = bench.CONFIGS["C5"]
     assert cfg["k"] == 64
     _run_config(cfg, 16, 2, monkeypatch, check_stages=True)
+
+
+def test_c5_recipe_deep_levels_parity(monkeypatch):
+    """C5's recipe at 64x64 leaves: the ensemble's deep levels (>= 512 nodes)
+    take the staged gather-apply-scatter kernel (deep.cu) and its top levels
+    the pipelined GEMM -- every stage solve of a step and the step against the
+    oracle."""
+    cfg = dict(bench.CONFIGS["C5"], k=16)
+    _run_config(cfg, 64, 1, monkeypatch, check_stages=True)
+
+
+def test_many_rhs_solve_matches_single_rhs_solves():
+    """A 32-rhs solve on 64x64 leaves (deep levels by k_deep, top levels by the
+    level GEMMs) equals the loop of one-rhs solves (fused subtree kernels and
+    the dataflow kernel) to 1e-12."""
+    import torch
+    import paper_2306_02526_b200 as hb
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 64, 64, 8)
+    ops = hb.build(tree, hb.OperatorCoefficients(c11=1.0, c22=1.0), sigma=1.0, dt_gamma=1e-3)
+    rng = np.random.default_rng(5)
+    k = 32
+    fb = torch.as_tensor(rng.standard_normal((k, tree.boundary_ids.size)), device="cuda")
+    body = torch.as_tensor(rng.standard_normal((k, tree.N)), device="cuda")
+    U = ops.solve_device(fb, body, torch.empty((k, tree.N), dtype=torch.float64, device="cuda"))
+    for i in range(0, k, 7):
+        u = ops.solve_device(fb[i:i + 1], body[i:i + 1], torch.empty((1, tree.N), dtype=torch.float64, device="cuda"))
+        assert rel_l2(U[i].cpu().numpy(), u[0].cpu().numpy()) < 1e-12, i
