@@ -96,15 +96,21 @@ def make_problem(mod, cfg):
     """ParabolicProblem of the config for the package ``mod`` (ours or the
     oracle-facing description); returns (problem kwargs)."""
     kind = cfg["kind"]
+    plain = cfg.get("plain", False)   # --plain-fields: the reference caller's numpy callables, undeclared g
     if kind == "heat":
-        q = mod.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
-        f = mod.SeparableField.product(phi, np.cos)
+        if plain:
+            q = lambda t, pts: phi(pts) * (-np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
+            f = lambda t, pts: phi(pts) * np.cos(t)
+        else:
+            q = mod.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
+            f = mod.SeparableField.product(phi, np.cos)
         return dict(coeffs=mod.OperatorCoefficients(c11=1.0, c22=1.0), q=q, f=f,
                     u0=lambda pts: phi(pts))
     if kind == "allen_cahn":
         coef = sine_modes(0)
+        g = lambda t, u, ux, uy: u - u ** 3
         return dict(coeffs=mod.OperatorCoefficients(c11=0.01, c22=0.01),
-                    g=mod.declare_nonlinear(lambda t, u, ux, uy: u - u ** 3, ux=False, uy=False, pure=True),
+                    g=g if plain else mod.declare_nonlinear(g, ux=False, uy=False, pure=True),
                     u0=lambda pts: sine_field(coef, pts),
                     time_independent_bc=True)
     if kind == "burgers_var":
@@ -189,7 +195,8 @@ def config_block(cfg):
     N = q * (p * L + 2 * n)
     ops = sum(n3 * n3 + 2 * n3 * n12 for _, n3, n12 in level_shapes(n, p)) * 8
     return {"workload": f"{cfg['name']}: {n}x{n} leaves, p={p}, {cfg['kind']}, ARK4 dt={cfg['dt']}, "
-                        f"k={cfg['k']}, one ARK4 step per bench step (5 stage solves)",
+                        f"k={cfg['k']}, one ARK4 step per bench step (5 stage solves)"
+                        + (", plain numpy field callables / undeclared g" if cfg.get("plain") else ""),
             "N_dof": N,
             "l2": ("inputs larger than L2, no flush (level operators streamed per stage solve %.2f GB "
                    "> 126 MB L2; state %.1f MB)" % (ops / 1e9, 8e-6 * N * cfg["k"])) if ops > 126e6 else
@@ -472,13 +479,16 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plain-fields", action="store_true",
+                    help="q / f as plain numpy callables and g undeclared (the reference caller's code, "
+                         "evaluated at cuts of the captured step)")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--layout", default=None, choices=[None, "auto", "per_node", "shared"],
                     help="operator storage (default: shared for constant coefficients)")
     ap.add_argument("--shard", default="auto", choices=["auto", "subtree", "replicas"],
                     help="N > 1 GPUs: subtree-shard one problem (auto) or run replicas")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config], plain=args.plain_fields)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":

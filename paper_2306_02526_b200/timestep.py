@@ -449,6 +449,35 @@ class _Field:
         a = a.reshape(self.k, self.n) if (a.ndim > 1 or self.k == 1) else a.reshape(1, self.n)
         return torch.as_tensor(np.ascontiguousarray(a), device=self.dev)
 
+    _pool = None       # host threads for chunked evaluations (shared)
+    _pointwise = None  # per field: whether fn(t, pts) evaluates point by point (checked on first use)
+
+    def host_eval(self, t):
+        """fn(t, pts) on the host.  A field callable is a function of the
+        points; when it is evaluated point by point (checked once: the chunked
+        evaluation equals the whole-array call bitwise) large point sets are
+        evaluated in chunks on all host cores (numpy releases the GIL), else
+        as one call, as the reference does."""
+        fn, pts = self.fn, self.pts
+        if self._pointwise is False or self.n < (1 << 16) or os.environ.get("HPSB_NO_FIELD_THREADS") == "1":
+            return np.asarray(fn(t, pts), dtype=float)
+        if _Field._pool is None:
+            from concurrent.futures import ThreadPoolExecutor
+            _Field._pool = ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1)))
+        nw = _Field._pool._max_workers
+        cuts = [self.n * i // nw for i in range(nw + 1)]
+        parts = list(_Field._pool.map(lambda i: np.asarray(fn(t, pts[cuts[i]:cuts[i + 1]]), dtype=float),
+                                      range(nw)))
+        if any(p.shape[-1:] != (cuts[i + 1] - cuts[i],) for i, p in enumerate(parts)):
+            self._pointwise = False
+            return np.asarray(fn(t, pts), dtype=float)
+        chunked = np.concatenate(parts, axis=-1)
+        if self._pointwise is None:
+            full = np.asarray(fn(t, pts), dtype=float)
+            self._pointwise = full.shape == chunked.shape and np.array_equal(full, chunked)
+            return full
+        return chunked
+
     stepper = None     # the TimeStepper whose step may be captured (host evaluations become cuts)
 
     def _host_value(self, t):
@@ -460,7 +489,7 @@ class _Field:
             return st._dummy((1, self.n))
         if st is not None and st._seg is not None:
             return st._cut_field(self, t)
-        return self._stack(self.fn(t, self.pts))
+        return self._stack(self.host_eval(t))
 
     def terms(self, t, scale=1.0):
         """(coef, tensor) terms of scale*F(t); evaluates non-separable F now."""
@@ -636,7 +665,7 @@ class TimeStepper:
         a = np.asarray(F.fn(t, F.pts), dtype=float)      # shape only (host)
         rows = F.k if (a.ndim > 1 or F.k == 1) else 1
         tgt = self._cut_buf((rows, F.n))
-        self._eager(lambda tc=t: tgt.copy_(F._stack(F.fn(self._replay_t + tc, F.pts))))
+        self._eager(lambda tc=t: tgt.copy_(F._stack(F.host_eval(self._replay_t + tc))))
         return tgt
 
     def _dummy(self, shape):

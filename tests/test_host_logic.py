@@ -1,6 +1,7 @@
 """Host-side stepping logic that needs no GPU."""
 import sys
 
+import numpy as np
 import pytest
 import torch
 
@@ -51,3 +52,20 @@ def test_fresh_result_detection():
     for name, (g, want) in cases.items():
         r, refs = _refs_after_call(g, 0.0, U, ux, ux)
         assert _is_fresh(r, refs) == want, name
+
+
+def test_field_host_eval_chunks_only_pointwise_callables():
+    """Plain (numpy) field callables on large point sets are evaluated in
+    chunks on all host cores only if that is bitwise the whole-array call
+    (checked on first use); otherwise always as one call (the reference's)."""
+    from paper_2306_02526_b200.timestep import _Field
+    pts = np.random.default_rng(0).random((200_000, 2))
+    fn = lambda t, p: np.sin(2 * np.pi * p[:, 0]) * np.cos(t) + p[:, 1] ** 2
+    F = _Field(fn, pts, 1, "cpu")
+    a = F.host_eval(0.3)
+    assert F._pointwise is True and np.array_equal(a, fn(0.3, pts))
+    assert np.array_equal(F.host_eval(0.7), fn(0.7, pts))
+    glob = lambda t, p: p[:, 0] / p[:, 0].max()        # depends on every point: not chunkable
+    G = _Field(glob, pts, 1, "cpu")
+    assert np.array_equal(G.host_eval(0.0), glob(0.0, pts)) and G._pointwise is False
+    assert np.array_equal(G.host_eval(1.0), glob(1.0, pts))
