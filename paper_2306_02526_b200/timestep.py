@@ -37,6 +37,7 @@ import numpy as np
 
 from . import _lib
 from .device import cuda_device, current_stream_handle, torch
+from . import npgpu
 from .errors import DivergenceError, HpstepError, UnsupportedConfigurationError
 from .operators import EllipticDiscretization
 from .solver import HpsOperatorSet, device_plan, graph_workspace
@@ -405,6 +406,22 @@ def _call_g(g, t, U, ux, uy):
             g._hb_torch = False
         except AttributeError:
             pass
+    # numpy code: on device arrays whose ufuncs run with torch (npgpu), once it has matched the host call
+    if getattr(g, "_hb_npdev", None) is not False and os.environ.get("HPSB_NO_DEVICE_FIELDS") != "1":
+        try:
+            r = npgpu.plain(g(t, npgpu.wrap(U), npgpu.wrap(ux), npgpu.wrap(uy)))
+        except Exception:
+            r = None
+        ok = r is not None and r.is_cuda == U.is_cuda
+        if ok and getattr(g, "_hb_npdev", None) is None:
+            h = np.asarray(g(t, U.cpu().numpy(), ux.cpu().numpy(), uy.cpu().numpy()), dtype=float)
+            ok = npgpu.matches_host(torch.broadcast_to(r, U.shape), np.broadcast_to(h, U.shape))
+        try:
+            g._hb_npdev = ok
+        except AttributeError:
+            pass
+        if ok:
+            return torch.broadcast_to(r, U.shape).contiguous()
     r = np.asarray(g(t, U.cpu().numpy(), ux.cpu().numpy(), uy.cpu().numpy()), dtype=float)
     return torch.as_tensor(np.broadcast_to(r, U.shape), device=U.device).contiguous()
 
@@ -451,6 +468,39 @@ class _Field:
 
     _pool = None       # host threads for chunked evaluations (shared)
     _pointwise = None  # per field: whether fn(t, pts) evaluates point by point (checked on first use)
+    _device_ok = None  # per field: whether fn runs on device arrays and agrees with the host (first use)
+    _pts_dev = None
+
+    def device_eval(self, t):
+        """fn(t, pts) with the points as a device array whose numpy ufuncs run
+        on the GPU (npgpu.DeviceArray), as a (k or 1, n) tensor; None when fn
+        leaves the device (an unmapped numpy call, a numpy result) or its first
+        device result differs from the host call beyond rounding."""
+        if self._device_ok is False or os.environ.get("HPSB_NO_DEVICE_FIELDS") == "1":
+            return None
+        if self._pts_dev is None:
+            self._pts_dev = torch.as_tensor(np.ascontiguousarray(self.pts, dtype=float), device=self.dev)
+        try:
+            r = npgpu.plain(self.fn(t, npgpu.wrap(self._pts_dev)))
+        except Exception:
+            r = None
+        if r is None or r.numel() not in (self.n, self.k * self.n):
+            self._device_ok = False
+            return None
+        r = r.reshape(self.k, self.n) if (r.ndim > 1 or self.k == 1) else r.reshape(1, self.n)
+        if self._device_ok is None:
+            h = np.asarray(self.fn(t, self.pts), dtype=float)
+            h = h.reshape(self.k, self.n) if (h.ndim > 1 or self.k == 1) else h.reshape(1, self.n)
+            self._device_ok = npgpu.matches_host(r, h)
+            if not self._device_ok:
+                return None
+        return r
+
+    def eval_now(self, t):
+        """F(t) of a non-separable F as a device tensor: on the device when F
+        runs there, else on the host (chunked when pointwise) and copied."""
+        v = self.device_eval(t)
+        return v if v is not None else self._stack(self.host_eval(t))
 
     def host_eval(self, t):
         """fn(t, pts) on the host.  A field callable is a function of the
@@ -464,6 +514,8 @@ class _Field:
         if _Field._pool is None:
             from concurrent.futures import ThreadPoolExecutor
             _Field._pool = ThreadPoolExecutor(max_workers=max(1, min(32, os.cpu_count() or 1)))
+            # a forked child does not inherit the threads: it starts its own pool
+            os.register_at_fork(after_in_child=lambda: setattr(_Field, "_pool", None))
         nw = _Field._pool._max_workers
         cuts = [self.n * i // nw for i in range(nw + 1)]
         parts = list(_Field._pool.map(lambda i: np.asarray(fn(t, pts[cuts[i]:cuts[i + 1]]), dtype=float),
@@ -489,7 +541,7 @@ class _Field:
             return st._dummy((1, self.n))
         if st is not None and st._seg is not None:
             return st._cut_field(self, t)
-        return self._stack(self.host_eval(t))
+        return self.eval_now(t)
 
     def terms(self, t, scale=1.0):
         """(coef, tensor) terms of scale*F(t); evaluates non-separable F now."""
@@ -665,7 +717,7 @@ class TimeStepper:
         a = np.asarray(F.fn(t, F.pts), dtype=float)      # shape only (host)
         rows = F.k if (a.ndim > 1 or F.k == 1) else 1
         tgt = self._cut_buf((rows, F.n))
-        self._eager(lambda tc=t: tgt.copy_(F._stack(F.host_eval(self._replay_t + tc))))
+        self._eager(lambda tc=t: tgt.copy_(F.eval_now(self._replay_t + tc)))
         return tgt
 
     def _dummy(self, shape):

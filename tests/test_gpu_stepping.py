@@ -338,3 +338,43 @@ def test_ark5_stages_match_reference(golden, monkeypatch):
     for i, (a, b) in enumerate(zip(stages, z["stages"])):
         assert rel_l2(a[0], b) < TOL, f"stage {i + 1}"
     assert rel_l2(s.u, z["u1"]) < TOL
+
+
+def test_plain_numpy_fields_and_g_run_on_device_arrays():
+    """The reference caller's plain numpy callables (q, f, an undeclared g)
+    run on the GPU through npgpu.DeviceArray once they matched the host call;
+    the trajectory equals the one with SeparableField / declared g, and a
+    callable outside the mapped numpy subset still runs (on the host)."""
+    import numpy as np
+    import paper_2306_02526_b200 as hb
+    from paper_2306_02526_b200.timestep import _Field
+    pts = np.random.default_rng(1).random((5000, 2))
+    fn = lambda t, p: np.where(p[:, 0] > 0.5, np.sin(2 * np.pi * p[:, 1]), np.exp(-p[:, 0])) * np.cos(t)
+    F = _Field(fn, pts, 1, "cuda")
+    v = F.eval_now(0.4)
+    assert F._device_ok is True and v.is_cuda
+    assert np.abs(v.cpu().numpy()[0] - fn(0.4, pts)).max() < 1e-14
+    h = lambda t, p: np.linalg.norm(p, axis=1) * t        # not mapped: host
+    H = _Field(h, pts, 1, "cuda")
+    assert np.array_equal(H.eval_now(0.4).cpu().numpy()[0], h(0.4, pts)) and H._device_ok is False
+
+    tree = hb.build_tree(((0.0, 1.0), (0.0, 1.0)), 8, 8, 10)
+    phi = lambda p: np.sin(2 * np.pi * p[:, 0]) * np.sin(2 * np.pi * p[:, 1])
+    def run(plain):
+        if plain:
+            q = lambda t, p: phi(p) * (-np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
+            f = lambda t, p: phi(p) * np.cos(t)
+            g = lambda t, u, ux, uy: -0.1 * np.sin(u)
+        else:
+            q = hb.SeparableField.product(phi, lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t))
+            f = hb.SeparableField.product(phi, np.cos)
+            g = hb.declare_nonlinear(lambda t, u, ux, uy: -0.1 * torch_sin(u), ux=False, uy=False, pure=True)
+        prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0), q=q, f=f, g=g, u0=phi)
+        st = hb.TimeStepper(tree, prob, "ARK4", dt=1e-3)
+        return st.run(st.initial_state(), 3).u, st
+    import torch
+    torch_sin = torch.sin
+    a, _ = run(False)
+    b, st = run(True)
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+    assert getattr(st.problem.g, "_hb_npdev", None) is True

@@ -69,3 +69,6 @@ def test_field_host_eval_chunks_only_pointwise_callables():
     G = _Field(glob, pts, 1, "cpu")
     assert np.array_equal(G.host_eval(0.0), glob(0.0, pts)) and G._pointwise is False
     assert np.array_equal(G.host_eval(1.0), glob(1.0, pts))
+    _Field._pool.shutdown()   # no idle threads left behind for the forking tests
+    _Field._pool = None
+
