@@ -419,6 +419,7 @@ static double* ops_alloc(Ops& O, size_t doubles, bool zero) {
 void hps_ops_destroy(hps_ops* h) {
   if (!h) return;
   for (void* p : h->O.allocs) cudaFree(p);
+  for (void* p : h->O.aux) cudaFree(p);
   delete h;
 }
 
@@ -719,6 +720,7 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
     sTchild = O.shared_leaf ? 0 : (long long)n12 * n12;
   }
   if (P.depth > 0) O.root_T = O.lo[0].T;
+  if (int rc = sub_mma_prepare(O, st)) return fail(rc);
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     set_error("cuda error at end of build: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(HPS_ERR_CUDA);
@@ -1110,6 +1112,12 @@ int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops**
     LevelOps& lo = O.lo[d];
     lo.Up.base = at(lidx[5 * d]); lo.S.base = at(lidx[5 * d + 1]);
     lo.Ush = at(lidx[5 * d + 2]); lo.Ssh = at(lidx[5 * d + 3]); lo.T = at(lidx[5 * d + 4]);
+  }
+  if (int rc = sub_mma_prepare(O, 0)) { hps_ops_destroy(h); return rc; }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    hps_ops_destroy(h);
+    set_error("hps_ops_load: %s", cudaGetErrorString(cudaGetLastError()));
+    return HPS_ERR_CUDA;
   }
   *out = h;
   return HPS_OK;

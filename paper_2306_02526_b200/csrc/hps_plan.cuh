@@ -110,6 +110,10 @@ struct LevelOps {
   double* Ush = nullptr;   // (n3 + n12) x ld3
   double* Ssh = nullptr;   // n3 x ld12
   double* T = nullptr;     // c x n12 x n12 row-major (only when keep_dtn)
+  // fused subtree levels, shared layout: fragment-ordered Up / S for the
+  // tensor-core subtree kernels (subtree.cu, sub_mma_prepare), or null
+  const double* UpF = nullptr;
+  const double* SF = nullptr;
 };
 
 struct Ops {
@@ -130,7 +134,9 @@ struct Ops {
   size_t bytes = 0;            // device bytes owned
   std::vector<void*> allocs;
   std::vector<size_t> alloc_bytes;
+  std::vector<void*> aux;      // derived device data rebuilt after build / load (not dumped)
 };
+int sub_mma_prepare(Ops& O, cudaStream_t st);
 
 int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st);
 // rows [0, R1) of each node from src1, rows [R1, R) from src2

@@ -349,6 +349,304 @@ __global__ void __launch_bounds__(NT, KM == 1 ? 4 : 1) k_sub_down_local(SubArgs 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core subtree levels (shared operators, one rhs).
+//
+// The SIMT applies above are issue-bound: ~20 instructions per fma go to
+// address arithmetic, index gathers and operator loads (ncu: k_sub_up issues
+// 40 M warp instructions for 65 M fmas per C2 solve; its time is that
+// instruction count over the SMs' issue slots).  Here a level's apply
+//     Y[row][node] = sum_c Op[row][c] X[node][c]
+// runs as DMMA m8n8k4 tiles, (8 operator rows) x (8 nodes) x (4 columns) per
+// instruction:
+//  * A fragments from a fragment-ordered copy of the level operator
+//    (sub_mma_prepare: tile (m, k) is 32 consecutive doubles in lane order,
+//    zero padded to whole 8-row tiles and to k-steps in multiples of 4), so a
+//    warp's operator load is one coalesced 256-byte line with no predicates
+//    (L1-cached: the CTAs of an SM read the same level tiles);
+//  * B fragments from the CTA's staged node vectors (row stride = 4 mod 16
+//    doubles: conflict-free), zero padded to 16 columns;
+//  * the level's index tables (child-flux offsets, slot maps) staged in
+//    shared memory before the dependency wait; the subtree's leaf fluxes
+//    staged by one coalesced copy.
+// Work units are (row tile, node tile, column split) spread over the warps;
+// split partials meet in shared memory and are added in split order, so the
+// results are deterministic.  Levels with fewer than 8 nodes in a subtree pad
+// the node tile.
+constexpr int MW = NT / 32;      // warps per CTA
+constexpr int kRedUnits = 16;    // partial 8 x 8 tiles in shared memory
+constexpr int kRedMma = kRedUnits * 64;
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// staged node-vector stride: = 4 (mod 16) doubles (the 8 x 4 B-fragment reads
+// of a warp, node = lane / 4, column = lane % 4, hit distinct banks), with
+// room for the zero padding to 16 columns
+__host__ __device__ __forceinline__ int mma_xs(int C) { return ((C + 15) & ~15) + 4; }
+
+// Y = Op X^T for one (level, operator): units (m, n, s) over the warps.
+// F: fragment-ordered operator (mt x kt4 tiles of 32); xs: [node][XS], vn nodes.
+// pre(node, row, ctx) runs before the k-loop of a single-split unit (prefetch of
+// epilogue operands), out(node, row, y, ctx) after it.
+struct MmaShape { int mt, kt4, ks, kper; };
+
+template <class Pre, class Out>
+__device__ __forceinline__ void mma_apply(const double* __restrict__ F, const MmaShape sh, int R, const double* xs,
+                                          int XS, int vn, double* red, Pre pre, Out out) {
+  const int mt = sh.mt, nt = (vn + 7) >> 3, mn = mt * nt, ks = sh.ks;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gr = lane >> 2, gc = lane & 3;
+  for (int u = warp; u < mn * ks; u += MW) {
+    const int s = ks == 1 ? 0 : u / mn, t = u - s * mn, n = t / mt, m = t - n * mt;
+    const int row = m * 8 + gr, node = n * 8 + 2 * gc;
+    const int k0 = s * sh.kper, kn = min(sh.kt4 - k0, sh.kper);
+    const double* ap = F + ((size_t)m * sh.kt4 + k0) * 32 + lane;
+    const double* bp = xs + min(n * 8 + gr, vn - 1) * XS + k0 * 4 + gc;
+    typename Pre::Ctx cx{};
+    if (ks == 1 && row < R) pre(node, row, cx);
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < kn; k += 4) {
+      const double a0 = __ldg(ap), a1 = __ldg(ap + 32), a2 = __ldg(ap + 64), a3 = __ldg(ap + 96);
+      const double b0 = bp[0], b1 = bp[4], b2 = bp[8], b3 = bp[12];
+      dmma8(d0, d1, a0, b0);
+      dmma8(e0, e1, a1, b1);
+      dmma8(d0, d1, a2, b2);
+      dmma8(e0, e1, a3, b3);
+      ap += 128;
+      bp += 16;
+    }
+    d0 += e0;
+    d1 += e1;
+    if (ks == 1) {
+      if (row < R) {
+        if (node < vn) out(node, row, d0, cx, 0);
+        if (node + 1 < vn) out(node + 1, row, d1, cx, 1);
+      }
+    } else {
+      double* rp = red + (size_t)u * 64 + gr * 8 + 2 * gc;
+      rp[0] = d0;
+      rp[1] = d1;
+    }
+  }
+  if (ks > 1) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < mn * 64; i += NT) {
+      const int t = i >> 6, e = i & 63, n = t / mt, row = (t - n * mt) * 8 + (e >> 3), node = n * 8 + (e & 7);
+      if (row >= R || node >= vn) continue;
+      double y = red[i];
+      for (int s = 1; s < ks; ++s) y += red[(size_t)s * mn * 64 + i];
+      typename Pre::Ctx cx{};
+      pre.single(node, row, cx);
+      out(node, row, y, cx, 0);
+    }
+  }
+}
+
+// (idx over nodes x width W) decoded incrementally: one division per thread per level
+struct Walk {
+  int j, c, dj, dc, W;
+  __device__ __forceinline__ Walk(int W_) : W(W_) {
+    j = threadIdx.x / W; c = threadIdx.x - j * W; dj = NT / W; dc = NT - dj * W;
+  }
+  __device__ __forceinline__ void next() {
+    j += dj; c += dc;
+    if (c >= W) { c -= W; ++j; }
+  }
+};
+
+struct MLevel {       // per fused level, the tensor-core path
+  const double *UpF, *SF;
+  MmaShape up, dn;
+  int tab;            // k_sub_up_mma: offset of the level's index table (ints) in shared memory
+};
+
+struct MmaArgs {
+  MLevel ml[MAXF];
+  int tab_ints;       // k_sub_up_mma: index tables (ints)
+  int sl_ints;        // k_sub_down_mma: slot maps (ints)
+  int hcap, rcap, xcap;
+};
+
+struct NoCtx { int z; };
+struct PreNone {
+  using Ctx = NoCtx;
+  __device__ __forceinline__ void operator()(int, int, Ctx&) const {}
+  __device__ __forceinline__ void single(int, int, Ctx&) const {}
+};
+
+__global__ void __launch_bounds__(NT, 4) k_sub_up_mma(SubArgs a, MmaArgs m) {
+  extern __shared__ double sm[];
+  double* Hs = sm;                 // children's fluxes of the current level [child][cs]
+  double* Hn = Hs + m.hcap;        // this level's fluxes [node][n12]
+  double* r3s = Hn + m.hcap;       // [node][mma_xs(n3)]
+  double* red = r3s + m.rcap;      // kRedMma
+  int* tab = reinterpret_cast<int*>(red + kRedMma);
+  const int b = a.b0 + blockIdx.x, tid = threadIdx.x;
+  pdl_trigger();
+  // index tables (plan constants) before the dependency wait: per level
+  // [g3a (n3) | g3b (n3) | gh (n12)], offsets relative to child 0 of a node
+  for (int e = 0; e < a.nf; ++e) {
+    const FLevel& L = a.lv[e];
+    const int cs = e == a.nf - 1 ? (int)a.hs : L.nbc, n3 = L.n3, n12 = L.n12;
+    int* t = tab + m.ml[e].tab;
+    for (int i = tid; i < 2 * n3 + n12; i += NT) {
+      int v;
+      if (i < n3) v = L.i3a[i];
+      else if (i < 2 * n3) v = cs + L.i3b[i - n3];
+      else {
+        const int r = i - 2 * n3;
+        v = r < L.n1a ? L.i1a[r] : cs + L.i2b[r - L.n1a];
+      }
+      t[i] = v;
+    }
+  }
+  pdl_wait();
+  {  // the subtree's leaf fluxes: one contiguous block
+    const int npn = 1 << (a.nf - 1);
+    const double* src = a.Hleaf + 2LL * b * npn * a.hs;
+    const int n = 2 * npn * (int)a.hs;
+    for (int i = tid; i < n; i += NT) Hs[i] = src[i];
+  }
+  for (int e = a.nf - 1; e >= 0; --e) {
+    const FLevel& L = a.lv[e];
+    const MLevel& M = m.ml[e];
+    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, XS = mma_xs(n3), W = (n3 + 15) & ~15;
+    const int cs = e == a.nf - 1 ? (int)a.hs : L.nbc;
+    const int* g3 = tab + M.tab;
+    const int* gh = g3 + 2 * n3;
+    __syncthreads();
+    {
+      Walk w(W);
+      for (int idx = tid; idx < npn * W; idx += NT, w.next()) {
+        double v = 0.0;
+        if (w.c < n3) {
+          const double* hc = Hs + 2 * w.j * cs;
+          v = hc[g3[n3 + w.c]] - hc[g3[w.c]];
+          if (a.jump) v = v - a.inv_dt * a.jump[L.j3[(long long)(node0 + w.j) * n3 + w.c]];
+        }
+        r3s[w.j * XS + w.c] = v;
+      }
+    }
+    __syncthreads();
+    // [w3; h - base] = [X33^-1; Tstack X33^-1] r3 for the subtree's nodes of this level
+    mma_apply(M.UpF, M.up, L.Up.R, r3s, XS, npn, red, PreNone{},
+              [&](int j, int row, double y, NoCtx&, int) {
+                if (row < n3) {
+                  L.W3[(long long)(node0 + j) * n3 + row] = y;
+                  return;
+                }
+                const int r = row - n3;
+                const double h = Hs[2 * j * cs + gh[r]] + y;
+                Hn[j * n12 + r] = h;
+                if (e == 0) a.H_dF[(long long)(node0 + j) * n12 + r] = h;
+              });
+    if (a.dF + e == 0) break;  // the root's outer flux is never consumed
+    double* t = Hs; Hs = Hn; Hn = t;
+  }
+}
+
+struct DnCtx { double w[2]; int id[2]; };
+struct PreDown {
+  using Ctx = DnCtx;
+  const double* W3; const int* j3; long long base; int n3, has_w3, vn;
+  __device__ __forceinline__ void single(int node, int row, Ctx& c) const {
+    const long long nd = base + (long long)node * n3 + row;
+    c.w[0] = has_w3 ? W3[nd] : 0.0;
+    c.id[0] = j3[nd];
+  }
+  __device__ __forceinline__ void operator()(int node, int row, Ctx& c) const {  // nodes node, node + 1
+    const long long nd = base + (long long)node * n3 + row;
+    if (node < vn) {
+      c.w[0] = has_w3 ? W3[nd] : 0.0;
+      c.id[0] = j3[nd];
+    }
+    if (node + 1 < vn) {
+      c.w[1] = has_w3 ? W3[nd + n3] : 0.0;
+      c.id[1] = j3[nd + n3];
+    }
+  }
+};
+
+__global__ void __launch_bounds__(NT, 4) k_sub_down_mma(SubArgs a, MmaArgs m) {
+  extern __shared__ double sm[];
+  double* red = sm;                        // kRedMma
+  double* xs = red + kRedMma;              // [node][mma_xs(n12)]
+  double* uloc = xs + m.xcap;              // [nslots]
+  int* sls = reinterpret_cast<int*>(uloc + ((a.nslots + 1) & ~1));  // slot maps of every level
+  const int b = a.b0 + blockIdx.x, tid = threadIdx.x;
+  pdl_trigger();
+  const int n12r = a.lv[0].n12;
+  const int gi = tid < n12r ? a.gidx_root[(long long)b * n12r + tid] : 0;
+  for (int i = tid; i < m.sl_ints; i += NT) sls[i] = a.slots[i];
+  pdl_wait();
+  for (int col = tid; col < n12r; col += NT) uloc[col] = a.u[col == tid ? gi : a.gidx_root[(long long)b * n12r + col]];
+  for (int e = 0; e < a.nf; ++e) {
+    const FLevel& L = a.lv[e];
+    const MLevel& M = m.ml[e];
+    const int npn = 1 << e, node0 = b * npn, n3 = L.n3, n12 = L.n12, jb = a.j3_base[e], XS = mma_xs(n12);
+    const int W = (n12 + 15) & ~15;
+    const int* sl = sls + a.slot_off[e];
+    __syncthreads();
+    {
+      Walk w(W);
+      for (int idx = tid; idx < npn * W; idx += NT, w.next())
+        xs[w.j * XS + w.c] = w.c < n12 ? uloc[sl[w.j * n12 + w.c]] : 0.0;
+    }
+    __syncthreads();
+    PreDown pd{L.W3, L.j3, (long long)node0 * n3, n3, a.has_w3, npn};
+    mma_apply(M.SF, M.dn, n3, xs, XS, npn, red, pd, [&](int j, int row, double y, DnCtx& c, int h) {
+      y = y + c.w[h];
+      uloc[jb + j * n3 + row] = y;
+      a.u[c.id[h]] = y;
+    });
+  }
+}
+
+// fragment-ordered copy of a column-major panel tile (R x C, column stride TS)
+__global__ void k_frag(const double* __restrict__ src, int R, int C, int TS, int mt, int kt4, double* dst) {
+  const long long n = (long long)mt * kt4 * 32;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += gridDim.x * 256LL) {
+    const int lane = (int)(i & 31);
+    const long long t = i >> 5;
+    const int k = (int)(t % kt4), mm = (int)(t / kt4);
+    const int r = mm * 8 + (lane >> 2), c = k * 4 + (lane & 3);
+    dst[i] = (r < R && c < C) ? src[(size_t)c * TS + r] : 0.0;
+  }
+}
+
+MmaShape mma_shape(int R, int C, int vn) {
+  MmaShape s;
+  s.mt = (R + 7) / 8;
+  s.kt4 = (((C + 3) / 4) + 3) & ~3;
+  const int mn = s.mt * ((vn + 7) / 8);
+  // column splits of whole 4-step groups: fewest (rounds of units) x (latency + k-steps)
+  constexpr int kLat = 24, kRed = 24;
+  const int g = s.kt4 / 4;
+  long long best = -1;
+  s.ks = 1; s.kper = s.kt4;
+  for (int ks = 1; ks <= 8 && ks <= g; ++ks) {
+    if (ks > 1 && mn * ks > kRedUnits) break;
+    const int kper = ((g + ks - 1) / ks) * 4;
+    const int used = (s.kt4 + kper - 1) / kper;
+    if (used != ks) continue;
+    const long long cost = (long long)((mn * ks + MW - 1) / MW) * (kLat + kper) + (ks > 1 ? kRed : 0);
+    if (best < 0 || cost < best) { best = cost; s.ks = ks; s.kper = kper; }
+  }
+  return s;
+}
+
+bool sub_mma_enabled() {
+  static const bool off = [] {
+    const char* e = getenv("HPSB_NO_SUB_MMA");
+    return e && e[0] == '1';
+  }();
+  return !off;
+}
+
 void fill_args(const Ops& ops, const Workspace& ws, int k, SubArgs& a) {
   const Plan& P = *ops.plan;
   static const int fold = [] {
@@ -401,8 +699,37 @@ bool shared_sub(const SubArgs& a) {
   return true;
 }
 
-template <class K>
-int launch_sub(K kern, int nsub, int KM, int k, size_t smem, const SubArgs& a, cudaStream_t st) {
+// the tensor-core path: shared operators with fragment-ordered copies, one rhs, subtree-local slots
+bool fill_mma(const Ops& ops, const SubArgs& a, MmaArgs& m) {
+  const Plan& P = *ops.plan;
+  if (!sub_mma_enabled() || a.k != 1 || !ops.shared_levels) return false;
+  int tab = 0, hcap = 0, rcap = 0, xcap = 0;
+  for (int e = 0; e < a.nf; ++e) {
+    const LevelOps& lo = ops.lo[P.dF + e];
+    if (!lo.UpF || !lo.SF) return false;
+    const FLevel& L = a.lv[e];
+    const int npn = 1 << e;
+    MLevel& M = m.ml[e];
+    M.UpF = lo.UpF; M.SF = lo.SF;
+    M.up = mma_shape(L.Up.R, L.n3, npn);
+    M.dn = mma_shape(L.n3, L.n12, npn);
+    M.tab = tab;
+    tab += 2 * L.n3 + L.n12;
+    const int cs = e == a.nf - 1 ? (int)a.hs : L.nbc;
+    hcap = std::max(hcap, std::max(2 * npn * cs, npn * L.n12));
+    rcap = std::max(rcap, npn * mma_xs(L.n3));
+    xcap = std::max(xcap, npn * mma_xs(L.n12));
+  }
+  m.tab_ints = tab;
+  m.hcap = (hcap + 1) & ~1;
+  m.rcap = (rcap + 1) & ~1;
+  m.xcap = (xcap + 1) & ~1;
+  m.sl_ints = P.sub_local ? (int)P.sub_slot_off[a.nf] : 0;
+  return true;
+}
+
+template <class K, class... X>
+int launch_sub(K kern, int nsub, int KM, int k, size_t smem, const SubArgs& a, cudaStream_t st, const X&... x) {
   if (smem > 227 * 1024) {
     set_error("subtree kernel needs %zu bytes of shared memory", smem);
     return -1;
@@ -412,7 +739,7 @@ int launch_sub(K kern, int nsub, int KM, int k, size_t smem, const SubArgs& a, c
   HPSB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (nsub <= 0) return 0;
   dim3 grid((unsigned)nsub, (unsigned)cdiv(k, KM));
-  HPSB_CUDA(launch_pdl(kern, grid, dim3(NT), smem, st, a));
+  HPSB_CUDA(launch_pdl(kern, grid, dim3(NT), smem, st, a, x...));
   HPSB_LAUNCH_CHECK();
   return 0;
 }
@@ -439,6 +766,31 @@ int fuse_level(const Plan& P) {
   return best;
 }
 
+// fragment-ordered copies of the fused levels' shared operators for the
+// tensor-core subtree kernels (not part of an operator dump: rebuilt on load)
+int sub_mma_prepare(Ops& O, cudaStream_t st) {
+  const Plan& P = *O.plan;
+  if (!O.shared_levels || P.dF >= P.depth) return 0;
+  for (int d = P.dF; d < P.depth; ++d) {
+    LevelOps& lo = O.lo[d];
+    if (!lo.Up.base || !lo.S.base || lo.Up.c != 1 || lo.S.c != 1) return 0;
+    const int npn = 1 << (d - P.dF);
+    const MmaShape u = mma_shape(lo.Up.R, lo.Up.C, npn), s = mma_shape(lo.S.R, lo.S.C, npn);
+    const size_t nu = (size_t)u.mt * u.kt4 * 32, ns = (size_t)s.mt * s.kt4 * 32;
+    double* p = nullptr;
+    if (cudaMalloc(&p, (nu + ns) * 8) != cudaSuccess) { cudaGetLastError(); return 0; }  // SIMT kernels instead
+    O.aux.push_back(p);
+    k_frag<<<(unsigned)std::min<size_t>((nu + 255) / 256, 1184), 256, 0, st>>>(lo.Up.base, lo.Up.R, lo.Up.C, lo.Up.TS,
+                                                                                u.mt, u.kt4, p);
+    k_frag<<<(unsigned)std::min<size_t>((ns + 255) / 256, 1184), 256, 0, st>>>(lo.S.base, lo.S.R, lo.S.C, lo.S.TS,
+                                                                                s.mt, s.kt4, p + nu);
+    HPSB_LAUNCH_CHECK();
+    lo.UpF = p;
+    lo.SF = p + nu;
+  }
+  return 0;
+}
+
 int mb_subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, long long sh, long long hs,
                   int b0, int b1, cudaStream_t st);
 int mb_subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double* u, long long ld_u, int b0,
@@ -459,6 +811,13 @@ int subtree_up(const Ops& ops, const Workspace& ws, int k, const double* Hleaf, 
   a.jump = jump; a.jump_k = ld_jump; a.inv_dt = inv_dt;
   const int KM = k == 1 ? 1 : 4;
   const bool shm = KM == 1 && shared_sub(a);
+  if (shm) {
+    MmaArgs m{};
+    if (fill_mma(ops, a, m)) {
+      size_t sm2 = (size_t)(2 * m.hcap + m.rcap + kRedMma) * 8 + (size_t)m.tab_ints * 4;
+      return launch_sub(k_sub_up_mma, b1 - b0, 1, k, sm2, a, st, m);
+    }
+  }
   const size_t smem = (size_t)(KM * (2 * a.hcap + a.rcap) + red_doubles(KM, shm)) * 8;
   if (shm) return launch_sub(k_sub_up<1, true>, b1 - b0, 1, k, smem, a, st);
   if (KM == 1) return launch_sub(k_sub_up<1>, b1 - b0, 1, k, smem, a, st);
@@ -481,6 +840,13 @@ int subtree_down(const Ops& ops, const Workspace& ws, int k, bool has_w3, double
   int xcap = 0;
   for (int e = 0; e < a.nf; ++e) xcap = std::max(xcap, (1 << e) * ((a.lv[e].n12 + 1) & ~1));
   const bool shm = KM == 1 && shared_sub(a);
+  if (P.sub_local && shm) {
+    MmaArgs m{};
+    if (fill_mma(ops, a, m)) {
+      const size_t sm2 = (size_t)(kRedMma + m.xcap + ((a.nslots + 1) & ~1)) * 8 + (size_t)m.sl_ints * 4;
+      if (sm2 <= 200 * 1024) return launch_sub(k_sub_down_mma, b1 - b0, 1, k, sm2, a, st, m);
+    }
+  }
   if (P.sub_local) {
     const size_t smem = (size_t)(KM * xcap + red_doubles(KM, shm) + ((KM * a.nslots + 1) & ~1)) * 8;
     if (smem <= 200 * 1024) {
