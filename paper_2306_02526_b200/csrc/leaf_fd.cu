@@ -36,6 +36,8 @@ struct FdArgs {
   const double* u; long long ld_u;   // FD_DOWN: solution rows (boundary values read through lbg)
   double* uint; long long ld_uint;   // FD_DOWN: interior output (leaf l at l*ni)
   double* lu; long long ld_lu;       // FD_DOWN, optional: L u at the interiors (the stage history)
+  double lu_sigma, lu_inv_dtg;       // FD_DOWN with lu: inv_dtg != 0 -> L u = (sigma u_int - r) / dtg from the
+                                     // solved interior equation instead of two more leaf-grid products
   unsigned long long* guard;         // ... and max |u| over the leaves' grids (bits, NaN sticky)
   int nterm; const double* tv[kFdTerms]; const double* tdc;  // FD_UP_T: body load = sum_t tdc[t] tv[t] ...
   long long tld[kFdTerms];                                   // (rhs row strides of the terms, 0 = shared row)
@@ -250,46 +252,52 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   // FD_DOWN: 16-byte stores of u_int pairs (every leaf block starts at an even offset when Q is even)
   const bool vec = MODE == FD_DOWN && Q % 2 == 0 &&
                    (reinterpret_cast<uintptr_t>(a.uint + (long long)kk * a.ld_uint) & 15) == 0;
+  const bool vec_lu = MODE == FD_DOWN && Q % 2 == 0 && a.lu &&
+                      (reinterpret_cast<uintptr_t>(a.lu + (long long)kk * a.ld_lu) & 15) == 0 &&
+                      (reinterpret_cast<uintptr_t>(g) & 15) == 0;
   const int nwarps = gridDim.x * 8;
   constexpr int NR = (NI + 31) / 32;  // body-load values per lane
   constexpr int NU = (NB + 31) / 32;  // boundary values per lane (FD_DOWN)
   double nxt[NR];                     // next leaf's body load, prefetched during this leaf
   double nub[DOWNLIKE ? NU : 1];
+  // FD_UP_T: the stage combination in term order (the fma order of k_combine).
+  // The first two terms of the NEXT leaf are issued before this leaf's products
+  // (fetch) and stay in flight across them; finish() sums them and streams the
+  // remaining terms two loads at a time, then writes the formed load out
+  double va[MODE == FD_UP_T ? NR : 1], vb[MODE == FD_UP_T ? NR : 1];
+  auto ldt = [&](double* v, int t, int leaf) {
+    const double* src = a.tv[t] + kk * a.tld[t] + (long long)leaf * NI;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = (leaf < a.L && e < NI) ? __ldcs(src + e) : 0.0;
+    }
+  };
+  auto finish = [&](int leaf) {
+#pragma unroll
+    for (int i = 0; i < NR; ++i) nxt[i] = 0.0;
+    for (int t = 0; t < a.nterm; t += 2) {
+      const double c0 = __ldg(a.tdc + t);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) nxt[i] = fma(c0, va[i], nxt[i]);
+      if (t + 1 >= a.nterm) break;
+      if (t + 2 < a.nterm) ldt(va, t + 2, leaf);
+      const double c1 = __ldg(a.tdc + t + 1);
+#pragma unroll
+      for (int i = 0; i < NR; ++i) nxt[i] = fma(c1, vb[i], nxt[i]);
+      if (t + 3 < a.nterm) ldt(vb, t + 3, leaf);
+    }
+    double* ro = a.rout + kk * a.ld_rout + (long long)leaf * NI;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const int e = lane + 32 * i;
+      if (e < NI) ro[e] = nxt[i];
+    }
+  };
   auto fetch = [&](int leaf) {
     if (MODE == FD_UP_T) {
-      // the stage combination in term order (the fma order of k_combine), the
-      // next term's loads in flight while one is summed
-      double va[NR], vb[NR];
-      auto ldt = [&](double (&v)[NR], int t) {
-        const double* src = a.tv[t] + kk * a.tld[t] + (long long)leaf * NI;
-#pragma unroll
-        for (int i = 0; i < NR; ++i) {
-          const int e = lane + 32 * i;
-          v[i] = (leaf < a.L && e < NI) ? __ldcs(src + e) : 0.0;
-        }
-      };
-#pragma unroll
-      for (int i = 0; i < NR; ++i) nxt[i] = 0.0;
-      ldt(va, 0);
-      for (int t = 0; t < a.nterm; t += 2) {
-        if (t + 1 < a.nterm) ldt(vb, t + 1);
-        const double c0 = __ldg(a.tdc + t);
-#pragma unroll
-        for (int i = 0; i < NR; ++i) nxt[i] = fma(c0, va[i], nxt[i]);
-        if (t + 1 >= a.nterm) break;
-        if (t + 2 < a.nterm) ldt(va, t + 2);
-        const double c1 = __ldg(a.tdc + t + 1);
-#pragma unroll
-        for (int i = 0; i < NR; ++i) nxt[i] = fma(c1, vb[i], nxt[i]);
-      }
-      if (leaf < a.L) {
-        double* ro = a.rout + kk * a.ld_rout + (long long)leaf * NI;
-#pragma unroll
-        for (int i = 0; i < NR; ++i) {
-          const int e = lane + 32 * i;
-          if (e < NI) ro[e] = nxt[i];
-        }
-      }
+      ldt(va, 0, leaf);
+      if (a.nterm > 1) ldt(vb, 1, leaf);
       return;
     }
 #pragma unroll
@@ -308,6 +316,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
   };
   fetch(blockIdx.x * 8 + warp);
   for (int l = blockIdx.x * 8 + warp; l < a.L; l += nwarps) {
+    if (MODE == FD_UP_T) finish(l);
     if (MODE == FD_LU) {
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
@@ -478,6 +487,28 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     }
     store(bufA, SA);
     __syncwarp();
+    // FD_DOWN with the stage history from the solved interior equation: r in
+    // the fragment layout, in flight during the last product (an L1 / L2 hit)
+    const bool lu_res = MODE == FD_DOWN && a.lu && a.lu_inv_dtg != 0.0;
+    double2 rf[2][2];
+    if (MODE == FD_DOWN && lu_res) {
+      const double* rr = g ? g + (long long)l * NI : nullptr;
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 2; ++nj) {
+          const int x = mi * 8 + gr, y = nj * 8 + 2 * gc;
+          rf[mi][nj] = make_double2(0.0, 0.0);
+          if (rr && x < Q && y < Q) {
+            if (vec_lu && y + 1 < Q) {
+              rf[mi][nj] = *reinterpret_cast<const double2*>(rr + x * Q + y);
+            } else {
+              rf[mi][nj].x = rr[x * Q + y];
+              if (y + 1 < Q) rf[mi][nj].y = rr[x * Q + y + 1];
+            }
+          }
+        }
+    }
     // W = T3 Vy^T  (A operand from bufA)
     clear();
 #pragma unroll
@@ -507,7 +538,30 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
             }
           }
         }
-      if (!a.lu) {
+      if (lu_res) {
+        // the interior rows of the leaf system just solved read
+        //   sigma u_int - dtg (L u)_int = r   (A = sigma I - dtg L, operators.py:252-269),
+        // so the stage history L u_i (timestep.py:259-261) is (sigma u_int - r) / dtg to the
+        // solve's residual (~1e-15 relative)
+        double* lo = a.lu + kk * a.ld_lu + (long long)l * NI;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int nj = 0; nj < 2; ++nj) {
+            const int x = mi * 8 + gr, y = nj * 8 + 2 * gc;
+            if (x < Q && y < Q) {
+              const double l0 = (a.lu_sigma * acc[mi][nj][0] - rf[mi][nj].x) * a.lu_inv_dtg;
+              const double l1 = (a.lu_sigma * acc[mi][nj][1] - rf[mi][nj].y) * a.lu_inv_dtg;
+              if (vec_lu && y + 1 < Q) {
+                *reinterpret_cast<double2*>(lo + x * Q + y) = make_double2(l0, l1);
+              } else {
+                lo[x * Q + y] = l0;
+                if (y + 1 < Q) lo[x * Q + y + 1] = l1;
+              }
+            }
+          }
+      }
+      if (!a.lu || lu_res) {
         if (a.guard) {  // max |u| over the leaf's grid: interior fragments and boundary values
 #pragma unroll
           for (int mi = 0; mi < 2; ++mi)
@@ -689,6 +743,8 @@ int leaf_fd_down(const Ops& ops, int k, int nleaf, const double* g, long long ld
   a.L = nleaf; a.k = k; a.g = g; a.ld_g = ld_g; a.lbg = lbg; a.u = u; a.ld_u = ld_u;
   a.uint = uint; a.ld_uint = ld_uint; a.mats = ops.fd;
   a.lu = lu; a.ld_lu = ld_lu; a.guard = reinterpret_cast<unsigned long long*>(guard);
+  static const bool lu_products = getenv("HPSB_LU_PRODUCTS") != nullptr;
+  if (lu && !lu_products && ops.dtg != 0.0) { a.lu_sigma = ops.sigma; a.lu_inv_dtg = 1.0 / ops.dtg; }
   return launch_fd_mma<FD_DOWN>(*ops.plan, a, nleaf, k, st);
 }
 
