@@ -1110,6 +1110,29 @@ class TimeStepper:
     def _root_batch(self):
         return self.ops.fuses_stage_history and self.ops.root_dirichlet_ok and self.solve_timer is None
 
+    def _root_sep_products(self):
+        """Rows S_root F_m of a separable f = sum_m tau_m(t) F_m(x) (single-row
+        terms, at most 8), cached on the operator set; None when f is not
+        separable or HPSB_NO_ROOT_SEP=1.  Computed by the first pass that needs
+        them (the coefficient pass that precedes every capture included); never
+        launched inside a capture."""
+        if os.environ.get("HPSB_NO_ROOT_SEP") == "1":
+            return None
+        F = self._F
+        if F.fn is None or F.sep is None or not (1 <= len(F.sep) <= 8) or any(v.shape[0] != 1 for v in F.sep):
+            return None
+        cache = getattr(self.ops, "_root_sep", None)
+        if cache is not None and cache[0] is F:
+            return cache[1]
+        if torch.cuda.is_current_stream_capturing():
+            return None
+        rows = torch.cat(list(F.sep), dim=0).contiguous()
+        P = torch.empty((rows.shape[0], self.tree.level_maps[0].n3), dtype=torch.float64, device=self._dev)
+        self.ops.root_dirichlet_device(rows, P)
+        P = [P[m:m + 1] for m in range(rows.shape[0])]
+        self.ops._root_sep = (F, P)
+        return P
+
     def _fused_stage(self, fb, body, out, lu, guard, root_pre=None):
         """Stage solve with the history L u and the guard from the leaf kernel
         of the downward sweep (hps_solve_stage); False when not available."""
@@ -1240,7 +1263,13 @@ class TimeStepper:
         rpre = None
         if bcs is not None and k == 1 and s > 1 and self._root_batch():
             rpre = self._buf("rootpre", (s - 1, self.tree.level_maps[0].n3))
-            if not self._dry:
+            P = self._root_sep_products()
+            if P is not None:
+                # separable boundary data: S_root f(t_i) = sum_m tau_m(t_i) (S_root F_m), the
+                # products S_root F_m computed once per operator set -- no pass over the
+                # root operator per step
+                combine_rows([self._F.fn.factors(t + pair.c[i] * dt) for i in range(1, s)], P, rpre)
+            elif not self._dry:
                 self.ops.root_dirichlet_device(bcs[:s - 1], rpre)
         self._eval_lu(u, Lu[0])
         stage_q_g(0, t + pair.c[0] * dt, u)
