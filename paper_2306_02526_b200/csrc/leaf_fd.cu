@@ -200,6 +200,23 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       cMy[r * CSA + c] = a.mats[5 * NI + 8 * Q + 256 + e];
     }
   }
+  if (MODE == FD_DOWN) {
+    __syncthreads();
+    // coupling constants in the padding (see the staging of the leaf below)
+    for (int e = threadIdx.x; e < 64; e += 256) {
+      const int j = e >> 4, r = e & 15;
+      if (r >= Q) continue;
+      const double* bc = a.mats + 5 * NI + 4 * Q + j * Q;
+      double v = 0.0;
+      if (j < 2) {
+        for (int t = 0; t < Q; ++t) v = fma(cVxi[r * CSA + t], bc[t], v);
+        cVxi[r * CSA + Q + j] = -v;
+      } else {
+        for (int t = 0; t < Q; ++t) v = fma(bc[t], cVyit[t * CSB + r], v);
+        cVyit[(Q + j - 2) * CSB + r] = -v;
+      }
+    }
+  }
   if (UPH) {
     __syncthreads();
     // the fluxes of w = Vx T2 Vy^T need only projections of T2:
@@ -238,7 +255,6 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
         rVyit[i][k] = cVyit[(k * 4 + gc) * CSB + i * 8 + gr];
       }
   }
-  const double* Bc = cst + 4 * Q;
   for (int e = lane; e < 16 * (SB + SA); e += 32) bufB[e] = 0.0;  // zero padding stays zero
   __syncthreads();
   pdl_wait();
@@ -325,20 +341,32 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
       }
     }
     if (MODE == FD_DOWN) {
+      // R = r - A_ib u_b without forming it: the boundary values ride in the
+      // zero padding of the 16 x 16 tile -- east / west rows q, q + 1 meet the
+      // constant columns -Vx^-1 bx0, -Vx^-1 bx1 of the first product's A
+      // operand, north / south columns q, q + 1 pass through it (Vx^-1 u_S,
+      // Vx^-1 u_N) and meet the constant rows -by0 Vy^-T, -by1 Vy^-T of the
+      // second product's B operand: T2 = Vx^-1 (r - A_ib u_b) Vy^-T with no
+      // extra products (q + 2 <= 16) and no per-element coupling sums
+      const bool need_ub = a.lu && a.lu_inv_dtg == 0.0;  // the leaf-grid L u reads the ring from ub
 #pragma unroll
       for (int i = 0; i < NU; ++i) {
         const int b = lane + 32 * i;
-        if (b < NB) ub[b] = nub[i];
+        if (b < NB) {
+          int x, y;
+          if (b < Q) { x = Q; y = b; }
+          else if (b >= 3 * Q) { x = Q + 1; y = b - 3 * Q; }
+          else { x = (b - Q) >> 1; y = Q + ((b - Q) & 1); }
+          bufB[x * SB + y] = nub[i];
+          if (need_ub) ub[b] = nub[i];
+          const double av = fabs(nub[i]);
+          if (a.guard) gmax = (av > gmax || av != av) ? av : gmax;
+        }
       }
-      __syncwarp();
       int x = lane / Q, y = lane % Q;  // grid point of element lane + 32 i, advanced incrementally
 #pragma unroll
       for (int i = 0; i < NR; ++i) {
-        if (x < Q) {
-          const double cpl = Bc[x] * ub[y] + Bc[Q + x] * ub[3 * Q + y] + Bc[2 * Q + y] * ub[Q + 2 * x] +
-                             Bc[3 * Q + y] * ub[Q + 2 * x + 1];
-          bufB[x * SB + y] = nxt[i] - cpl;
-        }
+        if (x < Q) bufB[x * SB + y] = nxt[i];
         x += 32 / Q;
         y += 32 % Q;
         if (y >= Q) { y -= Q; ++x; }
@@ -372,9 +400,10 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     };
     if (MODE != FD_LU) {
     // T1 = Vx^-1 R  (B operand from bufB)
+    constexpr int KS1 = MODE == FD_DOWN ? KSL : KS;  // FD_DOWN: q + 2 columns (the boundary values)
     clear();
 #pragma unroll
-    for (int k = 0; k < KS; ++k) {
+    for (int k = 0; k < KS1; ++k) {
       double b0 = bufB[(k * 4 + gc) * SB + gr], b1 = bufB[(k * 4 + gc) * SB + 8 + gr];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
@@ -388,7 +417,7 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
     // T2 = (T1 Vy^-T) .* rden  (A operand from bufA)
     clear();
 #pragma unroll
-    for (int k = 0; k < KS; ++k) {
+    for (int k = 0; k < KS1; ++k) {
       double a0 = bufA[gr * SA + k * 4 + gc], a1 = bufA[(8 + gr) * SA + k * 4 + gc];
 #pragma unroll
       for (int nj = 0; nj < 2; ++nj) {
@@ -573,10 +602,6 @@ __global__ void __launch_bounds__(256, 2) k_leaf_fd_mma(FdArgs a) {
                 const double av = (x < Q && y < Q) ? fabs(acc[mi][nj][h]) : 0.0;
                 gmax = (av > gmax || av != av) ? av : gmax;
               }
-          for (int b = lane; b < NB; b += 32) {
-            const double av = fabs(ub[b]);
-            gmax = (av > gmax || av != av) ? av : gmax;
-          }
         }
         __syncwarp();
         continue;
