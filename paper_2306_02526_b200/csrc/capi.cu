@@ -721,6 +721,7 @@ int hps_ops_build(const hps_plan* hp, const hps_build_desc* d, void* stream, hps
   }
   if (P.depth > 0) O.root_T = O.lo[0].T;
   if (int rc = sub_mma_prepare(O, st)) return fail(rc);
+  if (int rc = mega_pairs_prepare(O, st)) return fail(rc);
   if (cudaStreamSynchronize(st) != cudaSuccess) {
     set_error("cuda error at end of build: %s", cudaGetErrorString(cudaGetLastError()));
     return fail(HPS_ERR_CUDA);
@@ -1114,6 +1115,7 @@ int hps_ops_load(const hps_plan* hp, const void* host, long long size, hps_ops**
     lo.Ush = at(lidx[5 * d + 2]); lo.Ssh = at(lidx[5 * d + 3]); lo.T = at(lidx[5 * d + 4]);
   }
   if (int rc = sub_mma_prepare(O, 0)) { hps_ops_destroy(h); return rc; }
+  if (int rc = mega_pairs_prepare(O, 0)) { hps_ops_destroy(h); return rc; }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     hps_ops_destroy(h);
     set_error("hps_ops_load: %s", cudaGetErrorString(cudaGetLastError()));

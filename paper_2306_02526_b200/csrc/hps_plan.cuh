@@ -116,6 +116,19 @@ struct LevelOps {
   const double* SF = nullptr;
 };
 
+// Level pair (d, d + 1) of the dataflow kernel's down sweep (mega.cu): level
+// d + 1's interface values straight from level d's boundary values,
+//   [u3_a; u3_b] = C1 u_bnd(p) + (PU w3(p) + [w3_a; w3_b]),
+// so the two levels are one dependent phase instead of two.
+struct MegaPair {
+  int d = -1;              // parent level
+  Panel C1;                // (2 n3_{d+1}) x n12_d: [S_c[:, A] E + S_c[:, B] S_p] for the alpha, beta child
+  Panel PU;                // (2 n3_{d+1}) x n3_d:  [S_c[:, i3a]; S_c[:, i3b]]
+  int* iota = nullptr;     // device c_d x n3_d: w3(p) positions relative to W3[d]
+  int* out = nullptr;      // device c_d x 2 n3_{d+1}: positions of the adjusted w3 rows relative to W3[d]
+  long long off = 0;       // W3c[d + 1] - W3[d] in doubles (workspace carve, k = 1) the tables were built for
+};
+
 struct Ops {
   Plan* plan = nullptr;
   double sigma = 0.0, dtg = 0.0;
@@ -135,8 +148,10 @@ struct Ops {
   std::vector<void*> allocs;
   std::vector<size_t> alloc_bytes;
   std::vector<void*> aux;      // derived device data rebuilt after build / load (not dumped)
+  std::vector<MegaPair> pairs; // level pairs of the dataflow kernel's down sweep (derived, shared layout)
 };
 int sub_mma_prepare(Ops& O, cudaStream_t st);
+int mega_pairs_prepare(Ops& O, cudaStream_t st);
 
 int pack_panel(const double* src, long long s_node, int ld, const Panel& pn, cudaStream_t st);
 // rows [0, R1) of each node from src1, rows [R1, R) from src2
@@ -151,6 +166,7 @@ struct Workspace {
   double* Ub = nullptr;     // k x L x nb
   std::vector<double*> H;   // per level d (d>=1): k x c x n12
   std::vector<double*> W3;  // per level: k x c x n3
+  std::vector<double*> W3c; // k = 1, per level d >= 1: c x n3, w3 adjusted by the parent's (level pairs, mega.cu)
   double* part = nullptr;   // split-K partials
   unsigned* cnt = nullptr;  // split-K semaphores (zero between launches)
   unsigned* mega_cnt = nullptr;  // persistent level kernel: completion counters (zero between launches)

@@ -50,6 +50,7 @@ struct MSeg {
   int up;                      // 1 = up pass, 0 = down pass
   int n0, nn;                  // node range [n0, n0 + nn)
   int R, K;                    // operator rows / columns
+  int dmul;                    // completion counters bumped per node (1; 2 = one per child: level pairs)
   const double* op; int TR;    // one-node panel (tiles of TR rows, column-major)
   int RB, NG, S, KC;           // row blocks, node groups, splits, columns per split
   int task0, ntasks;
@@ -60,7 +61,7 @@ struct MSeg {
   // dataflow
   unsigned* done;              // [nodes of the level] row blocks finished
   const unsigned* wchild; int wchild_t;   // up: children's counters (level d+1), target
-  const unsigned* wpar; int wpar_t;       // down: parents' counters (level d-1)
+  const unsigned* wpar; int wpar_t;       // down: parents' counters (level d-1; wpar_sh = 2: level d-2, see the pairs)
   const unsigned* wup; int wup_t;         // down: own nodes' up counters
   int Rc, Rp, Ru;              // pn: rows per node of the waited-on segments (targets vary per node)
   double* part; unsigned* sem; // split partials [S][NG*NB][R], semaphores [NG*RB]
@@ -343,7 +344,11 @@ __global__ void __launch_bounds__(MT) k_mega(MProg p, unsigned* exit_count) {
     }
     if (emit_now) {
       __syncthreads();
-      if (tid < nv) red_add_release(g.done + node0 + tid, 1u);
+      if (tid < nv) {
+        unsigned* dn = g.done + (node0 + tid) * g.dmul;
+        red_add_release(dn, 1u);
+        if (g.dmul == 2) red_add_release(dn + 1, 1u);
+      }
       if (p.trace && tid == 0) p.trace[MTS * t + 4] = gtime();
     }
     __syncthreads();  // xs / red / sidx are reused by the next task
@@ -531,6 +536,141 @@ int mega_depth(const Ops& ops) {
   return d;
 }
 
+// ---- level pairs of the down sweep ------------------------------------------
+// The down sweep is a chain of dependent level phases (~9 us each whatever
+// their size).  For a pair (d, d + 1) the children's interface values follow
+// from the parent's boundary values directly: with u_bnd(c) = [u_bnd(p)[A];
+// u3(p)[B]] and u3(p) = S_p u_bnd(p) + w3(p),
+//   u3(c) = (S_c[:, A] E_A + S_c[:, B] S_p) u_bnd(p) + S_c[:, B] w3(p) + w3(c),
+// so level d + 1 runs in the same phase as level d: one down segment over the
+// level-d nodes with the stacked operator C1 = [C1_alpha; C1_beta], and (off the
+// critical path, during the up sweep) one segment for the adjusted load
+// w3c(c) = w3(c) + S_c[:, B] w3(p).  Both are ordinary down segments of
+// k_mega: only their tables differ.
+static int pair_min_level() {
+  static const int v = [] {
+    if (const char* e = getenv("HPSB_NO_MEGA_PAIRS")) if (e[0] == '1') return 1 << 20;
+    const char* e = getenv("HPSB_MEGA_PAIR_MIN");
+    return e ? std::max(1, atoi(e)) : 2;
+  }();
+  return v;
+}
+
+__global__ void k_pair_gather(const double* __restrict__ Sc, int n3c, int n12c, const int* __restrict__ i3a,
+                              const int* __restrict__ i3b, int n3p, double* __restrict__ PU) {
+  const long long n = 2LL * n3c * n3p;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += gridDim.x * 256LL) {
+    const int t = (int)(i % n3p), r = (int)(i / n3p);
+    PU[i] = r < n3c ? Sc[(long long)r * n12c + i3a[t]] : Sc[(long long)(r - n3c) * n12c + i3b[t]];
+  }
+}
+
+__global__ void k_pair_scatter(const double* __restrict__ Sc, int n3c, int n12c, const int* __restrict__ i1a,
+                               const int* __restrict__ i2b, int n1a, int n12p, double* __restrict__ C1) {
+  const long long n = 2LL * n3c * n12p;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += gridDim.x * 256LL) {
+    const int col = (int)(i % n12p), r = (int)(i / n12p);
+    if (r < n3c) {
+      if (col < n1a) C1[i] += Sc[(long long)r * n12c + i1a[col]];
+    } else if (col >= n1a) {
+      C1[i] += Sc[(long long)(r - n3c) * n12c + i2b[col - n1a]];
+    }
+  }
+}
+
+int mega_pairs_prepare(Ops& O, cudaStream_t st) {
+  const Plan& P = *O.plan;
+  O.pairs.clear();
+  if (!O.shared_levels || P.nparts != 1) return 0;
+  Workspace w0;
+  carve_workspace(P, 1, reinterpret_cast<void*>((uintptr_t)4096), w0);
+  for (int d = pair_min_level(); d + 1 < P.dF && d + 1 < P.depth; ++d) {
+    const Level &lp = P.lv[d], &lc = P.lv[d + 1];
+    const LevelOps &op = O.lo[d], &oc = O.lo[d + 1];
+    if (!op.S.base || !oc.S.base || op.S.c != 1 || oc.S.c != 1) continue;
+    const int n3p = lp.n3, n12p = lp.n12, n3c = lc.n3, n12c = lc.n12, n1a = lp.n1a;
+    if (lp.nbc != n12c || lc.c != 2 * lp.c) continue;
+    {  // the children's boundary order against the parent's (node 0 / its two children)
+      std::vector<int> gp(n12p), jp(n3p), ga(n12c), gb(n12c);
+      HPSB_CUDA(cudaMemcpyAsync(gp.data(), lp.gidx_bnd, n12p * 4, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(jp.data(), lp.j3, n3p * 4, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(ga.data(), lc.gidx_bnd, n12c * 4, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaMemcpyAsync(gb.data(), lc.gidx_bnd + n12c, n12c * 4, cudaMemcpyDeviceToHost, st));
+      HPSB_CUDA(cudaStreamSynchronize(st));
+      bool ok = (int)lp.h_i1a.size() == n1a && (int)lp.h_i3a.size() == n3p && (int)lp.h_i3b.size() == n3p &&
+                (int)lp.h_i2b.size() == n12p - n1a;
+      for (int r = 0; ok && r < n1a; ++r) ok = ga[lp.h_i1a[r]] == gp[r];
+      for (int r = 0; ok && r < n12p - n1a; ++r) ok = gb[lp.h_i2b[r]] == gp[n1a + r];
+      for (int t = 0; ok && t < n3p; ++t) ok = ga[lp.h_i3a[t]] == jp[t] && gb[lp.h_i3b[t]] == jp[t];
+      if (!ok) continue;
+    }
+    MegaPair mp;
+    mp.d = d;
+    mp.C1 = make_panel(1, 2 * n3c, n12p);
+    mp.PU = make_panel(1, 2 * n3c, n3p);
+    const size_t nS = (size_t)n3c * n12c + (size_t)n3p * n12p, nPU = (size_t)2 * n3c * n3p,
+                 nC = (size_t)2 * n3c * n12p;
+    double *tmp = nullptr, *pan = nullptr;
+    int* tab = nullptr;
+    if (cudaMalloc(&tmp, (nS + nPU + nC) * 8) != cudaSuccess) { cudaGetLastError(); break; }
+    if (cudaMalloc(&pan, (mp.C1.total() + mp.PU.total()) * 8) != cudaSuccess ||
+        cudaMalloc(&tab, ((size_t)lp.c * n3p + (size_t)lp.c * 2 * n3c) * 4) != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(tmp);
+      if (pan) cudaFree(pan);
+      break;
+    }
+    O.aux.push_back(pan);
+    O.aux.push_back(tab);
+    mp.C1.base = pan;
+    mp.PU.base = pan + mp.C1.total();
+    double *Sc = tmp, *Sp = tmp + (size_t)n3c * n12c, *PU = tmp + nS, *C1 = PU + nPU;
+    int rc = unpack_panel(oc.S, 0, 0, n3c, Sc, st);
+    if (!rc) rc = unpack_panel(op.S, 0, 0, n3p, Sp, st);
+    if (rc) { cudaFree(tmp); return rc; }
+    k_pair_gather<<<(unsigned)std::min<size_t>((nPU + 255) / 256, 2368), 256, 0, st>>>(Sc, n3c, n12c, lp.i3a, lp.i3b,
+                                                                                       n3p, PU);
+    GemmArgs g{};
+    g.M = 2 * n3c; g.N = n12p; g.K = n3p; g.alpha = 1.0; g.beta = 0.0;
+    g.A = PU; g.lda = n3p; g.B = Sp; g.ldb = n12p; g.C = C1; g.ldc = n12p; g.batch = 1;
+    rc = gemm(g, st);
+    if (rc) { cudaFree(tmp); return rc; }
+    k_pair_scatter<<<(unsigned)std::min<size_t>((nC + 255) / 256, 2368), 256, 0, st>>>(Sc, n3c, n12c, lp.i1a, lp.i2b,
+                                                                                       n1a, n12p, C1);
+    HPSB_CUDA(cudaMemsetAsync(pan, 0, (mp.C1.total() + mp.PU.total()) * 8, st));
+    rc = pack_panel(C1, 0, n12p, mp.C1, st);
+    if (!rc) rc = pack_panel(PU, 0, n3p, mp.PU, st);
+    if (rc) { cudaFree(tmp); return rc; }
+    // tables of the adjusted-load segment (inputs and outputs relative to W3[d])
+    mp.off = w0.W3c[d + 1] - w0.W3[d];
+    std::vector<int> h((size_t)lp.c * n3p + (size_t)lp.c * 2 * n3c);
+    for (size_t i = 0; i < (size_t)lp.c * n3p; ++i) h[i] = (int)i;
+    for (size_t i = 0; i < (size_t)lp.c * 2 * n3c; ++i) h[(size_t)lp.c * n3p + i] = (int)(mp.off + (long long)i);
+    HPSB_CUDA(cudaMemcpyAsync(tab, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+    HPSB_CUDA(cudaStreamSynchronize(st));
+    cudaFree(tmp);
+    mp.iota = tab;
+    mp.out = tab + (size_t)lp.c * n3p;
+    O.pairs.push_back(mp);
+  }
+  return 0;
+}
+
+static const MegaPair* pair_at(const Ops& ops, int d) {
+  for (const MegaPair& mp : ops.pairs)
+    if (mp.d == d) return &mp;
+  return nullptr;
+}
+
+// rows / columns -> row blocks, node groups, splits of a shared-operator segment
+static void seg_dims(int R, int K, int nn, int& RB, int& NG, int& S, int& KC) {
+  RB = (R + MRB - 1) / MRB;
+  NG = (nn + MNB - 1) / MNB;
+  S = std::max(1, (K + MKC - 1) / MKC);
+  KC = (K + S - 1) / S;
+  S = (K + KC - 1) / KC;
+}
+
 // Counter / partial space of the workspace's mega region for one plan: every
 // wide level's nodes twice (up, down), semaphores and split partials of every
 // possible segment.  Sized generously from the plan alone.
@@ -561,7 +701,35 @@ void mega_scratch(const Plan& P, size_t& counters, size_t& part_doubles) {
       counters += sems;
       if (S > 1 || d == 0) part_doubles += parts;  // the root pair always uses partials
     }
+    if (d >= 1 && d + 1 < P.depth) {  // a level pair (d, d + 1): two more segments over the level-d nodes
+      const int R2 = 2 * P.lv[d + 1].n3;
+      counters += (size_t)lv.c;       // completion counters of the adjusted-load segment
+      for (int K : {lv.n12, lv.n3}) {
+        int RB, NG, S, KC;
+        seg_dims(R2, K, lv.c, RB, NG, S, KC);
+        counters += (size_t)RB * NG;
+        if (S > 1) part_doubles += (size_t)S * NG * MNB * R2;
+      }
+    }
   }
+}
+
+// resident CTAs of the dataflow kernel on this device
+static int mega_max_ctas(bool pnm) {
+  static int max_ctas_pn[2] = {0, 0};
+  int& max_ctas = max_ctas_pn[pnm];
+  if (!max_ctas) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pnm ? k_mega<true> : k_mega<false>, MT, 0) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      per_sm = 1;
+    }
+    int dev = 0, sms = kNumSMs;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    max_ctas = std::max(1, per_sm) * sms;
+  }
+  return max_ctas;
 }
 
 // Runs the up levels [u0, u1) (deepest first) and the down levels [d0, d1)
@@ -585,6 +753,55 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   for (int d = 0; d < P.depth; ++d) { dup[d] = c; c += P.lv[d].c; ddn[d] = c; c += P.lv[d].c; }
   double* part = ws.mega_part;
   int task = 0;
+  // level pairs of the down sweep (whole shared-layout solves with a body load)
+  const bool pairs_on = !pnm && !ops.pairs.empty() && P.nparts == 1 && u0 == 0 && d0 == 0 && u1 == d1 && has_w3;
+  // pairs are taken greedily from the top while both segments of the phase fit (about) one
+  // round of the resident CTAs: a phase that needs two rounds of tasks gains nothing
+  std::vector<const MegaPair*> sel(P.depth + 2, nullptr);
+  if (pairs_on) {
+    static const double frac = [] { const char* e = getenv("HPSB_MEGA_PAIR_FRAC"); return e ? atof(e) : 1.2; }();
+    for (int d = 1; d + 1 < d1;) {
+      const MegaPair* mp = pair_at(ops, d);
+      if (mp && ws.W3c[d + 1] && ws.W3c[d + 1] - ws.W3[d] == mp->off) {
+        int RB, NG, S, KC, R, K, RB2, NG2, S2, KC2;
+        mega_dims(P.lv[d], d == 0, false, P.lv[d].c, RB, NG, S, KC, R, K);
+        seg_dims(2 * P.lv[d + 1].n3, P.lv[d].n12, P.lv[d].c, RB2, NG2, S2, KC2);
+        if ((double)RB * NG * S + (double)RB2 * NG2 * S2 <= frac * mega_max_ctas(false)) {
+          sel[d] = mp;
+          d += 2;
+          continue;
+        }
+      }
+      ++d;
+    }
+  }
+  auto pair_parent = [&](int d) -> const MegaPair* { return d >= 1 && d + 1 < d1 ? sel[d] : nullptr; };
+  std::vector<unsigned*> dpu(P.depth, nullptr);  // completion counters of the adjusted-load segments
+  std::vector<int> rb_pu(P.depth, 0), rb_c1(P.depth, 0);
+  // a segment over the level-d nodes with its own operator and tables (the pairs)
+  auto add_custom = [&](int d, const Panel& pn, int K, const int* gidx, const int* j3, const double* W3add,
+                        double* uvec, unsigned* done, int dmul) -> MSeg* {
+    if (p.nseg >= MAXSEG) return nullptr;
+    const Level& lv = P.lv[d];
+    MSeg& g = p.s[p.nseg];
+    g.up = 0; g.dmul = dmul;
+    g.n0 = 0; g.nn = lv.c;
+    g.R = pn.R; g.K = K;
+    seg_dims(g.R, g.K, g.nn, g.RB, g.NG, g.S, g.KC);
+    if (pn.C != K || g.KC > MKC || pn.TS != pn.TR || (pn.TR & 1)) return nullptr;
+    g.op = pn.base; g.TR = pn.TR;
+    g.task0 = task; g.ntasks = g.RB * g.NG * g.S;
+    task += g.ntasks;
+    g.n3 = pn.R; g.n12 = K;
+    g.gidx = gidx; g.j3 = j3;
+    g.W3 = const_cast<double*>(W3add);
+    g.u = uvec;
+    g.done = done;
+    g.sem = c; c += (size_t)g.RB * g.NG;
+    if (g.S > 1) { g.part = part; part += (size_t)g.S * g.NG * MNB * g.R; }
+    ++p.nseg;
+    return &g;
+  };
   auto add = [&](int d, bool up) -> bool {
     if (p.nseg >= MAXSEG) return false;
     const Level& lv = P.lv[d];
@@ -598,6 +815,7 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     if (d >= P.lstar) { n0 = part0 * (lv.c / P.nparts); n1 = part1 * (lv.c / P.nparts); }
     if (pnm && n0 != 0) return false;  // per-node panels of a part range: per-level launches
     g.up = up;
+    g.dmul = 1;
     g.n0 = n0; g.nn = n1 - n0;
     mega_dims(lv, d == 0, up, g.nn, g.RB, g.NG, g.S, g.KC, g.R, g.K, pnm);
     if (g.R != pn.R || g.K != pn.C || g.KC > MKC) return false;
@@ -632,6 +850,12 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
       g.wpar = par_here ? (from_up ? dup[0] : ddn[d - 1]) : nullptr;
       int RBp = 0, x1, x2, x3, x4 = 0, x5;
       if (par_here) mega_dims(P.lv[d - 1], d - 1 == 0, from_up, 1, RBp, x1, x2, x3, x4, x5);
+      // the parent level is a pair's child: its counters (one per child) are bumped by
+      // the grandparents' own tasks and by the pair's tasks
+      if (par_here && d >= 2 && pair_parent(d - 2)) {
+        mega_dims(P.lv[d - 2], d - 2 == 0, false, 1, RBp, x1, x2, x3, x4, x5);
+        RBp += rb_c1[d - 2];
+      }
       g.wpar_t = RBp;
       g.Rp = par_here ? x4 : 0;
       const bool up_here = d >= u0 && d < u1;
@@ -651,13 +875,40 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
     iroot_dn = p.nseg;
     if (!add(0, false)) return 1;
   }
-  for (int d = u1 - 1; d >= u0; --d)
+  for (int d = u1 - 1; d >= u0; --d) {
     if (!add(d, true)) return 1;
+    // adjusted loads w3c = w3(c) + S_c[:, B] w3(p) of the pair (d + 1, d + 2): both levels' up
+    // tasks are lower-numbered; runs beside the rest of the up sweep
+    if (const MegaPair* mp = pair_parent(d + 1)) {
+      const int dp = d + 1;
+      dpu[dp] = c; c += P.lv[dp].c;
+      MSeg* g = add_custom(dp, mp->PU, P.lv[dp].n3, mp->iota, mp->out, ws.W3[dp + 1], ws.W3[dp], dpu[dp], 1);
+      if (!g) return 1;
+      g->wup = dup[dp];
+      int x1, x2, x3, x4, x5;
+      mega_dims(P.lv[dp], dp == 0, true, 1, g->wup_t, x1, x2, x3, x4, x5);
+      rb_pu[dp] = g->RB;
+      rb_c1[dp] = (2 * P.lv[dp + 1].n3 + MRB - 1) / MRB;
+    }
+  }
   if (rpre)
     for (int i = 0; i < p.nseg; ++i)
       if (p.s[i].up && p.s[i].Hout == nullptr) p.s[i].rootpre = root_pre;  // the root's up segment
-  for (int d = (pair || rpre) ? 1 : d0; d < d1; ++d)
+  for (int d = (pair || rpre) ? 1 : d0; d < d1; ++d) {
     if (!add(d, false)) return 1;
+    if (const MegaPair* mp = pair_parent(d)) {
+      // level d + 1 in the same phase: one segment over the level-d nodes with the stacked
+      // operator; both segments count on the children's counters
+      MSeg& par = p.s[p.nseg - 1];
+      par.dmul = 2;
+      par.done = ddn[d + 1];
+      MSeg* g = add_custom(d, mp->C1, P.lv[d].n12, P.lv[d].gidx_bnd, P.lv[d + 1].j3, ws.W3c[d + 1], u, ddn[d + 1], 2);
+      if (!g) return 1;
+      g->wpar = par.wpar; g->wpar_t = par.wpar_t;
+      g->wup = dpu[d]; g->wup_t = rb_pu[d];
+      ++d;  // level d + 1 is done by the pair
+    }
+  }
   if (pair) {
     MSeg& dn = p.s[iroot_dn];
     MSeg* upp = nullptr;
@@ -683,15 +934,7 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   p.ticket = c++;
   p.reset = cnt + 1;
   p.nreset = (int)(c - (cnt + 1));
-  static int max_ctas_pn[2] = {0, 0};
-  int& max_ctas = max_ctas_pn[pnm];
-  if (!max_ctas) {
-    int per_sm = 0;
-    HPSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pnm ? k_mega<true> : k_mega<false>, MT, 0));
-    int dev = 0, sms = kNumSMs;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    max_ctas = std::max(1, per_sm) * sms;
-  }
+  const int max_ctas = mega_max_ctas(pnm);
   int grid = std::min(max_ctas, p.ntasks);
   if (pair && mega_dedicated()) {  // a quarter of the CTAs stream the root's down product while the up sweep climbs
     grid = max_ctas;

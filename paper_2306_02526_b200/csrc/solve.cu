@@ -89,6 +89,8 @@ size_t workspace_bytes(const Plan& P, int k) {
     if (d >= 1) add((long long)P.lv[d].c * P.lv[d].n12);
     add((long long)P.lv[d].c * P.lv[d].n3);
   }
+  if (k == 1)
+    for (int d = 1; d < std::min(P.depth, P.dF); ++d) add((long long)P.lv[d].c * P.lv[d].n3);
   size_t part, cnt, xg = 0;
   scratch_sizes(P, k, part, cnt, &xg);
   n += (part * 8 + 255) & ~(size_t)255;
@@ -117,6 +119,9 @@ void carve_workspace(const Plan& P, int k, void* base, Workspace& ws) {
     if (d >= 1) ws.H[d] = take((long long)P.lv[d].c * P.lv[d].n12);
     ws.W3[d] = take((long long)P.lv[d].c * P.lv[d].n3);
   }
+  ws.W3c.assign(P.depth, nullptr);
+  if (k == 1)
+    for (int d = 1; d < std::min(P.depth, P.dF); ++d) ws.W3c[d] = take((long long)P.lv[d].c * P.lv[d].n3);
   size_t part, cnt, xg = 0;
   scratch_sizes(P, k, part, cnt, &xg);
   ws.part = (double*)p;
