@@ -105,6 +105,11 @@ void hps_plan_destroy(hps_plan* plan);
 int hps_ops_build(const hps_plan* plan, const hps_build_desc* desc, void* stream, hps_ops** out);
 void hps_ops_destroy(hps_ops* ops);
 size_t hps_ops_device_bytes(const hps_ops* ops);
+/* Diagnostics: number of level pairs prepared for the down sweep of the
+ * dataflow kernel (shared layout; 0 = none).  A pair (d, d + 1) computes level
+ * d + 1's interface values of solver.py:262-265 straight from level d's
+ * boundary values through a composite operator, in level d's phase. */
+int hps_ops_level_pairs(const hps_ops* ops);
 
 /* Enable the tensor-product leaf solve for a constant-coefficient operator
  * set (leaf_fd.cu): host = Vx^-1, Vy^-T, Vx, Vy^T, rden (q x q each, row-major;

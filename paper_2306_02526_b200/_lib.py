@@ -74,6 +74,7 @@ _i = ctypes.c_int
 SIGNATURES = {
     "hps_version": (ctypes.c_int, []),
     "hps_launch_count": (ctypes.c_longlong, []),
+    "hps_ops_level_pairs": (_i, [_vp]),
     "hps_last_error": (ctypes.c_char_p, []),
     "hps_last_error_node": (ctypes.c_longlong, []),
     "hps_plan_create": (ctypes.c_int, [ctypes.POINTER(PlanDesc), ctypes.POINTER(ctypes.c_void_p)]),

@@ -299,6 +299,8 @@ int hps_merge_node(int nbc, const double* Tc, int n1a, int n2b, int n3, const in
   return done(0);
 }
 long long hps_launch_count(void) { return g_launches.load(); }
+
+int hps_ops_level_pairs(const hps_ops* ops) { return ops ? (int)ops->O.pairs.size() : 0; }
 const char* hps_last_error(void) { return g_err; }
 long long hps_last_error_node(void) { return g_err_node; }
 

@@ -755,11 +755,11 @@ int mega_levels(const Ops& ops, const Workspace& ws, int u0, int u1, int d0, int
   int task = 0;
   // level pairs of the down sweep (whole shared-layout solves with a body load)
   const bool pairs_on = !pnm && !ops.pairs.empty() && P.nparts == 1 && u0 == 0 && d0 == 0 && u1 == d1 && has_w3;
-  // pairs are taken greedily from the top while both segments of the phase fit (about) one
-  // round of the resident CTAs: a phase that needs two rounds of tasks gains nothing
+  // pairs are taken greedily from the top while both segments of the phase fit one round of
+  // the resident CTAs: a phase that needs a second round of tasks gains nothing (measured)
   std::vector<const MegaPair*> sel(P.depth + 2, nullptr);
   if (pairs_on) {
-    static const double frac = [] { const char* e = getenv("HPSB_MEGA_PAIR_FRAC"); return e ? atof(e) : 1.2; }();
+    static const double frac = [] { const char* e = getenv("HPSB_MEGA_PAIR_FRAC"); return e ? atof(e) : 1.0; }();
     for (int d = 1; d + 1 < d1;) {
       const MegaPair* mp = pair_at(ops, d);
       if (mp && ws.W3c[d + 1] && ws.W3c[d + 1] - ws.W3[d] == mp->off) {

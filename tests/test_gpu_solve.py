@@ -324,3 +324,48 @@ def test_tensor_leaf_solve_every_order(p):
                      f=lambda t, pts: phi(pts) * np.cos(t))
     _, uref = ost.run(0.0, phi(ot.points), 2)
     assert rel_l2(s.u, uref) < TOL, p
+
+
+def test_level_pairs_match_unpaired_solve_and_oracle(tmp_path):
+    """The dataflow kernel's level pairs (mega.cu: a pair's child level from the
+    parent's boundary values through a composite operator) against the CPU
+    oracle (reference solver.py:258-268) and against the same solve with
+    HPSB_NO_MEGA_PAIRS=1 in a fresh process (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+
+    import paper_2306_02526_b200 as hb
+    from oracle import hps_oracle as O
+    from paper_2306_02526_b200 import _lib
+
+    n, p = 32, 8
+    unit = ((0.0, 1.0), (0.0, 1.0))
+    rng = np.random.default_rng(7)
+    tree = hb.build_tree(unit, n, n, p)
+    ops = hb.build(tree, hb.OperatorCoefficients(c11=1.0, c22=0.7, c=0.3), sigma=1.0, dt_gamma=2e-3)
+    assert _lib.load().hps_ops_level_pairs(ops.handle) > 0, "no level pairs prepared for a 32 x 32 tree"
+    f = rng.standard_normal(tree.boundary_ids.size)
+    g = rng.standard_normal(tree.N)
+    u = ops.solve_with_body_load(f, g)
+    ot = O.OTree(unit, n, n, p)
+    ref = O.OHps(O.ODisc(ot, O.OCoeffs(c11=1.0, c22=0.7, c=0.3)), 1.0, 2e-3).solve_with_body_load(f, g)
+    assert rel_l2(u, ref) < 1e-10
+    np.save(tmp_path / "f.npy", f)
+    np.save(tmp_path / "g.npy", g)
+    code = (
+        "import numpy as np, paper_2306_02526_b200 as hb\n"
+        "from paper_2306_02526_b200 import _lib\n"
+        f"tree = hb.build_tree((({unit[0][0]}, {unit[0][1]}), ({unit[1][0]}, {unit[1][1]})), {n}, {n}, {p})\n"
+        "ops = hb.build(tree, hb.OperatorCoefficients(c11=1.0, c22=0.7, c=0.3), sigma=1.0, dt_gamma=2e-3)\n"
+        "assert _lib.load().hps_ops_level_pairs(ops.handle) == 0\n"
+        f"u = ops.solve_with_body_load(np.load(r'{tmp_path / 'f.npy'}'), np.load(r'{tmp_path / 'g.npy'}'))\n"
+        f"np.save(r'{tmp_path / 'u.npy'}', u)\n")
+    env = dict(os.environ, HPSB_NO_MEGA_PAIRS="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env["PYTHONPATH"] = root + os.pathsep + env.get("PYTHONPATH", "")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    u0 = np.load(tmp_path / "u.npy")
+    assert rel_l2(u, u0) < 1e-12
+    assert not np.array_equal(u, u0), "the paired and unpaired solves agree bitwise: pairs not taken"
