@@ -401,8 +401,18 @@ __device__ __forceinline__ void mma_apply(const double* __restrict__ F, const Mm
                                           int XS, int vn, double* red, Pre pre, Out out) {
   const int mt = sh.mt, nt = (vn + 7) >> 3, mn = mt * nt, ks = sh.ks;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gr = lane >> 2, gc = lane & 3;
+  // unit u = (s * nt + n) * mt + m: the up sweep (many short units) decodes it once and
+  // advances it by MW per round; the down sweep (few long units, registers for the loads in
+  // flight) decodes it per unit
+  constexpr bool INC = UNR == 2;
+  int s = warp / mn, n = (warp - s * mn) / mt, m = warp - s * mn - n * mt;
   for (int u = warp; u < mn * ks; u += MW) {
-    const int s = ks == 1 ? 0 : u / mn, t = u - s * mn, n = t / mt, m = t - n * mt;
+    if (!INC) {
+      s = ks == 1 ? 0 : u / mn;
+      const int t = u - s * mn;
+      n = t / mt;
+      m = t - n * mt;
+    }
     const int row = m * 8 + gr, node = n * 8 + 2 * gc;
     const int k0 = s * sh.kper, kn = min(sh.kt4 - k0, sh.kper);
     const double* ap = F + ((size_t)m * sh.kt4 + k0) * 32 + lane;
@@ -432,6 +442,13 @@ __device__ __forceinline__ void mma_apply(const double* __restrict__ F, const Mm
       double* rp = red + (size_t)u * 64 + gr * 8 + 2 * gc;
       rp[0] = d0;
       rp[1] = d1;
+    }
+    if (INC) {
+      m += MW;
+      while (m >= mt) {
+        m -= mt;
+        if (++n == nt) { n = 0; ++s; }
+      }
     }
   }
   if (ks > 1) {
