@@ -378,3 +378,43 @@ def test_plain_numpy_fields_and_g_run_on_device_arrays():
     b, st = run(True)
     assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
     assert getattr(st.problem.g, "_hb_npdev", None) is True
+
+
+@pytest.mark.parametrize("root_sep", [True, False])
+def test_nonzero_separable_boundary_data_matches_oracle(root_sep, monkeypatch):
+    """Two-term separable Dirichlet data that does not vanish on the boundary
+    (the manufactured heat problems' data does): the root Dirichlet products
+    from the per-operator-set rows S_root F_m (root_sep) and from a pass over
+    the root operator per step, eager and captured, against the oracle
+    stepper (reference timestep.py:237-266, solver.py:259-265)."""
+    hb = _hb()
+    from oracle import hps_oracle as O
+    if not root_sep:
+        monkeypatch.setenv("HPSB_NO_ROOT_SEP", "1")
+    x, y = (lambda p: p[:, 0]), (lambda p: p[:, 1])
+    phi1 = lambda p: np.sin(x(p) + 2 * y(p)) + 2.0
+    phi2 = lambda p: x(p) * y(p) + np.cos(3 * x(p))
+    emt = lambda t: np.exp(-t)
+    # u = cos(t) phi1 + exp(-t) phi2;  q = u_t - lap u
+    f = hb.SeparableField([(phi1, np.cos), (phi2, emt)])
+    q = hb.SeparableField([(lambda p: -phi1(p), np.sin),
+                           (lambda p: -phi2(p) + 9 * np.cos(3 * x(p)), emt),
+                           (lambda p: 5 * np.sin(x(p) + 2 * y(p)), np.cos)])
+    uex = lambda t, p: np.cos(t) * phi1(p) + emt(t) * phi2(p)
+    n, p_, dt, nsteps = 8, 10, 2e-3, 4
+    tree = hb.build_tree(UNIT, n, n, p_)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0), q=q, f=f,
+                               u0=lambda pts: uex(0.0, pts))
+    ot = O.OTree(UNIT, n, n, p_)
+    ost = O.OStepper(ot, O.OCoeffs(c11=1.0, c22=1.0), O.ark4_tableau(), dt, q=q, f=f)
+    _, uref = ost.run(0.0, uex(0.0, ot.points), nsteps)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=dt)
+    s = st.run(st.initial_state(), nsteps)              # 1 eager step, then replays of the captured step
+    assert st._graph is not None
+    assert (getattr(st.ops, "_root_sep", None) is not None) == root_sep
+    assert rel_l2(s.u, uref) < TOL
+    assert rel_l2(s.u, uex(nsteps * dt, tree.points)) < 1e-6      # and the manufactured solution
+    monkeypatch.setenv("HPSB_NO_GRAPH", "1")
+    st2 = hb.TimeStepper(tree, prob, "ARK4", dt=dt)
+    s2 = st2.run(st2.initial_state(), nsteps)
+    assert rel_l2(s2.u, uref) < TOL
