@@ -203,21 +203,24 @@ def config_block(cfg):
                   "working set fits the 126 MB L2 (a latency-bound configuration; no flush)"}
 
 
-def kernel_bytes(shapes, dF, L, ni, nb, nbd, N, k=1):
-    """Algorithmic HBM bytes per launch of the stage-path kernels (shared
-    layout): every vector byte a kernel must read or write once,
-    every operator byte once per launch.  Up-level node: children's flux
+def kernel_bytes(shapes, dF, L, ni, nb, nbd, N, k=1, per_node=False):
+    """Algorithmic HBM bytes per launch of the stage-path kernels
+    (DESIGN.md): every vector byte a kernel must read or write once, every
+    operator byte once per launch (shared layout: one operator per level;
+    per_node: one per node, what the reference stores).  Up-level node: children's flux
     entries 2 n3 + n12 in, w3 n3 + flux n12 out, operator (n3 + n12) n3 (root
     n3 n3); down-level node: boundary values n12 + w3 n3 in, u3 n3 out,
     operator n3 n12 (root: precomputed by k_root_dir in the stage path).
     Returns {category: bytes or fn(nterms)}."""
+    nops = (lambda c: c) if per_node else (lambda c: 1)
+
     def up(lv, root):
         c, n3, n12 = lv
-        return 8 * (k * c * (3 * n3 + 2 * n12 - (n12 if root else 0)) + (n3 + (0 if root else n12)) * n3)
+        return 8 * (k * c * (3 * n3 + 2 * n12 - (n12 if root else 0)) + nops(c) * (n3 + (0 if root else n12)) * n3)
 
     def dn(lv, root):
         c, n3, n12 = lv
-        return 8 * (k * c * (n12 + 2 * n3) + (0 if root else n3 * n12))
+        return 8 * (k * c * (n12 + 2 * n3) + (0 if root else nops(c) * n3 * n12))
 
     wide = range(0, dF)
     fused = range(dF, len(shapes))
@@ -761,7 +764,8 @@ def kernel_table(kt, nsteps, tree, lib, st, k):
     shapes = [(lm.count, lm.n3, lm.n12) for lm in tree.level_maps]
     dF = lib.hps_plan_fused_level(st.ops.plan.handle)
     nbd = tree.boundary_ids.size
-    kb = kernel_bytes(shapes, dF, tree.L, tree.ni, tree.nb, nbd, tree.N, k)
+    kb = kernel_bytes(shapes, dF, tree.L, tree.ni, tree.nb, nbd, tree.N, k,
+                      per_node=getattr(st.ops, "layout", "shared") == "per_node")
     s = st.pair.s
     total = sum(v[0] for v in kt.values())
     # stage terms of the fused leaf-up kernel, stage i (1..s-1): u, L u_0..u_{i-1}, q's spatial parts
