@@ -418,3 +418,36 @@ def test_nonzero_separable_boundary_data_matches_oracle(root_sep, monkeypatch):
     st2 = hb.TimeStepper(tree, prob, "ARK4", dt=dt)
     s2 = st2.run(st2.initial_state(), nsteps)
     assert rel_l2(s2.u, uref) < TOL
+
+
+def test_stage_history_by_leaf_grid_products_switch():
+    """HPSB_LU_PRODUCTS=1 (read once per process): the fused stage's history
+    L u_i by the two leaf-grid products instead of the interior equation --
+    two ARK4 steps of the manufactured heat problem against the oracle in a
+    fresh process (reference timestep.py:259-261)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_2306_02526_b200 as hb\n"
+        "from oracle import hps_oracle as O\n"
+        "unit = ((0.0, 1.0), (0.0, 1.0))\n"
+        "phi = lambda p: np.sin(2 * np.pi * p[:, 0]) * np.sin(2 * np.pi * p[:, 1]) + p[:, 0]\n"
+        "tau = lambda t: -np.sin(t) + 8 * np.pi ** 2 * np.cos(t)\n"
+        "tree = hb.build_tree(unit, 8, 8, 12)\n"
+        "prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0),\n"
+        "    q=hb.SeparableField.product(phi, tau), f=hb.SeparableField.product(phi, np.cos), u0=phi)\n"
+        "st = hb.TimeStepper(tree, prob, 'ARK4', dt=1e-3)\n"
+        "s = st.run(st.initial_state(), 3)\n"
+        "ot = O.OTree(unit, 8, 8, 12)\n"
+        "ost = O.OStepper(ot, O.OCoeffs(c11=1.0, c22=1.0), O.ark4_tableau(), 1e-3,\n"
+        "    q=lambda t, p: phi(p) * tau(t), f=lambda t, p: phi(p) * np.cos(t))\n"
+        "_, uref = ost.run(0.0, phi(ot.points), 3)\n"
+        "err = np.linalg.norm(s.u - uref) / np.linalg.norm(uref)\n"
+        "assert err < 1e-10, err\n"
+        "print('ok', err)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HPSB_LU_PRODUCTS="1")
+    env["PYTHONPATH"] = root + os.pathsep + env.get("PYTHONPATH", "")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
