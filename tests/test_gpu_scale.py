@@ -138,3 +138,17 @@ def test_many_rhs_solve_matches_single_rhs_solves():
     for i in range(0, k, 7):
         u = ops.solve_device(fb[i:i + 1], body[i:i + 1], torch.empty((1, tree.N), dtype=torch.float64, device="cuda"))
         assert rel_l2(U[i].cpu().numpy(), u[0].cpu().numpy()) < 1e-12, i
+
+
+def test_c2_recipe_trajectory_stays_with_the_oracle():
+    """Forty ARK4 steps of the C2 recipe at 32x32 leaves (captured-graph
+    replays): the GPU trajectory stays with the oracle's far below the
+    per-step 1e-10 bar (~4e-15 per step here,
+    7e-15 at C2's full size -- C2 runs 1000 steps), reference timestep.py:237-266."""
+    cfg = bench.CONFIGS["C2"]
+    _, ost, u = bench.oracle_stepper(cfg, 32)
+    _, uref = ost.run(0.0, u, 40)
+    _, st = _gpu_stepper(cfg, 32)
+    s = st.run(st.initial_state(), 40)
+    assert st._graph is not None
+    assert rel_l2(s.u, uref) < 2e-12
