@@ -451,3 +451,25 @@ def test_stage_history_by_leaf_grid_products_switch():
     env["PYTHONPATH"] = root + os.pathsep + env.get("PYTHONPATH", "")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout[-500:], r.stderr[-2000:])
+
+
+@pytest.mark.parametrize("p", [7, 9, 11, 13, 15])
+def test_fused_stage_odd_leaf_orders_match_oracle(p):
+    """Odd interior orders q = p - 2 (unvectorised stores of u_int / L u in the
+    leaf kernel, q + 2 not a multiple of 4): three ARK4 steps with nonzero
+    boundary data against the oracle (reference timestep.py:237-266)."""
+    hb = _hb()
+    from oracle import hps_oracle as O
+    phi = lambda pts: np.cos(pts[:, 0] + 0.5) * np.cosh(0.7 * pts[:, 1])
+    tau = lambda t: 1.0 + 0.3 * np.sin(5 * t)
+    f = hb.SeparableField.product(phi, tau)
+    q = hb.SeparableField([(phi, lambda t: 1.5 * np.cos(5 * t)), (lambda pts: 0.51 * phi(pts), tau)])
+    n, dt = 4, 1e-3
+    tree = hb.build_tree(UNIT, n, n, p)
+    prob = hb.ParabolicProblem(coeffs=hb.OperatorCoefficients(c11=1.0, c22=1.0), q=q, f=f, u0=phi)
+    st = hb.TimeStepper(tree, prob, "ARK4", dt=dt)
+    s = st.run(st.initial_state(), 3)
+    ot = O.OTree(UNIT, n, n, p)
+    ost = O.OStepper(ot, O.OCoeffs(c11=1.0, c22=1.0), O.ark4_tableau(), dt, q=q, f=f)
+    _, uref = ost.run(0.0, phi(ot.points), 3)
+    assert rel_l2(s.u, uref) < TOL
